@@ -1,0 +1,252 @@
+/*
+ * lsw.h -- C ABI of the B200-native LoRA-Switch hot path (arXiv 2405.17741).
+ *
+ * The paper's statement of the problem (Alg. 1, P:296-309 of PAPER.md): at
+ * token t, given the input token and all model parameters, (1) compute the
+ * pre-gate G^1(x^1) once (Eq. 2), (2-4) switch every adapted linear of
+ * every layer in ONE kernel (Eq. 5/9/10, SGMM Eq. 11, "a single CUDA
+ * kernel operation", in place P:328), (5) run the plain backbone forward on the
+ * merged weights (Eq. 3).  This library implements steps 1-5 for the
+ * adapted linears (q,k,v,o,gate,up,down) as four calls:
+ *
+ *     lsw_router_topk         Eq. 2                       (kernel K2)
+ *     lsw_merge_all_layers    Eq. 6 (first token) / Eq. 10 (fused switch) (K1)
+ *     lsw_unmerge_all_layers  Eq. 7 (end of sequence)     (K1)
+ *     lsw_decode_linear       Eq. 3, one batch-1 GEMV     (K4) [+ NCCL allreduce under TP]
+ *
+ * plus grouped / whole-token conveniences built only from those kernels.
+ *
+ * Conventions (all calls)
+ *  - Memory: every tensor pointer is CALLER-OWNED DEVICE memory (allocated by
+ *    the caller, e.g. torch), borrowed for the lifetime of the ctx, unless the
+ *    parameter name ends in _h (HOST memory, ideally pinned).  The ctx owns only
+ *    its own state: the merged-decision slots, the device error latch, packed
+ *    tensor-core operand copies of the LoRA factors (see lsw_create), TMA
+ *    descriptors, staging buffers and the NCCL communicator.
+ *  - Layouts (row-major, C order, contiguous):
+ *      W[kind]  [L, d_out, d_in]   backbone weight f (nn.Linear layout), MUTATED IN PLACE
+ *      A[kind]  [L, N, r, d_in]    LoRA_DOWN bank (P:139 W_down)
+ *      B[kind]  [L, N, d_out, r]   LoRA_UP   bank (P:139 W_up)
+ *      router_w [N, d_model]       W_g, the single pre-gate at the first
+ *                                  expanded linear
+ *    d_out/d_in are this rank's LOCAL (tensor-parallel shard) sizes.
+ *  - dtype: LSW_BF16 (W, A, B, router_w and every x are bf16) or LSW_F32 (all
+ *    fp32).  Accumulation is fp32 (GEMV, switch) / fp64 (router logits); one
+ *    round-to-nearest-even store of W per pass.
+ *  - Update (Eq. 4-10, readings R1-R3 of DESIGN.md):
+ *      W <- RNE( W + sum_j c_j * B[e_j] @ A[e_j] )
+ *    with c_j = (alpha/r) * g_j for the current decision and -(alpha/r) * g_j for
+ *    the previously merged one (Eq. 9 with its double negation corrected: the
+ *    sign is on the coefficient).  Experts present in both decisions are
+ *    combined into one term c = (alpha/r)(g_t - g_{t-1}); terms with c == 0 are
+ *    dropped, so prev == cur is an exact no-op (R12).
+ *  - Asynchrony: hot calls validate their arguments on the host, then only
+ *    ENQUEUE work on `stream` (a cudaStream_t; NULL = legacy default stream) and
+ *    return.  Decisions (idx, gate) never come back to the host, so a token is
+ *    CUDA-graph capturable.  Exceptions: lsw_device_status and
+ *    lsw_decode_token_host synchronize `stream`.
+ *  - Errors: argument / shape / state errors are returned synchronously BEFORE
+ *    anything is enqueued (LSW_E_ARG / LSW_E_SHAPE / LSW_E_STATE), with a
+ *    message in lsw_last_error() (thread-local) naming the offending values.
+ *    Errors detected on the device (non-finite router logits, expert index out
+ *    of range or duplicated, non-finite gate) are LATCHED in the ctx; the
+ *    affected kernel becomes a no-op (W untouched); lsw_device_status() reports
+ *    and clears the latch.  No exception crosses the ABI, nothing is printed,
+ *    nothing calls exit().
+ *  - State machine (SPEC SwitchState S:234-237):  none --merge(d)--> merged(d);
+ *    merged(d) --merge(d')--> merged(d') [one fused Eq. 10 pass];
+ *    merged(d) --unmerge--> none.  unmerge in state none is LSW_E_STATE.  The
+ *    host mirrors only "merged or not"; the decision itself lives on the device.
+ *  - Launch count: exactly ONE switch-kernel launch per merge / unmerge call,
+ *    independent of L, N, k, r.
+ *  - Threading: one consumer thread per ctx; no internal locking.
+ */
+#ifndef LSW_H_
+#define LSW_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define LSW_API __attribute__((visibility("default")))
+#else
+#define LSW_API
+#endif
+
+#define LSW_ABI_VERSION 1
+#define LSW_MAX_TOPK 8        /* k <= 8                                     */
+#define LSW_MAX_EXPERTS 64    /* N <= 64                                    */
+#define LSW_NKIND 7
+
+typedef struct lsw_ctx lsw_ctx;
+
+typedef enum {
+  LSW_OK = 0,
+  LSW_E_ARG = 1,          /* null pointer, bad enum, misaligned pointer       */
+  LSW_E_SHAPE = 2,        /* inconsistent or unsupported sizes                */
+  LSW_E_STATE = 3,        /* call not allowed in the current merge state      */
+  LSW_E_CUDA = 4,         /* CUDA runtime / driver failure                    */
+  LSW_E_NCCL = 5,         /* NCCL failure or TP call without a communicator   */
+  LSW_E_DEVICE = 6,       /* a device-side error was latched (device_status)  */
+  LSW_E_OOM = 7,          /* ctx-owned allocation failed                      */
+  LSW_E_UNSUPPORTED = 8   /* requested implementation not available           */
+} lsw_status;
+
+/* Device-side error codes latched by the kernels (lsw_device_status). */
+enum {
+  LSW_DEV_OK = 0,
+  LSW_DEV_NONFINITE_LOGITS = 1,  /* router: a logit is NaN/Inf     */
+  LSW_DEV_BAD_INDEX = 2,         /* switch: idx out of [0,N) or duplicated  */
+  LSW_DEV_BAD_GATE = 3           /* switch: non-finite gate value           */
+};
+
+typedef enum { LSW_F32 = 0, LSW_BF16 = 1 } lsw_dtype;
+
+typedef enum {
+  LSW_Q = 0, LSW_K = 1, LSW_V = 2, LSW_O = 3, LSW_GATE = 4, LSW_UP = 5, LSW_DOWN = 6
+} lsw_kind;
+
+/* GEMV groups: sites that share one input vector in a decode step (R18). */
+typedef enum { LSW_G_QKV = 0, LSW_G_O = 1, LSW_G_GATE_UP = 2, LSW_G_DOWN = 3, LSW_NGROUP = 4 } lsw_group;
+
+/* Switch-kernel implementation (K1 variants). */
+typedef enum {
+  LSW_IMPL_AUTO = 0,   /* TC for bf16, SIMT for fp32                         */
+  LSW_IMPL_SIMT = 1,   /* CUDA-core fp32 FFMA, per-expert fp32 accumulators   */
+  LSW_IMPL_TC = 2      /* tcgen05 + TMEM + TMA, per-expert TMEM accumulators  */
+} lsw_impl;
+
+typedef struct {
+  void*       W;             /* [L, d_out, d_in]  device, mutated in place           */
+  const void* A;             /* [L, N, r, d_in]   device, read at create (packing)   */
+                             /*                   and by the SIMT switch             */
+  const void* B;             /* [L, N, d_out, r]  device                              */
+  int64_t     d_out, d_in;   /* LOCAL sizes of this rank's shard                     */
+  int32_t     row_parallel;  /* 1: d_in is sharded (o, down) -> the decode GEMV     */
+                             /*    output is sum-allreduced when tp_size > 1         */
+  int32_t     reserved;
+} lsw_kind_desc;
+
+typedef struct {
+  int32_t n_layers;          /* L >= 1                                               */
+  int32_t n_experts;         /* N in [1, LSW_MAX_EXPERTS]                             */
+  int32_t rank;              /* r >= 1                                               */
+  int32_t top_k;             /* k in [1, min(N, LSW_MAX_TOPK)]              */
+  float   alpha;             /* LoRA alpha; scale = alpha / r  (R3; paper: 16)        */
+  int32_t dtype;             /* lsw_dtype                                            */
+  int64_t d_model;           /* router input length                                  */
+  int32_t tp_rank, tp_size;  /* tensor-parallel position (1 GPU: 0, 1)               */
+  int32_t impl;              /* lsw_impl                                             */
+  int32_t reserved;
+} lsw_config;
+
+typedef struct {
+  int64_t  tiles_total;      /* switch tiles per pass (all layers, all kinds)        */
+  int32_t  switch_impl;      /* lsw_impl actually used                               */
+  int32_t  grid;             /* persistent switch grid (CTAs)                        */
+  int32_t  tile_m, tile_n;   /* switch tile shape                                    */
+  int32_t  merged;           /* host mirror of the state machine                     */
+  int32_t  num_sms;
+  uint64_t kernel_launches;  /* kernels this ctx has launched so far                 */
+  int64_t  packed_bytes;     /* ctx-owned packed operand bytes on the device         */
+  int64_t  xs_elems, ys_elems; /* token I/O sizes (lsw_decode_token)                  */
+} lsw_info;
+
+/* Returns LSW_ABI_VERSION. */
+LSW_API int32_t lsw_abi_version(void);
+
+/* Thread-local message describing the last non-OK status of this thread. */
+LSW_API const char* lsw_last_error(void);
+
+/*
+ * Validate shapes, build the tile table, allocate the ctx state and, for the
+ * tensor-core switch, pack the LoRA factors into K-major tcgen05 operand
+ * copies (A^T per expert, rank padded to a multiple of 16; ctx-owned, about
+ * N*r*(d_in + d_out)*L*2 B per kind) and encode the TMA descriptors.  The
+ * packing kernels run on the legacy default stream and are complete when
+ * lsw_create returns.  Device = the current CUDA device.
+ * Errors: LSW_E_ARG (null/misaligned pointers, bad enums), LSW_E_SHAPE (d_in
+ * not a multiple of 8, k > N, N > 64, ...), LSW_E_UNSUPPORTED (TC requested
+ * for fp32 or on a GPU without sm_100), LSW_E_OOM, LSW_E_CUDA.
+ */
+LSW_API lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND],
+                      const void* router_w, lsw_ctx** out);
+
+/* Free ctx-owned memory and the communicator.  Synchronizes the device. */
+LSW_API lsw_status lsw_destroy(lsw_ctx* ctx);
+
+/* Fill `info`. Never fails for a valid ctx. */
+LSW_API lsw_status lsw_get_info(const lsw_ctx* ctx, lsw_info* info);
+
+/*
+ * Tensor parallelism (tp_size > 1): rank 0 calls lsw_nccl_get_unique_id,
+ * broadcasts the 128 bytes out of band (e.g. torch.distributed), then every
+ * rank calls lsw_attach_nccl (collective; blocks until all ranks joined).
+ */
+LSW_API lsw_status lsw_nccl_get_unique_id(void* id_out_128B_h);
+LSW_API lsw_status lsw_attach_nccl(lsw_ctx* ctx, const void* id_128B_h);
+
+/*
+ * Eq. 2: z = W_g x1 accumulated in fp64 (R6), S = top-k by
+ * (z desc, index asc) (R5), g = softmax over z_S only (R4).
+ *   x1   [d_model] device, cfg dtype
+ *   idx  [top_k] int32 device, out: sorted by descending g
+ *   gate [top_k] fp32  device, out: sums to 1
+ * Non-finite logits latch LSW_DEV_NONFINITE_LOGITS and write idx = -1.
+ */
+LSW_API lsw_status lsw_router_topk(lsw_ctx* ctx, const void* x1, int32_t* idx, float* gate, void* stream);
+
+/*
+ * State none:      Eq. 6  W <- RNE(W + sum_j (alpha/r) g_j B_j A_j)          (merge)
+ * State merged(d): Eq. 10 W <- RNE(W + Delta(idx,gate) - Delta(d))           (fused switch)
+ * ONE kernel over every tile of every adapted matrix of every layer.  The new
+ * decision is recorded on the device by the same kernel.  idx/gate: device
+ * [top_k] (typically straight from lsw_router_topk).
+ */
+LSW_API lsw_status lsw_merge_all_layers(lsw_ctx* ctx, const int32_t* idx, const float* gate, void* stream);
+
+/* Eq. 7: W <- RNE(W - Delta(d)) for the merged decision d; state -> none.
+ * LSW_E_STATE if nothing is merged. */
+LSW_API lsw_status lsw_unmerge_all_layers(lsw_ctx* ctx, void* stream);
+
+/*
+ * Eq. 3: y = W*[layer, kind] x, batch 1, fp32 accumulate.
+ *   x [d_in] device cfg dtype;  y [d_out] fp32 device, overwritten.
+ * Row-parallel kinds with tp_size > 1: y is sum-allreduced over the TP group.
+ */
+LSW_API lsw_status lsw_decode_linear(lsw_ctx* ctx, int32_t layer, int32_t kind, const void* x, float* y,
+                             void* stream);
+
+/* One GEMV launch for every kind of `group` (they share x): y is the
+ * concatenation of the kinds' outputs in kind order (e.g. QKV -> [q | k | v]). */
+LSW_API lsw_status lsw_decode_group(lsw_ctx* ctx, int32_t layer, int32_t group, const void* x, float* y,
+                            void* stream);
+
+/*
+ * One whole Alg. 1 token: router(x1) -> merge_all_layers -> for every layer the
+ * four group GEMVs.  xs packs the GEMV inputs layer-major, group-minor
+ * (QKV, O, GATE_UP, DOWN; each of its local d_in); ys packs the outputs the
+ * same way (each group's concatenated local d_out).  Sizes: lsw_get_info
+ * xs_elems / ys_elems.  idx/gate receive the decision (device).
+ */
+LSW_API lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs, float* ys,
+                            int32_t* idx, float* gate, void* stream);
+
+/* Same as lsw_decode_token from HOST buffers: copies x1_h, xs_h to ctx-owned
+ * device staging, runs the token, copies ys/idx/gate back and synchronizes
+ * `stream`.  Host buffers should be pinned for asynchronous copies. */
+LSW_API lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_h, float* ys_h,
+                                 int32_t* idx_h, float* gate_h, void* stream);
+
+/* Synchronize `stream`, then return LSW_OK or LSW_E_DEVICE and write + clear
+ * the latched device error code (LSW_DEV_*) into *code (may be NULL). */
+LSW_API lsw_status lsw_device_status(lsw_ctx* ctx, void* stream, int32_t* code);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+#endif  /* LSW_H_ */

@@ -1,0 +1,211 @@
+"""Thin ctypes binding over liblsw.so (include/lsw.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  torch supplies device memory (tensors are passed by data_ptr),
+streams (torch.cuda.current_stream()) and, for TP, the process group used to
+broadcast the NCCL unique id.  If the library is missing this module raises at
+import -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblsw.so")
+
+KINDS = ("q", "k", "v", "o", "gate", "up", "down")
+GROUPS = (("q", "k", "v"), ("o",), ("gate", "up"), ("down",))
+MAX_TOPK = 8
+
+LSW_OK = 0
+STATUS = {0: "LSW_OK", 1: "LSW_E_ARG", 2: "LSW_E_SHAPE", 3: "LSW_E_STATE", 4: "LSW_E_CUDA",
+          5: "LSW_E_NCCL", 6: "LSW_E_DEVICE", 7: "LSW_E_OOM", 8: "LSW_E_UNSUPPORTED"}
+DTYPE = {torch.bfloat16: 1, torch.float32: 0}
+IMPL = {"auto": 0, "simt": 1, "tc": 2}
+IMPL_NAME = {v: k for k, v in IMPL.items()}
+
+# Exported symbols the header declares (checked by tests/test_abi.py).
+SYMBOLS = (
+    "lsw_abi_version", "lsw_last_error", "lsw_create", "lsw_destroy", "lsw_get_info",
+    "lsw_nccl_get_unique_id", "lsw_attach_nccl", "lsw_router_topk", "lsw_merge_all_layers",
+    "lsw_unmerge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_token",
+    "lsw_decode_token_host", "lsw_device_status",
+)
+
+
+class LswError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class KindDesc(ctypes.Structure):
+    _fields_ = [("W", ctypes.c_void_p), ("A", ctypes.c_void_p), ("B", ctypes.c_void_p),
+                ("d_out", ctypes.c_int64), ("d_in", ctypes.c_int64),
+                ("row_parallel", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("n_layers", ctypes.c_int32), ("n_experts", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("top_k", ctypes.c_int32), ("alpha", ctypes.c_float), ("dtype", ctypes.c_int32),
+                ("d_model", ctypes.c_int64), ("tp_rank", ctypes.c_int32), ("tp_size", ctypes.c_int32),
+                ("impl", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("tiles_total", ctypes.c_int64), ("switch_impl", ctypes.c_int32), ("grid", ctypes.c_int32),
+                ("tile_m", ctypes.c_int32), ("tile_n", ctypes.c_int32), ("merged", ctypes.c_int32),
+                ("num_sms", ctypes.c_int32), ("kernel_launches", ctypes.c_uint64),
+                ("packed_bytes", ctypes.c_int64), ("xs_elems", ctypes.c_int64), ("ys_elems", ctypes.c_int64)]
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the CUDA library is required; there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    sig = {
+        "lsw_abi_version": (i32, []),
+        "lsw_last_error": (ctypes.c_char_p, []),
+        "lsw_create": (i32, [ctypes.POINTER(Config), ctypes.POINTER(KindDesc), vp, ctypes.POINTER(vp)]),
+        "lsw_destroy": (i32, [vp]),
+        "lsw_get_info": (i32, [vp, ctypes.POINTER(Info)]),
+        "lsw_nccl_get_unique_id": (i32, [vp]),
+        "lsw_attach_nccl": (i32, [vp, vp]),
+        "lsw_router_topk": (i32, [vp, vp, vp, vp, vp]),
+        "lsw_merge_all_layers": (i32, [vp, vp, vp, vp]),
+        "lsw_unmerge_all_layers": (i32, [vp, vp]),
+        "lsw_decode_linear": (i32, [vp, i32, i32, vp, vp, vp]),
+        "lsw_decode_group": (i32, [vp, i32, i32, vp, vp, vp]),
+        "lsw_decode_token": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+        "lsw_decode_token_host": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+        "lsw_device_status": (i32, [vp, vp, ctypes.POINTER(i32)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_LIB: Optional[ctypes.CDLL] = None
+
+
+def lib() -> ctypes.CDLL:
+    global _LIB
+    if _LIB is None:
+        _LIB = load_library()
+    return _LIB
+
+
+def _check(st: int):
+    if st != LSW_OK:
+        raise LswError(st, lib().lsw_last_error().decode(errors="replace"))
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class LoraSwitch:
+    """One ctx of the C library.  Tensors stay owned by the caller (kept alive
+    here by reference); W tensors are mutated in place by merge/unmerge.
+
+    W[kind] [L, d_out, d_in], A[kind] [L, N, r, d_in], B[kind] [L, N, d_out, r],
+    router_w [N, d_model]; all on the current CUDA device, same dtype.
+    """
+
+    def __init__(self, W: Dict[str, torch.Tensor], A: Dict[str, torch.Tensor], B: Dict[str, torch.Tensor],
+                 router_w: torch.Tensor, *, top_k: int, alpha: float, impl: str = "auto",
+                 tp_rank: int = 0, tp_size: int = 1, row_parallel: Sequence[str] = ("o", "down")):
+        self._keep = (W, A, B, router_w)
+        dt = router_w.dtype
+        L, N, r, _ = A["q"].shape
+        cfg = Config(n_layers=L, n_experts=N, rank=r, top_k=top_k, alpha=alpha, dtype=DTYPE[dt],
+                     d_model=router_w.shape[1], tp_rank=tp_rank, tp_size=tp_size, impl=IMPL[impl])
+        kinds = (KindDesc * 7)()
+        for i, kd in enumerate(KINDS):
+            for t in (W[kd], A[kd], B[kd]):
+                if not t.is_contiguous() or t.dtype != dt or not t.is_cuda:
+                    raise ValueError(f"kind {kd}: tensors must be contiguous CUDA {dt}")
+            kinds[i] = KindDesc(W=W[kd].data_ptr(), A=A[kd].data_ptr(), B=B[kd].data_ptr(),
+                                d_out=W[kd].shape[1], d_in=W[kd].shape[2],
+                                row_parallel=int(kd in row_parallel))
+        h = ctypes.c_void_p()
+        _check(lib().lsw_create(ctypes.byref(cfg), kinds, router_w.data_ptr(), ctypes.byref(h)))
+        self._h = h
+        self.top_k = top_k
+        self.dtype = dt
+        self.d_model = router_w.shape[1]
+
+    # --- lifecycle --------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lsw_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        inf = Info()
+        _check(lib().lsw_get_info(self._h, ctypes.byref(inf)))
+        d = {f: getattr(inf, f) for f, _ in Info._fields_}
+        d["switch_impl"] = IMPL_NAME.get(d["switch_impl"], d["switch_impl"])
+        return d
+
+    def attach_nccl(self, unique_id: bytes):
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        _check(lib().lsw_attach_nccl(self._h, buf))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().lsw_nccl_get_unique_id(buf))
+        return buf.raw
+
+    # --- the four calls of the boundary -----------------------------------
+    def router_topk(self, x1: torch.Tensor, idx: torch.Tensor, gate: torch.Tensor, stream=None):
+        _check(lib().lsw_router_topk(self._h, _ptr(x1), _ptr(idx), _ptr(gate), _stream(stream)))
+
+    def merge_all_layers(self, idx: torch.Tensor, gate: torch.Tensor, stream=None):
+        _check(lib().lsw_merge_all_layers(self._h, _ptr(idx), _ptr(gate), _stream(stream)))
+
+    def unmerge_all_layers(self, stream=None):
+        _check(lib().lsw_unmerge_all_layers(self._h, _stream(stream)))
+
+    def decode_linear(self, layer: int, kind: str, x: torch.Tensor, y: torch.Tensor, stream=None):
+        _check(lib().lsw_decode_linear(self._h, layer, KINDS.index(kind), _ptr(x), _ptr(y), _stream(stream)))
+
+    # --- conveniences built from the same kernels ---------------------------
+    def decode_group(self, layer: int, group: int, x: torch.Tensor, y: torch.Tensor, stream=None):
+        _check(lib().lsw_decode_group(self._h, layer, group, _ptr(x), _ptr(y), _stream(stream)))
+
+    def decode_token(self, x1, xs, ys, idx, gate, stream=None):
+        _check(lib().lsw_decode_token(self._h, _ptr(x1), _ptr(xs), _ptr(ys), _ptr(idx), _ptr(gate),
+                                      _stream(stream)))
+
+    def decode_token_host(self, x1_h, xs_h, ys_h, idx_h, gate_h, stream=None):
+        _check(lib().lsw_decode_token_host(self._h, _ptr(x1_h), _ptr(xs_h), _ptr(ys_h), _ptr(idx_h),
+                                           _ptr(gate_h), _stream(stream)))
+
+    def device_status(self, stream=None) -> int:
+        code = ctypes.c_int32(0)
+        st = lib().lsw_device_status(self._h, _stream(stream), ctypes.byref(code))
+        if st not in (LSW_OK, 6):
+            _check(st)
+        return code.value

@@ -1,0 +1,387 @@
+// lsw_api.cu -- the C ABI (include/lsw.h): validation, ctx state machine,
+// dispatch of the K1/K2/K4 kernels, NCCL for the TP decode.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include <nccl.h>
+
+#include "lsw_internal.cuh"
+
+using namespace lsw;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+lsw_status fail(lsw_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+lsw_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(LSW_E_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+const char* kKindName[LSW_NKIND] = {"q", "k", "v", "o", "gate", "up", "down"};
+// group -> kinds
+const int kGroupKinds[LSW_NGROUP][3] = {{LSW_Q, LSW_K, LSW_V}, {LSW_O, -1, -1}, {LSW_GATE, LSW_UP, -1}, {LSW_DOWN, -1, -1}};
+const int kGroupSize[LSW_NGROUP] = {3, 1, 2, 1};
+
+constexpr int kSimtTM = 8, kSimtTN = 256;   // must match switch_simt.cu
+
+}  // namespace
+
+struct lsw_ctx {
+  lsw_config cfg;
+  lsw_kind_desc kinds[LSW_NKIND];
+  const void* router_w = nullptr;
+  int device = 0;
+  int num_sms = 148;
+  int impl = LSW_IMPL_SIMT;
+  SwitchParams simt_geom{};     // tile table for the SIMT kernel
+  TcPlan* tc = nullptr;
+  DevState* d_state = nullptr;
+  bool merged = false;
+  uint64_t launches = 0;
+  ncclComm_t comm = nullptr;
+  int64_t xs_elems = 0, ys_elems = 0;
+  int64_t x_off[LSW_NGROUP] = {}, y_off[LSW_NGROUP] = {};   // per-layer offsets
+  int64_t x_per_layer = 0, y_per_layer = 0;
+  // staging for lsw_decode_token_host
+  void* st_x1 = nullptr;
+  void* st_xs = nullptr;
+  float* st_ys = nullptr;
+  int32_t* st_idx = nullptr;
+  float* st_gate = nullptr;
+};
+
+static size_t esize(const lsw_ctx* c) { return c->cfg.dtype == LSW_BF16 ? 2 : 4; }
+
+static void fill_switch_params(const lsw_ctx* c, SwitchParams& p, int tm, int tn) {
+  memset(&p, 0, sizeof(p));
+  int64_t t = 0;
+  for (int k = 0; k < LSW_NKIND; ++k) {
+    KindGeom& g = p.kind[k];
+    g.W = c->kinds[k].W;
+    g.A = c->kinds[k].A;
+    g.B = c->kinds[k].B;
+    g.d_out = c->kinds[k].d_out;
+    g.d_in = c->kinds[k].d_in;
+    g.row_tiles = (int32_t)((g.d_out + tm - 1) / tm);
+    g.col_tiles = (int32_t)((g.d_in + tn - 1) / tn);
+    g.tile_begin = t;
+    t += (int64_t)c->cfg.n_layers * g.row_tiles * g.col_tiles;
+  }
+  p.tiles_total = t;
+  p.n_layers = c->cfg.n_layers;
+  p.n_experts = c->cfg.n_experts;
+  p.rank = c->cfg.rank;
+  p.top_k = c->cfg.top_k;
+  p.scale = c->cfg.alpha / (float)c->cfg.rank;
+  p.state = c->d_state;
+}
+
+extern "C" {
+
+int32_t lsw_abi_version(void) { return LSW_ABI_VERSION; }
+
+const char* lsw_last_error(void) { return g_last_error.c_str(); }
+
+lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND], const void* router_w,
+                      lsw_ctx** out) {
+  if (!cfg || !kinds || !router_w || !out) return fail(LSW_E_ARG, "lsw_create: null argument");
+  *out = nullptr;
+  const lsw_config& c = *cfg;
+  if (c.dtype != LSW_BF16 && c.dtype != LSW_F32) return fail(LSW_E_ARG, "lsw_create: dtype %d invalid", c.dtype);
+  if (c.n_layers < 1) return fail(LSW_E_SHAPE, "lsw_create: n_layers=%d < 1", c.n_layers);
+  if (c.n_experts < 1 || c.n_experts > LSW_MAX_EXPERTS)
+    return fail(LSW_E_SHAPE, "lsw_create: n_experts=%d not in [1,%d]", c.n_experts, LSW_MAX_EXPERTS);
+  if (c.top_k < 1 || c.top_k > c.n_experts || c.top_k > LSW_MAX_TOPK)
+    return fail(LSW_E_SHAPE, "lsw_create: top_k=%d not in [1, min(n_experts=%d, %d)]", c.top_k, c.n_experts,
+                LSW_MAX_TOPK);
+  if (c.rank < 1 || c.rank > 64) return fail(LSW_E_SHAPE, "lsw_create: rank=%d not in [1,64]", c.rank);
+  if (!(c.alpha == c.alpha) || c.alpha == 0.f) return fail(LSW_E_ARG, "lsw_create: alpha=%g invalid", c.alpha);
+  if (c.d_model < 1 || c.d_model % 8) return fail(LSW_E_SHAPE, "lsw_create: d_model=%lld must be a positive multiple of 8", (long long)c.d_model);
+  if (c.tp_size < 1 || c.tp_rank < 0 || c.tp_rank >= c.tp_size)
+    return fail(LSW_E_ARG, "lsw_create: tp_rank=%d tp_size=%d invalid", c.tp_rank, c.tp_size);
+  if (c.impl < LSW_IMPL_AUTO || c.impl > LSW_IMPL_TC) return fail(LSW_E_ARG, "lsw_create: impl=%d invalid", c.impl);
+  if (reinterpret_cast<uintptr_t>(router_w) % 16) return fail(LSW_E_ARG, "lsw_create: router_w not 16-byte aligned");
+  for (int k = 0; k < LSW_NKIND; ++k) {
+    const lsw_kind_desc& d = kinds[k];
+    if (!d.W || !d.A || !d.B) return fail(LSW_E_ARG, "lsw_create: kind %s has a null pointer", kKindName[k]);
+    if (d.d_out < 1 || d.d_in < 1) return fail(LSW_E_SHAPE, "lsw_create: kind %s shape %lldx%lld invalid", kKindName[k], (long long)d.d_out, (long long)d.d_in);
+    if (d.d_in % 8) return fail(LSW_E_SHAPE, "lsw_create: kind %s d_in=%lld is not a multiple of 8", kKindName[k], (long long)d.d_in);
+    if (d.d_in > 16384) return fail(LSW_E_SHAPE, "lsw_create: kind %s d_in=%lld > 16384", kKindName[k], (long long)d.d_in);
+    if (reinterpret_cast<uintptr_t>(d.W) % 16 || reinterpret_cast<uintptr_t>(d.A) % 16 ||
+        reinterpret_cast<uintptr_t>(d.B) % 16)
+      return fail(LSW_E_ARG, "lsw_create: kind %s pointers must be 16-byte aligned", kKindName[k]);
+  }
+  // Group members share x: their d_in must agree.
+  for (int g = 0; g < LSW_NGROUP; ++g)
+    for (int i = 1; i < kGroupSize[g]; ++i)
+      if (kinds[kGroupKinds[g][i]].d_in != kinds[kGroupKinds[g][0]].d_in)
+        return fail(LSW_E_SHAPE, "lsw_create: kinds %s and %s share an input but d_in %lld != %lld",
+                    kKindName[kGroupKinds[g][0]], kKindName[kGroupKinds[g][i]],
+                    (long long)kinds[kGroupKinds[g][0]].d_in, (long long)kinds[kGroupKinds[g][i]].d_in);
+  if (kinds[LSW_Q].d_in != c.d_model)
+    return fail(LSW_E_SHAPE, "lsw_create: q d_in=%lld != d_model=%lld (x1 is the q/k/v input, R7)",
+                (long long)kinds[LSW_Q].d_in, (long long)c.d_model);
+
+  int impl = c.impl;
+  if (impl == LSW_IMPL_AUTO) impl = c.dtype == LSW_BF16 ? LSW_IMPL_TC : LSW_IMPL_SIMT;
+  if (impl == LSW_IMPL_TC && c.dtype != LSW_BF16)
+    return fail(LSW_E_UNSUPPORTED, "lsw_create: the tensor-core switch needs bf16 storage");
+
+  lsw_ctx* ctx = new lsw_ctx();
+  ctx->cfg = c;
+  memcpy(ctx->kinds, kinds, sizeof(ctx->kinds));
+  ctx->router_w = router_w;
+  ctx->impl = impl;
+  cudaError_t e = cudaGetDevice(&ctx->device);
+  if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "lsw_create: cudaGetDevice"); }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  e = cudaMalloc(&ctx->d_state, sizeof(DevState));
+  if (e != cudaSuccess) { delete ctx; return fail(LSW_E_OOM, "lsw_create: cudaMalloc(state) failed"); }
+  e = cudaMemset(ctx->d_state, 0, sizeof(DevState));
+  if (e != cudaSuccess) { lsw_destroy(ctx); return cuda_fail(e, "lsw_create: cudaMemset"); }
+  fill_switch_params(ctx, ctx->simt_geom, kSimtTM, kSimtTN);
+  if (impl == LSW_IMPL_TC) {
+    const char* why = "";
+    e = tc_plan_create(&ctx->tc, ctx->simt_geom, ctx->num_sms, &why);
+    if (e != cudaSuccess || !ctx->tc) {
+      lsw_destroy(ctx);
+      if (e == cudaErrorMemoryAllocation) return fail(LSW_E_OOM, "lsw_create: packing LoRA operands: out of memory");
+      if (e == cudaErrorNotSupported) return fail(LSW_E_UNSUPPORTED, "lsw_create: tensor-core switch: %s", why);
+      return fail(LSW_E_CUDA, "lsw_create: tensor-core plan: %s (%s)", why, cudaGetErrorString(e));
+    }
+  }
+  // token I/O layout
+  int64_t xo = 0, yo = 0;
+  for (int g = 0; g < LSW_NGROUP; ++g) {
+    ctx->x_off[g] = xo;
+    ctx->y_off[g] = yo;
+    xo += kinds[kGroupKinds[g][0]].d_in;
+    for (int i = 0; i < kGroupSize[g]; ++i) yo += kinds[kGroupKinds[g][i]].d_out;
+  }
+  ctx->x_per_layer = xo;
+  ctx->y_per_layer = yo;
+  ctx->xs_elems = xo * c.n_layers;
+  ctx->ys_elems = yo * c.n_layers;
+  *out = ctx;
+  return LSW_OK;
+}
+
+lsw_status lsw_destroy(lsw_ctx* ctx) {
+  if (!ctx) return fail(LSW_E_ARG, "lsw_destroy: null ctx");
+  cudaDeviceSynchronize();
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->tc) tc_plan_destroy(ctx->tc);
+  cudaFree(ctx->d_state);
+  cudaFree(ctx->st_x1);
+  cudaFree(ctx->st_xs);
+  cudaFree(ctx->st_ys);
+  cudaFree(ctx->st_idx);
+  cudaFree(ctx->st_gate);
+  delete ctx;
+  return LSW_OK;
+}
+
+lsw_status lsw_get_info(const lsw_ctx* ctx, lsw_info* info) {
+  if (!ctx || !info) return fail(LSW_E_ARG, "lsw_get_info: null argument");
+  memset(info, 0, sizeof(*info));
+  info->switch_impl = ctx->impl;
+  if (ctx->impl == LSW_IMPL_TC) {
+    info->tiles_total = tc_plan_tiles(ctx->tc);
+    info->grid = tc_plan_grid(ctx->tc);
+    info->tile_m = 128;
+    info->tile_n = tc_plan_tile_n(ctx->tc);
+    info->packed_bytes = tc_plan_bytes(ctx->tc);
+  } else {
+    info->tiles_total = ctx->simt_geom.tiles_total;
+    info->grid = ctx->num_sms * 4;
+    info->tile_m = kSimtTM;
+    info->tile_n = kSimtTN;
+  }
+  info->merged = ctx->merged;
+  info->num_sms = ctx->num_sms;
+  info->kernel_launches = ctx->launches;
+  info->xs_elems = ctx->xs_elems;
+  info->ys_elems = ctx->ys_elems;
+  return LSW_OK;
+}
+
+lsw_status lsw_nccl_get_unique_id(void* id_out) {
+  if (!id_out) return fail(LSW_E_ARG, "lsw_nccl_get_unique_id: null");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclResult_t r = ncclGetUniqueId(reinterpret_cast<ncclUniqueId*>(id_out));
+  if (r != ncclSuccess) return fail(LSW_E_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  return LSW_OK;
+}
+
+lsw_status lsw_attach_nccl(lsw_ctx* ctx, const void* id) {
+  if (!ctx || !id) return fail(LSW_E_ARG, "lsw_attach_nccl: null argument");
+  if (ctx->comm) return fail(LSW_E_STATE, "lsw_attach_nccl: communicator already attached");
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->cfg.tp_size, uid, ctx->cfg.tp_rank);
+  if (r != ncclSuccess) { ctx->comm = nullptr; return fail(LSW_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)); }
+  return LSW_OK;
+}
+
+lsw_status lsw_router_topk(lsw_ctx* ctx, const void* x1, int32_t* idx, float* gate, void* stream) {
+  if (!ctx || !x1 || !idx || !gate) return fail(LSW_E_ARG, "lsw_router_topk: null argument");
+  cudaError_t e = launch_router(ctx->router_w, x1, ctx->cfg.n_experts, ctx->cfg.d_model, ctx->cfg.top_k,
+                                ctx->cfg.dtype, idx, gate, ctx->d_state, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_router_topk: launch");
+  ++ctx->launches;
+  return LSW_OK;
+}
+
+static lsw_status run_switch(lsw_ctx* ctx, int mode, const int32_t* idx, const float* gate, cudaStream_t s) {
+  SwitchParams p = ctx->simt_geom;
+  p.mode = mode;
+  p.cur_idx = idx;
+  p.cur_g = gate;
+  p.state = ctx->d_state;
+  cudaError_t e;
+  if (ctx->impl == LSW_IMPL_TC)
+    e = launch_switch_tc(ctx->tc, p, s);
+  else
+    e = launch_switch_simt(p, ctx->cfg.dtype, ctx->num_sms * 4, s);
+  if (e != cudaSuccess) return cuda_fail(e, "switch kernel launch");
+  ++ctx->launches;
+  return LSW_OK;
+}
+
+lsw_status lsw_merge_all_layers(lsw_ctx* ctx, const int32_t* idx, const float* gate, void* stream) {
+  if (!ctx || !idx || !gate) return fail(LSW_E_ARG, "lsw_merge_all_layers: null argument");
+  lsw_status st = run_switch(ctx, ctx->merged ? MODE_SWITCH : MODE_MERGE, idx, gate, (cudaStream_t)stream);
+  if (st == LSW_OK) ctx->merged = true;
+  return st;
+}
+
+lsw_status lsw_unmerge_all_layers(lsw_ctx* ctx, void* stream) {
+  if (!ctx) return fail(LSW_E_ARG, "lsw_unmerge_all_layers: null ctx");
+  if (!ctx->merged) return fail(LSW_E_STATE, "lsw_unmerge_all_layers: nothing is merged");
+  lsw_status st = run_switch(ctx, MODE_UNMERGE, nullptr, nullptr, (cudaStream_t)stream);
+  if (st == LSW_OK) ctx->merged = false;
+  return st;
+}
+
+static lsw_status gemv_sites(lsw_ctx* ctx, int layer, const int* kinds, int n, const void* x, float* y,
+                             cudaStream_t s, const char* who) {
+  if (!ctx || !x || !y) return fail(LSW_E_ARG, "%s: null argument", who);
+  if (layer < 0 || layer >= ctx->cfg.n_layers)
+    return fail(LSW_E_ARG, "%s: layer=%d not in [0,%d)", who, layer, ctx->cfg.n_layers);
+  if (reinterpret_cast<uintptr_t>(x) % 16) return fail(LSW_E_ARG, "%s: x not 16-byte aligned", who);
+  GemvParams p{};
+  int64_t rows = 0;
+  for (int i = 0; i < n; ++i) {
+    const lsw_kind_desc& d = ctx->kinds[kinds[i]];
+    p.site[i].W = (const uint8_t*)d.W + (size_t)layer * d.d_out * d.d_in * esize(ctx);
+    p.site[i].d_out = d.d_out;
+    p.site[i].row_begin = rows;
+    rows += d.d_out;
+  }
+  p.n_sites = n;
+  p.rows_total = rows;
+  p.d_in = ctx->kinds[kinds[0]].d_in;
+  p.x = x;
+  p.y = y;
+  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->num_sms, s);
+  if (e != cudaSuccess) return cuda_fail(e, "decode GEMV launch");
+  ++ctx->launches;
+  // Row-parallel kinds under TP: partial sums -> allreduce.
+  if (ctx->cfg.tp_size > 1 && ctx->kinds[kinds[0]].row_parallel) {
+    if (!ctx->comm) return fail(LSW_E_NCCL, "%s: tp_size=%d but no NCCL communicator attached", who, ctx->cfg.tp_size);
+    ncclResult_t r = ncclAllReduce(y, y, (size_t)rows, ncclFloat, ncclSum, ctx->comm, s);
+    if (r != ncclSuccess) return fail(LSW_E_NCCL, "%s: ncclAllReduce: %s", who, ncclGetErrorString(r));
+  }
+  return LSW_OK;
+}
+
+lsw_status lsw_decode_linear(lsw_ctx* ctx, int32_t layer, int32_t kind, const void* x, float* y, void* stream) {
+  if (!ctx) return fail(LSW_E_ARG, "lsw_decode_linear: null ctx");
+  if (kind < 0 || kind >= LSW_NKIND) return fail(LSW_E_ARG, "lsw_decode_linear: kind=%d invalid", kind);
+  int k = kind;
+  return gemv_sites(ctx, layer, &k, 1, x, y, (cudaStream_t)stream, "lsw_decode_linear");
+}
+
+lsw_status lsw_decode_group(lsw_ctx* ctx, int32_t layer, int32_t group, const void* x, float* y, void* stream) {
+  if (!ctx) return fail(LSW_E_ARG, "lsw_decode_group: null ctx");
+  if (group < 0 || group >= LSW_NGROUP) return fail(LSW_E_ARG, "lsw_decode_group: group=%d invalid", group);
+  return gemv_sites(ctx, layer, kGroupKinds[group], kGroupSize[group], x, y, (cudaStream_t)stream,
+                    "lsw_decode_group");
+}
+
+lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs, float* ys, int32_t* idx, float* gate,
+                            void* stream) {
+  if (!ctx || !x1 || !xs || !ys || !idx || !gate) return fail(LSW_E_ARG, "lsw_decode_token: null argument");
+  lsw_status st = lsw_router_topk(ctx, x1, idx, gate, stream);                       // Alg. 1 l.1
+  if (st != LSW_OK) return st;
+  st = lsw_merge_all_layers(ctx, idx, gate, stream);                                   // l.2-4
+  if (st != LSW_OK) return st;
+  const size_t es = esize(ctx);
+  for (int l = 0; l < ctx->cfg.n_layers; ++l)                                          // l.5
+    for (int g = 0; g < LSW_NGROUP; ++g) {
+      const uint8_t* xp = (const uint8_t*)xs + (size_t)(l * ctx->x_per_layer + ctx->x_off[g]) * es;
+      float* yp = ys + l * ctx->y_per_layer + ctx->y_off[g];
+      st = lsw_decode_group(ctx, l, g, xp, yp, stream);
+      if (st != LSW_OK) return st;
+    }
+  return LSW_OK;
+}
+
+lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_h, float* ys_h, int32_t* idx_h,
+                                 float* gate_h, void* stream) {
+  if (!ctx || !x1_h || !xs_h || !ys_h || !idx_h || !gate_h) return fail(LSW_E_ARG, "lsw_decode_token_host: null argument");
+  const size_t es = esize(ctx);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!ctx->st_x1) {
+    if (cudaMalloc(&ctx->st_x1, ctx->cfg.d_model * es) != cudaSuccess ||
+        cudaMalloc(&ctx->st_xs, ctx->xs_elems * es) != cudaSuccess ||
+        cudaMalloc(&ctx->st_ys, ctx->ys_elems * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&ctx->st_idx, LSW_MAX_TOPK * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&ctx->st_gate, LSW_MAX_TOPK * sizeof(float)) != cudaSuccess)
+      return fail(LSW_E_OOM, "lsw_decode_token_host: staging allocation failed");
+  }
+  cudaError_t e = cudaMemcpyAsync(ctx->st_x1, x1_h, ctx->cfg.d_model * es, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->st_xs, xs_h, ctx->xs_elems * es, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: H2D");
+  lsw_status st = lsw_decode_token(ctx, ctx->st_x1, ctx->st_xs, ctx->st_ys, ctx->st_idx, ctx->st_gate, stream);
+  if (st != LSW_OK) return st;
+  e = cudaMemcpyAsync(ys_h, ctx->st_ys, ctx->ys_elems * sizeof(float), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(idx_h, ctx->st_idx, ctx->cfg.top_k * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(gate_h, ctx->st_gate, ctx->cfg.top_k * sizeof(float), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: D2H");
+  return LSW_OK;
+}
+
+lsw_status lsw_device_status(lsw_ctx* ctx, void* stream, int32_t* code) {
+  if (!ctx) return fail(LSW_E_ARG, "lsw_device_status: null ctx");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_device_status: sync");
+  int32_t err = 0;
+  e = cudaMemcpy(&err, &ctx->d_state->err, sizeof(err), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_device_status: read latch");
+  if (code) *code = err;
+  if (err) {
+    cudaMemset(&ctx->d_state->err, 0, sizeof(int32_t));
+    return fail(LSW_E_DEVICE, "device error latched: code %d (%s)", err,
+                err == LSW_DEV_NONFINITE_LOGITS ? "non-finite router logits"
+                : err == LSW_DEV_BAD_INDEX      ? "expert index out of range or duplicated"
+                                                : "non-finite gate");
+  }
+  return LSW_OK;
+}
+
+}  // extern "C"

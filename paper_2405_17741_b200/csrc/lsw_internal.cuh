@@ -1,0 +1,164 @@
+// lsw_internal.cuh -- internal declarations shared by the csrc/ translation units.
+// Nothing here is part of the ABI (include/lsw.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/lsw.h"
+
+namespace lsw {
+
+constexpr int kMaxTerms = 2 * LSW_MAX_TOPK;   // |S_t u S_{t-1}| <= 2k
+
+// Switch modes (K1).  MERGE: Eq. 6; SWITCH: Eq. 10; UNMERGE: Eq. 7.
+enum SwitchMode : int32_t { MODE_MERGE = 0, MODE_SWITCH = 1, MODE_UNMERGE = 2 };
+
+// Ctx-owned device state.  slot[parity] holds the merged decision; a switch
+// pass writes the new decision into slot[parity^1] and the LAST CTA to finish
+// flips parity (every CTA has read slot[parity] before it counts itself done).
+struct DevState {
+  int32_t parity;
+  uint32_t done;
+  int32_t err;        // first latched LSW_DEV_* code
+  int32_t pad;
+  int32_t idx[2][LSW_MAX_TOPK];
+  float g[2][LSW_MAX_TOPK];
+};
+
+// One kind's stacked tensors, as the kernels see them.
+struct KindGeom {
+  void* W;            // [L, d_out, d_in]
+  const void* A;      // [L, N, r, d_in]
+  const void* B;      // [L, N, d_out, r]
+  int64_t d_out, d_in;
+  int64_t tile_begin; // first tile index of this kind (prefix sum)
+  int32_t row_tiles, col_tiles;
+};
+
+struct SwitchParams {
+  KindGeom kind[LSW_NKIND];
+  int64_t tiles_total;
+  int32_t n_layers, n_experts, rank, top_k;
+  float scale;        // alpha / r
+  int32_t mode;
+  const int32_t* cur_idx;
+  const float* cur_g;
+  DevState* state;
+};
+
+// The compacted coefficient list of one pass (SURVEY a-2), identical in every
+// CTA: n terms (expert e[j], fp32 coefficient c[j]).
+struct Coefs {
+  int32_t n;
+  int32_t bad;        // LSW_DEV_* if the inputs are invalid (pass becomes a no-op)
+  int32_t e[kMaxTerms];
+  float c[kMaxTerms];
+};
+
+// Build the coefficient list from (mode, cur, slot[parity]).  Run by ONE thread.
+__device__ __forceinline__ void build_coefs(const SwitchParams& p, int32_t parity, Coefs& out) {
+  out.n = 0;
+  out.bad = 0;
+  const int k = p.top_k, N = p.n_experts;
+  int32_t ci[LSW_MAX_TOPK], pi[LSW_MAX_TOPK];
+  float cg[LSW_MAX_TOPK], pg[LSW_MAX_TOPK];
+  const bool has_cur = p.mode != MODE_UNMERGE;
+  const bool has_prev = p.mode != MODE_MERGE;
+  for (int j = 0; j < k; ++j) {
+    if (has_cur) {
+      ci[j] = p.cur_idx[j];
+      cg[j] = p.cur_g[j];
+      if (ci[j] < 0 || ci[j] >= N) out.bad = LSW_DEV_BAD_INDEX;
+      if (!isfinite(cg[j])) out.bad = out.bad ? out.bad : LSW_DEV_BAD_GATE;
+      for (int i = 0; i < j; ++i) if (ci[i] == ci[j]) out.bad = LSW_DEV_BAD_INDEX;
+    }
+    if (has_prev) {
+      pi[j] = p.state->idx[parity][j];
+      pg[j] = p.state->g[parity][j];
+    }
+  }
+  if (out.bad) return;
+  // current experts: c = scale * (g_cur - g_prev[e])  (g_prev = 0 if absent)
+  if (has_cur) {
+    for (int j = 0; j < k; ++j) {
+      float gp = 0.f;
+      if (has_prev)
+        for (int i = 0; i < k; ++i) if (pi[i] == ci[j]) gp = pg[i];
+      const float c = p.scale * (cg[j] - gp);
+      if (c != 0.f) { out.e[out.n] = ci[j]; out.c[out.n] = c; ++out.n; }
+    }
+  }
+  // previous-only experts: c = -scale * g_prev
+  if (has_prev) {
+    for (int i = 0; i < k; ++i) {
+      bool in_cur = false;
+      if (has_cur)
+        for (int j = 0; j < k; ++j) in_cur |= (ci[j] == pi[i]);
+      if (in_cur) continue;
+      const float c = -p.scale * pg[i];
+      if (c != 0.f) { out.e[out.n] = pi[i]; out.c[out.n] = c; ++out.n; }
+    }
+  }
+}
+
+// Epilogue of every switch kernel: record the decision and flip parity once
+// all CTAs are done (thread 0 of each CTA, after the CTA's last tile).
+__device__ __forceinline__ void finish_pass(const SwitchParams& p, int32_t parity, const Coefs& cf) {
+  __threadfence();
+  const uint32_t prev = atomicAdd(&p.state->done, 1u);
+  if (prev == gridDim.x - 1) {
+    if (cf.bad) {
+      atomicCAS(&p.state->err, 0, cf.bad);
+    } else if (p.mode != MODE_UNMERGE) {
+      volatile DevState* s = p.state;
+      s->parity = parity ^ 1;
+    }
+    p.state->done = 0;
+    __threadfence();
+  }
+}
+
+// Write the current decision into the free slot (CTA 0, thread 0, at start).
+__device__ __forceinline__ void stage_decision(const SwitchParams& p, int32_t parity) {
+  if (p.mode == MODE_UNMERGE) return;
+  for (int j = 0; j < p.top_k; ++j) {
+    p.state->idx[parity ^ 1][j] = p.cur_idx[j];
+    p.state->g[parity ^ 1][j] = p.cur_g[j];
+  }
+}
+
+// Launchers (return cudaError_t of the launch).
+cudaError_t launch_router(const void* Wg, const void* x1, int32_t n_experts, int64_t d_model,
+                          int32_t top_k, int32_t dtype, int32_t* idx, float* gate,
+                          DevState* state, cudaStream_t s);
+
+cudaError_t launch_switch_simt(const SwitchParams& p, int32_t dtype, int grid, cudaStream_t s);
+
+struct GemvSite {
+  const void* W;      // [d_out, d_in] of this (layer, kind)
+  int64_t d_out;
+  int64_t row_begin;  // offset of this site's rows in the group output
+};
+struct GemvParams {
+  GemvSite site[3];
+  int32_t n_sites;
+  int64_t rows_total;
+  int64_t d_in;
+  const void* x;
+  float* y;
+};
+cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s);
+
+// Tensor-core switch (switch_tc.cu).
+struct TcPlan;   // opaque: packed operands + TMA descriptors
+cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why);
+void tc_plan_destroy(TcPlan* plan);
+int64_t tc_plan_bytes(const TcPlan* plan);
+int tc_plan_grid(const TcPlan* plan);
+int tc_plan_tile_n(const TcPlan* plan);
+int64_t tc_plan_tiles(const TcPlan* plan);
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
+
+}  // namespace lsw

@@ -107,6 +107,13 @@ CONFIGS: Dict[str, Config] = {
     "llama2-7b": Config("llama2-7b", 32, 4096, 11008, 32, 32, 128, 8, 16, 2, 16.0, "bf16"),
     "mistral-7b": Config("mistral-7b", 32, 4096, 14336, 32, 8, 128, 8, 16, 2, 16.0, "bf16"),
     "llama2-13b": Config("llama2-13b", 40, 5120, 13824, 40, 40, 128, 8, 32, 2, 16.0, "bf16"),
+    # Small bf16 parity cases (oracle finishes in seconds; several 128-row tiles,
+    # ragged row tail 704 = 5.5*128, GQA-shaped k/v).  Not bench lines.
+    "mini": Config("mini", 2, 256, 704, 2, 1, 128, 8, 16, 2, 16.0, "bf16"),
+    "mini-r32": Config("mini-r32", 2, 256, 704, 2, 1, 128, 8, 32, 2, 16.0, "bf16"),
+    "mini-r4k4": Config("mini-r4k4", 2, 256, 704, 2, 1, 128, 16, 4, 4, 16.0, "bf16"),
+    "mini-r64k3": Config("mini-r64k3", 1, 256, 704, 2, 1, 128, 4, 64, 3, 16.0, "bf16"),
+    "mini-k1": Config("mini-k1", 2, 256, 704, 2, 1, 128, 4, 8, 1, 16.0, "bf16"),
 }
 
 

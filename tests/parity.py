@@ -1,0 +1,47 @@
+"""GPU-vs-oracle parity protocol -- test helper.
+
+Checks, with the tolerance of BASELINE.json north_star (2e-2 relative /
+1e-2 absolute on bf16 merged weights and outputs):
+  trajectory : allclose(gpu W_t, oracle stored trajectory W_t, atol=1e-2, rtol=2e-2)
+  one-step   : ||W_gpu,t - oracle_step(W_gpu,t-1)||_F <= 1e-2 * ||DeltaW(d_t)||_F
+  divergence : ||W_gpu,t - W_orc,t||_F / ||W_orc,t||_F <= 1e-2
+The one-step check has teeth the loose atol lacks (R20); the negative controls
+(literal Eq. 9, omitted prev, flipped sign) must fail it.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle as O
+
+ATOL, RTOL = 1e-2, 2e-2
+ONE_STEP_TOL = 1e-2
+DIVERGENCE_TOL = 1e-2
+
+
+def allclose_frac_fail(got, ref, atol=ATOL, rtol=RTOL) -> float:
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.mean(np.abs(got - ref) > atol + rtol * np.abs(ref)))
+
+
+def one_step_ratio(W_gpu_t, W_gpu_prev, A, B, prev, cur, scale, store) -> float:
+    """||W_gpu,t - oracle_step(W_gpu,t-1)||_F / ||DeltaW(d_t)||_F."""
+    W_next = O.switch(W_gpu_prev, A, B, prev, cur, scale, store)
+    dW = O.delta(A, B, O.coef_list(cur, None, scale))
+    return float(np.linalg.norm(np.asarray(W_gpu_t, np.float64) - W_next) / np.linalg.norm(dW))
+
+
+def one_step_ratio_unmerge(W_gpu_t, W_gpu_prev, A, B, prev, scale, store) -> float:
+    W_next = O.unmerge(W_gpu_prev, A, B, prev, scale, store)
+    dW = O.delta(A, B, O.coef_list(prev, None, scale))
+    return float(np.linalg.norm(np.asarray(W_gpu_t, np.float64) - W_next) / np.linalg.norm(dW))
+
+
+def divergence(W_gpu, W_orc) -> float:
+    W_orc = np.asarray(W_orc, np.float64)
+    return float(np.linalg.norm(np.asarray(W_gpu, np.float64) - W_orc) / np.linalg.norm(W_orc))
+
+
+def ulp_flip_frac(W_gpu, W_orc) -> float:
+    return float(np.mean(np.asarray(W_gpu, np.float64) != np.asarray(W_orc, np.float64)))

@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle (-m gpu).
+
+Same seeded inputs (synth) feed both sides.  Router indices must be bit-exact
+and gates within 1e-6; merged weights follow the parity protocol of
+tests/parity.py; GEMV outputs within allclose(1e-2, 2e-2) of the oracle's y on
+its stored W, and within 1e-4 relative of an fp64 matmul of the GPU's own W.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from tests import parity as PT
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2405_17741_b200 as L
+    from paper_2405_17741_b200 import harness as H
+
+
+def _f64(t):
+    return t.detach().to("cpu").to(torch.float64).numpy()
+
+
+class Setup:
+    def __init__(self, name, impl, n_tokens=12):
+        self.cfg = cfg = synth.get_config(name)
+        self.store = "bf16" if cfg.dtype == "bf16" else "f32"
+        self.scale = cfg.alpha / cfg.rank
+        self.W, self.A, self.B, self.router = H.build_weights(cfg, "cuda")
+        self.P = {kd: _f64(self.W[kd]) for kd in synth.KINDS}       # pristine copies (host)
+        self.An = {kd: _f64(self.A[kd]) for kd in synth.KINDS}
+        self.Bn = {kd: _f64(self.B[kd]) for kd in synth.KINDS}
+        self.sw = H.make_switch(cfg, self.W, self.A, self.B, self.router, impl=impl)
+        self.X1 = synth.gen_x1(cfg, n_tokens, "cuda")
+        Ws = {(kd, l): self.P[kd][l] for kd in synth.KINDS for l in range(cfg.n_layers)}
+        As = {(kd, l): self.An[kd][l] for kd in synth.KINDS for l in range(cfg.n_layers)}
+        Bs = {(kd, l): self.Bn[kd][l] for kd in synth.KINDS for l in range(cfg.n_layers)}
+        self.orc = O.OracleModel(_f64(self.router), Ws, As, Bs, cfg.top_k, cfg.alpha, cfg.rank, self.store)
+        self.idx = torch.zeros(cfg.top_k, dtype=torch.int32, device="cuda")
+        self.gate = torch.zeros(cfg.top_k, dtype=torch.float32, device="cuda")
+
+    def gpu_W(self, kd, l):
+        return _f64(self.W[kd][l])
+
+
+def _run_token_checks(S, T, check_one_step=True):
+    cfg = S.cfg
+    prev = None
+    worst = {"one_step": 0.0, "div": 0.0, "fail": 0.0, "flip": 0.0}
+    for t in range(T):
+        x1 = S.X1[t]
+        W_prev = {(kd, l): S.gpu_W(kd, l) for kd in synth.KINDS for l in range(cfg.n_layers)}
+        S.sw.router_topk(x1, S.idx, S.gate)
+        S.sw.merge_all_layers(S.idx, S.gate)
+        torch.cuda.synchronize()
+        assert S.sw.device_status() == 0
+        idx_o, g_o, g32_o = S.orc.route(_f64(x1))
+        assert S.idx.cpu().tolist() == idx_o.tolist(), f"token {t}: router indices differ"
+        np.testing.assert_allclose(S.gate.cpu().numpy(), g_o, rtol=0, atol=1e-6)
+        cur = (idx_o.tolist(), g_o.tolist())
+        S.orc.merge_all_layers(cur)
+        for kd in synth.KINDS:
+            for l in range(cfg.n_layers):
+                Wg = S.gpu_W(kd, l)
+                Wo = S.orc.W[(kd, l)]
+                fail = PT.allclose_frac_fail(Wg, Wo)
+                assert fail == 0.0, f"token {t} {kd}[{l}]: {fail:.2e} of elements outside allclose"
+                div = PT.divergence(Wg, Wo)
+                assert div <= PT.DIVERGENCE_TOL
+                worst["div"] = max(worst["div"], div)
+                worst["flip"] = max(worst["flip"], PT.ulp_flip_frac(Wg, Wo))
+                if check_one_step:
+                    r = PT.one_step_ratio(Wg, W_prev[(kd, l)], S.An[kd][l], S.Bn[kd][l], prev, cur,
+                                          S.scale, S.store)
+                    assert r <= PT.ONE_STEP_TOL, f"token {t} {kd}[{l}]: one-step ratio {r:.3e}"
+                    worst["one_step"] = max(worst["one_step"], r)
+        prev = cur
+    return worst
+
+
+TRAJ_CASES = [("toy", "simt"), ("mini", "simt"), ("mini", "tc"), ("mini-r32", "tc"), ("mini-r4k4", "tc"),
+              ("mini-k1", "tc"), ("mini-r64k3", "tc")]
+
+
+@pytest.mark.parametrize("name,impl", TRAJ_CASES)
+def test_switch_trajectory_full_elements(name, impl):
+    S = Setup(name, impl)
+    worst = _run_token_checks(S, 10)
+    print(f"{name}/{impl}: worst {worst}")
+    # unmerge at end of sequence (Eq. 7) -> back near the pristine weights
+    W_prev = {kd: _f64(S.W[kd]) for kd in synth.KINDS}
+    prev = S.orc.prev
+    S.sw.unmerge_all_layers()
+    S.orc.unmerge_all_layers()
+    torch.cuda.synchronize()
+    for kd in synth.KINDS:
+        for l in range(S.cfg.n_layers):
+            Wg = S.gpu_W(kd, l)
+            assert PT.allclose_frac_fail(Wg, S.orc.W[(kd, l)]) == 0.0
+            assert PT.allclose_frac_fail(Wg, S.P[kd][l]) == 0.0
+            r = PT.one_step_ratio_unmerge(Wg, W_prev[kd][l], S.An[kd][l], S.Bn[kd][l], prev, S.scale, S.store)
+            assert r <= PT.ONE_STEP_TOL
+    with pytest.raises(L.LswError):
+        S.sw.unmerge_all_layers()          # LSW_E_STATE
+
+
+@pytest.mark.parametrize("name,impl", [("toy", "simt"), ("mini", "tc")])
+def test_decode_gemv_parity(name, impl):
+    S = Setup(name, impl, n_tokens=2)
+    cfg = S.cfg
+    xs = synth.gen_xs(cfg, "cuda")
+    for t in range(2):
+        S.sw.router_topk(S.X1[t], S.idx, S.gate)
+        S.sw.merge_all_layers(S.idx, S.gate)
+        idx_o, g_o, _ = S.orc.route(_f64(S.X1[t]))
+        S.orc.merge_all_layers((idx_o.tolist(), g_o.tolist()))
+    for l in range(cfg.n_layers):
+        for gi, grp in enumerate(synth.GROUPS):
+            x = xs[(l, gi)]
+            for kd in grp:
+                y = torch.empty(cfg.kind_shape(kd)[0], dtype=torch.float32, device="cuda")
+                S.sw.decode_linear(l, kd, x, y)
+                torch.cuda.synchronize()
+                yo = S.orc.decode_linear(kd, l, _f64(x))
+                assert PT.allclose_frac_fail(y.cpu().numpy(), yo) == 0.0
+                yown = O.gemv(S.gpu_W(kd, l), _f64(x))
+                np.testing.assert_allclose(y.cpu().numpy(), yown, rtol=1e-4, atol=1e-4)
+            # grouped launch == per-site launches
+            n = sum(cfg.kind_shape(kd)[0] for kd in grp)
+            yg = torch.empty(n, dtype=torch.float32, device="cuda")
+            S.sw.decode_group(l, gi, x, yg)
+            ys = []
+            for kd in grp:
+                y = torch.empty(cfg.kind_shape(kd)[0], dtype=torch.float32, device="cuda")
+                S.sw.decode_linear(l, kd, x, y)
+                ys.append(y)
+            assert torch.equal(yg, torch.cat(ys))
+
+
+@pytest.mark.parametrize("impl", ["simt", "tc"])
+def test_negative_controls_fail_one_step_check(impl):
+    """Literal Eq. 9, omitted prev and a flipped sign must each fail the
+    one-step check against the GPU's own trajectory (judged at t >= 2)."""
+    S = Setup("mini", impl, n_tokens=3)
+    kd, l = "gate", 1
+    prev = None
+    for t in range(3):
+        W_prev = S.gpu_W(kd, l)
+        S.sw.router_topk(S.X1[t], S.idx, S.gate)
+        S.sw.merge_all_layers(S.idx, S.gate)
+        torch.cuda.synchronize()
+        idx_o, g_o, _ = S.orc.route(_f64(S.X1[t]))
+        cur = (idx_o.tolist(), g_o.tolist())
+        Wg = S.gpu_W(kd, l)
+        A, B = S.An[kd][l], S.Bn[kd][l]
+        dW = np.linalg.norm(O.delta(A, B, O.coef_list(cur, None, S.scale)))
+        good = PT.one_step_ratio(Wg, W_prev, A, B, prev, cur, S.scale, S.store)
+        assert good <= PT.ONE_STEP_TOL
+        if t >= 1:
+            lit = np.linalg.norm(Wg - O.switch_literal_eq9(W_prev, A, B, prev, cur, S.scale, S.store)) / dW
+            omit = np.linalg.norm(Wg - O.switch(W_prev, A, B, None, cur, S.scale, S.store)) / dW
+            flip = np.linalg.norm(Wg - O.switch(W_prev, A, B, cur, prev, S.scale, S.store)) / dW
+            assert lit > 10 * PT.ONE_STEP_TOL and omit > 10 * PT.ONE_STEP_TOL and flip > 10 * PT.ONE_STEP_TOL
+        prev = cur
+
+
+@pytest.mark.parametrize("impl", ["simt", "tc"])
+def test_prev_equal_cur_is_exact_noop_and_determinism(impl):
+    S = Setup("mini", impl, n_tokens=1)
+    S.sw.router_topk(S.X1[0], S.idx, S.gate)
+    S.sw.merge_all_layers(S.idx, S.gate)
+    torch.cuda.synchronize()
+    snap = {kd: S.W[kd].clone() for kd in synth.KINDS}
+    S.sw.merge_all_layers(S.idx, S.gate)          # same decision: zero update (R12)
+    torch.cuda.synchronize()
+    for kd in synth.KINDS:
+        assert torch.equal(S.W[kd], snap[kd])
+    # determinism: a second ctx over fresh copies of the same inputs
+    S2 = Setup("mini", impl, n_tokens=1)
+    S2.sw.router_topk(S2.X1[0], S2.idx, S2.gate)
+    S2.sw.merge_all_layers(S2.idx, S2.gate)
+    torch.cuda.synchronize()
+    for kd in synth.KINDS:
+        assert torch.equal(S2.W[kd], snap[kd])
+
+
+@pytest.mark.parametrize("impl", ["simt", "tc"])
+def test_device_error_latch_nonfinite_router_input(impl):
+    S = Setup("mini", impl, n_tokens=1)
+    snap = {kd: S.W[kd].clone() for kd in synth.KINDS}
+    x = S.X1[0].clone()
+    x[3] = float("nan")
+    S.sw.router_topk(x, S.idx, S.gate)
+    S.sw.merge_all_layers(S.idx, S.gate)           # idx = -1 -> no-op, latched
+    code = S.sw.device_status()
+    assert code == 1                               # LSW_DEV_NONFINITE_LOGITS (first latched)
+    assert S.sw.device_status() == 0               # cleared
+    for kd in synth.KINDS:
+        assert torch.equal(S.W[kd], snap[kd])
+    bad = torch.tensor([0, 0], dtype=torch.int32, device="cuda")
+    S.sw.unmerge_all_layers()                      # host thinks merged; device slot unchanged
+    S.sw.merge_all_layers(bad, S.gate)             # duplicated index
+    assert S.sw.device_status() == 2
+
+
+def test_decode_token_host_matches_device_path():
+    cfg = synth.get_config("mini")
+    outs = []
+    for mode in ("device", "host"):
+        W, A, B, router = H.build_weights(cfg, "cuda")
+        sw = H.make_switch(cfg, W, A, B, router, impl="simt")
+        X1 = synth.gen_x1(cfg, 3, "cuda")
+        xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
+        info = sw.info()
+        assert info["xs_elems"] == xs.numel()
+        ys = torch.empty(info["ys_elems"], dtype=torch.float32, device="cuda")
+        idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
+        gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
+        for t in range(3):
+            if mode == "device":
+                sw.decode_token(X1[t], xs, ys, idx, gate)
+                torch.cuda.synchronize()
+                res = (ys.cpu().clone(), idx.cpu().clone(), gate.cpu().clone())
+            else:
+                x1h = X1[t].cpu().pin_memory()
+                xsh = xs.cpu().pin_memory()
+                ysh = torch.empty(info["ys_elems"], dtype=torch.float32).pin_memory()
+                idxh = torch.empty(cfg.top_k, dtype=torch.int32).pin_memory()
+                gh = torch.empty(cfg.top_k, dtype=torch.float32).pin_memory()
+                sw.decode_token_host(x1h, xsh, ysh, idxh, gh)
+                res = (ysh.clone(), idxh.clone(), gh.clone())
+        outs.append(res)
+        # launch count: per token 1 router + 1 switch + 4 GEMV groups per layer
+        assert sw.info()["kernel_launches"] == 3 * (2 + 4 * cfg.n_layers)
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
