@@ -3,17 +3,21 @@
 // y = W* x for every site of a group (sites that share x: q|k|v, o, gate|up,
 // down), one launch.  HBM-bound: each weight element is read once (2 B bf16).
 // One warp per output row: lanes stream the row with 128-bit loads (8 bf16 /
-// 4 fp32 per lane per step, coalesced 512 B per warp instruction), x is staged
-// once per CTA in shared memory, products accumulate in fp32, and the row sum
-// is a __shfl_xor_sync butterfly (north_star "warp-shuffle reductions").
-// Persistent grid: a multiple of the SM count; warps stride over rows.
+// 4 fp32 per lane per step, 512 B per warp instruction, fully coalesced) with
+// kUnroll independent loads in flight per lane; x is staged once per CTA in
+// shared memory; products accumulate in fp32 and the row sum is a
+// __shfl_xor_sync butterfly (north_star "warp-shuffle reductions").
+// Persistent, co-resident grid (a multiple of the SM count); rows are dealt
+// round-robin over CTAs first (row r -> CTA r % G), so every SM streams the
+// same number of rows (+-1) and the last round is spread over all SMs.
+#include <cstdlib>
+
 #include "lsw_internal.cuh"
 
 namespace lsw {
 
 constexpr int kGemvThreads = 512;
-constexpr int kGemvMaxDin = 16384;    // shared x: 32 KB bf16 / 64 KB fp32
-constexpr int kGemvUnroll = 4;        // independent 16-B loads in flight per lane
+constexpr int kGemvUnroll = 8;        // independent 16-B loads in flight per lane
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4 u, float* v) {
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -31,22 +35,51 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
   return r;
 }
 
-// bf16: a "chunk" is 8 elements (16 B).
+template <bool kBf16>
+__device__ __forceinline__ float dot_chunk(const uint4 w, const uint4* xs, int64_t c);
+
+template <>
+__device__ __forceinline__ float dot_chunk<true>(const uint4 wv, const uint4* xs, int64_t c) {
+  float w[8], x[8];
+  bf16x8_to_f32(wv, w);
+  bf16x8_to_f32(xs[c], x);
+  float a = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a = fmaf(w[q], x[q], a);
+  return a;
+}
+
+template <>
+__device__ __forceinline__ float dot_chunk<false>(const uint4 u, const uint4* xs, int64_t c) {
+  const float4 x = reinterpret_cast<const float4*>(xs)[c];
+  float a = __uint_as_float(u.x) * x.x;
+  a = fmaf(__uint_as_float(u.y), x.y, a);
+  a = fmaf(__uint_as_float(u.z), x.z, a);
+  a = fmaf(__uint_as_float(u.w), x.w, a);
+  return a;
+}
+
+// A "chunk" is 16 B: 8 bf16 or 4 fp32 elements.
+template <bool kBf16>
 __global__ void __launch_bounds__(kGemvThreads)
-gemv_bf16_kernel(const GemvParams p) {
+gemv_kernel(const GemvParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint4* xs = reinterpret_cast<uint4*>(smem_raw);
-  const int64_t nchunk = p.d_in / 8;
+  const int64_t nchunk = p.d_in / (kBf16 ? 8 : 4);
   const uint4* xg = reinterpret_cast<const uint4*>(p.x);
   for (int64_t i = threadIdx.x; i < nchunk; i += blockDim.x) xs[i] = xg[i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t row = warp; row < p.rows_total; row += nwarps) {
-    int s = 0;
-    while (s + 1 < p.n_sites && row >= p.site[s + 1].row_begin) ++s;
-    const uint4* wr = reinterpret_cast<const uint4*>(p.site[s].W) + (row - p.site[s].row_begin) * nchunk;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t G = gridDim.x;
+  // row r -> CTA r % G, warp (r / G) % nw
+  for (int64_t row = blockIdx.x + (int64_t)warp * G; row < p.rows_total; row += (int64_t)nw * G) {
+    // select the site with constant indices (no local-memory copy of the params)
+    const void* Wb = p.site[0].W;
+    int64_t rb = 0;
+    if (p.n_sites > 1 && row >= p.site[1].row_begin) { Wb = p.site[1].W; rb = p.site[1].row_begin; }
+    if (p.n_sites > 2 && row >= p.site[2].row_begin) { Wb = p.site[2].W; rb = p.site[2].row_begin; }
+    const uint4* wr = reinterpret_cast<const uint4*>(Wb) + (row - rb) * nchunk;
     float acc = 0.f;
     int64_t c = lane;
     for (; c + 32 * (kGemvUnroll - 1) < nchunk; c += 32 * kGemvUnroll) {
@@ -54,20 +87,17 @@ gemv_bf16_kernel(const GemvParams p) {
 #pragma unroll
       for (int u = 0; u < kGemvUnroll; ++u) wv[u] = ld_stream(wr + c + 32 * u);
 #pragma unroll
-      for (int u = 0; u < kGemvUnroll; ++u) {
-        float w[8], x[8];
-        bf16x8_to_f32(wv[u], w);
-        bf16x8_to_f32(xs[c + 32 * u], x);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc = fmaf(w[q], x[q], acc);
-      }
+      for (int u = 0; u < kGemvUnroll; ++u) acc += dot_chunk<kBf16>(wv[u], xs, c + 32 * u);
     }
-    for (; c < nchunk; c += 32) {
-      float w[8], x[8];
-      bf16x8_to_f32(ld_stream(wr + c), w);
-      bf16x8_to_f32(xs[c], x);
+    // ragged tail of the row: < kUnroll chunks per lane, still issued together
+    {
+      uint4 wv[kGemvUnroll];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc = fmaf(w[q], x[q], acc);
+      for (int u = 0; u < kGemvUnroll; ++u)
+        if (c + 32 * u < nchunk) wv[u] = ld_stream(wr + c + 32 * u);
+#pragma unroll
+      for (int u = 0; u < kGemvUnroll; ++u)
+        if (c + 32 * u < nchunk) acc += dot_chunk<kBf16>(wv[u], xs, c + 32 * u);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
@@ -75,52 +105,157 @@ gemv_bf16_kernel(const GemvParams p) {
   }
 }
 
-// fp32: a "chunk" is 4 elements (16 B).
-__global__ void __launch_bounds__(kGemvThreads)
-gemv_f32_kernel(const GemvParams p) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  float4* xs = reinterpret_cast<float4*>(smem_raw);
-  const int64_t nchunk = p.d_in / 4;
-  const float4* xg = reinterpret_cast<const float4*>(p.x);
-  for (int64_t i = threadIdx.x; i < nchunk; i += blockDim.x) xs[i] = xg[i];
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t row = warp; row < p.rows_total; row += nwarps) {
-    int s = 0;
-    while (s + 1 < p.n_sites && row >= p.site[s + 1].row_begin) ++s;
-    const float4* wr = reinterpret_cast<const float4*>(p.site[s].W) + (row - p.site[s].row_begin) * nchunk;
-    float acc = 0.f;
-    for (int64_t c = lane; c < nchunk; c += 32) {
-      const uint4 u = ld_stream(wr + c);
-      const float4 x = xs[c];
-      acc = fmaf(__uint_as_float(u.x), x.x, acc);
-      acc = fmaf(__uint_as_float(u.y), x.y, acc);
-      acc = fmaf(__uint_as_float(u.z), x.z, acc);
-      acc = fmaf(__uint_as_float(u.w), x.w, acc);
+// ---------------------------------------------------------------------------
+// Bulk-staged variant (default): one producer thread streams whole rows into a
+// ring of shared-memory slots with 1-D cp.async.bulk copies (one per row,
+// completion on an mbarrier), so ~200 KB per SM are in flight without any
+// register cost; 8 consumer warps reduce rows from shared memory (512 B per
+// warp instruction, conflict-free) against x (also in shared memory).
+constexpr int kBulkConsumers = 8;
+constexpr int kBulkThreads = 32 * (1 + kBulkConsumers);
+constexpr int kBulkMaxSlots = 32;
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint32_t g_mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+               : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok;
+}
+
+// Wait with a ~20 s watchdog (a protocol bug traps instead of hanging the GPU).
+__device__ __forceinline__ void g_mbar_wait(uint32_t bar, uint32_t parity) {
+  if (g_mbar_try(bar, parity)) return;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (uint32_t n = 1; !g_mbar_try(bar, parity); ++n) {
+    if ((n & 1023u) == 0) {
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) __trap();
     }
+  }
+}
+
+template <bool kBf16>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+gemv_bulk_kernel(const GemvParams p, int32_t slots, uint32_t slot_bytes) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t row_bytes = (uint32_t)(p.d_in * (kBf16 ? 2 : 4));
+  const uint32_t x_bytes = (row_bytes + 127) & ~127u;
+  uint8_t* xs = smem_raw;
+  uint8_t* ring = smem_raw + x_bytes;
+  const int64_t G = gridDim.x;
+  const int64_t my_rows = p.rows_total > blockIdx.x ? (p.rows_total - blockIdx.x + G - 1) / G : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < slots; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&full[s])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&empty[s])), "r"(1));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // x -> shared (all threads)
+  {
+    const uint4* xg = reinterpret_cast<const uint4*>(p.x);
+    uint4* xd = reinterpret_cast<uint4*>(xs);
+    for (uint32_t i = threadIdx.x; i < row_bytes / 16; i += blockDim.x) xd[i] = xg[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      for (int64_t i = 0; i < my_rows; ++i) {
+        const int s = (int)(i % slots);
+        const uint32_t ph = (uint32_t)((i / slots) & 1);
+        g_mbar_wait(s_u32(&empty[s]), ph ^ 1);
+        const int64_t row = blockIdx.x + i * G;
+        const void* Wb = p.site[0].W;
+        int64_t rb = 0;
+        if (p.n_sites > 1 && row >= p.site[1].row_begin) { Wb = p.site[1].W; rb = p.site[1].row_begin; }
+        if (p.n_sites > 2 && row >= p.site[2].row_begin) { Wb = p.site[2].W; rb = p.site[2].row_begin; }
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(Wb) + (row - rb) * (int64_t)row_bytes;
+        const uint32_t bar = s_u32(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+            ::"r"(s_u32(ring + (size_t)s * slot_bytes)), "l"(src), "r"(row_bytes), "r"(bar), "l"(pol)
+            : "memory");
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  const int64_t nchunk = row_bytes / 16;
+  const uint4* x4 = reinterpret_cast<const uint4*>(xs);
+  for (int64_t i = cw; i < my_rows; i += kBulkConsumers) {
+    const int s = (int)(i % slots);
+    g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
+    const uint4* w4 = reinterpret_cast<const uint4*>(ring + (size_t)s * slot_bytes);
+    float acc0 = 0.f, acc1 = 0.f;
+    int64_t c = lane;
+    for (; c + 32 < nchunk; c += 64) {
+      acc0 += dot_chunk<kBf16>(w4[c], x4, c);
+      acc1 += dot_chunk<kBf16>(w4[c + 32], x4, c + 32);
+    }
+    if (c < nchunk) acc0 += dot_chunk<kBf16>(w4[c], x4, c);
+    float acc = acc0 + acc1;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) p.y[row] = acc;
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[s])) : "memory");
+      p.y[blockIdx.x + i * G] = acc;
+    }
   }
+}
+
+static int gemv_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LSW_GEMV");
+    v = (e && e[0] == 'l') ? 0 : 1;       // "ldg" -> warp-per-row LDG kernel; default bulk
+  }
+  return v;
 }
 
 cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s) {
-  const size_t esz = dtype == LSW_BF16 ? 2 : 4;
-  const size_t smem = (size_t)p.d_in * esz;
+  const bool bf16 = dtype == LSW_BF16;
+  if (gemv_variant() == 1) {
+    const uint32_t row_bytes = (uint32_t)(p.d_in * (bf16 ? 2 : 4));
+    const uint32_t x_bytes = (row_bytes + 127) & ~127u;
+    const uint32_t slot_bytes = x_bytes;
+    const uint32_t budget = 220 * 1024;
+    int slots = (int)((budget - x_bytes) / slot_bytes);
+    if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
+    if (slots >= 2) {
+      const size_t smem = x_bytes + (size_t)slots * slot_bytes;
+      auto fn = bf16 ? gemv_bulk_kernel<true> : gemv_bulk_kernel<false>;
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int grid = (int)(p.rows_total < num_sms ? p.rows_total : num_sms);
+      if (grid < 1) grid = 1;
+      fn<<<grid, kBulkThreads, smem, s>>>(p, slots, slot_bytes);
+      return cudaGetLastError();
+    }
+  }
+  const size_t smem = (size_t)p.d_in * (bf16 ? 2 : 4);
+  auto fn = bf16 ? gemv_kernel<true> : gemv_kernel<false>;
+  static int occ_cache[2][8] = {};          // [dtype][smem bucket of 16 KB] -> CTAs per SM
+  const int bucket = (int)(smem >> 14) < 8 ? (int)(smem >> 14) : 7;
+  int& occ = occ_cache[bf16][bucket];
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (occ == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kGemvThreads, ((size_t)bucket + 1) << 14);
+    if (occ < 1) occ = 1;
+  }
   const int warps_per_cta = kGemvThreads / 32;
   int64_t want = (p.rows_total + warps_per_cta - 1) / warps_per_cta;
-  int64_t cap = (int64_t)num_sms * 4;
+  int64_t cap = (int64_t)num_sms * occ;
   int grid = (int)(want < cap ? want : cap);
   if (grid < 1) grid = 1;
-  if (dtype == LSW_BF16) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(gemv_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gemv_bf16_kernel<<<grid, kGemvThreads, smem, s>>>(p);
-  } else {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(gemv_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gemv_f32_kernel<<<grid, kGemvThreads, smem, s>>>(p);
-  }
+  fn<<<grid, kGemvThreads, smem, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -7,65 +7,75 @@
 // lsw_internal.cuh build_coefs).
 //
 // How:
-//  * Tile = 128 rows (UMMA M, one row per TMEM lane) x TN=64 columns of W.
-//    The tile sequence (kind, layer, row block, column block) is split into
-//    equal contiguous ranges, one per persistent CTA (grid = #SMs), so a CTA
-//    walks ALONG a 128-row strip: the strip's B slices (UMMA operand A,
-//    128 x r per expert, K-major) stay resident in shared memory while the W
-//    tile and the A slices (UMMA operand B: A^T, TN x r per expert, K-major,
-//    packed at create) stream through a multi-stage TMA/mbarrier ring.
-//  * One tcgen05.mma (kind::f16, bf16 in, fp32 accumulate) per expert per 16
-//    of r, each expert into ITS OWN TMEM accumulator: the gate coefficients
-//    c_j are then applied in fp32 in the epilogue (R13: exact fp32
-//    coefficients, not Eq. 5's bf16-rounded g*DOWN).  Accumulators are
-//    double-buffered in TMEM when 2 * terms * TN <= 512 columns, so the MMAs
-//    of tile i+1 overlap the epilogue of tile i.
+//  * A W tile is 128 rows x (64*nsub) columns (nsub = 2 by default, i.e. 256 B
+//    of each row per tile: B200's in-place read-modify-write stream loses ~20%
+//    of its bandwidth at 128-B row segments, scripts/membench.cu).  It is loaded
+//    by nsub 64-column TMA boxes (128B swizzle) into one ring stage, updated in
+//    place in shared memory and written back by nsub TMA bulk tensor stores.
+//    3-D tensor maps [L, d_out, d_in] zero-fill / clip ragged tiles and never
+//    spill into the next layer.
+//  * Each persistent CTA (grid = #SMs) walks one contiguous range of the tile
+//    sequence (kind, layer, row block, column block), i.e. ALONG 128-row strips:
+//    the strip's B slices (UMMA operand A: 128 x r per expert, K-major) stay
+//    resident in shared memory; the A slices (UMMA operand B: A^T, 64*nsub x r
+//    per expert, K-major) stream through their own ring.  Both come from ctx-
+//    owned copies packed at create time PRE-SWIZZLED into the exact shared-memory
+//    image the UMMA descriptors expect, so each slice is ONE contiguous
+//    cp.async.bulk copy (not 128 tiny 32-byte TMA rows).
+//  * One tcgen05.mma (kind::f16, bf16 in, fp32 accumulate, M=128, N=64, K=16)
+//    per expert per 16 of r per 64-column sub-tile, each expert into ITS OWN
+//    TMEM accumulator, double-buffered across sub-tiles: the gate coefficients
+//    c_j are applied in fp32 in the epilogue (R13: exact fp32 coefficients, not
+//    Eq. 5's bf16-rounded g*DOWN).
 //  * Epilogue (8 warps, 2 per TMEM lane quarter): tcgen05.ld the accumulators,
-//    delta = sum_j c_j acc_j, read the W tile from shared memory (128B-swizzled,
-//    conflict-free), W + delta in fp32, RNE to bf16, write back to the same
-//    shared buffer, then ONE TMA bulk tensor store writes the tile back in place
-//    (3-D tensor map [L, d_out, d_in]: ragged row/column tails are zero-filled
-//    on load and clipped on store, never spilling into the next layer).
-//  * Warp roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
-//    warps 2..9 = epilogue.
+//    W + sum_j c_j acc_j with packed fp32x2 FMAs (FFMA2), RNE to bf16, in place
+//    in the (conflict-free, 128B-swizzled) stage.
+//  * Warp roles: 0 = TMA/bulk producer, 1 = TMEM allocator + MMA issuer,
+//    2 = store warp (TMA stores, frees W stages as soon as they are read),
+//    3..10 = epilogue.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "lsw_internal.cuh"
 
 namespace lsw {
 
-constexpr int kTcTM = 128;
-constexpr int kTcTN = 64;                 // tile columns = UMMA N
+constexpr int kTcTM = 128;                 // tile rows = UMMA M = TMEM lanes
+constexpr int kTcTN = 64;                  // sub-tile columns = UMMA N
+constexpr int kSubBytes = kTcTM * kTcTN * 2;   // 16 KB: one swizzled W sub-tile
 constexpr int kTcEpiWarps = 8;
-constexpr int kTcThreads = 64 + 32 * kTcEpiWarps;
+constexpr int kTcFirstEpiWarp = 3;
+constexpr int kTcThreads = 32 * (kTcFirstEpiWarp + kTcEpiWarps);
 constexpr int kTcMaxStages = 8;
-constexpr int kWTileBytes = kTcTM * kTcTN * 2;   // 16 KB
+
+enum { ORDER_STRIP = 0, ORDER_SWEEP = 1 };
 
 struct TcMaps {
-  CUtensorMap w[LSW_NKIND];   // W   [L, d_out, d_in]      box {64, 128, 1}, 128B swizzle
-  CUtensorMap a[LSW_NKIND];   // A^T [L*N, d_in, rp]       box {rp, 64, 1}
-  CUtensorMap b[LSW_NKIND];   // B   [L*N, d_out, rp]      box {rp, 128, 1}
+  CUtensorMap w[LSW_NKIND];   // W [L, d_out, d_in], box {64, 128, 1}, 128B swizzle
 };
 
 struct TcKind {
   int64_t tile_begin;
   int32_t row_tiles, col_tiles;
+  int64_t din_pad, dout_pad;  // packed-operand row counts (multiples of 128)
+  const __nv_bfloat16* At;    // packed A^T [L*N, din_pad, rp], pre-swizzled
+  const __nv_bfloat16* Bp;    // packed B   [L*N, dout_pad, rp], pre-swizzled
 };
 
 struct TcGeom {
   TcKind kind[LSW_NKIND];
   int64_t tiles_total;
   int32_t n_layers, n_experts, rp;        // rp: rank padded to a multiple of 16
-  int32_t stages;                         // W+A ring depth
-  int32_t acc_bufs;                       // TMEM accumulator buffers (1 or 2)
-  int32_t b_bufs;                         // B-strip buffers (1 or 2)
+  int32_t nsub;                           // 64-column sub-tiles per W tile (1 or 2)
+  int32_t w_stages, a_stages, b_bufs, acc_bufs;
   int32_t max_terms;                      // 2k
   uint32_t tmem_cols;
-  uint32_t a_bytes_per_term;              // TN * rp * 2
+  uint32_t a_bytes_per_term;              // 64*nsub * rp * 2
   uint32_t b_bytes_per_term;              // 128 * rp * 2
+  uint32_t a_stage_bytes, b_buf_bytes, w_stage_bytes;
   uint32_t swz_mode;                      // UMMA layout type of the r-wide operands
   uint32_t smem_bytes;
 };
@@ -73,6 +83,7 @@ struct TcGeom {
 struct TcPlan {
   TcMaps maps;
   TcGeom geom;
+  int32_t order = ORDER_STRIP, chunk = 4, probe = 0;
   void* packed_At[LSW_NKIND] = {};
   void* packed_B[LSW_NKIND] = {};
   int64_t bytes = 0;
@@ -150,6 +161,15 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+// 1-D bulk copy global -> shared, completion on an mbarrier (transaction bytes)
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
+
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
@@ -198,12 +218,23 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
 
 // ------------------------------------------------------------------ tile walk
 
-struct TileCoord {
-  int kd, layer, rb, cb;
+// Per-CTA tile sequence over the global (kind, layer, row block, column block)
+// order.  ORDER_STRIP (default, measured best): one contiguous range per CTA.
+// ORDER_SWEEP: chunks of `chunk` consecutive tiles dealt round-robin.
+
+struct Cursor {
+  int64_t t;             // global tile index, -1 when done
+  int32_t kd, layer, rb, cb;
 };
 
-__device__ __forceinline__ TileCoord tile_coord(const TcGeom& g, int64_t t) {
-  TileCoord c;
+struct TileSeq {
+  int64_t T, t_begin, t_end;
+  int32_t order, chunk, G, b;
+};
+
+__device__ __forceinline__ void cursor_set(const TcGeom& g, Cursor& c, int64_t t) {
+  c.t = t;
+  if (t < 0) return;
   int kd = 0;
   while (kd + 1 < LSW_NKIND && t >= g.kind[kd + 1].tile_begin) ++kd;
   const TcKind& k = g.kind[kd];
@@ -214,13 +245,128 @@ __device__ __forceinline__ TileCoord tile_coord(const TcGeom& g, int64_t t) {
   local -= (int64_t)c.layer * per_layer;
   c.rb = (int)(local / k.col_tiles);
   c.cb = (int)(local - (int64_t)c.rb * k.col_tiles);
+}
+
+__device__ __forceinline__ Cursor cursor_first(const TcGeom& g, const TileSeq& q) {
+  Cursor c;
+  int64_t t = q.order == ORDER_STRIP ? (q.t_begin < q.t_end ? q.t_begin : -1)
+                                     : ((int64_t)q.b * q.chunk < q.T ? (int64_t)q.b * q.chunk : -1);
+  cursor_set(g, c, t);
   return c;
+}
+
+// Advance to the CTA's next tile: +1 inside a range/chunk (no division), a
+// jump (one division) between sweep chunks.
+__device__ __forceinline__ void cursor_next(const TcGeom& g, const TileSeq& q, Cursor& c) {
+  const int64_t t1 = c.t + 1;
+  const bool step = q.order == ORDER_STRIP ? (t1 < q.t_end) : (t1 % q.chunk != 0 && t1 < q.T);
+  if (step) {
+    c.t = t1;
+    if (++c.cb == g.kind[c.kd].col_tiles) {
+      c.cb = 0;
+      if (++c.rb == g.kind[c.kd].row_tiles) {
+        c.rb = 0;
+        if (++c.layer == g.n_layers) { c.layer = 0; ++c.kd; }
+      }
+    }
+    return;
+  }
+  if (q.order == ORDER_STRIP) { c.t = -1; return; }
+  const int64_t nq = c.t / q.chunk + q.G;
+  cursor_set(g, c, nq * q.chunk < q.T ? nq * q.chunk : -1);
+}
+
+__device__ __forceinline__ int64_t strip_id(const Cursor& c) { return c.t - c.cb; }
+
+// ring position: stage index + phase bit, advanced without division
+struct Ring {
+  uint32_t i, phase, n;
+  __device__ __forceinline__ void next() { if (++i == n) { i = 0; phase ^= 1u; } }
+};
+
+// ------------------------------------------------------------------ epilogue math
+
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);     // RNE, lo -> low half
+  return *reinterpret_cast<uint32_t*>(&b2);
+}
+
+// One 16-column chunk of one row: W (two swizzled 16-B smem chunks) <-
+// RNE(W + sum_j c_j acc_j), with the sum in fp32 pairs (FFMA2), W as the first
+// addend.  NT = number of accumulators (compile-time).
+template <int NT>
+__device__ __forceinline__ void epi_chunk(uint32_t tm_addr, const uint64_t* c2, uint8_t* wrow, int row, int col16) {
+  uint32_t acc[NT][16];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) tmem_ld16(tm_addr + j * kTcTN, acc[j]);
+  uint4* p0 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 0) ^ (row & 7)) << 4));
+  uint4* p1 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 1) ^ (row & 7)) << 4));
+  const uint4 u0 = *p0, u1 = *p1;
+  const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+  tmem_wait_ld();
+  uint32_t o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint64_t v = f2_pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+      v = ffma2(f2_pack(__uint_as_float(acc[j][2 * q]), __uint_as_float(acc[j][2 * q + 1])), c2[j], v);
+    o[q] = f2_to_bf16x2(v);
+  }
+  *p0 = make_uint4(o[0], o[1], o[2], o[3]);
+  *p1 = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+// General term count (> 4): groups of 4 accumulators.
+__device__ __forceinline__ void epi_chunk_many(uint32_t tm_addr, const float* cs, int nt, uint8_t* wrow, int row,
+                                               int col16) {
+  uint4* p0 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 0) ^ (row & 7)) << 4));
+  uint4* p1 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 1) ^ (row & 7)) << 4));
+  const uint4 u0 = *p0, u1 = *p1;
+  const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+  uint64_t v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = f2_pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
+  for (int j0 = 0; j0 < nt; j0 += 4) {
+    uint32_t acc[4][16];
+    const int nj = nt - j0 < 4 ? nt - j0 : 4;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+      if (jj < nj) tmem_ld16(tm_addr + (j0 + jj) * kTcTN, acc[jj]);
+    tmem_wait_ld();
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj)
+      if (jj < nj) {
+        const uint64_t c2 = f2_pack(cs[j0 + jj], cs[j0 + jj]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          v[q] = ffma2(f2_pack(__uint_as_float(acc[jj][2 * q]), __uint_as_float(acc[jj][2 * q + 1])), c2, v[q]);
+      }
+  }
+  uint32_t o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[q] = f2_to_bf16x2(v[q]);
+  *p0 = make_uint4(o[0], o[1], o[2], o[3]);
+  *p1 = make_uint4(o[4], o[5], o[6], o[7]);
 }
 
 // ------------------------------------------------------------------ the kernel
 
 struct TcArgs {
   TcGeom g;
+  int32_t order, chunk, probe;
   // coefficient inputs (same as SwitchParams)
   int32_t mode, top_k, n_experts;
   float scale;
@@ -235,19 +381,18 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
   __shared__ Coefs cf;
   __shared__ int32_t s_parity;
   __shared__ uint32_t s_tmem_base;
-  __shared__ __align__(8) uint64_t bar_full[kTcMaxStages], bar_empty[kTcMaxStages];
+  __shared__ __align__(8) uint64_t bar_wfull[kTcMaxStages], bar_wempty[kTcMaxStages], bar_wdone[kTcMaxStages];
+  __shared__ __align__(8) uint64_t bar_afull[2], bar_aempty[2];
   __shared__ __align__(8) uint64_t bar_bfull[2], bar_bempty[2];
   __shared__ __align__(8) uint64_t bar_accfull[2], bar_accempty[2];
 
   const TcGeom& g = args.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // shared layout: [stages x (W tile 16 KB | A slices)] [2 x B strip slices], 1 KB aligned
+  // shared layout (1 KB aligned): [w_stages x W tile][a_stages x A slices][b_bufs x B strip slices]
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t a_bytes = g.max_terms * g.a_bytes_per_term;
-  const uint32_t stage_bytes = (kWTileBytes + a_bytes + 1023) & ~1023u;
-  const uint32_t b_bytes = (g.max_terms * g.b_bytes_per_term + 1023) & ~1023u;
-  uint8_t* stage0 = base;
-  uint8_t* bstrip0 = base + (size_t)g.stages * stage_bytes;
+  uint8_t* wst0 = base;
+  uint8_t* ast0 = wst0 + (size_t)g.w_stages * g.w_stage_bytes;
+  uint8_t* bst0 = ast0 + (size_t)g.a_stages * g.a_stage_bytes;
 
   if (threadIdx.x == 0) {
     SwitchParams p{};
@@ -262,11 +407,14 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
     s_parity = parity;
     build_coefs(p, parity, cf);
     if (blockIdx.x == 0 && !cf.bad) stage_decision(p, parity);
-    for (int s = 0; s < g.stages; ++s) {
-      mbar_init(smem_u32(&bar_full[s]), 1);
-      mbar_init(smem_u32(&bar_empty[s]), 1);
+    for (int s = 0; s < g.w_stages; ++s) {
+      mbar_init(smem_u32(&bar_wfull[s]), 1);
+      mbar_init(smem_u32(&bar_wempty[s]), 1);
+      mbar_init(smem_u32(&bar_wdone[s]), kTcEpiWarps);
     }
     for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&bar_afull[s]), 1);
+      mbar_init(smem_u32(&bar_aempty[s]), 1);
       mbar_init(smem_u32(&bar_bfull[s]), 1);
       mbar_init(smem_u32(&bar_bempty[s]), 1);
       mbar_init(smem_u32(&bar_accfull[s]), 1);
@@ -274,13 +422,8 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0 && lane == 0) {
-    for (int k = 0; k < LSW_NKIND; ++k) {
-      prefetch_map(&maps.w[k]);
-      prefetch_map(&maps.a[k]);
-      prefetch_map(&maps.b[k]);
-    }
-  }
+  if (warp == 0 && lane == 0)
+    for (int k = 0; k < LSW_NKIND; ++k) prefetch_map(&maps.w[k]);
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  ::"r"(smem_u32(&s_tmem_base)), "r"(g.tmem_cols) : "memory");
@@ -291,164 +434,180 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
   tc_fence_after();
 
   const int nt = cf.bad ? 0 : cf.n;
-  const int64_t T = g.tiles_total;
-  const int64_t t_begin = T * blockIdx.x / gridDim.x;
-  const int64_t t_end = T * (blockIdx.x + 1) / gridDim.x;
+  // Tuning-only diagnostic levels (results are NOT the switch; never default):
+  //   probe=1: W stream only (no slices, no MMA, epilogue writes W back);
+  //   probe=2: full pipeline but the epilogue skips the TMEM reads / math.
+  const bool probe = args.probe == 1;
+  const bool skip_math = args.probe == 2;
+  const int nsub = g.nsub;
+  TileSeq seq;
+  seq.T = g.tiles_total;
+  seq.order = args.order;
+  seq.chunk = args.chunk < 1 ? 1 : args.chunk;
+  seq.G = gridDim.x;
+  seq.b = blockIdx.x;
+  seq.t_begin = seq.T * blockIdx.x / gridDim.x;
+  seq.t_end = seq.T * (blockIdx.x + 1) / gridDim.x;
   const uint32_t tmem_base = s_tmem_base;
+  const int tile_cols = kTcTN * nsub;
 
-  if (nt > 0 && t_begin < t_end) {
+  if (nt > 0) {
     if (warp == 0) {
-      // ============================ TMA producer ============================
+      // ============================ producer ===============================
       if (lane == 0) {
         const uint64_t pol_stream = policy_evict_first();
         const uint64_t pol_keep = policy_evict_last();
         int64_t strip_prev = -1;
-        uint32_t nstrip = 0;
-        uint32_t it = 0;
-        for (int64_t t = t_begin; t < t_end; ++t, ++it) {
-          const TileCoord c = tile_coord(g, t);
-          const int64_t strip = t - c.cb;            // unique id of the 128-row strip
-          if (strip != strip_prev) {
-            strip_prev = strip;
-            const uint32_t bs = nstrip % g.b_bufs, round = nstrip / g.b_bufs;
-            mbar_wait(smem_u32(&bar_bempty[bs]), (round & 1) ^ 1);
-            const uint32_t bar = smem_u32(&bar_bfull[bs]);
-            mbar_expect_tx(bar, nt * g.b_bytes_per_term);
-            uint8_t* dst = bstrip0 + (size_t)bs * b_bytes;
-            for (int j = 0; j < nt; ++j)
-              tma_load_3d(smem_u32(dst + j * g.b_bytes_per_term), &maps.b[c.kd], 0, c.rb * kTcTM,
-                          c.layer * g.n_experts + cf.e[j], bar, pol_keep);
-            ++nstrip;
+        Ring bring{0, 0, (uint32_t)g.b_bufs};
+        Ring aring{0, 0, (uint32_t)g.a_stages};
+        Ring wring{0, 0, (uint32_t)g.w_stages};
+        const size_t rpe = (size_t)g.rp;                   // elements per packed row
+        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
+          const TcKind& K = g.kind[c.kd];
+          if (!probe) {
+            if (strip_id(c) != strip_prev) {               // B slices of a new 128-row strip
+              if (strip_prev >= 0) bring.next();
+              strip_prev = strip_id(c);
+              mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
+              const uint32_t bar = smem_u32(&bar_bfull[bring.i]);
+              mbar_expect_tx(bar, nt * g.b_bytes_per_term);
+              uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
+              for (int j = 0; j < nt; ++j) {
+                const __nv_bfloat16* src =
+                    K.Bp + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.dout_pad + (size_t)c.rb * kTcTM) * rpe;
+                bulk_load(smem_u32(dst + j * g.b_bytes_per_term), src, g.b_bytes_per_term, bar, pol_keep);
+              }
+            }
+            // A^T slices of this tile's columns
+            mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
+            const uint32_t abar = smem_u32(&bar_afull[aring.i]);
+            mbar_expect_tx(abar, nt * g.a_bytes_per_term);
+            uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
+            for (int j = 0; j < nt; ++j) {
+              const __nv_bfloat16* src =
+                  K.At + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.din_pad + (size_t)c.cb * tile_cols) * rpe;
+              bulk_load(smem_u32(adst + j * g.a_bytes_per_term), src, g.a_bytes_per_term, abar, pol_keep);
+            }
+            aring.next();
           }
-          const uint32_t s = it % g.stages, round = it / g.stages;
-          mbar_wait(smem_u32(&bar_empty[s]), (round & 1) ^ 1);
-          const uint32_t bar = smem_u32(&bar_full[s]);
-          mbar_expect_tx(bar, kWTileBytes + nt * g.a_bytes_per_term);
-          uint8_t* st = stage0 + (size_t)s * stage_bytes;
-          tma_load_3d(smem_u32(st), &maps.w[c.kd], c.cb * kTcTN, c.rb * kTcTM, c.layer, bar, pol_stream);
-          for (int j = 0; j < nt; ++j)
-            tma_load_3d(smem_u32(st + kWTileBytes + j * g.a_bytes_per_term), &maps.a[c.kd], 0, c.cb * kTcTN,
-                        c.layer * g.n_experts + cf.e[j], bar, pol_keep);
+          // W tile: nsub adjacent 64-column boxes
+          mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
+          const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
+          mbar_expect_tx(wbar, nsub * kSubBytes);
+          uint8_t* wdst = wst0 + (size_t)wring.i * g.w_stage_bytes;
+          for (int sb = 0; sb < nsub; ++sb)
+            tma_load_3d(smem_u32(wdst + sb * kSubBytes), &maps.w[c.kd], c.cb * tile_cols + sb * kTcTN,
+                        c.rb * kTcTM, c.layer, wbar, pol_stream);
+          wring.next();
         }
       }
     } else if (warp == 1) {
       // ============================ MMA issuer ==============================
-      if (lane == 0) {
+      if (lane == 0 && !probe) {
         // instruction descriptor: D f32, A/B bf16, both K-major, N = 64, M = 128
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcTN >> 3) << 17) |
                                ((uint32_t)(kTcTM >> 4) << 24);
         const uint32_t row_bytes = g.rp * 2;
         const uint32_t sbo = 8 * row_bytes;
+        const int ksteps = g.rp / 16;
+        Ring bring{0, 0, (uint32_t)g.b_bufs};
+        Ring aring{0, 0, (uint32_t)g.a_stages};
+        Ring acc{0, 0, (uint32_t)g.acc_bufs};
+        Cursor c = cursor_first(g, seq);
         int64_t strip_prev = -1;
-        uint32_t nstrip = 0, bs = 0;
-        uint32_t it = 0;
-        for (int64_t t = t_begin; t < t_end; ++t, ++it) {
-          const TileCoord c = tile_coord(g, t);
-          const int64_t strip = t - c.cb;
+        while (c.t >= 0) {
+          const int64_t strip = strip_id(c);
           if (strip != strip_prev) {
+            if (strip_prev >= 0) bring.next();
             strip_prev = strip;
-            bs = nstrip % g.b_bufs;
-            mbar_wait(smem_u32(&bar_bfull[bs]), (nstrip / g.b_bufs) & 1);
-            ++nstrip;
+            mbar_wait(smem_u32(&bar_bfull[bring.i]), bring.phase);
           }
-          const uint32_t s = it % g.stages;
-          mbar_wait(smem_u32(&bar_full[s]), (it / g.stages) & 1);
-          const uint32_t ab = it % g.acc_bufs;
-          mbar_wait(smem_u32(&bar_accempty[ab]), ((it / g.acc_bufs) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t a_stage = smem_u32(stage0 + (size_t)s * stage_bytes + kWTileBytes);
-          const uint32_t b_strip = smem_u32(bstrip0 + (size_t)bs * b_bytes);
-          for (int j = 0; j < nt; ++j) {
-            const uint32_t d_tmem = tmem_base + (ab * g.max_terms + j) * kTcTN;
-            for (int kk = 0; kk < g.rp / 16; ++kk) {
-              const uint64_t adesc = umma_desc(b_strip + j * g.b_bytes_per_term + kk * 32, sbo, g.swz_mode);
-              const uint64_t bdesc = umma_desc(a_stage + j * g.a_bytes_per_term + kk * 32, sbo, g.swz_mode);
-              umma_f16(d_tmem, adesc, bdesc, idesc, kk > 0 ? 1u : 0u);
-            }
+          mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
+          const uint32_t a_stage = smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes);
+          const uint32_t b_strip = smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes);
+          for (int sb = 0; sb < nsub; ++sb) {
+            mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
+            tc_fence_after();
+            const uint32_t d0 = tmem_base + acc.i * g.max_terms * kTcTN;
+            const uint32_t a_sub = a_stage + sb * kTcTN * row_bytes;
+            for (int j = 0; j < nt; ++j)
+              for (int kk = 0; kk < ksteps; ++kk)
+                umma_f16(d0 + j * kTcTN, umma_desc(b_strip + j * g.b_bytes_per_term + kk * 32, sbo, g.swz_mode),
+                         umma_desc(a_sub + j * g.a_bytes_per_term + kk * 32, sbo, g.swz_mode), idesc,
+                         kk > 0 ? 1u : 0u);
+            umma_commit(smem_u32(&bar_accfull[acc.i]));
+            acc.next();
           }
-          umma_commit(smem_u32(&bar_accfull[ab]));
-          // B strip no longer needed after the last tile of the strip
-          const bool strip_ends = (t + 1 == t_end) || (c.cb + 1 == g.kind[c.kd].col_tiles);
-          if (strip_ends) umma_commit(smem_u32(&bar_bempty[bs]));
+          umma_commit(smem_u32(&bar_aempty[aring.i]));       // A slices consumed
+          aring.next();
+          // B strip no longer needed once this CTA's next tile is in another strip
+          cursor_next(g, seq, c);
+          if (c.t < 0 || strip_id(c) != strip) umma_commit(smem_u32(&bar_bempty[bring.i]));
         }
+      }
+    } else if (warp == 2) {
+      // ============================ store warp ==============================
+      if (lane == 0) {
+        const uint64_t pol_stream = policy_evict_first();
+        Ring wring{0, 0, (uint32_t)g.w_stages};
+        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
+          mbar_wait(smem_u32(&bar_wdone[wring.i]), wring.phase);     // epilogue wrote the tile
+          uint8_t* wsrc = wst0 + (size_t)wring.i * g.w_stage_bytes;
+          for (int sb = 0; sb < nsub; ++sb)
+            tma_store_3d(&maps.w[c.kd], smem_u32(wsrc + sb * kSubBytes), c.cb * tile_cols + sb * kTcTN,
+                         c.rb * kTcTM, c.layer, pol_stream);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read -> stage reusable
+          mbar_arrive(smem_u32(&bar_wempty[wring.i]));
+          wring.next();
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
     } else {
       // ============================ epilogue ================================
-      const int ew = warp - 2;                     // 0..7
+      const int ew = warp - kTcFirstEpiWarp;       // 0..7
       const int quarter = warp & 3;                // TMEM lane quarter this warp may access
-      const int half = ew >> 2;                    // which 32 of the 64 columns
+      const int half = ew >> 2;                    // which 32 of a sub-tile's 64 columns
       const int row = quarter * 32 + lane;         // tile-local row == TMEM lane
-      const bool store_thread = (ew == 0 && lane == 0);
-      const uint64_t pol_stream = policy_evict_first();
-      float cj[kMaxTerms];
+      uint64_t c2[4];
 #pragma unroll
-      for (int j = 0; j < kMaxTerms; ++j) cj[j] = j < nt ? cf.c[j] : 0.f;
-      uint32_t it = 0;
-      int32_t prev_stage = -1;
-      for (int64_t t = t_begin; t < t_end; ++t, ++it) {
-        const uint32_t s = it % g.stages;
-        const uint32_t ab = it % g.acc_bufs;
-        mbar_wait(smem_u32(&bar_full[s]), (it / g.stages) & 1);       // W tile landed (acquire)
-        mbar_wait(smem_u32(&bar_accfull[ab]), (it / g.acc_bufs) & 1);  // accumulators ready
-        tc_fence_after();
-        uint8_t* wt = stage0 + (size_t)s * stage_bytes;
-        const uint32_t tm_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + ab * g.max_terms * kTcTN;
+      for (int j = 0; j < 4; ++j) c2[j] = j < nt ? f2_pack(cf.c[j], cf.c[j]) : 0ull;
+      const int ntc = (probe || skip_math) ? 0 : nt;
+      Ring wring{0, 0, (uint32_t)g.w_stages};
+      Ring acc{0, 0, (uint32_t)g.acc_bufs};
+      for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
+        mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);          // W tile landed (acquire)
+        uint8_t* wt = wst0 + (size_t)wring.i * g.w_stage_bytes;
+        for (int sb = 0; sb < nsub; ++sb) {
+          if (!probe) mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);  // accumulators ready
+          tc_fence_after();
+          uint8_t* wrow = wt + sb * kSubBytes + row * 128;
+          const uint32_t tm_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * g.max_terms * kTcTN;
 #pragma unroll
-        for (int q2 = 0; q2 < 2; ++q2) {
-          const int col16 = half * 2 + q2;         // 16-column chunk 0..3
-          float d[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) d[i] = 0.f;
-          for (int j0 = 0; j0 < nt; j0 += 4) {
-            uint32_t acc[4][16];
-            const int nj = nt - j0 < 4 ? nt - j0 : 4;
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-              if (jj < nj) tmem_ld16(tm_row + (j0 + jj) * kTcTN + col16 * 16, acc[jj]);
-            tmem_wait_ld();
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-              if (jj < nj) {
-                const float c = cj[j0 + jj];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) d[i] = fmaf(c, __uint_as_float(acc[jj][i]), d[i]);
-              }
-          }
-          // W row chunk: two 16-B swizzled chunks (8 bf16 each) of this row's 128-B line
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int chunk = col16 * 2 + h;
-            uint4* p = reinterpret_cast<uint4*>(wt + row * 128 + ((chunk ^ (row & 7)) << 4));
-            uint4 u = *p;
-            uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float lo = __uint_as_float(w[i] << 16) + d[h * 8 + 2 * i];
-              const float hi = __uint_as_float(w[i] & 0xffff0000u) + d[h * 8 + 2 * i + 1];
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);
-              w[i] = *reinterpret_cast<uint32_t*>(&b2);
+          for (int q2 = 0; q2 < 2; ++q2) {
+            const int col16 = half * 2 + q2;       // 16-column chunk 0..3 of the sub-tile
+            const uint32_t ta = tm_row + col16 * 16;
+            switch (ntc) {
+              case 0: break;
+              case 1: epi_chunk<1>(ta, c2, wrow, row, col16); break;
+              case 2: epi_chunk<2>(ta, c2, wrow, row, col16); break;
+              case 3: epi_chunk<3>(ta, c2, wrow, row, col16); break;
+              case 4: epi_chunk<4>(ta, c2, wrow, row, col16); break;
+              default: epi_chunk_many(ta, cf.c, ntc, wrow, row, col16); break;
             }
-            *p = make_uint4(w[0], w[1], w[2], w[3]);
           }
+          // accumulators consumed -> MMA may reuse this TMEM buffer
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0 && !probe) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+          acc.next();
         }
-        // accumulators consumed -> MMA may reuse this TMEM buffer
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[ab]));
-        // make generic-proxy smem writes visible to the TMA (async proxy), then store
+        // generic-proxy smem writes -> visible to the TMA store (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        named_bar(1, 32 * kTcEpiWarps);
-        if (store_thread) {
-          const TileCoord c = tile_coord(g, t);
-          tma_store_3d(&maps.w[c.kd], smem_u32(wt), c.cb * kTcTN, c.rb * kTcTM, c.layer, pol_stream);
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          // the previous tile's store has finished reading smem -> free its stage
-          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          if (prev_stage >= 0) mbar_arrive(smem_u32(&bar_empty[prev_stage]));
-          prev_stage = (int32_t)s;
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
+        wring.next();
       }
-      if (store_thread) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
   }
   tc_fence_before();
@@ -468,26 +627,40 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
 
 // ------------------------------------------------------------------ packing
 
-// A [L*N, r, d_in] -> A^T [L*N, d_in, rp] (zero-padded rank)
-__global__ void pack_At_kernel(const __nv_bfloat16* __restrict__ A, __nv_bfloat16* __restrict__ At, int64_t LN,
-                               int r, int rp, int64_t d_in) {
-  const int64_t total = LN * d_in * rp;
+// Pre-swizzled K-major operand image: element (row, k) of a [rows, rp] operand
+// goes to 16-byte chunk (k/8) ^ f(row) of its row, f = the TMA/UMMA swizzle of
+// row-byte width RB = 2*rp (32B: (row>>2)&1, 64B: (row>>1)&3, 128B: row&7), so
+// a 1-D bulk copy of 128 rows to a 1 KB-aligned shared address reproduces what a
+// swizzled TMA load would have written.  Rows >= n_rows and ranks >= r are 0.
+__device__ __forceinline__ int64_t swz_off(int64_t row, int k, int rp) {
+  const int rb = 2 * rp;
+  const int f = (int)((row * rb / 128) & (rb / 16 - 1));
+  return row * rp + (((k >> 3) ^ f) << 3) + (k & 7);
+}
+
+// A [M, r, d_in] -> A^T [M, din_pad, rp]
+__global__ void pack_At_kernel(const __nv_bfloat16* __restrict__ A, __nv_bfloat16* __restrict__ At, int64_t M,
+                               int r, int rp, int64_t d_in, int64_t din_pad) {
+  const int64_t total = M * din_pad * rp;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int rho = (int)(i % rp);
-    const int64_t c = (i / rp) % d_in;
-    const int64_t m = i / ((int64_t)rp * d_in);
-    At[i] = rho < r ? A[(m * r + rho) * d_in + c] : __float2bfloat16(0.f);
+    const int k = (int)(i % rp);
+    const int64_t c = (i / rp) % din_pad;
+    const int64_t m = i / ((int64_t)rp * din_pad);
+    const __nv_bfloat16 v = (k < r && c < d_in) ? A[(m * r + k) * d_in + c] : __float2bfloat16(0.f);
+    At[m * din_pad * rp + swz_off(c, k, rp)] = v;
   }
 }
 
-// B [L*N, d_out, r] -> [L*N, d_out, rp] (zero-padded rank), only when r % 16 != 0
-__global__ void pack_B_kernel(const __nv_bfloat16* __restrict__ B, __nv_bfloat16* __restrict__ Bp, int64_t rows,
-                              int r, int rp) {
-  const int64_t total = rows * rp;
+// B [M, d_out, r] -> [M, dout_pad, rp]
+__global__ void pack_B_kernel(const __nv_bfloat16* __restrict__ B, __nv_bfloat16* __restrict__ Bp, int64_t M,
+                              int r, int rp, int64_t d_out, int64_t dout_pad) {
+  const int64_t total = M * dout_pad * rp;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int rho = (int)(i % rp);
-    const int64_t row = i / rp;
-    Bp[i] = rho < r ? B[row * r + rho] : __float2bfloat16(0.f);
+    const int k = (int)(i % rp);
+    const int64_t row = (i / rp) % dout_pad;
+    const int64_t m = i / ((int64_t)rp * dout_pad);
+    const __nv_bfloat16 v = (k < r && row < d_out) ? B[(m * d_out + row) * r + k] : __float2bfloat16(0.f);
+    Bp[m * dout_pad * rp + swz_off(row, k, rp)] = v;
   }
 }
 
@@ -505,19 +678,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-static bool encode3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
-                     uint32_t b1, CUtensorMapSwizzle swz) {
+static bool encode_w(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d_out, uint64_t L) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[3] = {d0, d1, d2};
-  cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
-  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint64_t dims[3] = {d_in, d_out, L};
+  cuuint64_t strides[2] = {d_in * 2, d_in * d_out * 2};
+  cuuint32_t box[3] = {(cuuint32_t)kTcTN, (cuuint32_t)kTcTM, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+
+static uint32_t align1k(uint32_t x) { return (x + 1023) & ~1023u; }
 
 cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, const char** why) {
   *out = nullptr;
@@ -535,35 +709,60 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   g.n_experts = sp.n_experts;
   g.rp = rp;
   g.max_terms = 2 * sp.top_k;
-  g.a_bytes_per_term = kTcTN * rp * 2;
-  g.b_bytes_per_term = kTcTM * rp * 2;
   g.swz_mode = rp == 16 ? 6u : rp == 32 ? 4u : 2u;        // SWIZZLE_32B / 64B / 128B (UMMA encoding)
-  const CUtensorMapSwizzle tswz = rp == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
-                                  : rp == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
   const uint32_t cols1 = (uint32_t)g.max_terms * kTcTN;
   if (cols1 > 512) { delete plan; *why = "2*top_k*64 TMEM columns exceed 512"; return cudaErrorNotSupported; }
   g.acc_bufs = cols1 * 2 <= 512 ? 2 : 1;
   uint32_t need = cols1 * g.acc_bufs, cols = 32;
   while (cols < need) cols <<= 1;
   g.tmem_cols = cols;
-  const uint32_t stage_bytes = (kWTileBytes + g.max_terms * g.a_bytes_per_term + 1023) & ~1023u;
-  const uint32_t b_bytes = (g.max_terms * g.b_bytes_per_term + 1023) & ~1023u;
+  // shared-memory plan: prefer 2 sub-tiles per W tile, >= 4 W stages, 2 A stages, 2 B buffers
   const uint32_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
-  int stages = kTcMaxStages, bbufs = 2;
-  while (stages > 2 && (uint32_t)stages * stage_bytes + bbufs * b_bytes > budget) --stages;
-  if ((uint32_t)stages * stage_bytes + bbufs * b_bytes > budget) bbufs = 1;
-  if ((uint32_t)stages * stage_bytes + bbufs * b_bytes > budget) {
-    delete plan; *why = "shared memory: rank * top_k too large"; return cudaErrorNotSupported;
+  g.b_bytes_per_term = kTcTM * rp * 2;
+  bool ok = false;
+  int nsub_env = 0;
+  if (const char* v = getenv("LSW_TC_NSUB")) nsub_env = atoi(v);
+  for (int nsub = 2; nsub >= 1 && !ok; --nsub) {
+    if (nsub_env && nsub != nsub_env) continue;
+    const uint32_t a_term = kTcTN * nsub * rp * 2;
+    const uint32_t a_stage = align1k(g.max_terms * a_term);
+    const uint32_t b_buf = align1k(g.max_terms * g.b_bytes_per_term);
+    const uint32_t w_stage = nsub * kSubBytes;
+    for (int bbufs = 2; bbufs >= 1 && !ok; --bbufs)
+      for (int astages = 2; astages >= 1 && !ok; --astages) {
+        int ws = (int)((budget - (int64_t)bbufs * b_buf - (int64_t)astages * a_stage) / w_stage);
+        if ((int64_t)budget < (int64_t)bbufs * b_buf + (int64_t)astages * a_stage) ws = 0;
+        if (ws > kTcMaxStages) ws = kTcMaxStages;
+        const int min_ws = nsub == 2 ? 4 : 3;
+        if (ws >= min_ws || (nsub == 1 && ws >= 2 && bbufs == 1 && astages == 1)) {
+          ok = true;
+          g.nsub = nsub;
+          g.w_stages = ws;
+          g.a_stages = astages;
+          g.b_bufs = bbufs;
+          g.a_bytes_per_term = a_term;
+          g.a_stage_bytes = a_stage;
+          g.b_buf_bytes = b_buf;
+          g.w_stage_bytes = w_stage;
+        }
+      }
   }
-  g.stages = stages;
-  g.b_bufs = bbufs;
-  g.smem_bytes = stages * stage_bytes + bbufs * b_bytes + 1024;
+  if (!ok) { delete plan; *why = "shared memory: rank * top_k too large"; return cudaErrorNotSupported; }
+  // tuning knobs (defaults are the measured best)
+  if (const char* v = getenv("LSW_TC_STAGES")) { int x = atoi(v); if (x >= 2 && x < g.w_stages) g.w_stages = x; }
+  if (const char* v = getenv("LSW_TC_ORDER")) plan->order = strcmp(v, "sweep") == 0 ? ORDER_SWEEP : ORDER_STRIP;
+  if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
+  if (const char* v = getenv("LSW_TC_PROBE")) plan->probe = atoi(v);
+  g.smem_bytes = g.w_stages * g.w_stage_bytes + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
   // tiles
+  const int tile_cols = kTcTN * g.nsub;
   int64_t t = 0;
   for (int k = 0; k < LSW_NKIND; ++k) {
     const KindGeom& kg = sp.kind[k];
     g.kind[k].row_tiles = (int32_t)((kg.d_out + kTcTM - 1) / kTcTM);
-    g.kind[k].col_tiles = (int32_t)((kg.d_in + kTcTN - 1) / kTcTN);
+    g.kind[k].col_tiles = (int32_t)((kg.d_in + tile_cols - 1) / tile_cols);
+    g.kind[k].din_pad = (int64_t)g.kind[k].col_tiles * tile_cols;
+    g.kind[k].dout_pad = (int64_t)g.kind[k].row_tiles * kTcTM;
     g.kind[k].tile_begin = t;
     t += (int64_t)sp.n_layers * g.kind[k].row_tiles * g.kind[k].col_tiles;
   }
@@ -571,27 +770,24 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   plan->grid = (int)(t < num_sms ? t : num_sms);
   if (plan->grid < 1) plan->grid = 1;
   // pack operands + encode maps
-  const int64_t LN = (int64_t)sp.n_layers * sp.n_experts;
+  const int64_t M = (int64_t)sp.n_layers * sp.n_experts;
   cudaError_t e = cudaSuccess;
   for (int k = 0; k < LSW_NKIND && e == cudaSuccess; ++k) {
     const KindGeom& kg = sp.kind[k];
-    const size_t at_bytes = (size_t)LN * kg.d_in * rp * 2;
+    const size_t at_bytes = (size_t)M * g.kind[k].din_pad * rp * 2;
+    const size_t b_bytes = (size_t)M * g.kind[k].dout_pad * rp * 2;
     e = cudaMalloc(&plan->packed_At[k], at_bytes);
     if (e != cudaSuccess) break;
-    plan->bytes += at_bytes;
-    pack_At_kernel<<<1024, 256>>>((const __nv_bfloat16*)kg.A, (__nv_bfloat16*)plan->packed_At[k], LN, r, rp, kg.d_in);
-    const void* Bsrc = kg.B;
-    if (rp != r) {
-      const size_t b_bytes_k = (size_t)LN * kg.d_out * rp * 2;
-      e = cudaMalloc(&plan->packed_B[k], b_bytes_k);
-      if (e != cudaSuccess) break;
-      plan->bytes += b_bytes_k;
-      pack_B_kernel<<<1024, 256>>>((const __nv_bfloat16*)kg.B, (__nv_bfloat16*)plan->packed_B[k], LN * kg.d_out, r, rp);
-      Bsrc = plan->packed_B[k];
-    }
-    if (!encode3d(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers, kTcTN, kTcTM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode3d(&plan->maps.a[k], plan->packed_At[k], rp, kg.d_in, LN, rp, kTcTN, tswz) ||
-        !encode3d(&plan->maps.b[k], Bsrc, rp, kg.d_out, LN, rp, kTcTM, tswz)) {
+    e = cudaMalloc(&plan->packed_B[k], b_bytes);
+    if (e != cudaSuccess) break;
+    plan->bytes += at_bytes + b_bytes;
+    pack_At_kernel<<<2048, 256>>>((const __nv_bfloat16*)kg.A, (__nv_bfloat16*)plan->packed_At[k], M, r, rp,
+                                  kg.d_in, g.kind[k].din_pad);
+    pack_B_kernel<<<2048, 256>>>((const __nv_bfloat16*)kg.B, (__nv_bfloat16*)plan->packed_B[k], M, r, rp,
+                                 kg.d_out, g.kind[k].dout_pad);
+    g.kind[k].At = (const __nv_bfloat16*)plan->packed_At[k];
+    g.kind[k].Bp = (const __nv_bfloat16*)plan->packed_B[k];
+    if (!encode_w(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers)) {
       *why = "cuTensorMapEncodeTiled failed";
       e = cudaErrorInvalidValue;
     }
@@ -620,12 +816,15 @@ void tc_plan_destroy(TcPlan* plan) {
 
 int64_t tc_plan_bytes(const TcPlan* plan) { return plan ? plan->bytes : 0; }
 int tc_plan_grid(const TcPlan* plan) { return plan ? plan->grid : 0; }
-int tc_plan_tile_n(const TcPlan*) { return kTcTN; }
+int tc_plan_tile_n(const TcPlan* plan) { return plan ? kTcTN * plan->geom.nsub : 0; }
 int64_t tc_plan_tiles(const TcPlan* plan) { return plan ? plan->geom.tiles_total : 0; }
 
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s) {
   TcArgs a;
   a.g = plan->geom;
+  a.order = plan->order;
+  a.chunk = plan->chunk;
+  a.probe = plan->probe;
   a.mode = p.mode;
   a.top_k = p.top_k;
   a.n_experts = p.n_experts;
