@@ -139,76 +139,102 @@ __device__ __forceinline__ void g_mbar_wait(uint32_t bar, uint32_t parity) {
 
 template <bool kBf16>
 __global__ void __launch_bounds__(kBulkThreads, 1)
-gemv_bulk_kernel(const GemvParams p, int32_t slots, uint32_t slot_bytes) {
+gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row_bytes = (uint32_t)(p.d_in * (kBf16 ? 2 : 4));
   const uint32_t x_bytes = (row_bytes + 127) & ~127u;
+  const size_t slot_bytes = (size_t)R * row_bytes;
   uint8_t* xs = smem_raw;
   uint8_t* ring = smem_raw + x_bytes;
   const int64_t G = gridDim.x;
-  const int64_t my_rows = p.rows_total > blockIdx.x ? (p.rows_total - blockIdx.x + G - 1) / G : 0;
+  const int64_t n_chunks = (p.rows_total + R - 1) / R;            // chunk c = rows [c*R, c*R + R)
+  const int64_t my_chunks = n_chunks > blockIdx.x ? (n_chunks - blockIdx.x + G - 1) / G : 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < slots; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&full[s])), "r"(1));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&empty[s])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&empty[s])), "r"(R));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // x -> shared (all threads)
-  {
-    const uint4* xg = reinterpret_cast<const uint4*>(p.x);
-    uint4* xd = reinterpret_cast<uint4*>(xs);
-    for (uint32_t i = threadIdx.x; i < row_bytes / 16; i += blockDim.x) xd[i] = xg[i];
-  }
-  __syncthreads();
+  __syncthreads();                                  // barrier inits visible
+  // Programmatic dependent launch: W may be prefetched before the previous
+  // grid completes only when the caller says so (early_w: the previous launch
+  // was a GEMV that itself waited for whatever wrote W).  Everything else
+  // (x, y) is touched only after griddepcontrol.wait.
+  if (!early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == 0) {
+    // producer: one bulk copy per contiguous run of a chunk's rows (a chunk is
+    // split only where it crosses from one site's matrix into the next);
+    // starts at once -- x is staged by the consumer warps in parallel
     if (lane == 0) {
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      for (int64_t i = 0; i < my_rows; ++i) {
+      for (int64_t i = 0; i < my_chunks; ++i) {
         const int s = (int)(i % slots);
-        const uint32_t ph = (uint32_t)((i / slots) & 1);
-        g_mbar_wait(s_u32(&empty[s]), ph ^ 1);
-        const int64_t row = blockIdx.x + i * G;
-        const void* Wb = p.site[0].W;
-        int64_t rb = 0;
-        if (p.n_sites > 1 && row >= p.site[1].row_begin) { Wb = p.site[1].W; rb = p.site[1].row_begin; }
-        if (p.n_sites > 2 && row >= p.site[2].row_begin) { Wb = p.site[2].W; rb = p.site[2].row_begin; }
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(Wb) + (row - rb) * (int64_t)row_bytes;
+        g_mbar_wait(s_u32(&empty[s]), (uint32_t)((i / slots) & 1) ^ 1);
+        const int64_t r0 = (blockIdx.x + i * G) * R;
+        const int64_t r1 = r0 + R < p.rows_total ? r0 + R : p.rows_total;
         const uint32_t bar = s_u32(&full[s]);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-            ::"r"(s_u32(ring + (size_t)s * slot_bytes)), "l"(src), "r"(row_bytes), "r"(bar), "l"(pol)
-            : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)((r1 - r0) * row_bytes)) : "memory");
+        int64_t r = r0;
+        while (r < r1) {
+          const void* Wb = p.site[0].W;
+          int64_t rb = 0, re = p.n_sites > 1 ? p.site[1].row_begin : p.rows_total;
+          if (p.n_sites > 1 && r >= p.site[1].row_begin) {
+            Wb = p.site[1].W; rb = p.site[1].row_begin; re = p.n_sites > 2 ? p.site[2].row_begin : p.rows_total;
+          }
+          if (p.n_sites > 2 && r >= p.site[2].row_begin) { Wb = p.site[2].W; rb = p.site[2].row_begin; re = p.rows_total; }
+          const int64_t run_end = r1 < re ? r1 : re;
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(Wb) + (r - rb) * (int64_t)row_bytes;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+              ::"r"(s_u32(ring + s * slot_bytes + (r - r0) * (size_t)row_bytes)), "l"(src),
+                "r"((uint32_t)((run_end - r) * row_bytes)), "r"(bar), "l"(pol)
+              : "memory");
+          r = run_end;
+        }
       }
     }
     return;
   }
+  if (early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after our wait: see above
+  // x -> shared (consumer warps), then a named barrier among the consumers only
+  {
+    const uint4* xg = reinterpret_cast<const uint4*>(p.x);
+    uint4* xd = reinterpret_cast<uint4*>(xs);
+    for (uint32_t i = threadIdx.x - 32; i < row_bytes / 16; i += blockDim.x - 32) xd[i] = xg[i];
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
+  // consumers: unit u = (local chunk i, row k in chunk); warp cw takes u = cw mod 8
   const int cw = warp - 1;
-  const int64_t nchunk = row_bytes / 16;
+  const int64_t nchunk16 = row_bytes / 16;
   const uint4* x4 = reinterpret_cast<const uint4*>(xs);
-  for (int64_t i = cw; i < my_rows; i += kBulkConsumers) {
+  for (int64_t u = cw; u < my_chunks * R; u += kBulkConsumers) {
+    const int64_t i = u / R;
+    const int k = (int)(u - i * R);
     const int s = (int)(i % slots);
+    const int64_t row = (blockIdx.x + i * G) * R + k;
     g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
-    const uint4* w4 = reinterpret_cast<const uint4*>(ring + (size_t)s * slot_bytes);
-    float acc0 = 0.f, acc1 = 0.f;
-    int64_t c = lane;
-    for (; c + 32 < nchunk; c += 64) {
-      acc0 += dot_chunk<kBf16>(w4[c], x4, c);
-      acc1 += dot_chunk<kBf16>(w4[c + 32], x4, c + 32);
-    }
-    if (c < nchunk) acc0 += dot_chunk<kBf16>(w4[c], x4, c);
-    float acc = acc0 + acc1;
+    if (row < p.rows_total) {
+      const uint4* w4 = reinterpret_cast<const uint4*>(ring + s * slot_bytes + (size_t)k * row_bytes);
+      float acc0 = 0.f, acc1 = 0.f;
+      int64_t c = lane;
+      for (; c + 32 < nchunk16; c += 64) {
+        acc0 += dot_chunk<kBf16>(w4[c], x4, c);
+        acc1 += dot_chunk<kBf16>(w4[c + 32], x4, c + 32);
+      }
+      if (c < nchunk16) acc0 += dot_chunk<kBf16>(w4[c], x4, c);
+      float acc = acc0 + acc1;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    __syncwarp();
-    if (lane == 0) {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[s])) : "memory");
-      p.y[blockIdx.x + i * G] = acc;
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) p.y[row] = acc;
     }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[s])) : "memory");
   }
 }
 
@@ -221,23 +247,42 @@ static int gemv_variant() {
   return v;
 }
 
-cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s) {
+cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w) {
   const bool bf16 = dtype == LSW_BF16;
   if (gemv_variant() == 1) {
+    // bulk-copy throughput grows with bytes per operation (scripts/membench.cu:
+    // 4 KB ops 2.6 TB/s ... 32 KB ops 7.3 TB/s): move R >= 1 rows per op, ~32 KB
     const uint32_t row_bytes = (uint32_t)(p.d_in * (bf16 ? 2 : 4));
     const uint32_t x_bytes = (row_bytes + 127) & ~127u;
-    const uint32_t slot_bytes = x_bytes;
-    const uint32_t budget = 220 * 1024;
+    int R = (int)(32768 / row_bytes);
+    if (R < 1) R = 1;
+    if (R > 8) R = 8;
+    const size_t slot_bytes = (size_t)R * row_bytes;
+    const size_t budget = 220 * 1024;
     int slots = (int)((budget - x_bytes) / slot_bytes);
     if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
     if (slots >= 2) {
       const size_t smem = x_bytes + (size_t)slots * slot_bytes;
       auto fn = bf16 ? gemv_bulk_kernel<true> : gemv_bulk_kernel<false>;
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      int grid = (int)(p.rows_total < num_sms ? p.rows_total : num_sms);
+      static size_t smem_set[2] = {0, 0};     // attribute set once per kernel (not per launch)
+      if (smem > smem_set[bf16]) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        smem_set[bf16] = smem;
+      }
+      const int64_t n_chunks = (p.rows_total + R - 1) / R;
+      int grid = (int)(n_chunks < num_sms ? n_chunks : num_sms);
       if (grid < 1) grid = 1;
-      fn<<<grid, kBulkThreads, smem, s>>>(p, slots, slot_bytes);
-      return cudaGetLastError();
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(grid);
+      lc.blockDim = dim3(kBulkThreads);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      return cudaLaunchKernelEx(&lc, fn, p, slots, R, (int32_t)(early_w ? 1 : 0));
     }
   }
   const size_t smem = (size_t)p.d_in * (bf16 ? 2 : 4);
@@ -245,7 +290,11 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
   static int occ_cache[2][8] = {};          // [dtype][smem bucket of 16 KB] -> CTAs per SM
   const int bucket = (int)(smem >> 14) < 8 ? (int)(smem >> 14) : 7;
   int& occ = occ_cache[bf16][bucket];
-  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static size_t smem_set[2] = {0, 0};
+  if (smem > 48 * 1024 && smem > smem_set[bf16]) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set[bf16] = smem;
+  }
   if (occ == 0) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kGemvThreads, ((size_t)bucket + 1) << 14);
     if (occ < 1) occ = 1;

@@ -276,7 +276,7 @@ lsw_status lsw_unmerge_all_layers(lsw_ctx* ctx, void* stream) {
 }
 
 static lsw_status gemv_sites(lsw_ctx* ctx, int layer, const int* kinds, int n, const void* x, float* y,
-                             cudaStream_t s, const char* who) {
+                             cudaStream_t s, const char* who, bool early_w = false) {
   if (!ctx || !x || !y) return fail(LSW_E_ARG, "%s: null argument", who);
   if (layer < 0 || layer >= ctx->cfg.n_layers)
     return fail(LSW_E_ARG, "%s: layer=%d not in [0,%d)", who, layer, ctx->cfg.n_layers);
@@ -295,7 +295,7 @@ static lsw_status gemv_sites(lsw_ctx* ctx, int layer, const int* kinds, int n, c
   p.d_in = ctx->kinds[kinds[0]].d_in;
   p.x = x;
   p.y = y;
-  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->num_sms, s);
+  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->num_sms, s, early_w);
   if (e != cudaSuccess) return cuda_fail(e, "decode GEMV launch");
   ++ctx->launches;
   // Row-parallel kinds under TP: partial sums -> allreduce.
@@ -333,7 +333,9 @@ lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs, float*
     for (int g = 0; g < LSW_NGROUP; ++g) {
       const uint8_t* xp = (const uint8_t*)xs + (size_t)(l * ctx->x_per_layer + ctx->x_off[g]) * es;
       float* yp = ys + l * ctx->y_per_layer + ctx->y_off[g];
-      st = lsw_decode_group(ctx, l, g, xp, yp, stream);
+      // every GEMV but the first after the switch may prefetch W under PDL
+      st = gemv_sites(ctx, l, kGroupKinds[g], kGroupSize[g], xp, yp, (cudaStream_t)stream, "lsw_decode_token",
+                      /*early_w=*/l > 0 || g > 0);
       if (st != LSW_OK) return st;
     }
   return LSW_OK;

@@ -149,7 +149,9 @@ struct GemvParams {
   const void* x;
   float* y;
 };
-cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s);
+// early_w: the previous launch on `s` was a GEMV (W may be prefetched before
+// griddepcontrol.wait; see gemv.cu).
+cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w = false);
 
 // Tensor-core switch (switch_tc.cu).
 struct TcPlan;   // opaque: packed operands + TMA descriptors

@@ -30,9 +30,11 @@
 //  * Epilogue (8 warps, 2 per TMEM lane quarter): tcgen05.ld the accumulators,
 //    W + sum_j c_j acc_j with packed fp32x2 FMAs (FFMA2), RNE to bf16, in place
 //    in the (conflict-free, 128B-swizzled) stage.
-//  * Warp roles: 0 = TMA/bulk producer, 1 = TMEM allocator + MMA issuer,
+//  * Warp roles: 0 = W producer (TMA), 1 = TMEM allocator + MMA issuer,
 //    2 = store warp (TMA stores, frees W stages as soon as they are read),
-//    3..10 = epilogue.
+//    3 = operand producer (bulk copies of the A/B slices), 4..11 = epilogue.
+//    W prefetch depth is therefore set by the W ring alone, not by the
+//    operand ring that the MMA releases.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -47,7 +49,7 @@ constexpr int kTcTM = 128;                 // tile rows = UMMA M = TMEM lanes
 constexpr int kTcTN = 64;                  // sub-tile columns = UMMA N
 constexpr int kSubBytes = kTcTM * kTcTN * 2;   // 16 KB: one swizzled W sub-tile
 constexpr int kTcEpiWarps = 8;
-constexpr int kTcFirstEpiWarp = 3;
+constexpr int kTcFirstEpiWarp = 4;
 constexpr int kTcThreads = 32 * (kTcFirstEpiWarp + kTcEpiWarps);
 constexpr int kTcMaxStages = 8;
 
@@ -60,8 +62,11 @@ struct TcMaps {
 struct TcKind {
   int64_t tile_begin;
   int32_t row_tiles, col_tiles;
+  __nv_bfloat16* W;           // [L, d_out, d_in] (written back by the epilogue in STG mode)
+  int64_t d_out, d_in;
   int64_t din_pad, dout_pad;  // packed-operand row counts (multiples of 128)
-  const __nv_bfloat16* At;    // packed A^T [L*N, din_pad, rp], pre-swizzled
+  const __nv_bfloat16* At;    // packed A^T [L, col_tiles, N, tile_cols, rp], pre-swizzled:
+                              // one tile's slices of all N experts are one contiguous block
   const __nv_bfloat16* Bp;    // packed B   [L*N, dout_pad, rp], pre-swizzled
 };
 
@@ -76,6 +81,9 @@ struct TcGeom {
   uint32_t a_bytes_per_term;              // 64*nsub * rp * 2
   uint32_t b_bytes_per_term;              // 128 * rp * 2
   uint32_t a_stage_bytes, b_buf_bytes, w_stage_bytes;
+  int32_t a_all;                          // 1: one bulk op fetches all N experts' A slices of a tile
+  int32_t store_stg;                      // 1: epilogue writes W back with coalesced STG.128 (LSU);
+                                          // 0: the store warp issues TMA bulk tensor stores
   uint32_t swz_mode;                      // UMMA layout type of the r-wide operands
   uint32_t smem_bytes;
 };
@@ -362,6 +370,89 @@ __device__ __forceinline__ void epi_chunk_many(uint32_t tm_addr, const float* cs
   *p1 = make_uint4(o[4], o[5], o[6], o[7]);
 }
 
+// ------------------------------------------------------------------ epilogue loop
+
+struct EpiCtx {
+  const TcGeom& g;
+  uint8_t* wst0;
+  uint32_t tmem_base;
+  int warp, lane;
+  bool probe;
+  uint64_t* bar_wfull;
+  uint64_t* bar_wdone;
+  uint64_t* bar_wempty;
+  uint64_t* bar_accfull;
+  uint64_t* bar_accempty;
+};
+
+// The epilogue warps' tile loop, specialised on the term count (NT = -1: any).
+template <int NT>
+__device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& seq, const Coefs& cf) {
+  const TcGeom& g = e.g;
+  const int ew = e.warp - kTcFirstEpiWarp;     // 0..7
+  const int quarter = e.warp & 3;              // TMEM lane quarter this warp may access
+  const int half = ew >> 2;                    // which 32 of a sub-tile's 64 columns
+  const int row = quarter * 32 + e.lane;       // tile-local row == TMEM lane
+  uint64_t c2[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) c2[j] = (NT > j) ? f2_pack(cf.c[j], cf.c[j]) : 0ull;
+  const int nt = cf.n;
+  Ring wring{0, 0, (uint32_t)g.w_stages};
+  Ring acc{0, 0, (uint32_t)g.acc_bufs};
+  for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
+    mbar_wait(smem_u32(&e.bar_wfull[wring.i]), wring.phase);            // W tile landed (acquire)
+    uint8_t* wt = e.wst0 + (size_t)wring.i * g.w_stage_bytes;
+    for (int sb = 0; sb < g.nsub; ++sb) {
+      if (!e.probe) mbar_wait(smem_u32(&e.bar_accfull[acc.i]), acc.phase);  // accumulators ready
+      tc_fence_after();
+      uint8_t* wrow = wt + sb * kSubBytes + row * 128;
+      const uint32_t tm_row = e.tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * g.max_terms * kTcTN;
+#pragma unroll
+      for (int q2 = 0; q2 < 2; ++q2) {
+        const int col16 = half * 2 + q2;       // 16-column chunk 0..3 of the sub-tile
+        const uint32_t ta = tm_row + col16 * 16;
+        if constexpr (NT > 0) epi_chunk<NT>(ta, c2, wrow, row, col16);
+        else if constexpr (NT < 0) epi_chunk_many(ta, cf.c, nt, wrow, row, col16);
+      }
+      // accumulators consumed -> MMA may reuse this TMEM buffer
+      tc_fence_before();
+      __syncwarp();
+      if (e.lane == 0 && !e.probe) mbar_arrive(smem_u32(&e.bar_accempty[acc.i]));
+      acc.next();
+    }
+    if (g.store_stg) {
+      // Copy-out through the LSU path, per warp (no cross-warp barrier): this
+      // warp computed rows 32*quarter.. +31, columns 32*half.. +31 of every
+      // sub-tile; re-read them from shared memory so that 4 lanes write one
+      // row's 64 contiguous bytes (two full 32-B sectors) per STG.128.
+      __syncwarp();
+      const TcKind& K = g.kind[c.kd];
+      const int64_t row0 = (int64_t)c.rb * kTcTM + quarter * 32, col0 = (int64_t)c.cb * kTcTN * g.nsub;
+      __nv_bfloat16* Wl = K.W + (int64_t)c.layer * K.d_out * K.d_in;
+      const int sub_r = e.lane >> 2, ch4 = e.lane & 3;   // 8 rows x 4 chunks per instruction
+      for (int sb = 0; sb < g.nsub; ++sb) {
+#pragma unroll
+        for (int rr = 0; rr < 32; rr += 8) {
+          const int r = quarter * 32 + rr + sub_r;       // tile-local row
+          const int ch = half * 4 + ch4;                 // 16-B chunk within the 128-B sub-tile row
+          const uint4 v = *reinterpret_cast<const uint4*>(wt + sb * kSubBytes + r * 128 + ((ch ^ (r & 7)) << 4));
+          const int64_t gr = row0 + rr + sub_r, gc = col0 + sb * kTcTN + ch * 8;
+          if (gr < K.d_out && gc < K.d_in) __stcs(reinterpret_cast<uint4*>(Wl + gr * K.d_in + gc), v);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (e.lane == 0) mbar_arrive(smem_u32(&e.bar_wempty[wring.i]));   // stage reusable
+    } else {
+      // generic-proxy smem writes -> visible to the TMA store (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (e.lane == 0) mbar_arrive(smem_u32(&e.bar_wdone[wring.i]));
+    }
+    wring.next();
+  }
+}
+
 // ------------------------------------------------------------------ the kernel
 
 struct TcArgs {
@@ -382,7 +473,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
   __shared__ int32_t s_parity;
   __shared__ uint32_t s_tmem_base;
   __shared__ __align__(8) uint64_t bar_wfull[kTcMaxStages], bar_wempty[kTcMaxStages], bar_wdone[kTcMaxStages];
-  __shared__ __align__(8) uint64_t bar_afull[2], bar_aempty[2];
+  __shared__ __align__(8) uint64_t bar_afull[4], bar_aempty[4];
   __shared__ __align__(8) uint64_t bar_bfull[2], bar_bempty[2];
   __shared__ __align__(8) uint64_t bar_accfull[2], bar_accempty[2];
 
@@ -409,12 +500,14 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
     if (blockIdx.x == 0 && !cf.bad) stage_decision(p, parity);
     for (int s = 0; s < g.w_stages; ++s) {
       mbar_init(smem_u32(&bar_wfull[s]), 1);
-      mbar_init(smem_u32(&bar_wempty[s]), 1);
+      mbar_init(smem_u32(&bar_wempty[s]), g.store_stg ? kTcEpiWarps : 1);
       mbar_init(smem_u32(&bar_wdone[s]), kTcEpiWarps);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < g.a_stages; ++s) {
       mbar_init(smem_u32(&bar_afull[s]), 1);
       mbar_init(smem_u32(&bar_aempty[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&bar_bfull[s]), 1);
       mbar_init(smem_u32(&bar_bempty[s]), 1);
       mbar_init(smem_u32(&bar_accfull[s]), 1);
@@ -453,44 +546,11 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
 
   if (nt > 0) {
     if (warp == 0) {
-      // ============================ producer ===============================
+      // ============================ W producer =============================
       if (lane == 0) {
         const uint64_t pol_stream = policy_evict_first();
-        const uint64_t pol_keep = policy_evict_last();
-        int64_t strip_prev = -1;
-        Ring bring{0, 0, (uint32_t)g.b_bufs};
-        Ring aring{0, 0, (uint32_t)g.a_stages};
         Ring wring{0, 0, (uint32_t)g.w_stages};
-        const size_t rpe = (size_t)g.rp;                   // elements per packed row
         for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
-          const TcKind& K = g.kind[c.kd];
-          if (!probe) {
-            if (strip_id(c) != strip_prev) {               // B slices of a new 128-row strip
-              if (strip_prev >= 0) bring.next();
-              strip_prev = strip_id(c);
-              mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
-              const uint32_t bar = smem_u32(&bar_bfull[bring.i]);
-              mbar_expect_tx(bar, nt * g.b_bytes_per_term);
-              uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
-              for (int j = 0; j < nt; ++j) {
-                const __nv_bfloat16* src =
-                    K.Bp + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.dout_pad + (size_t)c.rb * kTcTM) * rpe;
-                bulk_load(smem_u32(dst + j * g.b_bytes_per_term), src, g.b_bytes_per_term, bar, pol_keep);
-              }
-            }
-            // A^T slices of this tile's columns
-            mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
-            const uint32_t abar = smem_u32(&bar_afull[aring.i]);
-            mbar_expect_tx(abar, nt * g.a_bytes_per_term);
-            uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
-            for (int j = 0; j < nt; ++j) {
-              const __nv_bfloat16* src =
-                  K.At + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.din_pad + (size_t)c.cb * tile_cols) * rpe;
-              bulk_load(smem_u32(adst + j * g.a_bytes_per_term), src, g.a_bytes_per_term, abar, pol_keep);
-            }
-            aring.next();
-          }
-          // W tile: nsub adjacent 64-column boxes
           mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
           const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
           mbar_expect_tx(wbar, nsub * kSubBytes);
@@ -499,6 +559,48 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
             tma_load_3d(smem_u32(wdst + sb * kSubBytes), &maps.w[c.kd], c.cb * tile_cols + sb * kTcTN,
                         c.rb * kTcTM, c.layer, wbar, pol_stream);
           wring.next();
+        }
+      }
+    } else if (warp == 3) {
+      // ============================ operand producer ========================
+      if (lane == 0 && !probe) {
+        const uint64_t pol_keep = policy_evict_last();
+        int64_t strip_prev = -1;
+        Ring bring{0, 0, (uint32_t)g.b_bufs};
+        Ring aring{0, 0, (uint32_t)g.a_stages};
+        const size_t rpe = (size_t)g.rp;                   // elements per packed row
+        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
+          const TcKind& K = g.kind[c.kd];
+          if (strip_id(c) != strip_prev) {                 // B slices of a new 128-row strip
+            if (strip_prev >= 0) bring.next();
+            strip_prev = strip_id(c);
+            mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
+            const uint32_t bar = smem_u32(&bar_bfull[bring.i]);
+            mbar_expect_tx(bar, nt * g.b_bytes_per_term);
+            uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
+            for (int j = 0; j < nt; ++j) {
+              const __nv_bfloat16* src =
+                  K.Bp + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.dout_pad + (size_t)c.rb * kTcTM) * rpe;
+              bulk_load(smem_u32(dst + j * g.b_bytes_per_term), src, g.b_bytes_per_term, bar, pol_keep);
+            }
+          }
+          // A^T slices of this tile's columns
+          mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
+          const uint32_t abar = smem_u32(&bar_afull[aring.i]);
+          uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
+          const __nv_bfloat16* blk =
+              K.At + (((size_t)c.layer * K.col_tiles + c.cb) * g.n_experts) * (size_t)tile_cols * rpe;
+          if (g.a_all) {
+            // one op for the whole block (bulk-copy throughput scales with bytes per op)
+            mbar_expect_tx(abar, g.n_experts * g.a_bytes_per_term);
+            bulk_load(smem_u32(adst), blk, g.n_experts * g.a_bytes_per_term, abar, pol_keep);
+          } else {
+            mbar_expect_tx(abar, nt * g.a_bytes_per_term);
+            for (int j = 0; j < nt; ++j)
+              bulk_load(smem_u32(adst + j * g.a_bytes_per_term), blk + (size_t)cf.e[j] * tile_cols * rpe,
+                        g.a_bytes_per_term, abar, pol_keep);
+          }
+          aring.next();
         }
       }
     } else if (warp == 1) {
@@ -530,11 +632,12 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
             tc_fence_after();
             const uint32_t d0 = tmem_base + acc.i * g.max_terms * kTcTN;
             const uint32_t a_sub = a_stage + sb * kTcTN * row_bytes;
-            for (int j = 0; j < nt; ++j)
+            for (int j = 0; j < nt; ++j) {
+              const uint32_t a_j = a_sub + (g.a_all ? cf.e[j] : j) * g.a_bytes_per_term;
               for (int kk = 0; kk < ksteps; ++kk)
                 umma_f16(d0 + j * kTcTN, umma_desc(b_strip + j * g.b_bytes_per_term + kk * 32, sbo, g.swz_mode),
-                         umma_desc(a_sub + j * g.a_bytes_per_term + kk * 32, sbo, g.swz_mode), idesc,
-                         kk > 0 ? 1u : 0u);
+                         umma_desc(a_j + kk * 32, sbo, g.swz_mode), idesc, kk > 0 ? 1u : 0u);
+            }
             umma_commit(smem_u32(&bar_accfull[acc.i]));
             acc.next();
           }
@@ -545,7 +648,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
           if (c.t < 0 || strip_id(c) != strip) umma_commit(smem_u32(&bar_bempty[bring.i]));
         }
       }
-    } else if (warp == 2) {
+    } else if (warp == 2 && !g.store_stg) {
       // ============================ store warp ==============================
       if (lane == 0) {
         const uint64_t pol_stream = policy_evict_first();
@@ -563,50 +666,17 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
         }
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
-    } else {
+    } else if (warp >= kTcFirstEpiWarp) {
       // ============================ epilogue ================================
-      const int ew = warp - kTcFirstEpiWarp;       // 0..7
-      const int quarter = warp & 3;                // TMEM lane quarter this warp may access
-      const int half = ew >> 2;                    // which 32 of a sub-tile's 64 columns
-      const int row = quarter * 32 + lane;         // tile-local row == TMEM lane
-      uint64_t c2[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) c2[j] = j < nt ? f2_pack(cf.c[j], cf.c[j]) : 0ull;
       const int ntc = (probe || skip_math) ? 0 : nt;
-      Ring wring{0, 0, (uint32_t)g.w_stages};
-      Ring acc{0, 0, (uint32_t)g.acc_bufs};
-      for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
-        mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);          // W tile landed (acquire)
-        uint8_t* wt = wst0 + (size_t)wring.i * g.w_stage_bytes;
-        for (int sb = 0; sb < nsub; ++sb) {
-          if (!probe) mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);  // accumulators ready
-          tc_fence_after();
-          uint8_t* wrow = wt + sb * kSubBytes + row * 128;
-          const uint32_t tm_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * g.max_terms * kTcTN;
-#pragma unroll
-          for (int q2 = 0; q2 < 2; ++q2) {
-            const int col16 = half * 2 + q2;       // 16-column chunk 0..3 of the sub-tile
-            const uint32_t ta = tm_row + col16 * 16;
-            switch (ntc) {
-              case 0: break;
-              case 1: epi_chunk<1>(ta, c2, wrow, row, col16); break;
-              case 2: epi_chunk<2>(ta, c2, wrow, row, col16); break;
-              case 3: epi_chunk<3>(ta, c2, wrow, row, col16); break;
-              case 4: epi_chunk<4>(ta, c2, wrow, row, col16); break;
-              default: epi_chunk_many(ta, cf.c, ntc, wrow, row, col16); break;
-            }
-          }
-          // accumulators consumed -> MMA may reuse this TMEM buffer
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0 && !probe) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
-          acc.next();
-        }
-        // generic-proxy smem writes -> visible to the TMA store (async proxy)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
-        wring.next();
+      EpiCtx ec{g, wst0, tmem_base, warp, lane, probe, bar_wfull, bar_wdone, bar_wempty, bar_accfull, bar_accempty};
+      switch (ntc) {
+        case 0: epilogue_loop<0>(ec, seq, cf); break;
+        case 1: epilogue_loop<1>(ec, seq, cf); break;
+        case 2: epilogue_loop<2>(ec, seq, cf); break;
+        case 3: epilogue_loop<3>(ec, seq, cf); break;
+        case 4: epilogue_loop<4>(ec, seq, cf); break;
+        default: epilogue_loop<-1>(ec, seq, cf); break;
       }
     }
   }
@@ -638,16 +708,21 @@ __device__ __forceinline__ int64_t swz_off(int64_t row, int k, int rp) {
   return row * rp + (((k >> 3) ^ f) << 3) + (k & 7);
 }
 
-// A [M, r, d_in] -> A^T [M, din_pad, rp]
-__global__ void pack_At_kernel(const __nv_bfloat16* __restrict__ A, __nv_bfloat16* __restrict__ At, int64_t M,
-                               int r, int rp, int64_t d_in, int64_t din_pad) {
-  const int64_t total = M * din_pad * rp;
+// A [L, N, r, d_in] -> A^T blocks [L, col_tiles, N, tc, rp] (tc = tile columns):
+// block (l, cb) holds, expert after expert, the pre-swizzled [tc, rp] slice
+// A_{l,e}^T[cb*tc : cb*tc + tc, :] (zero beyond d_in / r).
+__global__ void pack_At_kernel(const __nv_bfloat16* __restrict__ A, __nv_bfloat16* __restrict__ At, int64_t L,
+                               int N, int r, int rp, int64_t d_in, int64_t col_tiles, int tc) {
+  const int64_t din_pad = col_tiles * tc;
+  const int64_t total = L * N * din_pad * rp;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(i % rp);
     const int64_t c = (i / rp) % din_pad;
-    const int64_t m = i / ((int64_t)rp * din_pad);
+    const int64_t m = i / ((int64_t)rp * din_pad);       // l * N + e
+    const int64_t l = m / N, e = m % N;
     const __nv_bfloat16 v = (k < r && c < d_in) ? A[(m * r + k) * d_in + c] : __float2bfloat16(0.f);
-    At[m * din_pad * rp + swz_off(c, k, rp)] = v;
+    const int64_t blk = (l * col_tiles + c / tc) * N + e;
+    At[blk * tc * rp + swz_off(c % tc, k, rp)] = v;
   }
 }
 
@@ -722,14 +797,22 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   bool ok = false;
   int nsub_env = 0;
   if (const char* v = getenv("LSW_TC_NSUB")) nsub_env = atoi(v);
-  for (int nsub = 2; nsub >= 1 && !ok; --nsub) {
+  int a_all_env = 0;                                     // measured: per-expert ops are faster
+  int a_max = 2;                                         // A-slice ring depth (tuning: LSW_TC_ASTAGES)
+  if (const char* v = getenv("LSW_TC_ASTAGES")) { int x = atoi(v); if (x >= 1 && x <= 4) a_max = x; }
+  if (const char* v = getenv("LSW_TC_AALL")) a_all_env = atoi(v);
+  for (int cand = 0; cand < 4 && !ok; ++cand) {
+    const int nsub = cand < 2 ? 2 : 1;
+    const int a_all = (cand % 2 == 0) ? 1 : 0;           // prefer one op per tile for A
     if (nsub_env && nsub != nsub_env) continue;
+    if (a_all_env >= 0 && a_all != a_all_env) continue;
     const uint32_t a_term = kTcTN * nsub * rp * 2;
-    const uint32_t a_stage = align1k(g.max_terms * a_term);
+    if (a_all && (uint32_t)sp.n_experts * a_term > 32768) continue;
+    const uint32_t a_stage = align1k((a_all ? sp.n_experts : g.max_terms) * a_term);
     const uint32_t b_buf = align1k(g.max_terms * g.b_bytes_per_term);
     const uint32_t w_stage = nsub * kSubBytes;
     for (int bbufs = 2; bbufs >= 1 && !ok; --bbufs)
-      for (int astages = 2; astages >= 1 && !ok; --astages) {
+      for (int astages = a_max; astages >= 1 && !ok; --astages) {
         int ws = (int)((budget - (int64_t)bbufs * b_buf - (int64_t)astages * a_stage) / w_stage);
         if ((int64_t)budget < (int64_t)bbufs * b_buf + (int64_t)astages * a_stage) ws = 0;
         if (ws > kTcMaxStages) ws = kTcMaxStages;
@@ -742,6 +825,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
           g.b_bufs = bbufs;
           g.a_bytes_per_term = a_term;
           g.a_stage_bytes = a_stage;
+          g.a_all = a_all;
           g.b_buf_bytes = b_buf;
           g.w_stage_bytes = w_stage;
         }
@@ -753,6 +837,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   if (const char* v = getenv("LSW_TC_ORDER")) plan->order = strcmp(v, "sweep") == 0 ? ORDER_SWEEP : ORDER_STRIP;
   if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
   if (const char* v = getenv("LSW_TC_PROBE")) plan->probe = atoi(v);
+  g.store_stg = 1;
+  if (const char* v = getenv("LSW_TC_STORE")) g.store_stg = strcmp(v, "tma") != 0;
   g.smem_bytes = g.w_stages * g.w_stage_bytes + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
   // tiles
   const int tile_cols = kTcTN * g.nsub;
@@ -781,12 +867,15 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     e = cudaMalloc(&plan->packed_B[k], b_bytes);
     if (e != cudaSuccess) break;
     plan->bytes += at_bytes + b_bytes;
-    pack_At_kernel<<<2048, 256>>>((const __nv_bfloat16*)kg.A, (__nv_bfloat16*)plan->packed_At[k], M, r, rp,
-                                  kg.d_in, g.kind[k].din_pad);
+    pack_At_kernel<<<2048, 256>>>((const __nv_bfloat16*)kg.A, (__nv_bfloat16*)plan->packed_At[k], sp.n_layers,
+                                  sp.n_experts, r, rp, kg.d_in, g.kind[k].col_tiles, tile_cols);
     pack_B_kernel<<<2048, 256>>>((const __nv_bfloat16*)kg.B, (__nv_bfloat16*)plan->packed_B[k], M, r, rp,
                                  kg.d_out, g.kind[k].dout_pad);
     g.kind[k].At = (const __nv_bfloat16*)plan->packed_At[k];
     g.kind[k].Bp = (const __nv_bfloat16*)plan->packed_B[k];
+    g.kind[k].W = (__nv_bfloat16*)kg.W;
+    g.kind[k].d_out = kg.d_out;
+    g.kind[k].d_in = kg.d_in;
     if (!encode_w(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers)) {
       *why = "cuTensorMapEncodeTiled failed";
       e = cudaErrorInvalidValue;

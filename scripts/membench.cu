@@ -86,6 +86,61 @@ __global__ void rmw_strip_k(uint4* __restrict__ a, int rows, int cols_chunks, in
   }
 }
 
+
+// 1-D bulk-copy (TMA engine) streaming read: per CTA a ring of S slots of B
+// bytes; one producer thread issues cp.async.bulk, consumer warp 1 waits and
+// releases (no compute).  Measures the bulk-copy read ceiling per SM.
+__global__ void bulk_read_k(const uint8_t* __restrict__ a, size_t bytes, int S, int B) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ __align__(8) uint64_t full[64], empty[64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t nchunks = bytes / B;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&empty[s])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  size_t i = 0;
+  if (warp == 0 && lane == 0) {
+    for (size_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++i) {
+      const int s = (int)(i % S);
+      const uint32_t ph = (uint32_t)((i / S) & 1) ^ 1;
+      uint32_t eb = (uint32_t)__cvta_generic_to_shared(&empty[s]), fb = (uint32_t)__cvta_generic_to_shared(&full[s]);
+      uint32_t ok = 0;
+      while (!ok) asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}" : "=r"(ok) : "r"(eb), "r"(ph) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(B) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"((uint32_t)__cvta_generic_to_shared(sm + (size_t)s * B)), "l"(a + c * B), "r"(B), "r"(fb) : "memory");
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (size_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++i) {
+      const int s = (int)(i % S);
+      const uint32_t ph = (uint32_t)((i / S) & 1);
+      uint32_t eb = (uint32_t)__cvta_generic_to_shared(&empty[s]), fb = (uint32_t)__cvta_generic_to_shared(&full[s]);
+      uint32_t ok = 0;
+      while (!ok) asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}" : "=r"(ok) : "r"(fb), "r"(ph) : "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(eb) : "memory");
+    }
+  }
+}
+
+// LDGSTS (cp.async 16 B per thread) streaming read into a smem ring, all warps.
+__global__ void ldgsts_read_k(const uint4* __restrict__ a, size_t n, int depth) {
+  extern __shared__ __align__(128) uint4 sm4[];
+  const size_t per_iter = (size_t)gridDim.x * blockDim.x;
+  int it = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += per_iter, ++it) {
+    uint4* dst = sm4 + (size_t)(it % depth) * blockDim.x + threadIdx.x;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(a + i) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 6;" ::: "memory");
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 int main() {
   const size_t bytes = (size_t)8 << 30;     // 8 GiB per buffer
   const size_t n = bytes / 16;
@@ -129,6 +184,22 @@ int main() {
     timeit([&] { rmw_k<8><<<sms * occ, 256>>>(a, n, 0); }, 2.0 * bytes, nm);
     snprintf(nm, 64, "read U=8 grid=%dx%d", sms, occ);
     timeit([&] { read_k<8><<<sms * occ, 256>>>(a, n, o); }, 1.0 * bytes, nm);
+  }
+  for (int B : {4096, 8192, 16384, 32768}) {
+    for (int occ : {1, 2}) {
+      int S = (200 * 1024 / occ) / B;
+      if (S > 64) S = 64;
+      cudaFuncSetAttribute(bulk_read_k, cudaFuncAttributeMaxDynamicSharedMemorySize, S * B);
+      char nm[64];
+      snprintf(nm, 64, "bulk_read B=%d S=%d grid=%dx%d", B, S, sms, occ);
+      timeit([&] { bulk_read_k<<<sms * occ, 64, (size_t)S * B>>>((const uint8_t*)a, bytes, S, B); }, 1.0 * bytes, nm);
+    }
+  }
+  for (int occ : {1, 2, 4}) {
+    cudaFuncSetAttribute(ldgsts_read_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 512 * 16);
+    char nm[64];
+    snprintf(nm, 64, "ldgsts_read depth8 512thr grid=%dx%d", sms, occ);
+    timeit([&] { ldgsts_read_k<<<sms * occ, 512, 8 * 512 * 16>>>(a, n, 8); }, 1.0 * bytes, nm);
   }
   // strip pattern over a [rows x 4096 bf16] matrix (512 chunks per row)
   const int cols_chunks = 512;

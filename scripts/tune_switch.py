@@ -20,6 +20,7 @@ ap.add_argument("--config", default="llama2-7b")
 ap.add_argument("--layers", type=int, default=0)
 ap.add_argument("--iters", type=int, default=12)
 ap.add_argument("--impl", default="tc")
+ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("settings", nargs="*", default=["order=strip", "order=sweep,chunk=1", "order=sweep,chunk=4"])
 a = ap.parse_args()
 cfg = synth.get_config(a.config)
@@ -31,8 +32,8 @@ X1 = synth.gen_x1(cfg, a.iters + 4, "cuda")
 idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
 gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6452.8
-for setting in a.settings:
-    for k in ("LSW_TC_ORDER", "LSW_TC_CHUNK", "LSW_TC_STAGES", "LSW_TC_PROBE", "LSW_TC_NSUB"):
+for setting in [x for _ in range(a.repeat) for x in a.settings]:
+    for k in ("LSW_TC_ORDER", "LSW_TC_CHUNK", "LSW_TC_STAGES", "LSW_TC_PROBE", "LSW_TC_NSUB", "LSW_TC_AALL", "LSW_TC_STORE", "LSW_TC_ASTAGES"):
         os.environ.pop(k, None)
     for kv in setting.split(","):
         if not kv:
