@@ -1,0 +1,30 @@
+/*
+ * lsw_debug.h -- tuning hooks of liblsw.so.  Not part of the hot path and not
+ * needed by users; they expose measurement state that the kernels record only
+ * when enabled by environment variables read at lsw_create:
+ *
+ *   LSW_TC_TRACE=1   the tensor-core switch kernel stamps %globaltimer (ns) at
+ *                    12 pipeline events of its first 256 tiles in CTAs 0 and 1
+ *                    (layout [cta][tile][event], events in switch_tc.cu:
+ *                    W issued, A issued, A full, MMA start, MMA done, epilogue
+ *                    saw W, epilogue saw accumulators, stage freed, epilogue
+ *                    done, MMA got a free accumulator buffer); 0 = not reached.
+ */
+#ifndef LSW_DEBUG_H_
+#define LSW_DEBUG_H_
+
+#include "lsw.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Copy up to n uint64 trace words of the last switch launch into host_out (host
+ * memory).  Returns the number copied in *n_out (0 when tracing is off or the
+ * ctx uses the SIMT switch).  Synchronizes the device.  LSW_E_ARG on null. */
+LSW_API lsw_status lsw_debug_switch_trace(lsw_ctx* ctx, uint64_t* host_out, int64_t n, int64_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LSW_DEBUG_H_ */

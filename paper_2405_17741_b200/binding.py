@@ -34,6 +34,7 @@ SYMBOLS = (
     "lsw_nccl_get_unique_id", "lsw_attach_nccl", "lsw_router_topk", "lsw_merge_all_layers",
     "lsw_unmerge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_token",
     "lsw_decode_token_host", "lsw_device_status",
+    "lsw_debug_switch_trace",      # include/lsw_debug.h (tuning hook)
 )
 
 
@@ -85,6 +86,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lsw_decode_token": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_decode_token_host": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_device_status": (i32, [vp, vp, ctypes.POINTER(i32)]),
+        "lsw_debug_switch_trace": (i32, [vp, vp, i64, ctypes.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -202,6 +204,15 @@ class LoraSwitch:
     def decode_token_host(self, x1_h, xs_h, ys_h, idx_h, gate_h, stream=None):
         _check(lib().lsw_decode_token_host(self._h, _ptr(x1_h), _ptr(xs_h), _ptr(ys_h), _ptr(idx_h),
                                            _ptr(gate_h), _stream(stream)))
+
+    def debug_switch_trace(self):
+        """Tuning hook (include/lsw_debug.h): int64 ns timestamps [2, 256, 12]
+        of the last tensor-core switch launch when LSW_TC_TRACE was set ([cta, tile, event])."""
+        import numpy as np
+        buf = np.zeros(4 * 2048 * 12, dtype=np.uint64)
+        n = ctypes.c_int64(0)
+        _check(lib().lsw_debug_switch_trace(self._h, buf.ctypes.data, buf.size, ctypes.byref(n)))
+        return buf[: n.value].reshape(-1, 2048, 12) if n.value else None
 
     def device_status(self, stream=None) -> int:
         code = ctypes.c_int32(0)

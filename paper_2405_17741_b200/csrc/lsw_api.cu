@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include "lsw_internal.cuh"
+#include "../../include/lsw_debug.h"
 
 using namespace lsw;
 
@@ -383,6 +384,13 @@ lsw_status lsw_device_status(lsw_ctx* ctx, void* stream, int32_t* code) {
                 : err == LSW_DEV_BAD_INDEX      ? "expert index out of range or duplicated"
                                                 : "non-finite gate");
   }
+  return LSW_OK;
+}
+
+lsw_status lsw_debug_switch_trace(lsw_ctx* ctx, uint64_t* host_out, int64_t n, int64_t* n_out) {
+  if (!ctx || !host_out || !n_out) return fail(LSW_E_ARG, "lsw_debug_switch_trace: null argument");
+  cudaDeviceSynchronize();
+  *n_out = ctx->tc ? tc_plan_trace(ctx->tc, host_out, n) : 0;
   return LSW_OK;
 }
 

@@ -162,5 +162,6 @@ int tc_plan_grid(const TcPlan* plan);
 int tc_plan_tile_n(const TcPlan* plan);
 int64_t tc_plan_tiles(const TcPlan* plan);
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
+int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);   // tuning trace (lsw_debug.h)
 
 }  // namespace lsw

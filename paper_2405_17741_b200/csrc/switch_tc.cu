@@ -32,7 +32,9 @@
 //    in the (conflict-free, 128B-swizzled) stage.
 //  * Warp roles: 0 = W producer (TMA), 1 = TMEM allocator + MMA issuer,
 //    2 = store warp (TMA stores, frees W stages as soon as they are read),
-//    3 = operand producer (bulk copies of the A/B slices), 4..11 = epilogue.
+//    3 = operand producer (B strips by bulk copy; per-tile A slices by cp.async
+//    on the LSU path, so they do not queue behind W tiles in the TMA engine),
+//    4..11 = epilogue.
 //    W prefetch depth is therefore set by the W ring alone, not by the
 //    operand ring that the MMA releases.
 #include <cuda.h>
@@ -52,6 +54,7 @@ constexpr int kTcEpiWarps = 8;
 constexpr int kTcFirstEpiWarp = 4;
 constexpr int kTcThreads = 32 * (kTcFirstEpiWarp + kTcEpiWarps);
 constexpr int kTcMaxStages = 8;
+constexpr int kTcMaxAccBufs = 4;           // TMEM accumulator buffers (mbarrier pairs)
 
 enum { ORDER_STRIP = 0, ORDER_SWEEP = 1 };
 
@@ -82,6 +85,10 @@ struct TcGeom {
   uint32_t b_bytes_per_term;              // 128 * rp * 2
   uint32_t a_stage_bytes, b_buf_bytes, w_stage_bytes;
   int32_t a_all;                          // 1: one bulk op fetches all N experts' A slices of a tile
+  int32_t split;                          // 1: "split mode" -- c_j*B_j folded into B as 3 bf16 parts
+                                          //    (hi+mid+lo == the fp32 product), ONE accumulator per tile
+                                          //    (N = tile width), one MMA group per tile, 4 TMEM buffers;
+                                          // 0: one accumulator per expert term, c_j applied in the epilogue
   int32_t store_stg;                      // 1: epilogue writes W back with coalesced STG.128 (LSU);
                                           // 0: the store warp issues TMA bulk tensor stores
   uint32_t swz_mode;                      // UMMA layout type of the r-wide operands
@@ -92,6 +99,7 @@ struct TcPlan {
   TcMaps maps;
   TcGeom geom;
   int32_t order = ORDER_STRIP, chunk = 4, probe = 0;
+  uint64_t* trace = nullptr;  // LSW_TC_TRACE: [kTraceCtas][kTraceTiles][kTraceEvents] device timestamps
   void* packed_At[LSW_NKIND] = {};
   void* packed_B[LSW_NKIND] = {};
   int64_t bytes = 0;
@@ -128,6 +136,21 @@ __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// Tuning trace (LSW_TC_TRACE): %globaltimer stamps of pipeline events for the
+// first kTraceTiles tiles of kTraceCtas CTAs spread over the grid
+// (CTA b is traced as slot b / kTraceStride when b % kTraceStride == 0),
+// layout [slot][tile][event].
+constexpr int kTraceTiles = 2048, kTraceEvents = 12, kTraceCtas = 4, kTraceStride = 49;
+enum { EV_W_ISSUED = 0, EV_A_ISSUED, EV_A_FULL, EV_MMA_START, EV_MMA_DONE, EV_EPI_WFULL, EV_EPI_ACC0,
+       EV_STAGE_FREE, EV_EPI_DONE, EV_MMA_ACC0, EV_MMA_ISSUED0, EV_EPI_SUB0_DONE };
+__device__ __forceinline__ void trace_ev(uint64_t* tr, uint32_t it, int ev) {
+  if (tr && blockIdx.x % kTraceStride == 0 && it < (uint32_t)kTraceTiles) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    tr[((size_t)(blockIdx.x / kTraceStride) * kTraceTiles + it) * kTraceEvents + ev] = t;
+  }
 }
 
 // Wait for the phase with parity `parity` to complete.  A watchdog traps after
@@ -209,6 +232,13 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 }
 
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// elect.sync: true in exactly one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}" : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
@@ -378,16 +408,21 @@ struct EpiCtx {
   uint32_t tmem_base;
   int warp, lane;
   bool probe;
+  bool skip_math;
   uint64_t* bar_wfull;
   uint64_t* bar_wdone;
   uint64_t* bar_wempty;
   uint64_t* bar_accfull;
   uint64_t* bar_accempty;
+  uint64_t* trace;
 };
 
-// The epilogue warps' tile loop, specialised on the term count (NT = -1: any).
+// The epilogue warps' tile loop, specialised on the term count (NT = -1: any;
+// NT = kSplitNT: split mode, one pre-scaled accumulator per tile).
+constexpr int kSplitNT = 100;
 template <int NT>
 __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& seq, const Coefs& cf) {
+  constexpr bool SPLIT = NT == kSplitNT;
   const TcGeom& g = e.g;
   const int ew = e.warp - kTcFirstEpiWarp;     // 0..7
   const int quarter = e.warp & 3;              // TMEM lane quarter this warp may access
@@ -395,30 +430,44 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
   const int row = quarter * 32 + e.lane;       // tile-local row == TMEM lane
   uint64_t c2[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) c2[j] = (NT > j) ? f2_pack(cf.c[j], cf.c[j]) : 0ull;
+  for (int j = 0; j < 4; ++j) c2[j] = (!SPLIT && NT > j) ? f2_pack(cf.c[j], cf.c[j]) : 0ull;
+  if (SPLIT) c2[0] = f2_pack(1.f, 1.f);        // W + acc (coefficients are already in the MMA)
   const int nt = cf.n;
+  // per-term mode: one TMEM buffer (max_terms x 64 columns) per sub-tile;
+  // split mode: one buffer (64*nsub columns) per tile
+  const uint32_t buf_cols = SPLIT ? kTcTN * g.nsub : g.max_terms * kTcTN;
   Ring wring{0, 0, (uint32_t)g.w_stages};
   Ring acc{0, 0, (uint32_t)g.acc_bufs};
-  for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
+  uint64_t* tr = (ew == 0 && e.lane == 0) ? e.trace : nullptr;
+  uint32_t it = 0;
+  for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
     mbar_wait(smem_u32(&e.bar_wfull[wring.i]), wring.phase);            // W tile landed (acquire)
+    trace_ev(tr, it, EV_EPI_WFULL);
     uint8_t* wt = e.wst0 + (size_t)wring.i * g.w_stage_bytes;
     for (int sb = 0; sb < g.nsub; ++sb) {
-      if (!e.probe) mbar_wait(smem_u32(&e.bar_accfull[acc.i]), acc.phase);  // accumulators ready
+      if (!e.probe && (!SPLIT || sb == 0))
+        mbar_wait(smem_u32(&e.bar_accfull[acc.i]), acc.phase);          // accumulators ready
+      if (sb == 0) trace_ev(tr, it, EV_EPI_ACC0);
       tc_fence_after();
       uint8_t* wrow = wt + sb * kSubBytes + row * 128;
-      const uint32_t tm_row = e.tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * g.max_terms * kTcTN;
+      const uint32_t tm_row = e.tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * buf_cols +
+                              (SPLIT ? sb * kTcTN : 0);
 #pragma unroll
       for (int q2 = 0; q2 < 2; ++q2) {
         const int col16 = half * 2 + q2;       // 16-column chunk 0..3 of the sub-tile
         const uint32_t ta = tm_row + col16 * 16;
-        if constexpr (NT > 0) epi_chunk<NT>(ta, c2, wrow, row, col16);
+        if constexpr (SPLIT) { if (!e.skip_math) epi_chunk<1>(ta, c2, wrow, row, col16); }
+        else if constexpr (NT > 0) epi_chunk<NT>(ta, c2, wrow, row, col16);
         else if constexpr (NT < 0) epi_chunk_many(ta, cf.c, nt, wrow, row, col16);
       }
-      // accumulators consumed -> MMA may reuse this TMEM buffer
-      tc_fence_before();
-      __syncwarp();
-      if (e.lane == 0 && !e.probe) mbar_arrive(smem_u32(&e.bar_accempty[acc.i]));
-      acc.next();
+      if (!SPLIT || sb == g.nsub - 1) {
+        // accumulators consumed -> MMA may reuse this TMEM buffer
+        tc_fence_before();
+        __syncwarp();
+        if (e.lane == 0 && !e.probe) mbar_arrive(smem_u32(&e.bar_accempty[acc.i]));
+        acc.next();
+      }
+      if (sb == 0) trace_ev(tr, it, EV_EPI_SUB0_DONE);
     }
     if (g.store_stg) {
       // Copy-out through the LSU path, per warp (no cross-warp barrier): this
@@ -449,6 +498,7 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
       __syncwarp();
       if (e.lane == 0) mbar_arrive(smem_u32(&e.bar_wdone[wring.i]));
     }
+    trace_ev(tr, it, EV_EPI_DONE);
     wring.next();
   }
 }
@@ -458,6 +508,7 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
 struct TcArgs {
   TcGeom g;
   int32_t order, chunk, probe;
+  uint64_t* trace;            // tuning: per-tile event timestamps of CTAs 0,1 (LSW_TC_TRACE), or null
   // coefficient inputs (same as SwitchParams)
   int32_t mode, top_k, n_experts;
   float scale;
@@ -475,7 +526,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
   __shared__ __align__(8) uint64_t bar_wfull[kTcMaxStages], bar_wempty[kTcMaxStages], bar_wdone[kTcMaxStages];
   __shared__ __align__(8) uint64_t bar_afull[4], bar_aempty[4];
   __shared__ __align__(8) uint64_t bar_bfull[2], bar_bempty[2];
-  __shared__ __align__(8) uint64_t bar_accfull[2], bar_accempty[2];
+  __shared__ __align__(8) uint64_t bar_accfull[kTcMaxAccBufs], bar_accempty[kTcMaxAccBufs];
 
   const TcGeom& g = args.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -504,12 +555,14 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
       mbar_init(smem_u32(&bar_wdone[s]), kTcEpiWarps);
     }
     for (int s = 0; s < g.a_stages; ++s) {
-      mbar_init(smem_u32(&bar_afull[s]), 1);
+      mbar_init(smem_u32(&bar_afull[s]), 32);             // one arrival per operand-warp lane
       mbar_init(smem_u32(&bar_aempty[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&bar_bfull[s]), 1);
       mbar_init(smem_u32(&bar_bempty[s]), 1);
+    }
+    for (int s = 0; s < g.acc_bufs; ++s) {
       mbar_init(smem_u32(&bar_accfull[s]), 1);
       mbar_init(smem_u32(&bar_accempty[s]), kTcEpiWarps);
     }
@@ -550,7 +603,8 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
       if (lane == 0) {
         const uint64_t pol_stream = policy_evict_first();
         Ring wring{0, 0, (uint32_t)g.w_stages};
-        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
+        uint32_t it = 0;
+        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
           mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
           const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
           mbar_expect_tx(wbar, nsub * kSubBytes);
@@ -558,65 +612,121 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
           for (int sb = 0; sb < nsub; ++sb)
             tma_load_3d(smem_u32(wdst + sb * kSubBytes), &maps.w[c.kd], c.cb * tile_cols + sb * kTcTN,
                         c.rb * kTcTM, c.layer, wbar, pol_stream);
+          trace_ev(args.trace, it, EV_W_ISSUED);
           wring.next();
         }
       }
     } else if (warp == 3) {
       // ============================ operand producer ========================
-      if (lane == 0 && !probe) {
+      if (!probe) {
         const uint64_t pol_keep = policy_evict_last();
         int64_t strip_prev = -1;
         Ring bring{0, 0, (uint32_t)g.b_bufs};
         Ring aring{0, 0, (uint32_t)g.a_stages};
         const size_t rpe = (size_t)g.rp;                   // elements per packed row
-        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
+        uint64_t* tr = lane == 0 ? args.trace : nullptr;
+        uint32_t it = 0;
+        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
           const TcKind& K = g.kind[c.kd];
-          if (strip_id(c) != strip_prev) {                 // B slices of a new 128-row strip
+          if (strip_id(c) != strip_prev && g.split) {
+            // Split mode: B slices of a new 128-row strip, scaled by their fp32
+            // coefficient and split exactly into hi + mid + lo bf16 parts
+            // (v = fl32(c_j b); hi = rne(v); mid = rne(v - hi); lo = v - hi - mid),
+            // written at the same (pre-swizzled) positions of 3 part arrays.
             if (strip_prev >= 0) bring.next();
             strip_prev = strip_id(c);
-            mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
-            const uint32_t bar = smem_u32(&bar_bfull[bring.i]);
-            mbar_expect_tx(bar, nt * g.b_bytes_per_term);
+            mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);   // MMAs of the old strip done
             uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
+            const uint32_t chunks = g.b_bytes_per_term / 16;
             for (int j = 0; j < nt; ++j) {
-              const __nv_bfloat16* src =
-                  K.Bp + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.dout_pad + (size_t)c.rb * kTcTM) * rpe;
-              bulk_load(smem_u32(dst + j * g.b_bytes_per_term), src, g.b_bytes_per_term, bar, pol_keep);
+              const uint4* src = reinterpret_cast<const uint4*>(
+                  K.Bp + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.dout_pad + (size_t)c.rb * kTcTM) * rpe);
+              const float cj = cf.c[j];
+              uint8_t* p0 = dst + (size_t)(3 * j + 0) * g.b_bytes_per_term;
+              for (uint32_t q = lane; q < chunks; q += 32) {
+                const uint4 u = __ldg(src + q);
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+                uint32_t hi[4], mid[4], lo[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  float v[2] = {__uint_as_float(w[i] << 16) * cj, __uint_as_float(w[i] & 0xffff0000u) * cj};
+                  __nv_bfloat162 h = __floats2bfloat162_rn(v[0], v[1]);
+                  const float r0 = v[0] - __low2float(h), r1 = v[1] - __high2float(h);
+                  __nv_bfloat162 m = __floats2bfloat162_rn(r0, r1);
+                  __nv_bfloat162 l = __floats2bfloat162_rn(r0 - __low2float(m), r1 - __high2float(m));
+                  hi[i] = *reinterpret_cast<uint32_t*>(&h);
+                  mid[i] = *reinterpret_cast<uint32_t*>(&m);
+                  lo[i] = *reinterpret_cast<uint32_t*>(&l);
+                }
+                reinterpret_cast<uint4*>(p0)[q] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                reinterpret_cast<uint4*>(p0 + g.b_bytes_per_term)[q] = make_uint4(mid[0], mid[1], mid[2], mid[3]);
+                reinterpret_cast<uint4*>(p0 + 2 * g.b_bytes_per_term)[q] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+              }
             }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA (async)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_bfull[bring.i]));
+          } else if (strip_id(c) != strip_prev) {          // B slices of a new 128-row strip (bulk, rare)
+            if (strip_prev >= 0) bring.next();
+            strip_prev = strip_id(c);
+            if (lane == 0) {
+              mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
+              const uint32_t bar = smem_u32(&bar_bfull[bring.i]);
+              mbar_expect_tx(bar, nt * g.b_bytes_per_term);
+              uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
+              for (int j = 0; j < nt; ++j) {
+                const __nv_bfloat16* src =
+                    K.Bp + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.dout_pad + (size_t)c.rb * kTcTM) * rpe;
+                bulk_load(smem_u32(dst + j * g.b_bytes_per_term), src, g.b_bytes_per_term, bar, pol_keep);
+              }
+            }
+            __syncwarp();
           }
-          // A^T slices of this tile's columns
+          // A^T slices of this tile's columns, through the LSU (cp.async, 16 B per
+          // lane) rather than the TMA engine: 4-KB bulk ops would queue behind
+          // the W tiles already in the SM's TMA queue and arrive microseconds late.
           mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
-          const uint32_t abar = smem_u32(&bar_afull[aring.i]);
           uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
           const __nv_bfloat16* blk =
               K.At + (((size_t)c.layer * K.col_tiles + c.cb) * g.n_experts) * (size_t)tile_cols * rpe;
-          if (g.a_all) {
-            // one op for the whole block (bulk-copy throughput scales with bytes per op)
-            mbar_expect_tx(abar, g.n_experts * g.a_bytes_per_term);
-            bulk_load(smem_u32(adst), blk, g.n_experts * g.a_bytes_per_term, abar, pol_keep);
-          } else {
-            mbar_expect_tx(abar, nt * g.a_bytes_per_term);
-            for (int j = 0; j < nt; ++j)
-              bulk_load(smem_u32(adst + j * g.a_bytes_per_term), blk + (size_t)cf.e[j] * tile_cols * rpe,
-                        g.a_bytes_per_term, abar, pol_keep);
+          for (int j = 0; j < nt; ++j) {
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(blk + (size_t)cf.e[j] * tile_cols * rpe);
+            const uint32_t dst = smem_u32(adst + j * g.a_bytes_per_term);
+            for (uint32_t off = lane * 16; off < g.a_bytes_per_term; off += 32 * 16)
+              asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+                           ::"r"(dst + off), "l"(src + off), "l"(pol_keep) : "memory");
           }
+          // the A stage's mbarrier tracks these copies asynchronously (one
+          // arrival per lane when its copies land); the MMA thread issues the
+          // generic->async proxy fence after its wait
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar_afull[aring.i]))
+                       : "memory");
+          trace_ev(tr, it, EV_A_ISSUED);
           aring.next();
         }
       }
     } else if (warp == 1) {
       // ============================ MMA issuer ==============================
-      if (lane == 0 && !probe) {
+      // The whole warp runs the loop (all values warp-uniform, so operands stay
+      // in uniform registers); one elected lane issues each tcgen05 instruction.
+      if (!probe) {
         // instruction descriptor: D f32, A/B bf16, both K-major, N = 64, M = 128
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcTN >> 3) << 17) |
                                ((uint32_t)(kTcTM >> 4) << 24);
         const uint32_t row_bytes = g.rp * 2;
         const uint32_t sbo = 8 * row_bytes;
         const int ksteps = g.rp / 16;
+        // smem descriptors advance linearly with the start address (>> 4, no carry
+        // out of the 14-bit field: addresses < 256 KB)
+        const uint64_t desc0 = umma_desc(0, sbo, g.swz_mode);
+        const uint64_t b_term = g.b_bytes_per_term >> 4, a_term = g.a_bytes_per_term >> 4;
+        uint64_t* tr = lane == 0 ? args.trace : nullptr;
         Ring bring{0, 0, (uint32_t)g.b_bufs};
         Ring aring{0, 0, (uint32_t)g.a_stages};
         Ring acc{0, 0, (uint32_t)g.acc_bufs};
         Cursor c = cursor_first(g, seq);
         int64_t strip_prev = -1;
+        uint32_t it = 0;
         while (c.t >= 0) {
           const int64_t strip = strip_id(c);
           if (strip != strip_prev) {
@@ -625,27 +735,61 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
             mbar_wait(smem_u32(&bar_bfull[bring.i]), bring.phase);
           }
           mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
-          const uint32_t a_stage = smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes);
-          const uint32_t b_strip = smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes);
-          for (int sb = 0; sb < nsub; ++sb) {
+          // A slices were written by cp.async (generic proxy); order them before
+          // the tensor core's (async-proxy) operand reads
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          trace_ev(tr, it, EV_MMA_START);
+          const uint64_t a_desc = desc0 + (smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes) >> 4);
+          const uint64_t b_desc = desc0 + (smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes) >> 4);
+          if (g.split) {
+            // ONE group per tile: N = 64*nsub columns, all terms x 3 parts into one accumulator
             mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
+            trace_ev(tr, it, EV_MMA_ACC0);
             tc_fence_after();
-            const uint32_t d0 = tmem_base + acc.i * g.max_terms * kTcTN;
-            const uint32_t a_sub = a_stage + sb * kTcTN * row_bytes;
-            for (int j = 0; j < nt; ++j) {
-              const uint32_t a_j = a_sub + (g.a_all ? cf.e[j] : j) * g.a_bytes_per_term;
-              for (int kk = 0; kk < ksteps; ++kk)
-                umma_f16(d0 + j * kTcTN, umma_desc(b_strip + j * g.b_bytes_per_term + kk * 32, sbo, g.swz_mode),
-                         umma_desc(a_j + kk * 32, sbo, g.swz_mode), idesc, kk > 0 ? 1u : 0u);
+            const uint32_t idesc_t = (idesc & ~(0x3Fu << 17)) | ((uint32_t)((kTcTN * nsub) >> 3) << 17);
+            const uint32_t d = tmem_base + acc.i * (kTcTN * nsub);
+            if (elect_one()) {
+              uint32_t accum = 0;
+              for (int j = 0; j < nt; ++j)
+                for (int p = 0; p < 3; ++p)
+                  for (int kk = 0; kk < ksteps; ++kk) {
+                    umma_f16(d, b_desc + (3 * j + p) * b_term + kk * 2, a_desc + j * a_term + kk * 2, idesc_t, accum);
+                    accum = 1;
+                  }
+              umma_commit(smem_u32(&bar_accfull[acc.i]));
             }
-            umma_commit(smem_u32(&bar_accfull[acc.i]));
+            __syncwarp();
+            trace_ev(tr, it, EV_MMA_ISSUED0);
             acc.next();
           }
-          umma_commit(smem_u32(&bar_aempty[aring.i]));       // A slices consumed
-          aring.next();
+          for (int sb = 0; sb < nsub && !g.split; ++sb) {
+            mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
+            if (sb == 0) trace_ev(tr, it, EV_MMA_ACC0);
+            tc_fence_after();
+            const uint32_t d0 = tmem_base + acc.i * g.max_terms * kTcTN;
+            const uint64_t a_sub = a_desc + ((sb * kTcTN * row_bytes) >> 4);
+            if (elect_one()) {
+              for (int j = 0; j < nt; ++j)
+                for (int kk = 0; kk < ksteps; ++kk)
+                  umma_f16(d0 + j * kTcTN, b_desc + j * b_term + kk * 2, a_sub + j * a_term + kk * 2, idesc,
+                           kk > 0 ? 1u : 0u);
+              umma_commit(smem_u32(&bar_accfull[acc.i]));
+            }
+            __syncwarp();
+            if (sb == 0) trace_ev(tr, it, EV_MMA_ISSUED0);
+            acc.next();
+          }
           // B strip no longer needed once this CTA's next tile is in another strip
           cursor_next(g, seq, c);
-          if (c.t < 0 || strip_id(c) != strip) umma_commit(smem_u32(&bar_bempty[bring.i]));
+          const bool strip_ends = c.t < 0 || strip_id(c) != strip;
+          if (elect_one()) {
+            umma_commit(smem_u32(&bar_aempty[aring.i]));     // A slices consumed
+            if (strip_ends) umma_commit(smem_u32(&bar_bempty[bring.i]));
+          }
+          __syncwarp();
+          trace_ev(tr, it, EV_MMA_DONE);
+          ++it;
+          aring.next();
         }
       }
     } else if (warp == 2 && !g.store_stg) {
@@ -653,7 +797,8 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
       if (lane == 0) {
         const uint64_t pol_stream = policy_evict_first();
         Ring wring{0, 0, (uint32_t)g.w_stages};
-        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c)) {
+        uint32_t it = 0;
+        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
           mbar_wait(smem_u32(&bar_wdone[wring.i]), wring.phase);     // epilogue wrote the tile
           uint8_t* wsrc = wst0 + (size_t)wring.i * g.w_stage_bytes;
           for (int sb = 0; sb < nsub; ++sb)
@@ -662,6 +807,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read -> stage reusable
           mbar_arrive(smem_u32(&bar_wempty[wring.i]));
+          trace_ev(args.trace, it, EV_STAGE_FREE);
           wring.next();
         }
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -669,8 +815,13 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
     } else if (warp >= kTcFirstEpiWarp) {
       // ============================ epilogue ================================
       const int ntc = (probe || skip_math) ? 0 : nt;
-      EpiCtx ec{g, wst0, tmem_base, warp, lane, probe, bar_wfull, bar_wdone, bar_wempty, bar_accfull, bar_accempty};
-      switch (ntc) {
+      EpiCtx ec{g, wst0, tmem_base, warp, lane, probe, skip_math, bar_wfull, bar_wdone, bar_wempty, bar_accfull,
+                bar_accempty,
+                args.trace};
+      // split mode always runs the split loop (its TMEM buffer protocol differs);
+      // with probe/skip_math it only skips the math
+      switch (g.split && nt > 0 && !probe ? kSplitNT : ntc) {
+        case kSplitNT: epilogue_loop<kSplitNT>(ec, seq, cf); break;
         case 0: epilogue_loop<0>(ec, seq, cf); break;
         case 1: epilogue_loop<1>(ec, seq, cf); break;
         case 2: epilogue_loop<2>(ec, seq, cf); break;
@@ -785,60 +936,75 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   g.rp = rp;
   g.max_terms = 2 * sp.top_k;
   g.swz_mode = rp == 16 ? 6u : rp == 32 ? 4u : 2u;        // SWIZZLE_32B / 64B / 128B (UMMA encoding)
-  const uint32_t cols1 = (uint32_t)g.max_terms * kTcTN;
-  if (cols1 > 512) { delete plan; *why = "2*top_k*64 TMEM columns exceed 512"; return cudaErrorNotSupported; }
-  g.acc_bufs = cols1 * 2 <= 512 ? 2 : 1;
-  uint32_t need = cols1 * g.acc_bufs, cols = 32;
-  while (cols < need) cols <<= 1;
-  g.tmem_cols = cols;
-  // shared-memory plan: prefer 2 sub-tiles per W tile, >= 4 W stages, 2 A stages, 2 B buffers
+  // Shared-memory / TMEM plan.  Candidates in order of preference:
+  //   split mode, 128-column tiles (one accumulator of 128 columns per tile, 4 TMEM
+  //     buffers; B strip holds 3 parts per term, single-buffered);
+  //   per-term mode, 128-column tiles (max_terms x 64 TMEM columns per sub-tile);
+  //   per-term mode, 64-column tiles.
+  // Each needs >= 2 A stages and enough W stages (4 for 128-column tiles).
   const uint32_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
   g.b_bytes_per_term = kTcTM * rp * 2;
   bool ok = false;
-  int nsub_env = 0;
+  int nsub_env = 0, split_env = -1;
   if (const char* v = getenv("LSW_TC_NSUB")) nsub_env = atoi(v);
-  int a_all_env = 0;                                     // measured: per-expert ops are faster
-  int a_max = 2;                                         // A-slice ring depth (tuning: LSW_TC_ASTAGES)
+  if (const char* v = getenv("LSW_TC_SPLIT")) split_env = atoi(v);
+  int a_max = 3;                                         // A-slice ring depth (tuning: LSW_TC_ASTAGES)
   if (const char* v = getenv("LSW_TC_ASTAGES")) { int x = atoi(v); if (x >= 1 && x <= 4) a_max = x; }
-  if (const char* v = getenv("LSW_TC_AALL")) a_all_env = atoi(v);
-  for (int cand = 0; cand < 4 && !ok; ++cand) {
+  // measured (scripts/tune_switch.py, 7B shape): per-term 4583 GB/s vs split 3756 GB/s --
+  // split mode triples the MMAs and the SS operand reads; it is opt-in (LSW_TC_SPLIT=1)
+  if (split_env < 0) split_env = 0;
+  for (int cand = 0; cand < 3 && !ok; ++cand) {
+    const int split = cand == 0 ? 1 : 0;
     const int nsub = cand < 2 ? 2 : 1;
-    const int a_all = (cand % 2 == 0) ? 1 : 0;           // prefer one op per tile for A
     if (nsub_env && nsub != nsub_env) continue;
-    if (a_all_env >= 0 && a_all != a_all_env) continue;
+    if (split_env >= 0 && split != split_env) continue;
+    // TMEM
+    const uint32_t buf_cols = split ? kTcTN * nsub : (uint32_t)g.max_terms * kTcTN;
+    if (buf_cols > 512) continue;
+    const int acc_bufs = split ? (int)(512 / buf_cols < 4 ? 512 / buf_cols : 4) : (buf_cols * 2 <= 512 ? 2 : 1);
+    // shared memory
     const uint32_t a_term = kTcTN * nsub * rp * 2;
-    if (a_all && (uint32_t)sp.n_experts * a_term > 32768) continue;
-    const uint32_t a_stage = align1k((a_all ? sp.n_experts : g.max_terms) * a_term);
-    const uint32_t b_buf = align1k(g.max_terms * g.b_bytes_per_term);
+    const uint32_t a_stage = align1k(g.max_terms * a_term);
+    const uint32_t b_buf = align1k(g.max_terms * (split ? 3 : 1) * g.b_bytes_per_term);
     const uint32_t w_stage = nsub * kSubBytes;
-    for (int bbufs = 2; bbufs >= 1 && !ok; --bbufs)
-      for (int astages = a_max; astages >= 1 && !ok; --astages) {
+    for (int bbufs = split ? 1 : 2; bbufs >= 1 && !ok; --bbufs)
+      for (int astages = a_max; astages >= 2 && !ok; --astages) {
         int ws = (int)((budget - (int64_t)bbufs * b_buf - (int64_t)astages * a_stage) / w_stage);
         if ((int64_t)budget < (int64_t)bbufs * b_buf + (int64_t)astages * a_stage) ws = 0;
         if (ws > kTcMaxStages) ws = kTcMaxStages;
-        const int min_ws = nsub == 2 ? 4 : 3;
-        if (ws >= min_ws || (nsub == 1 && ws >= 2 && bbufs == 1 && astages == 1)) {
+        const int min_ws = nsub == 2 ? 4 : 2;
+        if (ws >= min_ws) {
           ok = true;
+          g.split = split;
           g.nsub = nsub;
           g.w_stages = ws;
           g.a_stages = astages;
           g.b_bufs = bbufs;
+          g.acc_bufs = acc_bufs;
           g.a_bytes_per_term = a_term;
           g.a_stage_bytes = a_stage;
-          g.a_all = a_all;
+          g.a_all = 0;
           g.b_buf_bytes = b_buf;
           g.w_stage_bytes = w_stage;
+          uint32_t cols = 32;
+          while (cols < buf_cols * acc_bufs) cols <<= 1;
+          g.tmem_cols = cols;
         }
       }
   }
-  if (!ok) { delete plan; *why = "shared memory: rank * top_k too large"; return cudaErrorNotSupported; }
+  if (!ok) { delete plan; *why = "shared memory / TMEM: rank * top_k too large"; return cudaErrorNotSupported; }
   // tuning knobs (defaults are the measured best)
   if (const char* v = getenv("LSW_TC_STAGES")) { int x = atoi(v); if (x >= 2 && x < g.w_stages) g.w_stages = x; }
   if (const char* v = getenv("LSW_TC_ORDER")) plan->order = strcmp(v, "sweep") == 0 ? ORDER_SWEEP : ORDER_STRIP;
   if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
   if (const char* v = getenv("LSW_TC_PROBE")) plan->probe = atoi(v);
-  g.store_stg = 1;
-  if (const char* v = getenv("LSW_TC_STORE")) g.store_stg = strcmp(v, "tma") != 0;
+  if (getenv("LSW_TC_TRACE")) {
+    const size_t tb = sizeof(uint64_t) * kTraceCtas * kTraceTiles * kTraceEvents;
+    if (cudaMalloc(&plan->trace, tb) == cudaSuccess) cudaMemset(plan->trace, 0, tb);
+    else plan->trace = nullptr;
+  }
+  g.store_stg = 0;                                       // measured: TMA store 4466 vs STG 4222 GB/s
+  if (const char* v = getenv("LSW_TC_STORE")) g.store_stg = strcmp(v, "stg") == 0;
   g.smem_bytes = g.w_stages * g.w_stage_bytes + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
   // tiles
   const int tile_cols = kTcTN * g.nsub;
@@ -854,6 +1020,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   }
   g.tiles_total = t;
   plan->grid = (int)(t < num_sms ? t : num_sms);
+  // testing knob: fewer CTAs -> many tiles per CTA even for small shapes (ring wrap-around)
+  if (const char* v = getenv("LSW_TC_GRID")) { int x = atoi(v); if (x >= 1 && x < plan->grid) plan->grid = x; }
   if (plan->grid < 1) plan->grid = 1;
   // pack operands + encode maps
   const int64_t M = (int64_t)sp.n_layers * sp.n_experts;
@@ -900,6 +1068,7 @@ void tc_plan_destroy(TcPlan* plan) {
     cudaFree(plan->packed_At[k]);
     cudaFree(plan->packed_B[k]);
   }
+  cudaFree(plan->trace);
   delete plan;
 }
 
@@ -908,12 +1077,21 @@ int tc_plan_grid(const TcPlan* plan) { return plan ? plan->grid : 0; }
 int tc_plan_tile_n(const TcPlan* plan) { return plan ? kTcTN * plan->geom.nsub : 0; }
 int64_t tc_plan_tiles(const TcPlan* plan) { return plan ? plan->geom.tiles_total : 0; }
 
+int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n) {
+  if (!plan || !plan->trace) return 0;
+  const int64_t total = (int64_t)kTraceCtas * kTraceTiles * kTraceEvents;
+  if (n > total) n = total;
+  if (cudaMemcpy(host, plan->trace, n * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return n;
+}
+
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s) {
   TcArgs a;
   a.g = plan->geom;
   a.order = plan->order;
   a.chunk = plan->chunk;
   a.probe = plan->probe;
+  a.trace = plan->trace;
   a.mode = p.mode;
   a.top_k = p.top_k;
   a.n_experts = p.n_experts;

@@ -33,7 +33,7 @@ idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
 gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6452.8
 for setting in [x for _ in range(a.repeat) for x in a.settings]:
-    for k in ("LSW_TC_ORDER", "LSW_TC_CHUNK", "LSW_TC_STAGES", "LSW_TC_PROBE", "LSW_TC_NSUB", "LSW_TC_AALL", "LSW_TC_STORE", "LSW_TC_ASTAGES"):
+    for k in ("LSW_TC_ORDER", "LSW_TC_CHUNK", "LSW_TC_STAGES", "LSW_TC_PROBE", "LSW_TC_NSUB", "LSW_TC_AALL", "LSW_TC_STORE", "LSW_TC_ASTAGES", "LSW_TC_SPLIT"):
         os.environ.pop(k, None)
     for kv in setting.split(","):
         if not kv:

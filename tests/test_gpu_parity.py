@@ -107,6 +107,25 @@ def test_switch_trajectory_full_elements(name, impl):
         S.sw.unmerge_all_layers()          # LSW_E_STATE
 
 
+@pytest.mark.parametrize("grid", [1, 3])
+@pytest.mark.parametrize("split", ["1", "0"])
+@pytest.mark.parametrize("name", ["mini", "mini-r32"])
+def test_tc_switch_many_tiles_per_cta(monkeypatch, name, split, grid):
+    """The mini shapes give every CTA a single tile at the default grid; force a
+    tiny grid so every ring (W, A, B, TMEM accumulators) wraps many times, in
+    both accumulator modes (split: pre-scaled B parts; per-term accumulators)."""
+    monkeypatch.setenv("LSW_TC_GRID", str(grid))
+    monkeypatch.setenv("LSW_TC_SPLIT", split)
+    try:
+        S = Setup(name, "tc", n_tokens=6)
+    except L.LswError as e:           # split mode not available for this shape
+        assert split == "1" and "UNSUPPORTED" in str(e)
+        pytest.skip(str(e))
+    assert S.sw.info()["grid"] == grid
+    worst = _run_token_checks(S, 5)
+    print(f"{name} split={split} grid={grid}: worst {worst}")
+
+
 @pytest.mark.parametrize("name,impl", [("toy", "simt"), ("mini", "tc")])
 def test_decode_gemv_parity(name, impl):
     S = Setup(name, impl, n_tokens=2)
