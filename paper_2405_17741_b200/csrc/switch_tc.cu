@@ -14,14 +14,15 @@
 //    place in shared memory and written back by nsub TMA bulk tensor stores.
 //    3-D tensor maps [L, d_out, d_in] zero-fill / clip ragged tiles and never
 //    spill into the next layer.
-//  * Each persistent CTA (grid = #SMs) walks one contiguous range of the tile
-//    sequence (kind, layer, row block, column block), i.e. ALONG 128-row strips:
-//    the strip's B slices (UMMA operand A: 128 x r per expert, K-major) stay
-//    resident in shared memory; the A slices (UMMA operand B: A^T, 64*nsub x r
-//    per expert, K-major) stream through their own ring.  Both come from ctx-
-//    owned copies packed at create time PRE-SWIZZLED into the exact shared-memory
-//    image the UMMA descriptors expect, so each slice is ONE contiguous
-//    cp.async.bulk copy (not 128 tiny 32-byte TMA rows).
+//  * The tile sequence (kind, layer, row block, column block) is cut into chunks
+//    of 32 consecutive tiles dealt round-robin to the persistent CTAs (grid =
+//    #SMs): a CTA walks ALONG a 128-row strip within its chunk, so the strip's B
+//    slices (UMMA operand A: 128 x r per expert, K-major) stay resident in
+//    shared memory, while all CTAs together sweep one matrix at a time, so the
+//    A slices (UMMA operand B: A^T, 64*nsub x r per expert, K-major), re-read by
+//    every row strip, stay L2-resident.  Both come from ctx-owned copies packed
+//    at create time PRE-SWIZZLED into the exact shared-memory image the UMMA
+//    descriptors expect (B: one cp.async.bulk per slice; A: cp.async, below).
 //  * One tcgen05.mma (kind::f16, bf16 in, fp32 accumulate, M=128, N=64, K=16)
 //    per expert per 16 of r per 64-column sub-tile, each expert into ITS OWN
 //    TMEM accumulator, double-buffered across sub-tiles: the gate coefficients
@@ -98,7 +99,11 @@ struct TcGeom {
 struct TcPlan {
   TcMaps maps;
   TcGeom geom;
-  int32_t order = ORDER_STRIP, chunk = 4, probe = 0;
+  // Tile order (measured, 7B shape, same run): strip 4.60-4.67 TB/s, sweep with
+  // 32-tile chunks 5.02-5.03 TB/s.  With strip order the 148 CTAs work on ~148
+  // different matrices, so the per-tile A^T slices (re-read once per row strip)
+  // fall out of L2; the chunked sweep keeps all CTAs on ~one matrix.
+  int32_t order = ORDER_SWEEP, chunk = 32, probe = 0;
   uint64_t* trace = nullptr;  // LSW_TC_TRACE: [kTraceCtas][kTraceTiles][kTraceEvents] device timestamps
   void* packed_At[LSW_NKIND] = {};
   void* packed_B[LSW_NKIND] = {};
@@ -257,7 +262,8 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
 // ------------------------------------------------------------------ tile walk
 
 // Per-CTA tile sequence over the global (kind, layer, row block, column block)
-// order.  ORDER_STRIP (default, measured best): one contiguous range per CTA.
+// order.  ORDER_STRIP: one contiguous range per CTA.  ORDER_SWEEP (default,
+// measured best): chunks of consecutive tiles dealt round-robin to the CTAs.
 // ORDER_SWEEP: chunks of `chunk` consecutive tiles dealt round-robin.
 
 struct Cursor {
