@@ -138,7 +138,7 @@ __device__ __forceinline__ void g_mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 template <bool kBf16>
-__global__ void __launch_bounds__(kBulkThreads, 1)
+__global__ void __launch_bounds__(kBulkThreads, 2)
 gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
@@ -258,7 +258,11 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
     if (R < 1) R = 1;
     if (R > 8) R = 8;
     const size_t slot_bytes = (size_t)R * row_bytes;
-    const size_t budget = 220 * 1024;
+    // ~110 KB per CTA so the NEXT GEMV's CTA fits beside this one on the SM:
+    // under programmatic dependent launch it starts (and prefetches W) while
+    // this kernel drains, instead of after it.  LSW_GEMV_SMEM_KB overrides.
+    size_t budget = 110 * 1024;
+    if (const char* v = getenv("LSW_GEMV_SMEM_KB")) { long x = atol(v); if (x >= 32 && x <= 224) budget = (size_t)x * 1024; }
     int slots = (int)((budget - x_bytes) / slot_bytes);
     if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
     if (slots >= 2) {
