@@ -138,7 +138,7 @@ __device__ __forceinline__ void g_mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 template <bool kBf16>
-__global__ void __launch_bounds__(kBulkThreads, 2)
+__global__ void __launch_bounds__(kBulkThreads, 1)
 gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
@@ -151,11 +151,17 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) 
   const int64_t G = gridDim.x;
   const int64_t n_chunks = (p.rows_total + R - 1) / R;            // chunk c = rows [c*R, c*R + R)
   const int64_t my_chunks = n_chunks > blockIdx.x ? (n_chunks - blockIdx.x + G - 1) / G : 0;
+  // Chunks issued so far.  A consumer warp takes only every 8th row, so it can
+  // reach a slot's NEXT-but-one fill while the next fill is not yet issued; the
+  // full barrier's parity would then alias an already completed phase.  Waiting
+  // for the ticket first makes the parity wait unambiguous.
+  __shared__ volatile int64_t issued;
   if (threadIdx.x == 0) {
     for (int s = 0; s < slots; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&full[s])), "r"(1));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&empty[s])), "r"(R));
     }
+    issued = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();                                  // barrier inits visible
@@ -196,6 +202,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) 
               : "memory");
           r = run_end;
         }
+        issued = i + 1;                             // ticket: chunk i's fill is armed
       }
     }
     return;
@@ -218,6 +225,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) 
     const int k = (int)(u - i * R);
     const int s = (int)(i % slots);
     const int64_t row = (blockIdx.x + i * G) * R + k;
+    while (issued <= i) __nanosleep(64);
     g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
     if (row < p.rows_total) {
       const uint4* w4 = reinterpret_cast<const uint4*>(ring + s * slot_bytes + (size_t)k * row_bytes);
@@ -258,10 +266,10 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
     if (R < 1) R = 1;
     if (R > 8) R = 8;
     const size_t slot_bytes = (size_t)R * row_bytes;
-    // ~110 KB per CTA so the NEXT GEMV's CTA fits beside this one on the SM:
-    // under programmatic dependent launch it starts (and prefetches W) while
-    // this kernel drains, instead of after it.  LSW_GEMV_SMEM_KB overrides.
-    size_t budget = 110 * 1024;
+    // Ring budget.  Measured (7B token of GEMVs): 220 KB 2.37 ms, 110 KB 2.59 ms,
+    // 72 KB 3.49 ms -- a deep ring per SM beats letting the next GEMV's CTA
+    // co-reside under PDL.  LSW_GEMV_SMEM_KB overrides.
+    size_t budget = 220 * 1024;
     if (const char* v = getenv("LSW_GEMV_SMEM_KB")) { long x = atol(v); if (x >= 32 && x <= 224) budget = (size_t)x * 1024; }
     int slots = (int)((budget - x_bytes) / slot_bytes);
     if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;

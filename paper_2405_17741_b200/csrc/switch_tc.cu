@@ -103,7 +103,7 @@ struct TcPlan {
   // 32-tile chunks 5.02-5.03 TB/s.  With strip order the 148 CTAs work on ~148
   // different matrices, so the per-tile A^T slices (re-read once per row strip)
   // fall out of L2; the chunked sweep keeps all CTAs on ~one matrix.
-  int32_t order = ORDER_SWEEP, chunk = 32, probe = 0;
+  int32_t order = ORDER_SWEEP, chunk = 48, probe = 0;   // chunk 24/32/48/64: 5317/5183/5358/5286 GB/s
   uint64_t* trace = nullptr;  // LSW_TC_TRACE: [kTraceCtas][kTraceTiles][kTraceEvents] device timestamps
   void* packed_At[LSW_NKIND] = {};
   void* packed_B[LSW_NKIND] = {};
