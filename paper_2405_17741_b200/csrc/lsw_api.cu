@@ -296,12 +296,16 @@ static lsw_status gemv_sites(lsw_ctx* ctx, int layer, const int* kinds, int n, c
   p.d_in = ctx->kinds[kinds[0]].d_in;
   p.x = x;
   p.y = y;
+  // Row-parallel kinds under TP need the communicator: checked before anything
+  // is enqueued (header contract).
+  const bool allreduce = ctx->cfg.tp_size > 1 && ctx->kinds[kinds[0]].row_parallel;
+  if (allreduce && !ctx->comm)
+    return fail(LSW_E_NCCL, "%s: tp_size=%d but no NCCL communicator attached", who, ctx->cfg.tp_size);
   cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->num_sms, s, early_w);
   if (e != cudaSuccess) return cuda_fail(e, "decode GEMV launch");
   ++ctx->launches;
   // Row-parallel kinds under TP: partial sums -> allreduce.
-  if (ctx->cfg.tp_size > 1 && ctx->kinds[kinds[0]].row_parallel) {
-    if (!ctx->comm) return fail(LSW_E_NCCL, "%s: tp_size=%d but no NCCL communicator attached", who, ctx->cfg.tp_size);
+  if (allreduce) {
     ncclResult_t r = ncclAllReduce(y, y, (size_t)rows, ncclFloat, ncclSum, ctx->comm, s);
     if (r != ncclSuccess) return fail(LSW_E_NCCL, "%s: ncclAllReduce: %s", who, ncclGetErrorString(r));
   }
