@@ -297,15 +297,7 @@ def run_ours(args, cfg):
         e0.record(stream)
         sw.merge_all_layers(idx, gate, stream)
         e1.record(stream)
-        for l in range(cfg.n_layers):
-            xo = l * (info["xs_elems"] // cfg.n_layers)
-            yo = l * (info["ys_elems"] // cfg.n_layers)
-            for gi, grp in enumerate(synth.GROUPS):
-                d_in = cfg.local_shape(grp[0], rank, world)[1]
-                n_out = sum(cfg.local_shape(k, rank, world)[0] for k in grp)
-                sw.decode_group(l, gi, xs[xo:xo + d_in], ys[yo:yo + n_out], stream)
-                xo += d_in
-                yo += n_out
+        sw.decode_all_layers(xs, ys, stream)
         e2.record(stream)
     torch.cuda.synchronize()
     for t in range(args.steps):

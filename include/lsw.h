@@ -154,6 +154,9 @@ typedef struct {
   uint64_t kernel_launches;  /* kernels this ctx has launched so far                 */
   int64_t  packed_bytes;     /* ctx-owned packed operand bytes on the device         */
   int64_t  xs_elems, ys_elems; /* token I/O sizes (lsw_decode_token)                  */
+  int32_t  switch_kernel;    /* tensor-core switch kernel: 1 = per-term TMEM (v1),    */
+                             /* 2 = term groups (any k <= 4, r <= 64); 0 = SIMT      */
+  int32_t  reserved;
 } lsw_info;
 
 /* Returns LSW_ABI_VERSION. */
@@ -227,11 +230,21 @@ LSW_API lsw_status lsw_decode_group(lsw_ctx* ctx, int32_t layer, int32_t group, 
                             void* stream);
 
 /*
- * One whole Alg. 1 token: router(x1) -> merge_all_layers -> for every layer the
- * four group GEMVs.  xs packs the GEMV inputs layer-major, group-minor
- * (QKV, O, GATE_UP, DOWN; each of its local d_in); ys packs the outputs the
- * same way (each group's concatenated local d_out).  Sizes: lsw_get_info
- * xs_elems / ys_elems.  idx/gate receive the decision (device).
+ * Alg. 1 l.5 (Eq. 3) for a whole token on the current weights: for
+ * every layer, in order, the four group GEMVs (QKV, O, GATE_UP, DOWN).
+ * xs packs the GEMV inputs layer-major, group-minor (each of its local d_in,
+ * cfg dtype); ys packs the fp32 outputs the same way (each group's concatenated
+ * local d_out).  Sizes: lsw_get_info xs_elems / ys_elems.  tp_size == 1: ONE
+ * persistent launch in which group g reads its x only after every CTA has
+ * finished group g-1 (decoder order); tp_size > 1: one launch per group plus
+ * the NCCL all-reduce of the row-parallel groups.  Results are bitwise equal
+ * to lsw_decode_group called group by group.
+ */
+LSW_API lsw_status lsw_decode_all_layers(lsw_ctx* ctx, const void* xs, float* ys, void* stream);
+
+/*
+ * One whole Alg. 1 token: router(x1) -> merge_all_layers -> lsw_decode_all_layers.
+ * idx/gate receive the decision (device).
  */
 LSW_API lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs, float* ys,
                             int32_t* idx, float* gate, void* stream);

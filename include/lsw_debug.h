@@ -4,11 +4,13 @@
  * when enabled by environment variables read at lsw_create:
  *
  *   LSW_TC_TRACE=1   the tensor-core switch kernel stamps %globaltimer (ns) at
- *                    12 pipeline events of its first 256 tiles in CTAs 0 and 1
- *                    (layout [cta][tile][event], events in switch_tc.cu:
- *                    W issued, A issued, A full, MMA start, MMA done, epilogue
- *                    saw W, epilogue saw accumulators, stage freed, epilogue
- *                    done, MMA got a free accumulator buffer); 0 = not reached.
+ *                    16 pipeline event slots of its first 2048 tiles in 4 CTAs
+ *                    spread over the grid (layout [cta][tile][event], events in
+ *                    switch_tc.cu EV_*: W issued, A issued, A full, MMA start,
+ *                    MMA done, epilogue saw W, epilogue saw accumulators, stage
+ *                    freed, epilogue done, MMA got a free accumulator buffer,
+ *                    MMAs issued, first sub-tile done, A production began, A
+ *                    ring slot free); 0 = not reached.
  */
 #ifndef LSW_DEBUG_H_
 #define LSW_DEBUG_H_

@@ -32,7 +32,7 @@ IMPL_NAME = {v: k for k, v in IMPL.items()}
 SYMBOLS = (
     "lsw_abi_version", "lsw_last_error", "lsw_create", "lsw_destroy", "lsw_get_info",
     "lsw_nccl_get_unique_id", "lsw_attach_nccl", "lsw_router_topk", "lsw_merge_all_layers",
-    "lsw_unmerge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_token",
+    "lsw_unmerge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers", "lsw_decode_token",
     "lsw_decode_token_host", "lsw_device_status",
     "lsw_debug_switch_trace",      # include/lsw_debug.h (tuning hook)
 )
@@ -61,10 +61,13 @@ class Info(ctypes.Structure):
     _fields_ = [("tiles_total", ctypes.c_int64), ("switch_impl", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("tile_m", ctypes.c_int32), ("tile_n", ctypes.c_int32), ("merged", ctypes.c_int32),
                 ("num_sms", ctypes.c_int32), ("kernel_launches", ctypes.c_uint64),
-                ("packed_bytes", ctypes.c_int64), ("xs_elems", ctypes.c_int64), ("ys_elems", ctypes.c_int64)]
+                ("packed_bytes", ctypes.c_int64), ("xs_elems", ctypes.c_int64), ("ys_elems", ctypes.c_int64),
+                ("switch_kernel", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
-def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+def load_library(path: str = LIB_PATH, strict: bool = True) -> ctypes.CDLL:
+    """strict=False (tuning scripts only: A/B against an older build) skips
+    entry points the library does not export."""
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                           "(the CUDA library is required; there is no CPU fallback)")
@@ -83,12 +86,15 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "lsw_unmerge_all_layers": (i32, [vp, vp]),
         "lsw_decode_linear": (i32, [vp, i32, i32, vp, vp, vp]),
         "lsw_decode_group": (i32, [vp, i32, i32, vp, vp, vp]),
+        "lsw_decode_all_layers": (i32, [vp, vp, vp, vp]),
         "lsw_decode_token": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_decode_token_host": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_device_status": (i32, [vp, vp, ctypes.POINTER(i32)]),
         "lsw_debug_switch_trace": (i32, [vp, vp, i64, ctypes.POINTER(i64)]),
     }
     for name, (res, args) in sig.items():
+        if not strict and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
@@ -197,6 +203,10 @@ class LoraSwitch:
     def decode_group(self, layer: int, group: int, x: torch.Tensor, y: torch.Tensor, stream=None):
         _check(lib().lsw_decode_group(self._h, layer, group, _ptr(x), _ptr(y), _stream(stream)))
 
+    def decode_all_layers(self, xs, ys, stream=None):
+        """Every group GEMV of every layer (packed xs -> packed ys), decoder order."""
+        _check(lib().lsw_decode_all_layers(self._h, _ptr(xs), _ptr(ys), _stream(stream)))
+
     def decode_token(self, x1, xs, ys, idx, gate, stream=None):
         _check(lib().lsw_decode_token(self._h, _ptr(x1), _ptr(xs), _ptr(ys), _ptr(idx), _ptr(gate),
                                       _stream(stream)))
@@ -207,12 +217,12 @@ class LoraSwitch:
 
     def debug_switch_trace(self):
         """Tuning hook (include/lsw_debug.h): int64 ns timestamps [2, 256, 12]
-        of the last tensor-core switch launch when LSW_TC_TRACE was set ([cta, tile, event])."""
+        of the last tensor-core switch launch when LSW_TC_TRACE was set ([cta, tile, event], 16 events)."""
         import numpy as np
-        buf = np.zeros(4 * 2048 * 12, dtype=np.uint64)
+        buf = np.zeros(4 * 2048 * 16, dtype=np.uint64)
         n = ctypes.c_int64(0)
         _check(lib().lsw_debug_switch_trace(self._h, buf.ctypes.data, buf.size, ctypes.byref(n)))
-        return buf[: n.value].reshape(-1, 2048, 12) if n.value else None
+        return buf[: n.value].reshape(-1, 2048, 16) if n.value else None
 
     def device_status(self, stream=None) -> int:
         code = ctypes.c_int32(0)

@@ -246,6 +246,241 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) 
   }
 }
 
+// ---------------------------------------------------------------------------
+// K4b: the whole token's GEMVs in one persistent launch.  The groups' chunks
+// (R rows each) form one global sequence, chunk c -> CTA c % G, so every SM
+// streams the same number of bytes (+-1 chunk) over the token.  The producer
+// runs through ALL of its chunks back to back (W does not depend on x), so the
+// HBM stream does not drain at group boundaries the way it does between
+// launches; the consumers keep the decoder's order: x of group g is copied in
+// only after all CTAs have counted group g-1 done on a device-wide counter
+// (release add / acquire load), and y of group g-1 is complete by then.
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wait_counter(const unsigned long long* p, unsigned long long target) {
+  if ((long long)(ld_acquire_u64(p) - target) >= 0) return;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
+  for (uint32_t n = 1; (long long)(ld_acquire_u64(p) - target) < 0; ++n) {
+    __nanosleep(32);
+    if ((n & 1023u) == 0) {
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) __trap();
+    }
+  }
+}
+
+template <bool kBf16>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+gemv_token_kernel(const TokGroup* __restrict__ grp, int32_t n_groups, int64_t total_chunks,
+                  const uint8_t* __restrict__ xs, float* __restrict__ ys, int32_t slots, uint32_t slot_bytes,
+                  uint32_t x_cap, unsigned long long* done, unsigned long long base, int32_t flags) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots], xbar;
+  __shared__ volatile int64_t issued;               // ticket, as in gemv_bulk_kernel
+  constexpr int64_t es = kBf16 ? 2 : 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* xsm = smem_raw;
+  uint8_t* ring = smem_raw + x_cap;
+  const int64_t G = gridDim.x, b = blockIdx.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < slots; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&full[s])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&empty[s])), "r"(kBulkConsumers));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&xbar)), "r"(1));
+    issued = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // W is written by the switch before us
+  if (warp == 0) {
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      int g = 0;
+      int64_t next = n_groups > 1 ? grp[1].chunk_begin : total_chunks;
+      int64_t i = 0;
+      for (int64_t c = b; c < total_chunks; c += G, ++i) {
+        while (c >= next) { ++g; next = g + 1 < n_groups ? grp[g + 1].chunk_begin : total_chunks; }
+        const TokGroup* t = grp + g;
+        const int s = (int)(i % slots);
+        g_mbar_wait(s_u32(&empty[s]), (uint32_t)((i / slots) & 1) ^ 1);
+        const int64_t rows = t->rows, R = t->R, rb_ = t->row_bytes;
+        const int64_t r0 = (c - t->chunk_begin) * R;
+        const int64_t r1 = r0 + R < rows ? r0 + R : rows;
+        const uint32_t bar = s_u32(&full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                     "r"((uint32_t)((r1 - r0) * rb_)) : "memory");
+        const int ns = t->n_sites;
+        for (int q = 0; q < ns; ++q) {       // one bulk copy per site the chunk overlaps
+          const int64_t sb = t->row_begin[q], se = q + 1 < ns ? t->row_begin[q + 1] : rows;
+          const int64_t a = r0 > sb ? r0 : sb, e = r1 < se ? r1 : se;
+          if (a >= e) continue;
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(t->W[q]) + (a - sb) * rb_;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+              ::"r"(s_u32(ring + (size_t)s * slot_bytes + (a - r0) * rb_)), "l"(src),
+                "r"((uint32_t)((e - a) * rb_)), "r"(bar), "l"(pol)
+              : "memory");
+        }
+        issued = i + 1;
+      }
+    }
+    return;
+  }
+  const int cw = warp - 1;
+  int64_t i0 = 0;                                   // this CTA's chunks before group g
+  uint32_t xphase = 0;
+  for (int g = 0; g < n_groups; ++g) {
+    const TokGroup* t = grp + g;
+    const int64_t cb = t->chunk_begin, ce = g + 1 < n_groups ? grp[g + 1].chunk_begin : total_chunks;
+    const int64_t rows = t->rows, R = t->R;
+    const uint32_t row_bytes = t->row_bytes;
+    const int64_t first = cb + (((b - cb) % G) + G) % G;
+    const int64_t nj = first < ce ? (ce - first + G - 1) / G : 0;
+    if (nj > 0) {
+      // decoder order: x of group g only after every CTA has finished group g-1
+      if (threadIdx.x == 32) {
+        if (g > 0 && !(flags & 1)) wait_counter(done, base + (unsigned long long)g * (unsigned long long)G);
+        const uint32_t xb = s_u32(&xbar);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(xb), "r"(row_bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(s_u32(xsm)), "l"(xs + t->x_off * es), "r"(row_bytes), "r"(xb) : "memory");
+      }
+      g_mbar_wait(s_u32(&xbar), xphase & 1);
+      ++xphase;
+      const int64_t nchunk16 = row_bytes / 16;
+      const uint4* x4 = reinterpret_cast<const uint4*>(xsm);
+      float* yg = ys + t->y_off;
+      for (int64_t j = 0; j < nj; ++j) {
+        const int64_t i = i0 + j;
+        const int s = (int)(i % slots);
+        const int64_t r0 = (first + j * G - cb) * R;
+        const int64_t nr = rows - r0 < R ? rows - r0 : R;
+        while (issued <= i) __nanosleep(64);
+        g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
+        // rows of the flat sequence (j*R + k) are dealt to warps round-robin
+        for (int64_t k = ((cw - (j * R) % kBulkConsumers) % kBulkConsumers + kBulkConsumers) % kBulkConsumers;
+             k < nr; k += kBulkConsumers) {
+          const uint4* w4 = reinterpret_cast<const uint4*>(ring + (size_t)s * slot_bytes + (size_t)k * row_bytes);
+          float acc0 = 0.f, acc1 = 0.f;
+          int64_t c = lane;
+          for (; c + 32 < nchunk16; c += 64) {
+            acc0 += dot_chunk<kBf16>(w4[c], x4, c);
+            acc1 += dot_chunk<kBf16>(w4[c + 32], x4, c + 32);
+          }
+          if (c < nchunk16) acc0 += dot_chunk<kBf16>(w4[c], x4, c);
+          float acc = acc0 + acc1;
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+          if (lane == 0) yg[r0 + k] = acc;
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[s])) : "memory");
+      }
+      i0 += nj;
+    }
+    // this CTA is done with group g: x buffer free, its y rows written
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
+    if (threadIdx.x == 32) {
+      __threadfence();
+      asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(done), "l"(1ull) : "memory");
+    }
+  }
+}
+
+cudaError_t tok_plan_create(TokPlan* plan, TokGroup* groups, int32_t n_groups, int num_sms) {
+  *plan = TokPlan{};
+  // rows per chunk: ~32 KB per bulk copy (LSW_GEMV_SLOT_KB), at most 8 rows
+  uint32_t target = 32 * 1024;
+  if (const char* v = getenv("LSW_GEMV_SLOT_KB")) { long x = atol(v); if (x >= 4 && x <= 96) target = (uint32_t)x * 1024; }
+  uint32_t slot = 0, xcap = 0;
+  int64_t chunks = 0;
+  for (int g = 0; g < n_groups; ++g) {
+    TokGroup& t = groups[g];
+    int R = (int)(target / t.row_bytes);
+    if (R < 1) R = 1;
+    if (R > 8) R = 8;
+    t.R = R;
+    t.chunk_begin = chunks;
+    chunks += (t.rows + R - 1) / R;
+    const uint32_t sb = (uint32_t)R * t.row_bytes;
+    if (sb > slot) slot = sb;
+    const uint32_t xb = (t.row_bytes + 127) & ~127u;
+    if (xb > xcap) xcap = xb;
+  }
+  slot = (slot + 127) & ~127u;
+  size_t budget = 220 * 1024;
+  if (const char* v = getenv("LSW_GEMV_SMEM_KB")) { long x = atol(v); if (x >= 32 && x <= 224) budget = (size_t)x * 1024; }
+  int slots = budget > xcap ? (int)((budget - xcap) / slot) : 0;
+  if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
+  if (slots < 2) return cudaErrorNotSupported;
+  int grid = (int)(chunks < num_sms ? chunks : num_sms);
+  if (const char* v = getenv("LSW_GEMV_GRID")) { long x = atol(v); if (x >= 1 && x < grid) grid = (int)x; }
+  if (grid < 1) grid = 1;
+  cudaError_t e = cudaMalloc(&plan->d_groups, sizeof(TokGroup) * (size_t)n_groups);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(plan->d_groups, groups, sizeof(TokGroup) * (size_t)n_groups, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cudaFree(plan->d_groups); plan->d_groups = nullptr; return e; }
+  plan->n_groups = n_groups;
+  plan->total_chunks = chunks;
+  plan->slot_bytes = slot;
+  plan->x_cap = xcap;
+  plan->slots = slots;
+  plan->grid = grid;
+  plan->smem = (size_t)xcap + (size_t)slots * slot;
+  if (const char* v = getenv("LSW_GEMV_TOKEN_FLAGS")) plan->flags = atoi(v);
+  return cudaSuccess;
+}
+
+void tok_plan_destroy(TokPlan* plan) {
+  if (plan->d_groups) cudaFree(plan->d_groups);
+  *plan = TokPlan{};
+}
+
+cudaError_t launch_gemv_token(const TokPlan& plan, const void* xs, float* ys, unsigned long long* done,
+                              unsigned long long base, int32_t dtype, cudaStream_t s) {
+  const bool bf16 = dtype == LSW_BF16;
+  auto fn = bf16 ? gemv_token_kernel<true> : gemv_token_kernel<false>;
+  static size_t smem_set[2] = {0, 0};
+  if (plan.smem > smem_set[bf16]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    if (e != cudaSuccess) return e;
+    smem_set[bf16] = plan.smem;
+  }
+  // The group counter needs every CTA resident at once: one CTA per SM, grid
+  // <= SM count, and a cooperative launch so the driver guarantees it.
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(plan.grid);
+  lc.blockDim = dim3(kBulkThreads);
+  lc.dynamicSmemBytes = plan.smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 2;
+  static int use_pdl = 1;                 // dropped once if the driver refuses cooperative + PDL
+  lc.numAttrs = use_pdl ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&lc, fn, (const TokGroup*)plan.d_groups, plan.n_groups, plan.total_chunks,
+                                     (const uint8_t*)xs, ys, plan.slots, plan.slot_bytes, plan.x_cap, done, base, plan.flags);
+  if (e != cudaSuccess && use_pdl) {
+    (void)cudaGetLastError();
+    use_pdl = 0;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, fn, (const TokGroup*)plan.d_groups, plan.n_groups, plan.total_chunks,
+                           (const uint8_t*)xs, ys, plan.slots, plan.slot_bytes, plan.x_cap, done, base, plan.flags);
+  }
+  return e;
+}
+
 static int gemv_variant() {
   static int v = -1;
   if (v < 0) {

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include <nccl.h>
 
@@ -55,6 +56,8 @@ struct lsw_ctx {
   int64_t xs_elems = 0, ys_elems = 0;
   int64_t x_off[LSW_NGROUP] = {}, y_off[LSW_NGROUP] = {};   // per-layer offsets
   int64_t x_per_layer = 0, y_per_layer = 0;
+  TokPlan tok{};                        // whole-token GEMV (tp_size == 1), else empty
+  unsigned long long tok_base = 0;      // DevState::tok_done before the next token launch
   // staging for lsw_decode_token_host
   void* st_x1 = nullptr;
   void* st_xs = nullptr;
@@ -175,6 +178,31 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
   ctx->y_per_layer = yo;
   ctx->xs_elems = xo * c.n_layers;
   ctx->ys_elems = yo * c.n_layers;
+  // whole-token GEMV plan (single GPU; TP keeps per-group launches for the all-reduce)
+  const char* tv = getenv("LSW_GEMV_TOKEN");
+  if (c.tp_size == 1 && tv && tv[0] == '1') {
+    std::vector<TokGroup> tg((size_t)c.n_layers * LSW_NGROUP);
+    for (int l = 0; l < c.n_layers; ++l)
+      for (int g = 0; g < LSW_NGROUP; ++g) {
+        TokGroup& t = tg[(size_t)l * LSW_NGROUP + g];
+        memset(&t, 0, sizeof(t));
+        int64_t rows = 0;
+        for (int i = 0; i < kGroupSize[g]; ++i) {
+          const lsw_kind_desc& d = kinds[kGroupKinds[g][i]];
+          t.W[i] = (const uint8_t*)d.W + (size_t)l * d.d_out * d.d_in * esize(ctx);
+          t.row_begin[i] = rows;
+          rows += d.d_out;
+        }
+        t.n_sites = kGroupSize[g];
+        t.rows = rows;
+        t.row_bytes = (uint32_t)(kinds[kGroupKinds[g][0]].d_in * esize(ctx));
+        t.x_off = l * ctx->x_per_layer + ctx->x_off[g];
+        t.y_off = l * ctx->y_per_layer + ctx->y_off[g];
+      }
+    e = tok_plan_create(&ctx->tok, tg.data(), (int32_t)tg.size(), ctx->num_sms);
+    if (e == cudaErrorMemoryAllocation) { lsw_destroy(ctx); return fail(LSW_E_OOM, "lsw_create: token GEMV table"); }
+    if (e != cudaSuccess) { (void)cudaGetLastError(); ctx->tok = TokPlan{}; }   // per-group launches instead
+  }
   *out = ctx;
   return LSW_OK;
 }
@@ -184,6 +212,7 @@ lsw_status lsw_destroy(lsw_ctx* ctx) {
   cudaDeviceSynchronize();
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->tc) tc_plan_destroy(ctx->tc);
+  tok_plan_destroy(&ctx->tok);
   cudaFree(ctx->d_state);
   cudaFree(ctx->st_x1);
   cudaFree(ctx->st_xs);
@@ -204,6 +233,7 @@ lsw_status lsw_get_info(const lsw_ctx* ctx, lsw_info* info) {
     info->tile_m = 128;
     info->tile_n = tc_plan_tile_n(ctx->tc);
     info->packed_bytes = tc_plan_bytes(ctx->tc);
+    info->switch_kernel = tc_plan_kernel(ctx->tc);
   } else {
     info->tiles_total = ctx->simt_geom.tiles_total;
     info->grid = ctx->num_sms * 4;
@@ -333,14 +363,28 @@ lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs, float*
   if (st != LSW_OK) return st;
   st = lsw_merge_all_layers(ctx, idx, gate, stream);                                   // l.2-4
   if (st != LSW_OK) return st;
+  return lsw_decode_all_layers(ctx, xs, ys, stream);                                  // l.5
+}
+
+lsw_status lsw_decode_all_layers(lsw_ctx* ctx, const void* xs, float* ys, void* stream) {
+  if (!ctx || !xs || !ys) return fail(LSW_E_ARG, "lsw_decode_all_layers: null argument");
+  if (reinterpret_cast<uintptr_t>(xs) % 16) return fail(LSW_E_ARG, "lsw_decode_all_layers: xs not 16-byte aligned");
+  if (ctx->tok.d_groups) {
+    cudaError_t e = launch_gemv_token(ctx->tok, xs, ys, &ctx->d_state->tok_done, ctx->tok_base, ctx->cfg.dtype,
+                                      (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_all_layers: token GEMV launch");
+    ctx->tok_base += (unsigned long long)ctx->tok.n_groups * (unsigned long long)ctx->tok.grid;
+    ++ctx->launches;
+    return LSW_OK;
+  }
   const size_t es = esize(ctx);
-  for (int l = 0; l < ctx->cfg.n_layers; ++l)                                          // l.5
+  for (int l = 0; l < ctx->cfg.n_layers; ++l)
     for (int g = 0; g < LSW_NGROUP; ++g) {
       const uint8_t* xp = (const uint8_t*)xs + (size_t)(l * ctx->x_per_layer + ctx->x_off[g]) * es;
       float* yp = ys + l * ctx->y_per_layer + ctx->y_off[g];
-      // every GEMV but the first after the switch may prefetch W under PDL
-      st = gemv_sites(ctx, l, kGroupKinds[g], kGroupSize[g], xp, yp, (cudaStream_t)stream, "lsw_decode_token",
-                      /*early_w=*/l > 0 || g > 0);
+      // every GEMV but the first may prefetch W under PDL (the first may follow the switch)
+      lsw_status st = gemv_sites(ctx, l, kGroupKinds[g], kGroupSize[g], xp, yp, (cudaStream_t)stream,
+                                 "lsw_decode_all_layers", /*early_w=*/l > 0 || g > 0);
       if (st != LSW_OK) return st;
     }
   return LSW_OK;

@@ -25,6 +25,7 @@ struct DevState {
   int32_t pad;
   int32_t idx[2][LSW_MAX_TOPK];
   float g[2][LSW_MAX_TOPK];
+  unsigned long long tok_done;   // group-completion counter of the whole-token GEMV (gemv.cu)
 };
 
 // One kind's stacked tensors, as the kernels see them.
@@ -153,6 +154,35 @@ struct GemvParams {
 // griddepcontrol.wait; see gemv.cu).
 cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w = false);
 
+// Whole-token decode GEMV (gemv.cu, K4b): every group of every layer in ONE
+// persistent launch.  The W stream runs ahead across group boundaries; group
+// g's x is read only after every CTA has finished group g-1 (a device-wide
+// counter), so the launch keeps the layer-by-layer dependency of a decoder.
+struct TokGroup {
+  const void* W[3];         // site matrices [d_out, d_in] of this (layer, group)
+  int64_t row_begin[3];     // first output row of each site (row_begin[0] = 0)
+  int64_t rows;             // group output rows (sum of the sites' d_out)
+  int64_t x_off, y_off;     // offsets (elements) into the packed xs / ys
+  int64_t chunk_begin;      // first global chunk of this group (filled by the planner)
+  int32_t n_sites, R;       // R: rows per chunk (filled by the planner)
+  uint32_t row_bytes, pad;
+};
+struct TokPlan {
+  TokGroup* d_groups = nullptr;   // device copy of the table
+  int32_t n_groups = 0;
+  int64_t total_chunks = 0;
+  uint32_t slot_bytes = 0, x_cap = 0;
+  int32_t slots = 0, grid = 0;
+  int32_t flags = 0;              // tuning only (LSW_GEMV_TOKEN_FLAGS): bit 0 = skip the group wait
+  size_t smem = 0;
+};
+// groups: host table with W/row_begin/rows/x_off/y_off/n_sites/row_bytes set.
+cudaError_t tok_plan_create(TokPlan* plan, TokGroup* groups, int32_t n_groups, int num_sms);
+void tok_plan_destroy(TokPlan* plan);
+// done: DevState::tok_done; base: its value when this launch starts.
+cudaError_t launch_gemv_token(const TokPlan& plan, const void* xs, float* ys, unsigned long long* done,
+                              unsigned long long base, int32_t dtype, cudaStream_t s);
+
 // Tensor-core switch (switch_tc.cu).
 struct TcPlan;   // opaque: packed operands + TMA descriptors
 cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why);
@@ -163,5 +193,6 @@ int tc_plan_tile_n(const TcPlan* plan);
 int64_t tc_plan_tiles(const TcPlan* plan);
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
 int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);   // tuning trace (lsw_debug.h)
+int tc_plan_kernel(const TcPlan* plan);   // 1: v1 (switch_tc.cu), 2: term groups (switch_tc_tg.cu)
 
 }  // namespace lsw

@@ -1,0 +1,41 @@
+// switch_tc_impl.cuh -- the two tensor-core switch kernels behind lsw::tc_plan_*
+// (switch_tc_dispatch.cu picks one per ctx at create time):
+//
+//   v1 (switch_tc.cu): every term of a 64-column sub-tile in its own TMEM
+//      accumulator, two buffers of 2k x 64 columns -- needs 2k <= 4 and one
+//      tile's A slices for all terms in shared memory; the measured fastest
+//      where it fits (7B: 0.83 of the copy peak).
+//   tg (switch_tc_tg.cu): a tile's terms stream through TMEM tg at a time
+//      with an fp32 running sum in the epilogue, A slices staged per
+//      (sub-tile, term group): any k <= 4, any r <= 64.
+#pragma once
+
+#include "lsw_internal.cuh"
+
+namespace lsw {
+namespace v1 {
+struct TcPlan;
+// strict: refuse (cudaErrorNotSupported) a degraded plan (64-column tiles,
+// single TMEM buffer, split mode) instead of building it
+cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why, bool strict);
+void tc_plan_destroy(TcPlan* plan);
+int64_t tc_plan_bytes(const TcPlan* plan);
+int tc_plan_grid(const TcPlan* plan);
+int tc_plan_tile_n(const TcPlan* plan);
+int64_t tc_plan_tiles(const TcPlan* plan);
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
+int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);
+}  // namespace v1
+
+namespace tg {
+struct TcPlan;
+cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why);
+void tc_plan_destroy(TcPlan* plan);
+int64_t tc_plan_bytes(const TcPlan* plan);
+int tc_plan_grid(const TcPlan* plan);
+int tc_plan_tile_n(const TcPlan* plan);
+int64_t tc_plan_tiles(const TcPlan* plan);
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
+int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);
+}  // namespace tg
+}  // namespace lsw

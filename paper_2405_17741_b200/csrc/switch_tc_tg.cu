@@ -1,4 +1,4 @@
-// switch_tc.cu -- K1-tc: the all-layer in-place switch on the 5th-gen tensor cores.
+// switch_tc_tg.cu -- K1-tc (term-group variant): the all-layer in-place switch on the 5th-gen tensor cores.
 //
 // What it computes (identical to K1-simt): for every adapted matrix m of every
 // layer, in ONE persistent launch (SGMM Eq. 11; in place P:328):
@@ -33,11 +33,12 @@
 //    in the (conflict-free, 128B-swizzled) stage.
 //  * Warp roles: 0 = W producer (TMA), 1 = TMEM allocator + MMA issuer,
 //    2 = store warp (TMA stores, frees W stages as soon as they are read),
-//    3 = operand producer (B strips by bulk copy; per-tile A slices by cp.async
-//    on the LSU path, so they do not queue behind W tiles in the TMA engine),
-//    4..11 = epilogue.
-//    W prefetch depth is therefore set by the W ring alone, not by the
-//    operand ring that the MMA releases.
+//    3 = operand producer (B strips and per-(sub-tile, term group) A slices by
+//    TMA bulk copies), 4..11 = epilogue.  A tile's 2k terms stream through
+//    TMEM buffers tg terms at a time; the epilogue keeps an fp32 running sum
+//    (so any k fits TMEM) and, having seen a group's accumulators, releases
+//    that group's A slot (and, at a strip's end, the B strip), so the MMA warp
+//    commits exactly once per group (each commit drains the tensor pipe).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -48,7 +49,7 @@
 #include "switch_tc_impl.cuh"
 
 namespace lsw {
-namespace v1 {
+namespace tg {
 
 constexpr int kTcTM = 128;                 // tile rows = UMMA M = TMEM lanes
 constexpr int kTcTN = 64;                  // sub-tile columns = UMMA N
@@ -58,6 +59,7 @@ constexpr int kTcFirstEpiWarp = 4;
 constexpr int kTcThreads = 32 * (kTcFirstEpiWarp + kTcEpiWarps);
 constexpr int kTcMaxStages = 8;
 constexpr int kTcMaxAccBufs = 4;           // TMEM accumulator buffers (mbarrier pairs)
+constexpr int kTcMaxAStages = 8;           // A-slice ring depth (units of one sub-tile x one term group)
 
 enum { ORDER_STRIP = 0, ORDER_SWEEP = 1 };
 
@@ -83,15 +85,13 @@ struct TcGeom {
   int32_t nsub;                           // 64-column sub-tiles per W tile (1 or 2)
   int32_t w_stages, a_stages, b_bufs, acc_bufs;
   int32_t max_terms;                      // 2k
+  int32_t tg;                             // terms per group: one TMEM buffer holds tg accumulators
+                                          // of 64 columns; a tile's terms stream through the
+                                          // buffers group by group (fp32 running sum in the epilogue)
   uint32_t tmem_cols;
-  uint32_t a_bytes_per_term;              // 64*nsub * rp * 2
+  uint32_t a_sub_bytes;                   // one term's A^T slice of one sub-tile: 64 * rp * 2
   uint32_t b_bytes_per_term;              // 128 * rp * 2
-  uint32_t a_stage_bytes, b_buf_bytes, w_stage_bytes;
-  int32_t a_all;                          // 1: one bulk op fetches all N experts' A slices of a tile
-  int32_t split;                          // 1: "split mode" -- c_j*B_j folded into B as 3 bf16 parts
-                                          //    (hi+mid+lo == the fp32 product), ONE accumulator per tile
-                                          //    (N = tile width), one MMA group per tile, 4 TMEM buffers;
-                                          // 0: one accumulator per expert term, c_j applied in the epilogue
+  uint32_t a_stage_bytes, b_buf_bytes, w_stage_bytes;   // A stage = one (sub-tile, group) unit
   int32_t store_stg;                      // 1: epilogue writes W back with coalesced STG.128 (LSU);
                                           // 0: the store warp issues TMA bulk tensor stores
   uint32_t swz_mode;                      // UMMA layout type of the r-wide operands
@@ -151,7 +151,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // layout [slot][tile][event].
 constexpr int kTraceTiles = 2048, kTraceEvents = 16, kTraceCtas = 4, kTraceStride = 49;
 enum { EV_W_ISSUED = 0, EV_A_ISSUED, EV_A_FULL, EV_MMA_START, EV_MMA_DONE, EV_EPI_WFULL, EV_EPI_ACC0,
-       EV_STAGE_FREE, EV_EPI_DONE, EV_MMA_ACC0, EV_MMA_ISSUED0, EV_EPI_SUB0_DONE };
+       EV_STAGE_FREE, EV_EPI_DONE, EV_MMA_ACC0, EV_MMA_ISSUED0, EV_EPI_SUB0_DONE, EV_A_BEGIN, EV_A_WAITED, EV_EPI_ACC1, EV_MMA_ISSUED1 };
 __device__ __forceinline__ void trace_ev(uint64_t* tr, uint32_t it, int ev) {
   if (tr && blockIdx.x % kTraceStride == 0 && it < (uint32_t)kTraceTiles) {
     uint64_t t;
@@ -349,63 +349,42 @@ __device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t v) {
   return *reinterpret_cast<uint32_t*>(&b2);
 }
 
-// One 16-column chunk of one row: W (two swizzled 16-B smem chunks) <-
-// RNE(W + sum_j c_j acc_j), with the sum in fp32 pairs (FFMA2), W as the first
-// addend.  NT = number of accumulators (compile-time).
-template <int NT>
-__device__ __forceinline__ void epi_chunk(uint32_t tm_addr, const uint64_t* c2, uint8_t* wrow, int row, int col16) {
-  uint32_t acc[NT][16];
-#pragma unroll
-  for (int j = 0; j < NT; ++j) tmem_ld16(tm_addr + j * kTcTN, acc[j]);
-  uint4* p0 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 0) ^ (row & 7)) << 4));
-  uint4* p1 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 1) ^ (row & 7)) << 4));
-  const uint4 u0 = *p0, u1 = *p1;
+// The epilogue keeps, per thread, one row x 32 columns of a sub-tile (two
+// 16-column chunks) as fp32 pairs: v = W first, then v <- c_j * acc_j + v for
+// j ascending (FFMA2), term group by term group, then ONE RNE to bf16.  The
+// order of the additions does not depend on the grouping.
+__device__ __forceinline__ void w_load16(const uint8_t* wrow, int row, int col16, uint64_t* v) {
+  const uint4 u0 = *reinterpret_cast<const uint4*>(wrow + (((col16 * 2 + 0) ^ (row & 7)) << 4));
+  const uint4 u1 = *reinterpret_cast<const uint4*>(wrow + (((col16 * 2 + 1) ^ (row & 7)) << 4));
   const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-  tmem_wait_ld();
-  uint32_t o[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    uint64_t v = f2_pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
-#pragma unroll
-    for (int j = 0; j < NT; ++j)
-      v = ffma2(f2_pack(__uint_as_float(acc[j][2 * q]), __uint_as_float(acc[j][2 * q + 1])), c2[j], v);
-    o[q] = f2_to_bf16x2(v);
-  }
-  *p0 = make_uint4(o[0], o[1], o[2], o[3]);
-  *p1 = make_uint4(o[4], o[5], o[6], o[7]);
-}
-
-// General term count (> 4): groups of 4 accumulators.
-__device__ __forceinline__ void epi_chunk_many(uint32_t tm_addr, const float* cs, int nt, uint8_t* wrow, int row,
-                                               int col16) {
-  uint4* p0 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 0) ^ (row & 7)) << 4));
-  uint4* p1 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 1) ^ (row & 7)) << 4));
-  const uint4 u0 = *p0, u1 = *p1;
-  const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-  uint64_t v[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) v[q] = f2_pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
-  for (int j0 = 0; j0 < nt; j0 += 4) {
-    uint32_t acc[4][16];
-    const int nj = nt - j0 < 4 ? nt - j0 : 4;
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj)
-      if (jj < nj) tmem_ld16(tm_addr + (j0 + jj) * kTcTN, acc[jj]);
-    tmem_wait_ld();
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj)
-      if (jj < nj) {
-        const uint64_t c2 = f2_pack(cs[j0 + jj], cs[j0 + jj]);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          v[q] = ffma2(f2_pack(__uint_as_float(acc[jj][2 * q]), __uint_as_float(acc[jj][2 * q + 1])), c2, v[q]);
-      }
-  }
+}
+
+__device__ __forceinline__ void w_store16(uint8_t* wrow, int row, int col16, const uint64_t* v) {
   uint32_t o[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) o[q] = f2_to_bf16x2(v[q]);
-  *p0 = make_uint4(o[0], o[1], o[2], o[3]);
-  *p1 = make_uint4(o[4], o[5], o[6], o[7]);
+  *reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 0) ^ (row & 7)) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+  *reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 1) ^ (row & 7)) << 4)) = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+// One term group of one 16-column chunk: v <- c_j * acc_j + v for the group's
+// N accumulators at tm_addr + jj * 64 columns (N compile-time: no divergent
+// branches around the warp-collective TMEM loads).
+template <int N>
+__device__ __forceinline__ void epi_group16(uint32_t tm_addr, const float* cs, uint64_t* v) {
+  uint32_t acc[N][16];
+#pragma unroll
+  for (int jj = 0; jj < N; ++jj) tmem_ld16(tm_addr + jj * kTcTN, acc[jj]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int jj = 0; jj < N; ++jj) {
+    const uint64_t c2 = f2_pack(cs[jj], cs[jj]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      v[q] = ffma2(f2_pack(__uint_as_float(acc[jj][2 * q]), __uint_as_float(acc[jj][2 * q + 1])), c2, v[q]);
+  }
 }
 
 // ------------------------------------------------------------------ epilogue loop
@@ -422,58 +401,83 @@ struct EpiCtx {
   uint64_t* bar_wempty;
   uint64_t* bar_accfull;
   uint64_t* bar_accempty;
+  uint64_t* bar_aempty;        // A / B slots: released here once their MMAs are known complete
+  uint64_t* bar_bempty;
   uint64_t* trace;
 };
 
-// The epilogue warps' tile loop, specialised on the term count (NT = -1: any;
-// NT = kSplitNT: split mode, one pre-scaled accumulator per tile).
-constexpr int kSplitNT = 100;
-template <int NT>
+// The epilogue warps' tile loop, specialised on the group size TG (1..4; 0:
+// probe / skip_math, no TMEM reads) and the size TL of the last group.  Per
+// sub-tile: W -> fp32 running sum, one TMEM buffer per term group (wait full,
+// read, FFMA2, release), RNE back into the stage.
+template <int TG, int TL>
 __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& seq, const Coefs& cf) {
-  constexpr bool SPLIT = NT == kSplitNT;
   const TcGeom& g = e.g;
   const int ew = e.warp - kTcFirstEpiWarp;     // 0..7
   const int quarter = e.warp & 3;              // TMEM lane quarter this warp may access
   const int half = ew >> 2;                    // which 32 of a sub-tile's 64 columns
   const int row = quarter * 32 + e.lane;       // tile-local row == TMEM lane
-  uint64_t c2[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) c2[j] = (!SPLIT && NT > j) ? f2_pack(cf.c[j], cf.c[j]) : 0ull;
-  if (SPLIT) c2[0] = f2_pack(1.f, 1.f);        // W + acc (coefficients are already in the MMA)
   const int nt = cf.n;
-  // per-term mode: one TMEM buffer (max_terms x 64 columns) per sub-tile;
-  // split mode: one buffer (64*nsub columns) per tile
-  const uint32_t buf_cols = SPLIT ? kTcTN * g.nsub : g.max_terms * kTcTN;
+  const int tg = g.tg;                         // == TG unless TG == 0 or the list is shorter
+  const int ngroups = (nt + tg - 1) / tg;
+  const uint32_t buf_cols = (uint32_t)tg * kTcTN;
   Ring wring{0, 0, (uint32_t)g.w_stages};
   Ring acc{0, 0, (uint32_t)g.acc_bufs};
-  uint64_t* tr = (ew == 0 && e.lane == 0) ? e.trace : nullptr;
+  Ring aring{0, 0, (uint32_t)g.a_stages}, bring{0, 0, (uint32_t)g.b_bufs};
+  const bool releaser = ew == 0 && e.lane == 0;  // frees A units / B strips for the producer
+  uint64_t* tr = releaser ? e.trace : nullptr;
   uint32_t it = 0;
+  int64_t bstrip = -1;
   for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
+    if (releaser && !e.probe) {
+      // first tile of a new B strip: every MMA of the previous strip is done
+      // (this warp has seen all of its accumulators), so its B buffer is free
+      const int64_t st = strip_id(c);
+      if (st != bstrip) {
+        if (bstrip >= 0) {
+          mbar_arrive(smem_u32(&e.bar_bempty[bring.i]));
+          bring.next();
+        }
+        bstrip = st;
+      }
+    }
     mbar_wait(smem_u32(&e.bar_wfull[wring.i]), wring.phase);            // W tile landed (acquire)
     trace_ev(tr, it, EV_EPI_WFULL);
     uint8_t* wt = e.wst0 + (size_t)wring.i * g.w_stage_bytes;
     for (int sb = 0; sb < g.nsub; ++sb) {
-      if (!e.probe && (!SPLIT || sb == 0))
-        mbar_wait(smem_u32(&e.bar_accfull[acc.i]), acc.phase);          // accumulators ready
-      if (sb == 0) trace_ev(tr, it, EV_EPI_ACC0);
-      tc_fence_after();
       uint8_t* wrow = wt + sb * kSubBytes + row * 128;
-      const uint32_t tm_row = e.tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * buf_cols +
-                              (SPLIT ? sb * kTcTN : 0);
-#pragma unroll
-      for (int q2 = 0; q2 < 2; ++q2) {
-        const int col16 = half * 2 + q2;       // 16-column chunk 0..3 of the sub-tile
-        const uint32_t ta = tm_row + col16 * 16;
-        if constexpr (SPLIT) { if (!e.skip_math) epi_chunk<1>(ta, c2, wrow, row, col16); }
-        else if constexpr (NT > 0) epi_chunk<NT>(ta, c2, wrow, row, col16);
-        else if constexpr (NT < 0) epi_chunk_many(ta, cf.c, nt, wrow, row, col16);
+      uint64_t v[2][8];
+      if (TG > 0) {
+        w_load16(wrow, row, half * 2 + 0, v[0]);
+        w_load16(wrow, row, half * 2 + 1, v[1]);
       }
-      if (!SPLIT || sb == g.nsub - 1) {
-        // accumulators consumed -> MMA may reuse this TMEM buffer
-        tc_fence_before();
+      for (int gi = 0; gi < ngroups && !e.probe; ++gi) {
+        mbar_wait(smem_u32(&e.bar_accfull[acc.i]), acc.phase);          // this group's accumulators
+        if (sb == 0 && gi == 0) trace_ev(tr, it, EV_EPI_ACC0);
+        if (sb == 1 && gi == 0) trace_ev(tr, it, EV_EPI_ACC1);
+        // the group's MMAs are complete: its A unit may be overwritten
+        if (releaser) mbar_arrive(smem_u32(&e.bar_aempty[aring.i]));
+        aring.next();
+        tc_fence_after();
+        if constexpr (TG > 0) {
+          const uint32_t tm_row = e.tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * buf_cols;
+          const float* cs = cf.c + gi * TG;
+          if (gi + 1 < ngroups) {
+#pragma unroll
+            for (int q2 = 0; q2 < 2; ++q2) epi_group16<TG>(tm_row + (half * 2 + q2) * 16, cs, v[q2]);
+          } else {
+#pragma unroll
+            for (int q2 = 0; q2 < 2; ++q2) epi_group16<TL>(tm_row + (half * 2 + q2) * 16, cs, v[q2]);
+          }
+        }
+        tc_fence_before();                     // accumulators consumed -> MMA may reuse the buffer
         __syncwarp();
-        if (e.lane == 0 && !e.probe) mbar_arrive(smem_u32(&e.bar_accempty[acc.i]));
+        if (e.lane == 0) mbar_arrive(smem_u32(&e.bar_accempty[acc.i]));
         acc.next();
+      }
+      if (TG > 0) {
+        w_store16(wrow, row, half * 2 + 0, v[0]);
+        w_store16(wrow, row, half * 2 + 1, v[1]);
       }
       if (sb == 0) trace_ev(tr, it, EV_EPI_SUB0_DONE);
     }
@@ -532,7 +536,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
   __shared__ int32_t s_parity;
   __shared__ uint32_t s_tmem_base;
   __shared__ __align__(8) uint64_t bar_wfull[kTcMaxStages], bar_wempty[kTcMaxStages], bar_wdone[kTcMaxStages];
-  __shared__ __align__(8) uint64_t bar_afull[4], bar_aempty[4];
+  __shared__ __align__(8) uint64_t bar_afull[kTcMaxAStages], bar_aempty[kTcMaxAStages];
   __shared__ __align__(8) uint64_t bar_bfull[2], bar_bempty[2];
   __shared__ __align__(8) uint64_t bar_accfull[kTcMaxAccBufs], bar_accempty[kTcMaxAccBufs];
 
@@ -563,7 +567,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
       mbar_init(smem_u32(&bar_wdone[s]), kTcEpiWarps);
     }
     for (int s = 0; s < g.a_stages; ++s) {
-      mbar_init(smem_u32(&bar_afull[s]), 32);             // one arrival per operand-warp lane
+      mbar_init(smem_u32(&bar_afull[s]), 1);              // the producer's expect_tx arrival
       mbar_init(smem_u32(&bar_aempty[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -626,7 +630,12 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
       }
     } else if (warp == 3) {
       // ============================ operand producer ========================
-      if (!probe) {
+      // B strips and A slices by TMA bulk copies (async proxy: the MMA reads
+      // them after its mbarrier wait, no proxy fence).  One A ring unit per
+      // (sub-tile, term group): the group's slices of the sub-tile's 64 columns,
+      // each contiguous in the packed image.  Ring slots are released by the
+      // epilogue once the unit's accumulators are complete (see epilogue_loop).
+      if (!probe && lane == 0) {
         const uint64_t pol_keep = policy_evict_last();
         int64_t strip_prev = -1;
         Ring bring{0, 0, (uint32_t)g.b_bufs};
@@ -634,89 +643,51 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
         const size_t rpe = (size_t)g.rp;                   // elements per packed row
         uint64_t* tr = lane == 0 ? args.trace : nullptr;
         uint32_t it = 0;
+        const int tg = g.tg;
         for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
           const TcKind& K = g.kind[c.kd];
-          if (strip_id(c) != strip_prev && g.split) {
-            // Split mode: B slices of a new 128-row strip, scaled by their fp32
-            // coefficient and split exactly into hi + mid + lo bf16 parts
-            // (v = fl32(c_j b); hi = rne(v); mid = rne(v - hi); lo = v - hi - mid),
-            // written at the same (pre-swizzled) positions of 3 part arrays.
+          if (strip_id(c) != strip_prev) {                 // B slices of a new 128-row strip (rare)
             if (strip_prev >= 0) bring.next();
             strip_prev = strip_id(c);
-            mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);   // MMAs of the old strip done
+            mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
+            const uint32_t bar = smem_u32(&bar_bfull[bring.i]);
+            mbar_expect_tx(bar, nt * g.b_bytes_per_term);
             uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
-            const uint32_t chunks = g.b_bytes_per_term / 16;
             for (int j = 0; j < nt; ++j) {
-              const uint4* src = reinterpret_cast<const uint4*>(
-                  K.Bp + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.dout_pad + (size_t)c.rb * kTcTM) * rpe);
-              const float cj = cf.c[j];
-              uint8_t* p0 = dst + (size_t)(3 * j + 0) * g.b_bytes_per_term;
-              for (uint32_t q = lane; q < chunks; q += 32) {
-                const uint4 u = __ldg(src + q);
-                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-                uint32_t hi[4], mid[4], lo[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  float v[2] = {__uint_as_float(w[i] << 16) * cj, __uint_as_float(w[i] & 0xffff0000u) * cj};
-                  __nv_bfloat162 h = __floats2bfloat162_rn(v[0], v[1]);
-                  const float r0 = v[0] - __low2float(h), r1 = v[1] - __high2float(h);
-                  __nv_bfloat162 m = __floats2bfloat162_rn(r0, r1);
-                  __nv_bfloat162 l = __floats2bfloat162_rn(r0 - __low2float(m), r1 - __high2float(m));
-                  hi[i] = *reinterpret_cast<uint32_t*>(&h);
-                  mid[i] = *reinterpret_cast<uint32_t*>(&m);
-                  lo[i] = *reinterpret_cast<uint32_t*>(&l);
-                }
-                reinterpret_cast<uint4*>(p0)[q] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                reinterpret_cast<uint4*>(p0 + g.b_bytes_per_term)[q] = make_uint4(mid[0], mid[1], mid[2], mid[3]);
-                reinterpret_cast<uint4*>(p0 + 2 * g.b_bytes_per_term)[q] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-              }
+              const __nv_bfloat16* src =
+                  K.Bp + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.dout_pad + (size_t)c.rb * kTcTM) * rpe;
+              bulk_load(smem_u32(dst + j * g.b_bytes_per_term), src, g.b_bytes_per_term, bar, pol_keep);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> MMA (async)
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&bar_bfull[bring.i]));
-          } else if (strip_id(c) != strip_prev) {          // B slices of a new 128-row strip (bulk, rare)
-            if (strip_prev >= 0) bring.next();
-            strip_prev = strip_id(c);
-            if (lane == 0) {
-              mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
-              const uint32_t bar = smem_u32(&bar_bfull[bring.i]);
-              mbar_expect_tx(bar, nt * g.b_bytes_per_term);
-              uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
-              for (int j = 0; j < nt; ++j) {
-                const __nv_bfloat16* src =
-                    K.Bp + (((size_t)c.layer * g.n_experts + cf.e[j]) * K.dout_pad + (size_t)c.rb * kTcTM) * rpe;
-                bulk_load(smem_u32(dst + j * g.b_bytes_per_term), src, g.b_bytes_per_term, bar, pol_keep);
-              }
-            }
-            __syncwarp();
           }
-          // A^T slices of this tile's columns, through the LSU (cp.async, 16 B per
-          // lane) rather than the TMA engine: 4-KB bulk ops would queue behind
-          // the W tiles already in the SM's TMA queue and arrive microseconds late.
-          mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
-          uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
           const __nv_bfloat16* blk =
               K.At + (((size_t)c.layer * K.col_tiles + c.cb) * g.n_experts) * (size_t)tile_cols * rpe;
-          for (int j = 0; j < nt; ++j) {
-            const uint8_t* src = reinterpret_cast<const uint8_t*>(blk + (size_t)cf.e[j] * tile_cols * rpe);
-            const uint32_t dst = smem_u32(adst + j * g.a_bytes_per_term);
-            for (uint32_t off = lane * 16; off < g.a_bytes_per_term; off += 32 * 16)
-              asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
-                           ::"r"(dst + off), "l"(src + off), "l"(pol_keep) : "memory");
-          }
-          // the A stage's mbarrier tracks these copies asynchronously (one
-          // arrival per lane when its copies land); the MMA thread issues the
-          // generic->async proxy fence after its wait
-          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bar_afull[aring.i]))
-                       : "memory");
+          trace_ev(tr, it, EV_A_BEGIN);
+          for (int sb = 0; sb < nsub; ++sb)
+            for (int j0 = 0; j0 < nt; j0 += tg) {
+              mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
+              if (sb == 0 && j0 == 0) trace_ev(tr, it, EV_A_WAITED);
+              uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
+              const int n_in = nt - j0 < tg ? nt - j0 : tg;
+              const uint32_t bar = smem_u32(&bar_afull[aring.i]);
+              mbar_expect_tx(bar, (uint32_t)n_in * g.a_sub_bytes);
+              for (int jj = 0; jj < n_in; ++jj)
+                bulk_load(smem_u32(adst + jj * g.a_sub_bytes),
+                          blk + ((size_t)cf.e[j0 + jj] * tile_cols + (size_t)sb * kTcTN) * rpe, g.a_sub_bytes, bar,
+                          pol_keep);
+              aring.next();
+            }
           trace_ev(tr, it, EV_A_ISSUED);
-          aring.next();
         }
       }
     } else if (warp == 1) {
       // ============================ MMA issuer ==============================
       // The whole warp runs the loop (all values warp-uniform, so operands stay
       // in uniform registers); one elected lane issues each tcgen05 instruction.
+      // ONE commit per MMA group (measured, scripts/mmabench3.cu: every commit
+      // drains the tensor pipe, ~340 ns per group whatever its size, while an
+      // extra MMA inside a group costs ~20 ns), so the A / B slots are released
+      // by the epilogue after it has seen the group's accumulators, not by
+      // further commits.
       if (!probe) {
         // instruction descriptor: D f32, A/B bf16, both K-major, N = 64, M = 128
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcTN >> 3) << 17) |
@@ -727,77 +698,49 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
         // smem descriptors advance linearly with the start address (>> 4, no carry
         // out of the 14-bit field: addresses < 256 KB)
         const uint64_t desc0 = umma_desc(0, sbo, g.swz_mode);
-        const uint64_t b_term = g.b_bytes_per_term >> 4, a_term = g.a_bytes_per_term >> 4;
+        const uint64_t b_term = g.b_bytes_per_term >> 4, a_term = g.a_sub_bytes >> 4;
+        const int tg = g.tg;
+        const uint32_t buf_cols = (uint32_t)tg * kTcTN;
         uint64_t* tr = lane == 0 ? args.trace : nullptr;
         Ring bring{0, 0, (uint32_t)g.b_bufs};
         Ring aring{0, 0, (uint32_t)g.a_stages};
         Ring acc{0, 0, (uint32_t)g.acc_bufs};
-        Cursor c = cursor_first(g, seq);
         int64_t strip_prev = -1;
         uint32_t it = 0;
-        while (c.t >= 0) {
+        for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
           const int64_t strip = strip_id(c);
           if (strip != strip_prev) {
             if (strip_prev >= 0) bring.next();
             strip_prev = strip;
             mbar_wait(smem_u32(&bar_bfull[bring.i]), bring.phase);
           }
-          mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
-          // A slices were written by cp.async (generic proxy); order them before
-          // the tensor core's (async-proxy) operand reads
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           trace_ev(tr, it, EV_MMA_START);
-          const uint64_t a_desc = desc0 + (smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes) >> 4);
           const uint64_t b_desc = desc0 + (smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes) >> 4);
-          if (g.split) {
-            // ONE group per tile: N = 64*nsub columns, all terms x 3 parts into one accumulator
-            mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
-            trace_ev(tr, it, EV_MMA_ACC0);
-            tc_fence_after();
-            const uint32_t idesc_t = (idesc & ~(0x3Fu << 17)) | ((uint32_t)((kTcTN * nsub) >> 3) << 17);
-            const uint32_t d = tmem_base + acc.i * (kTcTN * nsub);
-            if (elect_one()) {
-              uint32_t accum = 0;
-              for (int j = 0; j < nt; ++j)
-                for (int p = 0; p < 3; ++p)
-                  for (int kk = 0; kk < ksteps; ++kk) {
-                    umma_f16(d, b_desc + (3 * j + p) * b_term + kk * 2, a_desc + j * a_term + kk * 2, idesc_t, accum);
-                    accum = 1;
-                  }
-              umma_commit(smem_u32(&bar_accfull[acc.i]));
+          // one MMA group per (sub-tile, term group): tg accumulators of 64 columns
+          for (int sb = 0; sb < nsub; ++sb)
+            for (int j0 = 0; j0 < nt; j0 += tg) {
+              mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
+              if (sb == 0 && j0 == 0) trace_ev(tr, it, EV_A_FULL);
+              mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
+              if (sb == 0 && j0 == 0) trace_ev(tr, it, EV_MMA_ACC0);
+              tc_fence_after();
+              const uint32_t d0 = tmem_base + acc.i * buf_cols;
+              const uint64_t a_desc = desc0 + (smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes) >> 4);
+              const int n_in = nt - j0 < tg ? nt - j0 : tg;
+              if (elect_one()) {
+                for (int jj = 0; jj < n_in; ++jj)
+                  for (int kk = 0; kk < ksteps; ++kk)
+                    umma_f16(d0 + jj * kTcTN, b_desc + (j0 + jj) * b_term + kk * 2, a_desc + jj * a_term + kk * 2,
+                             idesc, kk > 0 ? 1u : 0u);
+                umma_commit(smem_u32(&bar_accfull[acc.i]));
+              }
+              __syncwarp();
+              if (sb == 0 && j0 == 0) trace_ev(tr, it, EV_MMA_ISSUED0);
+              if (sb == 1 && j0 == 0) trace_ev(tr, it, EV_MMA_ISSUED1);
+              acc.next();
+              aring.next();
             }
-            __syncwarp();
-            trace_ev(tr, it, EV_MMA_ISSUED0);
-            acc.next();
-          }
-          for (int sb = 0; sb < nsub && !g.split; ++sb) {
-            mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
-            if (sb == 0) trace_ev(tr, it, EV_MMA_ACC0);
-            tc_fence_after();
-            const uint32_t d0 = tmem_base + acc.i * g.max_terms * kTcTN;
-            const uint64_t a_sub = a_desc + ((sb * kTcTN * row_bytes) >> 4);
-            if (elect_one()) {
-              for (int j = 0; j < nt; ++j)
-                for (int kk = 0; kk < ksteps; ++kk)
-                  umma_f16(d0 + j * kTcTN, b_desc + j * b_term + kk * 2, a_sub + j * a_term + kk * 2, idesc,
-                           kk > 0 ? 1u : 0u);
-              umma_commit(smem_u32(&bar_accfull[acc.i]));
-            }
-            __syncwarp();
-            if (sb == 0) trace_ev(tr, it, EV_MMA_ISSUED0);
-            acc.next();
-          }
-          // B strip no longer needed once this CTA's next tile is in another strip
-          cursor_next(g, seq, c);
-          const bool strip_ends = c.t < 0 || strip_id(c) != strip;
-          if (elect_one()) {
-            umma_commit(smem_u32(&bar_aempty[aring.i]));     // A slices consumed
-            if (strip_ends) umma_commit(smem_u32(&bar_bempty[bring.i]));
-          }
-          __syncwarp();
           trace_ev(tr, it, EV_MMA_DONE);
-          ++it;
-          aring.next();
         }
       }
     } else if (warp == 2 && !g.store_stg) {
@@ -824,18 +767,23 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
       // ============================ epilogue ================================
       const int ntc = (probe || skip_math) ? 0 : nt;
       EpiCtx ec{g, wst0, tmem_base, warp, lane, probe, skip_math, bar_wfull, bar_wdone, bar_wempty, bar_accfull,
-                bar_accempty,
-                args.trace};
-      // split mode always runs the split loop (its TMEM buffer protocol differs);
-      // with probe/skip_math it only skips the math
-      switch (g.split && nt > 0 && !probe ? kSplitNT : ntc) {
-        case kSplitNT: epilogue_loop<kSplitNT>(ec, seq, cf); break;
-        case 0: epilogue_loop<0>(ec, seq, cf); break;
-        case 1: epilogue_loop<1>(ec, seq, cf); break;
-        case 2: epilogue_loop<2>(ec, seq, cf); break;
-        case 3: epilogue_loop<3>(ec, seq, cf); break;
-        case 4: epilogue_loop<4>(ec, seq, cf); break;
-        default: epilogue_loop<-1>(ec, seq, cf); break;
+                bar_accempty, bar_aempty, bar_bempty, args.trace};
+      // group sizes of this pass: full groups of tg (a compacted list may be
+      // shorter than one group) and the last group's
+      const int tgc = ntc == 0 ? 0 : (ntc < g.tg ? ntc : g.tg);
+      const int tl = ntc == 0 ? 0 : ntc - (ntc - 1) / g.tg * g.tg;
+      switch (tgc * 8 + tl) {
+        case 1 * 8 + 1: epilogue_loop<1, 1>(ec, seq, cf); break;
+        case 2 * 8 + 1: epilogue_loop<2, 1>(ec, seq, cf); break;
+        case 2 * 8 + 2: epilogue_loop<2, 2>(ec, seq, cf); break;
+        case 3 * 8 + 1: epilogue_loop<3, 1>(ec, seq, cf); break;
+        case 3 * 8 + 2: epilogue_loop<3, 2>(ec, seq, cf); break;
+        case 3 * 8 + 3: epilogue_loop<3, 3>(ec, seq, cf); break;
+        case 4 * 8 + 1: epilogue_loop<4, 1>(ec, seq, cf); break;
+        case 4 * 8 + 2: epilogue_loop<4, 2>(ec, seq, cf); break;
+        case 4 * 8 + 3: epilogue_loop<4, 3>(ec, seq, cf); break;
+        case 4 * 8 + 4: epilogue_loop<4, 4>(ec, seq, cf); break;
+        default: epilogue_loop<0, 0>(ec, seq, cf); break;   // probe / skip_math
       }
     }
   }
@@ -927,7 +875,7 @@ static bool encode_w(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d
 
 static uint32_t align1k(uint32_t x) { return (x + 1023) & ~1023u; }
 
-cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, const char** why, bool strict) {
+cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, const char** why) {
   *out = nullptr;
   int dev = 0, major = 0, minor = 0;
   cudaGetDevice(&dev);
@@ -946,54 +894,56 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   g.rp = rp;
   g.max_terms = 2 * sp.top_k;
   g.swz_mode = rp == 16 ? 6u : rp == 32 ? 4u : 2u;        // SWIZZLE_32B / 64B / 128B (UMMA encoding)
-  // Shared-memory / TMEM plan.  Candidates in order of preference:
-  //   split mode, 128-column tiles (one accumulator of 128 columns per tile, 4 TMEM
-  //     buffers; B strip holds 3 parts per term, single-buffered);
-  //   per-term mode, 128-column tiles (max_terms x 64 TMEM columns per sub-tile);
-  //   per-term mode, 64-column tiles.
-  // Each needs >= 2 A stages and enough W stages (4 for 128-column tiles).
+  // Shared-memory / TMEM plan.  TMEM: acc_bufs buffers of tg x 64 columns (a
+  // tile's 2k terms stream through them tg at a time, so any k fits).  Shared
+  // memory: W stages (32 KB per 128x128 tile), B strip buffers (all terms'
+  // 128 x rp slices, reused along the strip), A stages (one sub-tile x one term
+  // group each).  Search order: 128-column tiles with >= 4 W stages, then with 3,
+  // then 64-column tiles; within that the default group size first (the whole
+  // list when 2k <= 4, else two balanced groups), then smaller groups; B double-
+  // buffered before single; the first plan with >= 4 A stages wins, else the
+  // first with >= 2.
   const uint32_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
   g.b_bytes_per_term = kTcTM * rp * 2;
+  g.a_sub_bytes = kTcTN * rp * 2;
   bool ok = false;
-  int nsub_env = 0, split_env = -1;
+  int nsub_env = 0, tg_env = 0, a_max = kTcMaxAStages;
   if (const char* v = getenv("LSW_TC_NSUB")) nsub_env = atoi(v);
-  if (const char* v = getenv("LSW_TC_SPLIT")) split_env = atoi(v);
-  int a_max = 3;                                         // A-slice ring depth (tuning: LSW_TC_ASTAGES)
-  if (const char* v = getenv("LSW_TC_ASTAGES")) { int x = atoi(v); if (x >= 1 && x <= 4) a_max = x; }
-  // measured (scripts/tune_switch.py, 7B shape): per-term 4583 GB/s vs split 3756 GB/s --
-  // split mode triples the MMAs and the SS operand reads; it is opt-in (LSW_TC_SPLIT=1)
-  if (split_env < 0) split_env = 0;
-  for (int cand = 0; cand < 3 && !ok; ++cand) {
-    const int split = cand == 0 ? 1 : 0;
-    const int nsub = cand < 2 ? 2 : 1;
-    if (nsub_env && nsub != nsub_env) continue;
-    if (split_env >= 0 && split != split_env) continue;
-    // TMEM
-    const uint32_t buf_cols = split ? kTcTN * nsub : (uint32_t)g.max_terms * kTcTN;
-    if (buf_cols > 512) continue;
-    const int acc_bufs = split ? (int)(512 / buf_cols < 4 ? 512 / buf_cols : 4) : (buf_cols * 2 <= 512 ? 2 : 1);
-    // shared memory
-    const uint32_t a_term = kTcTN * nsub * rp * 2;
-    const uint32_t a_stage = align1k(g.max_terms * a_term);
-    const uint32_t b_buf = align1k(g.max_terms * (split ? 3 : 1) * g.b_bytes_per_term);
-    const uint32_t w_stage = nsub * kSubBytes;
-    for (int bbufs = split ? 1 : 2; bbufs >= 1 && !ok; --bbufs)
-      for (int astages = a_max; astages >= 2 && !ok; --astages) {
-        int ws = (int)((budget - (int64_t)bbufs * b_buf - (int64_t)astages * a_stage) / w_stage);
-        if ((int64_t)budget < (int64_t)bbufs * b_buf + (int64_t)astages * a_stage) ws = 0;
-        if (ws > kTcMaxStages) ws = kTcMaxStages;
-        const int min_ws = nsub == 2 ? 4 : 2;
-        if (ws >= min_ws) {
+  if (const char* v = getenv("LSW_TC_TG")) tg_env = atoi(v);
+  if (const char* v = getenv("LSW_TC_ASTAGES")) { int x = atoi(v); if (x >= 2 && x <= kTcMaxAStages) a_max = x; }
+  const int mt = g.max_terms;
+  const int tg_default = mt <= 4 ? mt : (mt + 1) / 2;
+  for (int pass = 0; pass < 2 && !ok; ++pass) {
+    const int a_need = pass == 0 ? 4 : 2;
+    for (int shape = 0; shape < 3 && !ok; ++shape) {
+      const int nsub = shape < 2 ? 2 : 1;
+      const int min_ws = shape == 0 ? 4 : shape == 1 ? 3 : 2;
+      if (nsub_env && nsub != nsub_env) continue;
+      const uint32_t w_stage = nsub * kSubBytes;
+      for (int tgi = 0; tgi <= 4 && !ok; ++tgi) {
+        const int tg = tgi == 0 ? tg_default : 5 - tgi;           // default, then 4, 3, 2, 1
+        if (tg > mt || (tgi > 0 && tg == tg_default) || (tg_env && tg != tg_env)) continue;
+        const uint32_t buf_cols = (uint32_t)tg * kTcTN;
+        int acc_bufs = (int)(512 / buf_cols);
+        if (acc_bufs > kTcMaxAccBufs) acc_bufs = kTcMaxAccBufs;
+        if (acc_bufs < 2) continue;
+        const uint32_t a_stage = align1k((uint32_t)tg * g.a_sub_bytes);
+        const uint32_t b_buf = align1k((uint32_t)mt * g.b_bytes_per_term);
+        for (int bbufs = 2; bbufs >= 1 && !ok; --bbufs) {
+          const int64_t rest = (int64_t)budget - (int64_t)bbufs * b_buf - (int64_t)min_ws * w_stage;
+          if (rest < (int64_t)a_need * a_stage) continue;
+          int astages = (int)(rest / a_stage);
+          if (astages > a_max) astages = a_max;
+          int ws = (int)(((int64_t)budget - (int64_t)bbufs * b_buf - (int64_t)astages * a_stage) / w_stage);
+          if (ws > kTcMaxStages) ws = kTcMaxStages;
           ok = true;
-          g.split = split;
           g.nsub = nsub;
+          g.tg = tg;
           g.w_stages = ws;
           g.a_stages = astages;
           g.b_bufs = bbufs;
           g.acc_bufs = acc_bufs;
-          g.a_bytes_per_term = a_term;
           g.a_stage_bytes = a_stage;
-          g.a_all = 0;
           g.b_buf_bytes = b_buf;
           g.w_stage_bytes = w_stage;
           uint32_t cols = 32;
@@ -1001,14 +951,9 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
           g.tmem_cols = cols;
         }
       }
+    }
   }
-  if (!ok) { delete plan; *why = "shared memory / TMEM: rank * top_k too large"; return cudaErrorNotSupported; }
-  if (strict && (g.split || g.nsub != 2 || g.acc_bufs < 2)) {
-    // degraded plan: the term-group kernel (switch_tc_tg.cu) serves this shape
-    delete plan;
-    *why = "v1: no double-buffered 128-column plan";
-    return cudaErrorNotSupported;
-  }
+  if (!ok) { delete plan; *why = "shared memory: rank * top_k too large"; return cudaErrorNotSupported; }
   // tuning knobs (defaults are the measured best)
   if (const char* v = getenv("LSW_TC_STAGES")) { int x = atoi(v); if (x >= 2 && x < g.w_stages) g.w_stages = x; }
   if (const char* v = getenv("LSW_TC_ORDER")) plan->order = strcmp(v, "sweep") == 0 ? ORDER_SWEEP : ORDER_STRIP;
@@ -1119,5 +1064,5 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   return cudaGetLastError();
 }
 
-}  // namespace v1
+}  // namespace tg
 }  // namespace lsw

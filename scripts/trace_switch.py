@@ -14,7 +14,10 @@ import synth  # noqa: E402
 from paper_2405_17741_b200 import harness as H  # noqa: E402
 
 EV = ["W_issued", "A_issued", "A_full", "MMA_start", "MMA_done", "EPI_wfull", "EPI_acc0", "stage_free",
-      "EPI_done", "MMA_acc0", "MMA_issued0", "EPI_sub0_done"]
+      "EPI_done", "MMA_acc0", "MMA_issued0", "EPI_sub0_done", "A_begin", "A_waited", "EPI_acc1", "MMA_issued1"]
+if os.environ.get("LSW_TRACE_LIB"):          # A/B against another build of the library
+    from paper_2405_17741_b200 import binding as _B
+    _B._LIB = _B.load_library(os.environ["LSW_TRACE_LIB"], strict=False)
 cfg = synth.get_config(sys.argv[1] if len(sys.argv) > 1 else "llama2-7b")
 W, A, B, router = H.build_weights(cfg, "cuda")
 sw = H.make_switch(cfg, W, A, B, router, impl="tc")
@@ -46,10 +49,15 @@ for slot, cta in enumerate((0, 49, 98, 147)):
         if w1 > w0:
             print(f"   tiles {w0:5d}-{w1:5d}: us/tile {(done[w1] - done[w0]) / (w1 - w0) / 1e3:.3f}")
     d = lambda a, b: np.median(T[:, EV.index(b)] - T[:, EV.index(a)]) / 1e3
-    for a, b in [("W_issued", "EPI_wfull"), ("A_issued", "A_full"), ("MMA_acc0", "MMA_issued0"),
+    for a, b in [("W_issued", "EPI_wfull"), ("A_issued", "A_full"), ("MMA_start", "A_full"), ("A_begin", "A_waited"), ("A_waited", "A_issued"), ("MMA_issued0", "MMA_issued1"), ("MMA_issued1", "MMA_done"),
+                 ("MMA_issued1", "EPI_acc1"), ("EPI_sub0_done", "EPI_acc1"), ("EPI_acc1", "EPI_done"), ("A_full", "MMA_acc0"),
+                 ("MMA_acc0", "MMA_issued0"), ("MMA_issued0", "MMA_done"),
                  ("MMA_issued0", "EPI_acc0"), ("EPI_acc0", "EPI_sub0_done"), ("EPI_sub0_done", "EPI_done"),
                  ("EPI_done", "stage_free")]:
         print(f"   {a:>13s} -> {b:<13s} median {d(a, b):8.3f} us")
+    nxt = np.median(T[1:, EV.index("MMA_start")] - T[:-1, EV.index("MMA_done")]) / 1e3
+    print(f"   MMA_done(t) -> MMA_start(t+1) median {nxt:8.3f} us;  MMA_start period "
+          f"{np.median(np.diff(T[:, EV.index('MMA_start')])) / 1e3:.3f} us")
     w_wait = T[1:, EV.index("EPI_wfull")] - T[:-1, EV.index("EPI_done")]
     a_wait = T[:, EV.index("EPI_acc0")] - T[:, EV.index("EPI_wfull")]
     print(f"   epilogue idle per tile: waiting W mean {np.mean(w_wait) / 1e3:.3f} us, "

@@ -59,6 +59,19 @@ for rep in range(5):
     tok.append(e0.elapsed_time(e1))
 tb = H.token_bytes(cfg)
 med = statistics.median(tok)
+res["groups_gemv_ms"] = round(med, 4)
+res["groups_gemv_GBps"] = round(tb["gemv"] / (med * 1e-3) / 1e9, 1)
+# whole-token launch (lsw_decode_all_layers: one persistent GEMV when tp_size == 1)
+tok = []
+for rep in range(10):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sw.decode_all_layers(xs_p, ys)
+    e1.record()
+    torch.cuda.synchronize()
+    tok.append(e0.elapsed_time(e1))
+med = statistics.median(tok)
 res["token_gemv_ms"] = round(med, 4)
 res["token_gemv_GBps"] = round(tb["gemv"] / (med * 1e-3) / 1e9, 1)
+res["env"] = {k: v for k, v in os.environ.items() if k.startswith("LSW_")}
 print(json.dumps(res), flush=True)

@@ -21,8 +21,12 @@ ap.add_argument("--layers", type=int, default=0)
 ap.add_argument("--iters", type=int, default=12)
 ap.add_argument("--impl", default="tc")
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--lib", default="", help="load this liblsw.so instead of the package's (A/B of two builds)")
 ap.add_argument("settings", nargs="*", default=["order=strip", "order=sweep,chunk=1", "order=sweep,chunk=4"])
 a = ap.parse_args()
+if a.lib:
+    from paper_2405_17741_b200 import binding as _B
+    _B._LIB = _B.load_library(a.lib, strict=False)
 cfg = synth.get_config(a.config)
 if a.layers:
     cfg = cfg.with_(n_layers=a.layers)
@@ -33,7 +37,8 @@ idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
 gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6452.8
 for setting in [x for _ in range(a.repeat) for x in a.settings]:
-    for k in ("LSW_TC_ORDER", "LSW_TC_CHUNK", "LSW_TC_STAGES", "LSW_TC_PROBE", "LSW_TC_NSUB", "LSW_TC_AALL", "LSW_TC_STORE", "LSW_TC_ASTAGES", "LSW_TC_SPLIT"):
+    for k in ("LSW_TC_ORDER", "LSW_TC_CHUNK", "LSW_TC_STAGES", "LSW_TC_PROBE", "LSW_TC_NSUB", "LSW_TC_AALL", "LSW_TC_STORE", "LSW_TC_ASTAGES", "LSW_TC_SPLIT", "LSW_TC_TG", "LSW_TC_BACKOFF", "LSW_TC_ACOPY", "LSW_TC_ADEPTH", "LSW_TC_ALOADER",
+              "LSW_TC_GRID"):
         os.environ.pop(k, None)
     for kv in setting.split(","):
         if not kv:

@@ -113,6 +113,7 @@ CONFIGS: Dict[str, Config] = {
     "mini-r32": Config("mini-r32", 2, 256, 704, 2, 1, 128, 8, 32, 2, 16.0, "bf16"),
     "mini-r4k4": Config("mini-r4k4", 2, 256, 704, 2, 1, 128, 16, 4, 4, 16.0, "bf16"),
     "mini-r64k3": Config("mini-r64k3", 1, 256, 704, 2, 1, 128, 4, 64, 3, 16.0, "bf16"),
+    "mini-r48": Config("mini-r48", 1, 256, 704, 2, 1, 128, 4, 48, 2, 16.0, "bf16"),
     "mini-k1": Config("mini-k1", 2, 256, 704, 2, 1, 128, 4, 8, 1, 16.0, "bf16"),
 }
 

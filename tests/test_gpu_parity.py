@@ -82,7 +82,7 @@ def _run_token_checks(S, T, check_one_step=True):
 
 
 TRAJ_CASES = [("toy", "simt"), ("mini", "simt"), ("mini", "tc"), ("mini-r32", "tc"), ("mini-r4k4", "tc"),
-              ("mini-k1", "tc"), ("mini-r64k3", "tc")]
+              ("mini-k1", "tc"), ("mini-r64k3", "tc"), ("mini-r48", "tc")]
 
 
 @pytest.mark.parametrize("name,impl", TRAJ_CASES)
@@ -107,23 +107,37 @@ def test_switch_trajectory_full_elements(name, impl):
         S.sw.unmerge_all_layers()          # LSW_E_STATE
 
 
+TC_VARIANTS = [("v1", {}), ("v1", {"LSW_TC_SPLIT": "1"}), ("tg", {}), ("tg", {"LSW_TC_TG": "1"}),
+               ("tg", {"LSW_TC_TG": "2"})]
+
+
 @pytest.mark.parametrize("grid", [1, 3])
-@pytest.mark.parametrize("split", ["1", "0"])
-@pytest.mark.parametrize("name", ["mini", "mini-r32"])
-def test_tc_switch_many_tiles_per_cta(monkeypatch, name, split, grid):
+@pytest.mark.parametrize("variant", range(len(TC_VARIANTS)))
+@pytest.mark.parametrize("name", ["mini", "mini-r32", "mini-r4k4", "mini-r64k3"])
+def test_tc_switch_many_tiles_per_cta(monkeypatch, name, variant, grid):
     """The mini shapes give every CTA a single tile at the default grid; force a
-    tiny grid so every ring (W, A, B, TMEM accumulators) wraps many times, in
-    both accumulator modes (split: pre-scaled B parts; per-term accumulators)."""
+    tiny grid so every ring (W, A, B, TMEM accumulators) wraps many times, for
+    both tensor-core kernels: v1 (per-term accumulators; split mode: pre-scaled
+    B parts) and the term-group kernel with its default, 1- and 2-term groups
+    (a tile's terms then stream through several TMEM buffers into one fp32
+    running sum)."""
+    kernel, env = TC_VARIANTS[variant]
     monkeypatch.setenv("LSW_TC_GRID", str(grid))
-    monkeypatch.setenv("LSW_TC_SPLIT", split)
+    monkeypatch.setenv("LSW_TC_KERNEL", kernel)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = synth.get_config(name)
+    if int(env.get("LSW_TC_TG", "0")) > 2 * cfg.top_k:
+        pytest.skip("group larger than the term list")
     try:
         S = Setup(name, "tc", n_tokens=6)
-    except L.LswError as e:           # split mode not available for this shape
-        assert split == "1" and "UNSUPPORTED" in str(e)
+    except L.LswError as e:           # v1 / split mode have no plan for this shape
+        assert kernel == "v1" and "UNSUPPORTED" in str(e)
         pytest.skip(str(e))
-    assert S.sw.info()["grid"] == grid
+    info = S.sw.info()
+    assert info["grid"] == grid and info["switch_kernel"] == (1 if kernel == "v1" else 2)
     worst = _run_token_checks(S, 5)
-    print(f"{name} split={split} grid={grid}: worst {worst}")
+    print(f"{name} {kernel} {env} grid={grid}: worst {worst}")
 
 
 @pytest.mark.parametrize("name,impl", [("toy", "simt"), ("mini", "tc")])
@@ -225,7 +239,9 @@ def test_device_error_latch_nonfinite_router_input(impl):
     assert S.sw.device_status() == 2
 
 
-def test_decode_token_host_matches_device_path():
+@pytest.mark.parametrize("token_kernel", ["0", "1"])
+def test_decode_token_host_matches_device_path(monkeypatch, token_kernel):
+    monkeypatch.setenv("LSW_GEMV_TOKEN", token_kernel)
     cfg = synth.get_config("mini")
     outs = []
     for mode in ("device", "host"):
@@ -252,7 +268,56 @@ def test_decode_token_host_matches_device_path():
                 sw.decode_token_host(x1h, xsh, ysh, idxh, gh)
                 res = (ysh.clone(), idxh.clone(), gh.clone())
         outs.append(res)
-        # launch count: per token 1 router + 1 switch + 4 GEMV groups per layer
-        assert sw.info()["kernel_launches"] == 3 * (2 + 4 * cfg.n_layers)
+        # launch count: per token 1 router + 1 switch + the GEMVs (one whole-token
+        # launch, or 4 group launches per layer)
+        gemvs = 1 if token_kernel == "1" else 4 * cfg.n_layers
+        assert sw.info()["kernel_launches"] == 3 * (2 + gemvs)
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("grid,slot_kb", [(None, None), (1, None), (3, "4"), (7, "6")])
+@pytest.mark.parametrize("name,impl", [("toy", "simt"), ("mini", "tc"), ("mini-r32", "tc")])
+def test_decode_all_layers_token_kernel(monkeypatch, name, impl, grid, slot_kb):
+    """The whole-token GEMV launch (K4b) equals the per-group launches bitwise
+    (same per-row reduction order) and the oracle within the GEMV tolerance;
+    small grids / slots make every CTA wrap its ring across many groups."""
+    monkeypatch.setenv("LSW_GEMV_TOKEN", "1")
+    if grid is not None:
+        monkeypatch.setenv("LSW_GEMV_GRID", str(grid))
+    if slot_kb is not None:
+        monkeypatch.setenv("LSW_GEMV_SLOT_KB", slot_kb)
+    S = Setup(name, impl, n_tokens=2)
+    cfg = S.cfg
+    info = S.sw.info()
+    xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
+    S.sw.router_topk(S.X1[0], S.idx, S.gate)
+    S.sw.merge_all_layers(S.idx, S.gate)
+    idx_o, g_o, _ = S.orc.route(_f64(S.X1[0]))
+    S.orc.merge_all_layers((idx_o.tolist(), g_o.tolist()))
+    ys = [torch.full((info["ys_elems"],), float("nan"), device="cuda") for _ in range(3)]
+    n0 = S.sw.info()["kernel_launches"]
+    S.sw.decode_all_layers(xs, ys[0])
+    S.sw.decode_all_layers(xs, ys[1])            # the group counter carries over launches
+    assert S.sw.info()["kernel_launches"] == n0 + 2
+    xo = yo = 0
+    xs_l = []
+    for l in range(cfg.n_layers):
+        for gi, grp in enumerate(synth.GROUPS):
+            d_in = cfg.kind_shape(grp[0])[1]
+            n_out = sum(cfg.kind_shape(k)[0] for k in grp)
+            S.sw.decode_group(l, gi, xs[xo:xo + d_in], ys[2][yo:yo + n_out])
+            xs_l.append((l, grp, xo, d_in, yo))
+            xo += d_in
+            yo += n_out
+    torch.cuda.synchronize()
+    assert S.sw.device_status() == 0
+    assert torch.equal(ys[0], ys[1]) and torch.equal(ys[0], ys[2])
+    xs_h, ys_h = xs.cpu(), ys[0].cpu().numpy()
+    for l, grp, xo, d_in, yo in xs_l:
+        x = _f64(xs_h[xo:xo + d_in])
+        for kd in grp:
+            n = cfg.kind_shape(kd)[0]
+            yo_ = S.orc.decode_linear(kd, l, x)
+            assert PT.allclose_frac_fail(ys_h[yo:yo + n], yo_) == 0.0
+            yo += n
