@@ -111,7 +111,7 @@ gemv_kernel(const GemvParams p) {
 // completion on an mbarrier), so ~200 KB per SM are in flight without any
 // register cost; 8 consumer warps reduce rows from shared memory (512 B per
 // warp instruction, conflict-free) against x (also in shared memory).
-constexpr int kBulkConsumers = 8;
+constexpr int kBulkConsumers = 16;   // measured (7B token of GEMVs): 8 warps 2.39 ms, 16 2.25, 24 2.24
 constexpr int kBulkThreads = 32 * (1 + kBulkConsumers);
 constexpr int kBulkMaxSlots = 32;
 
@@ -137,6 +137,95 @@ __device__ __forceinline__ void g_mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
+// x as the consumer warps read it: bf16 x is widened once per GEMV into two
+// fp32 planes (elements 0-3 and 4-7 of every 16-B chunk of the row, each plane
+// read conflict-free with one LDS.128 per lane), so the inner loop is one
+// LDS.128 of W, two of x, 8 bf16->fp32 unpacks and 4 packed FFMA2 per 8
+// elements (measured: the unpack + scalar-FMA loop was the bottleneck of the
+// bulk GEMV, 5.5 TB/s against 7.2 TB/s for the same stream without the math).
+__host__ __device__ inline uint32_t x_stage_bytes(uint32_t row_bytes, bool bf16) {
+  return ((bf16 ? 2 * row_bytes : row_bytes) + 127) & ~127u;
+}
+
+template <bool kBf16>
+__device__ __forceinline__ void stage_x(const void* xg, uint8_t* xs, uint32_t row_bytes, int tid, int nthreads) {
+  const uint4* src = reinterpret_cast<const uint4*>(xg);
+  const int n16 = (int)(row_bytes / 16);
+  if (kBf16) {
+    float4* lo = reinterpret_cast<float4*>(xs);
+    float4* hi = lo + n16;
+    for (int i = tid; i < n16; i += nthreads) {
+      const uint4 u = src[i];
+      lo[i] = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                          __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
+      hi[i] = make_float4(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xffff0000u),
+                          __uint_as_float(u.w << 16), __uint_as_float(u.w & 0xffff0000u));
+    }
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(xs);
+    for (int i = tid; i < n16; i += nthreads) dst[i] = src[i];
+  }
+}
+
+__device__ __forceinline__ uint64_t g_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t g_ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ float g_sum2(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo + hi;
+}
+// acc (fp32 pairs) += bf16 chunk w * x chunk (lo, hi planes)
+__device__ __forceinline__ uint64_t dot8_f2(const uint4 w, const float4 lo, const float4 hi, uint64_t acc) {
+  acc = g_ffma2(g_pack(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u)), g_pack(lo.x, lo.y), acc);
+  acc = g_ffma2(g_pack(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u)), g_pack(lo.z, lo.w), acc);
+  acc = g_ffma2(g_pack(__uint_as_float(w.z << 16), __uint_as_float(w.z & 0xffff0000u)), g_pack(hi.x, hi.y), acc);
+  acc = g_ffma2(g_pack(__uint_as_float(w.w << 16), __uint_as_float(w.w & 0xffff0000u)), g_pack(hi.z, hi.w), acc);
+  return acc;
+}
+
+// One row of W (in shared memory) against the staged x, reduced over the warp.
+template <bool kBf16>
+__device__ __forceinline__ float row_dot(const uint8_t* wrow, const uint8_t* xs, int64_t n16, int lane) {
+  const uint4* w4 = reinterpret_cast<const uint4*>(wrow);
+  float acc;
+  if (kBf16) {
+    const float4* lo = reinterpret_cast<const float4*>(xs);
+    const float4* hi = lo + n16;
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;     // (+0.f, +0.f) pairs
+    int64_t c = lane;
+    for (; c + 96 < n16; c += 128) {              // 4 independent chunks per lane in flight
+      const uint4 w0 = w4[c], w1 = w4[c + 32], w2 = w4[c + 64], w3 = w4[c + 96];
+      a0 = dot8_f2(w0, lo[c], hi[c], a0);
+      a1 = dot8_f2(w1, lo[c + 32], hi[c + 32], a1);
+      a2 = dot8_f2(w2, lo[c + 64], hi[c + 64], a2);
+      a3 = dot8_f2(w3, lo[c + 96], hi[c + 96], a3);
+    }
+    for (; c < n16; c += 32) a0 = dot8_f2(w4[c], lo[c], hi[c], a0);
+    acc = (g_sum2(a0) + g_sum2(a1)) + (g_sum2(a2) + g_sum2(a3));
+  } else {
+    const uint4* x4 = reinterpret_cast<const uint4*>(xs);
+    float acc0 = 0.f, acc1 = 0.f;
+    int64_t c = lane;
+    for (; c + 32 < n16; c += 64) {
+      acc0 += dot_chunk<false>(w4[c], x4, c);
+      acc1 += dot_chunk<false>(w4[c + 32], x4, c + 32);
+    }
+    if (c < n16) acc0 += dot_chunk<false>(w4[c], x4, c);
+    acc = acc0 + acc1;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  return acc;
+}
+
 template <bool kBf16>
 __global__ void __launch_bounds__(kBulkThreads, 1)
 gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) {
@@ -144,7 +233,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) 
   __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row_bytes = (uint32_t)(p.d_in * (kBf16 ? 2 : 4));
-  const uint32_t x_bytes = (row_bytes + 127) & ~127u;
+  const uint32_t x_bytes = x_stage_bytes(row_bytes, kBf16);
   const size_t slot_bytes = (size_t)R * row_bytes;
   uint8_t* xs = smem_raw;
   uint8_t* ring = smem_raw + x_bytes;
@@ -210,16 +299,11 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) 
   if (early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after our wait: see above
   // x -> shared (consumer warps), then a named barrier among the consumers only
-  {
-    const uint4* xg = reinterpret_cast<const uint4*>(p.x);
-    uint4* xd = reinterpret_cast<uint4*>(xs);
-    for (uint32_t i = threadIdx.x - 32; i < row_bytes / 16; i += blockDim.x - 32) xd[i] = xg[i];
-  }
+  stage_x<kBf16>(p.x, xs, row_bytes, threadIdx.x - 32, blockDim.x - 32);
   asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
   // consumers: unit u = (local chunk i, row k in chunk); warp cw takes u = cw mod 8
   const int cw = warp - 1;
   const int64_t nchunk16 = row_bytes / 16;
-  const uint4* x4 = reinterpret_cast<const uint4*>(xs);
   for (int64_t u = cw; u < my_chunks * R; u += kBulkConsumers) {
     const int64_t i = u / R;
     const int k = (int)(u - i * R);
@@ -228,17 +312,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) 
     while (issued <= i) __nanosleep(64);
     g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
     if (row < p.rows_total) {
-      const uint4* w4 = reinterpret_cast<const uint4*>(ring + s * slot_bytes + (size_t)k * row_bytes);
-      float acc0 = 0.f, acc1 = 0.f;
-      int64_t c = lane;
-      for (; c + 32 < nchunk16; c += 64) {
-        acc0 += dot_chunk<kBf16>(w4[c], x4, c);
-        acc1 += dot_chunk<kBf16>(w4[c + 32], x4, c + 32);
-      }
-      if (c < nchunk16) acc0 += dot_chunk<kBf16>(w4[c], x4, c);
-      float acc = acc0 + acc1;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      const float acc = row_dot<kBf16>(ring + s * slot_bytes + (size_t)k * row_bytes, xs, nchunk16, lane);
       if (lane == 0) p.y[row] = acc;
     }
     __syncwarp();
@@ -280,7 +354,7 @@ gemv_token_kernel(const TokGroup* __restrict__ grp, int32_t n_groups, int64_t to
                   const uint8_t* __restrict__ xs, float* __restrict__ ys, int32_t slots, uint32_t slot_bytes,
                   uint32_t x_cap, unsigned long long* done, unsigned long long base, int32_t flags) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots], xbar;
+  __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
   __shared__ volatile int64_t issued;               // ticket, as in gemv_bulk_kernel
   constexpr int64_t es = kBf16 ? 2 : 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -292,36 +366,53 @@ gemv_token_kernel(const TokGroup* __restrict__ grp, int32_t n_groups, int64_t to
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&full[s])), "r"(1));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&empty[s])), "r"(kBulkConsumers));
     }
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&xbar)), "r"(1));
     issued = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");   // W is written by the switch before us
   if (warp == 0) {
+    // the group table (a few KB) into L1 once: per-group descriptor reads
+    // below then hit L1 instead of paying an L2 round trip per group
+    for (int off = lane * 128; off < n_groups * (int)sizeof(TokGroup); off += 32 * 128)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const uint8_t*>(grp) + off));
     if (lane == 0) {
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      int g = 0;
-      int64_t next = n_groups > 1 ? grp[1].chunk_begin : total_chunks;
+      // the current group's descriptor, held in registers
+      int g = -1;
+      int64_t next = 0, cb = 0, rows = 0, R = 1, rb_ = 0;
+      int ns = 1;
+      const uint8_t* W0 = nullptr;
+      const uint8_t* W1 = nullptr;
+      const uint8_t* W2 = nullptr;
+      int64_t sb1 = 0, sb2 = 0;
       int64_t i = 0;
       for (int64_t c = b; c < total_chunks; c += G, ++i) {
-        while (c >= next) { ++g; next = g + 1 < n_groups ? grp[g + 1].chunk_begin : total_chunks; }
-        const TokGroup* t = grp + g;
+        while (c >= next) {
+          ++g;
+          const TokGroup* t = grp + g;
+          cb = t->chunk_begin; rows = t->rows; R = t->R; rb_ = t->row_bytes; ns = t->n_sites;
+          W0 = reinterpret_cast<const uint8_t*>(t->W[0]);
+          W1 = reinterpret_cast<const uint8_t*>(t->W[1]);
+          W2 = reinterpret_cast<const uint8_t*>(t->W[2]);
+          sb1 = ns > 1 ? t->row_begin[1] : rows;
+          sb2 = ns > 2 ? t->row_begin[2] : rows;
+          next = g + 1 < n_groups ? grp[g + 1].chunk_begin : total_chunks;
+        }
         const int s = (int)(i % slots);
         g_mbar_wait(s_u32(&empty[s]), (uint32_t)((i / slots) & 1) ^ 1);
-        const int64_t rows = t->rows, R = t->R, rb_ = t->row_bytes;
-        const int64_t r0 = (c - t->chunk_begin) * R;
+        const int64_t r0 = (c - cb) * R;
         const int64_t r1 = r0 + R < rows ? r0 + R : rows;
         const uint32_t bar = s_u32(&full[s]);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                      "r"((uint32_t)((r1 - r0) * rb_)) : "memory");
-        const int ns = t->n_sites;
         for (int q = 0; q < ns; ++q) {       // one bulk copy per site the chunk overlaps
-          const int64_t sb = t->row_begin[q], se = q + 1 < ns ? t->row_begin[q + 1] : rows;
+          const int64_t sb = q == 0 ? 0 : q == 1 ? sb1 : sb2;
+          const int64_t se = q == 0 ? sb1 : q == 1 ? sb2 : rows;
           const int64_t a = r0 > sb ? r0 : sb, e = r1 < se ? r1 : se;
           if (a >= e) continue;
-          const uint8_t* src = reinterpret_cast<const uint8_t*>(t->W[q]) + (a - sb) * rb_;
+          const uint8_t* src = (q == 0 ? W0 : q == 1 ? W1 : W2) + (a - sb) * rb_;
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
               ::"r"(s_u32(ring + (size_t)s * slot_bytes + (a - r0) * rb_)), "l"(src),
@@ -335,7 +426,6 @@ gemv_token_kernel(const TokGroup* __restrict__ grp, int32_t n_groups, int64_t to
   }
   const int cw = warp - 1;
   int64_t i0 = 0;                                   // this CTA's chunks before group g
-  uint32_t xphase = 0;
   for (int g = 0; g < n_groups; ++g) {
     const TokGroup* t = grp + g;
     const int64_t cb = t->chunk_begin, ce = g + 1 < n_groups ? grp[g + 1].chunk_begin : total_chunks;
@@ -345,17 +435,12 @@ gemv_token_kernel(const TokGroup* __restrict__ grp, int32_t n_groups, int64_t to
     const int64_t nj = first < ce ? (ce - first + G - 1) / G : 0;
     if (nj > 0) {
       // decoder order: x of group g only after every CTA has finished group g-1
-      if (threadIdx.x == 32) {
-        if (g > 0 && !(flags & 1)) wait_counter(done, base + (unsigned long long)g * (unsigned long long)G);
-        const uint32_t xb = s_u32(&xbar);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(xb), "r"(row_bytes) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                     ::"r"(s_u32(xsm)), "l"(xs + t->x_off * es), "r"(row_bytes), "r"(xb) : "memory");
-      }
-      g_mbar_wait(s_u32(&xbar), xphase & 1);
-      ++xphase;
+      if (threadIdx.x == 32 && g > 0 && !(flags & 1))
+        wait_counter(done, base + (unsigned long long)g * (unsigned long long)G);
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
+      stage_x<kBf16>(xs + t->x_off * es, xsm, row_bytes, threadIdx.x - 32, 32 * kBulkConsumers);
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
       const int64_t nchunk16 = row_bytes / 16;
-      const uint4* x4 = reinterpret_cast<const uint4*>(xsm);
       float* yg = ys + t->y_off;
       for (int64_t j = 0; j < nj; ++j) {
         const int64_t i = i0 + j;
@@ -366,18 +451,8 @@ gemv_token_kernel(const TokGroup* __restrict__ grp, int32_t n_groups, int64_t to
         g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
         // rows of the flat sequence (j*R + k) are dealt to warps round-robin
         for (int64_t k = ((cw - (j * R) % kBulkConsumers) % kBulkConsumers + kBulkConsumers) % kBulkConsumers;
-             k < nr; k += kBulkConsumers) {
-          const uint4* w4 = reinterpret_cast<const uint4*>(ring + (size_t)s * slot_bytes + (size_t)k * row_bytes);
-          float acc0 = 0.f, acc1 = 0.f;
-          int64_t c = lane;
-          for (; c + 32 < nchunk16; c += 64) {
-            acc0 += dot_chunk<kBf16>(w4[c], x4, c);
-            acc1 += dot_chunk<kBf16>(w4[c + 32], x4, c + 32);
-          }
-          if (c < nchunk16) acc0 += dot_chunk<kBf16>(w4[c], x4, c);
-          float acc = acc0 + acc1;
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+             k < nr && !(flags & 2); k += kBulkConsumers) {    // flags bit 1: tuning probe, stream only
+          const float acc = row_dot<kBf16>(ring + (size_t)s * slot_bytes + (size_t)k * row_bytes, xsm, nchunk16, lane);
           if (lane == 0) yg[r0 + k] = acc;
         }
         __syncwarp();
@@ -394,7 +469,7 @@ gemv_token_kernel(const TokGroup* __restrict__ grp, int32_t n_groups, int64_t to
   }
 }
 
-cudaError_t tok_plan_create(TokPlan* plan, TokGroup* groups, int32_t n_groups, int num_sms) {
+cudaError_t tok_plan_create(TokPlan* plan, TokGroup* groups, int32_t n_groups, int num_sms, bool bf16) {
   *plan = TokPlan{};
   // rows per chunk: ~32 KB per bulk copy (LSW_GEMV_SLOT_KB), at most 8 rows
   uint32_t target = 32 * 1024;
@@ -411,7 +486,7 @@ cudaError_t tok_plan_create(TokPlan* plan, TokGroup* groups, int32_t n_groups, i
     chunks += (t.rows + R - 1) / R;
     const uint32_t sb = (uint32_t)R * t.row_bytes;
     if (sb > slot) slot = sb;
-    const uint32_t xb = (t.row_bytes + 127) & ~127u;
+    const uint32_t xb = x_stage_bytes(t.row_bytes, bf16);
     if (xb > xcap) xcap = xb;
   }
   slot = (slot + 127) & ~127u;
@@ -496,7 +571,7 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
     // bulk-copy throughput grows with bytes per operation (scripts/membench.cu:
     // 4 KB ops 2.6 TB/s ... 32 KB ops 7.3 TB/s): move R >= 1 rows per op, ~32 KB
     const uint32_t row_bytes = (uint32_t)(p.d_in * (bf16 ? 2 : 4));
-    const uint32_t x_bytes = (row_bytes + 127) & ~127u;
+    const uint32_t x_bytes = x_stage_bytes(row_bytes, bf16);
     int R = (int)(32768 / row_bytes);
     if (R < 1) R = 1;
     if (R > 8) R = 8;

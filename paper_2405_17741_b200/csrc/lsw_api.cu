@@ -199,7 +199,7 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
         t.x_off = l * ctx->x_per_layer + ctx->x_off[g];
         t.y_off = l * ctx->y_per_layer + ctx->y_off[g];
       }
-    e = tok_plan_create(&ctx->tok, tg.data(), (int32_t)tg.size(), ctx->num_sms);
+    e = tok_plan_create(&ctx->tok, tg.data(), (int32_t)tg.size(), ctx->num_sms, c.dtype == LSW_BF16);
     if (e == cudaErrorMemoryAllocation) { lsw_destroy(ctx); return fail(LSW_E_OOM, "lsw_create: token GEMV table"); }
     if (e != cudaSuccess) { (void)cudaGetLastError(); ctx->tok = TokPlan{}; }   // per-group launches instead
   }

@@ -173,11 +173,12 @@ struct TokPlan {
   int64_t total_chunks = 0;
   uint32_t slot_bytes = 0, x_cap = 0;
   int32_t slots = 0, grid = 0;
-  int32_t flags = 0;              // tuning only (LSW_GEMV_TOKEN_FLAGS): bit 0 = skip the group wait
+  int32_t flags = 0;              // tuning only (LSW_GEMV_TOKEN_FLAGS): bit 0 = skip the group wait,
+                                  // bit 1 = skip the dot products (stream-only probe)
   size_t smem = 0;
 };
 // groups: host table with W/row_begin/rows/x_off/y_off/n_sites/row_bytes set.
-cudaError_t tok_plan_create(TokPlan* plan, TokGroup* groups, int32_t n_groups, int num_sms);
+cudaError_t tok_plan_create(TokPlan* plan, TokGroup* groups, int32_t n_groups, int num_sms, bool bf16);
 void tok_plan_destroy(TokPlan* plan);
 // done: DevState::tok_done; base: its value when this launch starts.
 cudaError_t launch_gemv_token(const TokPlan& plan, const void* xs, float* ys, unsigned long long* done,
