@@ -320,6 +320,23 @@ def run_ours(args, cfg):
         um_ms.append(a.elapsed_time(b))
         mg_ms.append(b.elapsed_time(c))
 
+    # restore-from-pristine switch: W <- RNE(P + Delta(d_t)), same
+    # 4 B/element as the fused switch; P = a copy of the weights as they are now
+    # (timing only: the bytes and the kernel do not depend on P's values)
+    rs_ms = []
+    if not args.no_restore:
+        P = {kd: W[kd].clone() for kd in synth.KINDS}
+        sw.attach_pristine(P)
+        for t in range(min(args.steps, 10)):
+            sw.router_topk(X1[t], idx, gate, stream)
+            a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            a.record(stream)
+            sw.restore_merge_all_layers(idx, gate, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            rs_ms.append(a.elapsed_time(b))
+        del P
+
     # end-to-end through the public API with host buffers
     x1h = torch.empty(cfg.d_model, dtype=cfg.torch_dtype).pin_memory()
     xsh = xs.cpu().pin_memory()
@@ -376,6 +393,8 @@ def run_ours(args, cfg):
             "gemv_GBps": tb["gemv"] / (gemv_med * 1e-3) / 1e9,
             "merge_GBps": tb["merge"] / (statistics.median(mg_ms) * 1e-3) / 1e9,
             "unmerge_GBps": tb["merge"] / (statistics.median(um_ms) * 1e-3) / 1e9,
+            "restore_ms": statistics.median(rs_ms) if rs_ms else None,
+            "restore_GBps": tb["merge"] / (statistics.median(rs_ms) * 1e-3) / 1e9 if rs_ms else None,
             "roofline": {"bound": "hbm", "achieved": sw_gbs, "peak": peak, "unit": "GB/s",
                          "frac": sw_gbs / peak, "traffic": _ncu_traffic(cfg, info),
                          "traffic_source": "profiles/ncu_switch_traffic.json (dram__bytes_read.sum + "
@@ -408,6 +427,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--switch-impl", default="auto", choices=["auto", "tc", "simt"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-restore", action="store_true", help="skip the restore-from-pristine timing "
+                    "(it needs one extra copy of the weights)")
     ap.add_argument("--ref-seconds", type=float, default=4.0,
                     help="oracle seconds per reference-arm step (cpu_baseline uses max(this, 10))")
     args = ap.parse_args()

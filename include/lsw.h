@@ -217,6 +217,21 @@ LSW_API lsw_status lsw_merge_all_layers(lsw_ctx* ctx, const int32_t* idx, const 
 LSW_API lsw_status lsw_unmerge_all_layers(lsw_ctx* ctx, void* stream);
 
 /*
+ * Restore-from-pristine switch (the paper rejects it for memory,
+ * P:266, which B200's 180 GB makes affordable):  W <- RNE(P + Delta(idx, gate))
+ * for every adapted matrix of every layer, ONE launch, from any state; state ->
+ * merged(idx, gate).  Same 4 B/element as the fused switch, k (not 2k) terms,
+ * and no drift: W after a token depends only on that token's decision.
+ *   lsw_attach_pristine: P[kind] [L, d_out, d_in] caller-owned DEVICE copies
+ *   of the original W (same layout and dtype, 16-byte aligned), borrowed for
+ *   the ctx lifetime; call once.  LSW_E_ARG on null / misaligned pointers.
+ *   lsw_restore_merge_all_layers: LSW_E_STATE if no pristine copy is attached.
+ */
+LSW_API lsw_status lsw_attach_pristine(lsw_ctx* ctx, const void* const P[LSW_NKIND]);
+LSW_API lsw_status lsw_restore_merge_all_layers(lsw_ctx* ctx, const int32_t* idx, const float* gate,
+                                                void* stream);
+
+/*
  * Eq. 3: y = W*[layer, kind] x, batch 1, fp32 accumulate.
  *   x [d_in] device cfg dtype;  y [d_out] fp32 device, overwritten.
  * Row-parallel kinds with tp_size > 1: y is sum-allreduced over the TP group.

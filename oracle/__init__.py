@@ -21,10 +21,11 @@ softmax), equal logits, shift invariance; delta/merge -> textbook LoRA merge
 (torch fp64), Eq.5 concatenation identity (dyadic, bit-exact); Eq.3==Eq.2
 merged forward (dyadic, bit-exact); Eq.7 unmerge inverts Eq.6 (dyadic); Eq.10
 == Eq.7 then Eq.6 (dyadic) with the literal Eq.9 as a failing negative
-control; drift closed form eps1*sqrt(T); gemv -> torch fp64 matmul; TP shard
-invariance.  No function here is "parity unpinned".
+control; restore-from-pristine -> textbook LoRA merge of P (torch fp64) and ==
+the switch chain from P (dyadic); drift closed form eps1*sqrt(T); gemv ->
+torch fp64 matmul; TP shard invariance.  No function here is "parity unpinned".
 """
 from .lsw_oracle import (  # noqa: F401
     rne, router, router_fast, coef_list, coef_list_literal_eq9, delta, merge, unmerge, switch,
-    switch_literal_eq9, gemv, unmerged_forward, drift, OracleModel,
+    switch_literal_eq9, restore, gemv, unmerged_forward, drift, OracleModel,
 )

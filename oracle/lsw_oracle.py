@@ -174,6 +174,13 @@ def switch(W, A_m, B_m, prev: Optional[Decision], cur: Decision, scale: float,
     return rne(np.asarray(W, np.float64) + delta(A_m, B_m, coef_list(cur, prev, scale)), store)
 
 
+def restore(P, A_m, B_m, cur: Decision, scale: float, store: Optional[str]) -> np.ndarray:
+    """SURVEY 8f #1 (the alternative P:266 rejects for memory): rebuild the
+    merged weight from the pristine copy P every token, f*^t = P + DOWN^t x UP^t
+    (Eq. 6 applied to P), one rounding.  No dependence on earlier tokens."""
+    return rne(np.asarray(P, np.float64) + delta(A_m, B_m, coef_list(cur, None, scale)), store)
+
+
 def switch_literal_eq9(W, A_m, B_m, prev, cur, scale, store):
     """NEGATIVE CONTROL: Eq. 10 with the literal (double-negated) Eq. 9."""
     return rne(np.asarray(W, np.float64) + delta(A_m, B_m, coef_list_literal_eq9(cur, prev, scale)), store)
@@ -248,6 +255,12 @@ class OracleModel:
     def merge_all_layers(self, cur: Decision):
         for key in self.W:
             self.W[key] = switch(self.W[key], self.A[key], self.B[key], self.prev, cur, self.scale, self.store)
+        self.prev = (tuple(int(e) for e in cur[0]), tuple(float(g) for g in cur[1]))
+
+    # restore from the pristine copies (R11 state: merged(cur))
+    def restore_merge_all_layers(self, P, cur: Decision):
+        for key in self.W:
+            self.W[key] = restore(P[key], self.A[key], self.B[key], cur, self.scale, self.store)
         self.prev = (tuple(int(e) for e in cur[0]), tuple(float(g) for g in cur[1]))
 
     # End of sequence -- Eq. 7

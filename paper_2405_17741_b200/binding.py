@@ -32,7 +32,7 @@ IMPL_NAME = {v: k for k, v in IMPL.items()}
 SYMBOLS = (
     "lsw_abi_version", "lsw_last_error", "lsw_create", "lsw_destroy", "lsw_get_info",
     "lsw_nccl_get_unique_id", "lsw_attach_nccl", "lsw_router_topk", "lsw_merge_all_layers",
-    "lsw_unmerge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers", "lsw_decode_token",
+    "lsw_unmerge_all_layers", "lsw_attach_pristine", "lsw_restore_merge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers", "lsw_decode_token",
     "lsw_decode_token_host", "lsw_device_status",
     "lsw_debug_switch_trace",      # include/lsw_debug.h (tuning hook)
 )
@@ -84,6 +84,8 @@ def load_library(path: str = LIB_PATH, strict: bool = True) -> ctypes.CDLL:
         "lsw_router_topk": (i32, [vp, vp, vp, vp, vp]),
         "lsw_merge_all_layers": (i32, [vp, vp, vp, vp]),
         "lsw_unmerge_all_layers": (i32, [vp, vp]),
+        "lsw_attach_pristine": (i32, [vp, ctypes.POINTER(vp)]),
+        "lsw_restore_merge_all_layers": (i32, [vp, vp, vp, vp]),
         "lsw_decode_linear": (i32, [vp, i32, i32, vp, vp, vp]),
         "lsw_decode_group": (i32, [vp, i32, i32, vp, vp, vp]),
         "lsw_decode_all_layers": (i32, [vp, vp, vp, vp]),
@@ -192,6 +194,20 @@ class LoraSwitch:
 
     def merge_all_layers(self, idx: torch.Tensor, gate: torch.Tensor, stream=None):
         _check(lib().lsw_merge_all_layers(self._h, _ptr(idx), _ptr(gate), _stream(stream)))
+
+    def attach_pristine(self, P: Dict[str, torch.Tensor]):
+        """Pristine copies of W (same shapes/dtype, device) for the restore switch."""
+        for kd in KINDS:
+            t = P[kd]
+            if not t.is_contiguous() or t.dtype != self.dtype or not t.is_cuda:
+                raise ValueError(f"pristine {kd}: must be a contiguous CUDA {self.dtype} tensor")
+        self._keep_p = P
+        arr = (ctypes.c_void_p * 7)(*[P[kd].data_ptr() for kd in KINDS])
+        _check(lib().lsw_attach_pristine(self._h, arr))
+
+    def restore_merge_all_layers(self, idx: torch.Tensor, gate: torch.Tensor, stream=None):
+        """W <- RNE(P + Delta(idx, gate)) from the attached pristine copy, any state."""
+        _check(lib().lsw_restore_merge_all_layers(self._h, _ptr(idx), _ptr(gate), _stream(stream)))
 
     def unmerge_all_layers(self, stream=None):
         _check(lib().lsw_unmerge_all_layers(self._h, _stream(stream)))

@@ -57,6 +57,7 @@ struct lsw_ctx {
   int64_t x_off[LSW_NGROUP] = {}, y_off[LSW_NGROUP] = {};   // per-layer offsets
   int64_t x_per_layer = 0, y_per_layer = 0;
   TokPlan tok{};                        // whole-token GEMV (tp_size == 1), else empty
+  bool has_pristine = false;            // lsw_attach_pristine called (RESTORE mode available)
   unsigned long long tok_base = 0;      // DevState::tok_done before the next token launch
   // staging for lsw_decode_token_host
   void* st_x1 = nullptr;
@@ -294,6 +295,33 @@ static lsw_status run_switch(lsw_ctx* ctx, int mode, const int32_t* idx, const f
 lsw_status lsw_merge_all_layers(lsw_ctx* ctx, const int32_t* idx, const float* gate, void* stream) {
   if (!ctx || !idx || !gate) return fail(LSW_E_ARG, "lsw_merge_all_layers: null argument");
   lsw_status st = run_switch(ctx, ctx->merged ? MODE_SWITCH : MODE_MERGE, idx, gate, (cudaStream_t)stream);
+  if (st == LSW_OK) ctx->merged = true;
+  return st;
+}
+
+lsw_status lsw_attach_pristine(lsw_ctx* ctx, const void* const P[LSW_NKIND]) {
+  if (!ctx || !P) return fail(LSW_E_ARG, "lsw_attach_pristine: null argument");
+  for (int k = 0; k < LSW_NKIND; ++k) {
+    if (!P[k]) return fail(LSW_E_ARG, "lsw_attach_pristine: kind %s: null pointer", kKindName[k]);
+    if (reinterpret_cast<uintptr_t>(P[k]) % 16)
+      return fail(LSW_E_ARG, "lsw_attach_pristine: kind %s: pointer not 16-byte aligned", kKindName[k]);
+  }
+  for (int k = 0; k < LSW_NKIND; ++k) ctx->simt_geom.kind[k].P = P[k];
+  if (ctx->tc) {
+    cudaError_t e = tc_plan_set_pristine(ctx->tc, ctx->simt_geom);
+    if (e != cudaSuccess) {
+      for (int k = 0; k < LSW_NKIND; ++k) ctx->simt_geom.kind[k].P = nullptr;
+      return fail(LSW_E_ARG, "lsw_attach_pristine: cuTensorMapEncodeTiled failed");
+    }
+  }
+  ctx->has_pristine = true;
+  return LSW_OK;
+}
+
+lsw_status lsw_restore_merge_all_layers(lsw_ctx* ctx, const int32_t* idx, const float* gate, void* stream) {
+  if (!ctx || !idx || !gate) return fail(LSW_E_ARG, "lsw_restore_merge_all_layers: null argument");
+  if (!ctx->has_pristine) return fail(LSW_E_STATE, "lsw_restore_merge_all_layers: no pristine copy attached");
+  lsw_status st = run_switch(ctx, MODE_RESTORE, idx, gate, (cudaStream_t)stream);
   if (st == LSW_OK) ctx->merged = true;
   return st;
 }

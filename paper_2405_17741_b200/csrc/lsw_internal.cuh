@@ -12,8 +12,10 @@ namespace lsw {
 
 constexpr int kMaxTerms = 2 * LSW_MAX_TOPK;   // |S_t u S_{t-1}| <= 2k
 
-// Switch modes (K1).  MERGE: Eq. 6; SWITCH: Eq. 10; UNMERGE: Eq. 7.
-enum SwitchMode : int32_t { MODE_MERGE = 0, MODE_SWITCH = 1, MODE_UNMERGE = 2 };
+// Switch modes (K1).  MERGE: Eq. 6; SWITCH: Eq. 10; UNMERGE: Eq. 7;
+// RESTORE: W <- RNE(P + Delta(cur)) from a pristine copy P --
+// the MERGE coefficient list, read from P instead of W.
+enum SwitchMode : int32_t { MODE_MERGE = 0, MODE_SWITCH = 1, MODE_UNMERGE = 2, MODE_RESTORE = 3 };
 
 // Ctx-owned device state.  slot[parity] holds the merged decision; a switch
 // pass writes the new decision into slot[parity^1] and the LAST CTA to finish
@@ -33,6 +35,7 @@ struct KindGeom {
   void* W;            // [L, d_out, d_in]
   const void* A;      // [L, N, r, d_in]
   const void* B;      // [L, N, d_out, r]
+  const void* P;      // pristine copy of W (RESTORE source), or null
   int64_t d_out, d_in;
   int64_t tile_begin; // first tile index of this kind (prefix sum)
   int32_t row_tiles, col_tiles;
@@ -66,7 +69,7 @@ __device__ __forceinline__ void build_coefs(const SwitchParams& p, int32_t parit
   int32_t ci[LSW_MAX_TOPK], pi[LSW_MAX_TOPK];
   float cg[LSW_MAX_TOPK], pg[LSW_MAX_TOPK];
   const bool has_cur = p.mode != MODE_UNMERGE;
-  const bool has_prev = p.mode != MODE_MERGE;
+  const bool has_prev = p.mode == MODE_SWITCH || p.mode == MODE_UNMERGE;
   for (int j = 0; j < k; ++j) {
     if (has_cur) {
       ci[j] = p.cur_idx[j];
@@ -195,5 +198,7 @@ int64_t tc_plan_tiles(const TcPlan* plan);
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
 int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);   // tuning trace (lsw_debug.h)
 int tc_plan_kernel(const TcPlan* plan);   // 1: v1 (switch_tc.cu), 2: term groups (switch_tc_tg.cu)
+// RESTORE source: encode tensor maps over geom.kind[k].P (lsw_attach_pristine)
+cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
 
 }  // namespace lsw

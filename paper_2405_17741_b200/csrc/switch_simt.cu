@@ -124,8 +124,9 @@ switch_simt_kernel(const SwitchParams p) {
           for (int q = 0; q < 8; ++q) delta[q] = fmaf(c, acc[q], delta[q]);
         }
         T* Wp = (T*)g.W + ((int64_t)layer * g.d_out + row) * g.d_in + col;
+        const T* Src = p.mode == MODE_RESTORE ? (const T*)g.P + ((int64_t)layer * g.d_out + row) * g.d_in + col : Wp;
         float w[8];
-        Vec8<T>::load(Wp, w);
+        Vec8<T>::load(Src, w);
 #pragma unroll
         for (int q = 0; q < 8; ++q) w[q] = w[q] + delta[q];
         Vec8<T>::store(Wp, w);

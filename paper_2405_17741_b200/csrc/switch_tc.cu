@@ -63,6 +63,7 @@ enum { ORDER_STRIP = 0, ORDER_SWEEP = 1 };
 
 struct TcMaps {
   CUtensorMap w[LSW_NKIND];   // W [L, d_out, d_in], box {64, 128, 1}, 128B swizzle
+  CUtensorMap p[LSW_NKIND];   // pristine copies (RESTORE source), same geometry
 };
 
 struct TcKind {
@@ -577,7 +578,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0)
-    for (int k = 0; k < LSW_NKIND; ++k) prefetch_map(&maps.w[k]);
+    for (int k = 0; k < LSW_NKIND; ++k) prefetch_map(args.mode == MODE_RESTORE ? &maps.p[k] : &maps.w[k]);
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                  ::"r"(smem_u32(&s_tmem_base)), "r"(g.tmem_cols) : "memory");
@@ -610,6 +611,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
       // ============================ W producer =============================
       if (lane == 0) {
         const uint64_t pol_stream = policy_evict_first();
+        const bool restore = args.mode == MODE_RESTORE;      // load from the pristine copy
         Ring wring{0, 0, (uint32_t)g.w_stages};
         uint32_t it = 0;
         for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
@@ -618,7 +620,8 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
           mbar_expect_tx(wbar, nsub * kSubBytes);
           uint8_t* wdst = wst0 + (size_t)wring.i * g.w_stage_bytes;
           for (int sb = 0; sb < nsub; ++sb)
-            tma_load_3d(smem_u32(wdst + sb * kSubBytes), &maps.w[c.kd], c.cb * tile_cols + sb * kTcTN,
+            tma_load_3d(smem_u32(wdst + sb * kSubBytes), restore ? &maps.p[c.kd] : &maps.w[c.kd],
+                        c.cb * tile_cols + sb * kTcTN,
                         c.rb * kTcTM, c.layer, wbar, pol_stream);
           trace_ev(args.trace, it, EV_W_ISSUED);
           wring.next();
@@ -1099,6 +1102,14 @@ int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n) {
   if (n > total) n = total;
   if (cudaMemcpy(host, plan->trace, n * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return n;
+}
+
+cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& sp) {
+  for (int k = 0; k < LSW_NKIND; ++k)
+    if (!sp.kind[k].P ||
+        !encode_w(&plan->maps.p[k], sp.kind[k].P, sp.kind[k].d_in, sp.kind[k].d_out, sp.n_layers))
+      return cudaErrorInvalidValue;
+  return cudaSuccess;
 }
 
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s) {

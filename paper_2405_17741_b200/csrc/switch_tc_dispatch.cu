@@ -54,6 +54,10 @@ cudaError_t launch_switch_tc(const TcPlan* p, const SwitchParams& sp, cudaStream
   return p->a ? v1::launch_switch_tc(p->a, sp, s) : tg::launch_switch_tc(p->b, sp, s);
 }
 
+cudaError_t tc_plan_set_pristine(TcPlan* p, const SwitchParams& geom) {
+  return p->a ? v1::tc_plan_set_pristine(p->a, geom) : tg::tc_plan_set_pristine(p->b, geom);
+}
+
 int64_t tc_plan_trace(const TcPlan* p, uint64_t* host, int64_t n) {
   return p->a ? v1::tc_plan_trace(p->a, host, n) : tg::tc_plan_trace(p->b, host, n);
 }

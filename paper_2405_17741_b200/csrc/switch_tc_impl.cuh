@@ -25,6 +25,7 @@ int tc_plan_tile_n(const TcPlan* plan);
 int64_t tc_plan_tiles(const TcPlan* plan);
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
 int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);
+cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
 }  // namespace v1
 
 namespace tg {
@@ -37,5 +38,6 @@ int tc_plan_tile_n(const TcPlan* plan);
 int64_t tc_plan_tiles(const TcPlan* plan);
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
 int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);
+cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
 }  // namespace tg
 }  // namespace lsw

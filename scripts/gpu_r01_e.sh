@@ -1,3 +1,2 @@
 #!/bin/bash
-timeout 300 python scripts/tune_gemv.py 2>&1 | tail -1 | cut -c1-330
-LSW_GEMV_SMEM_KB=200 timeout 300 python scripts/tune_gemv.py 2>&1 | tail -1 | cut -c1-330
+timeout 900 python -m pytest tests/test_gpu_restore.py tests/test_gpu_parity.py -q -x 2>&1 | tail -4

@@ -280,6 +280,26 @@ def test_switch_prev_none_is_merge_and_prev_eq_cur_is_noop():
     assert np.array_equal(O.switch(Wm, A, B, cur, cur, 2.0, "bf16"), Wm)
 
 
+def test_restore_is_textbook_merge_of_pristine_and_ends_any_switch_chain():
+    """restore(P, cur) = P + sum_j (alpha/r) g_j B_j A_j (textbook
+    LoRA merge, torch fp64) and equals, exactly on dyadic inputs, the end of any
+    Eq. 6 / Eq. 10 chain started from P -- i.e. it carries no history."""
+    W, A, B = _dyadic_site(21)
+    scale = 2.0
+    cur = ([2, 0], [0.75, 0.25])
+    Pt, At, Bt = (torch.from_numpy(np.asarray(t, np.float64)) for t in (W, A, B))
+    ref = Pt.clone()
+    for e, g in zip(*cur):
+        ref += scale * g * (Bt[e] @ At[e])
+    np.testing.assert_allclose(O.restore(W, A, B, cur, scale, None), ref.numpy(), rtol=1e-13, atol=1e-13)
+    chain = O.merge(W, A, B, ([1, 3], [0.5, 0.5]), scale, None)
+    chain = O.switch(chain, A, B, ([1, 3], [0.5, 0.5]), ([3, 2], [0.625, 0.375]), scale, None)
+    chain = O.switch(chain, A, B, ([3, 2], [0.625, 0.375]), cur, scale, None)
+    assert np.array_equal(O.restore(W, A, B, cur, scale, None), chain)
+    # negative control: restoring from the merged W instead of P adds the delta twice
+    assert not np.array_equal(O.restore(chain, A, B, cur, scale, None), chain)
+
+
 def test_coef_list_signs_and_order():
     cl = O.coef_list(([3, 1], [0.7, 0.3]), ([0, 3], [0.6, 0.4]), 2.0)
     assert cl == [(3, 1.4), (1, 0.6), (0, -1.2), (3, -0.8)]
