@@ -337,6 +337,20 @@ def run_ours(args, cfg):
             rs_ms.append(a.elapsed_time(b))
         del P
 
+    # unmerged decode (the honest comparison): router + Eq. 2 on the
+    # pristine weights, W read once (2 B/element) instead of switched and read (6)
+    un_ms = []
+    if world == 1:
+        sw.unmerge_all_layers(stream)
+        for t in range(min(args.steps, 10)):
+            a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            a.record(stream)
+            sw.router_topk(X1[t], idx, gate, stream)
+            sw.decode_all_layers_unmerged(xs, ys, idx, gate, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            un_ms.append(a.elapsed_time(b))
+
     # end-to-end through the public API with host buffers
     x1h = torch.empty(cfg.d_model, dtype=cfg.torch_dtype).pin_memory()
     xsh = xs.cpu().pin_memory()
@@ -395,6 +409,9 @@ def run_ours(args, cfg):
             "unmerge_GBps": tb["merge"] / (statistics.median(um_ms) * 1e-3) / 1e9,
             "restore_ms": statistics.median(rs_ms) if rs_ms else None,
             "restore_GBps": tb["merge"] / (statistics.median(rs_ms) * 1e-3) / 1e9 if rs_ms else None,
+            "unmerged_decode_ms_per_token": statistics.median(un_ms) if un_ms else None,
+            "unmerged_decode_GBps": (tb["unmerged_token"] / (statistics.median(un_ms) * 1e-3) / 1e9
+                                     if un_ms else None),
             "roofline": {"bound": "hbm", "achieved": sw_gbs, "peak": peak, "unit": "GB/s",
                          "frac": sw_gbs / peak, "traffic": _ncu_traffic(cfg, info),
                          "traffic_source": "profiles/ncu_switch_traffic.json (dram__bytes_read.sum + "

@@ -258,6 +258,23 @@ LSW_API lsw_status lsw_decode_group(lsw_ctx* ctx, int32_t layer, int32_t group, 
 LSW_API lsw_status lsw_decode_all_layers(lsw_ctx* ctx, const void* xs, float* ys, void* stream);
 
 /*
+ * Unmerged decode ("the honest comparison"; Eq. 2 at P:228 run
+ * without merging): y = W x + sum_j (alpha/r) g_j B[e_j] (A[e_j] x) for every
+ * site of `group`, on the UN-merged weights.  W is read once (2 B/element)
+ * instead of being switched (4 B) and then read (2 B).  One launch per group:
+ * the k*r LoRA-down products of each site are spread over the grid, then one
+ * device-wide barrier, then each row's LoRA-up term joins its reduction.
+ *   idx/gate: device [top_k] (from lsw_router_topk).  x, y as lsw_decode_group.
+ *   LSW_E_STATE if the ctx is merged (W must be the pristine weight);
+ *   LSW_E_UNSUPPORTED if tp_size > 1 (o/down would need an all-reduce of A x).
+ */
+LSW_API lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_t group, const void* x, float* y,
+                                             const int32_t* idx, const float* gate, void* stream);
+/* Every group of every layer, in order (layouts as lsw_decode_all_layers). */
+LSW_API lsw_status lsw_decode_all_layers_unmerged(lsw_ctx* ctx, const void* xs, float* ys, const int32_t* idx,
+                                                  const float* gate, void* stream);
+
+/*
  * One whole Alg. 1 token: router(x1) -> merge_all_layers -> lsw_decode_all_layers.
  * idx/gate receive the decision (device).
  */

@@ -32,7 +32,8 @@ IMPL_NAME = {v: k for k, v in IMPL.items()}
 SYMBOLS = (
     "lsw_abi_version", "lsw_last_error", "lsw_create", "lsw_destroy", "lsw_get_info",
     "lsw_nccl_get_unique_id", "lsw_attach_nccl", "lsw_router_topk", "lsw_merge_all_layers",
-    "lsw_unmerge_all_layers", "lsw_attach_pristine", "lsw_restore_merge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers", "lsw_decode_token",
+    "lsw_unmerge_all_layers", "lsw_attach_pristine", "lsw_restore_merge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers",
+    "lsw_decode_group_unmerged", "lsw_decode_all_layers_unmerged", "lsw_decode_token",
     "lsw_decode_token_host", "lsw_device_status",
     "lsw_debug_switch_trace",      # include/lsw_debug.h (tuning hook)
 )
@@ -89,6 +90,8 @@ def load_library(path: str = LIB_PATH, strict: bool = True) -> ctypes.CDLL:
         "lsw_decode_linear": (i32, [vp, i32, i32, vp, vp, vp]),
         "lsw_decode_group": (i32, [vp, i32, i32, vp, vp, vp]),
         "lsw_decode_all_layers": (i32, [vp, vp, vp, vp]),
+        "lsw_decode_group_unmerged": (i32, [vp, i32, i32, vp, vp, vp, vp, vp]),
+        "lsw_decode_all_layers_unmerged": (i32, [vp, vp, vp, vp, vp, vp]),
         "lsw_decode_token": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_decode_token_host": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_device_status": (i32, [vp, vp, ctypes.POINTER(i32)]),
@@ -222,6 +225,15 @@ class LoraSwitch:
     def decode_all_layers(self, xs, ys, stream=None):
         """Every group GEMV of every layer (packed xs -> packed ys), decoder order."""
         _check(lib().lsw_decode_all_layers(self._h, _ptr(xs), _ptr(ys), _stream(stream)))
+
+    def decode_group_unmerged(self, layer: int, group: int, x, y, idx, gate, stream=None):
+        """y = W x + sum_j (alpha/r) g_j B_j (A_j x) on the UN-merged weights (Eq. 2)."""
+        _check(lib().lsw_decode_group_unmerged(self._h, layer, group, _ptr(x), _ptr(y), _ptr(idx), _ptr(gate),
+                                               _stream(stream)))
+
+    def decode_all_layers_unmerged(self, xs, ys, idx, gate, stream=None):
+        _check(lib().lsw_decode_all_layers_unmerged(self._h, _ptr(xs), _ptr(ys), _ptr(idx), _ptr(gate),
+                                                    _stream(stream)))
 
     def decode_token(self, x1, xs, ys, idx, gate, stream=None):
         _check(lib().lsw_decode_token(self._h, _ptr(x1), _ptr(xs), _ptr(ys), _ptr(idx), _ptr(gate),

@@ -193,7 +193,8 @@ __device__ __forceinline__ uint64_t dot8_f2(const uint4 w, const float4 lo, cons
 
 // One row of W (in shared memory) against the staged x, reduced over the warp.
 template <bool kBf16>
-__device__ __forceinline__ float row_dot(const uint8_t* wrow, const uint8_t* xs, int64_t n16, int lane) {
+__device__ __forceinline__ float row_dot(const uint8_t* wrow, const uint8_t* xs, int64_t n16, int lane,
+                                         float extra_a = 0.f, float extra_b = 0.f, float extra_c = 1.f) {
   const uint4* w4 = reinterpret_cast<const uint4*>(wrow);
   float acc;
   if (kBf16) {
@@ -221,14 +222,77 @@ __device__ __forceinline__ float row_dot(const uint8_t* wrow, const uint8_t* xs,
     if (c < n16) acc0 += dot_chunk<false>(w4[c], x4, c);
     acc = acc0 + acc1;
   }
+  // this lane's share of a LoRA term (unmerged decode); multiplied only here so
+  // that a load feeding it is not waited for before the row's dot product
+  acc = fmaf(extra_a * extra_c, extra_b, acc);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   return acc;
 }
 
+// Unmerged decode, LoRA-down step: u[q][j][rho] = A_q[e_j][rho, :] . x for
+// every site q, selected expert j and rank index rho of a group -- one CTA per
+// dot product, its 8 warps on 8 consecutive K-slices (each lane <= 8 loads in
+// flight for d_in <= 16384), partial sums added in warp order (deterministic).
+// Launched (PDL) right before the group's GEMV, whose consumers read u after
+// griddepcontrol.wait; its W stream does not wait for this kernel.
+constexpr int kLoraDownWarps = 8;
+
 template <bool kBf16>
+__global__ void __launch_bounds__(32 * kLoraDownWarps)
+lora_down_kernel(const GemvParams p, const GemvLora L) {
+  __shared__ float part[kLoraDownWarps];
+  // let the group's GEMV launch at once (its W stream needs nothing from here;
+  // its consumers wait for this grid), then wait for x / idx to be final
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kr = L.k * L.r;
+  const int d = blockIdx.x;
+  const int q = d / kr, j = (d - q * kr) / L.r, rho = d - q * kr - j * L.r;
+  const int64_t es = kBf16 ? 2 : 4;
+  const int64_t n16 = p.d_in * es / 16;
+  const uint4* a4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(L.A[q]) +
+                                                   ((int64_t)L.idx[j] * L.r + rho) * p.d_in * es);
+  const uint4* x4 = reinterpret_cast<const uint4*>(p.x);
+  const int64_t per = (n16 + kLoraDownWarps - 1) / kLoraDownWarps;
+  const int64_t c_begin = warp * per, c_end = c_begin + per < n16 ? c_begin + per : n16;
+  float acc = 0.f;
+  for (int64_t c0 = c_begin + lane; c0 < c_end; c0 += 32 * 8) {
+    uint4 a[8], x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool in = c0 + 32 * u < c_end;
+      a[u] = in ? __ldg(a4 + c0 + 32 * u) : make_uint4(0, 0, 0, 0);
+      x[u] = in ? __ldg(x4 + c0 + 32 * u) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (kBf16) {
+        acc += dot_chunk<true>(a[u], x + u, 0);
+      } else {
+        const float4 xv = *reinterpret_cast<const float4*>(&x[u]);
+        acc = fmaf(__uint_as_float(a[u].x), xv.x, acc);
+        acc = fmaf(__uint_as_float(a[u].y), xv.y, acc);
+        acc = fmaf(__uint_as_float(a[u].z), xv.z, acc);
+        acc = fmaf(__uint_as_float(a[u].w), xv.w, acc);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) part[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float u = 0.f;
+    for (int w = 0; w < kLoraDownWarps; ++w) u += part[w];
+    L.u[d] = u;
+  }
+}
+
+template <bool kBf16, bool kLora>
 __global__ void __launch_bounds__(kBulkThreads, 1)
-gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) {
+gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, const GemvLora L) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -304,6 +368,22 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) 
   // consumers: unit u = (local chunk i, row k in chunk); warp cw takes u = cw mod 8
   const int cw = warp - 1;
   const int64_t nchunk16 = row_bytes / 16;
+  float ug[3] = {0.f, 0.f, 0.f};                  // kLora, k*r <= 32: this lane's u_q[j][rho] per site
+  float gj_l = 0.f;                                // and scale * g_j
+  int lane_e = -1, lane_rho = 0;
+  if (kLora) {
+    // u (the group's LoRA-down products, final sums) was written by the
+    // lora_down kernel that precedes this launch; griddepcontrol.wait above
+    // has made it visible.  Lane l < k*r keeps (j, rho) = (l / r, l % r).
+    const int kr = L.k * L.r;
+    if (kr <= 32 && lane < kr) {
+      const int j = lane / L.r;
+      lane_e = L.idx[j];
+      gj_l = L.scale * L.gate[j];
+      lane_rho = lane - j * L.r;
+      for (int q = 0; q < p.n_sites; ++q) ug[q] = __ldcg(L.u + q * kr + lane);
+    }
+  }
   for (int64_t u = cw; u < my_chunks * R; u += kBulkConsumers) {
     const int64_t i = u / R;
     const int k = (int)(u - i * R);
@@ -312,7 +392,35 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w) 
     while (issued <= i) __nanosleep(64);
     g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
     if (row < p.rows_total) {
-      const float acc = row_dot<kBf16>(ring + s * slot_bytes + (size_t)k * row_bytes, xs, nchunk16, lane);
+      float extra = 0.f, extra_u = 1.f, extra_g = 1.f;
+      if (kLora && !(L.flags & 4)) {
+        // this row's LoRA-up term, sum_j scale g_j B_q[e_j][row, :] . u_q[j]:
+        // lane l < k*r takes (j, rho) = (l / r, l % r).  The B element is
+        // loaded before the row's dot product so its latency overlaps it.
+        const int q = (p.n_sites > 2 && row >= p.site[2].row_begin) ? 2
+                      : (p.n_sites > 1 && row >= p.site[1].row_begin) ? 1 : 0;
+        const int64_t rl = row - p.site[q].row_begin, dq = p.site[q].d_out;
+        const int kr = L.k * L.r;
+        if (kr <= 32) {
+          if (lane_e >= 0) {
+            const int64_t off = ((int64_t)lane_e * dq + rl) * L.r + lane_rho;
+            extra = kBf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(L.B[q])[off])
+                          : reinterpret_cast<const float*>(L.B[q])[off];
+            extra_u = q == 0 ? ug[0] : q == 1 ? ug[1] : ug[2];
+            extra_g = gj_l;
+          }
+        } else {
+          for (int l = lane; l < kr; l += 32) {
+            const int j = l / L.r, rho = l - j * L.r;
+            const int64_t off = ((int64_t)L.idx[j] * dq + rl) * L.r + rho;
+            const float b = kBf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(L.B[q])[off])
+                                  : reinterpret_cast<const float*>(L.B[q])[off];
+            extra += (L.scale * L.gate[j]) * b * __ldcg(L.u + q * kr + l);
+          }
+        }
+      }
+      const float acc =
+          row_dot<kBf16>(ring + s * slot_bytes + (size_t)k * row_bytes, xs, nchunk16, lane, extra, extra_u, extra_g);
       if (lane == 0) p.y[row] = acc;
     }
     __syncwarp();
@@ -335,6 +443,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   return v;
 }
 
+// Spin (with a ~20 s watchdog) until a device-wide counter reaches target.
 __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsigned long long target) {
   if ((long long)(ld_acquire_u64(p) - target) >= 0) return;
   uint64_t t0, t;
@@ -565,7 +674,8 @@ static int gemv_variant() {
   return v;
 }
 
-cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w) {
+cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w,
+                        GemvLora* lora) {
   const bool bf16 = dtype == LSW_BF16;
   if (gemv_variant() == 1) {
     // bulk-copy throughput grows with bytes per operation (scripts/membench.cu:
@@ -585,11 +695,12 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
     if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
     if (slots >= 2) {
       const size_t smem = x_bytes + (size_t)slots * slot_bytes;
-      auto fn = bf16 ? gemv_bulk_kernel<true> : gemv_bulk_kernel<false>;
-      static size_t smem_set[2] = {0, 0};     // attribute set once per kernel (not per launch)
-      if (smem > smem_set[bf16]) {
+      auto fn = lora ? (bf16 ? gemv_bulk_kernel<true, true> : gemv_bulk_kernel<false, true>)
+                     : (bf16 ? gemv_bulk_kernel<true, false> : gemv_bulk_kernel<false, false>);
+      static size_t smem_set[2][2] = {{0, 0}, {0, 0}};   // attribute set once per kernel (not per launch)
+      if (smem > smem_set[lora != nullptr][bf16]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        smem_set[bf16] = smem;
+        smem_set[lora != nullptr][bf16] = smem;
       }
       const int64_t n_chunks = (p.rows_total + R - 1) / R;
       int grid = (int)(n_chunks < num_sms ? n_chunks : num_sms);
@@ -604,9 +715,23 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
       at[0].val.programmaticStreamSerializationAllowed = 1;
       lc.attrs = at;
       lc.numAttrs = 1;
-      return cudaLaunchKernelEx(&lc, fn, p, slots, R, (int32_t)(early_w ? 1 : 0));
+      const GemvLora none{};
+      if (lora) {
+        // LoRA-down products first (PDL): the GEMV below streams its W at once
+        // and its consumers read u after griddepcontrol.wait
+        cudaLaunchConfig_t ld{};
+        ld.gridDim = dim3(p.n_sites * lora->k * lora->r);
+        ld.blockDim = dim3(32 * kLoraDownWarps);
+        ld.stream = s;
+        ld.attrs = at;
+        ld.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&ld, bf16 ? lora_down_kernel<true> : lora_down_kernel<false>, p, *lora);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaLaunchKernelEx(&lc, fn, p, slots, R, (int32_t)(early_w || lora ? 1 : 0), lora ? *lora : none);
     }
   }
+  if (lora) return cudaErrorNotSupported;   // the LDG variant has no unmerged form
   const size_t smem = (size_t)p.d_in * (bf16 ? 2 : 4);
   auto fn = bf16 ? gemv_kernel<true> : gemv_kernel<false>;
   static int occ_cache[2][8] = {};          // [dtype][smem bucket of 16 KB] -> CTAs per SM

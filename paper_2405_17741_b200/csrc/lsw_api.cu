@@ -1,6 +1,7 @@
 // lsw_api.cu -- the C ABI (include/lsw.h): validation, ctx state machine,
 // dispatch of the K1/K2/K4 kernels, NCCL for the TP decode.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -58,6 +59,7 @@ struct lsw_ctx {
   int64_t x_per_layer = 0, y_per_layer = 0;
   TokPlan tok{};                        // whole-token GEMV (tp_size == 1), else empty
   bool has_pristine = false;            // lsw_attach_pristine called (RESTORE mode available)
+  float* lora_u = nullptr;              // unmerged decode: LoRA-down products scratch
   unsigned long long tok_base = 0;      // DevState::tok_done before the next token launch
   // staging for lsw_decode_token_host
   void* st_x1 = nullptr;
@@ -214,6 +216,7 @@ lsw_status lsw_destroy(lsw_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->tc) tc_plan_destroy(ctx->tc);
   tok_plan_destroy(&ctx->tok);
+  cudaFree(ctx->lora_u);
   cudaFree(ctx->d_state);
   cudaFree(ctx->st_x1);
   cudaFree(ctx->st_xs);
@@ -367,6 +370,75 @@ static lsw_status gemv_sites(lsw_ctx* ctx, int layer, const int* kinds, int n, c
     ncclResult_t r = ncclAllReduce(y, y, (size_t)rows, ncclFloat, ncclSum, ctx->comm, s);
     if (r != ncclSuccess) return fail(LSW_E_NCCL, "%s: ncclAllReduce: %s", who, ncclGetErrorString(r));
   }
+  return LSW_OK;
+}
+
+static lsw_status gemv_unmerged(lsw_ctx* ctx, int layer, int group, const void* x, float* y, const int32_t* idx,
+                                const float* gate, cudaStream_t s, const char* who, bool early_w) {
+  if (!ctx || !x || !y || !idx || !gate) return fail(LSW_E_ARG, "%s: null argument", who);
+  if (layer < 0 || layer >= ctx->cfg.n_layers)
+    return fail(LSW_E_ARG, "%s: layer=%d not in [0,%d)", who, layer, ctx->cfg.n_layers);
+  if (group < 0 || group >= LSW_NGROUP) return fail(LSW_E_ARG, "%s: group=%d invalid", who, group);
+  if (reinterpret_cast<uintptr_t>(x) % 16) return fail(LSW_E_ARG, "%s: x not 16-byte aligned", who);
+  if (ctx->merged) return fail(LSW_E_STATE, "%s: the ctx is merged (unmerged decode reads the pristine W)", who);
+  if (ctx->cfg.tp_size > 1) return fail(LSW_E_UNSUPPORTED, "%s: tp_size > 1", who);
+  if (!ctx->lora_u) {
+    const size_t n = (size_t)3 * ctx->cfg.top_k * ctx->cfg.rank;
+    if (cudaMalloc(&ctx->lora_u, n * sizeof(float)) != cudaSuccess)
+      return fail(LSW_E_OOM, "%s: scratch allocation failed", who);
+  }
+  const size_t es = esize(ctx);
+  GemvParams p{};
+  GemvLora L{};
+  int64_t rows = 0;
+  const int n = kGroupSize[group];
+  for (int i = 0; i < n; ++i) {
+    const lsw_kind_desc& d = ctx->kinds[kGroupKinds[group][i]];
+    p.site[i].W = (const uint8_t*)d.W + (size_t)layer * d.d_out * d.d_in * es;
+    p.site[i].d_out = d.d_out;
+    p.site[i].row_begin = rows;
+    rows += d.d_out;
+    L.A[i] = (const uint8_t*)d.A + (size_t)layer * ctx->cfg.n_experts * ctx->cfg.rank * d.d_in * es;
+    L.B[i] = (const uint8_t*)d.B + (size_t)layer * ctx->cfg.n_experts * d.d_out * ctx->cfg.rank * es;
+  }
+  p.n_sites = n;
+  p.rows_total = rows;
+  p.d_in = ctx->kinds[kGroupKinds[group][0]].d_in;
+  p.x = x;
+  p.y = y;
+  L.idx = idx;
+  L.gate = gate;
+  L.scale = ctx->cfg.alpha / (float)ctx->cfg.rank;
+  L.k = ctx->cfg.top_k;
+  L.r = ctx->cfg.rank;
+  L.u = ctx->lora_u;
+  if (const char* v = getenv("LSW_UNMERGED_FLAGS")) L.flags = atoi(v);   // tuning probes only
+  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->num_sms, s, early_w, &L);
+  if (e == cudaErrorNotSupported) return fail(LSW_E_UNSUPPORTED, "%s: needs the bulk GEMV (LSW_GEMV=ldg set)", who);
+  if (e != cudaSuccess) return cuda_fail(e, "unmerged decode GEMV launch");
+  ctx->launches += 2;                       // LoRA-down + GEMV
+  return LSW_OK;
+}
+
+lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_t group, const void* x, float* y,
+                                     const int32_t* idx, const float* gate, void* stream) {
+  return gemv_unmerged(ctx, layer, group, x, y, idx, gate, (cudaStream_t)stream, "lsw_decode_group_unmerged",
+                       /*early_w=*/true);
+}
+
+lsw_status lsw_decode_all_layers_unmerged(lsw_ctx* ctx, const void* xs, float* ys, const int32_t* idx,
+                                          const float* gate, void* stream) {
+  if (!ctx || !xs || !ys) return fail(LSW_E_ARG, "lsw_decode_all_layers_unmerged: null argument");
+  const size_t es = esize(ctx);
+  for (int l = 0; l < ctx->cfg.n_layers; ++l)
+    for (int g = 0; g < LSW_NGROUP; ++g) {
+      const uint8_t* xp = (const uint8_t*)xs + (size_t)(l * ctx->x_per_layer + ctx->x_off[g]) * es;
+      float* yp = ys + l * ctx->y_per_layer + ctx->y_off[g];
+      // W is never written on this path: every launch may prefetch it under PDL
+      lsw_status st = gemv_unmerged(ctx, l, g, xp, yp, idx, gate, (cudaStream_t)stream,
+                                    "lsw_decode_all_layers_unmerged", /*early_w=*/true);
+      if (st != LSW_OK) return st;
+    }
   return LSW_OK;
 }
 

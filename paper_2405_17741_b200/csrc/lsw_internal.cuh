@@ -153,9 +153,26 @@ struct GemvParams {
   const void* x;
   float* y;
 };
+// Unmerged decode (Eq. 2 at P:228 without merging):
+// y = W x + sum_j scale * g_j * B_{e_j} (A_{e_j} x) for every site of a group,
+// W being the un-merged (pristine) weight.  Two launches per group: the k*r
+// LoRA-down products per site (lora_down_kernel, gemv.cu), then the GEMV, which
+// folds each row's LoRA-up term into its reduction.
+struct GemvLora {
+  const void* A[3];          // site q: A_kind of this layer [N, r, d_in]
+  const void* B[3];          // site q: B_kind of this layer [N, d_out_q, r]
+  const int32_t* idx;        // [k] device
+  const float* gate;         // [k] device
+  float scale;               // alpha / r
+  int32_t k, r;
+  float* u;                  // scratch [n_sites * k * r] fp32
+  int32_t flags;             // tuning probe (LSW_UNMERGED_FLAGS): 4 = no LoRA-up term (results wrong)
+};
 // early_w: the previous launch on `s` was a GEMV (W may be prefetched before
-// griddepcontrol.wait; see gemv.cu).
-cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w = false);
+// griddepcontrol.wait; see gemv.cu).  lora: null for the merged-weight GEMV.
+// lora: also launches the group's LoRA-down kernel first (2 launches).
+cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w = false,
+                        GemvLora* lora = nullptr);
 
 // Whole-token decode GEMV (gemv.cu, K4b): every group of every layer in ONE
 // persistent launch.  The W stream runs ahead across group boundaries; group

@@ -70,7 +70,7 @@ def token_bytes(cfg: synth.Config, tp_size: int = 1) -> Dict[str, float]:
     gemv: s per W element + s*d_in + 4*d_out.  router: s*N*d_model + s*d_model.
     """
     s = cfg.elem_bytes
-    w = sw = mg = gv = 0
+    w = sw = mg = gv = um = 0
     for kd in synth.KINDS:
         d_out, d_in = cfg.local_shape(kd, 0, tp_size)
         n = d_out * d_in * cfg.n_layers
@@ -78,9 +78,11 @@ def token_bytes(cfg: synth.Config, tp_size: int = 1) -> Dict[str, float]:
         sw += 2 * s * n + s * (2 * cfg.top_k * cfg.rank) * (d_out + d_in) * cfg.n_layers
         mg += 2 * s * n + s * (cfg.top_k * cfg.rank) * (d_out + d_in) * cfg.n_layers
         gv += s * n + (s * d_in + 4 * d_out) * cfg.n_layers
+        # unmerged decode (Eq. 2): the GEMV's bytes + the k selected A and B slices
+        um += s * n + (s * d_in + 4 * d_out) * cfg.n_layers + s * (cfg.top_k * cfg.rank) * (d_out + d_in) * cfg.n_layers
     rt = s * cfg.n_experts * cfg.d_model + s * cfg.d_model
     return {"w_elems": w, "switch": sw, "merge": mg, "gemv": gv, "router": rt,
-            "token": sw + gv + rt}
+            "token": sw + gv + rt, "unmerged_token": um + rt}
 
 
 def token_flops(cfg: synth.Config, tp_size: int = 1, terms: int = None) -> float:

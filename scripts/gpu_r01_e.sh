@@ -1,2 +1,2 @@
 #!/bin/bash
-timeout 900 python -m pytest tests/test_gpu_restore.py tests/test_gpu_parity.py -q -x 2>&1 | tail -4
+timeout 900 python -m pytest tests/test_gpu_unmerged.py tests/test_gpu_restore.py tests/test_gpu_parity.py -q -x 2>&1 | tail -2
