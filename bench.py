@@ -337,11 +337,58 @@ def run_ours(args, cfg):
             rs_ms.append(a.elapsed_time(b))
         del P
 
+    # launch-count ablation (the paper's Tab. 6 "simple merge"):
+    # the Eq. 6 merge as 1 launch vs one launch per matrix (7 L), eager and
+    # replayed from a CUDA graph (each graph = merge + the single unmerge)
+    abl = None
+    if world == 1 and info["switch_impl"] == "tc":
+        sw.unmerge_all_layers(stream)
+
+        def _time(fn, n=5):
+            ms = []
+            for _ in range(n):
+                a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize()
+                ms.append(a.elapsed_time(b))
+            return statistics.median(ms)
+
+        single = lambda: sw.merge_all_layers(idx, gate, stream)
+        per_mat = lambda: sw.debug_merge_per_matrix(idx, gate, stream)
+        abl = {"launches_single": 1, "launches_per_matrix": 7 * cfg.n_layers}
+        for key, fn in (("single", single), ("per_matrix", per_mat)):
+            ms = []
+            for _ in range(5):
+                a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+                a.record(stream)
+                fn()
+                b.record(stream)
+                torch.cuda.synchronize()
+                ms.append(a.elapsed_time(b))
+                sw.unmerge_all_layers(stream)
+            abl[key + "_ms"] = statistics.median(ms)
+        gs = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        # graphs: capture merge + unmerge on the capture stream
+        for key, merge in (("single", lambda st: sw.merge_all_layers(idx, gate, st)),
+                           ("per_matrix", lambda st: sw.debug_merge_per_matrix(idx, gate, st))):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=gs):
+                merge(gs)
+                sw.unmerge_all_layers(gs)
+            abl[key + "_graph_merge_plus_unmerge_ms"] = _time(g.replay)
+            del g
+        um_only = _time(lambda: (sw.merge_all_layers(idx, gate, stream), sw.unmerge_all_layers(stream)))
+        abl["single_eager_merge_plus_unmerge_ms"] = um_only
+
     # unmerged decode (the honest comparison): router + Eq. 2 on the
     # pristine weights, W read once (2 B/element) instead of switched and read (6)
     un_ms = []
     if world == 1:
-        sw.unmerge_all_layers(stream)
+        if sw.info()["merged"]:
+            sw.unmerge_all_layers(stream)
         for t in range(min(args.steps, 10)):
             a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
             a.record(stream)
@@ -409,6 +456,7 @@ def run_ours(args, cfg):
             "unmerge_GBps": tb["merge"] / (statistics.median(um_ms) * 1e-3) / 1e9,
             "restore_ms": statistics.median(rs_ms) if rs_ms else None,
             "restore_GBps": tb["merge"] / (statistics.median(rs_ms) * 1e-3) / 1e9 if rs_ms else None,
+            "launch_ablation": abl,
             "unmerged_decode_ms_per_token": statistics.median(un_ms) if un_ms else None,
             "unmerged_decode_GBps": (tb["unmerged_token"] / (statistics.median(un_ms) * 1e-3) / 1e9
                                      if un_ms else None),

@@ -26,6 +26,14 @@ extern "C" {
  * ctx uses the SIMT switch).  Synchronizes the device.  LSW_E_ARG on null. */
 LSW_API lsw_status lsw_debug_switch_trace(lsw_ctx* ctx, uint64_t* host_out, int64_t n, int64_t* n_out);
 
+/* Launch-count ablation (the paper's "simple merge" row of
+ * Tab. 6): the Eq. 6 merge of lsw_merge_all_layers, but ONE launch
+ * of the same tensor-core kernel per adapted matrix (7 x L launches, each over
+ * that matrix's tiles).  Same result (bitwise) as the single launch.  State
+ * must be `none` (LSW_E_STATE otherwise) and becomes merged(idx, gate);
+ * LSW_E_UNSUPPORTED for the SIMT switch.  Enqueue-only (graph-capturable). */
+LSW_API lsw_status lsw_debug_merge_per_matrix(lsw_ctx* ctx, const int32_t* idx, const float* gate, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

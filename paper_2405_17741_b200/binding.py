@@ -35,7 +35,7 @@ SYMBOLS = (
     "lsw_unmerge_all_layers", "lsw_attach_pristine", "lsw_restore_merge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers",
     "lsw_decode_group_unmerged", "lsw_decode_all_layers_unmerged", "lsw_decode_token",
     "lsw_decode_token_host", "lsw_device_status",
-    "lsw_debug_switch_trace",      # include/lsw_debug.h (tuning hook)
+    "lsw_debug_switch_trace", "lsw_debug_merge_per_matrix",   # include/lsw_debug.h
 )
 
 
@@ -96,6 +96,7 @@ def load_library(path: str = LIB_PATH, strict: bool = True) -> ctypes.CDLL:
         "lsw_decode_token_host": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_device_status": (i32, [vp, vp, ctypes.POINTER(i32)]),
         "lsw_debug_switch_trace": (i32, [vp, vp, i64, ctypes.POINTER(i64)]),
+        "lsw_debug_merge_per_matrix": (i32, [vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         if not strict and not hasattr(lib, name):
@@ -242,6 +243,10 @@ class LoraSwitch:
     def decode_token_host(self, x1_h, xs_h, ys_h, idx_h, gate_h, stream=None):
         _check(lib().lsw_decode_token_host(self._h, _ptr(x1_h), _ptr(xs_h), _ptr(ys_h), _ptr(idx_h),
                                            _ptr(gate_h), _stream(stream)))
+
+    def debug_merge_per_matrix(self, idx, gate, stream=None):
+        """Launch-count ablation (include/lsw_debug.h): the merge as 7*L launches."""
+        _check(lib().lsw_debug_merge_per_matrix(self._h, _ptr(idx), _ptr(gate), _stream(stream)))
 
     def debug_switch_trace(self):
         """Tuning hook (include/lsw_debug.h): int64 ns timestamps [2, 256, 12]

@@ -535,6 +535,27 @@ lsw_status lsw_device_status(lsw_ctx* ctx, void* stream, int32_t* code) {
   return LSW_OK;
 }
 
+lsw_status lsw_debug_merge_per_matrix(lsw_ctx* ctx, const int32_t* idx, const float* gate, void* stream) {
+  if (!ctx || !idx || !gate) return fail(LSW_E_ARG, "lsw_debug_merge_per_matrix: null argument");
+  if (ctx->merged) return fail(LSW_E_STATE, "lsw_debug_merge_per_matrix: the ctx is merged");
+  if (!ctx->tc) return fail(LSW_E_UNSUPPORTED, "lsw_debug_merge_per_matrix: needs the tensor-core switch");
+  SwitchParams p = ctx->simt_geom;
+  p.mode = MODE_MERGE;
+  p.cur_idx = idx;
+  p.cur_g = gate;
+  p.state = ctx->d_state;
+  for (int k = 0; k < LSW_NKIND; ++k)
+    for (int l = 0; l < ctx->cfg.n_layers; ++l) {
+      int64_t t0 = 0;
+      const int64_t n = tc_plan_matrix_tiles(ctx->tc, k, l, &t0);
+      cudaError_t e = launch_switch_tc(ctx->tc, p, (cudaStream_t)stream, t0, n);
+      if (e != cudaSuccess) return cuda_fail(e, "lsw_debug_merge_per_matrix: launch");
+      ++ctx->launches;
+    }
+  ctx->merged = true;
+  return LSW_OK;
+}
+
 lsw_status lsw_debug_switch_trace(lsw_ctx* ctx, uint64_t* host_out, int64_t n, int64_t* n_out) {
   if (!ctx || !host_out || !n_out) return fail(LSW_E_ARG, "lsw_debug_switch_trace: null argument");
   cudaDeviceSynchronize();

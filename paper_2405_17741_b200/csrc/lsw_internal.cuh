@@ -212,7 +212,10 @@ int64_t tc_plan_bytes(const TcPlan* plan);
 int tc_plan_grid(const TcPlan* plan);
 int tc_plan_tile_n(const TcPlan* plan);
 int64_t tc_plan_tiles(const TcPlan* plan);
-cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
+// t_count > 0: only tiles [t0, t0 + t_count) (the launch-count ablation)
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0 = 0,
+                             int64_t t_count = 0);
+int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t0);   // tiles of one matrix
 int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);   // tuning trace (lsw_debug.h)
 int tc_plan_kernel(const TcPlan* plan);   // 1: v1 (switch_tc.cu), 2: term groups (switch_tc_tg.cu)
 // RESTORE source: encode tensor maps over geom.kind[k].P (lsw_attach_pristine)

@@ -50,8 +50,12 @@ int tc_plan_tile_n(const TcPlan* p) { return p->a ? v1::tc_plan_tile_n(p->a) : t
 int64_t tc_plan_tiles(const TcPlan* p) { return p->a ? v1::tc_plan_tiles(p->a) : tg::tc_plan_tiles(p->b); }
 int tc_plan_kernel(const TcPlan* p) { return p->a ? 1 : 2; }
 
-cudaError_t launch_switch_tc(const TcPlan* p, const SwitchParams& sp, cudaStream_t s) {
-  return p->a ? v1::launch_switch_tc(p->a, sp, s) : tg::launch_switch_tc(p->b, sp, s);
+cudaError_t launch_switch_tc(const TcPlan* p, const SwitchParams& sp, cudaStream_t s, int64_t t0, int64_t t_count) {
+  return p->a ? v1::launch_switch_tc(p->a, sp, s, t0, t_count) : tg::launch_switch_tc(p->b, sp, s, t0, t_count);
+}
+
+int64_t tc_plan_matrix_tiles(const TcPlan* p, int kind, int layer, int64_t* t0) {
+  return p->a ? v1::tc_plan_matrix_tiles(p->a, kind, layer, t0) : tg::tc_plan_matrix_tiles(p->b, kind, layer, t0);
 }
 
 cudaError_t tc_plan_set_pristine(TcPlan* p, const SwitchParams& geom) {

@@ -23,7 +23,9 @@ int64_t tc_plan_bytes(const TcPlan* plan);
 int tc_plan_grid(const TcPlan* plan);
 int tc_plan_tile_n(const TcPlan* plan);
 int64_t tc_plan_tiles(const TcPlan* plan);
-cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0 = 0,
+                             int64_t t_count = 0);
+int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t0);
 int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);
 cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
 }  // namespace v1
@@ -36,7 +38,9 @@ int64_t tc_plan_bytes(const TcPlan* plan);
 int tc_plan_grid(const TcPlan* plan);
 int tc_plan_tile_n(const TcPlan* plan);
 int64_t tc_plan_tiles(const TcPlan* plan);
-cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s);
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0 = 0,
+                             int64_t t_count = 0);
+int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t0);
 int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);
 cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
 }  // namespace tg

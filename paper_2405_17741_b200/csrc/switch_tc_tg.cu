@@ -275,7 +275,8 @@ struct Cursor {
 };
 
 struct TileSeq {
-  int64_t T, t_begin, t_end;
+  int64_t T, t_begin, t_end;   // T tiles of this launch, starting at global tile t0
+  int64_t t0;
   int32_t order, chunk, G, b;
 };
 
@@ -298,15 +299,15 @@ __device__ __forceinline__ Cursor cursor_first(const TcGeom& g, const TileSeq& q
   Cursor c;
   int64_t t = q.order == ORDER_STRIP ? (q.t_begin < q.t_end ? q.t_begin : -1)
                                      : ((int64_t)q.b * q.chunk < q.T ? (int64_t)q.b * q.chunk : -1);
-  cursor_set(g, c, t);
+  cursor_set(g, c, t < 0 ? -1 : q.t0 + t);
   return c;
 }
 
 // Advance to the CTA's next tile: +1 inside a range/chunk (no division), a
 // jump (one division) between sweep chunks.
 __device__ __forceinline__ void cursor_next(const TcGeom& g, const TileSeq& q, Cursor& c) {
-  const int64_t t1 = c.t + 1;
-  const bool step = q.order == ORDER_STRIP ? (t1 < q.t_end) : (t1 % q.chunk != 0 && t1 < q.T);
+  const int64_t t1 = c.t + 1, r1 = t1 - q.t0;          // r: position within this launch's range
+  const bool step = q.order == ORDER_STRIP ? (r1 < q.t_end) : (r1 % q.chunk != 0 && r1 < q.T);
   if (step) {
     c.t = t1;
     if (++c.cb == g.kind[c.kd].col_tiles) {
@@ -319,8 +320,8 @@ __device__ __forceinline__ void cursor_next(const TcGeom& g, const TileSeq& q, C
     return;
   }
   if (q.order == ORDER_STRIP) { c.t = -1; return; }
-  const int64_t nq = c.t / q.chunk + q.G;
-  cursor_set(g, c, nq * q.chunk < q.T ? nq * q.chunk : -1);
+  const int64_t nq = (c.t - q.t0) / q.chunk + q.G;
+  cursor_set(g, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
 }
 
 __device__ __forceinline__ int64_t strip_id(const Cursor& c) { return c.t - c.cb; }
@@ -528,6 +529,7 @@ struct TcArgs {
   const int32_t* cur_idx;
   const float* cur_g;
   DevState* state;
+  int64_t t0, t_count;        // tile range of this launch (t_count = 0: all tiles)
 };
 
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -600,7 +602,8 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
   const bool skip_math = args.probe == 2;
   const int nsub = g.nsub;
   TileSeq seq;
-  seq.T = g.tiles_total;
+  seq.T = args.t_count > 0 ? args.t_count : g.tiles_total;   // ablation: one matrix per launch
+  seq.t0 = args.t0;
   seq.order = args.order;
   seq.chunk = args.chunk < 1 ? 1 : args.chunk;
   seq.G = gridDim.x;
@@ -1057,8 +1060,18 @@ cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& sp) {
   return cudaSuccess;
 }
 
-cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s) {
+int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t0) {
+  const TcKind& k = plan->geom.kind[kind];
+  const int64_t per = (int64_t)k.row_tiles * k.col_tiles;
+  *t0 = k.tile_begin + (int64_t)layer * per;
+  return per;
+}
+
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0,
+                             int64_t t_count) {
   TcArgs a;
+  a.t0 = t0;
+  a.t_count = t_count;
   a.g = plan->geom;
   a.order = plan->order;
   a.chunk = plan->chunk;

@@ -116,3 +116,42 @@ def test_restore_state_machine():
     for kd in synth.KINDS:
         assert PT.allclose_frac_fail(_f64(W[kd]), _f64(P[kd])) == 0.0
     assert sw.device_status() == 0
+
+
+@pytest.mark.parametrize("name,kernel,grid", [("mini", "v1", None), ("mini", "tg", "3"), ("mini-r4k4", None, None)])
+def test_per_matrix_merge_ablation_is_bitwise_the_single_launch(monkeypatch, name, kernel, grid):
+    """SURVEY 8f #4 (launch-count ablation): the merge as one launch per matrix
+    (7 x L launches of the same kernel over that matrix's tiles) gives bitwise
+    the same weights as the single all-layer launch, and records the decision
+    (a fused switch afterwards is correct)."""
+    if kernel:
+        monkeypatch.setenv("LSW_TC_KERNEL", kernel)
+    if grid:
+        monkeypatch.setenv("LSW_TC_GRID", grid)
+    cfg = synth.get_config(name)
+    outs = []
+    for mode in ("single", "per_matrix"):
+        W, A, B, router = H.build_weights(cfg, "cuda")
+        sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+        X1 = synth.gen_x1(cfg, 2, "cuda")
+        idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
+        gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
+        sw.router_topk(X1[0], idx, gate)
+        n0 = sw.info()["kernel_launches"]
+        if mode == "single":
+            sw.merge_all_layers(idx, gate)
+            assert sw.info()["kernel_launches"] - n0 == 1
+        else:
+            sw.debug_merge_per_matrix(idx, gate)
+            assert sw.info()["kernel_launches"] - n0 == 7 * cfg.n_layers
+            with pytest.raises(L.LswError):
+                sw.debug_merge_per_matrix(idx, gate)        # merged: refused
+        merged = {kd: W[kd].clone() for kd in synth.KINDS}
+        sw.router_topk(X1[1], idx, gate)
+        sw.merge_all_layers(idx, gate)                        # fused switch from the recorded decision
+        torch.cuda.synchronize()
+        assert sw.device_status() == 0
+        outs.append((merged, {kd: W[kd].clone() for kd in synth.KINDS}))
+    for kd in synth.KINDS:
+        assert torch.equal(outs[0][0][kd], outs[1][0][kd]), kd
+        assert torch.equal(outs[0][1][kd], outs[1][1][kd]), kd
