@@ -682,9 +682,11 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
     // 4 KB ops 2.6 TB/s ... 32 KB ops 7.3 TB/s): move R >= 1 rows per op, ~32 KB
     const uint32_t row_bytes = (uint32_t)(p.d_in * (bf16 ? 2 : 4));
     const uint32_t x_bytes = x_stage_bytes(row_bytes, bf16);
-    int R = (int)(32768 / row_bytes);
+    uint32_t op_bytes = 32768;                       // tuning: LSW_GEMV_OP_KB
+    if (const char* v = getenv("LSW_GEMV_OP_KB")) { long x = atol(v); if (x >= 4 && x <= 96) op_bytes = (uint32_t)x * 1024; }
+    int R = (int)(op_bytes / row_bytes);
     if (R < 1) R = 1;
-    if (R > 8) R = 8;
+    if (R > 16) R = 16;
     const size_t slot_bytes = (size_t)R * row_bytes;
     // Ring budget.  Measured (7B token of GEMVs): 220 KB 2.37 ms, 110 KB 2.59 ms,
     // 72 KB 3.49 ms -- a deep ring per SM beats letting the next GEMV's CTA

@@ -988,7 +988,9 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
         int ws = (int)((budget - (int64_t)bbufs * b_buf - (int64_t)astages * a_stage) / w_stage);
         if ((int64_t)budget < (int64_t)bbufs * b_buf + (int64_t)astages * a_stage) ws = 0;
         if (ws > kTcMaxStages) ws = kTcMaxStages;
-        const int min_ws = nsub == 2 ? 4 : 2;
+        int min_ws = nsub == 2 ? 4 : 2;
+        if (split)
+          if (const char* v = getenv("LSW_TC_SPLIT_MINWS")) { int x = atoi(v); if (x >= 2 && x <= 4) min_ws = x; }
         if (ws >= min_ws) {
           ok = true;
           g.split = split;
