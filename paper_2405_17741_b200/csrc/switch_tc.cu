@@ -93,6 +93,7 @@ struct TcGeom {
                                           //    (hi+mid+lo == the fp32 product), ONE accumulator per tile
                                           //    (N = tile width), one MMA group per tile, 4 TMEM buffers;
                                           // 0: one accumulator per expert term, c_j applied in the epilogue
+  int32_t w4d;                            // 1: W moved by ONE 4-D TMA op per tile (LSW_TC_W4D)
   int32_t store_stg;                      // 1: epilogue writes W back with coalesced STG.128 (LSU);
                                           // 0: the store warp issues TMA bulk tensor stores
   uint32_t swz_mode;                      // UMMA layout type of the r-wide operands
@@ -186,6 +187,25 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t sr
   asm volatile(
       "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
       ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(src), "l"(policy)
+      : "memory");
+}
+
+// 4-D view [L, col block, d_out, 64] of W: ONE op moves a whole 128 x 128 tile
+// (both 64-column sub-tiles, in the same smem order as two 3-D boxes)
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3, uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int32_t c0, int32_t c1,
+                                             int32_t c2, int32_t c3, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], [%5], %6;"
+      ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(src), "l"(policy)
       : "memory");
 }
 
@@ -622,10 +642,13 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
           const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
           mbar_expect_tx(wbar, nsub * kSubBytes);
           uint8_t* wdst = wst0 + (size_t)wring.i * g.w_stage_bytes;
-          for (int sb = 0; sb < nsub; ++sb)
-            tma_load_3d(smem_u32(wdst + sb * kSubBytes), restore ? &maps.p[c.kd] : &maps.w[c.kd],
-                        c.cb * tile_cols + sb * kTcTN,
-                        c.rb * kTcTM, c.layer, wbar, pol_stream);
+          if (g.w4d)
+            tma_load_4d(smem_u32(wdst), restore ? &maps.p[c.kd] : &maps.w[c.kd], 0, c.rb * kTcTM, c.cb * nsub,
+                        c.layer, wbar, pol_stream);
+          else
+            for (int sb = 0; sb < nsub; ++sb)
+              tma_load_3d(smem_u32(wdst + sb * kSubBytes), restore ? &maps.p[c.kd] : &maps.w[c.kd],
+                          c.cb * tile_cols + sb * kTcTN, c.rb * kTcTM, c.layer, wbar, pol_stream);
           trace_ev(args.trace, it, EV_W_ISSUED);
           wring.next();
         }
@@ -815,9 +838,12 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
         for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
           mbar_wait(smem_u32(&bar_wdone[wring.i]), wring.phase);     // epilogue wrote the tile
           uint8_t* wsrc = wst0 + (size_t)wring.i * g.w_stage_bytes;
-          for (int sb = 0; sb < nsub; ++sb)
-            tma_store_3d(&maps.w[c.kd], smem_u32(wsrc + sb * kSubBytes), c.cb * tile_cols + sb * kTcTN,
-                         c.rb * kTcTM, c.layer, pol_stream);
+          if (g.w4d)
+            tma_store_4d(&maps.w[c.kd], smem_u32(wsrc), 0, c.rb * kTcTM, c.cb * nsub, c.layer, pol_stream);
+          else
+            for (int sb = 0; sb < nsub; ++sb)
+              tma_store_3d(&maps.w[c.kd], smem_u32(wsrc + sb * kSubBytes), c.cb * tile_cols + sb * kTcTN,
+                           c.rb * kTcTM, c.layer, pol_stream);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read -> stage reusable
           mbar_arrive(smem_u32(&bar_wempty[wring.i]));
@@ -916,6 +942,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }
   return fn;
+}
+
+// 4-D view (w4d): dims {64, d_out, d_in / 64, L}, box {64, 128, nsub, 1} -- one
+// TMA op per W tile.  Needs d_in % 64 == 0.
+static bool encode_w4(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d_out, uint64_t L, int nsub) {
+  auto enc = get_encode();
+  if (!enc || d_in % 64) return false;
+  cuuint64_t dims[4] = {64, d_out, d_in / 64, L};
+  cuuint64_t strides[3] = {d_in * 2, 128, d_in * d_out * 2};
+  cuuint32_t box[4] = {(cuuint32_t)kTcTN, (cuuint32_t)kTcTM, (cuuint32_t)nsub, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 static bool encode_w(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d_out, uint64_t L) {
@@ -1027,6 +1068,10 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     if (cudaMalloc(&plan->trace, tb) == cudaSuccess) cudaMemset(plan->trace, 0, tb);
     else plan->trace = nullptr;
   }
+  g.w4d = 0;
+  if (const char* v = getenv("LSW_TC_W4D")) g.w4d = atoi(v) != 0;
+  for (int k = 0; k < LSW_NKIND; ++k) if (sp.kind[k].d_in % 64) g.w4d = 0;
+  if (g.nsub != 2 || g.split) g.w4d = 0;
   g.store_stg = 0;                                       // measured: TMA store 4466 vs STG 4222 GB/s
   if (const char* v = getenv("LSW_TC_STORE")) g.store_stg = strcmp(v, "stg") == 0;
   // tuning probe (W stream only): all of shared memory as W stages
@@ -1073,7 +1118,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     g.kind[k].W = (__nv_bfloat16*)kg.W;
     g.kind[k].d_out = kg.d_out;
     g.kind[k].d_in = kg.d_in;
-    if (!encode_w(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers)) {
+    if (!(g.w4d ? encode_w4(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers, g.nsub)
+                : encode_w(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers))) {
       *why = "cuTensorMapEncodeTiled failed";
       e = cudaErrorInvalidValue;
     }
@@ -1117,7 +1163,9 @@ int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n) {
 cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& sp) {
   for (int k = 0; k < LSW_NKIND; ++k)
     if (!sp.kind[k].P ||
-        !encode_w(&plan->maps.p[k], sp.kind[k].P, sp.kind[k].d_in, sp.kind[k].d_out, sp.n_layers))
+        !(plan->geom.w4d ? encode_w4(&plan->maps.p[k], sp.kind[k].P, sp.kind[k].d_in, sp.kind[k].d_out, sp.n_layers,
+                                     plan->geom.nsub)
+                         : encode_w(&plan->maps.p[k], sp.kind[k].P, sp.kind[k].d_in, sp.kind[k].d_out, sp.n_layers)))
       return cudaErrorInvalidValue;
   return cudaSuccess;
 }
