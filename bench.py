@@ -383,6 +383,18 @@ def run_ours(args, cfg):
         um_only = _time(lambda: (sw.merge_all_layers(idx, gate, stream), sw.unmerge_all_layers(stream)))
         abl["single_eager_merge_plus_unmerge_ms"] = um_only
 
+    # fused switch + decode: router + ONE launch that switches and
+    # computes the GEMVs in decoder order (4 B/element, 4L segment barriers)
+    fu_ms = []
+    if world == 1 and info["switch_impl"] == "tc" and info.get("switch_kernel") == 1:
+        for t in range(min(args.steps, 10)):
+            a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            a.record(stream)
+            sw.decode_token_fused(X1[t], xs, ys, idx, gate, stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            fu_ms.append(a.elapsed_time(b))
+
     # unmerged decode (the honest comparison): router + Eq. 2 on the
     # pristine weights, W read once (2 B/element) instead of switched and read (6)
     un_ms = []
@@ -457,6 +469,7 @@ def run_ours(args, cfg):
             "restore_ms": statistics.median(rs_ms) if rs_ms else None,
             "restore_GBps": tb["merge"] / (statistics.median(rs_ms) * 1e-3) / 1e9 if rs_ms else None,
             "launch_ablation": abl,
+            "fused_decode_ms_per_token": statistics.median(fu_ms) if fu_ms else None,
             "unmerged_decode_ms_per_token": statistics.median(un_ms) if un_ms else None,
             "unmerged_decode_GBps": (tb["unmerged_token"] / (statistics.median(un_ms) * 1e-3) / 1e9
                                      if un_ms else None),

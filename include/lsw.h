@@ -281,6 +281,22 @@ LSW_API lsw_status lsw_decode_all_layers_unmerged(lsw_ctx* ctx, const void* xs, 
 LSW_API lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs, float* ys,
                             int32_t* idx, float* gate, void* stream);
 
+/*
+ * Fused switch + decode: the same token as lsw_decode_token --
+ * router, then every adapted matrix of every layer switched in ONE launch --
+ * but the switch kernel also computes the group GEMVs from the freshly
+ * rounded weight tiles, so W is read once and written once per token (4
+ * B/element instead of 6).  Tiles are walked in decoder order, one segment per
+ * (layer, group); a segment's outputs are accumulated only after every tile of
+ * the previous segment is done (y final), as a decoder needs.  W ends exactly
+ * as after lsw_merge_all_layers (bitwise); ys equals lsw_decode_all_layers on
+ * those weights up to fp32 summation order (atomic accumulation, not bitwise
+ * reproducible).  Layouts as lsw_decode_token.  LSW_E_UNSUPPORTED unless the
+ * ctx uses the per-term tensor-core kernel (2k <= 4 terms, tp_size == 1).
+ */
+LSW_API lsw_status lsw_decode_token_fused(lsw_ctx* ctx, const void* x1, const void* xs, float* ys, int32_t* idx,
+                                          float* gate, void* stream);
+
 /* Same as lsw_decode_token from HOST buffers: copies x1_h, xs_h to ctx-owned
  * device staging, runs the token, copies ys/idx/gate back and synchronizes
  * `stream`.  Host buffers should be pinned for asynchronous copies. */

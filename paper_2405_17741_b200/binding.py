@@ -33,7 +33,7 @@ SYMBOLS = (
     "lsw_abi_version", "lsw_last_error", "lsw_create", "lsw_destroy", "lsw_get_info",
     "lsw_nccl_get_unique_id", "lsw_attach_nccl", "lsw_router_topk", "lsw_merge_all_layers",
     "lsw_unmerge_all_layers", "lsw_attach_pristine", "lsw_restore_merge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers",
-    "lsw_decode_group_unmerged", "lsw_decode_all_layers_unmerged", "lsw_decode_token",
+    "lsw_decode_group_unmerged", "lsw_decode_all_layers_unmerged", "lsw_decode_token", "lsw_decode_token_fused",
     "lsw_decode_token_host", "lsw_device_status",
     "lsw_debug_switch_trace", "lsw_debug_merge_per_matrix",   # include/lsw_debug.h
 )
@@ -93,6 +93,7 @@ def load_library(path: str = LIB_PATH, strict: bool = True) -> ctypes.CDLL:
         "lsw_decode_group_unmerged": (i32, [vp, i32, i32, vp, vp, vp, vp, vp]),
         "lsw_decode_all_layers_unmerged": (i32, [vp, vp, vp, vp, vp, vp]),
         "lsw_decode_token": (i32, [vp, vp, vp, vp, vp, vp, vp]),
+        "lsw_decode_token_fused": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_decode_token_host": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_device_status": (i32, [vp, vp, ctypes.POINTER(i32)]),
         "lsw_debug_switch_trace": (i32, [vp, vp, i64, ctypes.POINTER(i64)]),
@@ -239,6 +240,11 @@ class LoraSwitch:
     def decode_token(self, x1, xs, ys, idx, gate, stream=None):
         _check(lib().lsw_decode_token(self._h, _ptr(x1), _ptr(xs), _ptr(ys), _ptr(idx), _ptr(gate),
                                       _stream(stream)))
+
+    def decode_token_fused(self, x1, xs, ys, idx, gate, stream=None):
+        """The token with the switch and the GEMVs fused in one launch (4 B/element)."""
+        _check(lib().lsw_decode_token_fused(self._h, _ptr(x1), _ptr(xs), _ptr(ys), _ptr(idx), _ptr(gate),
+                                            _stream(stream)))
 
     def decode_token_host(self, x1_h, xs_h, ys_h, idx_h, gate_h, stream=None):
         _check(lib().lsw_decode_token_host(self._h, _ptr(x1_h), _ptr(xs_h), _ptr(ys_h), _ptr(idx_h),

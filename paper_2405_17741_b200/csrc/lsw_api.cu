@@ -60,6 +60,7 @@ struct lsw_ctx {
   TokPlan tok{};                        // whole-token GEMV (tp_size == 1), else empty
   bool has_pristine = false;            // lsw_attach_pristine called (RESTORE mode available)
   float* lora_u = nullptr;              // unmerged decode: LoRA-down products scratch
+  bool fused_ready = false;             // fused switch + decode segment table built
   unsigned long long tok_base = 0;      // DevState::tok_done before the next token launch
   // staging for lsw_decode_token_host
   void* st_x1 = nullptr;
@@ -487,6 +488,39 @@ lsw_status lsw_decode_all_layers(lsw_ctx* ctx, const void* xs, float* ys, void* 
                                  "lsw_decode_all_layers", /*early_w=*/l > 0 || g > 0);
       if (st != LSW_OK) return st;
     }
+  return LSW_OK;
+}
+
+lsw_status lsw_decode_token_fused(lsw_ctx* ctx, const void* x1, const void* xs, float* ys, int32_t* idx,
+                                  float* gate, void* stream) {
+  if (!ctx || !x1 || !xs || !ys || !idx || !gate) return fail(LSW_E_ARG, "lsw_decode_token_fused: null argument");
+  if (reinterpret_cast<uintptr_t>(xs) % 16) return fail(LSW_E_ARG, "lsw_decode_token_fused: xs not 16-byte aligned");
+  if (!ctx->tc || ctx->cfg.tp_size != 1)
+    return fail(LSW_E_UNSUPPORTED, "lsw_decode_token_fused: needs the tensor-core switch and tp_size == 1");
+  if (!ctx->fused_ready) {
+    int nk[LSW_NGROUP];
+    for (int g = 0; g < LSW_NGROUP; ++g) nk[g] = kGroupSize[g];
+    cudaError_t e = tc_plan_set_fused(ctx->tc, ctx->cfg.n_layers, ctx->x_off, ctx->y_off, ctx->x_per_layer,
+                                      ctx->y_per_layer, kGroupKinds, nk);
+    if (e == cudaErrorNotSupported)
+      return fail(LSW_E_UNSUPPORTED, "lsw_decode_token_fused: this rank / top-k uses the term-group kernel");
+    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_fused: segment table");
+    ctx->fused_ready = true;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  lsw_status st = lsw_router_topk(ctx, x1, idx, gate, stream);                       // Alg. 1 l.1
+  if (st != LSW_OK) return st;
+  cudaError_t e = cudaMemsetAsync(ys, 0, ctx->ys_elems * sizeof(float), s);         // accumulated
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_fused: memset");
+  SwitchParams p = ctx->simt_geom;
+  p.mode = ctx->merged ? MODE_SWITCH : MODE_MERGE;                                   // l.2-5, one launch
+  p.cur_idx = idx;
+  p.cur_g = gate;
+  p.state = ctx->d_state;
+  e = launch_switch_tc_fused(ctx->tc, p, s, xs, ys);
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_fused: launch");
+  ++ctx->launches;
+  ctx->merged = true;
   return LSW_OK;
 }
 

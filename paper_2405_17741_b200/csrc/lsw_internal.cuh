@@ -216,6 +216,11 @@ int64_t tc_plan_tiles(const TcPlan* plan);
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0 = 0,
                              int64_t t_count = 0);
 int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t0);   // tiles of one matrix
+// Fused switch + decode (v1 kernel only, else cudaErrorNotSupported)
+cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
+                              int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]);
+cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, const void* xs,
+                                   float* ys);
 int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);   // tuning trace (lsw_debug.h)
 int tc_plan_kernel(const TcPlan* plan);   // 1: v1 (switch_tc.cu), 2: term groups (switch_tc_tg.cu)
 // RESTORE source: encode tensor maps over geom.kind[k].P (lsw_attach_pristine)

@@ -100,9 +100,26 @@ struct TcGeom {
   uint32_t smem_bytes;
 };
 
+// Fused switch + decode: tiles walked in decoder order, one
+// segment per (layer, GEMV group); every tile's freshly rounded W also feeds
+// y_seg += W_tile x_seg in the epilogue.  Segment s's epilogue work starts only
+// after every tile of segment s-1 is done (its y final), as a decoder needs.
+struct FusedSeg {
+  int64_t tile_begin, tile_count;   // fused-order tiles of this segment
+  int32_t layer, n_kinds;
+  int32_t kinds[3];                 // kind ids in group order
+  int32_t pad;
+  int64_t x_off;                    // elements into xs of this segment's input
+  int64_t y_off[3];                 // elements into ys of each kind's row 0
+};
+
 struct TcPlan {
   TcMaps maps;
   TcGeom geom;
+  FusedSeg* d_segs = nullptr;       // fused mode: device table (tc_plan_set_fused)
+  int32_t n_segs = 0;
+  int64_t fused_tiles = 0;
+  unsigned long long* d_seg_done = nullptr;
   // Tile order (measured, 7B shape, same run): strip 4.60-4.67 TB/s, sweep with
   // 32-tile chunks 5.02-5.03 TB/s.  With strip order the 148 CTAs work on ~148
   // different matrices, so the per-tile A^T slices (re-read once per row strip)
@@ -292,13 +309,57 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
 struct Cursor {
   int64_t t;             // global tile index, -1 when done
   int32_t kd, layer, rb, cb;
+  int32_t seg, kidx;     // fused order: segment and kind index within its group
 };
 
 struct TileSeq {
   int64_t T, t_begin, t_end;   // T tiles of this launch, starting at global tile t0
   int64_t t0;
   int32_t order, chunk, G, b;
+  const FusedSeg* segs;        // non-null: fused (decoder) tile order
+  int32_t n_seg;
 };
+
+// fused order: segment (binary search), then kind within the group, rb, cb
+__device__ __forceinline__ void cursor_set_fused(const TcGeom& g, const TileSeq& q, Cursor& c, int64_t t) {
+  c.t = t;
+  if (t < 0) return;
+  int lo = 0, hi = q.n_seg - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (q.segs[mid].tile_begin <= t) lo = mid; else hi = mid - 1;
+  }
+  const FusedSeg& S = q.segs[lo];
+  int64_t off = t - S.tile_begin;
+  int ki = 0, kd = S.kinds[0];
+  for (; ki < S.n_kinds; ++ki) {
+    kd = S.kinds[ki];
+    const int64_t per = (int64_t)g.kind[kd].row_tiles * g.kind[kd].col_tiles;
+    if (off < per) break;
+    off -= per;
+  }
+  c.seg = lo;
+  c.kidx = ki;
+  c.kd = kd;
+  c.layer = S.layer;
+  c.rb = (int)(off / g.kind[kd].col_tiles);
+  c.cb = (int)(off - (int64_t)c.rb * g.kind[kd].col_tiles);
+}
+
+__device__ __forceinline__ void cursor_step_fused(const TcGeom& g, const TileSeq& q, Cursor& c) {
+  if (++c.cb == g.kind[c.kd].col_tiles) {
+    c.cb = 0;
+    if (++c.rb == g.kind[c.kd].row_tiles) {
+      c.rb = 0;
+      if (++c.kidx == q.segs[c.seg].n_kinds) {
+        c.kidx = 0;
+        ++c.seg;
+        c.layer = q.segs[c.seg].layer;
+      }
+      c.kd = q.segs[c.seg].kinds[c.kidx];
+    }
+  }
+}
 
 __device__ __forceinline__ void cursor_set(const TcGeom& g, Cursor& c, int64_t t) {
   c.t = t;
@@ -319,7 +380,8 @@ __device__ __forceinline__ Cursor cursor_first(const TcGeom& g, const TileSeq& q
   Cursor c;
   int64_t t = q.order == ORDER_STRIP ? (q.t_begin < q.t_end ? q.t_begin : -1)
                                      : ((int64_t)q.b * q.chunk < q.T ? (int64_t)q.b * q.chunk : -1);
-  cursor_set(g, c, t < 0 ? -1 : q.t0 + t);
+  if (q.segs) cursor_set_fused(g, q, c, t < 0 ? -1 : q.t0 + t);
+  else cursor_set(g, c, t < 0 ? -1 : q.t0 + t);
   return c;
 }
 
@@ -328,6 +390,11 @@ __device__ __forceinline__ Cursor cursor_first(const TcGeom& g, const TileSeq& q
 __device__ __forceinline__ void cursor_next(const TcGeom& g, const TileSeq& q, Cursor& c) {
   const int64_t t1 = c.t + 1, r1 = t1 - q.t0;          // r: position within this launch's range
   const bool step = q.order == ORDER_STRIP ? (r1 < q.t_end) : (r1 % q.chunk != 0 && r1 < q.T);
+  if (step && q.segs) {
+    c.t = t1;
+    cursor_step_fused(g, q, c);
+    return;
+  }
   if (step) {
     c.t = t1;
     if (++c.cb == g.kind[c.kd].col_tiles) {
@@ -341,7 +408,8 @@ __device__ __forceinline__ void cursor_next(const TcGeom& g, const TileSeq& q, C
   }
   if (q.order == ORDER_STRIP) { c.t = -1; return; }
   const int64_t nq = (c.t - q.t0) / q.chunk + q.G;
-  cursor_set(g, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
+  if (q.segs) cursor_set_fused(g, q, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
+  else cursor_set(g, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
 }
 
 __device__ __forceinline__ int64_t strip_id(const Cursor& c) { return c.t - c.cb; }
@@ -374,8 +442,9 @@ __device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t v) {
 // One 16-column chunk of one row: W (two swizzled 16-B smem chunks) <-
 // RNE(W + sum_j c_j acc_j), with the sum in fp32 pairs (FFMA2), W as the first
 // addend.  NT = number of accumulators (compile-time).
-template <int NT>
-__device__ __forceinline__ void epi_chunk(uint32_t tm_addr, const uint64_t* c2, uint8_t* wrow, int row, int col16) {
+template <int NT, bool FUSED = false>
+__device__ __forceinline__ void epi_chunk(uint32_t tm_addr, const uint64_t* c2, uint8_t* wrow, int row, int col16,
+                                          const uint4* x16 = nullptr, float* ydot = nullptr) {
   uint32_t acc[NT][16];
 #pragma unroll
   for (int j = 0; j < NT; ++j) tmem_ld16(tm_addr + j * kTcTN, acc[j]);
@@ -395,6 +464,18 @@ __device__ __forceinline__ void epi_chunk(uint32_t tm_addr, const uint64_t* c2, 
   }
   *p0 = make_uint4(o[0], o[1], o[2], o[3]);
   *p1 = make_uint4(o[4], o[5], o[6], o[7]);
+  if constexpr (FUSED) {
+    // the GEMV on the stored (rounded) weights: 16 columns of this row x x
+    const uint32_t xw[8] = {x16[0].x, x16[0].y, x16[0].z, x16[0].w, x16[1].x, x16[1].y, x16[1].z, x16[1].w};
+    uint64_t a = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      a = ffma2(f2_pack(__uint_as_float(o[q] << 16), __uint_as_float(o[q] & 0xffff0000u)),
+                f2_pack(__uint_as_float(xw[q] << 16), __uint_as_float(xw[q] & 0xffff0000u)), a);
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+    *ydot += lo + hi;
+  }
 }
 
 // General term count (> 4): groups of 4 accumulators.
@@ -432,6 +513,25 @@ __device__ __forceinline__ void epi_chunk_many(uint32_t tm_addr, const float* cs
 
 // ------------------------------------------------------------------ epilogue loop
 
+struct TcArgs {
+  TcGeom g;
+  int32_t order, chunk, probe;
+  uint64_t* trace;            // tuning: per-tile event timestamps of CTAs 0,1 (LSW_TC_TRACE), or null
+  // coefficient inputs (same as SwitchParams)
+  int32_t mode, top_k, n_experts;
+  float scale;
+  const int32_t* cur_idx;
+  const float* cur_g;
+  DevState* state;
+  int64_t t0, t_count;        // tile range of this launch (t_count = 0: all tiles)
+  // fused switch + decode (null segs: plain switch)
+  const FusedSeg* segs;
+  int32_t n_seg;
+  const __nv_bfloat16* xs;    // packed GEMV inputs (lsw_decode_token layout)
+  float* ys;                  // packed outputs, zeroed before the launch (accumulated)
+  unsigned long long* seg_done;   // [n_seg], zeroed before the launch
+};
+
 struct EpiCtx {
   const TcGeom& g;
   uint8_t* wst0;
@@ -445,12 +545,29 @@ struct EpiCtx {
   uint64_t* bar_accfull;
   uint64_t* bar_accempty;
   uint64_t* trace;
+  const TcArgs* args;          // fused switch + decode: segs, xs, ys, seg_done
 };
 
+// Spin (with a ~20 s watchdog) until a device-wide counter reaches target.
+__device__ __forceinline__ void wait_count(const unsigned long long* p, unsigned long long target) {
+  auto load = [&]() {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+  };
+  if (load() >= target) return;
+  const uint64_t t0 = globaltimer();
+  for (uint32_t n = 1; load() < target; ++n) {
+    __nanosleep(64);
+    if ((n & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) __trap();
+  }
+}
+
 // The epilogue warps' tile loop, specialised on the term count (NT = -1: any;
-// NT = kSplitNT: split mode, one pre-scaled accumulator per tile).
+// NT = kSplitNT: split mode, one pre-scaled accumulator per tile).  FUSED:
+// also y += W_new x for the tile (fused switch + decode, decoder order).
 constexpr int kSplitNT = 100;
-template <int NT>
+template <int NT, bool FUSED = false>
 __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& seq, const Coefs& cf) {
   constexpr bool SPLIT = NT == kSplitNT;
   const TcGeom& g = e.g;
@@ -470,11 +587,52 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
   Ring acc{0, 0, (uint32_t)g.acc_bufs};
   uint64_t* tr = (ew == 0 && e.lane == 0) ? e.trace : nullptr;
   uint32_t it = 0;
+  int cur_seg = -1;
+  int64_t seg_mine = 0;                        // FUSED: tiles of cur_seg this CTA finished
+  const bool leader = ew == 0 && e.lane == 0;
   for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
+    float ydot = 0.f;                          // FUSED: this thread's part of y[row] for the tile
+    const __nv_bfloat16* xt = nullptr;
+    int64_t x_lim = 0;
+    if constexpr (FUSED) {
+      const TcArgs& A = *e.args;
+      if (c.seg != cur_seg) {
+        // decoder order: x of segment s is final only once every tile of
+        // segment s-1 is done.  One thread per CTA publishes the CTA's count of
+        // the segment it leaves (after all 8 epilogue warps issued their y
+        // atomics) and waits for the previous segment's total (one counter
+        // update per CTA and segment, not per tile: a single hot address)
+        named_bar(3, 32 * kTcEpiWarps);
+        if (leader) {
+          if (cur_seg >= 0) {
+            __threadfence();
+            asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(A.seg_done + cur_seg),
+                         "l"((unsigned long long)seg_mine) : "memory");
+          }
+          if (c.seg > 0) wait_count(&A.seg_done[c.seg - 1], (unsigned long long)A.segs[c.seg - 1].tile_count);
+        }
+        named_bar(3, 32 * kTcEpiWarps);
+        cur_seg = c.seg;
+        seg_mine = 0;
+      }
+      const int64_t col0 = (int64_t)c.cb * kTcTN * g.nsub;
+      xt = A.xs + A.segs[c.seg].x_off + col0;
+      x_lim = g.kind[c.kd].d_in - col0;        // columns of this tile inside d_in
+    }
     mbar_wait(smem_u32(&e.bar_wfull[wring.i]), wring.phase);            // W tile landed (acquire)
     trace_ev(tr, it, EV_EPI_WFULL);
     uint8_t* wt = e.wst0 + (size_t)wring.i * g.w_stage_bytes;
     for (int sb = 0; sb < g.nsub; ++sb) {
+      uint4 xq[2][2];
+      if constexpr (FUSED) {
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cl = sb * kTcTN + (half * 2 + q2) * 16 + h * 8;   // 8 columns (16 B) of x
+            xq[q2][h] = cl < x_lim ? *reinterpret_cast<const uint4*>(xt + cl) : make_uint4(0, 0, 0, 0);
+          }
+      }
       if (!e.probe && (!SPLIT || sb == 0))
         mbar_wait(smem_u32(&e.bar_accfull[acc.i]), acc.phase);          // accumulators ready
       if (sb == 0) trace_ev(tr, it, EV_EPI_ACC0);
@@ -487,6 +645,7 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
         const int col16 = half * 2 + q2;       // 16-column chunk 0..3 of the sub-tile
         const uint32_t ta = tm_row + col16 * 16;
         if constexpr (SPLIT) { if (!e.skip_math) epi_chunk<1>(ta, c2, wrow, row, col16); }
+        else if constexpr (FUSED) epi_chunk<NT, true>(ta, c2, wrow, row, col16, xq[q2], &ydot);
         else if constexpr (NT > 0) epi_chunk<NT>(ta, c2, wrow, row, col16);
         else if constexpr (NT < 0) epi_chunk_many(ta, cf.c, nt, wrow, row, col16);
       }
@@ -528,25 +687,29 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
       __syncwarp();
       if (e.lane == 0) mbar_arrive(smem_u32(&e.bar_wdone[wring.i]));
     }
+    if constexpr (FUSED) {
+      const TcArgs& A = *e.args;
+      const int64_t grow = (int64_t)c.rb * kTcTM + row;
+      if (grow < g.kind[c.kd].d_out) atomicAdd(A.ys + A.segs[c.seg].y_off[c.kidx] + grow, ydot);
+      ++seg_mine;
+    }
     trace_ev(tr, it, EV_EPI_DONE);
     wring.next();
+  }
+  if constexpr (FUSED) {
+    if (cur_seg >= 0) {                        // publish the last segment this CTA worked on
+      named_bar(3, 32 * kTcEpiWarps);
+      if (leader) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(e.args->seg_done + cur_seg),
+                     "l"((unsigned long long)seg_mine) : "memory");
+      }
+    }
   }
 }
 
 // ------------------------------------------------------------------ the kernel
 
-struct TcArgs {
-  TcGeom g;
-  int32_t order, chunk, probe;
-  uint64_t* trace;            // tuning: per-tile event timestamps of CTAs 0,1 (LSW_TC_TRACE), or null
-  // coefficient inputs (same as SwitchParams)
-  int32_t mode, top_k, n_experts;
-  float scale;
-  const int32_t* cur_idx;
-  const float* cur_g;
-  DevState* state;
-  int64_t t0, t_count;        // tile range of this launch (t_count = 0: all tiles)
-};
 
 __global__ void __launch_bounds__(kTcThreads, 1)
 switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ TcArgs args) {
@@ -626,6 +789,8 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
   seq.b = blockIdx.x;
   seq.t_begin = seq.T * blockIdx.x / gridDim.x;
   seq.t_end = seq.T * (blockIdx.x + 1) / gridDim.x;
+  seq.segs = args.segs;
+  seq.n_seg = args.n_seg;
   const uint32_t tmem_base = s_tmem_base;
   const int tile_cols = kTcTN * nsub;
 
@@ -856,10 +1021,18 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
       // ============================ epilogue ================================
       const int ntc = (probe || skip_math) ? 0 : nt;
       EpiCtx ec{g, wst0, tmem_base, warp, lane, probe, skip_math, bar_wfull, bar_wdone, bar_wempty, bar_accfull,
-                bar_accempty,
-                args.trace};
+                bar_accempty, args.trace, &args};
       // split mode always runs the split loop (its TMEM buffer protocol differs);
       // with probe/skip_math it only skips the math
+      const bool fused = args.segs != nullptr && !probe && !skip_math && !g.split;
+      if (fused) {
+        switch (ntc) {
+          case 1: epilogue_loop<1, true>(ec, seq, cf); break;
+          case 2: epilogue_loop<2, true>(ec, seq, cf); break;
+          case 3: epilogue_loop<3, true>(ec, seq, cf); break;
+          default: epilogue_loop<4, true>(ec, seq, cf); break;   // host allows fused only for 2k <= 4
+        }
+      } else
       switch (g.split && nt > 0 && !probe ? kSplitNT : ntc) {
         case kSplitNT: epilogue_loop<kSplitNT>(ec, seq, cf); break;
         case 0: epilogue_loop<0>(ec, seq, cf); break;
@@ -1139,6 +1312,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
 
 void tc_plan_destroy(TcPlan* plan) {
   if (!plan) return;
+  cudaFree(plan->d_segs);
+  cudaFree(plan->d_seg_done);
   for (int k = 0; k < LSW_NKIND; ++k) {
     cudaFree(plan->packed_At[k]);
     cudaFree(plan->packed_B[k]);
@@ -1177,9 +1352,82 @@ int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t
   return per;
 }
 
+cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
+                              int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]) {
+  const TcGeom& g = plan->geom;
+  if (g.split || g.max_terms > 4) return cudaErrorNotSupported;
+  const int n = 4 * n_layers;
+  FusedSeg* h = new FusedSeg[n];
+  int64_t t = 0;
+  for (int l = 0; l < n_layers; ++l)
+    for (int gi = 0; gi < 4; ++gi) {
+      FusedSeg& S = h[l * 4 + gi];
+      memset(&S, 0, sizeof(S));
+      S.tile_begin = t;
+      S.layer = l;
+      S.n_kinds = nk[gi];
+      S.x_off = l * x_per_layer + x_off[gi];
+      int64_t yo = l * y_per_layer + y_off[gi];
+      for (int i = 0; i < nk[gi]; ++i) {
+        const int kd = kinds[gi][i];
+        S.kinds[i] = kd;
+        S.y_off[i] = yo;
+        yo += g.kind[kd].d_out;
+        S.tile_count += (int64_t)g.kind[kd].row_tiles * g.kind[kd].col_tiles;
+      }
+      t += S.tile_count;
+    }
+  cudaError_t e = cudaSuccess;
+  if (!plan->d_segs) e = cudaMalloc(&plan->d_segs, sizeof(FusedSeg) * n);
+  if (e == cudaSuccess && !plan->d_seg_done) e = cudaMalloc(&plan->d_seg_done, sizeof(unsigned long long) * n);
+  if (e == cudaSuccess) e = cudaMemcpy(plan->d_segs, h, sizeof(FusedSeg) * n, cudaMemcpyHostToDevice);
+  delete[] h;
+  if (e != cudaSuccess) return e;
+  plan->n_segs = n;
+  plan->fused_tiles = t;
+  return cudaSuccess;
+}
+
+cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, const void* xs,
+                                   float* ys) {
+  if (!plan->d_segs) return cudaErrorNotSupported;
+  cudaError_t e = cudaMemsetAsync(plan->d_seg_done, 0, sizeof(unsigned long long) * plan->n_segs, s);
+  if (e != cudaSuccess) return e;
+  TcArgs a;
+  a.g = plan->geom;
+  a.order = ORDER_SWEEP;
+  // segment barriers: a CTA's share of one segment is a few tiles, so deal
+  // small chunks (large ones would leave most CTAs idle at every barrier)
+  a.chunk = 8;
+  if (const char* v = getenv("LSW_TC_FUSED_CHUNK")) { int x = atoi(v); if (x >= 1) a.chunk = x; }
+  a.probe = 0;
+  a.trace = plan->trace;
+  a.mode = p.mode;
+  a.top_k = p.top_k;
+  a.n_experts = p.n_experts;
+  a.scale = p.scale;
+  a.cur_idx = p.cur_idx;
+  a.cur_g = p.cur_g;
+  a.state = p.state;
+  a.t0 = 0;
+  a.t_count = plan->fused_tiles;
+  a.segs = plan->d_segs;
+  a.n_seg = plan->n_segs;
+  a.xs = (const __nv_bfloat16*)xs;
+  a.ys = ys;
+  a.seg_done = plan->d_seg_done;
+  switch_tc_kernel<<<plan->grid, kTcThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0,
                              int64_t t_count) {
   TcArgs a;
+  a.segs = nullptr;
+  a.n_seg = 0;
+  a.xs = nullptr;
+  a.ys = nullptr;
+  a.seg_done = nullptr;
   a.t0 = t0;
   a.t_count = t_count;
   a.g = plan->geom;

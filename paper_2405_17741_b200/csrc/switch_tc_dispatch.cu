@@ -62,6 +62,17 @@ cudaError_t tc_plan_set_pristine(TcPlan* p, const SwitchParams& geom) {
   return p->a ? v1::tc_plan_set_pristine(p->a, geom) : tg::tc_plan_set_pristine(p->b, geom);
 }
 
+cudaError_t tc_plan_set_fused(TcPlan* p, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
+                              int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]) {
+  if (!p->a) return cudaErrorNotSupported;          // the term-group kernel has no fused mode
+  return v1::tc_plan_set_fused(p->a, n_layers, x_off, y_off, x_per_layer, y_per_layer, kinds, nk);
+}
+
+cudaError_t launch_switch_tc_fused(const TcPlan* p, const SwitchParams& sp, cudaStream_t s, const void* xs, float* ys) {
+  if (!p->a) return cudaErrorNotSupported;
+  return v1::launch_switch_tc_fused(p->a, sp, s, xs, ys);
+}
+
 int64_t tc_plan_trace(const TcPlan* p, uint64_t* host, int64_t n) {
   return p->a ? v1::tc_plan_trace(p->a, host, n) : tg::tc_plan_trace(p->b, host, n);
 }

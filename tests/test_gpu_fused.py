@@ -1,0 +1,94 @@
+"""Fused switch + decode on the GPU (-m gpu).
+
+lsw_decode_token_fused runs the router and ONE launch that switches every
+adapted matrix and computes the group GEMVs from the freshly rounded tiles,
+in decoder order with a segment barrier per (layer, group).  Checked through
+the C ABI: the weights after every token are bitwise those of the separate
+path (lsw_decode_token: switch launch + GEMV launches), the outputs equal its
+outputs up to fp32 summation order, and the first token's outputs match the
+oracle's GEMV on the oracle's merged weights; small grids make every CTA
+cross many segment barriers.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from tests import parity as PT
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2405_17741_b200 as L
+    from paper_2405_17741_b200 import harness as H
+
+
+def _f64(t):
+    return t.detach().to("cpu").to(torch.float64).numpy()
+
+
+@pytest.mark.parametrize("name,grid", [("mini", None), ("mini", "3"), ("mini", "1"), ("mini-r32", None),
+                                       ("mini-k1", "5")])
+def test_fused_token_equals_separate_path(monkeypatch, name, grid):
+    monkeypatch.setenv("LSW_TC_KERNEL", "v1")
+    if grid:
+        monkeypatch.setenv("LSW_TC_GRID", grid)
+    cfg = synth.get_config(name)
+    ctxs = []
+    for _ in range(2):
+        W, A, B, router = H.build_weights(cfg, "cuda")
+        sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+        ctxs.append((sw, W, A, B))
+    info = ctxs[0][0].info()
+    assert info["switch_kernel"] == 1
+    X1 = synth.gen_x1(cfg, 5, "cuda")
+    xs_d = synth.gen_xs(cfg, "cuda")
+    xs = H.pack_xs(cfg, xs_d)
+    outs = [dict(ys=torch.empty(info["ys_elems"], device="cuda"),
+                 idx=torch.empty(cfg.top_k, dtype=torch.int32, device="cuda"),
+                 gate=torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")) for _ in range(2)]
+    P = {kd: _f64(ctxs[0][1][kd]) for kd in synth.KINDS}
+    for t in range(4):
+        (sa, Wa, Aa, Ba), (sb, Wb, _, _) = ctxs
+        oa, ob = outs
+        sa.decode_token(X1[t], xs, oa["ys"], oa["idx"], oa["gate"])
+        n0 = sb.info()["kernel_launches"]
+        sb.decode_token_fused(X1[t], xs, ob["ys"], ob["idx"], ob["gate"])
+        assert sb.info()["kernel_launches"] - n0 == 2          # router + the fused launch
+        torch.cuda.synchronize()
+        assert sa.device_status() == 0 and sb.device_status() == 0
+        assert torch.equal(oa["idx"], ob["idx"]) and torch.equal(oa["gate"], ob["gate"])
+        for kd in synth.KINDS:
+            assert torch.equal(Wa[kd], Wb[kd]), (t, kd)
+        ya, yb = oa["ys"].cpu().numpy(), ob["ys"].cpu().numpy()
+        np.testing.assert_allclose(yb, ya, rtol=1e-4, atol=1e-4 * float(np.abs(ya).max()))
+        if t == 0:
+            # first token: a plain merge; outputs vs the oracle's GEMV on its merged weights
+            cur = (ob["idx"].cpu().tolist(), ob["gate"].cpu().double().tolist())
+            scale = cfg.alpha / cfg.rank
+            yo = 0
+            for l in range(cfg.n_layers):
+                for gi, grp in enumerate(synth.GROUPS):
+                    x = _f64(xs_d[(l, gi)])
+                    for kd in grp:
+                        d_out = cfg.kind_shape(kd)[0]
+                        Wm = O.merge(P[kd][l], _f64(Aa[kd][l]), _f64(Ba[kd][l]), cur, scale, "bf16")
+                        ref = O.gemv(Wm, x)
+                        assert PT.allclose_frac_fail(yb[yo:yo + d_out], ref) == 0.0, (l, kd)
+                        yo += d_out
+
+
+def test_fused_unsupported_for_term_group_kernel(monkeypatch):
+    monkeypatch.setenv("LSW_TC_KERNEL", "tg")
+    cfg = synth.get_config("mini")
+    W, A, B, router = H.build_weights(cfg, "cuda")
+    sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+    info = sw.info()
+    xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
+    ys = torch.empty(info["ys_elems"], device="cuda")
+    idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
+    gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
+    with pytest.raises(L.LswError) as ei:
+        sw.decode_token_fused(synth.gen_x1(cfg, 1, "cuda")[0], xs, ys, idx, gate)
+    assert "UNSUPPORTED" in str(ei.value)
