@@ -47,8 +47,21 @@
 #include "lsw_internal.cuh"
 #include "switch_tc_impl.cuh"
 
+// This file is compiled twice: as lsw::v1 (the switch kernel) and, from
+// switch_tc_fused.cu with LSW_TC_FUSED=1, as lsw::v1f (the same kernel with the
+// fused switch + decode epilogue).  Keeping the fused code out of
+// the plain build leaves the switch kernel's code generation untouched
+// (measured: one binary with both epilogues made the switch 4-12 % slower).
+#ifndef LSW_TC_FUSED
+#define LSW_TC_FUSED 0
+#endif
+
 namespace lsw {
+#if LSW_TC_FUSED
+namespace v1f {
+#else
 namespace v1 {
+#endif
 
 constexpr int kTcTM = 128;                 // tile rows = UMMA M = TMEM lanes
 constexpr int kTcTN = 64;                  // sub-tile columns = UMMA N
@@ -309,17 +322,22 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
 struct Cursor {
   int64_t t;             // global tile index, -1 when done
   int32_t kd, layer, rb, cb;
+#if LSW_TC_FUSED
   int32_t seg, kidx;     // fused order: segment and kind index within its group
+#endif
 };
 
 struct TileSeq {
   int64_t T, t_begin, t_end;   // T tiles of this launch, starting at global tile t0
   int64_t t0;
   int32_t order, chunk, G, b;
-  const FusedSeg* segs;        // non-null: fused (decoder) tile order
+#if LSW_TC_FUSED
+  const FusedSeg* segs;        // fused (decoder) tile order
   int32_t n_seg;
+#endif
 };
 
+#if LSW_TC_FUSED
 // fused order: segment (binary search), then kind within the group, rb, cb
 __device__ __forceinline__ void cursor_set_fused(const TcGeom& g, const TileSeq& q, Cursor& c, int64_t t) {
   c.t = t;
@@ -360,6 +378,7 @@ __device__ __forceinline__ void cursor_step_fused(const TcGeom& g, const TileSeq
     }
   }
 }
+#endif
 
 __device__ __forceinline__ void cursor_set(const TcGeom& g, Cursor& c, int64_t t) {
   c.t = t;
@@ -380,8 +399,11 @@ __device__ __forceinline__ Cursor cursor_first(const TcGeom& g, const TileSeq& q
   Cursor c;
   int64_t t = q.order == ORDER_STRIP ? (q.t_begin < q.t_end ? q.t_begin : -1)
                                      : ((int64_t)q.b * q.chunk < q.T ? (int64_t)q.b * q.chunk : -1);
-  if (q.segs) cursor_set_fused(g, q, c, t < 0 ? -1 : q.t0 + t);
-  else cursor_set(g, c, t < 0 ? -1 : q.t0 + t);
+#if LSW_TC_FUSED
+  cursor_set_fused(g, q, c, t < 0 ? -1 : q.t0 + t);
+#else
+  cursor_set(g, c, t < 0 ? -1 : q.t0 + t);
+#endif
   return c;
 }
 
@@ -390,11 +412,13 @@ __device__ __forceinline__ Cursor cursor_first(const TcGeom& g, const TileSeq& q
 __device__ __forceinline__ void cursor_next(const TcGeom& g, const TileSeq& q, Cursor& c) {
   const int64_t t1 = c.t + 1, r1 = t1 - q.t0;          // r: position within this launch's range
   const bool step = q.order == ORDER_STRIP ? (r1 < q.t_end) : (r1 % q.chunk != 0 && r1 < q.T);
-  if (step && q.segs) {
+#if LSW_TC_FUSED
+  if (step) {
     c.t = t1;
     cursor_step_fused(g, q, c);
     return;
   }
+#endif
   if (step) {
     c.t = t1;
     if (++c.cb == g.kind[c.kd].col_tiles) {
@@ -408,8 +432,11 @@ __device__ __forceinline__ void cursor_next(const TcGeom& g, const TileSeq& q, C
   }
   if (q.order == ORDER_STRIP) { c.t = -1; return; }
   const int64_t nq = (c.t - q.t0) / q.chunk + q.G;
-  if (q.segs) cursor_set_fused(g, q, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
-  else cursor_set(g, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
+#if LSW_TC_FUSED
+  cursor_set_fused(g, q, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
+#else
+  cursor_set(g, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
+#endif
 }
 
 __device__ __forceinline__ int64_t strip_id(const Cursor& c) { return c.t - c.cb; }
@@ -442,9 +469,8 @@ __device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t v) {
 // One 16-column chunk of one row: W (two swizzled 16-B smem chunks) <-
 // RNE(W + sum_j c_j acc_j), with the sum in fp32 pairs (FFMA2), W as the first
 // addend.  NT = number of accumulators (compile-time).
-template <int NT, bool FUSED = false>
-__device__ __forceinline__ void epi_chunk(uint32_t tm_addr, const uint64_t* c2, uint8_t* wrow, int row, int col16,
-                                          const uint4* x16 = nullptr, float* ydot = nullptr) {
+template <int NT>
+__device__ __forceinline__ void epi_chunk(uint32_t tm_addr, const uint64_t* c2, uint8_t* wrow, int row, int col16) {
   uint32_t acc[NT][16];
 #pragma unroll
   for (int j = 0; j < NT; ++j) tmem_ld16(tm_addr + j * kTcTN, acc[j]);
@@ -464,19 +490,29 @@ __device__ __forceinline__ void epi_chunk(uint32_t tm_addr, const uint64_t* c2, 
   }
   *p0 = make_uint4(o[0], o[1], o[2], o[3]);
   *p1 = make_uint4(o[4], o[5], o[6], o[7]);
-  if constexpr (FUSED) {
-    // the GEMV on the stored (rounded) weights: 16 columns of this row x x
-    const uint32_t xw[8] = {x16[0].x, x16[0].y, x16[0].z, x16[0].w, x16[1].x, x16[1].y, x16[1].z, x16[1].w};
-    uint64_t a = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      a = ffma2(f2_pack(__uint_as_float(o[q] << 16), __uint_as_float(o[q] & 0xffff0000u)),
-                f2_pack(__uint_as_float(xw[q] << 16), __uint_as_float(xw[q] & 0xffff0000u)), a);
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
-    *ydot += lo + hi;
-  }
 }
+
+#if LSW_TC_FUSED
+// epi_chunk, then the GEMV on the stored (rounded) weights: ydot += this row's
+// 16 new W values x x (16 bf16 in x16[0..1])
+template <int NT>
+__device__ __forceinline__ void epi_chunk_fused(uint32_t tm_addr, const uint64_t* c2, uint8_t* wrow, int row,
+                                                int col16, const uint4* x16, float* ydot) {
+  epi_chunk<NT>(tm_addr, c2, wrow, row, col16);
+  const uint4 u0 = *reinterpret_cast<const uint4*>(wrow + (((col16 * 2 + 0) ^ (row & 7)) << 4));
+  const uint4 u1 = *reinterpret_cast<const uint4*>(wrow + (((col16 * 2 + 1) ^ (row & 7)) << 4));
+  const uint32_t o[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+  const uint32_t xw[8] = {x16[0].x, x16[0].y, x16[0].z, x16[0].w, x16[1].x, x16[1].y, x16[1].z, x16[1].w};
+  uint64_t a = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    a = ffma2(f2_pack(__uint_as_float(o[q] << 16), __uint_as_float(o[q] & 0xffff0000u)),
+              f2_pack(__uint_as_float(xw[q] << 16), __uint_as_float(xw[q] & 0xffff0000u)), a);
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+  *ydot += lo + hi;
+}
+#endif
 
 // General term count (> 4): groups of 4 accumulators.
 __device__ __forceinline__ void epi_chunk_many(uint32_t tm_addr, const float* cs, int nt, uint8_t* wrow, int row,
@@ -524,12 +560,13 @@ struct TcArgs {
   const float* cur_g;
   DevState* state;
   int64_t t0, t_count;        // tile range of this launch (t_count = 0: all tiles)
-  // fused switch + decode (null segs: plain switch)
-  const FusedSeg* segs;
+#if LSW_TC_FUSED
+  const FusedSeg* segs;       // decoder-order segment table
   int32_t n_seg;
   const __nv_bfloat16* xs;    // packed GEMV inputs (lsw_decode_token layout)
   float* ys;                  // packed outputs, zeroed before the launch (accumulated)
   unsigned long long* seg_done;   // [n_seg], zeroed before the launch
+#endif
 };
 
 struct EpiCtx {
@@ -545,9 +582,12 @@ struct EpiCtx {
   uint64_t* bar_accfull;
   uint64_t* bar_accempty;
   uint64_t* trace;
-  const TcArgs* args;          // fused switch + decode: segs, xs, ys, seg_done
+#if LSW_TC_FUSED
+  const TcArgs* args;          // segs, xs, ys, seg_done
+#endif
 };
 
+#if LSW_TC_FUSED
 // Spin (with a ~20 s watchdog) until a device-wide counter reaches target.
 __device__ __forceinline__ void wait_count(const unsigned long long* p, unsigned long long target) {
   auto load = [&]() {
@@ -562,12 +602,12 @@ __device__ __forceinline__ void wait_count(const unsigned long long* p, unsigned
     if ((n & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) __trap();
   }
 }
+#endif
 
 // The epilogue warps' tile loop, specialised on the term count (NT = -1: any;
-// NT = kSplitNT: split mode, one pre-scaled accumulator per tile).  FUSED:
-// also y += W_new x for the tile (fused switch + decode, decoder order).
+// NT = kSplitNT: split mode, one pre-scaled accumulator per tile).
 constexpr int kSplitNT = 100;
-template <int NT, bool FUSED = false>
+template <int NT>
 __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& seq, const Coefs& cf) {
   constexpr bool SPLIT = NT == kSplitNT;
   const TcGeom& g = e.g;
@@ -587,21 +627,25 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
   Ring acc{0, 0, (uint32_t)g.acc_bufs};
   uint64_t* tr = (ew == 0 && e.lane == 0) ? e.trace : nullptr;
   uint32_t it = 0;
+#if LSW_TC_FUSED
   int cur_seg = -1;
-  int64_t seg_mine = 0;                        // FUSED: tiles of cur_seg this CTA finished
+  int64_t seg_mine = 0;                        // tiles of cur_seg this CTA finished
   const bool leader = ew == 0 && e.lane == 0;
+#endif
   for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
-    float ydot = 0.f;                          // FUSED: this thread's part of y[row] for the tile
-    const __nv_bfloat16* xt = nullptr;
-    int64_t x_lim = 0;
-    if constexpr (FUSED) {
+#if LSW_TC_FUSED
+    float ydot = 0.f;                          // this thread's part of y[row] for the tile
+    const __nv_bfloat16* xt;
+    int64_t x_lim;
+    {
       const TcArgs& A = *e.args;
       if (c.seg != cur_seg) {
         // decoder order: x of segment s is final only once every tile of
         // segment s-1 is done.  One thread per CTA publishes the CTA's count of
         // the segment it leaves (after all 8 epilogue warps issued their y
         // atomics) and waits for the previous segment's total (one counter
-        // update per CTA and segment, not per tile: a single hot address)
+        // update per CTA and segment -- per tile and warp, the single hot
+        // address serialised: 14.4 ms per 7B token instead of 8.4)
         named_bar(3, 32 * kTcEpiWarps);
         if (leader) {
           if (cur_seg >= 0) {
@@ -619,20 +663,21 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
       xt = A.xs + A.segs[c.seg].x_off + col0;
       x_lim = g.kind[c.kd].d_in - col0;        // columns of this tile inside d_in
     }
+#endif
     mbar_wait(smem_u32(&e.bar_wfull[wring.i]), wring.phase);            // W tile landed (acquire)
     trace_ev(tr, it, EV_EPI_WFULL);
     uint8_t* wt = e.wst0 + (size_t)wring.i * g.w_stage_bytes;
     for (int sb = 0; sb < g.nsub; ++sb) {
+#if LSW_TC_FUSED
       uint4 xq[2][2];
-      if constexpr (FUSED) {
 #pragma unroll
-        for (int q2 = 0; q2 < 2; ++q2)
+      for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int cl = sb * kTcTN + (half * 2 + q2) * 16 + h * 8;   // 8 columns (16 B) of x
-            xq[q2][h] = cl < x_lim ? *reinterpret_cast<const uint4*>(xt + cl) : make_uint4(0, 0, 0, 0);
-          }
-      }
+        for (int h = 0; h < 2; ++h) {
+          const int cl = sb * kTcTN + (half * 2 + q2) * 16 + h * 8;     // 8 columns (16 B) of x
+          xq[q2][h] = cl < x_lim ? *reinterpret_cast<const uint4*>(xt + cl) : make_uint4(0, 0, 0, 0);
+        }
+#endif
       if (!e.probe && (!SPLIT || sb == 0))
         mbar_wait(smem_u32(&e.bar_accfull[acc.i]), acc.phase);          // accumulators ready
       if (sb == 0) trace_ev(tr, it, EV_EPI_ACC0);
@@ -644,9 +689,12 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
       for (int q2 = 0; q2 < 2; ++q2) {
         const int col16 = half * 2 + q2;       // 16-column chunk 0..3 of the sub-tile
         const uint32_t ta = tm_row + col16 * 16;
+#if LSW_TC_FUSED
+        if constexpr (NT > 0 && !SPLIT) epi_chunk_fused<NT>(ta, c2, wrow, row, col16, xq[q2], &ydot);
+#else
         if constexpr (SPLIT) { if (!e.skip_math) epi_chunk<1>(ta, c2, wrow, row, col16); }
-        else if constexpr (FUSED) epi_chunk<NT, true>(ta, c2, wrow, row, col16, xq[q2], &ydot);
         else if constexpr (NT > 0) epi_chunk<NT>(ta, c2, wrow, row, col16);
+#endif
         else if constexpr (NT < 0) epi_chunk_many(ta, cf.c, nt, wrow, row, col16);
       }
       if (!SPLIT || sb == g.nsub - 1) {
@@ -687,25 +735,27 @@ __device__ __forceinline__ void epilogue_loop(const EpiCtx& e, const TileSeq& se
       __syncwarp();
       if (e.lane == 0) mbar_arrive(smem_u32(&e.bar_wdone[wring.i]));
     }
-    if constexpr (FUSED) {
+#if LSW_TC_FUSED
+    {
       const TcArgs& A = *e.args;
       const int64_t grow = (int64_t)c.rb * kTcTM + row;
       if (grow < g.kind[c.kd].d_out) atomicAdd(A.ys + A.segs[c.seg].y_off[c.kidx] + grow, ydot);
       ++seg_mine;
     }
+#endif
     trace_ev(tr, it, EV_EPI_DONE);
     wring.next();
   }
-  if constexpr (FUSED) {
-    if (cur_seg >= 0) {                        // publish the last segment this CTA worked on
-      named_bar(3, 32 * kTcEpiWarps);
-      if (leader) {
-        __threadfence();
-        asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(e.args->seg_done + cur_seg),
-                     "l"((unsigned long long)seg_mine) : "memory");
-      }
+#if LSW_TC_FUSED
+  if (cur_seg >= 0) {                          // publish the last segment this CTA worked on
+    named_bar(3, 32 * kTcEpiWarps);
+    if (leader) {
+      __threadfence();
+      asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(e.args->seg_done + cur_seg),
+                   "l"((unsigned long long)seg_mine) : "memory");
     }
   }
+#endif
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -789,8 +839,10 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
   seq.b = blockIdx.x;
   seq.t_begin = seq.T * blockIdx.x / gridDim.x;
   seq.t_end = seq.T * (blockIdx.x + 1) / gridDim.x;
+#if LSW_TC_FUSED
   seq.segs = args.segs;
   seq.n_seg = args.n_seg;
+#endif
   const uint32_t tmem_base = s_tmem_base;
   const int tile_cols = kTcTN * nsub;
 
@@ -1021,18 +1073,13 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
       // ============================ epilogue ================================
       const int ntc = (probe || skip_math) ? 0 : nt;
       EpiCtx ec{g, wst0, tmem_base, warp, lane, probe, skip_math, bar_wfull, bar_wdone, bar_wempty, bar_accfull,
-                bar_accempty, args.trace, &args};
+                bar_accempty, args.trace
+#if LSW_TC_FUSED
+                , &args
+#endif
+      };
       // split mode always runs the split loop (its TMEM buffer protocol differs);
       // with probe/skip_math it only skips the math
-      const bool fused = args.segs != nullptr && !probe && !skip_math && !g.split;
-      if (fused) {
-        switch (ntc) {
-          case 1: epilogue_loop<1, true>(ec, seq, cf); break;
-          case 2: epilogue_loop<2, true>(ec, seq, cf); break;
-          case 3: epilogue_loop<3, true>(ec, seq, cf); break;
-          default: epilogue_loop<4, true>(ec, seq, cf); break;   // host allows fused only for 2k <= 4
-        }
-      } else
       switch (g.split && nt > 0 && !probe ? kSplitNT : ntc) {
         case kSplitNT: epilogue_loop<kSplitNT>(ec, seq, cf); break;
         case 0: epilogue_loop<0>(ec, seq, cf); break;
@@ -1058,6 +1105,46 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
     finish_pass(p, s_parity, cf);
   }
 }
+
+#if LSW_TC_FUSED
+// ------------------------------------------------------------------ fused launcher (v1f)
+
+// Launch the fused kernel with the plain build's plan data (v1 and v1f TcMaps /
+// TcGeom are the same source, hence the same layout).
+cudaError_t launch_fused_raw(const void* maps, const void* geom, int grid, uint32_t smem, int32_t order_chunk,
+                             const SwitchParams& p, cudaStream_t s, const void* segs, int32_t n_seg, int64_t tiles,
+                             const void* xs, float* ys, unsigned long long* seg_done, uint64_t* trace) {
+  static uint32_t smem_set = 0;
+  if (smem > smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(switch_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    smem_set = smem;
+  }
+  TcArgs a;
+  a.g = *reinterpret_cast<const TcGeom*>(geom);
+  a.order = ORDER_SWEEP;
+  a.chunk = order_chunk;
+  a.probe = 0;
+  a.trace = trace;
+  a.mode = p.mode;
+  a.top_k = p.top_k;
+  a.n_experts = p.n_experts;
+  a.scale = p.scale;
+  a.cur_idx = p.cur_idx;
+  a.cur_g = p.cur_g;
+  a.state = p.state;
+  a.t0 = 0;
+  a.t_count = tiles;
+  a.segs = reinterpret_cast<const FusedSeg*>(segs);
+  a.n_seg = n_seg;
+  a.xs = reinterpret_cast<const __nv_bfloat16*>(xs);
+  a.ys = ys;
+  a.seg_done = seg_done;
+  switch_tc_kernel<<<grid, kTcThreads, smem, s>>>(*reinterpret_cast<const TcMaps*>(maps), a);
+  return cudaGetLastError();
+}
+
+#else   // the plain build: packing, planning, launches
 
 // ------------------------------------------------------------------ packing
 
@@ -1352,6 +1439,29 @@ int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t
   return per;
 }
 
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0,
+                             int64_t t_count) {
+  TcArgs a;
+  a.t0 = t0;
+  a.t_count = t_count;
+  a.g = plan->geom;
+  a.order = plan->order;
+  a.chunk = plan->chunk;
+  a.probe = plan->probe;
+  a.trace = plan->trace;
+  a.mode = p.mode;
+  a.top_k = p.top_k;
+  a.n_experts = p.n_experts;
+  a.scale = p.scale;
+  a.cur_idx = p.cur_idx;
+  a.cur_g = p.cur_g;
+  a.state = p.state;
+  switch_tc_kernel<<<plan->grid, kTcThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ fused switch + decode (host)
+
 cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
                               int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]) {
   const TcGeom& g = plan->geom;
@@ -1393,58 +1503,16 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   if (!plan->d_segs) return cudaErrorNotSupported;
   cudaError_t e = cudaMemsetAsync(plan->d_seg_done, 0, sizeof(unsigned long long) * plan->n_segs, s);
   if (e != cudaSuccess) return e;
-  TcArgs a;
-  a.g = plan->geom;
-  a.order = ORDER_SWEEP;
   // segment barriers: a CTA's share of one segment is a few tiles, so deal
-  // small chunks (large ones would leave most CTAs idle at every barrier)
-  a.chunk = 8;
-  if (const char* v = getenv("LSW_TC_FUSED_CHUNK")) { int x = atoi(v); if (x >= 1) a.chunk = x; }
-  a.probe = 0;
-  a.trace = plan->trace;
-  a.mode = p.mode;
-  a.top_k = p.top_k;
-  a.n_experts = p.n_experts;
-  a.scale = p.scale;
-  a.cur_idx = p.cur_idx;
-  a.cur_g = p.cur_g;
-  a.state = p.state;
-  a.t0 = 0;
-  a.t_count = plan->fused_tiles;
-  a.segs = plan->d_segs;
-  a.n_seg = plan->n_segs;
-  a.xs = (const __nv_bfloat16*)xs;
-  a.ys = ys;
-  a.seg_done = plan->d_seg_done;
-  switch_tc_kernel<<<plan->grid, kTcThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
-  return cudaGetLastError();
+  // small chunks (measured 7B: chunk 4-8 8.4 ms, 1 12.6, 16 10.7, 32 22.8)
+  int chunk = 8;
+  if (const char* v = getenv("LSW_TC_FUSED_CHUNK")) { int x = atoi(v); if (x >= 1) chunk = x; }
+  return v1f::launch_fused_raw(&plan->maps, &plan->geom, plan->grid, plan->geom.smem_bytes, chunk, p, s,
+                               plan->d_segs, plan->n_segs, plan->fused_tiles, xs, ys, plan->d_seg_done,
+                               plan->trace);
 }
 
-cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0,
-                             int64_t t_count) {
-  TcArgs a;
-  a.segs = nullptr;
-  a.n_seg = 0;
-  a.xs = nullptr;
-  a.ys = nullptr;
-  a.seg_done = nullptr;
-  a.t0 = t0;
-  a.t_count = t_count;
-  a.g = plan->geom;
-  a.order = plan->order;
-  a.chunk = plan->chunk;
-  a.probe = plan->probe;
-  a.trace = plan->trace;
-  a.mode = p.mode;
-  a.top_k = p.top_k;
-  a.n_experts = p.n_experts;
-  a.scale = p.scale;
-  a.cur_idx = p.cur_idx;
-  a.cur_g = p.cur_g;
-  a.state = p.state;
-  switch_tc_kernel<<<plan->grid, kTcThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
-  return cudaGetLastError();
-}
+#endif  // LSW_TC_FUSED
 
-}  // namespace v1
+}  // namespace v1 / v1f
 }  // namespace lsw

@@ -35,6 +35,13 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
                                    float* ys);
 }  // namespace v1
 
+// the v1 kernel compiled with the fused epilogue (switch_tc_fused.cu)
+namespace v1f {
+cudaError_t launch_fused_raw(const void* maps, const void* geom, int grid, uint32_t smem, int32_t order_chunk,
+                             const SwitchParams& p, cudaStream_t s, const void* segs, int32_t n_seg, int64_t tiles,
+                             const void* xs, float* ys, unsigned long long* seg_done, uint64_t* trace);
+}  // namespace v1f
+
 namespace tg {
 struct TcPlan;
 cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why);
