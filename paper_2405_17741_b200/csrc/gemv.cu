@@ -322,7 +322,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   // grid completes only when the caller says so (early_w: the previous launch
   // was a GEMV that itself waited for whatever wrote W).  Everything else
   // (x, y) is touched only after griddepcontrol.wait.
-  if (!early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!(early_w & 1)) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (warp == 0) {
     // producer: one bulk copy per contiguous run of a chunk's rows (a chunk is
     // split only where it crosses from one site's matrix into the next);
@@ -360,7 +360,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     }
     return;
   }
-  if (early_w) asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (early_w & 1) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after our wait: see above
   // x -> shared (consumer warps), then a named barrier among the consumers only
   stage_x<kBf16>(p.x, xs, row_bytes, threadIdx.x - 32, blockDim.x - 32);
@@ -391,7 +391,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     const int64_t row = (blockIdx.x + i * G) * R + k;
     while (issued <= i) __nanosleep(64);
     g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
-    if (row < p.rows_total) {
+    if (row < p.rows_total && !(early_w & 2)) {    // early_w bit 1: tuning probe, stream only
       float extra = 0.f, extra_u = 1.f, extra_g = 1.f;
       if (kLora && !(L.flags & 4)) {
         // this row's LoRA-up term, sum_j scale g_j B_q[e_j][row, :] . u_q[j]:
@@ -730,7 +730,9 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
         cudaError_t e = cudaLaunchKernelEx(&ld, bf16 ? lora_down_kernel<true> : lora_down_kernel<false>, p, *lora);
         if (e != cudaSuccess) return e;
       }
-      return cudaLaunchKernelEx(&lc, fn, p, slots, R, (int32_t)(early_w || lora ? 1 : 0), lora ? *lora : none);
+      static const int probe = getenv("LSW_GEMV_PROBE") ? atoi(getenv("LSW_GEMV_PROBE")) : 0;   // tuning only
+      return cudaLaunchKernelEx(&lc, fn, p, slots, R, (int32_t)((early_w || lora ? 1 : 0) | (probe ? 2 : 0)),
+                                lora ? *lora : none);
     }
   }
   if (lora) return cudaErrorNotSupported;   // the LDG variant has no unmerged form

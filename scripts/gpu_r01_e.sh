@@ -1,7 +1,3 @@
 #!/bin/bash
-for rep in 1 2; do
-python scripts/tune_switch.py --lib build/bs_4bf23d2/liblsw.so "order=sweep" 2>&1 | grep setting | sed "s/^/prev /"
-python scripts/tune_switch.py "order=sweep" 2>&1 | grep setting | sed 's/^/HEAD /'
-done
-timeout 600 python -m pytest tests/test_gpu_fused.py tests/test_gpu_restore.py -q -x 2>&1 | tail -1
-timeout 600 python scripts/time_fused.py
+timeout 300 python scripts/tune_gemv.py 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('math', d['groups_gemv_ms'], d['groups_gemv_GBps'], d['token_gemv_ms'])"
+LSW_GEMV_PROBE=1 timeout 300 python scripts/tune_gemv.py 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('stream-only', d['groups_gemv_ms'], d['groups_gemv_GBps'], d['token_gemv_ms'])"
