@@ -93,6 +93,8 @@ struct TcGeom {
   uint32_t a_sub_bytes;                   // one term's A^T slice of one sub-tile: 64 * rp * 2
   uint32_t b_bytes_per_term;              // 128 * rp * 2
   uint32_t a_stage_bytes, b_buf_bytes, w_stage_bytes;   // A stage = one (sub-tile, group) unit
+  int32_t mma2;                           // 1: warps 1 and 2 issue alternate MMA groups; the W
+                                          //    producer thread also stores (LSW_TC_MMA2)
   int32_t store_stg;                      // 1: epilogue writes W back with coalesced STG.128 (LSU);
                                           // 0: the store warp issues TMA bulk tensor stores
   uint32_t swz_mode;                      // UMMA layout type of the r-wide operands
@@ -621,8 +623,25 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
         const bool restore = args.mode == MODE_RESTORE;      // load from the pristine copy
         Ring wring{0, 0, (uint32_t)g.w_stages};
         uint32_t it = 0;
+        // mma2: this thread also stores finished tiles (warp 2 issues MMAs):
+        // a stage's previous tile is written back before the stage is reloaded
+        Cursor held[kTcMaxStages];
+        auto store_stage = [&](uint32_t st, uint32_t parity) {
+          mbar_wait(smem_u32(&bar_wdone[st]), parity);             // epilogue wrote the tile
+          const Cursor& h = held[st];
+          uint8_t* wsrc = wst0 + (size_t)st * g.w_stage_bytes;
+          for (int sb = 0; sb < nsub; ++sb)
+            tma_store_3d(&maps.w[h.kd], smem_u32(wsrc + sb * kSubBytes), h.cb * tile_cols + sb * kTcTN,
+                         h.rb * kTcTM, h.layer, pol_stream);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // smem read -> reusable
+        };
         for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
-          mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
+          if (g.mma2) {
+            if (it >= (uint32_t)g.w_stages) store_stage(wring.i, wring.phase ^ 1);
+          } else {
+            mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
+          }
           const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
           mbar_expect_tx(wbar, nsub * kSubBytes);
           uint8_t* wdst = wst0 + (size_t)wring.i * g.w_stage_bytes;
@@ -630,8 +649,17 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
             tma_load_3d(smem_u32(wdst + sb * kSubBytes), restore ? &maps.p[c.kd] : &maps.w[c.kd],
                         c.cb * tile_cols + sb * kTcTN,
                         c.rb * kTcTM, c.layer, wbar, pol_stream);
+          held[wring.i] = c;
           trace_ev(args.trace, it, EV_W_ISSUED);
           wring.next();
+        }
+        if (g.mma2) {
+          // drain: the last min(stages, tiles) tiles, oldest first
+          const uint32_t pending = it < (uint32_t)g.w_stages ? it : (uint32_t)g.w_stages;
+          Ring r = wring;
+          if (it < (uint32_t)g.w_stages) r = Ring{0, 0, (uint32_t)g.w_stages};   // nothing wrapped yet
+          for (uint32_t j = 0; j < pending; ++j, r.next()) store_stage(r.i, it < (uint32_t)g.w_stages ? 0u : r.phase ^ 1);
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         }
       }
     } else if (warp == 3) {
@@ -685,7 +713,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
           trace_ev(tr, it, EV_A_ISSUED);
         }
       }
-    } else if (warp == 1) {
+    } else if (warp == 1 || (warp == 2 && g.mma2)) {
       // ============================ MMA issuer ==============================
       // The whole warp runs the loop (all values warp-uniform, so operands stay
       // in uniform registers); one elected lane issues each tcgen05 instruction.
@@ -707,12 +735,16 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
         const uint64_t b_term = g.b_bytes_per_term >> 4, a_term = g.a_sub_bytes >> 4;
         const int tg = g.tg;
         const uint32_t buf_cols = (uint32_t)tg * kTcTN;
-        uint64_t* tr = lane == 0 ? args.trace : nullptr;
+        // mma2: warps 1 and 2 issue alternate MMA groups (each commit drains
+        // only its own warp's MMAs, measured: two issuers reach 1.45x the
+        // groups per microsecond of one, scripts/mmabench2.cu)
+        const uint32_t me = (uint32_t)(warp - 1), n_iss = g.mma2 ? 2u : 1u;
+        uint64_t* tr = (lane == 0 && warp == 1) ? args.trace : nullptr;
         Ring bring{0, 0, (uint32_t)g.b_bufs};
         Ring aring{0, 0, (uint32_t)g.a_stages};
         Ring acc{0, 0, (uint32_t)g.acc_bufs};
         int64_t strip_prev = -1;
-        uint32_t it = 0;
+        uint32_t it = 0, unit = 0;
         for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
           const int64_t strip = strip_id(c);
           if (strip != strip_prev) {
@@ -724,7 +756,12 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
           const uint64_t b_desc = desc0 + (smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes) >> 4);
           // one MMA group per (sub-tile, term group): tg accumulators of 64 columns
           for (int sb = 0; sb < nsub; ++sb)
-            for (int j0 = 0; j0 < nt; j0 += tg) {
+            for (int j0 = 0; j0 < nt; j0 += tg, ++unit) {
+              if (unit % n_iss != me) {               // the other issuer's group
+                acc.next();
+                aring.next();
+                continue;
+              }
               mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
               if (sb == 0 && j0 == 0) trace_ev(tr, it, EV_A_FULL);
               mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
@@ -749,7 +786,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
           trace_ev(tr, it, EV_MMA_DONE);
         }
       }
-    } else if (warp == 2 && !g.store_stg) {
+    } else if (warp == 2 && !g.store_stg && !g.mma2) {
       // ============================ store warp ==============================
       if (lane == 0) {
         const uint64_t pol_stream = policy_evict_first();
@@ -972,6 +1009,11 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   }
   g.store_stg = 0;                                       // measured: TMA store 4466 vs STG 4222 GB/s
   if (const char* v = getenv("LSW_TC_STORE")) g.store_stg = strcmp(v, "stg") == 0;
+  // measured (8-layer 7B shape): r16 k3 0.51 -> 0.54, k4 0.46 -> 0.49, r32 k3 0.46 -> 0.54,
+  // r64 k2 0.35 -> 0.40 of the copy peak; k1 (2 terms) 0.86 -> 0.84
+  g.mma2 = g.max_terms > 2;
+  if (const char* v = getenv("LSW_TC_MMA2")) g.mma2 = atoi(v) != 0;
+  if (g.store_stg) g.mma2 = 0;
   g.smem_bytes = g.w_stages * g.w_stage_bytes + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
   // tiles
   const int tile_cols = kTcTN * g.nsub;

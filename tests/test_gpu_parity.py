@@ -108,7 +108,7 @@ def test_switch_trajectory_full_elements(name, impl):
 
 
 TC_VARIANTS = [("v1", {}), ("v1", {"LSW_TC_SPLIT": "1"}), ("tg", {}), ("tg", {"LSW_TC_TG": "1"}),
-               ("tg", {"LSW_TC_TG": "2"})]
+               ("tg", {"LSW_TC_TG": "2"}), ("tg", {"LSW_TC_MMA2": "0"}), ("tg", {"LSW_TC_MMA2": "1", "LSW_TC_TG": "1"})]
 
 
 @pytest.mark.parametrize("grid", [1, 3])
