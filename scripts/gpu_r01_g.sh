@@ -1,7 +1,7 @@
 #!/bin/bash
 # round-1 evidence run G: full GPU tests, bench (3 configs), launch list, ncu of both kernels
 mkdir -p gpurun_out
-TAG=r01m
+TAG=r01n
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
 timeout 2400 python -m pytest tests -q -m gpu 2>&1 | tail -3
 timeout 900 python bench.py --steps 20 --warmup 5 2>&1 | tail -1 | tee gpurun_out/bench_${TAG}.json
