@@ -107,6 +107,7 @@ struct TcGeom {
                                           //    (N = tile width), one MMA group per tile, 4 TMEM buffers;
                                           // 0: one accumulator per expert term, c_j applied in the epilogue
   int32_t w4d;                            // 1: W moved by ONE 4-D TMA op per tile (LSW_TC_W4D)
+  int32_t w_policy;                       // W loads/stores L2 policy: 0 evict_first, 1 evict_normal
   int32_t store_stg;                      // 1: epilogue writes W back with coalesced STG.128 (LSU);
                                           // 0: the store warp issues TMA bulk tensor stores
   uint32_t swz_mode;                      // UMMA layout type of the r-wide operands
@@ -242,6 +243,11 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t sr
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -850,7 +856,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
     if (warp == 0) {
       // ============================ W producer =============================
       if (lane == 0) {
-        const uint64_t pol_stream = policy_evict_first();
+        const uint64_t pol_stream = g.w_policy ? policy_evict_normal() : policy_evict_first();
         const bool restore = args.mode == MODE_RESTORE;      // load from the pristine copy
         Ring wring{0, 0, (uint32_t)g.w_stages};
         uint32_t it = 0;
@@ -1049,7 +1055,7 @@ switch_tc_kernel(const __grid_constant__ TcMaps maps, const __grid_constant__ Tc
     } else if (warp == 2 && !g.store_stg) {
       // ============================ store warp ==============================
       if (lane == 0) {
-        const uint64_t pol_stream = policy_evict_first();
+        const uint64_t pol_stream = g.w_policy ? policy_evict_normal() : policy_evict_first();
         Ring wring{0, 0, (uint32_t)g.w_stages};
         uint32_t it = 0;
         for (Cursor c = cursor_first(g, seq); c.t >= 0; cursor_next(g, seq, c), ++it) {
@@ -1206,6 +1212,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 4-D view (w4d): dims {64, d_out, d_in / 64, L}, box {64, 128, nsub, 1} -- one
 // TMA op per W tile.  Needs d_in % 64 == 0.
+// tuning knob LSW_TC_L2PROMO = 0 (none) / 64 / 128 / 256 (default) bytes
+static CUtensorMapL2promotion l2_promotion() {
+  const char* v = getenv("LSW_TC_L2PROMO");
+  const int x = v ? atoi(v) : 256;
+  return x == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : x == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : x == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 static bool encode_w4(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d_out, uint64_t L, int nsub) {
   auto enc = get_encode();
   if (!enc || d_in % 64) return false;
@@ -1214,7 +1228,7 @@ static bool encode_w4(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t 
   cuuint32_t box[4] = {(cuuint32_t)kTcTN, (cuuint32_t)kTcTM, (cuuint32_t)nsub, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -1227,7 +1241,7 @@ static bool encode_w(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d
   cuuint32_t box[3] = {(cuuint32_t)kTcTN, (cuuint32_t)kTcTM, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -1330,6 +1344,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   }
   g.w4d = 0;
   if (const char* v = getenv("LSW_TC_W4D")) g.w4d = atoi(v) != 0;
+  g.w_policy = 0;
+  if (const char* v = getenv("LSW_TC_WPOLICY")) g.w_policy = strcmp(v, "normal") == 0;
   for (int k = 0; k < LSW_NKIND; ++k) if (sp.kind[k].d_in % 64) g.w4d = 0;
   if (g.nsub != 2 || g.split) g.w4d = 0;
   g.store_stg = 0;                                       // measured: TMA store 4466 vs STG 4222 GB/s
