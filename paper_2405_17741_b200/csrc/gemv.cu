@@ -290,6 +290,33 @@ lora_down_kernel(const GemvParams p, const GemvLora L) {
   }
 }
 
+// Unmerged decode: the pre-gate's decision is known for EVERY layer at the
+// start of the token, so the selected LoRA-down rows of all layers can
+// be pulled into L2 (evict_last; the W streams are evict_first) before the
+// first group -- each lora_down_kernel then reads them at L2 latency.
+__global__ void lora_prefetch_kernel(LoraPrefetch q) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  const int total = LSW_NKIND * q.n_layers * q.k;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int kd = i / (q.n_layers * q.k), rem = i - kd * q.n_layers * q.k;
+    const int l = rem / q.k, j = rem - l * q.k;
+    const int64_t block = (int64_t)q.r * q.d_in[kd] * q.es;           // one expert's r rows
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(q.A[kd]) +
+                         ((int64_t)l * q.n_experts + q.idx[j]) * block;
+    for (int64_t off = 0; off < block; off += 65536) {
+      const uint32_t n = (uint32_t)(block - off < 65536 ? block - off : 65536);
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src + off), "r"(n), "l"(pol)
+                   : "memory");
+    }
+  }
+}
+
+cudaError_t launch_lora_prefetch(const LoraPrefetch& q, cudaStream_t s) {
+  lora_prefetch_kernel<<<16, 128, 0, s>>>(q);
+  return cudaGetLastError();
+}
+
 template <bool kBf16, bool kLora>
 __global__ void __launch_bounds__(kBulkThreads, 1)
 gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, const GemvLora L) {

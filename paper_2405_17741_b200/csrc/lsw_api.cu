@@ -429,8 +429,25 @@ lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_t group,
 
 lsw_status lsw_decode_all_layers_unmerged(lsw_ctx* ctx, const void* xs, float* ys, const int32_t* idx,
                                           const float* gate, void* stream) {
-  if (!ctx || !xs || !ys) return fail(LSW_E_ARG, "lsw_decode_all_layers_unmerged: null argument");
+  if (!ctx || !xs || !ys || !idx || !gate) return fail(LSW_E_ARG, "lsw_decode_all_layers_unmerged: null argument");
+  if (ctx->merged) return fail(LSW_E_STATE, "lsw_decode_all_layers_unmerged: the ctx is merged");
   const size_t es = esize(ctx);
+  // opt-in (LSW_UNMERGED_PREFETCH=1): measured 3.65 vs 3.56 ms per 7B token
+  // without -- the LoRA-down latency is not what bounds this path
+  static const bool prefetch = getenv("LSW_UNMERGED_PREFETCH") && getenv("LSW_UNMERGED_PREFETCH")[0] == '1';
+  if (prefetch) {
+    LoraPrefetch q{};
+    for (int k = 0; k < LSW_NKIND; ++k) { q.A[k] = ctx->kinds[k].A; q.d_in[k] = ctx->kinds[k].d_in; }
+    q.n_layers = ctx->cfg.n_layers;
+    q.n_experts = ctx->cfg.n_experts;
+    q.r = ctx->cfg.rank;
+    q.k = ctx->cfg.top_k;
+    q.es = (int32_t)es;
+    q.idx = idx;
+    cudaError_t e = launch_lora_prefetch(q, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_all_layers_unmerged: prefetch");
+    ++ctx->launches;
+  }
   for (int l = 0; l < ctx->cfg.n_layers; ++l)
     for (int g = 0; g < LSW_NGROUP; ++g) {
       const uint8_t* xp = (const uint8_t*)xs + (size_t)(l * ctx->x_per_layer + ctx->x_off[g]) * es;

@@ -170,6 +170,15 @@ struct GemvLora {
 };
 // early_w: the previous launch on `s` was a GEMV (W may be prefetched before
 // griddepcontrol.wait; see gemv.cu).  lora: null for the merged-weight GEMV.
+// Unmerged decode: pull the selected experts' LoRA-down rows of every layer
+// into L2 at the start of the token (the pre-gated decision is known for all).
+struct LoraPrefetch {
+  const void* A[LSW_NKIND];   // [L, N, r, d_in] per kind
+  int64_t d_in[LSW_NKIND];
+  int32_t n_layers, n_experts, r, k, es;
+  const int32_t* idx;         // [k] device
+};
+cudaError_t launch_lora_prefetch(const LoraPrefetch& q, cudaStream_t s);
 // lora: also launches the group's LoRA-down kernel first (2 launches).
 cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w = false,
                         GemvLora* lora = nullptr);

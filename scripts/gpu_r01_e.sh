@@ -1,2 +1,4 @@
 #!/bin/bash
-python scripts/tune_switch.py --repeat 2 "order=sweep" "l2promo=0" "l2promo=128" "wpolicy=normal" "probe=1" "probe=1,l2promo=0" "probe=1,wpolicy=normal" 2>&1 | grep setting
+timeout 600 python scripts/time_unmerged.py
+LSW_UNMERGED_PREFETCH=0 timeout 600 python scripts/time_unmerged.py
+timeout 600 python -m pytest tests/test_gpu_unmerged.py -q -x 2>&1 | tail -1
