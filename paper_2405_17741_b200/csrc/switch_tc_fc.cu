@@ -1,0 +1,587 @@
+// switch_tc_fc.cu -- K1-tc (folded-coefficient variant): the all-layer in-place
+// switch on the 5th-gen tensor cores with ONE accumulator per tile.
+//
+// What it computes (identical to K1-simt / v1 / tg): for every adapted matrix m
+// of every layer, in ONE persistent launch (SGMM Eq. 11; "a single
+// CUDA kernel operation" P:240; in place P:328):
+//     W_m <- RNE( W_m + sum_j c_j * B_{m,e_j} @ A_{m,e_j} )
+// with the Eq. 5/9/10 coefficient list (Eq. 9 sign corrected, R1; compacted,
+// lsw_internal.cuh build_coefs).
+//
+// How it differs from v1 / tg: Eq. 5 concatenates
+// the selected experts along the rank dimension and folds the gate into one
+// factor, so the whole update of a tile is ONE contraction of depth sum_j r_j.
+// Folding c_j into a bf16 factor would round it (R13), so each folded factor is
+// stored as an exact-to-2^-16 pair of bf16 parts, hi_j = bf16(c_j B_j) and
+// lo_j = bf16(c_j B_j - hi_j), and the tile is
+//     D = sum_j (hi_j + lo_j) @ A_j          (K = 2 * sum_j rp)
+// accumulated in fp32 in ONE TMEM buffer by one chain of tcgen05.mma (M = 128,
+// N = 128) and ONE commit per tile.  The epilogue then only adds D to W and
+// rounds once.  Against per-term accumulators (v1 / tg) this removes one TMEM
+// read and one FFMA per term and element and all but one commit per tile -- the
+// costs that bound those kernels at 2k >= 4 terms -- for twice
+// the tensor-core work, which stays far below the HBM time while
+// 2 * sum_j rp <= ~320 (rp = 16: k <= 4; rp = 32: k <= 2).
+//  * The fold runs once per 128-row strip (B slices are reused along the
+//    strip): the operand warp bulk-copies the raw pre-swizzled B slices into
+//    the strip buffer and rewrites them in place as (hi, lo) parts; the
+//    element positions of the swizzled image do not change.
+//  * W tiles 128 x 128 (two 64-column 128B-swizzled TMA boxes), TMA loads (warp
+//    0), TMA bulk stores (warp 2), chunked sweep tile order -- as in tg.
+#include <cstdlib>
+#include <cstring>
+
+#include "switch_tc_impl.cuh"
+#include "tc_common.cuh"
+
+namespace lsw {
+namespace fc {
+
+using namespace tcx;
+
+constexpr int kTM = 128;                    // tile rows = UMMA M = TMEM lanes
+constexpr int kTN = 128;                    // tile columns = UMMA N = accumulator columns
+constexpr int kSubCols = 64;                // W sub-tile columns (one 128B-swizzle TMA box)
+constexpr int kSubBytes = kTM * kSubCols * 2;   // 16 KB
+constexpr int kEpiWarps = 8;
+constexpr int kFirstEpiWarp = 4;
+constexpr int kThreads = 32 * (kFirstEpiWarp + kEpiWarps);
+constexpr int kMaxStages = 8;
+constexpr int kMaxAStages = 8;
+constexpr int kAccBufs = 4;                 // 4 x 128 columns = all of TMEM
+
+struct Maps {
+  CUtensorMap w[LSW_NKIND];   // W [L, d_out, d_in], box {64, 128, 1}, 128B swizzle
+  CUtensorMap p[LSW_NKIND];   // pristine copies (RESTORE source), same geometry
+};
+
+struct Geom {
+  TileKinds tk;
+  const __nv_bfloat16* At[LSW_NKIND];   // packed A^T [L, col_tiles, N, 128, rp], pre-swizzled
+  const __nv_bfloat16* Bp[LSW_NKIND];   // packed B   [L*N, dout_pad, rp], pre-swizzled
+  int64_t dout_pad[LSW_NKIND];
+  int64_t tiles_total;
+  int32_t n_experts, rp;
+  int32_t w_stages, a_stages, b_bufs;
+  uint32_t term_bytes;                  // one term's 128 x rp operand slice (A^T of a tile, or B of a strip)
+  uint32_t a_stage_bytes, b_buf_bytes;  // A stage: all terms of one tile; B buffer: (hi, lo) of all terms
+  uint32_t swz_mode;                    // UMMA layout type of the r-wide operands
+  uint32_t smem_bytes;
+};
+
+struct TcPlan {
+  Maps maps;
+  Geom geom;
+  int32_t chunk = 48;
+  void* packed_At[LSW_NKIND] = {};
+  void* packed_B[LSW_NKIND] = {};
+  int64_t bytes = 0;
+  int grid = 0;
+};
+
+struct Args {
+  Geom g;
+  int32_t chunk;
+  int32_t mode, top_k, n_experts;
+  float scale;
+  const int32_t* cur_idx;
+  const float* cur_g;
+  DevState* state;
+  int64_t t0, t_count;        // tile range of this launch (t_count = 0: all tiles)
+};
+
+// ------------------------------------------------------------------ fold
+
+// Eight bf16 B elements -> (hi, lo) parts of c * b: x = fl32(c * b),
+// hi = RNE_bf16(x), lo = RNE_bf16(x - hi) (x - hi is exact in fp32), so
+// hi + lo = x to within 2^-16 |x| (R13: the coefficient is not rounded to bf16).
+__device__ __forceinline__ void fold8(const uint4 raw, float c, uint4& hi, uint4& lo) {
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float x0 = c * __uint_as_float(w[q] << 16), x1 = c * __uint_as_float(w[q] & 0xffff0000u);
+    const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
+    const float2 hf = __bfloat1622float2(hb);
+    const __nv_bfloat162 lb = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
+    h[q] = *reinterpret_cast<const uint32_t*>(&hb);
+    l[q] = *reinterpret_cast<const uint32_t*>(&lb);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// ------------------------------------------------------------------ epilogue
+
+// W (bf16, 128B-swizzled sub-tile row) + 16 accumulator columns -> RNE in place
+__device__ __forceinline__ void epi16(uint8_t* wrow, int row, int col16, const uint32_t* acc) {
+  uint4* p0 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 0) ^ (row & 7)) << 4));
+  uint4* p1 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 1) ^ (row & 7)) << 4));
+  const uint4 u0 = *p0, u1 = *p1;
+  const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+  uint32_t o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint64_t v = fadd2(f2_pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u)),
+                             f2_pack(__uint_as_float(acc[2 * q]), __uint_as_float(acc[2 * q + 1])));
+    o[q] = f2_to_bf16x2(v);
+  }
+  *p0 = make_uint4(o[0], o[1], o[2], o[3]);
+  *p1 = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+// ------------------------------------------------------------------ the kernel
+
+__global__ void __launch_bounds__(kThreads, 1)
+switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ Coefs cf;
+  __shared__ int32_t s_parity;
+  __shared__ uint32_t s_tmem_base;
+  __shared__ __align__(8) uint64_t bar_wfull[kMaxStages], bar_wempty[kMaxStages], bar_wdone[kMaxStages];
+  __shared__ __align__(8) uint64_t bar_afull[kMaxAStages], bar_aempty[kMaxAStages];
+  __shared__ __align__(8) uint64_t bar_braw[2], bar_bfull[2], bar_bempty[2];
+  __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
+
+  const Geom& g = args.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // shared layout (1 KB aligned): [w_stages x W tile][a_stages x A slices][b_bufs x (hi, lo) B strip]
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* wst0 = base;
+  uint8_t* ast0 = wst0 + (size_t)g.w_stages * (2 * kSubBytes);
+  uint8_t* bst0 = ast0 + (size_t)g.a_stages * g.a_stage_bytes;
+
+  if (threadIdx.x == 0) {
+    SwitchParams p{};
+    p.mode = args.mode;
+    p.top_k = args.top_k;
+    p.n_experts = args.n_experts;
+    p.scale = args.scale;
+    p.cur_idx = args.cur_idx;
+    p.cur_g = args.cur_g;
+    p.state = args.state;
+    const int32_t parity = *(volatile int32_t*)&args.state->parity;
+    s_parity = parity;
+    build_coefs(p, parity, cf);
+    if (blockIdx.x == 0 && !cf.bad) stage_decision(p, parity);
+    for (int s = 0; s < g.w_stages; ++s) {
+      mbar_init(smem_u32(&bar_wfull[s]), 1);
+      mbar_init(smem_u32(&bar_wempty[s]), 1);
+      mbar_init(smem_u32(&bar_wdone[s]), kEpiWarps);
+    }
+    for (int s = 0; s < g.a_stages; ++s) {
+      mbar_init(smem_u32(&bar_afull[s]), 1);
+      mbar_init(smem_u32(&bar_aempty[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(&bar_braw[s]), 1);
+      mbar_init(smem_u32(&bar_bfull[s]), 1);
+      mbar_init(smem_u32(&bar_bempty[s]), 1);
+    }
+    for (int s = 0; s < kAccBufs; ++s) {
+      mbar_init(smem_u32(&bar_accfull[s]), 1);
+      mbar_init(smem_u32(&bar_accempty[s]), kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0)
+    for (int k = 0; k < LSW_NKIND; ++k) prefetch_map(args.mode == MODE_RESTORE ? &maps.p[k] : &maps.w[k]);
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(&s_tmem_base)), "r"(kAccBufs * kTN) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  const int nt = cf.bad ? 0 : cf.n;
+  TileSeq seq;
+  seq.T = args.t_count > 0 ? args.t_count : g.tiles_total;
+  seq.t0 = args.t0;
+  seq.chunk = args.chunk < 1 ? 1 : args.chunk;
+  seq.G = gridDim.x;
+  seq.b = blockIdx.x;
+  const TileKinds& tk = g.tk;
+  const uint32_t tmem_base = s_tmem_base;
+
+  if (nt > 0) {
+    if (warp == 0) {
+      // ============================ W producer =============================
+      if (lane == 0) {
+        const uint64_t pol_stream = policy_evict_first();
+        const CUtensorMap* src = args.mode == MODE_RESTORE ? maps.p : maps.w;   // RESTORE reads P
+        Ring wring{0, 0, (uint32_t)g.w_stages};
+        for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+          mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
+          const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
+          mbar_expect_tx(wbar, 2 * kSubBytes);
+          uint8_t* wdst = wst0 + (size_t)wring.i * (2 * kSubBytes);
+          for (int sb = 0; sb < 2; ++sb)
+            tma_load_3d(smem_u32(wdst + sb * kSubBytes), &src[c.kd], c.cb * kTN + sb * kSubCols, c.rb * kTM,
+                        c.layer, wbar, pol_stream);
+          wring.next();
+        }
+      }
+    } else if (warp == 2) {
+      // ============================ store warp ==============================
+      if (lane == 0) {
+        const uint64_t pol_stream = policy_evict_first();
+        Ring wring{0, 0, (uint32_t)g.w_stages};
+        for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+          mbar_wait(smem_u32(&bar_wdone[wring.i]), wring.phase);     // epilogue wrote the tile
+          uint8_t* wsrc = wst0 + (size_t)wring.i * (2 * kSubBytes);
+          for (int sb = 0; sb < 2; ++sb)
+            tma_store_3d(&maps.w[c.kd], smem_u32(wsrc + sb * kSubBytes), c.cb * kTN + sb * kSubCols, c.rb * kTM,
+                         c.layer, pol_stream);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read -> stage reusable
+          mbar_arrive(smem_u32(&bar_wempty[wring.i]));
+          wring.next();
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      }
+    } else if (warp == 3) {
+      // ============================ operand producer ========================
+      // Per strip (rare): raw B slices of all terms by bulk copies into the lo
+      // slots, then the whole warp folds them into (hi, lo) parts in place and
+      // publishes the buffer to the MMA warp (generic -> async proxy fence).
+      // Per tile: all terms' A^T slices (each one contiguous block) into one A
+      // stage, released by the epilogue once the tile's accumulator is complete.
+      const uint64_t pol_keep = policy_evict_last();
+      const size_t rpe = (size_t)g.rp;
+      const uint32_t tb = g.term_bytes;
+      const uint32_t vec_per_term = tb / 16;
+      int64_t strip_prev = -1;
+      Ring bring{0, 0, (uint32_t)g.b_bufs};
+      Ring aring{0, 0, (uint32_t)g.a_stages};
+      for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+        if (strip_id(c) != strip_prev) {
+          if (strip_prev >= 0) bring.next();
+          strip_prev = strip_id(c);
+          mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
+          uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
+          const uint32_t rbar = smem_u32(&bar_braw[bring.i]);
+          if (lane == 0) {
+            mbar_expect_tx(rbar, nt * tb);
+            for (int j = 0; j < nt; ++j) {
+              const __nv_bfloat16* src = g.Bp[c.kd] + (((size_t)c.layer * g.n_experts + cf.e[j]) * g.dout_pad[c.kd] +
+                                                       (size_t)c.rb * kTM) * rpe;
+              bulk_load(smem_u32(dst + (2 * j + 1) * tb), src, tb, rbar, pol_keep);
+            }
+          }
+          mbar_wait(rbar, bring.phase);
+          for (uint32_t v = lane; v < (uint32_t)nt * vec_per_term; v += 32) {
+            const uint32_t j = v / vec_per_term, o = (v - j * vec_per_term) * 16;
+            uint4* plo = reinterpret_cast<uint4*>(dst + (2 * j + 1) * tb + o);
+            uint4 hi, lo;
+            fold8(*plo, cf.c[j], hi, lo);
+            *reinterpret_cast<uint4*>(dst + 2 * j * tb + o) = hi;
+            *plo = lo;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bar_bfull[bring.i]));
+        }
+        if (lane == 0) {
+          const __nv_bfloat16* blk =
+              g.At[c.kd] + (((size_t)c.layer * tk.col_tiles[c.kd] + c.cb) * g.n_experts) * (size_t)kTN * rpe;
+          mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
+          uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
+          const uint32_t bar = smem_u32(&bar_afull[aring.i]);
+          mbar_expect_tx(bar, nt * tb);
+          for (int j = 0; j < nt; ++j)
+            bulk_load(smem_u32(adst + j * tb), blk + (size_t)cf.e[j] * kTN * rpe, tb, bar, pol_keep);
+        }
+        __syncwarp();
+        aring.next();
+      }
+    } else if (warp == 1) {
+      // ============================ MMA issuer ==============================
+      // One chain per tile: for every term, the hi and lo parts times the A^T
+      // slice, K = rp each in steps of 16, into the tile's single accumulator;
+      // ONE commit per tile.
+      // instruction descriptor: D f32, A/B bf16, both K-major, N = 128, M = 128
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTN >> 3) << 17) |
+                             ((uint32_t)(kTM >> 4) << 24);
+      const uint32_t sbo = 8 * (uint32_t)g.rp * 2;
+      const int ksteps = g.rp / 16;
+      const uint64_t desc0 = umma_desc(0, sbo, g.swz_mode);
+      const uint64_t term = g.term_bytes >> 4;
+      Ring bring{0, 0, (uint32_t)g.b_bufs};
+      Ring aring{0, 0, (uint32_t)g.a_stages};
+      Ring acc{0, 0, (uint32_t)kAccBufs};
+      int64_t strip_prev = -1;
+      for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+        if (strip_id(c) != strip_prev) {
+          if (strip_prev >= 0) bring.next();
+          strip_prev = strip_id(c);
+          mbar_wait(smem_u32(&bar_bfull[bring.i]), bring.phase);
+        }
+        mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
+        mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
+        tc_fence_after();
+        const uint64_t b_desc = desc0 + (smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes) >> 4);
+        const uint64_t a_desc = desc0 + (smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes) >> 4);
+        const uint32_t d = tmem_base + acc.i * kTN;
+        if (elect_one()) {
+          for (int j = 0; j < nt; ++j)
+            for (int part = 0; part < 2; ++part)
+              for (int kk = 0; kk < ksteps; ++kk)
+                umma_f16(d, b_desc + (2 * j + part) * term + kk * 2, a_desc + j * term + kk * 2, idesc,
+                         (j | part | kk) != 0 ? 1u : 0u);
+          umma_commit(smem_u32(&bar_accfull[acc.i]));
+        }
+        __syncwarp();
+        acc.next();
+        aring.next();
+      }
+    } else if (warp >= kFirstEpiWarp) {
+      // ============================ epilogue ================================
+      // Warp w reads TMEM lane quarter w % 4 (rows 32*(w%4) ..) and one 64-column
+      // half of the tile (= one W sub-tile): per thread one row x 64 columns.
+      const int ew = warp - kFirstEpiWarp;
+      const int quarter = warp & 3, half = ew >> 2;
+      const int row = quarter * 32 + lane;
+      const bool releaser = ew == 0 && lane == 0;   // frees A stages / B strips for the producer
+      Ring wring{0, 0, (uint32_t)g.w_stages};
+      Ring acc{0, 0, (uint32_t)kAccBufs};
+      Ring aring{0, 0, (uint32_t)g.a_stages}, bring{0, 0, (uint32_t)g.b_bufs};
+      int64_t bstrip = -1;
+      for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+        if (releaser) {
+          // first tile of a new strip: every MMA of the previous strip is done
+          // (its last accumulator has been seen), so its B buffer is free
+          const int64_t st = strip_id(c);
+          if (st != bstrip) {
+            if (bstrip >= 0) {
+              mbar_arrive(smem_u32(&bar_bempty[bring.i]));
+              bring.next();
+            }
+            bstrip = st;
+          }
+        }
+        mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);      // the tile's MMAs are complete
+        if (releaser) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
+        aring.next();
+        tc_fence_after();
+        const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTN + half * kSubCols;
+        uint32_t a[4][16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tmem_ld16(tm + q * 16, a[q]);
+        tmem_wait_ld();
+        tc_fence_before();                         // accumulator consumed -> MMA may reuse the buffer
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+        acc.next();
+        mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);      // W tile landed
+        uint8_t* wrow = wst0 + (size_t)wring.i * (2 * kSubBytes) + half * kSubBytes + row * 128;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) epi16(wrow, row, q, a[q]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> TMA store
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
+        wring.next();
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAccBufs * kTN)
+                 : "memory");
+  }
+  if (threadIdx.x == 0) {
+    SwitchParams p{};
+    p.mode = args.mode;
+    p.state = args.state;
+    finish_pass(p, s_parity, cf);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static bool encode_w(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d_out, uint64_t L) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {d_in, d_out, L};
+  cuuint64_t strides[2] = {d_in * 2, d_in * d_out * 2};
+  cuuint32_t box[3] = {(cuuint32_t)kSubCols, (cuuint32_t)kTM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static uint32_t align1k(uint32_t x) { return (x + 1023) & ~1023u; }
+
+// The tensor-core work of a tile relative to its HBM time: 2 * nt * rp / 16
+// MMAs of 128 x 128 x 16 (~35-55 ns each) against ~1.5 us of W traffic.
+int fc_mmas_per_tile(const SwitchParams& sp) {
+  const int rp = sp.rank <= 16 ? 16 : sp.rank <= 32 ? 32 : 64;
+  return 2 * (2 * sp.top_k) * rp / 16;
+}
+
+cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, const char** why) {
+  *out = nullptr;
+  int dev = 0, major = 0, minor = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) { *why = "needs an sm_100 (B200) device"; return cudaErrorNotSupported; }
+  const int r = sp.rank, rp = r <= 16 ? 16 : r <= 32 ? 32 : 64;
+  if (r > 64) { *why = "rank > 64"; return cudaErrorNotSupported; }
+  TcPlan* plan = new TcPlan();
+  Geom& g = plan->geom;
+  memset(&g, 0, sizeof(g));
+  g.tk.n_layers = sp.n_layers;
+  g.n_experts = sp.n_experts;
+  g.rp = rp;
+  g.swz_mode = rp == 16 ? 6u : rp == 32 ? 4u : 2u;        // SWIZZLE_32B / 64B / 128B (UMMA encoding)
+  g.term_bytes = kTM * rp * 2;
+  const int mt = 2 * sp.top_k;
+  g.a_stage_bytes = align1k((uint32_t)mt * g.term_bytes);
+  g.b_buf_bytes = align1k((uint32_t)(2 * mt) * g.term_bytes);
+  const uint32_t w_stage = 2 * kSubBytes;
+  // Shared-memory plan: first W stages >= 4, B double-buffered, A stages >= 3,
+  // then relax (B single, A 2, W 3); what is left goes to more W stages.
+  const int64_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
+  struct Try { int ws, bb, as; };
+  const Try tries[] = {{4, 2, 3}, {4, 1, 3}, {4, 2, 2}, {4, 1, 2}, {3, 2, 2}, {3, 1, 2}, {2, 1, 2}};
+  int bb_env = 0, as_env = 0, ws_env = 0;
+  if (const char* v = getenv("LSW_FC_BBUFS")) bb_env = atoi(v);
+  if (const char* v = getenv("LSW_FC_ASTAGES")) as_env = atoi(v);
+  if (const char* v = getenv("LSW_FC_STAGES")) ws_env = atoi(v);
+  bool ok = false;
+  for (const Try& t : tries) {
+    const int bb = bb_env >= 1 && bb_env <= 2 ? bb_env : t.bb;
+    const int as = as_env >= 2 && as_env <= kMaxAStages ? as_env : t.as;
+    const int64_t rest = budget - (int64_t)bb * g.b_buf_bytes - (int64_t)as * g.a_stage_bytes;
+    if (rest < (int64_t)t.ws * w_stage) continue;
+    int ws = (int)(rest / w_stage);
+    if (ws > kMaxStages) ws = kMaxStages;
+    if (ws_env >= 2 && ws_env < ws) ws = ws_env;
+    g.w_stages = ws;
+    g.a_stages = as;
+    g.b_bufs = bb;
+    ok = true;
+    break;
+  }
+  if (!ok) { delete plan; *why = "shared memory: rank * top_k too large for the folded kernel"; return cudaErrorNotSupported; }
+  if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
+  g.smem_bytes = g.w_stages * w_stage + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
+  // tiles
+  int64_t t = 0;
+  for (int k = 0; k < LSW_NKIND; ++k) {
+    const KindGeom& kg = sp.kind[k];
+    g.tk.row_tiles[k] = (int32_t)((kg.d_out + kTM - 1) / kTM);
+    g.tk.col_tiles[k] = (int32_t)((kg.d_in + kTN - 1) / kTN);
+    g.dout_pad[k] = (int64_t)g.tk.row_tiles[k] * kTM;
+    g.tk.tile_begin[k] = t;
+    t += (int64_t)sp.n_layers * g.tk.row_tiles[k] * g.tk.col_tiles[k];
+  }
+  g.tiles_total = t;
+  plan->grid = (int)(t < num_sms ? t : num_sms);
+  if (const char* v = getenv("LSW_TC_GRID")) { int x = atoi(v); if (x >= 1 && x < plan->grid) plan->grid = x; }
+  if (plan->grid < 1) plan->grid = 1;
+  // pack operands + encode maps (same packed images as the term-group kernel,
+  // with 128-column A^T blocks)
+  const int64_t M = (int64_t)sp.n_layers * sp.n_experts;
+  cudaError_t e = cudaSuccess;
+  for (int k = 0; k < LSW_NKIND && e == cudaSuccess; ++k) {
+    const KindGeom& kg = sp.kind[k];
+    const int64_t din_pad = (int64_t)g.tk.col_tiles[k] * kTN;
+    const size_t at_bytes = (size_t)M * din_pad * rp * 2;
+    const size_t b_bytes = (size_t)M * g.dout_pad[k] * rp * 2;
+    e = cudaMalloc(&plan->packed_At[k], at_bytes);
+    if (e != cudaSuccess) break;
+    e = cudaMalloc(&plan->packed_B[k], b_bytes);
+    if (e != cudaSuccess) break;
+    plan->bytes += at_bytes + b_bytes;
+    pack_At_kernel<<<2048, 256>>>((const __nv_bfloat16*)kg.A, (__nv_bfloat16*)plan->packed_At[k], sp.n_layers,
+                                  sp.n_experts, r, rp, kg.d_in, g.tk.col_tiles[k], kTN);
+    pack_B_kernel<<<2048, 256>>>((const __nv_bfloat16*)kg.B, (__nv_bfloat16*)plan->packed_B[k], M, r, rp,
+                                 kg.d_out, g.dout_pad[k]);
+    g.At[k] = (const __nv_bfloat16*)plan->packed_At[k];
+    g.Bp[k] = (const __nv_bfloat16*)plan->packed_B[k];
+    if (!encode_w(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers)) {
+      *why = "cuTensorMapEncodeTiled failed";
+      e = cudaErrorInvalidValue;
+    }
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(switch_fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+  if (e != cudaSuccess) {
+    if (!*why || !**why) *why = cudaGetErrorString(e);
+    tc_plan_destroy(plan);
+    return e;
+  }
+  *out = plan;
+  return cudaSuccess;
+}
+
+void tc_plan_destroy(TcPlan* plan) {
+  if (!plan) return;
+  for (int k = 0; k < LSW_NKIND; ++k) {
+    cudaFree(plan->packed_At[k]);
+    cudaFree(plan->packed_B[k]);
+  }
+  delete plan;
+}
+
+int64_t tc_plan_bytes(const TcPlan* plan) { return plan ? plan->bytes : 0; }
+int tc_plan_grid(const TcPlan* plan) { return plan ? plan->grid : 0; }
+int tc_plan_tile_n(const TcPlan* plan) { return plan ? kTN : 0; }
+int64_t tc_plan_tiles(const TcPlan* plan) { return plan ? plan->geom.tiles_total : 0; }
+
+cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& sp) {
+  for (int k = 0; k < LSW_NKIND; ++k)
+    if (!sp.kind[k].P ||
+        !encode_w(&plan->maps.p[k], sp.kind[k].P, sp.kind[k].d_in, sp.kind[k].d_out, sp.n_layers))
+      return cudaErrorInvalidValue;
+  return cudaSuccess;
+}
+
+int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t0) {
+  const Geom& g = plan->geom;
+  const int64_t per = (int64_t)g.tk.row_tiles[kind] * g.tk.col_tiles[kind];
+  *t0 = g.tk.tile_begin[kind] + (int64_t)layer * per;
+  return per;
+}
+
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0,
+                             int64_t t_count) {
+  Args a;
+  a.t0 = t0;
+  a.t_count = t_count;
+  a.g = plan->geom;
+  a.chunk = plan->chunk;
+  a.mode = p.mode;
+  a.top_k = p.top_k;
+  a.n_experts = p.n_experts;
+  a.scale = p.scale;
+  a.cur_idx = p.cur_idx;
+  a.cur_g = p.cur_g;
+  a.state = p.state;
+  switch_fc_kernel<<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  return cudaGetLastError();
+}
+
+}  // namespace fc
+}  // namespace lsw

@@ -8,6 +8,10 @@
 //   tg (switch_tc_tg.cu): a tile's terms stream through TMEM tg at a time
 //      with an fp32 running sum in the epilogue, A slices staged per
 //      (sub-tile, term group): any k <= 4, any r <= 64.
+//   fc (switch_tc_fc.cu): the coefficients folded into the B factors as exact
+//      (hi, lo) bf16 pairs, ONE accumulator and one commit per 128 x 128 tile
+//      (Eq. 5's concatenation, K = 2 * sum_j rp): twice the tensor-core work,
+//      a fraction of the epilogue's TMEM reads and FMAs and of the commits.
 #pragma once
 
 #include "lsw_internal.cuh"
@@ -56,4 +60,25 @@ int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t
 int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);
 cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
 }  // namespace tg
+
+namespace fc {
+struct TcPlan;
+// tcgen05.mma instructions (128 x 128 x 16) per tile at 2k terms
+int fc_mmas_per_tile(const SwitchParams& geom);
+cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why);
+void tc_plan_destroy(TcPlan* plan);
+int64_t tc_plan_bytes(const TcPlan* plan);
+int tc_plan_grid(const TcPlan* plan);
+int tc_plan_tile_n(const TcPlan* plan);
+int64_t tc_plan_tiles(const TcPlan* plan);
+cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0 = 0,
+                             int64_t t_count = 0);
+int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t0);
+cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
+}  // namespace fc
+
+// the fc kernel is the default from kFcMinMmas MMAs per tile on (i.e. unless
+// 2k * rp <= 32, where tg is ~1 % faster), wherever its shared-memory plan fits
+// (measured, scripts/sweep_bench.py)
+constexpr int kFcMinMmas = 8;
 }  // namespace lsw

@@ -1,0 +1,275 @@
+// tc_common.cuh -- PTX wrappers, tile walk and operand packing for the
+// folded-coefficient tensor-core switch kernel (switch_tc_fc.cu).  Internal;
+// the v1 and term-group kernels keep their own copies so that their compiled
+// code stays exactly as measured.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "lsw_internal.cuh"
+
+namespace lsw {
+namespace tcx {
+
+// ------------------------------------------------------------------ PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Wait for the phase with parity `parity` to complete.  A watchdog traps after
+// ~20 s so a protocol bug fails the launch instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  if (mbar_try(bar, parity)) return;
+  const uint64_t t0 = globaltimer();
+  uint32_t n = 0;
+  while (!mbar_try(bar, parity)) {
+    if ((++n & 1023u) == 0 && globaltimer() - t0 > 20000000000ull) __trap();
+  }
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            int32_t c2, uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int32_t c0, int32_t c1,
+                                             int32_t c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
+      ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(src), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// 1-D bulk copy global -> shared, completion on an mbarrier (transaction bytes)
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                          uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+
+// UMMA shared-memory descriptor (K-major, swizzled): start>>4 [0,14), LBO>>4
+// [16,30) (unused for swizzled K-major; 1), SBO>>4 [32,46) = 8 rows * row
+// bytes, version 1 at [46,48), layout type [61,64).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t sbo_bytes, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7) << 61;
+  return d;
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// elect.sync: true in exactly one lane of the (converged) warp
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}" : "=r"(p));
+  return p != 0;
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// ------------------------------------------------------------------ fp32x2 / bf16 helpers
+
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  __nv_bfloat162 b2 = __floats2bfloat162_rn(lo, hi);     // RNE, lo -> low half
+  return *reinterpret_cast<uint32_t*>(&b2);
+}
+
+// ------------------------------------------------------------------ tile walk
+
+// Per-CTA tile sequence over the global (kind, layer, row block, column block)
+// order: chunks of `chunk` consecutive tiles dealt round-robin to the CTAs, so a
+// CTA walks along 128-row strips while all CTAs sweep ~one matrix at a time.
+struct Cursor {
+  int64_t t;             // global tile index, -1 when done
+  int32_t kd, layer, rb, cb;
+};
+
+struct TileSeq {
+  int64_t T, t0;         // T tiles of this launch, starting at global tile t0
+  int32_t chunk, G, b;
+};
+
+struct TileKinds {
+  int64_t tile_begin[LSW_NKIND];
+  int32_t row_tiles[LSW_NKIND], col_tiles[LSW_NKIND];
+  int32_t n_layers;
+};
+
+__device__ __forceinline__ void cursor_set(const TileKinds& g, Cursor& c, int64_t t) {
+  c.t = t;
+  if (t < 0) return;
+  int kd = 0;
+  while (kd + 1 < LSW_NKIND && t >= g.tile_begin[kd + 1]) ++kd;
+  int64_t local = t - g.tile_begin[kd];
+  const int64_t per_layer = (int64_t)g.row_tiles[kd] * g.col_tiles[kd];
+  c.kd = kd;
+  c.layer = (int)(local / per_layer);
+  local -= (int64_t)c.layer * per_layer;
+  c.rb = (int)(local / g.col_tiles[kd]);
+  c.cb = (int)(local - (int64_t)c.rb * g.col_tiles[kd]);
+}
+
+__device__ __forceinline__ Cursor cursor_first(const TileKinds& g, const TileSeq& q) {
+  Cursor c;
+  const int64_t t = (int64_t)q.b * q.chunk < q.T ? (int64_t)q.b * q.chunk : -1;
+  cursor_set(g, c, t < 0 ? -1 : q.t0 + t);
+  return c;
+}
+
+__device__ __forceinline__ void cursor_next(const TileKinds& g, const TileSeq& q, Cursor& c) {
+  const int64_t t1 = c.t + 1, r1 = t1 - q.t0;
+  if (r1 % q.chunk != 0 && r1 < q.T) {
+    c.t = t1;
+    if (++c.cb == g.col_tiles[c.kd]) {
+      c.cb = 0;
+      if (++c.rb == g.row_tiles[c.kd]) {
+        c.rb = 0;
+        if (++c.layer == g.n_layers) { c.layer = 0; ++c.kd; }
+      }
+    }
+    return;
+  }
+  const int64_t nq = (c.t - q.t0) / q.chunk + q.G;
+  cursor_set(g, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
+}
+
+__device__ __forceinline__ int64_t strip_id(const Cursor& c) { return c.t - c.cb; }
+
+// ring position: stage index + phase bit, advanced without division
+struct Ring {
+  uint32_t i, phase, n;
+  __device__ __forceinline__ void next() { if (++i == n) { i = 0; phase ^= 1u; } }
+};
+
+// ------------------------------------------------------------------ operand packing
+
+// Pre-swizzled K-major operand image: element (row, k) of a [rows, rp] operand
+// goes to 16-byte chunk (k/8) ^ f(row) of its row, f = the TMA/UMMA swizzle of
+// row-byte width RB = 2*rp (32B: (row>>2)&1, 64B: (row>>1)&3, 128B: row&7), so
+// a 1-D bulk copy of 128 rows to a 1 KB-aligned shared address reproduces what a
+// swizzled TMA load would have written.  Rows >= n_rows and ranks >= r are 0.
+__device__ __forceinline__ int64_t swz_off(int64_t row, int k, int rp) {
+  const int rb = 2 * rp;
+  const int f = (int)((row * rb / 128) & (rb / 16 - 1));
+  return row * rp + (((k >> 3) ^ f) << 3) + (k & 7);
+}
+
+// A [L, N, r, d_in] -> A^T blocks [L, col_tiles, N, tc, rp] (tc = tile columns):
+// block (l, cb) holds, expert after expert, the pre-swizzled [tc, rp] slice
+// A_{l,e}^T[cb*tc : cb*tc + tc, :] (zero beyond d_in / r).
+static __global__ void pack_At_kernel(const __nv_bfloat16* __restrict__ A, __nv_bfloat16* __restrict__ At,
+                                      int64_t L, int N, int r, int rp, int64_t d_in, int64_t col_tiles, int tc) {
+  const int64_t din_pad = col_tiles * tc;
+  const int64_t total = L * N * din_pad * rp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % rp);
+    const int64_t c = (i / rp) % din_pad;
+    const int64_t m = i / ((int64_t)rp * din_pad);       // l * N + e
+    const int64_t l = m / N, e = m % N;
+    const __nv_bfloat16 v = (k < r && c < d_in) ? A[(m * r + k) * d_in + c] : __float2bfloat16(0.f);
+    const int64_t blk = (l * col_tiles + c / tc) * N + e;
+    At[blk * tc * rp + swz_off(c % tc, k, rp)] = v;
+  }
+}
+
+// B [M, d_out, r] -> [M, dout_pad, rp]
+static __global__ void pack_B_kernel(const __nv_bfloat16* __restrict__ B, __nv_bfloat16* __restrict__ Bp, int64_t M,
+                                     int r, int rp, int64_t d_out, int64_t dout_pad) {
+  const int64_t total = M * dout_pad * rp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % rp);
+    const int64_t row = (i / rp) % dout_pad;
+    const int64_t m = i / ((int64_t)rp * dout_pad);
+    const __nv_bfloat16 v = (k < r && row < d_out) ? B[(m * d_out + row) * r + k] : __float2bfloat16(0.f);
+    Bp[m * dout_pad * rp + swz_off(row, k, rp)] = v;
+  }
+}
+
+}  // namespace tcx
+}  // namespace lsw

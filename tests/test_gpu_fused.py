@@ -79,16 +79,47 @@ def test_fused_token_equals_separate_path(monkeypatch, name, grid):
                         yo += d_out
 
 
-def test_fused_unsupported_for_term_group_kernel(monkeypatch):
-    monkeypatch.setenv("LSW_TC_KERNEL", "tg")
+@pytest.mark.parametrize("kernel", ["fc", "tg"])
+def test_fused_on_a_ctx_that_switches_with_another_kernel(monkeypatch, kernel):
+    """The fused launch exists in the v1 kernel only; a ctx whose switch kernel
+    is fc or tg builds a v1 plan for it on first use.  Plain tokens (the ctx's
+    own kernel) and fused tokens (v1) alternate on the same W and decision
+    slot: W stays on the oracle's stored trajectory and every token's outputs
+    match the oracle's GEMV on it."""
+    monkeypatch.setenv("LSW_TC_KERNEL", kernel)
     cfg = synth.get_config("mini")
     W, A, B, router = H.build_weights(cfg, "cuda")
     sw = H.make_switch(cfg, W, A, B, router, impl="tc")
     info = sw.info()
-    xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
+    assert info["switch_kernel"] == {"tg": 2, "fc": 3}[kernel]
+    Ws = {(kd, l): _f64(W[kd][l]) for kd in synth.KINDS for l in range(cfg.n_layers)}
+    As = {(kd, l): _f64(A[kd][l]) for kd in synth.KINDS for l in range(cfg.n_layers)}
+    Bs = {(kd, l): _f64(B[kd][l]) for kd in synth.KINDS for l in range(cfg.n_layers)}
+    orc = O.OracleModel(_f64(router), Ws, As, Bs, cfg.top_k, cfg.alpha, cfg.rank, "bf16")
+    X1 = synth.gen_x1(cfg, 4, "cuda")
+    xs_d = synth.gen_xs(cfg, "cuda")
+    xs = H.pack_xs(cfg, xs_d)
     ys = torch.empty(info["ys_elems"], device="cuda")
     idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
     gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
-    with pytest.raises(L.LswError) as ei:
-        sw.decode_token_fused(synth.gen_x1(cfg, 1, "cuda")[0], xs, ys, idx, gate)
-    assert "UNSUPPORTED" in str(ei.value)
+    for t in range(4):
+        if t % 2:
+            sw.decode_token_fused(X1[t], xs, ys, idx, gate)
+        else:
+            sw.decode_token(X1[t], xs, ys, idx, gate)
+        torch.cuda.synchronize()
+        assert sw.device_status() == 0
+        idx_o, g_o, _ = orc.route(_f64(X1[t]))
+        assert idx.cpu().tolist() == idx_o.tolist()
+        orc.merge_all_layers((idx_o.tolist(), g_o.tolist()))
+        yb = ys.cpu().numpy()
+        yo = 0
+        for l in range(cfg.n_layers):
+            for gi, grp in enumerate(synth.GROUPS):
+                x = _f64(xs_d[(l, gi)])
+                for kd in grp:
+                    assert PT.allclose_frac_fail(_f64(W[kd][l]), orc.W[(kd, l)]) == 0.0, (t, l, kd)
+                    d_out = cfg.kind_shape(kd)[0]
+                    ref = O.gemv(orc.W[(kd, l)], x)
+                    assert PT.allclose_frac_fail(yb[yo:yo + d_out], ref) == 0.0, (t, l, kd)
+                    yo += d_out

@@ -108,7 +108,9 @@ def test_switch_trajectory_full_elements(name, impl):
 
 
 TC_VARIANTS = [("v1", {}), ("v1", {"LSW_TC_SPLIT": "1"}), ("tg", {}), ("tg", {"LSW_TC_TG": "1"}),
-               ("tg", {"LSW_TC_TG": "2"}), ("tg", {"LSW_TC_MMA2": "0"}), ("tg", {"LSW_TC_MMA2": "1", "LSW_TC_TG": "1"})]
+               ("tg", {"LSW_TC_TG": "2"}), ("tg", {"LSW_TC_MMA2": "0"}), ("tg", {"LSW_TC_MMA2": "1", "LSW_TC_TG": "1"}),
+               ("fc", {}), ("fc", {"LSW_FC_BBUFS": "1", "LSW_FC_ASTAGES": "2"})]
+KERNEL_ID = {"v1": 1, "tg": 2, "fc": 3}
 
 
 @pytest.mark.parametrize("grid", [1, 3])
@@ -117,10 +119,11 @@ TC_VARIANTS = [("v1", {}), ("v1", {"LSW_TC_SPLIT": "1"}), ("tg", {}), ("tg", {"L
 def test_tc_switch_many_tiles_per_cta(monkeypatch, name, variant, grid):
     """The mini shapes give every CTA a single tile at the default grid; force a
     tiny grid so every ring (W, A, B, TMEM accumulators) wraps many times, for
-    both tensor-core kernels: v1 (per-term accumulators; split mode: pre-scaled
-    B parts) and the term-group kernel with its default, 1- and 2-term groups
+    the tensor-core kernels: v1 (per-term accumulators; split mode: pre-scaled
+    B parts), the term-group kernel with its default, 1- and 2-term groups
     (a tile's terms then stream through several TMEM buffers into one fp32
-    running sum)."""
+    running sum) and the folded-coefficient kernel (one accumulator per tile;
+    single B buffer: every strip change waits for the previous strip's MMAs)."""
     kernel, env = TC_VARIANTS[variant]
     monkeypatch.setenv("LSW_TC_GRID", str(grid))
     monkeypatch.setenv("LSW_TC_KERNEL", kernel)
@@ -131,11 +134,11 @@ def test_tc_switch_many_tiles_per_cta(monkeypatch, name, variant, grid):
         pytest.skip("group larger than the term list")
     try:
         S = Setup(name, "tc", n_tokens=6)
-    except L.LswError as e:           # v1 / split mode have no plan for this shape
-        assert kernel == "v1" and "UNSUPPORTED" in str(e)
+    except L.LswError as e:           # v1 / split mode / fc have no plan for this shape
+        assert kernel in ("v1", "fc") and "UNSUPPORTED" in str(e)
         pytest.skip(str(e))
     info = S.sw.info()
-    assert info["grid"] == grid and info["switch_kernel"] == (1 if kernel == "v1" else 2)
+    assert info["grid"] == grid and info["switch_kernel"] == KERNEL_ID[kernel]
     worst = _run_token_checks(S, 5)
     print(f"{name} {kernel} {env} grid={grid}: worst {worst}")
 

@@ -35,7 +35,7 @@ def _ctx(cfg, impl):
     return sw, W, A, B, router, P
 
 
-CASES = [("toy", "simt", None), ("mini", "tc", "v1"), ("mini", "tc", "tg"), ("mini-r4k4", "tc", None),
+CASES = [("toy", "simt", None), ("mini", "tc", "v1"), ("mini", "tc", "tg"), ("mini", "tc", "fc"), ("mini-r4k4", "tc", None),
          ("mini-r64k3", "tc", None), ("mini-k1", "tc", None)]
 
 
@@ -118,7 +118,8 @@ def test_restore_state_machine():
     assert sw.device_status() == 0
 
 
-@pytest.mark.parametrize("name,kernel,grid", [("mini", "v1", None), ("mini", "tg", "3"), ("mini-r4k4", None, None)])
+@pytest.mark.parametrize("name,kernel,grid", [("mini", "v1", None), ("mini", "tg", "3"), ("mini", "fc", "3"),
+                                                  ("mini-r4k4", None, None)])
 def test_per_matrix_merge_ablation_is_bitwise_the_single_launch(monkeypatch, name, kernel, grid):
     """SURVEY 8f #4 (launch-count ablation): the merge as one launch per matrix
     (7 x L launches of the same kernel over that matrix's tiles) gives bitwise
