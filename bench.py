@@ -113,6 +113,11 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+SWITCH_KERNELS = {1: "switch_tc_kernel [v1, per-term TMEM accumulators]",
+                  2: "switch_tc_kernel [tg, term groups]",
+                  3: "switch_fc_kernel [fc, folded coefficients, one accumulator per tile]"}
+
+
 def _ncu_traffic(cfg, info):
     """DRAM traffic per switch launch from the committed ncu capture
     (profiles/ncu_switch_traffic.json), scaled from its layer count to this
@@ -121,6 +126,8 @@ def _ncu_traffic(cfg, info):
         with open(os.path.join(ROOT, "profiles", "ncu_switch_traffic.json")) as f:
             d = json.load(f)
         if d.get("config") != cfg.name or d.get("switch_impl") != info["switch_impl"]:
+            return None
+        if d.get("switch_kernel") not in (None, info.get("switch_kernel")):
             return None
         return d["dram_bytes_per_layer"] * cfg.n_layers
     except Exception:
@@ -386,7 +393,11 @@ def run_ours(args, cfg):
     # fused switch + decode: router + ONE launch that switches and
     # computes the GEMVs in decoder order (4 B/element, 4L segment barriers)
     fu_ms = []
-    if world == 1 and info["switch_impl"] == "tc" and info.get("switch_kernel") == 1:
+    if world == 1 and info["switch_impl"] == "tc" and 2 * cfg.top_k <= 4:
+        # (the fused launch is a build of the v1 kernel; a ctx switching with fc
+        # builds a v1 plan on the first call -- untimed warm-up token first)
+        sw.decode_token_fused(X1[0], xs, ys, idx, gate, stream)
+        torch.cuda.synchronize()
         for t in range(min(args.steps, 10)):
             a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
             a.record(stream)
@@ -478,7 +489,8 @@ def run_ours(args, cfg):
                          "traffic_source": "profiles/ncu_switch_traffic.json (dram__bytes_read.sum + "
                                            "dram__bytes_write.sum of one ncu --set full capture of the same "
                                            "kernel on an identical-tile slice of the model, per layer x layers)",
-                         "kernel": "switch_tc_kernel (fused Eq. 10 switch)",
+                         "kernel": SWITCH_KERNELS.get(info.get("switch_kernel"), "switch_simt_kernel")
+                                   + " (fused Eq. 10 switch)",
                          "peak_source": peak_src,
                          "bytes_per_launch": tb["switch"]},
             "cpu_baseline": cpu,

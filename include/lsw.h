@@ -155,7 +155,8 @@ typedef struct {
   int64_t  packed_bytes;     /* ctx-owned packed operand bytes on the device         */
   int64_t  xs_elems, ys_elems; /* token I/O sizes (lsw_decode_token)                  */
   int32_t  switch_kernel;    /* tensor-core switch kernel: 1 = per-term TMEM (v1),    */
-                             /* 2 = term groups (any k <= 4, r <= 64); 0 = SIMT      */
+                             /* 2 = term groups (any k <= 4, r <= 64), 3 = folded    */
+                             /* coefficients, one accumulator per tile; 0 = SIMT     */
   int32_t  reserved;
 } lsw_info;
 
@@ -288,11 +289,15 @@ LSW_API lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs
  * rounded weight tiles, so W is read once and written once per token (4
  * B/element instead of 6).  Tiles are walked in decoder order, one segment per
  * (layer, group); a segment's outputs are accumulated only after every tile of
- * the previous segment is done (y final), as a decoder needs.  W ends exactly
- * as after lsw_merge_all_layers (bitwise); ys equals lsw_decode_all_layers on
- * those weights up to fp32 summation order (atomic accumulation, not bitwise
- * reproducible).  Layouts as lsw_decode_token.  LSW_E_UNSUPPORTED unless the
- * ctx uses the per-term tensor-core kernel (2k <= 4 terms, tp_size == 1).
+ * the previous segment is done (y final), as a decoder needs.  The fused
+ * launch is a build of the per-term (v1) tensor-core kernel: W ends exactly as
+ * after lsw_merge_all_layers with that kernel (bitwise; a ctx that switches
+ * with another kernel builds a v1 plan on the first call, and its W then stays
+ * within the parity tolerance of the oracle's trajectory); ys equals
+ * lsw_decode_all_layers on those weights up to fp32 summation order (atomic
+ * accumulation, not bitwise reproducible).  Layouts as lsw_decode_token.
+ * LSW_E_UNSUPPORTED unless v1 has a plan for the shape (2k <= 4 terms) and
+ * tp_size == 1.
  */
 LSW_API lsw_status lsw_decode_token_fused(lsw_ctx* ctx, const void* x1, const void* xs, float* ys, int32_t* idx,
                                           float* gate, void* stream);

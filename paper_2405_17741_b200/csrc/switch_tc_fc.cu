@@ -73,6 +73,7 @@ struct TcPlan {
   Maps maps;
   Geom geom;
   int32_t chunk = 48;
+  int32_t probe = 0;          // tuning only (LSW_TC_PROBE=1): W stream alone, W written back unchanged
   void* packed_At[LSW_NKIND] = {};
   void* packed_B[LSW_NKIND] = {};
   int64_t bytes = 0;
@@ -81,7 +82,7 @@ struct TcPlan {
 
 struct Args {
   Geom g;
-  int32_t chunk;
+  int32_t chunk, probe;
   int32_t mode, top_k, n_experts;
   float scale;
   const int32_t* cur_idx;
@@ -241,7 +242,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         }
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
-    } else if (warp == 3) {
+    } else if (warp == 3 && !args.probe) {
       // ============================ operand producer ========================
       // Per strip (rare): raw B slices of all terms by bulk copies into the lo
       // slots, then the whole warp folds them into (hi, lo) parts in place and
@@ -296,7 +297,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         __syncwarp();
         aring.next();
       }
-    } else if (warp == 1) {
+    } else if (warp == 1 && !args.probe) {
       // ============================ MMA issuer ==============================
       // One chain per tile: for every term, the hi and lo parts times the A^T
       // slice, K = rp each in steps of 16, into the tile's single accumulator;
@@ -349,6 +350,14 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       Ring aring{0, 0, (uint32_t)g.a_stages}, bring{0, 0, (uint32_t)g.b_bufs};
       int64_t bstrip = -1;
       for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+        if (args.probe) {                          // tuning: the W stream alone
+          mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
+          wring.next();
+          continue;
+        }
         if (releaser) {
           // first tile of a new strip: every MMA of the previous strip is done
           // (its last accumulator has been seen), so its B buffer is free
@@ -483,6 +492,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   }
   if (!ok) { delete plan; *why = "shared memory: rank * top_k too large for the folded kernel"; return cudaErrorNotSupported; }
   if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
+  if (const char* v = getenv("LSW_TC_PROBE")) plan->probe = atoi(v) == 1;
   g.smem_bytes = g.w_stages * w_stage + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
   // tiles
   int64_t t = 0;
@@ -572,6 +582,7 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   a.t_count = t_count;
   a.g = plan->geom;
   a.chunk = plan->chunk;
+  a.probe = plan->probe;
   a.mode = p.mode;
   a.top_k = p.top_k;
   a.n_experts = p.n_experts;

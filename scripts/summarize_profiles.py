@@ -59,9 +59,11 @@ if "switch" in summary and summary["switch"]:
         return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
     tot = gb(rec["dram__bytes_read.sum"]) + gb(rec["dram__bytes_write.sum"])
     with open(os.path.join(prof, "ncu_switch_traffic.json"), "w") as f:
+        kname = rec["kernel"]
         json.dump({"config": "llama2-7b", "switch_impl": "tc", "capture_layers": 4, "round_tag": tag,
+                   "kernel": kname, "switch_kernel": 3 if "switch_fc" in kname else None,
                    "dram_bytes_capture": tot, "dram_bytes_per_layer": tot / 4,
-                   "note": "ncu --set full of switch_tc_kernel (fused switch) on the 7B shape with 4 layers "
+                   "note": "ncu --set full of the switch kernel (fused switch) on the 7B shape with 4 layers "
                            "(identical per-matrix tiles); bench.py scales per layer x layers"}, f, indent=1)
 
 # launch list shares
