@@ -191,13 +191,44 @@ __device__ __forceinline__ uint64_t dot8_f2(const uint4 w, const float4 lo, cons
   return acc;
 }
 
+// acc (fp32 pairs) += bf16 chunk w * bf16 chunk x: the same element pairs and
+// FFMA2 order as dot8_f2 (bitwise-identical results), x widened in registers
+__device__ __forceinline__ uint64_t dot8_bb(const uint4 w, const uint4 x, uint64_t acc) {
+  acc = g_ffma2(g_pack(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u)),
+                g_pack(__uint_as_float(x.x << 16), __uint_as_float(x.x & 0xffff0000u)), acc);
+  acc = g_ffma2(g_pack(__uint_as_float(w.y << 16), __uint_as_float(w.y & 0xffff0000u)),
+                g_pack(__uint_as_float(x.y << 16), __uint_as_float(x.y & 0xffff0000u)), acc);
+  acc = g_ffma2(g_pack(__uint_as_float(w.z << 16), __uint_as_float(w.z & 0xffff0000u)),
+                g_pack(__uint_as_float(x.z << 16), __uint_as_float(x.z & 0xffff0000u)), acc);
+  acc = g_ffma2(g_pack(__uint_as_float(w.w << 16), __uint_as_float(w.w & 0xffff0000u)),
+                g_pack(__uint_as_float(x.w << 16), __uint_as_float(x.w & 0xffff0000u)), acc);
+  return acc;
+}
+
 // One row of W (in shared memory) against the staged x, reduced over the warp.
-template <bool kBf16>
+// kXB: x staged as raw bf16 (one LDS.128 of x per 8 elements instead of two of
+// the fp32 planes: the consumers' shared-memory traffic per W byte drops from
+// 3x to 2x, the ring fill adds 1x).
+template <bool kBf16, bool kXB = false>
 __device__ __forceinline__ float row_dot(const uint8_t* wrow, const uint8_t* xs, int64_t n16, int lane,
                                          float extra_a = 0.f, float extra_b = 0.f, float extra_c = 1.f) {
   const uint4* w4 = reinterpret_cast<const uint4*>(wrow);
   float acc;
-  if (kBf16) {
+  if (kBf16 && kXB) {
+    const uint4* x4 = reinterpret_cast<const uint4*>(xs);
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    int64_t c = lane;
+    for (; c + 96 < n16; c += 128) {
+      const uint4 w0 = w4[c], w1 = w4[c + 32], w2 = w4[c + 64], w3 = w4[c + 96];
+      const uint4 x0 = x4[c], x1 = x4[c + 32], x2 = x4[c + 64], x3 = x4[c + 96];
+      a0 = dot8_bb(w0, x0, a0);
+      a1 = dot8_bb(w1, x1, a1);
+      a2 = dot8_bb(w2, x2, a2);
+      a3 = dot8_bb(w3, x3, a3);
+    }
+    for (; c < n16; c += 32) a0 = dot8_bb(w4[c], x4[c], a0);
+    acc = (g_sum2(a0) + g_sum2(a1)) + (g_sum2(a2) + g_sum2(a3));
+  } else if (kBf16) {
     const float4* lo = reinterpret_cast<const float4*>(xs);
     const float4* hi = lo + n16;
     uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;     // (+0.f, +0.f) pairs
@@ -317,14 +348,14 @@ cudaError_t launch_lora_prefetch(const LoraPrefetch& q, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <bool kBf16, bool kLora>
+template <bool kBf16, bool kLora, bool kXB>
 __global__ void __launch_bounds__(kBulkThreads, 1)
 gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, const GemvLora L) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row_bytes = (uint32_t)(p.d_in * (kBf16 ? 2 : 4));
-  const uint32_t x_bytes = x_stage_bytes(row_bytes, kBf16);
+  const uint32_t x_bytes = x_stage_bytes(row_bytes, kBf16 && !kXB);
   const size_t slot_bytes = (size_t)R * row_bytes;
   uint8_t* xs = smem_raw;
   uint8_t* ring = smem_raw + x_bytes;
@@ -390,7 +421,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   if (early_w & 1) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after our wait: see above
   // x -> shared (consumer warps), then a named barrier among the consumers only
-  stage_x<kBf16>(p.x, xs, row_bytes, threadIdx.x - 32, blockDim.x - 32);
+  stage_x<kBf16 && !kXB>(p.x, xs, row_bytes, threadIdx.x - 32, blockDim.x - 32);
   asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
   // consumers: unit u = (local chunk i, row k in chunk); warp cw takes u = cw mod 8
   const int cw = warp - 1;
@@ -447,7 +478,8 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
         }
       }
       const float acc =
-          row_dot<kBf16>(ring + s * slot_bytes + (size_t)k * row_bytes, xs, nchunk16, lane, extra, extra_u, extra_g);
+          row_dot<kBf16, kXB>(ring + s * slot_bytes + (size_t)k * row_bytes, xs, nchunk16, lane, extra, extra_u,
+                              extra_g);
       if (lane == 0) p.y[row] = acc;
     }
     __syncwarp();
@@ -707,8 +739,10 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
   if (gemv_variant() == 1) {
     // bulk-copy throughput grows with bytes per operation (scripts/membench.cu:
     // 4 KB ops 2.6 TB/s ... 32 KB ops 7.3 TB/s): move R >= 1 rows per op, ~32 KB
+    // x staged as raw bf16 (default) or widened to fp32 planes (LSW_GEMV_XF32=1)
+    static const bool xb = getenv("LSW_GEMV_XF32") == nullptr;
     const uint32_t row_bytes = (uint32_t)(p.d_in * (bf16 ? 2 : 4));
-    const uint32_t x_bytes = x_stage_bytes(row_bytes, bf16);
+    const uint32_t x_bytes = x_stage_bytes(row_bytes, bf16 && !xb);
     uint32_t op_bytes = 32768;                       // tuning: LSW_GEMV_OP_KB
     if (const char* v = getenv("LSW_GEMV_OP_KB")) { long x = atol(v); if (x >= 4 && x <= 96) op_bytes = (uint32_t)x * 1024; }
     int R = (int)(op_bytes / row_bytes);
@@ -724,8 +758,10 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
     if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
     if (slots >= 2) {
       const size_t smem = x_bytes + (size_t)slots * slot_bytes;
-      auto fn = lora ? (bf16 ? gemv_bulk_kernel<true, true> : gemv_bulk_kernel<false, true>)
-                     : (bf16 ? gemv_bulk_kernel<true, false> : gemv_bulk_kernel<false, false>);
+      auto fn = lora ? (bf16 ? (xb ? gemv_bulk_kernel<true, true, true> : gemv_bulk_kernel<true, true, false>)
+                             : gemv_bulk_kernel<false, true, false>)
+                     : (bf16 ? (xb ? gemv_bulk_kernel<true, false, true> : gemv_bulk_kernel<true, false, false>)
+                             : gemv_bulk_kernel<false, false, false>);
       static size_t smem_set[2][2] = {{0, 0}, {0, 0}};   // attribute set once per kernel (not per launch)
       if (smem > smem_set[lora != nullptr][bf16]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
