@@ -67,6 +67,8 @@ struct Geom {
   uint32_t a_stage_bytes, b_buf_bytes;  // A stage: all terms of one tile; B buffer: (hi, lo) of all terms
   uint32_t swz_mode;                    // UMMA layout type of the r-wide operands
   uint32_t smem_bytes;
+  int32_t wrm;                          // 1: W tile moved row-major by one 4-D TMA op (256 B per row
+                                        //    contiguous in smem and in the request stream; LSW_FC_WRM)
 };
 
 struct TcPlan {
@@ -114,11 +116,17 @@ __device__ __forceinline__ void fold8(const uint4 raw, float c, uint4& hi, uint4
 
 // ------------------------------------------------------------------ epilogue
 
-// W (bf16, 128B-swizzled sub-tile row) + 16 accumulator columns -> RNE in place
-__device__ __forceinline__ void epi16(uint8_t* wrow, int row, int col16, const uint32_t* acc) {
-  uint4* p0 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 0) ^ (row & 7)) << 4));
-  uint4* p1 = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + 1) ^ (row & 7)) << 4));
-  const uint4 u0 = *p0, u1 = *p1;
+// W (bf16, one 128-B swizzle unit: 64 columns of a row) + 16 accumulator
+// columns -> RNE in place; key = the unit's swizzle phase (unit index & 7).
+// flip: this lane touches the odd 16-B chunk of the pair first -- with the
+// row-major tile (units 2r + h, keys 2r + h mod 8) lanes r and r + 4 share a
+// key, and flipping the order for r & 4 keeps every 8 lanes of one LDS/STS.128
+// on 8 distinct bank groups.
+__device__ __forceinline__ void epi16(uint8_t* wrow, int key, int flip, int col16, const uint32_t* acc) {
+  uint4* pa = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + flip) ^ key) << 4));
+  uint4* pb = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + (flip ^ 1)) ^ key) << 4));
+  const uint4 ua = *pa, ub = *pb;
+  const uint4 u0 = flip ? ub : ua, u1 = flip ? ua : ub;
   const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
   uint32_t o[8];
 #pragma unroll
@@ -127,8 +135,9 @@ __device__ __forceinline__ void epi16(uint8_t* wrow, int row, int col16, const u
                              f2_pack(__uint_as_float(acc[2 * q]), __uint_as_float(acc[2 * q + 1])));
     o[q] = f2_to_bf16x2(v);
   }
-  *p0 = make_uint4(o[0], o[1], o[2], o[3]);
-  *p1 = make_uint4(o[4], o[5], o[6], o[7]);
+  const uint4 o0 = make_uint4(o[0], o[1], o[2], o[3]), o1 = make_uint4(o[4], o[5], o[6], o[7]);
+  *pa = flip ? o1 : o0;
+  *pb = flip ? o0 : o1;
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -218,9 +227,12 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
           mbar_expect_tx(wbar, 2 * kSubBytes);
           uint8_t* wdst = wst0 + (size_t)wring.i * (2 * kSubBytes);
-          for (int sb = 0; sb < 2; ++sb)
-            tma_load_3d(smem_u32(wdst + sb * kSubBytes), &src[c.kd], c.cb * kTN + sb * kSubCols, c.rb * kTM,
-                        c.layer, wbar, pol_stream);
+          if (g.wrm)
+            tma_load_4d(smem_u32(wdst), &src[c.kd], 0, c.cb * 2, c.rb * kTM, c.layer, wbar, pol_stream);
+          else
+            for (int sb = 0; sb < 2; ++sb)
+              tma_load_3d(smem_u32(wdst + sb * kSubBytes), &src[c.kd], c.cb * kTN + sb * kSubCols, c.rb * kTM,
+                          c.layer, wbar, pol_stream);
           wring.next();
         }
       }
@@ -232,9 +244,12 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
           mbar_wait(smem_u32(&bar_wdone[wring.i]), wring.phase);     // epilogue wrote the tile
           uint8_t* wsrc = wst0 + (size_t)wring.i * (2 * kSubBytes);
-          for (int sb = 0; sb < 2; ++sb)
-            tma_store_3d(&maps.w[c.kd], smem_u32(wsrc + sb * kSubBytes), c.cb * kTN + sb * kSubCols, c.rb * kTM,
-                         c.layer, pol_stream);
+          if (g.wrm)
+            tma_store_4d(&maps.w[c.kd], smem_u32(wsrc), 0, c.cb * 2, c.rb * kTM, c.layer, pol_stream);
+          else
+            for (int sb = 0; sb < 2; ++sb)
+              tma_store_3d(&maps.w[c.kd], smem_u32(wsrc + sb * kSubBytes), c.cb * kTN + sb * kSubCols,
+                           c.rb * kTM, c.layer, pol_stream);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read -> stage reusable
           mbar_arrive(smem_u32(&bar_wempty[wring.i]));
@@ -384,9 +399,11 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
         acc.next();
         mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);      // W tile landed
-        uint8_t* wrow = wst0 + (size_t)wring.i * (2 * kSubBytes) + half * kSubBytes + row * 128;
+        // default: two [128 rows][64 cols] boxes; wrm: one [128 rows][2 x 64 cols] box
+        const int unit = g.wrm ? 2 * row + half : half * kTM + row;
+        uint8_t* wrow = wst0 + (size_t)wring.i * (2 * kSubBytes) + unit * 128;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) epi16(wrow, row, q, a[q]);
+        for (int q = 0; q < 4; ++q) epi16(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> TMA store
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
@@ -434,6 +451,26 @@ static bool encode_w(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// Row-major 4-D view {64, d_in / 64, d_out, L}, box {64, 2, 128, 1}: one op
+// moves a 128 x 128 tile with each row's 256 B requested (and laid out in
+// shared memory) contiguously; needs d_in % 64 == 0.
+static bool encode_w_rm(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d_out, uint64_t L) {
+  auto enc = get_encode();
+  if (!enc || d_in % 64) return false;
+  cuuint64_t dims[4] = {64, d_in / 64, d_out, L};
+  cuuint64_t strides[3] = {128, d_in * 2, d_in * d_out * 2};
+  cuuint32_t box[4] = {64, 2, (cuuint32_t)kTM, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static bool encode_any(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t d_out, uint64_t L, bool rm) {
+  return rm ? encode_w_rm(m, base, d_in, d_out, L) : encode_w(m, base, d_in, d_out, L);
 }
 
 static uint32_t align1k(uint32_t x) { return (x + 1023) & ~1023u; }
@@ -493,6 +530,11 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   if (!ok) { delete plan; *why = "shared memory: rank * top_k too large for the folded kernel"; return cudaErrorNotSupported; }
   if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
   if (const char* v = getenv("LSW_TC_PROBE")) plan->probe = atoi(v) == 1;
+  // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
+  // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
+  g.wrm = 1;
+  if (const char* v = getenv("LSW_FC_WRM")) g.wrm = atoi(v) != 0;
+  for (int k = 0; k < LSW_NKIND; ++k) if (sp.kind[k].d_in % 64) g.wrm = 0;   // ragged TP shards: 3-D boxes
   g.smem_bytes = g.w_stages * w_stage + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
   // tiles
   int64_t t = 0;
@@ -528,7 +570,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
                                  kg.d_out, g.dout_pad[k]);
     g.At[k] = (const __nv_bfloat16*)plan->packed_At[k];
     g.Bp[k] = (const __nv_bfloat16*)plan->packed_B[k];
-    if (!encode_w(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers)) {
+    if (!encode_any(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers, g.wrm)) {
       *why = "cuTensorMapEncodeTiled failed";
       e = cudaErrorInvalidValue;
     }
@@ -563,7 +605,7 @@ int64_t tc_plan_tiles(const TcPlan* plan) { return plan ? plan->geom.tiles_total
 cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& sp) {
   for (int k = 0; k < LSW_NKIND; ++k)
     if (!sp.kind[k].P ||
-        !encode_w(&plan->maps.p[k], sp.kind[k].P, sp.kind[k].d_in, sp.kind[k].d_out, sp.n_layers))
+        !encode_any(&plan->maps.p[k], sp.kind[k].P, sp.kind[k].d_in, sp.kind[k].d_out, sp.n_layers, plan->geom.wrm))
       return cudaErrorInvalidValue;
   return cudaSuccess;
 }
