@@ -59,6 +59,69 @@ __device__ __forceinline__ float dot_chunk<false>(const uint4 u, const uint4* xs
   return a;
 }
 
+__device__ __forceinline__ int site_of(const GemvParams& p, int64_t row) {
+  return (p.n_sites > 2 && row >= p.site[2].row_begin) ? 2 : (p.n_sites > 1 && row >= p.site[1].row_begin) ? 1 : 0;
+}
+
+// site-indexed kernel parameters without dynamic indexing (which would copy the
+// parameter struct to local memory)
+template <typename T>
+__device__ __forceinline__ T sel3(int q, T a, T b, T c) { return q == 0 ? a : q == 1 ? b : c; }
+
+// Unmerged decode, the LoRA-up term of one row (Eq. 2):
+// sum_j (alpha/r) g_j sum_rho B_q[e_j][row, rho] u_q[j][rho], in (j, rho) order;
+// 16-B loads of B when a row's r elements are whole chunks.
+template <bool kBf16>
+__device__ __forceinline__ float lora_up_row(const GemvParams& p, const GemvLora& L, const float* us, int64_t row,
+                                             int kr) {
+  const int q = site_of(p, row);
+  const int64_t rl = row - sel3(q, p.site[0].row_begin, p.site[1].row_begin, p.site[2].row_begin);
+  const int64_t dq = sel3(q, p.site[0].d_out, p.site[1].d_out, p.site[2].d_out);
+  const void* Bq = sel3(q, L.B[0], L.B[1], L.B[2]);
+  float e = 0.f;
+  for (int j = 0; j < L.k; ++j) {
+    const int64_t off = ((int64_t)L.idx[j] * dq + rl) * L.r;
+    const float gj = L.scale * L.gate[j];
+    const float* uq = us + q * kr + j * L.r;
+    if (kBf16 && (L.r % 8) == 0) {
+      const uint4* b4 = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(Bq) + off);
+      for (int v = 0; v < L.r / 8; ++v) {
+        float b[8];
+        bf16x8_to_f32(__ldg(b4 + v), b);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) e = fmaf(gj * b[h], uq[8 * v + h], e);
+      }
+    } else {
+      for (int rho = 0; rho < L.r; ++rho) {
+        const float b = kBf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(Bq)[off + rho])
+                              : reinterpret_cast<const float*>(Bq)[off + rho];
+        e = fmaf(gj * b, uq[rho], e);
+      }
+    }
+  }
+  return e;
+}
+
+// Both operands in registers (16 B each: 8 bf16 or 4 fp32), fp32 sum in order.
+template <bool kBf16>
+__device__ __forceinline__ float dot_chunk_vv(const uint4 a, const uint4 x) {
+  float s;
+  if (kBf16) {
+    float av[8], xv[8];
+    bf16x8_to_f32(a, av);
+    bf16x8_to_f32(x, xv);
+    s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s = fmaf(av[q], xv[q], s);
+  } else {
+    s = __uint_as_float(a.x) * __uint_as_float(x.x);
+    s = fmaf(__uint_as_float(a.y), __uint_as_float(x.y), s);
+    s = fmaf(__uint_as_float(a.z), __uint_as_float(x.z), s);
+    s = fmaf(__uint_as_float(a.w), __uint_as_float(x.w), s);
+  }
+  return s;
+}
+
 // A "chunk" is 16 B: 8 bf16 or 4 fp32 elements.
 template <bool kBf16>
 __global__ void __launch_bounds__(kGemvThreads)
@@ -113,6 +176,9 @@ gemv_kernel(const GemvParams p) {
 // warp instruction, conflict-free) against x (also in shared memory).
 constexpr int kBulkConsumers = 16;   // measured (7B token of GEMVs): 8 warps 2.39 ms, 16 2.25, 24 2.24
 constexpr int kBulkThreads = 32 * (1 + kBulkConsumers);
+constexpr int kLoraWarps = 4;        // unmerged GEMV: extra warps computing the LoRA-down products
+constexpr int kMaxDots = 3 * LSW_MAX_TOPK * 64;   // n_sites * k * r
+constexpr int kMaxLocal = 1024;      // unmerged GEMV: row sums kept in shared memory up to this many rows per CTA
 constexpr int kBulkMaxSlots = 32;
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -122,6 +188,12 @@ __device__ __forceinline__ uint32_t g_mbar_try(uint32_t bar, uint32_t parity) {
   asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
                : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
   return ok;
+}
+
+__device__ __forceinline__ uint64_t g_globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 // Wait with a ~20 s watchdog (a protocol bug traps instead of hanging the GPU).
@@ -191,6 +263,22 @@ __device__ __forceinline__ uint64_t dot8_f2(const uint4 w, const float4 lo, cons
   return acc;
 }
 
+// One 16-B chunk of a LoRA-down row against x as staged (raw bf16, fp32
+// planes, or fp32), fp32 products summed in element order.
+template <bool kBf16, bool kXB>
+__device__ __forceinline__ float lora_chunk(const uint4 a, const uint8_t* xs, int64_t c, int64_t n16) {
+  if (kBf16 && kXB) return dot_chunk<true>(a, reinterpret_cast<const uint4*>(xs), c);
+  if (!kBf16) return dot_chunk<false>(a, reinterpret_cast<const uint4*>(xs), c);
+  const float4 lo = reinterpret_cast<const float4*>(xs)[c], hi = reinterpret_cast<const float4*>(xs)[n16 + c];
+  const float x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+  float w[8];
+  bf16x8_to_f32(a, w);
+  float s = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s = fmaf(w[q], x[q], s);
+  return s;
+}
+
 // acc (fp32 pairs) += bf16 chunk w * bf16 chunk x: the same element pairs and
 // FFMA2 order as dot8_f2 (bitwise-identical results), x widened in registers
 __device__ __forceinline__ uint64_t dot8_bb(const uint4 w, const uint4 x, uint64_t acc) {
@@ -210,8 +298,7 @@ __device__ __forceinline__ uint64_t dot8_bb(const uint4 w, const uint4 x, uint64
 // the fp32 planes: the consumers' shared-memory traffic per W byte drops from
 // 3x to 2x, the ring fill adds 1x).
 template <bool kBf16, bool kXB = false>
-__device__ __forceinline__ float row_dot(const uint8_t* wrow, const uint8_t* xs, int64_t n16, int lane,
-                                         float extra_a = 0.f, float extra_b = 0.f, float extra_c = 1.f) {
+__device__ __forceinline__ float row_dot(const uint8_t* wrow, const uint8_t* xs, int64_t n16, int lane) {
   const uint4* w4 = reinterpret_cast<const uint4*>(wrow);
   float acc;
   if (kBf16 && kXB) {
@@ -253,78 +340,15 @@ __device__ __forceinline__ float row_dot(const uint8_t* wrow, const uint8_t* xs,
     if (c < n16) acc0 += dot_chunk<false>(w4[c], x4, c);
     acc = acc0 + acc1;
   }
-  // this lane's share of a LoRA term (unmerged decode); multiplied only here so
-  // that a load feeding it is not waited for before the row's dot product
-  acc = fmaf(extra_a * extra_c, extra_b, acc);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   return acc;
 }
 
-// Unmerged decode, LoRA-down step: u[q][j][rho] = A_q[e_j][rho, :] . x for
-// every site q, selected expert j and rank index rho of a group -- one CTA per
-// dot product, its 8 warps on 8 consecutive K-slices (each lane <= 8 loads in
-// flight for d_in <= 16384), partial sums added in warp order (deterministic).
-// Launched (PDL) right before the group's GEMV, whose consumers read u after
-// griddepcontrol.wait; its W stream does not wait for this kernel.
-constexpr int kLoraDownWarps = 8;
-
-template <bool kBf16>
-__global__ void __launch_bounds__(32 * kLoraDownWarps)
-lora_down_kernel(const GemvParams p, const GemvLora L) {
-  __shared__ float part[kLoraDownWarps];
-  // let the group's GEMV launch at once (its W stream needs nothing from here;
-  // its consumers wait for this grid), then wait for x / idx to be final
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kr = L.k * L.r;
-  const int d = blockIdx.x;
-  const int q = d / kr, j = (d - q * kr) / L.r, rho = d - q * kr - j * L.r;
-  const int64_t es = kBf16 ? 2 : 4;
-  const int64_t n16 = p.d_in * es / 16;
-  const uint4* a4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(L.A[q]) +
-                                                   ((int64_t)L.idx[j] * L.r + rho) * p.d_in * es);
-  const uint4* x4 = reinterpret_cast<const uint4*>(p.x);
-  const int64_t per = (n16 + kLoraDownWarps - 1) / kLoraDownWarps;
-  const int64_t c_begin = warp * per, c_end = c_begin + per < n16 ? c_begin + per : n16;
-  float acc = 0.f;
-  for (int64_t c0 = c_begin + lane; c0 < c_end; c0 += 32 * 8) {
-    uint4 a[8], x[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const bool in = c0 + 32 * u < c_end;
-      a[u] = in ? __ldg(a4 + c0 + 32 * u) : make_uint4(0, 0, 0, 0);
-      x[u] = in ? __ldg(x4 + c0 + 32 * u) : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (kBf16) {
-        acc += dot_chunk<true>(a[u], x + u, 0);
-      } else {
-        const float4 xv = *reinterpret_cast<const float4*>(&x[u]);
-        acc = fmaf(__uint_as_float(a[u].x), xv.x, acc);
-        acc = fmaf(__uint_as_float(a[u].y), xv.y, acc);
-        acc = fmaf(__uint_as_float(a[u].z), xv.z, acc);
-        acc = fmaf(__uint_as_float(a[u].w), xv.w, acc);
-      }
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) part[warp] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float u = 0.f;
-    for (int w = 0; w < kLoraDownWarps; ++w) u += part[w];
-    L.u[d] = u;
-  }
-}
-
 // Unmerged decode: the pre-gate's decision is known for EVERY layer at the
 // start of the token, so the selected LoRA-down rows of all layers can
 // be pulled into L2 (evict_last; the W streams are evict_first) before the
-// first group -- each lora_down_kernel then reads them at L2 latency.
+// first group -- each GEMV's LoRA-down products then read them at L2 latency.
 __global__ void lora_prefetch_kernel(LoraPrefetch q) {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -349,7 +373,7 @@ cudaError_t launch_lora_prefetch(const LoraPrefetch& q, cudaStream_t s) {
 }
 
 template <bool kBf16, bool kLora, bool kXB>
-__global__ void __launch_bounds__(kBulkThreads, 1)
+__global__ void __launch_bounds__(kLora ? kBulkThreads + 32 * kLoraWarps : kBulkThreads, 1)
 gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, const GemvLora L) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
@@ -420,28 +444,85 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   }
   if (early_w & 1) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after our wait: see above
+  const int kr = kLora ? L.k * L.r : 0;
+  const int n_dots = kLora ? p.n_sites * kr : 0;
+  // unmerged form: u (all LoRA-down products of the group), staged by the
+  // LoRA-down warps once every CTA has published its share
+  __shared__ float us[kLora ? kMaxDots : 1];
+  __shared__ float acc_s[kLora ? kMaxLocal : 1], e_s[kLora ? kMaxLocal : 1];   // this CTA's rows (if they fit)
+  const int64_t n_local = my_chunks * R;
+  if (kLora && warp > kBulkConsumers) {
+    // LoRA-down (Eq. 2, A_{e_j} x) by the kLoraWarps extra warps, while the
+    // consumers stream W: the group's n_sites * k * r dot products are dealt
+    // over the grid (dot d -> CTA d % G), each split over the dot warps' K
+    // ranges (x read from global, L2-hot), partial sums added in warp order
+    // (deterministic), published as u[d] and a release increment of the
+    // arrival counter.  Then these warps wait for every CTA's products, stage
+    // u in shared memory and compute the LoRA-up terms of the CTA's rows.
+    __shared__ float part[kLoraWarps];
+    const int dw = warp - 1 - kBulkConsumers;
+    const int64_t n16 = row_bytes / 16;
+    const int64_t per = (n16 + kLoraWarps - 1) / kLoraWarps;
+    const uint4* x4 = reinterpret_cast<const uint4*>(p.x);
+    for (int d = blockIdx.x; d < n_dots; d += (int)G) {
+      const int q = d / kr, j = (d - q * kr) / L.r, rho = d - q * kr - j * L.r;
+      const uint4* a4 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(sel3(q, L.A[0], L.A[1], L.A[2])) +
+                                                       ((int64_t)L.idx[j] * L.r + rho) * row_bytes);
+      const int64_t c0 = dw * per, c1 = c0 + per < n16 ? c0 + per : n16;
+      float acc = 0.f;
+      for (int64_t c = c0 + lane; c < c1; c += 32 * 8) {
+        uint4 a[8], x[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const bool in = c + 32 * v < c1;
+          a[v] = in ? __ldg(a4 + c + 32 * v) : make_uint4(0, 0, 0, 0);
+          x[v] = in ? __ldg(x4 + c + 32 * v) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v) acc += dot_chunk_vv<kBf16>(a[v], x[v]);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0) part[dw] = acc;
+      asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");
+      if (dw == 0 && lane == 0) {
+        float u = 0.f;
+        for (int w = 0; w < kLoraWarps; ++w) u += part[w];
+        L.u[d] = u;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(L.arrive) : "memory");
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");   // part[] reusable
+    }
+    if (dw == 0 && lane == 0) {
+      uint32_t v;
+      const uint64_t t0 = g_globaltimer();
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(L.arrive) : "memory");
+        if (v >= (uint32_t)n_dots) break;
+        __nanosleep(64);
+        if (g_globaltimer() - t0 > 20000000000ull) __trap();
+      }
+    }
+    asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");
+    for (int d = threadIdx.x - 32 * (1 + kBulkConsumers); d < n_dots; d += 32 * kLoraWarps) us[d] = __ldcg(L.u + d);
+    asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");
+    // LoRA-up terms of this CTA's rows, one lane per row, while the consumers
+    // still stream (their row sums wait in acc_s; joined at the end)
+    if (n_local <= kMaxLocal && !(L.flags & 4))
+      for (int64_t t = threadIdx.x - 32 * (1 + kBulkConsumers); t < n_local; t += 32 * kLoraWarps) {
+        const int64_t row = (blockIdx.x + (t / R) * G) * R + t % R;
+        e_s[t] = row < p.rows_total ? lora_up_row<kBf16>(p, L, us, row, kr) : 0.f;
+      }
+    asm volatile("bar.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");
+    return;
+  }
   // x -> shared (consumer warps), then a named barrier among the consumers only
-  stage_x<kBf16 && !kXB>(p.x, xs, row_bytes, threadIdx.x - 32, blockDim.x - 32);
+  stage_x<kBf16 && !kXB>(p.x, xs, row_bytes, threadIdx.x - 32, 32 * kBulkConsumers);
   asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
-  // consumers: unit u = (local chunk i, row k in chunk); warp cw takes u = cw mod 8
+  // consumers: unit u = (local chunk i, row k in chunk); warp cw takes u = cw mod 16
   const int cw = warp - 1;
   const int64_t nchunk16 = row_bytes / 16;
-  float ug[3] = {0.f, 0.f, 0.f};                  // kLora, k*r <= 32: this lane's u_q[j][rho] per site
-  float gj_l = 0.f;                                // and scale * g_j
-  int lane_e = -1, lane_rho = 0;
-  if (kLora) {
-    // u (the group's LoRA-down products, final sums) was written by the
-    // lora_down kernel that precedes this launch; griddepcontrol.wait above
-    // has made it visible.  Lane l < k*r keeps (j, rho) = (l / r, l % r).
-    const int kr = L.k * L.r;
-    if (kr <= 32 && lane < kr) {
-      const int j = lane / L.r;
-      lane_e = L.idx[j];
-      gj_l = L.scale * L.gate[j];
-      lane_rho = lane - j * L.r;
-      for (int q = 0; q < p.n_sites; ++q) ug[q] = __ldcg(L.u + q * kr + lane);
-    }
-  }
+  const bool in_smem = kLora && n_local <= kMaxLocal;
   for (int64_t u = cw; u < my_chunks * R; u += kBulkConsumers) {
     const int64_t i = u / R;
     const int k = (int)(u - i * R);
@@ -450,40 +531,43 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     while (issued <= i) __nanosleep(64);
     g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
     if (row < p.rows_total && !(early_w & 2)) {    // early_w bit 1: tuning probe, stream only
-      float extra = 0.f, extra_u = 1.f, extra_g = 1.f;
-      if (kLora && !(L.flags & 4)) {
-        // this row's LoRA-up term, sum_j scale g_j B_q[e_j][row, :] . u_q[j]:
-        // lane l < k*r takes (j, rho) = (l / r, l % r).  The B element is
-        // loaded before the row's dot product so its latency overlaps it.
-        const int q = (p.n_sites > 2 && row >= p.site[2].row_begin) ? 2
-                      : (p.n_sites > 1 && row >= p.site[1].row_begin) ? 1 : 0;
-        const int64_t rl = row - p.site[q].row_begin, dq = p.site[q].d_out;
-        const int kr = L.k * L.r;
-        if (kr <= 32) {
-          if (lane_e >= 0) {
-            const int64_t off = ((int64_t)lane_e * dq + rl) * L.r + lane_rho;
-            extra = kBf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(L.B[q])[off])
-                          : reinterpret_cast<const float*>(L.B[q])[off];
-            extra_u = q == 0 ? ug[0] : q == 1 ? ug[1] : ug[2];
-            extra_g = gj_l;
-          }
-        } else {
-          for (int l = lane; l < kr; l += 32) {
-            const int j = l / L.r, rho = l - j * L.r;
-            const int64_t off = ((int64_t)L.idx[j] * dq + rl) * L.r + rho;
-            const float b = kBf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(L.B[q])[off])
-                                  : reinterpret_cast<const float*>(L.B[q])[off];
-            extra += (L.scale * L.gate[j]) * b * __ldcg(L.u + q * kr + l);
-          }
-        }
+      const float acc = row_dot<kBf16, kXB>(ring + s * slot_bytes + (size_t)k * row_bytes, xs, nchunk16, lane);
+      if (lane == 0) {
+        if (in_smem) acc_s[u] = acc;
+        else p.y[row] = acc;
       }
-      const float acc =
-          row_dot<kBf16, kXB>(ring + s * slot_bytes + (size_t)k * row_bytes, xs, nchunk16, lane, extra, extra_u,
-                              extra_g);
-      if (lane == 0) p.y[row] = acc;
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[s])) : "memory");
+  }
+  if (kLora) {
+    // Eq. 2: y = (W x) + LoRA-up term, one rounding of the sum per row
+    asm volatile("bar.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");   // e_s / us ready
+    const bool up = !(L.flags & 4) && !(early_w & 2);
+    if (in_smem) {
+      for (int64_t t = threadIdx.x - 32; t < n_local; t += 32 * kBulkConsumers) {
+        const int64_t row = (blockIdx.x + (t / R) * G) * R + t % R;
+        if (row < p.rows_total && !(early_w & 2)) p.y[row] = up ? acc_s[t] + e_s[t] : acc_s[t];
+      }
+    } else if (up) {
+      // many rows per CTA (small grids): the terms now, one lane per row
+      for (int64_t t = threadIdx.x - 32; t < n_local; t += 32 * kBulkConsumers) {
+        const int64_t row = (blockIdx.x + (t / R) * G) * R + t % R;
+        if (row < p.rows_total) p.y[row] = p.y[row] + lora_up_row<kBf16>(p, L, us, row, kr);
+      }
+    }
+    // the last CTA to leave resets both counters for the next launch (which
+    // publishes its dots only after this grid has completed: griddepcontrol.wait)
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
+    if (cw == 0 && lane == 0) {
+      uint32_t prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(L.depart) : "memory");
+      if (prev == gridDim.x - 1) {
+        *reinterpret_cast<volatile uint32_t*>(L.arrive) = 0;
+        *reinterpret_cast<volatile uint32_t*>(L.depart) = 0;
+        __threadfence();
+      }
+    }
   }
 }
 
@@ -752,7 +836,8 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
     // Ring budget.  Measured (7B token of GEMVs): 220 KB 2.37 ms, 110 KB 2.59 ms,
     // 72 KB 3.49 ms -- a deep ring per SM beats letting the next GEMV's CTA
     // co-reside under PDL.  LSW_GEMV_SMEM_KB overrides.
-    size_t budget = 220 * 1024;
+    // (the unmerged form keeps ~12 KB of static shared memory: u, row sums, terms)
+    size_t budget = lora ? 208 * 1024 : 220 * 1024;
     if (const char* v = getenv("LSW_GEMV_SMEM_KB")) { long x = atol(v); if (x >= 32 && x <= 224) budget = (size_t)x * 1024; }
     int slots = (int)((budget - x_bytes) / slot_bytes);
     if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
@@ -772,7 +857,7 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
       if (grid < 1) grid = 1;
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3(grid);
-      lc.blockDim = dim3(kBulkThreads);
+      lc.blockDim = dim3(kBulkThreads + (lora ? 32 * kLoraWarps : 0));
       lc.dynamicSmemBytes = smem;
       lc.stream = s;
       cudaLaunchAttribute at[1];
@@ -781,18 +866,6 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
       lc.attrs = at;
       lc.numAttrs = 1;
       const GemvLora none{};
-      if (lora) {
-        // LoRA-down products first (PDL): the GEMV below streams its W at once
-        // and its consumers read u after griddepcontrol.wait
-        cudaLaunchConfig_t ld{};
-        ld.gridDim = dim3(p.n_sites * lora->k * lora->r);
-        ld.blockDim = dim3(32 * kLoraDownWarps);
-        ld.stream = s;
-        ld.attrs = at;
-        ld.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&ld, bf16 ? lora_down_kernel<true> : lora_down_kernel<false>, p, *lora);
-        if (e != cudaSuccess) return e;
-      }
       static const int probe = getenv("LSW_GEMV_PROBE") ? atoi(getenv("LSW_GEMV_PROBE")) : 0;   // tuning only
       return cudaLaunchKernelEx(&lc, fn, p, slots, R, (int32_t)((early_w || lora ? 1 : 0) | (probe ? 2 : 0)),
                                 lora ? *lora : none);

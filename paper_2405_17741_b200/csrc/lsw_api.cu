@@ -47,6 +47,7 @@ struct lsw_ctx {
   const void* router_w = nullptr;
   int device = 0;
   int num_sms = 148;
+  int gemv_sms = 148;                   // GEMV grid cap: num_sms (testing knob LSW_GEMV_GRID, read at create)
   int impl = LSW_IMPL_SIMT;
   SwitchParams simt_geom{};     // tile table for the SIMT kernel
   TcPlan* tc = nullptr;
@@ -155,6 +156,8 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
   cudaError_t e = cudaGetDevice(&ctx->device);
   if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "lsw_create: cudaGetDevice"); }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  ctx->gemv_sms = ctx->num_sms;
+  if (const char* v = getenv("LSW_GEMV_GRID")) { int x = atoi(v); if (x >= 1 && x < ctx->gemv_sms) ctx->gemv_sms = x; }
   e = cudaMalloc(&ctx->d_state, sizeof(DevState));
   if (e != cudaSuccess) { delete ctx; return fail(LSW_E_OOM, "lsw_create: cudaMalloc(state) failed"); }
   e = cudaMemset(ctx->d_state, 0, sizeof(DevState));
@@ -363,7 +366,7 @@ static lsw_status gemv_sites(lsw_ctx* ctx, int layer, const int* kinds, int n, c
   const bool allreduce = ctx->cfg.tp_size > 1 && ctx->kinds[kinds[0]].row_parallel;
   if (allreduce && !ctx->comm)
     return fail(LSW_E_NCCL, "%s: tp_size=%d but no NCCL communicator attached", who, ctx->cfg.tp_size);
-  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->num_sms, s, early_w);
+  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->gemv_sms, s, early_w);
   if (e != cudaSuccess) return cuda_fail(e, "decode GEMV launch");
   ++ctx->launches;
   // Row-parallel kinds under TP: partial sums -> allreduce.
@@ -413,11 +416,13 @@ static lsw_status gemv_unmerged(lsw_ctx* ctx, int layer, int group, const void* 
   L.k = ctx->cfg.top_k;
   L.r = ctx->cfg.rank;
   L.u = ctx->lora_u;
+  L.arrive = &ctx->d_state->lora_arrive;
+  L.depart = &ctx->d_state->lora_depart;
   if (const char* v = getenv("LSW_UNMERGED_FLAGS")) L.flags = atoi(v);   // tuning probes only
-  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->num_sms, s, early_w, &L);
+  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->gemv_sms, s, early_w, &L);
   if (e == cudaErrorNotSupported) return fail(LSW_E_UNSUPPORTED, "%s: needs the bulk GEMV (LSW_GEMV=ldg set)", who);
   if (e != cudaSuccess) return cuda_fail(e, "unmerged decode GEMV launch");
-  ctx->launches += 2;                       // LoRA-down + GEMV
+  ctx->launches += 1;                       // LoRA-down, GEMV and LoRA-up in one launch
   return LSW_OK;
 }
 

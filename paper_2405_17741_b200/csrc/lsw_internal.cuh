@@ -28,6 +28,8 @@ struct DevState {
   int32_t idx[2][LSW_MAX_TOPK];
   float g[2][LSW_MAX_TOPK];
   unsigned long long tok_done;   // group-completion counter of the whole-token GEMV (gemv.cu)
+  uint32_t lora_arrive;          // unmerged GEMV: LoRA-down products published in this launch
+  uint32_t lora_depart;          // unmerged GEMV: CTAs done (the last one resets both)
 };
 
 // One kind's stacked tensors, as the kernels see them.
@@ -155,9 +157,10 @@ struct GemvParams {
 };
 // Unmerged decode (Eq. 2 at P:228 without merging):
 // y = W x + sum_j scale * g_j * B_{e_j} (A_{e_j} x) for every site of a group,
-// W being the un-merged (pristine) weight.  Two launches per group: the k*r
-// LoRA-down products per site (lora_down_kernel, gemv.cu), then the GEMV, which
-// folds each row's LoRA-up term into its reduction.
+// W being the un-merged (pristine) weight.  ONE launch per group: the GEMV's
+// CTAs compute the k*r LoRA-down products per site (dealt over the grid,
+// published through a device counter) before streaming their W rows, and add
+// the LoRA-up term to their rows at the end of the stream (gemv.cu).
 struct GemvLora {
   const void* A[3];          // site q: A_kind of this layer [N, r, d_in]
   const void* B[3];          // site q: B_kind of this layer [N, d_out_q, r]
@@ -166,6 +169,8 @@ struct GemvLora {
   float scale;               // alpha / r
   int32_t k, r;
   float* u;                  // scratch [n_sites * k * r] fp32
+  uint32_t* arrive;          // DevState::lora_arrive / lora_depart (zero between launches)
+  uint32_t* depart;
   int32_t flags;             // tuning probe (LSW_UNMERGED_FLAGS): 4 = no LoRA-up term (results wrong)
 };
 // early_w: the previous launch on `s` was a GEMV (W may be prefetched before
@@ -179,7 +184,7 @@ struct LoraPrefetch {
   const int32_t* idx;         // [k] device
 };
 cudaError_t launch_lora_prefetch(const LoraPrefetch& q, cudaStream_t s);
-// lora: also launches the group's LoRA-down kernel first (2 launches).
+// lora: the unmerged form (LoRA-down and LoRA-up inside the same launch).
 cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w = false,
                         GemvLora* lora = nullptr);
 

@@ -17,8 +17,14 @@ ap.add_argument("--config", default="llama2-7b")
 ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--tokens", type=int, default=4)
 ap.add_argument("--impl", default="auto")
+ap.add_argument("--rank", type=int, default=0, help="override the config's LoRA rank (sweep cells)")
+ap.add_argument("--topk", type=int, default=0, help="override the config's top-k (sweep cells)")
 a = ap.parse_args()
 cfg = synth.get_config(a.config).with_(n_layers=a.layers)
+if a.rank:
+    cfg = cfg.with_(rank=a.rank)
+if a.topk:
+    cfg = cfg.with_(top_k=a.topk)
 W, A, B, router = H.build_weights(cfg, "cuda")
 sw = H.make_switch(cfg, W, A, B, router, impl=a.impl)
 X1 = synth.gen_x1(cfg, a.tokens, "cuda")

@@ -21,7 +21,7 @@ def t(fn, n=8):
         a.record(); fn(); b.record(); torch.cuda.synchronize(); ms.append(a.elapsed_time(b))
     return round(statistics.median(ms), 4)
 res = {"merged_gemvs": t(lambda: sw.decode_all_layers(xs, ys))}
-for f in ["0"]:
+for f in ["0", "4"]:
     os.environ["LSW_UNMERGED_FLAGS"] = f
     res["unmerged_flags" + f] = t(lambda: sw.decode_all_layers_unmerged(xs, ys, idx, gate))
 os.environ.pop("LSW_UNMERGED_FLAGS", None)

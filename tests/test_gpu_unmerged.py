@@ -1,7 +1,9 @@
 """Unmerged decode (Eq. 2 at P:228 without merging) vs the oracle (-m gpu).
 
 lsw_decode_group_unmerged computes y = W x + sum_j (alpha/r) g_j B_j (A_j x) on
-the pristine weights in one launch per group.  Checked through the C ABI
+the pristine weights in one launch per group (LoRA-down products dealt over
+the grid and published through a device counter, LoRA-up added at the end of
+each CTA's stream).  Checked through the C ABI
 against oracle.unmerged_forward on the same seeded inputs (fp64), for bf16 and
 fp32 storage, k*r below and above one warp (32), and k = 1..4; the whole-layer
 call equals the per-group calls bitwise; the merged path (Eq. 3 on the merged
@@ -26,9 +28,15 @@ def _f64(t):
     return t.detach().to("cpu").to(torch.float64).numpy()
 
 
-@pytest.mark.parametrize("name,impl", [("toy", "simt"), ("mini", "tc"), ("mini-r32", "tc"), ("mini-r64k3", "tc"),
-                                       ("mini-r4k4", "tc"), ("mini-k1", "tc")])
-def test_unmerged_decode_matches_oracle(name, impl):
+@pytest.mark.parametrize("name,impl,grid", [("toy", "simt", None), ("mini", "tc", None), ("mini-r32", "tc", None),
+                                            ("mini-r64k3", "tc", None), ("mini-r4k4", "tc", None),
+                                            ("mini-k1", "tc", None), ("mini", "tc", "3"), ("mini-r64k3", "tc", "2")])
+def test_unmerged_decode_matches_oracle(monkeypatch, name, impl, grid):
+    """grid: a GEMV grid of a few CTAs, so each CTA computes many LoRA-down
+    products over several warps and the device counters are reset and reused
+    across many launches."""
+    if grid:
+        monkeypatch.setenv("LSW_GEMV_GRID", grid)
     cfg = synth.get_config(name)
     W, A, B, router = H.build_weights(cfg, "cuda")
     sw = H.make_switch(cfg, W, A, B, router, impl=impl)
