@@ -263,8 +263,10 @@ LSW_API lsw_status lsw_decode_all_layers(lsw_ctx* ctx, const void* xs, float* ys
  * without merging): y = W x + sum_j (alpha/r) g_j B[e_j] (A[e_j] x) for every
  * site of `group`, on the UN-merged weights.  W is read once (2 B/element)
  * instead of being switched (4 B) and then read (2 B).  One launch per group:
- * the k*r LoRA-down products of each site are spread over the grid, then one
- * device-wide barrier, then each row's LoRA-up term joins its reduction.
+ * extra warps of each CTA compute the group's k*r LoRA-down products per site
+ * (spread over the grid, published through a device counter) and the LoRA-up
+ * terms of the CTA's rows while its W rows stream; y = (W x) + term, one
+ * rounding of the sum per row; deterministic (fixed reduction orders).
  *   idx/gate: device [top_k] (from lsw_router_topk).  x, y as lsw_decode_group.
  *   LSW_E_STATE if the ctx is merged (W must be the pristine weight);
  *   LSW_E_UNSUPPORTED if tp_size > 1 (o/down would need an all-reduce of A x).
