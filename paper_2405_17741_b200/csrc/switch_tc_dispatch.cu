@@ -97,11 +97,16 @@ cudaError_t tc_plan_set_pristine(TcPlan* p, const SwitchParams& geom) {
                          fc::tc_plan_set_pristine(p->c, geom));
 }
 
-// The fused switch + decode exists in the v1 kernel only: when the ctx switches
-// with another kernel, a v1 plan (its own packed operands) is built for it on
-// first use; W after a fused token is bitwise what the plain v1 switch stores.
+// The fused switch + decode: the fc kernel's own fused build when the ctx
+// switches with fc (W after a fused token is bitwise what its plain switch
+// stores); else the v1 kernel's -- a ctx switching with tg builds a v1 plan
+// (its own packed operands) on first use.
 cudaError_t tc_plan_set_fused(TcPlan* p, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
                               int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]) {
+  if (p->which == 3) {
+    const cudaError_t e = fc::tc_plan_set_fused(p->c, n_layers, x_off, y_off, x_per_layer, y_per_layer, kinds, nk);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (!p->a) {
     const char* why = "";
     cudaError_t e = v1::tc_plan_create(&p->a, p->geom, p->num_sms, &why, /*strict=*/true);
@@ -111,6 +116,10 @@ cudaError_t tc_plan_set_fused(TcPlan* p, int n_layers, const int64_t x_off[4], c
 }
 
 cudaError_t launch_switch_tc_fused(const TcPlan* p, const SwitchParams& sp, cudaStream_t s, const void* xs, float* ys) {
+  if (p->which == 3) {
+    const cudaError_t e = fc::launch_switch_tc_fused(p->c, sp, s, xs, ys);
+    if (e != cudaErrorNotSupported) return e;
+  }
   if (!p->a) return cudaErrorNotSupported;
   return v1::launch_switch_tc_fused(p->a, sp, s, xs, ys);
 }

@@ -60,6 +60,7 @@ struct Geom {
   const __nv_bfloat16* At[LSW_NKIND];   // packed A^T [L, col_tiles, N, 128, rp], pre-swizzled
   const __nv_bfloat16* Bp[LSW_NKIND];   // packed B   [L*N, dout_pad, rp], pre-swizzled
   int64_t dout_pad[LSW_NKIND];
+  int64_t d_in[LSW_NKIND], d_out[LSW_NKIND];
   int64_t tiles_total;
   int32_t n_experts, rp;
   int32_t w_stages, a_stages, b_bufs;
@@ -71,9 +72,25 @@ struct Geom {
                                         //    contiguous in smem and in the request stream; LSW_FC_WRM)
 };
 
+// Fused switch + decode: one segment per (layer, GEMV group),
+// tiles walked in decoder order; the epilogue also accumulates
+// y_seg += RNE(W_new) x_seg from the freshly rounded tile.
+struct FusedSeg {
+  int64_t tile_begin, tile_count;   // fused-order tiles of this segment
+  int32_t layer, n_kinds;
+  int32_t kinds[3];                 // kind ids in group order
+  int32_t pad;
+  int64_t x_off;                    // elements into xs of this segment's input
+  int64_t y_off[3];                 // elements into ys of each kind's row 0
+};
+
 struct TcPlan {
   Maps maps;
   Geom geom;
+  FusedSeg* d_segs = nullptr;       // fused mode (tc_plan_set_fused)
+  unsigned long long* d_seg_done = nullptr;
+  int32_t n_segs = 0;
+  int64_t fused_tiles = 0;
   int32_t chunk = 48;
   int32_t probe = 0;          // tuning only (LSW_TC_PROBE=1): W stream alone, W written back unchanged
   void* packed_At[LSW_NKIND] = {};
@@ -91,7 +108,99 @@ struct Args {
   const float* cur_g;
   DevState* state;
   int64_t t0, t_count;        // tile range of this launch (t_count = 0: all tiles)
+  // fused switch + decode only
+  const FusedSeg* segs;
+  int32_t n_seg;
+  const __nv_bfloat16* xs;
+  float* ys;
+  unsigned long long* seg_done;   // [n_seg], zeroed before the launch
 };
+
+// ------------------------------------------------------------------ tile walk
+
+// The plain pass walks tcx's (kind, layer, rb, cb) order in chunks dealt
+// round-robin over the CTAs; the fused pass the decoder order: segment (layer,
+// group), kind within the group, rb, cb.
+struct FCursor : Cursor {
+  int32_t seg, kidx;
+};
+
+// fused order: CTA b takes, in every segment s (T_s tiles), the contiguous
+// range [T_s * b / G, T_s * (b + 1) / G) -- every CTA finishes each segment at
+// about the same time, so the decoder-order barrier between segments waits
+// for ~one tile of imbalance, not for a whole chunk of another CTA.
+__device__ __forceinline__ void fused_at(const TileKinds& g, const Args& a, FCursor& c, int seg, int64_t t) {
+  const FusedSeg& S = a.segs[seg];
+  int64_t off = t - S.tile_begin;
+  int ki = 0, kd = S.kinds[0];
+  for (; ki < S.n_kinds; ++ki) {
+    kd = S.kinds[ki];
+    const int64_t per = (int64_t)g.row_tiles[kd] * g.col_tiles[kd];
+    if (off < per) break;
+    off -= per;
+  }
+  c.t = t;
+  c.seg = seg;
+  c.kidx = ki;
+  c.kd = kd;
+  c.layer = S.layer;
+  c.rb = (int)(off / g.col_tiles[kd]);
+  c.cb = (int)(off - (int64_t)c.rb * g.col_tiles[kd]);
+}
+
+// this CTA's first tile in segment >= seg (t = -1: none left)
+__device__ __forceinline__ void fused_from(const TileKinds& g, const TileSeq& q, const Args& a, FCursor& c, int seg) {
+  for (; seg < a.n_seg; ++seg) {
+    const FusedSeg& S = a.segs[seg];
+    const int64_t lo = S.tile_count * q.b / q.G, hi = S.tile_count * (q.b + 1) / q.G;
+    if (lo < hi) { fused_at(g, a, c, seg, S.tile_begin + lo); return; }
+  }
+  c.t = -1;
+}
+
+template <bool kF>
+__device__ __forceinline__ FCursor cur_first(const TileKinds& g, const TileSeq& q, const Args& a) {
+  FCursor c;
+  if constexpr (kF) {
+    fused_from(g, q, a, c, 0);
+  } else {
+    static_cast<Cursor&>(c) = cursor_first(g, q);
+  }
+  return c;
+}
+
+template <bool kF>
+__device__ __forceinline__ void cur_next(const TileKinds& g, const TileSeq& q, const Args& a, FCursor& c) {
+  if constexpr (kF) {
+    const FusedSeg& S = a.segs[c.seg];
+    if (c.t + 1 < S.tile_begin + S.tile_count * (q.b + 1) / q.G) {
+      ++c.t;
+      if (++c.cb == g.col_tiles[c.kd]) {
+        c.cb = 0;
+        if (++c.rb == g.row_tiles[c.kd]) {
+          c.rb = 0;
+          ++c.kidx;
+          c.kd = S.kinds[c.kidx];
+        }
+      }
+      return;
+    }
+    fused_from(g, q, a, c, c.seg + 1);
+  } else {
+    cursor_next(g, q, static_cast<Cursor&>(c));
+  }
+}
+
+__device__ __forceinline__ void wait_count(const unsigned long long* p, unsigned long long target) {
+  unsigned long long v;
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    if (v >= target) return;
+    __nanosleep(64);
+    if (globaltimer() - t0 > 20000000000ull) __trap();
+  }
+}
 
 // ------------------------------------------------------------------ fold
 
@@ -140,8 +249,34 @@ __device__ __forceinline__ void epi16(uint8_t* wrow, int key, int flip, int col1
   *pb = flip ? o0 : o1;
 }
 
+// As epi16, and y += RNE(W + D) . x over the 16 columns (fp32 FMA in column
+// order; x: 16 bf16 of this thread's columns).
+__device__ __forceinline__ float epi16_dot(uint8_t* wrow, int key, int flip, int col16, const uint32_t* acc,
+                                           const uint4 x0, const uint4 x1, float y) {
+  uint4* pa = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + flip) ^ key) << 4));
+  uint4* pb = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + (flip ^ 1)) ^ key) << 4));
+  const uint4 ua = *pa, ub = *pb;
+  const uint4 u0 = flip ? ub : ua, u1 = flip ? ua : ub;
+  const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+  const uint32_t xw[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+  uint32_t o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint64_t v = fadd2(f2_pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u)),
+                             f2_pack(__uint_as_float(acc[2 * q]), __uint_as_float(acc[2 * q + 1])));
+    o[q] = f2_to_bf16x2(v);
+    y = fmaf(__uint_as_float(o[q] << 16), __uint_as_float(xw[q] << 16), y);
+    y = fmaf(__uint_as_float(o[q] & 0xffff0000u), __uint_as_float(xw[q] & 0xffff0000u), y);
+  }
+  const uint4 o0 = make_uint4(o[0], o[1], o[2], o[3]), o1 = make_uint4(o[4], o[5], o[6], o[7]);
+  *pa = flip ? o1 : o0;
+  *pb = flip ? o0 : o1;
+  return y;
+}
+
 // ------------------------------------------------------------------ the kernel
 
+template <bool kF>
 __global__ void __launch_bounds__(kThreads, 1)
 switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -222,7 +357,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         const uint64_t pol_stream = policy_evict_first();
         const CUtensorMap* src = args.mode == MODE_RESTORE ? maps.p : maps.w;   // RESTORE reads P
         Ring wring{0, 0, (uint32_t)g.w_stages};
-        for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+        for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
           mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
           const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
           mbar_expect_tx(wbar, 2 * kSubBytes);
@@ -241,7 +376,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       if (lane == 0) {
         const uint64_t pol_stream = policy_evict_first();
         Ring wring{0, 0, (uint32_t)g.w_stages};
-        for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+        for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
           mbar_wait(smem_u32(&bar_wdone[wring.i]), wring.phase);     // epilogue wrote the tile
           uint8_t* wsrc = wst0 + (size_t)wring.i * (2 * kSubBytes);
           if (g.wrm)
@@ -257,7 +392,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         }
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
-    } else if (warp == 3 && !args.probe) {
+    } else if (warp == 3 && !(args.probe & 1)) {
       // ============================ operand producer ========================
       // Per strip (rare): raw B slices of all terms by bulk copies into the lo
       // slots, then the whole warp folds them into (hi, lo) parts in place and
@@ -271,7 +406,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       int64_t strip_prev = -1;
       Ring bring{0, 0, (uint32_t)g.b_bufs};
       Ring aring{0, 0, (uint32_t)g.a_stages};
-      for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+      for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
         if (strip_id(c) != strip_prev) {
           if (strip_prev >= 0) bring.next();
           strip_prev = strip_id(c);
@@ -312,7 +447,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         __syncwarp();
         aring.next();
       }
-    } else if (warp == 1 && !args.probe) {
+    } else if (warp == 1 && !(args.probe & 1)) {
       // ============================ MMA issuer ==============================
       // One chain per tile: for every term, the hi and lo parts times the A^T
       // slice, K = rp each in steps of 16, into the tile's single accumulator;
@@ -328,7 +463,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       Ring aring{0, 0, (uint32_t)g.a_stages};
       Ring acc{0, 0, (uint32_t)kAccBufs};
       int64_t strip_prev = -1;
-      for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
+      for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
         if (strip_id(c) != strip_prev) {
           if (strip_prev >= 0) bring.next();
           strip_prev = strip_id(c);
@@ -364,8 +499,36 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       Ring acc{0, 0, (uint32_t)kAccBufs};
       Ring aring{0, 0, (uint32_t)g.a_stages}, bring{0, 0, (uint32_t)g.b_bufs};
       int64_t bstrip = -1;
-      for (Cursor c = cursor_first(tk, seq); c.t >= 0; cursor_next(tk, seq, c)) {
-        if (args.probe) {                          // tuning: the W stream alone
+      int cur_seg = -1;                            // fused: segment of the previous tile
+      unsigned long long seg_mine = 0;             // fused: tiles of cur_seg this CTA finished
+      for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
+        uint4 xv[8];                               // fused: x of this thread's 64 columns
+        if constexpr (kF) {
+          if (c.seg != cur_seg) {
+            // decoder order: x of segment s is final only once every tile of
+            // segment s-1 is done -- one thread per CTA publishes the CTA's
+            // count of the segment it leaves and waits for the previous total
+            asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
+            if (releaser) {
+              if (cur_seg >= 0) {
+                __threadfence();
+                asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(args.seg_done + cur_seg),
+                             "l"(seg_mine) : "memory");
+              }
+              if (c.seg > 0 && !(args.probe & 4))
+                wait_count(&args.seg_done[c.seg - 1], (unsigned long long)args.segs[c.seg - 1].tile_count);
+            }
+            asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
+            cur_seg = c.seg;
+            seg_mine = 0;
+          }
+          const int64_t col0 = (int64_t)c.cb * kTN + half * kSubCols;
+          const int64_t lim = g.d_in[c.kd] - col0;      // columns of this half inside d_in
+          const uint4* xp = reinterpret_cast<const uint4*>(args.xs + args.segs[c.seg].x_off + col0);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) xv[v] = 8 * v < lim ? __ldg(xp + v) : make_uint4(0, 0, 0, 0);
+        }
+        if (args.probe & 1) {                      // tuning: the W stream alone
           mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -402,12 +565,32 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         // default: two [128 rows][64 cols] boxes; wrm: one [128 rows][2 x 64 cols] box
         const int unit = g.wrm ? 2 * row + half : half * kTM + row;
         uint8_t* wrow = wst0 + (size_t)wring.i * (2 * kSubBytes) + unit * 128;
+        if (kF && !(args.probe & 8)) {
+          float y = 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) epi16(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q]);
+          for (int q = 0; q < 4; ++q)
+            y = epi16_dot(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q], xv[2 * q], xv[2 * q + 1], y);
+          const int64_t grow = (int64_t)c.rb * kTM + row;
+          if (grow < g.d_out[c.kd]) atomicAdd(args.ys + args.segs[c.seg].y_off[c.kidx] + grow, y);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) epi16(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q]);
+        }
+        if constexpr (kF) ++seg_mine;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> TMA store
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
         wring.next();
+      }
+      if constexpr (kF) {
+        if (cur_seg >= 0) {                        // publish the last segment this CTA worked on
+          asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
+          if (releaser) {
+            __threadfence();
+            asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(args.seg_done + cur_seg),
+                         "l"(seg_mine) : "memory");
+          }
+        }
       }
     }
   }
@@ -503,17 +686,27 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   g.a_stage_bytes = align1k((uint32_t)mt * g.term_bytes);
   g.b_buf_bytes = align1k((uint32_t)(2 * mt) * g.term_bytes);
   const uint32_t w_stage = 2 * kSubBytes;
-  // Shared-memory plan: first W stages >= 4, B double-buffered, A stages >= 3,
-  // then relax (B single, A 2, W 3); what is left goes to more W stages.
+  // Shared-memory plan, in order of preference (measured, 7B shape: W 3 + B 2 +
+  // A 3 0.895 of the copy peak vs W 4 + B 1 + A 3 0.868 -- a single B buffer
+  // drains the MMA pipeline at every strip change, a 4th W stage buys nothing);
+  // what is left goes to more W stages.
   const int64_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
   struct Try { int ws, bb, as; };
-  const Try tries[] = {{4, 2, 3}, {4, 1, 3}, {4, 2, 2}, {4, 1, 2}, {3, 2, 2}, {3, 1, 2}, {2, 1, 2}};
+  const Try tries[] = {{4, 2, 3}, {3, 2, 3}, {4, 2, 2}, {3, 2, 2}, {4, 1, 3}, {4, 1, 2}, {3, 1, 2}, {2, 1, 2}};
   int bb_env = 0, as_env = 0, ws_env = 0;
   if (const char* v = getenv("LSW_FC_BBUFS")) bb_env = atoi(v);
   if (const char* v = getenv("LSW_FC_ASTAGES")) as_env = atoi(v);
   if (const char* v = getenv("LSW_FC_STAGES")) ws_env = atoi(v);
   bool ok = false;
+  if (bb_env >= 1 && bb_env <= 2 && as_env >= 2 && as_env <= kMaxAStages && ws_env >= 2 && ws_env <= kMaxStages &&
+      budget >= (int64_t)bb_env * g.b_buf_bytes + (int64_t)as_env * g.a_stage_bytes + (int64_t)ws_env * w_stage) {
+    g.w_stages = ws_env;                     // tuning: an explicit plan (all three knobs set)
+    g.a_stages = as_env;
+    g.b_bufs = bb_env;
+    ok = true;
+  }
   for (const Try& t : tries) {
+    if (ok) break;
     const int bb = bb_env >= 1 && bb_env <= 2 ? bb_env : t.bb;
     const int as = as_env >= 2 && as_env <= kMaxAStages ? as_env : t.as;
     const int64_t rest = budget - (int64_t)bb * g.b_buf_bytes - (int64_t)as * g.a_stage_bytes;
@@ -525,7 +718,6 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     g.a_stages = as;
     g.b_bufs = bb;
     ok = true;
-    break;
   }
   if (!ok) { delete plan; *why = "shared memory: rank * top_k too large for the folded kernel"; return cudaErrorNotSupported; }
   if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
@@ -543,6 +735,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     g.tk.row_tiles[k] = (int32_t)((kg.d_out + kTM - 1) / kTM);
     g.tk.col_tiles[k] = (int32_t)((kg.d_in + kTN - 1) / kTN);
     g.dout_pad[k] = (int64_t)g.tk.row_tiles[k] * kTM;
+    g.d_in[k] = kg.d_in;
+    g.d_out[k] = kg.d_out;
     g.tk.tile_begin[k] = t;
     t += (int64_t)sp.n_layers * g.tk.row_tiles[k] * g.tk.col_tiles[k];
   }
@@ -578,7 +772,9 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(switch_fc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+    e = cudaFuncSetAttribute(switch_fc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(switch_fc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
   if (e != cudaSuccess) {
     if (!*why || !**why) *why = cudaGetErrorString(e);
     tc_plan_destroy(plan);
@@ -594,6 +790,8 @@ void tc_plan_destroy(TcPlan* plan) {
     cudaFree(plan->packed_At[k]);
     cudaFree(plan->packed_B[k]);
   }
+  cudaFree(plan->d_segs);
+  cudaFree(plan->d_seg_done);
   delete plan;
 }
 
@@ -632,7 +830,78 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   a.cur_idx = p.cur_idx;
   a.cur_g = p.cur_g;
   a.state = p.state;
-  switch_fc_kernel<<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  a.segs = nullptr;
+  a.n_seg = 0;
+  a.xs = nullptr;
+  a.ys = nullptr;
+  a.seg_done = nullptr;
+  switch_fc_kernel<false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  return cudaGetLastError();
+}
+
+// Fused switch + decode: segment table in decoder order (layer, group), built
+// once per ctx.
+cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
+                              int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]) {
+  const Geom& g = plan->geom;
+  for (int k = 0; k < LSW_NKIND; ++k) if (g.d_in[k] % 8) return cudaErrorNotSupported;   // 16-B x loads
+  const int n = 4 * n_layers;
+  FusedSeg* h = new FusedSeg[n];
+  int64_t t = 0;
+  for (int l = 0; l < n_layers; ++l)
+    for (int gi = 0; gi < 4; ++gi) {
+      FusedSeg& S = h[l * 4 + gi];
+      memset(&S, 0, sizeof(S));
+      S.tile_begin = t;
+      S.layer = l;
+      S.n_kinds = nk[gi];
+      S.x_off = l * x_per_layer + x_off[gi];
+      int64_t yo = l * y_per_layer + y_off[gi];
+      for (int i = 0; i < nk[gi]; ++i) {
+        const int kd = kinds[gi][i];
+        S.kinds[i] = kd;
+        S.y_off[i] = yo;
+        yo += g.d_out[kd];
+        S.tile_count += (int64_t)g.tk.row_tiles[kd] * g.tk.col_tiles[kd];
+      }
+      t += S.tile_count;
+    }
+  cudaError_t e = cudaSuccess;
+  if (!plan->d_segs) e = cudaMalloc(&plan->d_segs, sizeof(FusedSeg) * n);
+  if (e == cudaSuccess && !plan->d_seg_done) e = cudaMalloc(&plan->d_seg_done, sizeof(unsigned long long) * n);
+  if (e == cudaSuccess) e = cudaMemcpy(plan->d_segs, h, sizeof(FusedSeg) * n, cudaMemcpyHostToDevice);
+  delete[] h;
+  if (e != cudaSuccess) return e;
+  plan->n_segs = n;
+  plan->fused_tiles = t;
+  return cudaSuccess;
+}
+
+cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, const void* xs,
+                                   float* ys) {
+  if (!plan->d_segs) return cudaErrorNotSupported;
+  cudaError_t e = cudaMemsetAsync(plan->d_seg_done, 0, sizeof(unsigned long long) * plan->n_segs, s);
+  if (e != cudaSuccess) return e;
+  Args a;
+  a.t0 = 0;
+  a.t_count = plan->fused_tiles;
+  a.g = plan->geom;
+  a.chunk = 1;                     // unused: per-segment ranges (fused_from)
+  a.probe = 0;            // tuning only (LSW_FC_FUSED_PROBE): 4 = no segment wait, 8 = no GEMV (results wrong)
+  if (const char* v = getenv("LSW_FC_FUSED_PROBE")) a.probe = atoi(v) & 12;
+  a.mode = p.mode;
+  a.top_k = p.top_k;
+  a.n_experts = p.n_experts;
+  a.scale = p.scale;
+  a.cur_idx = p.cur_idx;
+  a.cur_g = p.cur_g;
+  a.state = p.state;
+  a.segs = plan->d_segs;
+  a.n_seg = plan->n_segs;
+  a.xs = static_cast<const __nv_bfloat16*>(xs);
+  a.ys = ys;
+  a.seg_done = plan->d_seg_done;
+  switch_fc_kernel<true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   return cudaGetLastError();
 }
 

@@ -75,6 +75,11 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
                              int64_t t_count = 0);
 int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t0);
 cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
+// fused switch + decode: decoder-order segment table, then launches
+cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
+                              int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]);
+cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, const void* xs,
+                                   float* ys);
 }  // namespace fc
 
 // the fc kernel is the default from kFcMinMmas MMAs per tile on (i.e. unless

@@ -21,6 +21,8 @@ ap.add_argument("--layers", type=int, default=0)
 ap.add_argument("--iters", type=int, default=12)
 ap.add_argument("--impl", default="tc")
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--rank", type=int, default=0, help="override the config's LoRA rank (sweep cells)")
+ap.add_argument("--topk", type=int, default=0, help="override the config's top-k (sweep cells)")
 ap.add_argument("--lib", default="", help="load this liblsw.so instead of the package's (A/B of two builds)")
 ap.add_argument("settings", nargs="*", default=["order=strip", "order=sweep,chunk=1", "order=sweep,chunk=4"])
 a = ap.parse_args()
@@ -30,6 +32,10 @@ if a.lib:
 cfg = synth.get_config(a.config)
 if a.layers:
     cfg = cfg.with_(n_layers=a.layers)
+if a.rank:
+    cfg = cfg.with_(rank=a.rank)
+if a.topk:
+    cfg = cfg.with_(top_k=a.topk)
 W, A, B, router = H.build_weights(cfg, "cuda")
 tb = H.token_bytes(cfg)
 X1 = synth.gen_x1(cfg, a.iters + 4, "cuda")

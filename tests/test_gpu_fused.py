@@ -1,7 +1,8 @@
 """Fused switch + decode on the GPU (-m gpu).
 
-lsw_decode_token_fused runs the router and ONE launch that switches every
-adapted matrix and computes the group GEMVs from the freshly rounded tiles,
+lsw_decode_token_fused runs the router and ONE launch (the ctx's fc kernel, or
+v1) that switches every adapted matrix and computes the group GEMVs from the
+freshly rounded tiles,
 in decoder order with a segment barrier per (layer, group).  Checked through
 the C ABI: the weights after every token are bitwise those of the separate
 path (lsw_decode_token: switch launch + GEMV launches), the outputs equal its
@@ -28,10 +29,13 @@ def _f64(t):
     return t.detach().to("cpu").to(torch.float64).numpy()
 
 
+@pytest.mark.parametrize("kernel", ["v1", "fc"])
 @pytest.mark.parametrize("name,grid", [("mini", None), ("mini", "3"), ("mini", "1"), ("mini-r32", None),
-                                       ("mini-k1", "5")])
-def test_fused_token_equals_separate_path(monkeypatch, name, grid):
-    monkeypatch.setenv("LSW_TC_KERNEL", "v1")
+                                       ("mini-k1", "5"), ("mini-r4k4", "2")])
+def test_fused_token_equals_separate_path(monkeypatch, name, grid, kernel):
+    if kernel == "v1" and name == "mini-r4k4":
+        pytest.skip("v1 has no plan for 2k = 8 terms")
+    monkeypatch.setenv("LSW_TC_KERNEL", kernel)
     if grid:
         monkeypatch.setenv("LSW_TC_GRID", grid)
     cfg = synth.get_config(name)
@@ -41,7 +45,7 @@ def test_fused_token_equals_separate_path(monkeypatch, name, grid):
         sw = H.make_switch(cfg, W, A, B, router, impl="tc")
         ctxs.append((sw, W, A, B))
     info = ctxs[0][0].info()
-    assert info["switch_kernel"] == 1
+    assert info["switch_kernel"] == {"v1": 1, "fc": 3}[kernel]
     X1 = synth.gen_x1(cfg, 5, "cuda")
     xs_d = synth.gen_xs(cfg, "cuda")
     xs = H.pack_xs(cfg, xs_d)
@@ -81,8 +85,8 @@ def test_fused_token_equals_separate_path(monkeypatch, name, grid):
 
 @pytest.mark.parametrize("kernel", ["fc", "tg"])
 def test_fused_on_a_ctx_that_switches_with_another_kernel(monkeypatch, kernel):
-    """The fused launch exists in the v1 kernel only; a ctx whose switch kernel
-    is fc or tg builds a v1 plan for it on first use.  Plain tokens (the ctx's
+    """The fused launch exists in the v1 and fc kernels; a ctx whose switch
+    kernel is tg builds a v1 plan for it on first use.  Plain tokens (the ctx's
     own kernel) and fused tokens (v1) alternate on the same W and decision
     slot: W stays on the oracle's stored trajectory and every token's outputs
     match the oracle's GEMV on it."""
