@@ -465,7 +465,15 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       int64_t strip_prev = -1;
       for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
         if (strip_id(c) != strip_prev) {
-          if (strip_prev >= 0) bring.next();
+          if (strip_prev >= 0) {
+            // every MMA of the previous strip is issued: its B buffer is free
+            // once they complete -- released by a commit here, not after the
+            // epilogue (up to kAccBufs tiles behind) has seen them, so a single
+            // B buffer is refolded while the epilogue drains the accumulators
+            if (elect_one()) umma_commit(smem_u32(&bar_bempty[bring.i]));
+            __syncwarp();
+            bring.next();
+          }
           strip_prev = strip_id(c);
           mbar_wait(smem_u32(&bar_bfull[bring.i]), bring.phase);
         }
@@ -494,11 +502,10 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       const int ew = warp - kFirstEpiWarp;
       const int quarter = warp & 3, half = ew >> 2;
       const int row = quarter * 32 + lane;
-      const bool releaser = ew == 0 && lane == 0;   // frees A stages / B strips for the producer
+      const bool releaser = ew == 0 && lane == 0;   // frees A stages for the producer
       Ring wring{0, 0, (uint32_t)g.w_stages};
       Ring acc{0, 0, (uint32_t)kAccBufs};
-      Ring aring{0, 0, (uint32_t)g.a_stages}, bring{0, 0, (uint32_t)g.b_bufs};
-      int64_t bstrip = -1;
+      Ring aring{0, 0, (uint32_t)g.a_stages};
       int cur_seg = -1;                            // fused: segment of the previous tile
       unsigned long long seg_mine = 0;             // fused: tiles of cur_seg this CTA finished
       for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
@@ -535,18 +542,6 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
           wring.next();
           continue;
-        }
-        if (releaser) {
-          // first tile of a new strip: every MMA of the previous strip is done
-          // (its last accumulator has been seen), so its B buffer is free
-          const int64_t st = strip_id(c);
-          if (st != bstrip) {
-            if (bstrip >= 0) {
-              mbar_arrive(smem_u32(&bar_bempty[bring.i]));
-              bring.next();
-            }
-            bstrip = st;
-          }
         }
         mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);      // the tile's MMAs are complete
         if (releaser) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
