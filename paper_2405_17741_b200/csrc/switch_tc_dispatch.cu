@@ -34,10 +34,20 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, 
   const bool prefer_fc = fc::fc_mmas_per_tile(geom) >= kFcMinMmas;
   const bool prefer_tg = 2 * geom.top_k <= 2;
   if (force_fc || (!force_v1 && !force_tg && prefer_fc)) {
-    e = fc::tc_plan_create(&p->c, geom, num_sms, why);
+    // fc's two modes (measured): the folded one up to 2k * rp =
+    // 128 at r <= 32 (the BASELINE configs), the per-term one for r = 64 and
+    // for r = 32 with k >= 3; either falls back to the other if its shared-
+    // memory plan does not fit (LSW_FC_PT forces one inside fc)
+    const int rp = geom.rank <= 16 ? 16 : geom.rank <= 32 ? 32 : 64;
+    const int pt_first = (rp == 64 || (rp == 32 && geom.top_k >= 3)) ? 1 : 0;
+    for (int m = 0; m < 2 && e != cudaSuccess; ++m) {
+      e = fc::tc_plan_create(&p->c, geom, num_sms, why, m == 0 ? pt_first : 1 - pt_first);
+      if (e != cudaSuccess && e != cudaErrorNotSupported) { delete p; return e; }
+      if (e != cudaSuccess) { (void)cudaGetLastError(); p->c = nullptr; }
+    }
     if (e == cudaSuccess) p->which = 3;
-    else if (e != cudaErrorNotSupported || force_fc) { delete p; return e; }
-    else { (void)cudaGetLastError(); *why = ""; }
+    else if (force_fc) { delete p; return e; }
+    else *why = "";
   }
   if (e != cudaSuccess && !force_tg && (force_v1 || !prefer_tg)) {
     e = v1::tc_plan_create(&p->a, geom, num_sms, why, /*strict=*/!force_v1);

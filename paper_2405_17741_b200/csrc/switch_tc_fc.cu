@@ -49,6 +49,7 @@ constexpr int kThreads = 32 * (kFirstEpiWarp + kEpiWarps);
 constexpr int kMaxStages = 8;
 constexpr int kMaxAStages = 8;
 constexpr int kAccBufs = 4;                 // 4 x 128 columns = all of TMEM
+constexpr int kPtGroup = 2;                 // per-term mode: terms per MMA group / TMEM buffer
 
 struct Maps {
   CUtensorMap w[LSW_NKIND];   // W [L, d_out, d_in], box {64, 128, 1}, 128B swizzle
@@ -70,6 +71,10 @@ struct Geom {
   uint32_t smem_bytes;
   int32_t wrm;                          // 1: W tile moved row-major by one 4-D TMA op (256 B per row
                                         //    contiguous in smem and in the request stream; LSW_FC_WRM)
+  int32_t pt;                           // 1: per-term mode (no fold): each term its own fp32 TMEM
+                                        //    accumulator of 128 columns, kPtGroup terms per commit
+  int32_t acc_bufs;                     // TMEM accumulator buffers of acc_cols columns
+  uint32_t acc_cols;
 };
 
 // Fused switch + decode: one segment per (layer, GEMV group),
@@ -249,6 +254,32 @@ __device__ __forceinline__ void epi16(uint8_t* wrow, int key, int flip, int col1
   *pb = flip ? o0 : o1;
 }
 
+// per-term mode: one 16-column chunk of a W row (swizzle key / flip as epi16)
+// widened to fp32 pairs, and the pairs rounded (RNE) back in place
+__device__ __forceinline__ void w_load16(const uint8_t* wrow, int key, int flip, int col16, uint64_t* v) {
+  const uint4 ua = *reinterpret_cast<const uint4*>(wrow + (((col16 * 2 + flip) ^ key) << 4));
+  const uint4 ub = *reinterpret_cast<const uint4*>(wrow + (((col16 * 2 + (flip ^ 1)) ^ key) << 4));
+  const uint4 u0 = flip ? ub : ua, u1 = flip ? ua : ub;
+  const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = f2_pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u));
+}
+
+__device__ __forceinline__ void w_store16(uint8_t* wrow, int key, int flip, int col16, const uint64_t* v) {
+  uint32_t o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[q] = f2_to_bf16x2(v[q]);
+  const uint4 o0 = make_uint4(o[0], o[1], o[2], o[3]), o1 = make_uint4(o[4], o[5], o[6], o[7]);
+  *reinterpret_cast<uint4*>(wrow + (((col16 * 2 + flip) ^ key) << 4)) = flip ? o1 : o0;
+  *reinterpret_cast<uint4*>(wrow + (((col16 * 2 + (flip ^ 1)) ^ key) << 4)) = flip ? o0 : o1;
+}
+
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 // As epi16, and y += RNE(W + D) . x over the 16 columns (fp32 FMA in column
 // order; x: 16 bf16 of this thread's columns).
 __device__ __forceinline__ float epi16_dot(uint8_t* wrow, int key, int flip, int col16, const uint32_t* acc,
@@ -276,7 +307,7 @@ __device__ __forceinline__ float epi16_dot(uint8_t* wrow, int key, int flip, int
 
 // ------------------------------------------------------------------ the kernel
 
-template <bool kF>
+template <bool kF, bool kPT>
 __global__ void __launch_bounds__(kThreads, 1)
 switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -323,7 +354,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       mbar_init(smem_u32(&bar_bfull[s]), 1);
       mbar_init(smem_u32(&bar_bempty[s]), 1);
     }
-    for (int s = 0; s < kAccBufs; ++s) {
+    for (int s = 0; s < g.acc_bufs; ++s) {
       mbar_init(smem_u32(&bar_accfull[s]), 1);
       mbar_init(smem_u32(&bar_accempty[s]), kEpiWarps);
     }
@@ -393,6 +424,45 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
     } else if (warp == 3 && !(args.probe & 1)) {
+      if constexpr (kPT) {
+        // per-term mode: raw B slices per strip and A^T slices per (tile, term
+        // group), all by bulk copies completing on the consumers' barriers
+        if (lane == 0) {
+          const uint64_t pol_keep = policy_evict_last();
+          const size_t rpe = (size_t)g.rp;
+          const uint32_t tb = g.term_bytes;
+          int64_t strip_prev = -1;
+          Ring bring{0, 0, (uint32_t)g.b_bufs};
+          Ring aring{0, 0, (uint32_t)g.a_stages};
+          for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
+            if (strip_id(c) != strip_prev) {
+              if (strip_prev >= 0) bring.next();
+              strip_prev = strip_id(c);
+              mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
+              uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
+              const uint32_t bar = smem_u32(&bar_bfull[bring.i]);
+              mbar_expect_tx(bar, nt * tb);
+              for (int j = 0; j < nt; ++j)
+                bulk_load(smem_u32(dst + j * tb),
+                          g.Bp[c.kd] + (((size_t)c.layer * g.n_experts + cf.e[j]) * g.dout_pad[c.kd] +
+                                        (size_t)c.rb * kTM) * rpe,
+                          tb, bar, pol_keep);
+            }
+            const __nv_bfloat16* blk =
+                g.At[c.kd] + (((size_t)c.layer * tk.col_tiles[c.kd] + c.cb) * g.n_experts) * (size_t)kTN * rpe;
+            for (int j0 = 0; j0 < nt; j0 += kPtGroup) {
+              const int n_in = nt - j0 < kPtGroup ? nt - j0 : kPtGroup;
+              mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
+              uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
+              const uint32_t bar = smem_u32(&bar_afull[aring.i]);
+              mbar_expect_tx(bar, n_in * tb);
+              for (int jj = 0; jj < n_in; ++jj)
+                bulk_load(smem_u32(adst + jj * tb), blk + (size_t)cf.e[j0 + jj] * kTN * rpe, tb, bar, pol_keep);
+              aring.next();
+            }
+          }
+        }
+      } else {
       // ============================ operand producer ========================
       // Per strip (rare): raw B slices of all terms by bulk copies into the lo
       // slots, then the whole warp folds them into (hi, lo) parts in place and
@@ -447,6 +517,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         __syncwarp();
         aring.next();
       }
+      }  // !kPT
     } else if (warp == 1 && !(args.probe & 1)) {
       // ============================ MMA issuer ==============================
       // One chain per tile: for every term, the hi and lo parts times the A^T
@@ -461,7 +532,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       const uint64_t term = g.term_bytes >> 4;
       Ring bring{0, 0, (uint32_t)g.b_bufs};
       Ring aring{0, 0, (uint32_t)g.a_stages};
-      Ring acc{0, 0, (uint32_t)kAccBufs};
+      Ring acc{0, 0, (uint32_t)g.acc_bufs};
       int64_t strip_prev = -1;
       for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
         if (strip_id(c) != strip_prev) {
@@ -476,6 +547,30 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           }
           strip_prev = strip_id(c);
           mbar_wait(smem_u32(&bar_bfull[bring.i]), bring.phase);
+        }
+        if constexpr (kPT) {
+          // per-term mode: kPtGroup terms per group, each into its own 128-column
+          // accumulator of the group's TMEM buffer, one commit per group
+          const uint64_t b_desc = desc0 + (smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes) >> 4);
+          for (int j0 = 0; j0 < nt; j0 += kPtGroup) {
+            const int n_in = nt - j0 < kPtGroup ? nt - j0 : kPtGroup;
+            mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
+            mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
+            tc_fence_after();
+            const uint64_t a_desc = desc0 + (smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes) >> 4);
+            const uint32_t d = tmem_base + acc.i * g.acc_cols;
+            if (elect_one()) {
+              for (int jj = 0; jj < n_in; ++jj)
+                for (int kk = 0; kk < ksteps; ++kk)
+                  umma_f16(d + jj * kTN, b_desc + (j0 + jj) * term + kk * 2, a_desc + jj * term + kk * 2, idesc,
+                           kk > 0 ? 1u : 0u);
+              umma_commit(smem_u32(&bar_accfull[acc.i]));
+            }
+            __syncwarp();
+            acc.next();
+            aring.next();
+          }
+          continue;
         }
         mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
         mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
@@ -504,7 +599,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       const int row = quarter * 32 + lane;
       const bool releaser = ew == 0 && lane == 0;   // frees A stages for the producer
       Ring wring{0, 0, (uint32_t)g.w_stages};
-      Ring acc{0, 0, (uint32_t)kAccBufs};
+      Ring acc{0, 0, (uint32_t)g.acc_bufs};
       Ring aring{0, 0, (uint32_t)g.a_stages};
       int cur_seg = -1;                            // fused: segment of the previous tile
       unsigned long long seg_mine = 0;             // fused: tiles of cur_seg this CTA finished
@@ -538,6 +633,54 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         if (args.probe & 1) {                      // tuning: the W stream alone
           mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
+          wring.next();
+          continue;
+        }
+        if constexpr (kPT) {
+          // per-term mode: v = W, then v <- c_j * acc_j + v for j ascending
+          // (fp32, FFMA2; the order does not depend on the grouping), term
+          // group by term group as their accumulators complete; ONE RNE
+          mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);
+          const int unit = g.wrm ? 2 * row + half : half * kTM + row;
+          const int key = unit & 7, flip = g.wrm ? (row >> 2) & 1 : 0;
+          uint8_t* wrow = wst0 + (size_t)wring.i * (2 * kSubBytes) + unit * 128;
+          uint64_t v[4][8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w_load16(wrow, key, flip, q, v[q]);
+          for (int j0 = 0; j0 < nt; j0 += kPtGroup) {
+            const int n_in = nt - j0 < kPtGroup ? nt - j0 : kPtGroup;
+            mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);
+            if (releaser) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
+            aring.next();
+            tc_fence_after();
+            const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * g.acc_cols + half * kSubCols;
+            const uint64_t c0 = f2_pack(cf.c[j0], cf.c[j0]);
+            const uint64_t c1 = n_in > 1 ? f2_pack(cf.c[j0 + 1], cf.c[j0 + 1]) : 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t a0[16], a1[16];
+              tmem_ld16(tm + q * 16, a0);
+              if (n_in > 1) tmem_ld16(tm + kTN + q * 16, a1);
+              tmem_wait_ld();
+#pragma unroll
+              for (int p = 0; p < 8; ++p)
+                v[q][p] = ffma2(f2_pack(__uint_as_float(a0[2 * p]), __uint_as_float(a0[2 * p + 1])), c0, v[q][p]);
+              if (n_in > 1) {
+#pragma unroll
+                for (int p = 0; p < 8; ++p)
+                  v[q][p] = ffma2(f2_pack(__uint_as_float(a1[2 * p]), __uint_as_float(a1[2 * p + 1])), c1, v[q][p]);
+              }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+            acc.next();
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) w_store16(wrow, key, flip, q, v[q]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> TMA store
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
           wring.next();
@@ -660,7 +803,7 @@ int fc_mmas_per_tile(const SwitchParams& sp) {
   return 2 * (2 * sp.top_k) * rp / 16;
 }
 
-cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, const char** why) {
+cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, const char** why, int pt) {
   *out = nullptr;
   int dev = 0, major = 0, minor = 0;
   cudaGetDevice(&dev);
@@ -678,8 +821,21 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   g.swz_mode = rp == 16 ? 6u : rp == 32 ? 4u : 2u;        // SWIZZLE_32B / 64B / 128B (UMMA encoding)
   g.term_bytes = kTM * rp * 2;
   const int mt = 2 * sp.top_k;
-  g.a_stage_bytes = align1k((uint32_t)mt * g.term_bytes);
-  g.b_buf_bytes = align1k((uint32_t)(2 * mt) * g.term_bytes);
+  // per-term mode (LSW_FC_PT=1, or chosen by the dispatcher): B raw, A units of
+  // kPtGroup terms, TMEM buffers of kPtGroup x 128 columns
+  g.pt = pt;
+  if (const char* v = getenv("LSW_FC_PT")) g.pt = atoi(v) != 0;
+  if (g.pt) {
+    g.acc_cols = kPtGroup * kTN;
+    g.acc_bufs = 512 / (int)g.acc_cols;
+    g.a_stage_bytes = align1k((uint32_t)kPtGroup * g.term_bytes);
+    g.b_buf_bytes = align1k((uint32_t)mt * g.term_bytes);
+  } else {
+    g.acc_cols = kTN;
+    g.acc_bufs = kAccBufs;
+    g.a_stage_bytes = align1k((uint32_t)mt * g.term_bytes);
+    g.b_buf_bytes = align1k((uint32_t)(2 * mt) * g.term_bytes);
+  }
   const uint32_t w_stage = 2 * kSubBytes;
   // Shared-memory plan, in order of preference (measured, 7B shape: W 3 + B 2 +
   // A 3 0.895 of the copy peak vs W 4 + B 1 + A 3 0.868 -- a single B buffer
@@ -767,9 +923,14 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(switch_fc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+    e = cudaFuncSetAttribute(switch_fc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)g.smem_bytes);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(switch_fc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
+    e = cudaFuncSetAttribute(switch_fc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)g.smem_bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(switch_fc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)g.smem_bytes);
   if (e != cudaSuccess) {
     if (!*why || !**why) *why = cudaGetErrorString(e);
     tc_plan_destroy(plan);
@@ -830,7 +991,10 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   a.xs = nullptr;
   a.ys = nullptr;
   a.seg_done = nullptr;
-  switch_fc_kernel<false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  if (plan->geom.pt)
+    switch_fc_kernel<false, true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  else
+    switch_fc_kernel<false, false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   return cudaGetLastError();
 }
 
@@ -839,6 +1003,7 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
 cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
                               int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]) {
   const Geom& g = plan->geom;
+  if (g.pt) return cudaErrorNotSupported;                     // the fused epilogue is the folded one
   for (int k = 0; k < LSW_NKIND; ++k) if (g.d_in[k] % 8) return cudaErrorNotSupported;   // 16-B x loads
   const int n = 4 * n_layers;
   FusedSeg* h = new FusedSeg[n];
@@ -896,7 +1061,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   a.xs = static_cast<const __nv_bfloat16*>(xs);
   a.ys = ys;
   a.seg_done = plan->d_seg_done;
-  switch_fc_kernel<true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  switch_fc_kernel<true, false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   return cudaGetLastError();
 }
 

@@ -65,7 +65,8 @@ namespace fc {
 struct TcPlan;
 // tcgen05.mma instructions (128 x 128 x 16) per tile at 2k terms
 int fc_mmas_per_tile(const SwitchParams& geom);
-cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why);
+// pt: per-term mode (no fold, one fp32 TMEM accumulator per term; for large k*r)
+cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why, int pt);
 void tc_plan_destroy(TcPlan* plan);
 int64_t tc_plan_bytes(const TcPlan* plan);
 int tc_plan_grid(const TcPlan* plan);

@@ -44,14 +44,18 @@ gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6452.8
 for setting in [x for _ in range(a.repeat) for x in a.settings]:
     for k in ("LSW_TC_ORDER", "LSW_TC_CHUNK", "LSW_TC_STAGES", "LSW_TC_PROBE", "LSW_TC_NSUB", "LSW_TC_AALL", "LSW_TC_STORE", "LSW_TC_ASTAGES", "LSW_TC_SPLIT", "LSW_TC_TG", "LSW_TC_BACKOFF", "LSW_TC_ACOPY", "LSW_TC_ADEPTH", "LSW_TC_ALOADER", "LSW_TC_KERNEL", "LSW_TC_W4D", "LSW_TC_MMA2", "LSW_TC_L2PROMO", "LSW_TC_WPOLICY",
-              "LSW_TC_GRID", "LSW_FC_BBUFS", "LSW_FC_ASTAGES", "LSW_FC_STAGES", "LSW_FC_WRM"):
+              "LSW_TC_GRID", "LSW_FC_BBUFS", "LSW_FC_ASTAGES", "LSW_FC_STAGES", "LSW_FC_WRM", "LSW_FC_PT"):
         os.environ.pop(k, None)
     for kv in setting.split(","):
         if not kv:
             continue
         k, v = kv.split("=")
         os.environ[("LSW_" if k.startswith("fc_") else "LSW_TC_") + k.upper()] = v
-    sw = H.make_switch(cfg, W, A, B, router, impl=a.impl)
+    try:
+        sw = H.make_switch(cfg, W, A, B, router, impl=a.impl)
+    except Exception as e:  # noqa: BLE001  (no plan for this shape under these knobs)
+        print(json.dumps({"setting": setting, "error": str(e)[:120]}), flush=True)
+        continue
     probe = os.environ.get("LSW_TC_PROBE", "0") == "1"
     sw.router_topk(X1[0], idx, gate)
     sw.merge_all_layers(idx, gate)

@@ -109,7 +109,8 @@ def test_switch_trajectory_full_elements(name, impl):
 
 TC_VARIANTS = [("v1", {}), ("v1", {"LSW_TC_SPLIT": "1"}), ("tg", {}), ("tg", {"LSW_TC_TG": "1"}),
                ("tg", {"LSW_TC_TG": "2"}), ("tg", {"LSW_TC_MMA2": "0"}), ("tg", {"LSW_TC_MMA2": "1", "LSW_TC_TG": "1"}),
-               ("fc", {}), ("fc", {"LSW_FC_BBUFS": "1", "LSW_FC_ASTAGES": "2"}), ("fc", {"LSW_FC_WRM": "0"})]
+               ("fc", {}), ("fc", {"LSW_FC_BBUFS": "1", "LSW_FC_ASTAGES": "2"}), ("fc", {"LSW_FC_WRM": "0"}),
+               ("fc", {"LSW_FC_PT": "1"}), ("fc", {"LSW_FC_PT": "1", "LSW_FC_WRM": "0"})]
 KERNEL_ID = {"v1": 1, "tg": 2, "fc": 3}
 
 
