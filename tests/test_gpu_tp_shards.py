@@ -26,10 +26,13 @@ if torch.cuda.is_available():
     from paper_2405_17741_b200 import harness as H
 
 
-@pytest.mark.parametrize("name,impl", [("mini", "tc"), ("mini", "simt"), ("mini-r32", "tc")])
-def test_tp2_shards_match_full_model(name, impl):
+@pytest.mark.parametrize("name,impl,size", [("mini", "tc", 2), ("mini", "simt", 2), ("mini-r32", "tc", 2),
+                                            ("mini", "tc", 4), ("mini-r32", "tc", 8), ("mini-r64k3", "tc", 4)])
+def test_tp_shards_match_full_model(name, impl, size):
+    """size 4 / 8: ragged shards (d_ff 704 -> 176 / 88 columns of down, d_model
+    256 -> 32 columns of o: 3-D W boxes instead of the row-major 4-D view,
+    partial tiles) through the same kernels; r = 64, k = 3: the per-term mode."""
     cfg = synth.get_config(name)
-    size = 2
     full = H.build_weights(cfg, "cuda")
     sw_full = H.make_switch(cfg, *full, impl=impl)
     shards = [H.build_weights(cfg, "cuda", r, size) for r in range(size)]
@@ -65,7 +68,7 @@ def test_tp2_shards_match_full_model(name, impl):
                     parts.append(y)
                 torch.cuda.synchronize()
                 if kd in synth.ROW_PARALLEL:
-                    torch.testing.assert_close(parts[0] + parts[1], y_full, rtol=1e-5, atol=1e-5)
+                    torch.testing.assert_close(sum(parts[1:], parts[0]), y_full, rtol=1e-5, atol=1e-5)
                 else:
                     assert torch.equal(torch.cat(parts), y_full)
     for s in sws + [sw_full]:
