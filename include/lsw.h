@@ -293,20 +293,23 @@ LSW_API lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs
  * (layer, group); a segment's outputs are accumulated only after every tile of
  * the previous segment is done (y final), as a decoder needs.  The fused
  * launch is a build of the per-term (v1) tensor-core kernel: W ends exactly as
- * after lsw_merge_all_layers with that kernel (bitwise; a ctx that switches
- * with another kernel builds a v1 plan on the first call, and its W then stays
- * within the parity tolerance of the oracle's trajectory); ys equals
- * lsw_decode_all_layers on those weights up to fp32 summation order (atomic
- * accumulation, not bitwise reproducible).  Layouts as lsw_decode_token.
- * LSW_E_UNSUPPORTED unless v1 has a plan for the shape (2k <= 4 terms) and
- * tp_size == 1.
+ * after lsw_merge_all_layers with that kernel (bitwise: the fc kernel's own
+ * fused build for a ctx that switches with fc in its fold mode; else a v1
+ * plan, built on the first call, whose W stays within the parity tolerance of
+ * the oracle's trajectory); ys equals lsw_decode_all_layers on those weights up
+ * to fp32 summation order (atomic accumulation, not bitwise reproducible).
+ * Layouts as lsw_decode_token.  LSW_E_UNSUPPORTED unless one of the two has a
+ * plan for the shape and tp_size == 1.
  */
 LSW_API lsw_status lsw_decode_token_fused(lsw_ctx* ctx, const void* x1, const void* xs, float* ys, int32_t* idx,
                                           float* gate, void* stream);
 
 /* Same as lsw_decode_token from HOST buffers: copies x1_h, xs_h to ctx-owned
  * device staging, runs the token, copies ys/idx/gate back and synchronizes
- * `stream`.  Host buffers should be pinned for asynchronous copies. */
+ * `stream` (and a ctx-owned side stream).  The copies overlap the token: xs
+ * travels on the side stream while the router and the switch run, and each
+ * layer's outputs return as soon as that layer's GEMVs are done.  Host buffers
+ * should be pinned for asynchronous copies. */
 LSW_API lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_h, float* ys_h,
                                  int32_t* idx_h, float* gate_h, void* stream);
 

@@ -69,6 +69,8 @@ struct lsw_ctx {
   float* st_ys = nullptr;
   int32_t* st_idx = nullptr;
   float* st_gate = nullptr;
+  cudaStream_t st_side = nullptr;       // lsw_decode_token_host: copies overlapped with the token
+  std::vector<cudaEvent_t> st_ev;       // [0]: xs landed; [1 + l]: layer l's outputs final
 };
 
 static size_t esize(const lsw_ctx* c) { return c->cfg.dtype == LSW_BF16 ? 2 : 4; }
@@ -227,6 +229,8 @@ lsw_status lsw_destroy(lsw_ctx* ctx) {
   cudaFree(ctx->st_ys);
   cudaFree(ctx->st_idx);
   cudaFree(ctx->st_gate);
+  for (cudaEvent_t ev : ctx->st_ev) cudaEventDestroy(ev);
+  if (ctx->st_side) cudaStreamDestroy(ctx->st_side);
   delete ctx;
   return LSW_OK;
 }
@@ -559,15 +563,62 @@ lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_
         cudaMalloc(&ctx->st_gate, LSW_MAX_TOPK * sizeof(float)) != cudaSuccess)
       return fail(LSW_E_OOM, "lsw_decode_token_host: staging allocation failed");
   }
+  // Copies overlap the token (per-group GEMV path): x1 goes first on the
+  // token's stream (the router needs it); the GEMV inputs on a side stream
+  // while the router and the switch run; each layer's outputs go back on the
+  // side stream as soon as that layer's GEMVs are done.
+  const bool overlap = !ctx->tok.d_groups;
+  if (overlap && !ctx->st_side) {
+    if (cudaStreamCreateWithFlags(&ctx->st_side, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(LSW_E_CUDA, "lsw_decode_token_host: side stream");
+    ctx->st_ev.resize(1 + ctx->cfg.n_layers);
+    for (auto& ev : ctx->st_ev)
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+        return fail(LSW_E_CUDA, "lsw_decode_token_host: events");
+  }
   cudaError_t e = cudaMemcpyAsync(ctx->st_x1, x1_h, ctx->cfg.d_model * es, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->st_xs, xs_h, ctx->xs_elems * es, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: H2D");
-  lsw_status st = lsw_decode_token(ctx, ctx->st_x1, ctx->st_xs, ctx->st_ys, ctx->st_idx, ctx->st_gate, stream);
-  if (st != LSW_OK) return st;
-  e = cudaMemcpyAsync(ys_h, ctx->st_ys, ctx->ys_elems * sizeof(float), cudaMemcpyDeviceToHost, s);
+  if (!overlap) {
+    e = cudaMemcpyAsync(ctx->st_xs, xs_h, ctx->xs_elems * es, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: H2D");
+    lsw_status st = lsw_decode_token(ctx, ctx->st_x1, ctx->st_xs, ctx->st_ys, ctx->st_idx, ctx->st_gate, stream);
+    if (st != LSW_OK) return st;
+    e = cudaMemcpyAsync(ys_h, ctx->st_ys, ctx->ys_elems * sizeof(float), cudaMemcpyDeviceToHost, s);
+  } else {
+    cudaStream_t side = ctx->st_side;
+    // the side stream starts after everything already on `s` (the previous
+    // token's readers of st_xs / st_ys are done)
+    e = cudaEventRecord(ctx->st_ev[0], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->st_ev[0], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->st_xs, xs_h, ctx->xs_elems * es, cudaMemcpyHostToDevice, side);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->st_ev[0], side);
+    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: H2D");
+    lsw_status st = lsw_router_topk(ctx, ctx->st_x1, ctx->st_idx, ctx->st_gate, stream);          // Alg. 1 l.1
+    if (st != LSW_OK) return st;
+    st = lsw_merge_all_layers(ctx, ctx->st_idx, ctx->st_gate, stream);                          // l.2-4
+    if (st != LSW_OK) return st;
+    e = cudaStreamWaitEvent(s, ctx->st_ev[0], 0);                                                 // xs landed
+    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: wait");
+    for (int l = 0; l < ctx->cfg.n_layers; ++l) {                                                // l.5
+      for (int g = 0; g < LSW_NGROUP; ++g) {
+        const uint8_t* xp = (const uint8_t*)ctx->st_xs + (size_t)(l * ctx->x_per_layer + ctx->x_off[g]) * es;
+        float* yp = ctx->st_ys + l * ctx->y_per_layer + ctx->y_off[g];
+        st = gemv_sites(ctx, l, kGroupKinds[g], kGroupSize[g], xp, yp, s, "lsw_decode_token_host",
+                        /*early_w=*/l > 0 || g > 0);
+        if (st != LSW_OK) return st;
+      }
+      e = cudaEventRecord(ctx->st_ev[1 + l], s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->st_ev[1 + l], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ys_h + l * ctx->y_per_layer, ctx->st_ys + l * ctx->y_per_layer,
+                            ctx->y_per_layer * sizeof(float), cudaMemcpyDeviceToHost, side);
+      if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: D2H");
+    }
+  }
   if (e == cudaSuccess) e = cudaMemcpyAsync(idx_h, ctx->st_idx, ctx->cfg.top_k * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(gate_h, ctx->st_gate, ctx->cfg.top_k * sizeof(float), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && overlap) e = cudaStreamSynchronize(ctx->st_side);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: D2H");
   return LSW_OK;
 }
