@@ -292,8 +292,8 @@ LSW_API lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs
  * B/element instead of 6).  Tiles are walked in decoder order, one segment per
  * (layer, group); a segment's outputs are accumulated only after every tile of
  * the previous segment is done (y final), as a decoder needs.  The fused
- * launch is a build of the per-term (v1) tensor-core kernel: W ends exactly as
- * after lsw_merge_all_layers with that kernel (bitwise: the fc kernel's own
+ * launch is a build of the switch kernel: W ends exactly as after
+ * lsw_merge_all_layers with that kernel (bitwise: the fc kernel's own
  * fused build for a ctx that switches with fc in its fold mode; else a v1
  * plan, built on the first call, whose W stays within the parity tolerance of
  * the oracle's trajectory); ys equals lsw_decode_all_layers on those weights up
