@@ -842,8 +842,16 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   // drains the MMA pipeline at every strip change, a 4th W stage buys nothing);
   // what is left goes to more W stages.
   const int64_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
-  struct Try { int ws, bb, as; };
-  const Try tries[] = {{4, 2, 3}, {3, 2, 3}, {4, 2, 2}, {3, 2, 2}, {4, 1, 3}, {4, 1, 2}, {3, 1, 2}, {2, 1, 2}};
+  // A ring depth in units per tile u (fold: the whole tile's slices; per-term:
+  // one unit per kPtGroup terms).  Candidates (W stages, B buffers) in order of
+  // preference; for each the A stages that fit.  Pass 0 wants 2u + 1 A units
+  // (a tile of lookahead), pass 1 u + 1, pass 2 any >= 2; W stays >= 3 before
+  // the last resort (measured, 16-layer 7B shape: W 2 costs 7-15 %; W 3 + B 1
+  // + A 3 0.860 vs W 4 + B 1 + A 2 0.846 at k = 3; per-term r = 32 k = 3:
+  // W 3 + B 1 + A 5 0.656 vs W 3 + B 2 + A 2 0.626).
+  struct Cand { int ws, bb; };
+  const Cand cands[] = {{4, 2}, {3, 2}, {3, 1}, {4, 1}};
+  const int u = g.pt ? (mt + kPtGroup - 1) / kPtGroup : 1;
   int bb_env = 0, as_env = 0, ws_env = 0;
   if (const char* v = getenv("LSW_FC_BBUFS")) bb_env = atoi(v);
   if (const char* v = getenv("LSW_FC_ASTAGES")) as_env = atoi(v);
@@ -856,19 +864,32 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     g.b_bufs = bb_env;
     ok = true;
   }
-  for (const Try& t : tries) {
-    if (ok) break;
-    const int bb = bb_env >= 1 && bb_env <= 2 ? bb_env : t.bb;
-    const int as = as_env >= 2 && as_env <= kMaxAStages ? as_env : t.as;
-    const int64_t rest = budget - (int64_t)bb * g.b_buf_bytes - (int64_t)as * g.a_stage_bytes;
-    if (rest < (int64_t)t.ws * w_stage) continue;
-    int ws = (int)(rest / w_stage);
-    if (ws > kMaxStages) ws = kMaxStages;
-    if (ws_env >= 2 && ws_env < ws) ws = ws_env;
-    g.w_stages = ws;
-    g.a_stages = as;
-    g.b_bufs = bb;
-    ok = true;
+  for (int pass = 0; pass < 3 && !ok; ++pass) {
+    const int a_min = pass == 0 ? 2 * u + 1 : pass == 1 ? u + 1 : 2;
+    for (const Cand& c : cands) {
+      const int64_t rest = budget - (int64_t)c.ws * w_stage - (int64_t)c.bb * g.b_buf_bytes;
+      if (rest < 0) continue;
+      int as = (int)(rest / g.a_stage_bytes);
+      if (as > kMaxAStages) as = kMaxAStages;
+      if (as < a_min) continue;
+      g.w_stages = c.ws;
+      g.a_stages = as;
+      g.b_bufs = c.bb;
+      ok = true;
+      break;
+    }
+  }
+  if (!ok) {                                 // last resort: two W stages
+    for (int bb = 2; bb >= 1 && !ok; --bb) {
+      const int64_t rest = budget - 2 * (int64_t)w_stage - (int64_t)bb * g.b_buf_bytes;
+      int as = rest > 0 ? (int)(rest / g.a_stage_bytes) : 0;
+      if (as > kMaxAStages) as = kMaxAStages;
+      if (as < 2) continue;
+      g.w_stages = 2;
+      g.a_stages = as;
+      g.b_bufs = bb;
+      ok = true;
+    }
   }
   if (!ok) { delete plan; *why = "shared memory: rank * top_k too large for the folded kernel"; return cudaErrorNotSupported; }
   if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
