@@ -209,20 +209,26 @@ __device__ __forceinline__ void wait_count(const unsigned long long* p, unsigned
 
 // ------------------------------------------------------------------ fold
 
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 // Eight bf16 B elements -> (hi, lo) parts of c * b: x = fl32(c * b),
 // hi = RNE_bf16(x), lo = RNE_bf16(x - hi) (x - hi is exact in fp32), so
 // hi + lo = x to within 2^-16 |x| (R13: the coefficient is not rounded to bf16).
 __device__ __forceinline__ void fold8(const uint4 raw, float c, uint4& hi, uint4& lo) {
   const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
   uint32_t h[4], l[4];
+  const uint64_t c2 = f2_pack(c, c), m1 = f2_pack(-1.f, -1.f), z2 = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const float x0 = c * __uint_as_float(w[q] << 16), x1 = c * __uint_as_float(w[q] & 0xffff0000u);
-    const __nv_bfloat162 hb = __floats2bfloat162_rn(x0, x1);
-    const float2 hf = __bfloat1622float2(hb);
-    const __nv_bfloat162 lb = __floats2bfloat162_rn(x0 - hf.x, x1 - hf.y);
-    h[q] = *reinterpret_cast<const uint32_t*>(&hb);
-    l[q] = *reinterpret_cast<const uint32_t*>(&lb);
+    // x = c * b (packed, exact product rounded once), hi = RNE(x), lo = RNE(x - hi)
+    const uint64_t x = ffma2(f2_pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u)), c2, z2);
+    h[q] = f2_to_bf16x2(x);
+    const uint64_t hf = f2_pack(__uint_as_float(h[q] << 16), __uint_as_float(h[q] & 0xffff0000u));
+    l[q] = f2_to_bf16x2(ffma2(hf, m1, x));
   }
   hi = make_uint4(h[0], h[1], h[2], h[3]);
   lo = make_uint4(l[0], l[1], l[2], l[3]);
@@ -274,11 +280,6 @@ __device__ __forceinline__ void w_store16(uint8_t* wrow, int key, int flip, int 
   *reinterpret_cast<uint4*>(wrow + (((col16 * 2 + (flip ^ 1)) ^ key) << 4)) = flip ? o0 : o1;
 }
 
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
 
 // As epi16, and y += RNE(W + D) . x over the 16 columns (fp32 FMA in column
 // order; x: 16 bf16 of this thread's columns).
@@ -492,14 +493,19 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             }
           }
           mbar_wait(rbar, bring.phase);
-          for (uint32_t v = lane; v < (uint32_t)nt * vec_per_term; v += 32) {
-            const uint32_t j = v / vec_per_term, o = (v - j * vec_per_term) * 16;
-            uint4* plo = reinterpret_cast<uint4*>(dst + (2 * j + 1) * tb + o);
-            uint4 hi, lo;
-            fold8(*plo, cf.c[j], hi, lo);
-            *reinterpret_cast<uint4*>(dst + 2 * j * tb + o) = hi;
-            *plo = lo;
-          }
+          if (!(args.probe & 16))                    // probe 16 (tuning only): skip the fold math
+            for (int j = 0; j < nt; ++j) {
+              const float cj = cf.c[j];
+              uint4* phi = reinterpret_cast<uint4*>(dst + 2 * j * tb);
+              uint4* plo = reinterpret_cast<uint4*>(dst + (2 * j + 1) * tb);
+#pragma unroll 4
+              for (uint32_t v = lane; v < vec_per_term; v += 32) {
+                uint4 hi, lo;
+                fold8(plo[v], cj, hi, lo);
+                phi[v] = hi;
+                plo[v] = lo;
+              }
+            }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&bar_bfull[bring.i]));
@@ -893,7 +899,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   }
   if (!ok) { delete plan; *why = "shared memory: rank * top_k too large for the folded kernel"; return cudaErrorNotSupported; }
   if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
-  if (const char* v = getenv("LSW_TC_PROBE")) plan->probe = atoi(v) == 1;
+  if (const char* v = getenv("LSW_TC_PROBE")) plan->probe = atoi(v) & 17;   // 1: W stream only, 16: no fold math
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
   // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
   g.wrm = 1;
