@@ -234,6 +234,24 @@ __device__ __forceinline__ void fold8(const uint4 raw, float c, uint4& hi, uint4
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
+// Fold the strip buffer at dst in place (raw B in the lo slots -> hi, lo), the
+// 16-B vectors [v0, v1) of every term, by the 32 lanes of one warp.
+__device__ __forceinline__ void fold_range(uint8_t* dst, uint32_t tb, int nt, const float* c, uint32_t v0,
+                                           uint32_t v1, int lane) {
+  for (int j = 0; j < nt; ++j) {
+    const float cj = c[j];
+    uint4* phi = reinterpret_cast<uint4*>(dst + 2 * j * tb);
+    uint4* plo = reinterpret_cast<uint4*>(dst + (2 * j + 1) * tb);
+#pragma unroll 4
+    for (uint32_t v = v0 + lane; v < v1; v += 32) {
+      uint4 hi, lo;
+      fold8(plo[v], cj, hi, lo);
+      phi[v] = hi;
+      plo[v] = lo;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ epilogue
 
 // W (bf16, one 128-B swizzle unit: 64 columns of a row) + 16 accumulator
@@ -352,7 +370,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&bar_braw[s]), 1);
-      mbar_init(smem_u32(&bar_bfull[s]), 1);
+      mbar_init(smem_u32(&bar_bfull[s]), g.b_bufs == 1 && !g.pt ? 2 : 1);   // fold: + the MMA warp's half
       mbar_init(smem_u32(&bar_bempty[s]), 1);
     }
     for (int s = 0; s < g.acc_bufs; ++s) {
@@ -493,19 +511,10 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             }
           }
           mbar_wait(rbar, bring.phase);
+          // with a single B buffer the fold is on the MMA's critical path: the
+          // MMA warp, idle until it lands, folds the second half of every term
           if (!(args.probe & 16))                    // probe 16 (tuning only): skip the fold math
-            for (int j = 0; j < nt; ++j) {
-              const float cj = cf.c[j];
-              uint4* phi = reinterpret_cast<uint4*>(dst + 2 * j * tb);
-              uint4* plo = reinterpret_cast<uint4*>(dst + (2 * j + 1) * tb);
-#pragma unroll 4
-              for (uint32_t v = lane; v < vec_per_term; v += 32) {
-                uint4 hi, lo;
-                fold8(plo[v], cj, hi, lo);
-                phi[v] = hi;
-                plo[v] = lo;
-              }
-            }
+            fold_range(dst, tb, nt, cf.c, 0, g.b_bufs == 1 ? vec_per_term / 2 : vec_per_term, lane);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&bar_bfull[bring.i]));
@@ -552,6 +561,17 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             bring.next();
           }
           strip_prev = strip_id(c);
+          if (!kPT && g.b_bufs == 1) {
+            // single B buffer: fold the second half of every term here (the
+            // operand warp folds the first half), then publish it
+            uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
+            mbar_wait(smem_u32(&bar_braw[bring.i]), bring.phase);
+            if (!(args.probe & 16))
+              fold_range(dst, g.term_bytes, nt, cf.c, g.term_bytes / 32, g.term_bytes / 16, lane);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor core
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&bar_bfull[bring.i]));
+          }
           mbar_wait(smem_u32(&bar_bfull[bring.i]), bring.phase);
         }
         if constexpr (kPT) {
