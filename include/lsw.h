@@ -297,7 +297,8 @@ LSW_API lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs
  * fused build for a ctx that switches with fc in its fold mode; else a v1
  * plan, built on the first call, whose W stays within the parity tolerance of
  * the oracle's trajectory); ys equals lsw_decode_all_layers on those weights up
- * to fp32 summation order (atomic accumulation, not bitwise reproducible).
+ * to fp32 summation order (fc: accumulated in 64-bit fixed point, bitwise
+ * reproducible; v1: fp32 atomics, not bitwise reproducible).
  * Layouts as lsw_decode_token.  LSW_E_UNSUPPORTED unless one of the two has a
  * plan for the shape and tp_size == 1.
  */

@@ -87,6 +87,7 @@ struct FusedSeg {
   int32_t pad;
   int64_t x_off;                    // elements into xs of this segment's input
   int64_t y_off[3];                 // elements into ys of each kind's row 0
+  int64_t y_rows;                   // rows of the segment's outputs (ys[y_off[0] ..+ y_rows])
 };
 
 struct TcPlan {
@@ -94,6 +95,8 @@ struct TcPlan {
   Geom geom;
   FusedSeg* d_segs = nullptr;       // fused mode (tc_plan_set_fused)
   unsigned long long* d_seg_done = nullptr;
+  unsigned long long* d_ys_fx = nullptr;   // fixed-point output accumulators (2^-40), [ys_rows]
+  int64_t ys_rows = 0;
   int32_t n_segs = 0;
   int64_t fused_tiles = 0;
   int32_t chunk = 48;
@@ -118,8 +121,25 @@ struct Args {
   int32_t n_seg;
   const __nv_bfloat16* xs;
   float* ys;
+  unsigned long long* ys_fx;      // fixed-point accumulators of ys, zeroed before the launch
   unsigned long long* seg_done;   // [n_seg], zeroed before the launch
 };
+
+// Fused outputs are accumulated in 64-bit fixed point (2^-40 units): integer
+// adds are associative, so y is bitwise reproducible whatever the order of the
+// per-tile contributions (fp32 atomics are not); converted to fp32 once a
+// segment is complete.  |y| < 2^23 (R24: non-finite inputs are undefined).
+constexpr double kFx = 1099511627776.0;          // 2^40
+constexpr double kFxInv = 1.0 / 1099511627776.0;
+
+// Convert this CTA's slice of segment q's outputs (all epilogue threads).
+__device__ __forceinline__ void fx_convert(const Args& a, int q, int t, int nthr) {
+  const FusedSeg& S = a.segs[q];
+  const int64_t r0 = S.y_off[0] + S.y_rows * blockIdx.x / gridDim.x;
+  const int64_t r1 = S.y_off[0] + S.y_rows * (blockIdx.x + 1) / gridDim.x;
+  for (int64_t r = r0 + t; r < r1; r += nthr)
+    a.ys[r] = (float)((double)(long long)__ldcg(a.ys_fx + r) * kFxInv);
+}
 
 // ------------------------------------------------------------------ tile walk
 
@@ -628,6 +648,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       Ring acc{0, 0, (uint32_t)g.acc_bufs};
       Ring aring{0, 0, (uint32_t)g.a_stages};
       int cur_seg = -1;                            // fused: segment of the previous tile
+      int conv_next = 0;                           // fused: first segment whose outputs this CTA has not converted
       unsigned long long seg_mine = 0;             // fused: tiles of cur_seg this CTA finished
       for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
         uint4 xv[8];                               // fused: x of this thread's 64 columns
@@ -637,14 +658,18 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             // segment s-1 is done -- one thread per CTA publishes the CTA's
             // count of the segment it leaves and waits for the previous total
             asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
-            if (releaser) {
-              if (cur_seg >= 0) {
-                __threadfence();
-                asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(args.seg_done + cur_seg),
-                             "l"(seg_mine) : "memory");
-              }
-              if (c.seg > 0 && !(args.probe & 4))
-                wait_count(&args.seg_done[c.seg - 1], (unsigned long long)args.segs[c.seg - 1].tile_count);
+            if (releaser && cur_seg >= 0) {
+              __threadfence();
+              asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(args.seg_done + cur_seg),
+                           "l"(seg_mine) : "memory");
+            }
+            // every earlier segment complete (decoder order), then this CTA's
+            // slice of its outputs converted from fixed point
+            for (; conv_next < c.seg; ++conv_next) {
+              if (releaser && !(args.probe & 4))
+                wait_count(&args.seg_done[conv_next], (unsigned long long)args.segs[conv_next].tile_count);
+              asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
+              fx_convert(args, conv_next, threadIdx.x - 32 * kFirstEpiWarp, 32 * kEpiWarps);
             }
             asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
             cur_seg = c.seg;
@@ -735,7 +760,9 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           for (int q = 0; q < 4; ++q)
             y = epi16_dot(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q], xv[2 * q], xv[2 * q + 1], y);
           const int64_t grow = (int64_t)c.rb * kTM + row;
-          if (grow < g.d_out[c.kd]) atomicAdd(args.ys + args.segs[c.seg].y_off[c.kidx] + grow, y);
+          if (grow < g.d_out[c.kd])
+            atomicAdd(args.ys_fx + args.segs[c.seg].y_off[c.kidx] + grow,
+                      (unsigned long long)__double2ll_rn((double)y * kFx));
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q) epi16(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q]);
@@ -754,6 +781,12 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(args.seg_done + cur_seg),
                          "l"(seg_mine) : "memory");
           }
+        }
+        for (; conv_next < args.n_seg; ++conv_next) {   // the remaining segments' outputs
+          if (releaser && !(args.probe & 4))
+            wait_count(&args.seg_done[conv_next], (unsigned long long)args.segs[conv_next].tile_count);
+          asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
+          fx_convert(args, conv_next, threadIdx.x - 32 * kFirstEpiWarp, 32 * kEpiWarps);
         }
       }
     }
@@ -995,6 +1028,7 @@ void tc_plan_destroy(TcPlan* plan) {
   }
   cudaFree(plan->d_segs);
   cudaFree(plan->d_seg_done);
+  cudaFree(plan->d_ys_fx);
   delete plan;
 }
 
@@ -1037,6 +1071,7 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   a.n_seg = 0;
   a.xs = nullptr;
   a.ys = nullptr;
+  a.ys_fx = nullptr;
   a.seg_done = nullptr;
   if (plan->geom.pt)
     switch_fc_kernel<false, true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
@@ -1069,12 +1104,15 @@ cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4]
         S.kinds[i] = kd;
         S.y_off[i] = yo;
         yo += g.d_out[kd];
+        S.y_rows += g.d_out[kd];
         S.tile_count += (int64_t)g.tk.row_tiles[kd] * g.tk.col_tiles[kd];
       }
       t += S.tile_count;
+      if (S.y_off[0] + S.y_rows > plan->ys_rows) plan->ys_rows = S.y_off[0] + S.y_rows;
     }
   cudaError_t e = cudaSuccess;
-  if (!plan->d_segs) e = cudaMalloc(&plan->d_segs, sizeof(FusedSeg) * n);
+  if (!plan->d_ys_fx) e = cudaMalloc(&plan->d_ys_fx, sizeof(unsigned long long) * plan->ys_rows);
+  if (e == cudaSuccess && !plan->d_segs) e = cudaMalloc(&plan->d_segs, sizeof(FusedSeg) * n);
   if (e == cudaSuccess && !plan->d_seg_done) e = cudaMalloc(&plan->d_seg_done, sizeof(unsigned long long) * n);
   if (e == cudaSuccess) e = cudaMemcpy(plan->d_segs, h, sizeof(FusedSeg) * n, cudaMemcpyHostToDevice);
   delete[] h;
@@ -1088,6 +1126,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
                                    float* ys) {
   if (!plan->d_segs) return cudaErrorNotSupported;
   cudaError_t e = cudaMemsetAsync(plan->d_seg_done, 0, sizeof(unsigned long long) * plan->n_segs, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(plan->d_ys_fx, 0, sizeof(unsigned long long) * plan->ys_rows, s);
   if (e != cudaSuccess) return e;
   Args a;
   a.t0 = 0;
@@ -1107,6 +1146,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   a.n_seg = plan->n_segs;
   a.xs = static_cast<const __nv_bfloat16*>(xs);
   a.ys = ys;
+  a.ys_fx = plan->d_ys_fx;
   a.seg_done = plan->d_seg_done;
   switch_fc_kernel<true, false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   return cudaGetLastError();

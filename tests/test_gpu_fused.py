@@ -127,3 +127,37 @@ def test_fused_on_a_ctx_that_switches_with_another_kernel(monkeypatch, kernel):
                     ref = O.gemv(orc.W[(kd, l)], x)
                     assert PT.allclose_frac_fail(yb[yo:yo + d_out], ref) == 0.0, (t, l, kd)
                     yo += d_out
+
+
+@pytest.mark.parametrize("name,grid", [("mini", None), ("mini", "3"), ("mini-r32", None)])
+def test_fused_outputs_are_bitwise_reproducible(monkeypatch, name, grid):
+    """The fc fused launch accumulates each row's per-tile contributions in
+    64-bit fixed point (integer adds commute), so two runs on identical inputs
+    give bitwise-identical outputs whatever order the tiles finish in
+    (SURVEY §8c.5 item 5), not only bitwise-identical weights."""
+    monkeypatch.setenv("LSW_TC_KERNEL", "fc")
+    if grid:
+        monkeypatch.setenv("LSW_TC_GRID", grid)
+    cfg = synth.get_config(name)
+    X1 = synth.gen_x1(cfg, 3, "cuda")
+    xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
+    outs = []
+    for _ in range(2):
+        W, A, B, router = H.build_weights(cfg, "cuda")
+        sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+        info = sw.info()
+        assert info["switch_kernel"] == 3
+        ys = torch.empty(info["ys_elems"], device="cuda")
+        idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
+        gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
+        run = []
+        for t in range(3):
+            sw.decode_token_fused(X1[t], xs, ys, idx, gate)
+            torch.cuda.synchronize()
+            assert sw.device_status() == 0
+            run.append((ys.clone(), {kd: W[kd].clone() for kd in synth.KINDS}))
+        outs.append(run)
+    for (ya, Wa), (yb, Wb) in zip(*outs):
+        assert torch.equal(ya, yb)
+        for kd in synth.KINDS:
+            assert torch.equal(Wa[kd], Wb[kd])
