@@ -1,17 +1,19 @@
-// switch_tc_impl.cuh -- the two tensor-core switch kernels behind lsw::tc_plan_*
-// (switch_tc_dispatch.cu picks one per ctx at create time):
+// switch_tc_impl.cuh -- the three tensor-core switch kernels behind
+// lsw::tc_plan_* (switch_tc_dispatch.cu picks one per ctx at create time):
 //
 //   v1 (switch_tc.cu): every term of a 64-column sub-tile in its own TMEM
 //      accumulator, two buffers of 2k x 64 columns -- needs 2k <= 4 and one
-//      tile's A slices for all terms in shared memory; the measured fastest
-//      where it fits (7B: 0.83 of the copy peak).
+//      tile's A slices for all terms in shared memory (7B: 0.83 of the copy
+//      peak; superseded by fc, kept for the fused decode of tg ctxs and tests).
 //   tg (switch_tc_tg.cu): a tile's terms stream through TMEM tg at a time
 //      with an fp32 running sum in the epilogue, A slices staged per
 //      (sub-tile, term group): any k <= 4, any r <= 64.
-//   fc (switch_tc_fc.cu): the coefficients folded into the B factors as exact
-//      (hi, lo) bf16 pairs, ONE accumulator and one commit per 128 x 128 tile
-//      (Eq. 5's concatenation, K = 2 * sum_j rp): twice the tensor-core work,
-//      a fraction of the epilogue's TMEM reads and FMAs and of the commits.
+//   fc (switch_tc_fc.cu, the default): the coefficients folded into the B
+//      factors as exact (hi, lo) bf16 pairs, ONE accumulator and one commit per
+//      128 x 128 tile (Eq. 5's concatenation, K = 2 * sum_j rp): twice the
+//      tensor-core work, a fraction of the epilogue's TMEM reads and FMAs and
+//      of the commits (7B: 0.90 of the copy peak); its per-term mode (raw B,
+//      one accumulator per term, N = 128) for r = 64 and r = 32 with k >= 3.
 #pragma once
 
 #include "lsw_internal.cuh"
