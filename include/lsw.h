@@ -273,6 +273,21 @@ LSW_API lsw_status lsw_decode_all_layers(lsw_ctx* ctx, const void* xs, float* ys
  */
 LSW_API lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_t group, const void* x, float* y,
                                              const int32_t* idx, const float* gate, void* stream);
+/*
+ * Prefill ("For the prefilling phase, we have not
+ * implemented specific optimizations"): the unmerged forward of `group` for T
+ * prompt tokens, each with its OWN pre-gated decision, so nothing can be
+ * merged -- Eq. 2 as written:
+ *   Y[t] = W x_t + sum_j (alpha/r) gate[t][j] B[idx[t][j]] (A[idx[t][j]] x_t).
+ *   X: device [T, d_in] (storage dtype, row-major); idx: device int32 [T, top_k];
+ *   gate: device fp32 [T, top_k]; Y: device fp32 [T, rows], rows = the group's
+ *   output rows in site order (as lsw_decode_group).  The dense part is one
+ *   cuBLAS GEMM per site (fp32 accumulate), the LoRA parts two kernels.
+ *   LSW_E_STATE if the ctx is merged; LSW_E_UNSUPPORTED if tp_size > 1;
+ *   LSW_E_ARG for T outside [1, 2^20].  Invalid idx values are undefined.
+ */
+LSW_API lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const void* X, int64_t T,
+                                     const int32_t* idx, const float* gate, float* Y, void* stream);
 /* Every group of every layer, in order (layouts as lsw_decode_all_layers). */
 LSW_API lsw_status lsw_decode_all_layers_unmerged(lsw_ctx* ctx, const void* xs, float* ys, const int32_t* idx,
                                                   const float* gate, void* stream);

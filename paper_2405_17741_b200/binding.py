@@ -34,7 +34,7 @@ SYMBOLS = (
     "lsw_nccl_get_unique_id", "lsw_attach_nccl", "lsw_router_topk", "lsw_merge_all_layers",
     "lsw_unmerge_all_layers", "lsw_attach_pristine", "lsw_restore_merge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers",
     "lsw_decode_group_unmerged", "lsw_decode_all_layers_unmerged", "lsw_decode_token", "lsw_decode_token_fused",
-    "lsw_decode_token_host", "lsw_device_status",
+    "lsw_decode_token_host", "lsw_device_status", "lsw_prefill_group",
     "lsw_debug_switch_trace", "lsw_debug_merge_per_matrix",   # include/lsw_debug.h
 )
 
@@ -96,6 +96,7 @@ def load_library(path: str = LIB_PATH, strict: bool = True) -> ctypes.CDLL:
         "lsw_decode_token_fused": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_decode_token_host": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_device_status": (i32, [vp, vp, ctypes.POINTER(i32)]),
+        "lsw_prefill_group": (i32, [vp, i32, i32, vp, i64, vp, vp, vp, vp]),
         "lsw_debug_switch_trace": (i32, [vp, vp, i64, ctypes.POINTER(i64)]),
         "lsw_debug_merge_per_matrix": (i32, [vp, vp, vp, vp]),
     }
@@ -232,6 +233,12 @@ class LoraSwitch:
         """y = W x + sum_j (alpha/r) g_j B_j (A_j x) on the UN-merged weights (Eq. 2)."""
         _check(lib().lsw_decode_group_unmerged(self._h, layer, group, _ptr(x), _ptr(y), _ptr(idx), _ptr(gate),
                                                _stream(stream)))
+
+    def prefill_group(self, layer: int, group: int, X, idx, gate, Y, stream=None):
+        """Y[t] = W x_t + sum_j (alpha/r) g_tj B_j (A_j x_t) for T tokens with per-token decisions
+        (X [T, d_in], idx [T, k] int32, gate [T, k] fp32, Y [T, rows] fp32; unmerged ctx)."""
+        _check(lib().lsw_prefill_group(self._h, layer, group, _ptr(X), int(X.shape[0]), _ptr(idx), _ptr(gate),
+                                       _ptr(Y), _stream(stream)))
 
     def decode_all_layers_unmerged(self, xs, ys, idx, gate, stream=None):
         _check(lib().lsw_decode_all_layers_unmerged(self._h, _ptr(xs), _ptr(ys), _ptr(idx), _ptr(gate),

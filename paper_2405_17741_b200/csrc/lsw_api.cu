@@ -70,6 +70,9 @@ struct lsw_ctx {
   int32_t* st_idx = nullptr;
   float* st_gate = nullptr;
   cudaStream_t st_side = nullptr;       // lsw_decode_token_host: copies overlapped with the token
+  void* cublas = nullptr;               // lsw_prefill_group: cuBLAS handle (dense part)
+  float* prefill_u = nullptr;           // lsw_prefill_group: LoRA-down scratch
+  int64_t prefill_u_elems = 0;
   std::vector<cudaEvent_t> st_ev;       // [0]: xs landed; [1 + l]: layer l's outputs final
 };
 
@@ -230,6 +233,8 @@ lsw_status lsw_destroy(lsw_ctx* ctx) {
   cudaFree(ctx->st_idx);
   cudaFree(ctx->st_gate);
   for (cudaEvent_t ev : ctx->st_ev) cudaEventDestroy(ev);
+  prefill_cublas_destroy(ctx->cublas);
+  cudaFree(ctx->prefill_u);
   if (ctx->st_side) cudaStreamDestroy(ctx->st_side);
   delete ctx;
   return LSW_OK;
@@ -434,6 +439,57 @@ lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_t group,
                                      const int32_t* idx, const float* gate, void* stream) {
   return gemv_unmerged(ctx, layer, group, x, y, idx, gate, (cudaStream_t)stream, "lsw_decode_group_unmerged",
                        /*early_w=*/true);
+}
+
+lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const void* X, int64_t T,
+                             const int32_t* idx, const float* gate, float* Y, void* stream) {
+  const char* who = "lsw_prefill_group";
+  if (!ctx || !X || !idx || !gate || !Y) return fail(LSW_E_ARG, "%s: null argument", who);
+  if (T < 1 || T > (1 << 20)) return fail(LSW_E_ARG, "%s: T=%lld not in [1, 2^20]", who, (long long)T);
+  if (layer < 0 || layer >= ctx->cfg.n_layers)
+    return fail(LSW_E_ARG, "%s: layer=%d not in [0,%d)", who, layer, ctx->cfg.n_layers);
+  if (group < 0 || group >= LSW_NGROUP) return fail(LSW_E_ARG, "%s: group=%d invalid", who, group);
+  if (ctx->merged) return fail(LSW_E_STATE, "%s: the ctx is merged (prefill reads the pristine W)", who);
+  if (ctx->cfg.tp_size > 1) return fail(LSW_E_UNSUPPORTED, "%s: tp_size > 1", who);
+  if (!ctx->cublas && prefill_cublas_create(&ctx->cublas) != cudaSuccess)
+    return fail(LSW_E_CUDA, "%s: cublasCreate failed", who);
+  const int64_t need = T * 3 * ctx->cfg.top_k * ctx->cfg.rank;
+  if (need > ctx->prefill_u_elems) {
+    cudaFree(ctx->prefill_u);
+    ctx->prefill_u = nullptr;
+    if (cudaMalloc(&ctx->prefill_u, need * sizeof(float)) != cudaSuccess)
+      return fail(LSW_E_OOM, "%s: scratch allocation failed", who);
+    ctx->prefill_u_elems = need;
+  }
+  const size_t es = esize(ctx);
+  PrefillParams P{};
+  int64_t rows = 0;
+  const int n = kGroupSize[group];
+  for (int i = 0; i < n; ++i) {
+    const lsw_kind_desc& d = ctx->kinds[kGroupKinds[group][i]];
+    P.W[i] = (const uint8_t*)d.W + (size_t)layer * d.d_out * d.d_in * es;
+    P.A[i] = (const uint8_t*)d.A + (size_t)layer * ctx->cfg.n_experts * ctx->cfg.rank * d.d_in * es;
+    P.B[i] = (const uint8_t*)d.B + (size_t)layer * ctx->cfg.n_experts * d.d_out * ctx->cfg.rank * es;
+    P.d_out[i] = d.d_out;
+    P.row_begin[i] = rows;
+    rows += d.d_out;
+  }
+  P.n_sites = n;
+  P.k = ctx->cfg.top_k;
+  P.r = ctx->cfg.rank;
+  P.d_in = ctx->kinds[kGroupKinds[group][0]].d_in;
+  P.rows = rows;
+  P.T = T;
+  P.scale = ctx->cfg.alpha / (float)ctx->cfg.rank;
+  P.X = X;
+  P.idx = idx;
+  P.gate = gate;
+  P.U = ctx->prefill_u;
+  P.Y = Y;
+  cudaError_t e = launch_prefill(P, ctx->cfg.dtype, ctx->cublas, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: launch");
+  ctx->launches += 2;                       // LoRA-down + LoRA-up (the cuBLAS GEMMs are library calls)
+  return LSW_OK;
 }
 
 lsw_status lsw_decode_all_layers_unmerged(lsw_ctx* ctx, const void* xs, float* ys, const int32_t* idx,

@@ -218,6 +218,25 @@ void tok_plan_destroy(TokPlan* plan);
 cudaError_t launch_gemv_token(const TokPlan& plan, const void* xs, float* ys, unsigned long long* done,
                               unsigned long long base, int32_t dtype, cudaStream_t s);
 
+// Unmerged prefill of one group for T tokens (prefill.cu).
+struct PrefillParams {
+  const void* W[3];          // site q: W [d_out_q, d_in] of this layer (pristine)
+  const void* A[3];          // site q: A [N, r, d_in] of this layer
+  const void* B[3];          // site q: B [N, d_out_q, r] of this layer
+  int64_t d_out[3], row_begin[3];
+  int32_t n_sites, k, r, pad;
+  int64_t d_in, rows, T;
+  float scale;               // alpha / r
+  const void* X;             // [T, d_in]
+  const int32_t* idx;        // [T, k]
+  const float* gate;         // [T, k]
+  float* U;                  // scratch [T, 3, k*r]
+  float* Y;                  // [T, rows]
+};
+cudaError_t launch_prefill(const PrefillParams& P, int32_t dtype, void* cublas_handle, cudaStream_t s);
+cudaError_t prefill_cublas_create(void** handle);
+void prefill_cublas_destroy(void* handle);
+
 // Tensor-core switch (switch_tc.cu).
 struct TcPlan;   // opaque: packed operands + TMA descriptors
 cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why);

@@ -1,0 +1,82 @@
+"""Unmerged prefill vs the oracle (-m gpu).
+
+lsw_prefill_group evaluates Eq. 2 for T prompt tokens, each with its
+own pre-gated decision (the router applied to that token's x¹): the dense part
+by cuBLAS, the LoRA-down / LoRA-up parts by two kernels.  Checked through the C
+ABI against oracle.unmerged_forward token by token (fp64), for bf16 and fp32
+storage, k*r below and above a warp, ragged T; the result is deterministic;
+a merged ctx is refused.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2405_17741_b200 as L
+    from paper_2405_17741_b200 import harness as H
+
+
+def _f64(t):
+    return t.detach().to("cpu").to(torch.float64).numpy()
+
+
+@pytest.mark.parametrize("name,impl,T", [("toy", "simt", 5), ("mini", "tc", 7), ("mini-r64k3", "tc", 3),
+                                         ("mini-r4k4", "tc", 33)])
+def test_prefill_matches_oracle(name, impl, T):
+    cfg = synth.get_config(name)
+    W, A, B, router = H.build_weights(cfg, "cuda")
+    sw = H.make_switch(cfg, W, A, B, router, impl=impl)
+    X1 = synth.gen_x1(cfg, T, "cuda")
+    k = cfg.top_k
+    idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    gate = torch.empty(T, k, dtype=torch.float32, device="cuda")
+    for t in range(T):                              # each token's own pre-gated decision (Eq. 2)
+        sw.router_topk(X1[t], idx[t], gate[t])
+    torch.cuda.synchronize()
+    scale = cfg.alpha / cfg.rank
+    g = torch.Generator(device="cpu").manual_seed(2405177410 + 99)
+    for l in range(cfg.n_layers):
+        for gi, grp in enumerate(synth.GROUPS):
+            d_in = cfg.kind_shape(grp[0])[1]
+            rows = sum(cfg.kind_shape(kd)[0] for kd in grp)
+            X = torch.randn(T, d_in, generator=g).to(W[grp[0]].dtype).cuda()
+            Y = torch.full((T, rows), float("nan"), device="cuda")
+            sw.prefill_group(l, gi, X, idx, gate, Y)
+            torch.cuda.synchronize()
+            Y2 = torch.full((T, rows), float("nan"), device="cuda")
+            sw.prefill_group(l, gi, X, idx, gate, Y2)
+            torch.cuda.synchronize()
+            assert torch.equal(Y, Y2)               # deterministic
+            Yh = Y.cpu().numpy()
+            for t in range(T):
+                coefs = [(int(e), scale * float(gv)) for e, gv in zip(idx[t].tolist(), gate[t].tolist())]
+                o = 0
+                for kd in grp:
+                    d_out = cfg.kind_shape(kd)[0]
+                    ref = O.unmerged_forward(_f64(W[kd][l]), _f64(A[kd][l]), _f64(B[kd][l]), coefs, _f64(X[t]))
+                    np.testing.assert_allclose(Yh[t, o:o + d_out], ref, rtol=1e-4,
+                                               atol=1e-4 * float(np.abs(ref).max()))
+                    o += d_out
+    assert sw.device_status() == 0
+
+
+def test_prefill_refused_on_a_merged_ctx():
+    cfg = synth.get_config("mini")
+    W, A, B, router = H.build_weights(cfg, "cuda")
+    sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+    idx = torch.zeros(2, cfg.top_k, dtype=torch.int32, device="cuda")
+    gate = torch.zeros(2, cfg.top_k, dtype=torch.float32, device="cuda")
+    i1 = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
+    g1 = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
+    sw.router_topk(synth.gen_x1(cfg, 1, "cuda")[0], i1, g1)
+    sw.merge_all_layers(i1, g1)
+    X = torch.zeros(2, cfg.d_model, dtype=torch.bfloat16, device="cuda")
+    Y = torch.zeros(2, sum(cfg.kind_shape(kd)[0] for kd in synth.GROUPS[0]), device="cuda")
+    with pytest.raises(L.LswError) as ei:
+        sw.prefill_group(0, 0, X, idx, gate, Y)
+    assert "STATE" in str(ei.value)
