@@ -428,6 +428,43 @@ def run_ours(args, cfg):
             torch.cuda.synchronize()
             un_ms.append(a.elapsed_time(b))
 
+    # unmerged prefill: a 512-token prompt, every token with its
+    # own pre-gated decision, through every group of every layer (Eq. 2; the
+    # dense part is cuBLAS, the LoRA parts our kernels) -- reported, not timed
+    # into the decode metric
+    pf = None
+    if world == 1:
+        T_pf = 512
+        Xp = synth.gen_x1(cfg, T_pf, dev)
+        idx_pf = torch.empty(T_pf, cfg.top_k, dtype=torch.int32, device=dev)
+        gate_pf = torch.empty(T_pf, cfg.top_k, dtype=torch.float32, device=dev)
+        for t in range(T_pf):
+            sw.router_topk(Xp[t], idx_pf[t], gate_pf[t], stream)
+        d_ins = sorted({cfg.kind_shape(grp[0])[1] for grp in synth.GROUPS})
+        Xg = {d: torch.randn(T_pf, d, device=dev).to(Xp.dtype) for d in d_ins}
+        Yp = torch.empty(T_pf * max(sum(cfg.kind_shape(kd)[0] for kd in grp) for grp in synth.GROUPS), device=dev)
+
+        def prefill():
+            for l in range(cfg.n_layers):
+                for gi, grp in enumerate(synth.GROUPS):
+                    rows = sum(cfg.kind_shape(kd)[0] for kd in grp)
+                    sw.prefill_group(l, gi, Xg[cfg.kind_shape(grp[0])[1]], idx_pf, gate_pf,
+                                     Yp[:T_pf * rows].view(T_pf, rows), stream)
+        prefill()
+        torch.cuda.synchronize()
+        pf_ms = []
+        for _ in range(3):
+            a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            a.record(stream)
+            prefill()
+            b.record(stream)
+            torch.cuda.synchronize()
+            pf_ms.append(a.elapsed_time(b))
+        pf = {"tokens": T_pf, "ms": statistics.median(pf_ms),
+              "tokens_per_s": T_pf / (statistics.median(pf_ms) * 1e-3),
+              "note": "adapted-linear GEMMs of all layers (cuBLAS) + per-token LoRA (our kernels), "
+                      "router per token excluded"}
+
     # end-to-end through the public API with host buffers
     x1h = torch.empty(cfg.d_model, dtype=cfg.torch_dtype).pin_memory()
     xsh = xs.cpu().pin_memory()
@@ -491,6 +528,7 @@ def run_ours(args, cfg):
             "unmerged_decode_ms_per_token": statistics.median(un_ms) if un_ms else None,
             "unmerged_decode_GBps": (tb["unmerged_token"] / (statistics.median(un_ms) * 1e-3) / 1e9
                                      if un_ms else None),
+            "prefill": pf,
             "roofline": {"bound": "hbm", "achieved": sw_gbs, "peak": peak, "unit": "GB/s",
                          "frac": sw_gbs / peak, "traffic": _ncu_traffic(cfg, info),
                          "traffic_source": "profiles/ncu_switch_traffic.json (dram__bytes_read.sum + "

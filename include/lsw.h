@@ -281,8 +281,9 @@ LSW_API lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_
  *   Y[t] = W x_t + sum_j (alpha/r) gate[t][j] B[idx[t][j]] (A[idx[t][j]] x_t).
  *   X: device [T, d_in] (storage dtype, row-major); idx: device int32 [T, top_k];
  *   gate: device fp32 [T, top_k]; Y: device fp32 [T, rows], rows = the group's
- *   output rows in site order (as lsw_decode_group).  The dense part is one
- *   cuBLAS GEMM per site (fp32 accumulate), the LoRA parts two kernels.
+ *   output rows in site order (as lsw_decode_group).  The dense part and the
+ *   LoRA-down products of every expert are cuBLAS GEMMs per site (fp32
+ *   accumulate), the per-token LoRA-up step our kernel.
  *   LSW_E_STATE if the ctx is merged; LSW_E_UNSUPPORTED if tp_size > 1;
  *   LSW_E_ARG for T outside [1, 2^20].  Invalid idx values are undefined.
  */

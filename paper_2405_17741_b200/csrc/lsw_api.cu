@@ -453,7 +453,7 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
   if (ctx->cfg.tp_size > 1) return fail(LSW_E_UNSUPPORTED, "%s: tp_size > 1", who);
   if (!ctx->cublas && prefill_cublas_create(&ctx->cublas) != cudaSuccess)
     return fail(LSW_E_CUDA, "%s: cublasCreate failed", who);
-  const int64_t need = T * 3 * ctx->cfg.top_k * ctx->cfg.rank;
+  const int64_t need = T * 3 * ctx->cfg.n_experts * ctx->cfg.rank;
   if (need > ctx->prefill_u_elems) {
     cudaFree(ctx->prefill_u);
     ctx->prefill_u = nullptr;
@@ -477,6 +477,7 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
   P.n_sites = n;
   P.k = ctx->cfg.top_k;
   P.r = ctx->cfg.rank;
+  P.n_experts = ctx->cfg.n_experts;
   P.d_in = ctx->kinds[kGroupKinds[group][0]].d_in;
   P.rows = rows;
   P.T = T;
@@ -488,7 +489,7 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
   P.Y = Y;
   cudaError_t e = launch_prefill(P, ctx->cfg.dtype, ctx->cublas, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: launch");
-  ctx->launches += 2;                       // LoRA-down + LoRA-up (the cuBLAS GEMMs are library calls)
+  ctx->launches += 1;                       // LoRA-up (the dense and LoRA-down GEMMs are cuBLAS calls)
   return LSW_OK;
 }
 

@@ -224,13 +224,13 @@ struct PrefillParams {
   const void* A[3];          // site q: A [N, r, d_in] of this layer
   const void* B[3];          // site q: B [N, d_out_q, r] of this layer
   int64_t d_out[3], row_begin[3];
-  int32_t n_sites, k, r, pad;
+  int32_t n_sites, k, r, n_experts;
   int64_t d_in, rows, T;
   float scale;               // alpha / r
   const void* X;             // [T, d_in]
   const int32_t* idx;        // [T, k]
   const float* gate;         // [T, k]
-  float* U;                  // scratch [T, 3, k*r]
+  float* U;                  // scratch [T, 3, N*r]: every expert's LoRA-down products
   float* Y;                  // [T, rows]
 };
 cudaError_t launch_prefill(const PrefillParams& P, int32_t dtype, void* cublas_handle, cudaStream_t s);
