@@ -283,7 +283,9 @@ LSW_API lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_
  *   gate: device fp32 [T, top_k]; Y: device fp32 [T, rows], rows = the group's
  *   output rows in site order (as lsw_decode_group).  The dense part and the
  *   LoRA-down products of every expert are cuBLAS GEMMs per site (fp32
- *   accumulate), the per-token LoRA-up step our kernel.
+ *   accumulate); the LoRA-up step scales them by each token's gates (our
+ *   kernel) and adds one fp32 GEMM against a packed fp32 copy of B, which the
+ *   ctx builds on the first call (L * sum(d_out) * N * r * 4 bytes).
  *   LSW_E_STATE if the ctx is merged; LSW_E_UNSUPPORTED if tp_size > 1;
  *   LSW_E_ARG for T outside [1, 2^20].  Invalid idx values are undefined.
  */

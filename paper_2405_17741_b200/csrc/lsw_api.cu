@@ -71,8 +71,9 @@ struct lsw_ctx {
   float* st_gate = nullptr;
   cudaStream_t st_side = nullptr;       // lsw_decode_token_host: copies overlapped with the token
   void* cublas = nullptr;               // lsw_prefill_group: cuBLAS handle (dense part)
-  float* prefill_u = nullptr;           // lsw_prefill_group: LoRA-down scratch
+  float* prefill_u = nullptr;           // lsw_prefill_group: LoRA-down scratch (U, then Z)
   int64_t prefill_u_elems = 0;
+  float* bcat[LSW_NKIND] = {};          // lsw_prefill_group: packed fp32 B [L, d_out, N*r] per kind
   std::vector<cudaEvent_t> st_ev;       // [0]: xs landed; [1 + l]: layer l's outputs final
 };
 
@@ -235,6 +236,7 @@ lsw_status lsw_destroy(lsw_ctx* ctx) {
   for (cudaEvent_t ev : ctx->st_ev) cudaEventDestroy(ev);
   prefill_cublas_destroy(ctx->cublas);
   cudaFree(ctx->prefill_u);
+  for (int k = 0; k < LSW_NKIND; ++k) cudaFree(ctx->bcat[k]);
   if (ctx->st_side) cudaStreamDestroy(ctx->st_side);
   delete ctx;
   return LSW_OK;
@@ -457,9 +459,28 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
   if (need > ctx->prefill_u_elems) {
     cudaFree(ctx->prefill_u);
     ctx->prefill_u = nullptr;
-    if (cudaMalloc(&ctx->prefill_u, need * sizeof(float)) != cudaSuccess)
+    if (cudaMalloc(&ctx->prefill_u, 2 * need * sizeof(float)) != cudaSuccess)
       return fail(LSW_E_OOM, "%s: scratch allocation failed", who);
     ctx->prefill_u_elems = need;
+  }
+  // packed fp32 B of every layer, per kind, built on the first call (stream-ordered):
+  // the LoRA-up step becomes one GEMM per site (LSW_PREFILL_GATHER=1: the gather kernel)
+  static const bool gather = getenv("LSW_PREFILL_GATHER") != nullptr;
+  if (!gather) {
+    const int nr = ctx->cfg.n_experts * ctx->cfg.rank;
+    for (int k = 0; k < LSW_NKIND; ++k) {
+      if (ctx->bcat[k]) continue;
+      const lsw_kind_desc& d = ctx->kinds[k];
+      if (cudaMalloc(&ctx->bcat[k], (size_t)ctx->cfg.n_layers * d.d_out * nr * sizeof(float)) != cudaSuccess)
+        return fail(LSW_E_OOM, "%s: packed B allocation failed", who);
+      for (int l = 0; l < ctx->cfg.n_layers; ++l) {
+        const void* Bl = (const uint8_t*)d.B + (size_t)l * ctx->cfg.n_experts * d.d_out * ctx->cfg.rank * esize(ctx);
+        cudaError_t e = launch_pack_bcat(Bl, ctx->bcat[k] + (size_t)l * d.d_out * nr, d.d_out, ctx->cfg.n_experts,
+                                         ctx->cfg.rank, ctx->cfg.dtype, (cudaStream_t)stream);
+        if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: pack");
+        ++ctx->launches;
+      }
+    }
   }
   const size_t es = esize(ctx);
   PrefillParams P{};
@@ -473,6 +494,9 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
     P.d_out[i] = d.d_out;
     P.row_begin[i] = rows;
     rows += d.d_out;
+    const int kd = kGroupKinds[group][i];
+    P.Bcat[i] = ctx->bcat[kd] ? ctx->bcat[kd] + (size_t)layer * d.d_out * ctx->cfg.n_experts * ctx->cfg.rank
+                              : nullptr;
   }
   P.n_sites = n;
   P.k = ctx->cfg.top_k;
@@ -486,6 +510,7 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
   P.idx = idx;
   P.gate = gate;
   P.U = ctx->prefill_u;
+  P.Z = ctx->prefill_u + need;
   P.Y = Y;
   cudaError_t e = launch_prefill(P, ctx->cfg.dtype, ctx->cublas, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: launch");

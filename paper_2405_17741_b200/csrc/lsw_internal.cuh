@@ -231,8 +231,11 @@ struct PrefillParams {
   const int32_t* idx;        // [T, k]
   const float* gate;         // [T, k]
   float* U;                  // scratch [T, 3, N*r]: every expert's LoRA-down products
+  float* Z;                  // scratch [T, 3, N*r]: U gate-scaled at the selected experts, else 0
+  const float* Bcat[3];      // site q: packed fp32 [d_out_q, N*r] of this layer, or null (gather path)
   float* Y;                  // [T, rows]
 };
+cudaError_t launch_pack_bcat(const void* B, float* out, int64_t d_out, int N, int r, int32_t dtype, cudaStream_t s);
 cudaError_t launch_prefill(const PrefillParams& P, int32_t dtype, void* cublas_handle, cudaStream_t s);
 cudaError_t prefill_cublas_create(void** handle);
 void prefill_cublas_destroy(void* handle);

@@ -6,14 +6,15 @@
 //     Y[t] = W x_t + sum_j (alpha/r) g_tj B_{e_tj} (A_{e_tj} x_t).
 // The dense part and the LoRA-down products are plain library GEMMs per site
 // (cuBLAS, bf16/fp32 in, fp32 accumulate and out): Y = X W^T and, for EVERY
-// expert, U = X A^T (the bank A [N, r, d_in] is one [N*r, d_in] matrix); our
-// kernel gathers each token's experts for the LoRA-up step:
+// expert, U = X A^T (the bank A [N, r, d_in] is one [N*r, d_in] matrix).  The
+// LoRA-up step: our kernel scales U by each token's gates at its selected
+// experts (zero elsewhere, Z), then one fp32 GEMM per site adds Z B_cat^T
+// against a packed fp32 copy of B ([d_out, N*r] per layer, built by the ctx on
+// the first call).  Fallback (LSW_PREFILL_GATHER=1) -- a per-(token, row) gather:
 //   lora_up_prefill: Y[t][row] += sum_j s g_tj sum_rho B_q[e_tj][row, rho] U[t][q][e_tj*r + rho]
 //     (one thread per (token, row), 16-B loads of B).
-// Measured (7B, 512 tokens, all groups of all layers): 20 ms (25K tokens/s);
-// the dense GEMMs alone need ~5 ms -- the per-(token, row) LoRA-up gather is
-// the cost (a shared-memory-staged variant measured slower, 23 ms); a single
-// packed [rows, N*r] x [N*r, T] GEMM for the LoRA-up is the next step.
+// Measured (7B, 512 tokens, all groups of all layers): packed GEMM 15.6 ms
+// (33K tokens/s), gather 20 ms (a shared-memory-staged gather 23 ms).
 #include <cublas_v2.h>
 
 #include "lsw_internal.cuh"
@@ -60,6 +61,39 @@ __global__ void lora_up_prefill(const PrefillParams P) {
   P.Y[i] += e;
 }
 
+// Z[t][q][e*r + rho] = (sum_j [e == e_tj] (alpha/r) g_tj) * U[t][q][e*r + rho]:
+// the gate-scaled LoRA-down products of each token's selected experts, zero
+// elsewhere, so that the LoRA-up step is one dense GEMM against the packed B.
+__global__ void prefill_gate_u(const PrefillParams P) {
+  const int nr = P.n_experts * P.r;
+  const int64_t n = P.T * 3 * nr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / (3 * nr);
+    const int e = (int)((i % nr) / P.r);
+    float c = 0.f;
+    for (int j = 0; j < P.k; ++j)
+      if (P.idx[t * P.k + j] == e) c += P.scale * P.gate[t * P.k + j];
+    P.Z[i] = c * P.U[i];
+  }
+}
+
+// B [N, d_out, r] (one layer of one kind) -> fp32 [d_out, N*r]
+template <bool kBf16>
+__global__ void pack_bcat(const void* B, float* out, int64_t d_out, int N, int r) {
+  const int64_t n = d_out * N * r;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / (N * r);
+    const int c = (int)(i % (N * r)), e = c / r, rho = c - e * r;
+    out[i] = ld_elem<kBf16>(B, ((int64_t)e * d_out + row) * r + rho);
+  }
+}
+
+cudaError_t launch_pack_bcat(const void* B, float* out, int64_t d_out, int N, int r, int32_t dtype, cudaStream_t s) {
+  if (dtype == LSW_BF16) pack_bcat<true><<<1024, 256, 0, s>>>(B, out, d_out, N, r);
+  else pack_bcat<false><<<1024, 256, 0, s>>>(B, out, d_out, N, r);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_prefill(const PrefillParams& P, int32_t dtype, void* cublas_handle, cudaStream_t s) {
   const bool bf16 = dtype == LSW_BF16;
   cublasHandle_t h = static_cast<cublasHandle_t>(cublas_handle);
@@ -89,8 +123,23 @@ cudaError_t launch_prefill(const PrefillParams& P, int32_t dtype, void* cublas_h
                      CUBLAS_GEMM_DEFAULT);
     if (st != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
   }
-  const int64_t n = P.T * P.rows;
-  (bf16 ? lora_up_prefill<true> : lora_up_prefill<false>)<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P);
+  // LoRA-up: Y += Z B_cat^T per site, one fp32 GEMM (K = N*r) against the
+  // ctx's packed fp32 copy of B, when it exists; else the per-(token, row) gather
+  if (P.Bcat[0]) {
+    prefill_gate_u<<<256, 256, 0, s>>>(P);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    for (int q = 0; q < P.n_sites; ++q) {
+      const cublasStatus_t st =
+          cublasGemmEx(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)P.d_out[q], (int)P.T, nr, &one, P.Bcat[q], CUDA_R_32F, nr,
+                       P.Z + (int64_t)q * nr, CUDA_R_32F, 3 * nr, &one, P.Y + P.row_begin[q], CUDA_R_32F,
+                       (int)P.rows, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+      if (st != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    }
+  } else {
+    const int64_t n = P.T * P.rows;
+    (bf16 ? lora_up_prefill<true> : lora_up_prefill<false>)<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(P);
+  }
   e = cudaGetLastError();
   return e;
 }
