@@ -87,3 +87,22 @@ def test_product_package_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "lsw_oracle" not in src, f
+
+
+def test_null_ctx_is_refused_by_every_entry_point(L):
+    """Every hot call validates before it enqueues anything: a null ctx (or
+    null argument) returns LSW_E_ARG on a CPU-only box, no CUDA call made."""
+    lib = L.lib()
+    E_ARG = 1
+    assert lib.lsw_merge_all_layers(None, None, None, None) == E_ARG
+    assert lib.lsw_restore_merge_all_layers(None, None, None, None) == E_ARG
+    assert lib.lsw_decode_linear(None, 0, 0, None, None, None) == E_ARG
+    assert lib.lsw_decode_group(None, 0, 0, None, None, None) == E_ARG
+    assert lib.lsw_decode_all_layers(None, None, None, None) == E_ARG
+    assert lib.lsw_decode_group_unmerged(None, 0, 0, None, None, None, None, None) == E_ARG
+    assert lib.lsw_decode_all_layers_unmerged(None, None, None, None, None, None) == E_ARG
+    assert lib.lsw_decode_token(None, None, None, None, None, None, None) == E_ARG
+    assert lib.lsw_decode_token_fused(None, None, None, None, None, None, None) == E_ARG
+    assert lib.lsw_decode_token_host(None, None, None, None, None, None, None) == E_ARG
+    assert lib.lsw_prefill_group(None, 0, 0, None, 1, None, None, None, None) == E_ARG
+    assert b"null" in lib.lsw_last_error()
