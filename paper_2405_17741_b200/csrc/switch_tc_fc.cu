@@ -903,13 +903,16 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   const int64_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
   // A ring depth in units per tile u (fold: the whole tile's slices; per-term:
   // one unit per kPtGroup terms).  Candidates (W stages, B buffers) in order of
-  // preference; for each the A stages that fit.  Pass 0 wants 2u + 1 A units
+  // preference -- three W stages first: a fourth puts more W requests in flight
+  // than the HBM stream wants (k = 1, same box: W 3 + B 2 + A 4 0.895 vs W 4 +
+  // B 2 + A 3 0.85; the W-stream probe itself 0.872 with 4 stages vs 0.91 with
+  // 3); for each the A stages that fit.  Pass 0 wants 2u + 1 A units
   // (a tile of lookahead), pass 1 u + 1, pass 2 any >= 2; W stays >= 3 before
   // the last resort (measured, 16-layer 7B shape: W 2 costs 7-15 %; W 3 + B 1
   // + A 3 0.860 vs W 4 + B 1 + A 2 0.846 at k = 3; per-term r = 32 k = 3:
   // W 3 + B 1 + A 5 0.656 vs W 3 + B 2 + A 2 0.626).
   struct Cand { int ws, bb; };
-  const Cand cands[] = {{4, 2}, {3, 2}, {3, 1}, {4, 1}};
+  const Cand cands[] = {{3, 2}, {3, 1}, {4, 2}, {4, 1}};
   const int u = g.pt ? (mt + kPtGroup - 1) / kPtGroup : 1;
   int bb_env = 0, as_env = 0, ws_env = 0;
   if (const char* v = getenv("LSW_FC_BBUFS")) bb_env = atoi(v);

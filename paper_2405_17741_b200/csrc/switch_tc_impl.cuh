@@ -85,8 +85,8 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
                                    float* ys);
 }  // namespace fc
 
-// the fc kernel is the default from kFcMinMmas MMAs per tile on (i.e. unless
-// 2k * rp <= 32, where tg is ~1 % faster), wherever its shared-memory plan fits
-// (measured, scripts/sweep_bench.py)
-constexpr int kFcMinMmas = 8;
+// the fc kernel is the default from kFcMinMmas MMAs per tile on, wherever its
+// shared-memory plan fits (measured: with three W stages it is
+// ahead of tg at k = 1 too, 0.895 vs 0.856)
+constexpr int kFcMinMmas = 0;
 }  // namespace lsw
