@@ -835,9 +835,11 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
     const size_t slot_bytes = (size_t)R * row_bytes;
     // Ring budget.  Measured (7B token of GEMVs): 220 KB 2.37 ms, 110 KB 2.59 ms,
     // 72 KB 3.49 ms -- a deep ring per SM beats letting the next GEMV's CTA
-    // co-reside under PDL.  LSW_GEMV_SMEM_KB overrides.
+    // co-reside under PDL; with the bf16 x staging (same box, 2 runs each):
+    // 220 KB 2.172, 176 KB 2.164, 144 KB 2.32, 112 KB 2.53 ms -- five 32-KB
+    // slots in flight rather than six.  LSW_GEMV_SMEM_KB overrides.
     // (the unmerged form keeps ~12 KB of static shared memory: u, row sums, terms)
-    size_t budget = lora ? 208 * 1024 : 220 * 1024;
+    size_t budget = lora ? 208 * 1024 : 176 * 1024;
     if (const char* v = getenv("LSW_GEMV_SMEM_KB")) { long x = atol(v); if (x >= 32 && x <= 224) budget = (size_t)x * 1024; }
     int slots = (int)((budget - x_bytes) / slot_bytes);
     if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
