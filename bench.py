@@ -113,9 +113,9 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-SWITCH_KERNELS = {1: "switch_tc_kernel [v1, per-term TMEM accumulators]",
-                  2: "switch_tc_kernel [tg, term groups]",
-                  3: "switch_fc_kernel [fc, folded coefficients, one accumulator per tile]"}
+SWITCH_KERNELS = {3: "switch_fc_kernel [fold: folded coefficients, one accumulator per tile]",
+                  4: "switch_fc_kernel [per-term accumulators, B per strip]",
+                  5: "switch_fc_kernel [per-term accumulators, B per unit]"}
 
 
 def _ncu_traffic(cfg, info):
@@ -396,8 +396,8 @@ def run_ours(args, cfg):
     fu_ms = []
     fused_ok = False
     if world == 1 and info["switch_impl"] == "tc":
-        # (the fused launch is the fc kernel's fused build, or v1's -- an
-        # untimed warm-up token first builds its segment table)
+        # (the fused launch is the fold mode's fused build -- an untimed
+        # warm-up token first builds its segment table)
         try:
             sw.decode_token_fused(X1[0], xs, ys, idx, gate, stream)
             torch.cuda.synchronize()
@@ -408,7 +408,7 @@ def run_ours(args, cfg):
         for t in range(min(args.steps, 10)):
             a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
             a.record(stream)
-            sw.decode_token_fused(X1[t], xs, ys, idx, gate, stream)
+            sw.decode_token_fused(X1[t + 1], xs, ys, idx, gate, stream)   # X1[0] was the warm-up
             b.record(stream)
             torch.cuda.synchronize()
             fu_ms.append(a.elapsed_time(b))

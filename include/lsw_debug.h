@@ -1,16 +1,6 @@
 /*
- * lsw_debug.h -- tuning hooks of liblsw.so.  Not part of the hot path and not
- * needed by users; they expose measurement state that the kernels record only
- * when enabled by environment variables read at lsw_create:
- *
- *   LSW_TC_TRACE=1   the tensor-core switch kernel stamps %globaltimer (ns) at
- *                    16 pipeline event slots of its first 2048 tiles in 4 CTAs
- *                    spread over the grid (layout [cta][tile][event], events in
- *                    switch_tc.cu EV_*: W issued, A issued, A full, MMA start,
- *                    MMA done, epilogue saw W, epilogue saw accumulators, stage
- *                    freed, epilogue done, MMA got a free accumulator buffer,
- *                    MMAs issued, first sub-tile done, A production began, A
- *                    ring slot free); 0 = not reached.
+ * lsw_debug.h -- variant selection, tuning and ablation hooks of liblsw.so.
+ * Not part of the hot path and not needed by users.
  */
 #ifndef LSW_DEBUG_H_
 #define LSW_DEBUG_H_
@@ -21,10 +11,27 @@
 extern "C" {
 #endif
 
-/* Copy up to n uint64 trace words of the last switch launch into host_out (host
- * memory).  Returns the number copied in *n_out (0 when tracing is off or the
- * ctx uses the SIMT switch).  Synchronizes the device.  LSW_E_ARG on null. */
-LSW_API lsw_status lsw_debug_switch_trace(lsw_ctx* ctx, uint64_t* host_out, int64_t n, int64_t* n_out);
+/* Variant / tuning options, process-wide, read when a ctx is created
+ * (lsw_create): the library never reads the environment.  key NULL clears
+ * every option; value NULL unsets `key`.  Unknown keys are ignored.  Always
+ * LSW_OK.  Keys (defaults in brackets; results are identical for every value
+ * unless marked "probe"):
+ *   tc_kernel      fold | pt | bu   force a mode of the tensor-core switch
+ *                                   [chosen from r, k: DESIGN.md §5]
+ *   tc_grid        N      switch grid (CTAs) below the SM count      [#SMs]
+ *   tc_chunk       N      tiles per CTA chunk of the sweep order     [48]
+ *   fc_stages / fc_astages / fc_bbufs   explicit shared-memory plan (all three)
+ *   fc_wrm         0 | 1  W tile moved by one 4-D TMA op             [1]
+ *   gemv           ldg    the warp-per-row LDG GEMV instead of the bulk ring
+ *   gemv_grid      N      GEMV grid cap                               [#SMs]
+ *   gemv_op_kb     N      bytes per bulk copy, KB                     [32]
+ *   gemv_smem_kb   N      ring budget, KB                             [176 / 208]
+ *   prefill_gather 0 | 1  LoRA-up of the prefill by the gather kernel [0]
+ * Probes (deliberately WRONG results; only in a build with -DLSW_TUNING,
+ * ignored otherwise): tc_probe (1: W stream only; 16: no fold math),
+ * fc_fused_probe (4: no segment wait; 8: no GEMV), gemv_probe (stream only),
+ * unmerged_flags (4: no LoRA-up term). */
+LSW_API lsw_status lsw_debug_set_option(const char* key, const char* value);
 
 /* Launch-count ablation (the paper's "simple merge" row of
  * Tab. 6): the Eq. 6 merge of lsw_merge_all_layers, but ONE launch

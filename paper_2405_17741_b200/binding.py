@@ -35,7 +35,7 @@ SYMBOLS = (
     "lsw_unmerge_all_layers", "lsw_attach_pristine", "lsw_restore_merge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers",
     "lsw_decode_group_unmerged", "lsw_decode_all_layers_unmerged", "lsw_decode_token", "lsw_decode_token_fused",
     "lsw_decode_token_host", "lsw_device_status", "lsw_prefill_group",
-    "lsw_debug_switch_trace", "lsw_debug_merge_per_matrix",   # include/lsw_debug.h
+    "lsw_debug_set_option", "lsw_debug_merge_per_matrix",   # include/lsw_debug.h
 )
 
 
@@ -97,7 +97,7 @@ def load_library(path: str = LIB_PATH, strict: bool = True) -> ctypes.CDLL:
         "lsw_decode_token_host": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "lsw_device_status": (i32, [vp, vp, ctypes.POINTER(i32)]),
         "lsw_prefill_group": (i32, [vp, i32, i32, vp, i64, vp, vp, vp, vp]),
-        "lsw_debug_switch_trace": (i32, [vp, vp, i64, ctypes.POINTER(i64)]),
+        "lsw_debug_set_option": (i32, [ctypes.c_char_p, ctypes.c_char_p]),
         "lsw_debug_merge_per_matrix": (i32, [vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
@@ -110,6 +110,29 @@ def load_library(path: str = LIB_PATH, strict: bool = True) -> ctypes.CDLL:
 
 
 _LIB: Optional[ctypes.CDLL] = None
+
+
+def set_option(key: Optional[str], value=None):
+    """include/lsw_debug.h lsw_debug_set_option: variant / tuning options read
+    at ctx creation (key None clears all, value None unsets)."""
+    enc = lambda v: None if v is None else str(v).encode()
+    _check(lib().lsw_debug_set_option(enc(key), enc(value)))
+
+
+class options:
+    """Context manager: set options for the ctxs created inside, then clear them."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k in self.kv:
+            set_option(k, None)
 
 
 def lib() -> ctypes.CDLL:
@@ -260,15 +283,6 @@ class LoraSwitch:
     def debug_merge_per_matrix(self, idx, gate, stream=None):
         """Launch-count ablation (include/lsw_debug.h): the merge as 7*L launches."""
         _check(lib().lsw_debug_merge_per_matrix(self._h, _ptr(idx), _ptr(gate), _stream(stream)))
-
-    def debug_switch_trace(self):
-        """Tuning hook (include/lsw_debug.h): int64 ns timestamps [2, 256, 12]
-        of the last tensor-core switch launch when LSW_TC_TRACE was set ([cta, tile, event], 16 events)."""
-        import numpy as np
-        buf = np.zeros(4 * 2048 * 16, dtype=np.uint64)
-        n = ctypes.c_int64(0)
-        _check(lib().lsw_debug_switch_trace(self._h, buf.ctypes.data, buf.size, ctypes.byref(n)))
-        return buf[: n.value].reshape(-1, 2048, 16) if n.value else None
 
     def device_status(self, stream=None) -> int:
         code = ctypes.c_int32(0)

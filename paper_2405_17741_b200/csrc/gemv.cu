@@ -345,33 +345,6 @@ __device__ __forceinline__ float row_dot(const uint8_t* wrow, const uint8_t* xs,
   return acc;
 }
 
-// Unmerged decode: the pre-gate's decision is known for EVERY layer at the
-// start of the token, so the selected LoRA-down rows of all layers can
-// be pulled into L2 (evict_last; the W streams are evict_first) before the
-// first group -- each GEMV's LoRA-down products then read them at L2 latency.
-__global__ void lora_prefetch_kernel(LoraPrefetch q) {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  const int total = LSW_NKIND * q.n_layers * q.k;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int kd = i / (q.n_layers * q.k), rem = i - kd * q.n_layers * q.k;
-    const int l = rem / q.k, j = rem - l * q.k;
-    const int64_t block = (int64_t)q.r * q.d_in[kd] * q.es;           // one expert's r rows
-    const uint8_t* src = reinterpret_cast<const uint8_t*>(q.A[kd]) +
-                         ((int64_t)l * q.n_experts + q.idx[j]) * block;
-    for (int64_t off = 0; off < block; off += 65536) {
-      const uint32_t n = (uint32_t)(block - off < 65536 ? block - off : 65536);
-      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src + off), "r"(n), "l"(pol)
-                   : "memory");
-    }
-  }
-}
-
-cudaError_t launch_lora_prefetch(const LoraPrefetch& q, cudaStream_t s) {
-  lora_prefetch_kernel<<<16, 128, 0, s>>>(q);
-  return cudaGetLastError();
-}
-
 template <bool kBf16, bool kLora, bool kXB>
 __global__ void __launch_bounds__(kLora ? kBulkThreads + 32 * kLoraWarps : kBulkThreads, 1)
 gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, const GemvLora L) {
@@ -444,7 +417,22 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   }
   if (early_w & 1) asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after our wait: see above
-  const int kr = kLora ? L.k * L.r : 0;
+  // unmerged form: the decision is validated by every CTA alike (indices in
+  // [0, N) and distinct, gates finite -- as the switch's build_coefs); an
+  // invalid one drops the LoRA terms (y = W x) and latches the error
+  bool lora_ok = kLora;
+  if (kLora) {
+    int bad = 0;
+    for (int j = 0; j < L.k; ++j) {
+      const int32_t e = L.idx[j];
+      if (e < 0 || e >= L.n_experts) bad = LSW_DEV_BAD_INDEX;
+      for (int i = 0; i < j; ++i) if (L.idx[i] == e) bad = LSW_DEV_BAD_INDEX;
+      if (!bad && !isfinite(L.gate[j])) bad = LSW_DEV_BAD_GATE;
+    }
+    lora_ok = bad == 0;
+    if (bad && blockIdx.x == 0 && threadIdx.x == 32) atomicCAS(L.err, 0, bad);
+  }
+  const int kr = lora_ok ? L.k * L.r : 0;
   const int n_dots = kLora ? p.n_sites * kr : 0;
   // unmerged form: u (all LoRA-down products of the group), staged by the
   // LoRA-down warps once every CTA has published its share
@@ -508,7 +496,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");
     // LoRA-up terms of this CTA's rows, one lane per row, while the consumers
     // still stream (their row sums wait in acc_s; joined at the end)
-    if (n_local <= kMaxLocal && !(L.flags & 4))
+    if (n_local <= kMaxLocal && !(L.flags & 4) && lora_ok)
       for (int64_t t = threadIdx.x - 32 * (1 + kBulkConsumers); t < n_local; t += 32 * kLoraWarps) {
         const int64_t row = (blockIdx.x + (t / R) * G) * R + t % R;
         e_s[t] = row < p.rows_total ? lora_up_row<kBf16>(p, L, us, row, kr) : 0.f;
@@ -543,7 +531,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   if (kLora) {
     // Eq. 2: y = (W x) + LoRA-up term, one rounding of the sum per row
     asm volatile("bar.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");   // e_s / us ready
-    const bool up = !(L.flags & 4) && !(early_w & 2);
+    const bool up = !(L.flags & 4) && !(early_w & 2) && lora_ok;
     if (in_smem) {
       for (int64_t t = threadIdx.x - 32; t < n_local; t += 32 * kBulkConsumers) {
         const int64_t row = (blockIdx.x + (t / R) * G) * R + t % R;
@@ -571,265 +559,17 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   }
 }
 
-// ---------------------------------------------------------------------------
-// K4b: the whole token's GEMVs in one persistent launch.  The groups' chunks
-// (R rows each) form one global sequence, chunk c -> CTA c % G, so every SM
-// streams the same number of bytes (+-1 chunk) over the token.  The producer
-// runs through ALL of its chunks back to back (W does not depend on x), so the
-// HBM stream does not drain at group boundaries the way it does between
-// launches; the consumers keep the decoder's order: x of group g is copied in
-// only after all CTAs have counted group g-1 done on a device-wide counter
-// (release add / acquire load), and y of group g-1 is complete by then.
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Spin (with a ~20 s watchdog) until a device-wide counter reaches target.
-__device__ __forceinline__ void wait_counter(const unsigned long long* p, unsigned long long target) {
-  if ((long long)(ld_acquire_u64(p) - target) >= 0) return;
-  uint64_t t0, t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
-  for (uint32_t n = 1; (long long)(ld_acquire_u64(p) - target) < 0; ++n) {
-    __nanosleep(32);
-    if ((n & 1023u) == 0) {
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-      if (t - t0 > 20000000000ull) __trap();
-    }
-  }
-}
-
-template <bool kBf16>
-__global__ void __launch_bounds__(kBulkThreads, 1)
-gemv_token_kernel(const TokGroup* __restrict__ grp, int32_t n_groups, int64_t total_chunks,
-                  const uint8_t* __restrict__ xs, float* __restrict__ ys, int32_t slots, uint32_t slot_bytes,
-                  uint32_t x_cap, unsigned long long* done, unsigned long long base, int32_t flags) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[kBulkMaxSlots], empty[kBulkMaxSlots];
-  __shared__ volatile int64_t issued;               // ticket, as in gemv_bulk_kernel
-  constexpr int64_t es = kBf16 ? 2 : 4;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* xsm = smem_raw;
-  uint8_t* ring = smem_raw + x_cap;
-  const int64_t G = gridDim.x, b = blockIdx.x;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < slots; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&full[s])), "r"(1));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&empty[s])), "r"(kBulkConsumers));
-    }
-    issued = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // W is written by the switch before us
-  if (warp == 0) {
-    // the group table (a few KB) into L1 once: per-group descriptor reads
-    // below then hit L1 instead of paying an L2 round trip per group
-    for (int off = lane * 128; off < n_groups * (int)sizeof(TokGroup); off += 32 * 128)
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const uint8_t*>(grp) + off));
-    if (lane == 0) {
-      uint64_t pol;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      // the current group's descriptor, held in registers
-      int g = -1;
-      int64_t next = 0, cb = 0, rows = 0, R = 1, rb_ = 0;
-      int ns = 1;
-      const uint8_t* W0 = nullptr;
-      const uint8_t* W1 = nullptr;
-      const uint8_t* W2 = nullptr;
-      int64_t sb1 = 0, sb2 = 0;
-      int64_t i = 0;
-      for (int64_t c = b; c < total_chunks; c += G, ++i) {
-        while (c >= next) {
-          ++g;
-          const TokGroup* t = grp + g;
-          cb = t->chunk_begin; rows = t->rows; R = t->R; rb_ = t->row_bytes; ns = t->n_sites;
-          W0 = reinterpret_cast<const uint8_t*>(t->W[0]);
-          W1 = reinterpret_cast<const uint8_t*>(t->W[1]);
-          W2 = reinterpret_cast<const uint8_t*>(t->W[2]);
-          sb1 = ns > 1 ? t->row_begin[1] : rows;
-          sb2 = ns > 2 ? t->row_begin[2] : rows;
-          next = g + 1 < n_groups ? grp[g + 1].chunk_begin : total_chunks;
-        }
-        const int s = (int)(i % slots);
-        g_mbar_wait(s_u32(&empty[s]), (uint32_t)((i / slots) & 1) ^ 1);
-        const int64_t r0 = (c - cb) * R;
-        const int64_t r1 = r0 + R < rows ? r0 + R : rows;
-        const uint32_t bar = s_u32(&full[s]);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                     "r"((uint32_t)((r1 - r0) * rb_)) : "memory");
-        for (int q = 0; q < ns; ++q) {       // one bulk copy per site the chunk overlaps
-          const int64_t sb = q == 0 ? 0 : q == 1 ? sb1 : sb2;
-          const int64_t se = q == 0 ? sb1 : q == 1 ? sb2 : rows;
-          const int64_t a = r0 > sb ? r0 : sb, e = r1 < se ? r1 : se;
-          if (a >= e) continue;
-          const uint8_t* src = (q == 0 ? W0 : q == 1 ? W1 : W2) + (a - sb) * rb_;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-              ::"r"(s_u32(ring + (size_t)s * slot_bytes + (a - r0) * rb_)), "l"(src),
-                "r"((uint32_t)((e - a) * rb_)), "r"(bar), "l"(pol)
-              : "memory");
-        }
-        issued = i + 1;
-      }
-    }
-    return;
-  }
-  const int cw = warp - 1;
-  int64_t i0 = 0;                                   // this CTA's chunks before group g
-  for (int g = 0; g < n_groups; ++g) {
-    const TokGroup* t = grp + g;
-    const int64_t cb = t->chunk_begin, ce = g + 1 < n_groups ? grp[g + 1].chunk_begin : total_chunks;
-    const int64_t rows = t->rows, R = t->R;
-    const uint32_t row_bytes = t->row_bytes;
-    const int64_t first = cb + (((b - cb) % G) + G) % G;
-    const int64_t nj = first < ce ? (ce - first + G - 1) / G : 0;
-    if (nj > 0) {
-      // decoder order: x of group g only after every CTA has finished group g-1
-      if (threadIdx.x == 32 && g > 0 && !(flags & 1))
-        wait_counter(done, base + (unsigned long long)g * (unsigned long long)G);
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
-      stage_x<kBf16>(xs + t->x_off * es, xsm, row_bytes, threadIdx.x - 32, 32 * kBulkConsumers);
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
-      const int64_t nchunk16 = row_bytes / 16;
-      float* yg = ys + t->y_off;
-      for (int64_t j = 0; j < nj; ++j) {
-        const int64_t i = i0 + j;
-        const int s = (int)(i % slots);
-        const int64_t r0 = (first + j * G - cb) * R;
-        const int64_t nr = rows - r0 < R ? rows - r0 : R;
-        while (issued <= i) __nanosleep(64);
-        g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
-        // rows of the flat sequence (j*R + k) are dealt to warps round-robin
-        for (int64_t k = ((cw - (j * R) % kBulkConsumers) % kBulkConsumers + kBulkConsumers) % kBulkConsumers;
-             k < nr && !(flags & 2); k += kBulkConsumers) {    // flags bit 1: tuning probe, stream only
-          const float acc = row_dot<kBf16>(ring + (size_t)s * slot_bytes + (size_t)k * row_bytes, xsm, nchunk16, lane);
-          if (lane == 0) yg[r0 + k] = acc;
-        }
-        __syncwarp();
-        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[s])) : "memory");
-      }
-      i0 += nj;
-    }
-    // this CTA is done with group g: x buffer free, its y rows written
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
-    if (threadIdx.x == 32) {
-      __threadfence();
-      asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(done), "l"(1ull) : "memory");
-    }
-  }
-}
-
-cudaError_t tok_plan_create(TokPlan* plan, TokGroup* groups, int32_t n_groups, int num_sms, bool bf16) {
-  *plan = TokPlan{};
-  // rows per chunk: ~32 KB per bulk copy (LSW_GEMV_SLOT_KB), at most 8 rows
-  uint32_t target = 32 * 1024;
-  if (const char* v = getenv("LSW_GEMV_SLOT_KB")) { long x = atol(v); if (x >= 4 && x <= 96) target = (uint32_t)x * 1024; }
-  uint32_t slot = 0, xcap = 0;
-  int64_t chunks = 0;
-  for (int g = 0; g < n_groups; ++g) {
-    TokGroup& t = groups[g];
-    int R = (int)(target / t.row_bytes);
-    if (R < 1) R = 1;
-    if (R > 8) R = 8;
-    t.R = R;
-    t.chunk_begin = chunks;
-    chunks += (t.rows + R - 1) / R;
-    const uint32_t sb = (uint32_t)R * t.row_bytes;
-    if (sb > slot) slot = sb;
-    const uint32_t xb = x_stage_bytes(t.row_bytes, bf16);
-    if (xb > xcap) xcap = xb;
-  }
-  slot = (slot + 127) & ~127u;
-  size_t budget = 220 * 1024;
-  if (const char* v = getenv("LSW_GEMV_SMEM_KB")) { long x = atol(v); if (x >= 32 && x <= 224) budget = (size_t)x * 1024; }
-  int slots = budget > xcap ? (int)((budget - xcap) / slot) : 0;
-  if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
-  if (slots < 2) return cudaErrorNotSupported;
-  int grid = (int)(chunks < num_sms ? chunks : num_sms);
-  if (const char* v = getenv("LSW_GEMV_GRID")) { long x = atol(v); if (x >= 1 && x < grid) grid = (int)x; }
-  if (grid < 1) grid = 1;
-  cudaError_t e = cudaMalloc(&plan->d_groups, sizeof(TokGroup) * (size_t)n_groups);
-  if (e != cudaSuccess) return e;
-  e = cudaMemcpy(plan->d_groups, groups, sizeof(TokGroup) * (size_t)n_groups, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) { cudaFree(plan->d_groups); plan->d_groups = nullptr; return e; }
-  plan->n_groups = n_groups;
-  plan->total_chunks = chunks;
-  plan->slot_bytes = slot;
-  plan->x_cap = xcap;
-  plan->slots = slots;
-  plan->grid = grid;
-  plan->smem = (size_t)xcap + (size_t)slots * slot;
-  if (const char* v = getenv("LSW_GEMV_TOKEN_FLAGS")) plan->flags = atoi(v);
-  return cudaSuccess;
-}
-
-void tok_plan_destroy(TokPlan* plan) {
-  if (plan->d_groups) cudaFree(plan->d_groups);
-  *plan = TokPlan{};
-}
-
-cudaError_t launch_gemv_token(const TokPlan& plan, const void* xs, float* ys, unsigned long long* done,
-                              unsigned long long base, int32_t dtype, cudaStream_t s) {
-  const bool bf16 = dtype == LSW_BF16;
-  auto fn = bf16 ? gemv_token_kernel<true> : gemv_token_kernel<false>;
-  static size_t smem_set[2] = {0, 0};
-  if (plan.smem > smem_set[bf16]) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
-    if (e != cudaSuccess) return e;
-    smem_set[bf16] = plan.smem;
-  }
-  // The group counter needs every CTA resident at once: one CTA per SM, grid
-  // <= SM count, and a cooperative launch so the driver guarantees it.
-  cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(plan.grid);
-  lc.blockDim = dim3(kBulkThreads);
-  lc.dynamicSmemBytes = plan.smem;
-  lc.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  lc.attrs = at;
-  lc.numAttrs = 2;
-  static int use_pdl = 1;                 // dropped once if the driver refuses cooperative + PDL
-  lc.numAttrs = use_pdl ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&lc, fn, (const TokGroup*)plan.d_groups, plan.n_groups, plan.total_chunks,
-                                     (const uint8_t*)xs, ys, plan.slots, plan.slot_bytes, plan.x_cap, done, base, plan.flags);
-  if (e != cudaSuccess && use_pdl) {
-    (void)cudaGetLastError();
-    use_pdl = 0;
-    lc.numAttrs = 1;
-    e = cudaLaunchKernelEx(&lc, fn, (const TokGroup*)plan.d_groups, plan.n_groups, plan.total_chunks,
-                           (const uint8_t*)xs, ys, plan.slots, plan.slot_bytes, plan.x_cap, done, base, plan.flags);
-  }
-  return e;
-}
-
-static int gemv_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("LSW_GEMV");
-    v = (e && e[0] == 'l') ? 0 : 1;       // "ldg" -> warp-per-row LDG kernel; default bulk
-  }
-  return v;
-}
-
-cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w,
+cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, const GemvTune& t, cudaStream_t s, bool early_w,
                         GemvLora* lora) {
   const bool bf16 = dtype == LSW_BF16;
-  if (gemv_variant() == 1) {
+  const int num_sms = t.grid_cap;
+  if (!t.ldg) {
     // bulk-copy throughput grows with bytes per operation (scripts/membench.cu:
-    // 4 KB ops 2.6 TB/s ... 32 KB ops 7.3 TB/s): move R >= 1 rows per op, ~32 KB
-    // x staged as raw bf16 (default) or widened to fp32 planes (LSW_GEMV_XF32=1)
-    static const bool xb = getenv("LSW_GEMV_XF32") == nullptr;
+    // 4 KB ops 2.6 TB/s ... 32 KB ops 7.3 TB/s): move R >= 1 rows per op, ~32 KB;
+    // x staged in shared memory as raw bf16 / fp32
     const uint32_t row_bytes = (uint32_t)(p.d_in * (bf16 ? 2 : 4));
-    const uint32_t x_bytes = x_stage_bytes(row_bytes, bf16 && !xb);
-    uint32_t op_bytes = 32768;                       // tuning: LSW_GEMV_OP_KB
-    if (const char* v = getenv("LSW_GEMV_OP_KB")) { long x = atol(v); if (x >= 4 && x <= 96) op_bytes = (uint32_t)x * 1024; }
-    int R = (int)(op_bytes / row_bytes);
+    const uint32_t x_bytes = x_stage_bytes(row_bytes, false);
+    int R = (int)(t.op_bytes / row_bytes);
     if (R < 1) R = 1;
     if (R > 16) R = 16;
     const size_t slot_bytes = (size_t)R * row_bytes;
@@ -837,18 +577,15 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
     // 72 KB 3.49 ms -- a deep ring per SM beats letting the next GEMV's CTA
     // co-reside under PDL; with the bf16 x staging (same box, 2 runs each):
     // 220 KB 2.172, 176 KB 2.164, 144 KB 2.32, 112 KB 2.53 ms -- five 32-KB
-    // slots in flight rather than six.  LSW_GEMV_SMEM_KB overrides.
+    // slots in flight rather than six.
     // (the unmerged form keeps ~12 KB of static shared memory: u, row sums, terms)
-    size_t budget = lora ? 208 * 1024 : 176 * 1024;
-    if (const char* v = getenv("LSW_GEMV_SMEM_KB")) { long x = atol(v); if (x >= 32 && x <= 224) budget = (size_t)x * 1024; }
-    int slots = (int)((budget - x_bytes) / slot_bytes);
+    const size_t budget = lora ? t.budget_lora : t.budget;
+    int slots = budget > x_bytes ? (int)((budget - x_bytes) / slot_bytes) : 0;
     if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
     if (slots >= 2) {
       const size_t smem = x_bytes + (size_t)slots * slot_bytes;
-      auto fn = lora ? (bf16 ? (xb ? gemv_bulk_kernel<true, true, true> : gemv_bulk_kernel<true, true, false>)
-                             : gemv_bulk_kernel<false, true, false>)
-                     : (bf16 ? (xb ? gemv_bulk_kernel<true, false, true> : gemv_bulk_kernel<true, false, false>)
-                             : gemv_bulk_kernel<false, false, false>);
+      auto fn = lora ? (bf16 ? gemv_bulk_kernel<true, true, true> : gemv_bulk_kernel<false, true, false>)
+                     : (bf16 ? gemv_bulk_kernel<true, false, true> : gemv_bulk_kernel<false, false, false>);
       static size_t smem_set[2][2] = {{0, 0}, {0, 0}};   // attribute set once per kernel (not per launch)
       if (smem > smem_set[lora != nullptr][bf16]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -868,8 +605,7 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStr
       lc.attrs = at;
       lc.numAttrs = 1;
       const GemvLora none{};
-      static const int probe = getenv("LSW_GEMV_PROBE") ? atoi(getenv("LSW_GEMV_PROBE")) : 0;   // tuning only
-      return cudaLaunchKernelEx(&lc, fn, p, slots, R, (int32_t)((early_w || lora ? 1 : 0) | (probe ? 2 : 0)),
+      return cudaLaunchKernelEx(&lc, fn, p, slots, R, (int32_t)((early_w || lora ? 1 : 0) | (t.probe ? 2 : 0)),
                                 lora ? *lora : none);
     }
   }

@@ -4,6 +4,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -39,7 +41,32 @@ const int kGroupSize[LSW_NGROUP] = {3, 1, 2, 1};
 
 constexpr int kSimtTM = 8, kSimtTN = 256;   // must match switch_simt.cu
 
+// lsw_debug_set_option's table (process-wide; read at lsw_create)
+std::mutex g_opt_mu;
+std::map<std::string, std::string> g_opts;
+
 }  // namespace
+
+namespace lsw {
+const char* opt_str(const char* key) {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  auto it = g_opts.find(key);
+  // the map's nodes are stable until the key is set again (not while a ctx is created)
+  return it == g_opts.end() ? nullptr : it->second.c_str();
+}
+long opt_int(const char* key, long dflt) {
+  const char* v = opt_str(key);
+  return v ? strtol(v, nullptr, 10) : dflt;
+}
+long probe_int(const char* key) {
+#ifdef LSW_TUNING
+  return opt_int(key, 0);
+#else
+  (void)key;
+  return 0;
+#endif
+}
+}  // namespace lsw
 
 struct lsw_ctx {
   lsw_config cfg;
@@ -47,7 +74,7 @@ struct lsw_ctx {
   const void* router_w = nullptr;
   int device = 0;
   int num_sms = 148;
-  int gemv_sms = 148;                   // GEMV grid cap: num_sms (testing knob LSW_GEMV_GRID, read at create)
+  GemvTune gemv;                        // GEMV launch plan (grid cap = num_sms unless the gemv_grid option)
   int impl = LSW_IMPL_SIMT;
   SwitchParams simt_geom{};     // tile table for the SIMT kernel
   TcPlan* tc = nullptr;
@@ -58,11 +85,10 @@ struct lsw_ctx {
   int64_t xs_elems = 0, ys_elems = 0;
   int64_t x_off[LSW_NGROUP] = {}, y_off[LSW_NGROUP] = {};   // per-layer offsets
   int64_t x_per_layer = 0, y_per_layer = 0;
-  TokPlan tok{};                        // whole-token GEMV (tp_size == 1), else empty
   bool has_pristine = false;            // lsw_attach_pristine called (RESTORE mode available)
   float* lora_u = nullptr;              // unmerged decode: LoRA-down products scratch
   bool fused_ready = false;             // fused switch + decode segment table built
-  unsigned long long tok_base = 0;      // DevState::tok_done before the next token launch
+  int unmerged_flags = 0;               // tuning builds only (probe unmerged_flags)
   // staging for lsw_decode_token_host
   void* st_x1 = nullptr;
   void* st_xs = nullptr;
@@ -162,8 +188,13 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
   cudaError_t e = cudaGetDevice(&ctx->device);
   if (e != cudaSuccess) { delete ctx; return cuda_fail(e, "lsw_create: cudaGetDevice"); }
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
-  ctx->gemv_sms = ctx->num_sms;
-  if (const char* v = getenv("LSW_GEMV_GRID")) { int x = atoi(v); if (x >= 1 && x < ctx->gemv_sms) ctx->gemv_sms = x; }
+  ctx->gemv.grid_cap = ctx->num_sms;
+  { const long x = opt_int("gemv_grid", 0); if (x >= 1 && x < ctx->gemv.grid_cap) ctx->gemv.grid_cap = (int)x; }
+  { const long x = opt_int("gemv_op_kb", 0); if (x >= 4 && x <= 96) ctx->gemv.op_bytes = (uint32_t)x * 1024; }
+  { const long x = opt_int("gemv_smem_kb", 0); if (x >= 32 && x <= 224) ctx->gemv.budget = ctx->gemv.budget_lora = (size_t)x * 1024; }
+  { const char* v = opt_str("gemv"); ctx->gemv.ldg = v && strcmp(v, "ldg") == 0; }
+  ctx->gemv.probe = (int)probe_int("gemv_probe");
+  ctx->unmerged_flags = (int)probe_int("unmerged_flags");
   e = cudaMalloc(&ctx->d_state, sizeof(DevState));
   if (e != cudaSuccess) { delete ctx; return fail(LSW_E_OOM, "lsw_create: cudaMalloc(state) failed"); }
   e = cudaMemset(ctx->d_state, 0, sizeof(DevState));
@@ -191,31 +222,6 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
   ctx->y_per_layer = yo;
   ctx->xs_elems = xo * c.n_layers;
   ctx->ys_elems = yo * c.n_layers;
-  // whole-token GEMV plan (single GPU; TP keeps per-group launches for the all-reduce)
-  const char* tv = getenv("LSW_GEMV_TOKEN");
-  if (c.tp_size == 1 && tv && tv[0] == '1') {
-    std::vector<TokGroup> tg((size_t)c.n_layers * LSW_NGROUP);
-    for (int l = 0; l < c.n_layers; ++l)
-      for (int g = 0; g < LSW_NGROUP; ++g) {
-        TokGroup& t = tg[(size_t)l * LSW_NGROUP + g];
-        memset(&t, 0, sizeof(t));
-        int64_t rows = 0;
-        for (int i = 0; i < kGroupSize[g]; ++i) {
-          const lsw_kind_desc& d = kinds[kGroupKinds[g][i]];
-          t.W[i] = (const uint8_t*)d.W + (size_t)l * d.d_out * d.d_in * esize(ctx);
-          t.row_begin[i] = rows;
-          rows += d.d_out;
-        }
-        t.n_sites = kGroupSize[g];
-        t.rows = rows;
-        t.row_bytes = (uint32_t)(kinds[kGroupKinds[g][0]].d_in * esize(ctx));
-        t.x_off = l * ctx->x_per_layer + ctx->x_off[g];
-        t.y_off = l * ctx->y_per_layer + ctx->y_off[g];
-      }
-    e = tok_plan_create(&ctx->tok, tg.data(), (int32_t)tg.size(), ctx->num_sms, c.dtype == LSW_BF16);
-    if (e == cudaErrorMemoryAllocation) { lsw_destroy(ctx); return fail(LSW_E_OOM, "lsw_create: token GEMV table"); }
-    if (e != cudaSuccess) { (void)cudaGetLastError(); ctx->tok = TokPlan{}; }   // per-group launches instead
-  }
   *out = ctx;
   return LSW_OK;
 }
@@ -225,7 +231,6 @@ lsw_status lsw_destroy(lsw_ctx* ctx) {
   cudaDeviceSynchronize();
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->tc) tc_plan_destroy(ctx->tc);
-  tok_plan_destroy(&ctx->tok);
   cudaFree(ctx->lora_u);
   cudaFree(ctx->d_state);
   cudaFree(ctx->st_x1);
@@ -377,7 +382,7 @@ static lsw_status gemv_sites(lsw_ctx* ctx, int layer, const int* kinds, int n, c
   const bool allreduce = ctx->cfg.tp_size > 1 && ctx->kinds[kinds[0]].row_parallel;
   if (allreduce && !ctx->comm)
     return fail(LSW_E_NCCL, "%s: tp_size=%d but no NCCL communicator attached", who, ctx->cfg.tp_size);
-  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->gemv_sms, s, early_w);
+  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->gemv, s, early_w);
   if (e != cudaSuccess) return cuda_fail(e, "decode GEMV launch");
   ++ctx->launches;
   // Row-parallel kinds under TP: partial sums -> allreduce.
@@ -426,12 +431,14 @@ static lsw_status gemv_unmerged(lsw_ctx* ctx, int layer, int group, const void* 
   L.scale = ctx->cfg.alpha / (float)ctx->cfg.rank;
   L.k = ctx->cfg.top_k;
   L.r = ctx->cfg.rank;
+  L.n_experts = ctx->cfg.n_experts;
+  L.err = &ctx->d_state->err;
   L.u = ctx->lora_u;
   L.arrive = &ctx->d_state->lora_arrive;
   L.depart = &ctx->d_state->lora_depart;
-  if (const char* v = getenv("LSW_UNMERGED_FLAGS")) L.flags = atoi(v);   // tuning probes only
-  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->gemv_sms, s, early_w, &L);
-  if (e == cudaErrorNotSupported) return fail(LSW_E_UNSUPPORTED, "%s: needs the bulk GEMV (LSW_GEMV=ldg set)", who);
+  L.flags = ctx->unmerged_flags;
+  cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->gemv, s, early_w, &L);
+  if (e == cudaErrorNotSupported) return fail(LSW_E_UNSUPPORTED, "%s: needs the bulk GEMV (option gemv=ldg set)", who);
   if (e != cudaSuccess) return cuda_fail(e, "unmerged decode GEMV launch");
   ctx->launches += 1;                       // LoRA-down, GEMV and LoRA-up in one launch
   return LSW_OK;
@@ -465,7 +472,7 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
   }
   // packed fp32 B of every layer, per kind, built on the first call (stream-ordered):
   // the LoRA-up step becomes one GEMM per site (LSW_PREFILL_GATHER=1: the gather kernel)
-  static const bool gather = getenv("LSW_PREFILL_GATHER") != nullptr;
+  const bool gather = opt_int("prefill_gather", 0) != 0;
   if (!gather) {
     const int nr = ctx->cfg.n_experts * ctx->cfg.rank;
     for (int k = 0; k < LSW_NKIND; ++k) {
@@ -480,6 +487,9 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
         if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: pack");
         ++ctx->launches;
       }
+      // built once for the ctx's lifetime: finished before any stream may read it
+      cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+      if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: pack");
     }
   }
   const size_t es = esize(ctx);
@@ -523,22 +533,6 @@ lsw_status lsw_decode_all_layers_unmerged(lsw_ctx* ctx, const void* xs, float* y
   if (!ctx || !xs || !ys || !idx || !gate) return fail(LSW_E_ARG, "lsw_decode_all_layers_unmerged: null argument");
   if (ctx->merged) return fail(LSW_E_STATE, "lsw_decode_all_layers_unmerged: the ctx is merged");
   const size_t es = esize(ctx);
-  // opt-in (LSW_UNMERGED_PREFETCH=1): measured 3.65 vs 3.56 ms per 7B token
-  // without -- the LoRA-down latency is not what bounds this path
-  static const bool prefetch = getenv("LSW_UNMERGED_PREFETCH") && getenv("LSW_UNMERGED_PREFETCH")[0] == '1';
-  if (prefetch) {
-    LoraPrefetch q{};
-    for (int k = 0; k < LSW_NKIND; ++k) { q.A[k] = ctx->kinds[k].A; q.d_in[k] = ctx->kinds[k].d_in; }
-    q.n_layers = ctx->cfg.n_layers;
-    q.n_experts = ctx->cfg.n_experts;
-    q.r = ctx->cfg.rank;
-    q.k = ctx->cfg.top_k;
-    q.es = (int32_t)es;
-    q.idx = idx;
-    cudaError_t e = launch_lora_prefetch(q, (cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_all_layers_unmerged: prefetch");
-    ++ctx->launches;
-  }
   for (int l = 0; l < ctx->cfg.n_layers; ++l)
     for (int g = 0; g < LSW_NGROUP; ++g) {
       const uint8_t* xp = (const uint8_t*)xs + (size_t)(l * ctx->x_per_layer + ctx->x_off[g]) * es;
@@ -578,14 +572,6 @@ lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs, float*
 lsw_status lsw_decode_all_layers(lsw_ctx* ctx, const void* xs, float* ys, void* stream) {
   if (!ctx || !xs || !ys) return fail(LSW_E_ARG, "lsw_decode_all_layers: null argument");
   if (reinterpret_cast<uintptr_t>(xs) % 16) return fail(LSW_E_ARG, "lsw_decode_all_layers: xs not 16-byte aligned");
-  if (ctx->tok.d_groups) {
-    cudaError_t e = launch_gemv_token(ctx->tok, xs, ys, &ctx->d_state->tok_done, ctx->tok_base, ctx->cfg.dtype,
-                                      (cudaStream_t)stream);
-    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_all_layers: token GEMV launch");
-    ctx->tok_base += (unsigned long long)ctx->tok.n_groups * (unsigned long long)ctx->tok.grid;
-    ++ctx->launches;
-    return LSW_OK;
-  }
   const size_t es = esize(ctx);
   for (int l = 0; l < ctx->cfg.n_layers; ++l)
     for (int g = 0; g < LSW_NGROUP; ++g) {
@@ -645,12 +631,11 @@ lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_
         cudaMalloc(&ctx->st_gate, LSW_MAX_TOPK * sizeof(float)) != cudaSuccess)
       return fail(LSW_E_OOM, "lsw_decode_token_host: staging allocation failed");
   }
-  // Copies overlap the token (per-group GEMV path): x1 goes first on the
-  // token's stream (the router needs it); the GEMV inputs on a side stream
-  // while the router and the switch run; each layer's outputs go back on the
-  // side stream as soon as that layer's GEMVs are done.
-  const bool overlap = !ctx->tok.d_groups;
-  if (overlap && !ctx->st_side) {
+  // Copies overlap the token: x1 goes first on the token's stream (the router
+  // needs it); the GEMV inputs on a side stream while the router and the
+  // switch run; each layer's outputs go back on the side stream as soon as
+  // that layer's GEMVs are done.
+  if (!ctx->st_side) {
     if (cudaStreamCreateWithFlags(&ctx->st_side, cudaStreamNonBlocking) != cudaSuccess)
       return fail(LSW_E_CUDA, "lsw_decode_token_host: side stream");
     ctx->st_ev.resize(1 + ctx->cfg.n_layers);
@@ -660,47 +645,39 @@ lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_
   }
   cudaError_t e = cudaMemcpyAsync(ctx->st_x1, x1_h, ctx->cfg.d_model * es, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: H2D");
-  if (!overlap) {
-    e = cudaMemcpyAsync(ctx->st_xs, xs_h, ctx->xs_elems * es, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: H2D");
-    lsw_status st = lsw_decode_token(ctx, ctx->st_x1, ctx->st_xs, ctx->st_ys, ctx->st_idx, ctx->st_gate, stream);
-    if (st != LSW_OK) return st;
-    e = cudaMemcpyAsync(ys_h, ctx->st_ys, ctx->ys_elems * sizeof(float), cudaMemcpyDeviceToHost, s);
-  } else {
-    cudaStream_t side = ctx->st_side;
-    // the side stream starts after everything already on `s` (the previous
-    // token's readers of st_xs / st_ys are done)
-    e = cudaEventRecord(ctx->st_ev[0], s);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->st_ev[0], 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->st_xs, xs_h, ctx->xs_elems * es, cudaMemcpyHostToDevice, side);
-    if (e == cudaSuccess) e = cudaEventRecord(ctx->st_ev[0], side);
-    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: H2D");
-    lsw_status st = lsw_router_topk(ctx, ctx->st_x1, ctx->st_idx, ctx->st_gate, stream);          // Alg. 1 l.1
-    if (st != LSW_OK) return st;
-    st = lsw_merge_all_layers(ctx, ctx->st_idx, ctx->st_gate, stream);                          // l.2-4
-    if (st != LSW_OK) return st;
-    e = cudaStreamWaitEvent(s, ctx->st_ev[0], 0);                                                 // xs landed
-    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: wait");
-    for (int l = 0; l < ctx->cfg.n_layers; ++l) {                                                // l.5
-      for (int g = 0; g < LSW_NGROUP; ++g) {
-        const uint8_t* xp = (const uint8_t*)ctx->st_xs + (size_t)(l * ctx->x_per_layer + ctx->x_off[g]) * es;
-        float* yp = ctx->st_ys + l * ctx->y_per_layer + ctx->y_off[g];
-        st = gemv_sites(ctx, l, kGroupKinds[g], kGroupSize[g], xp, yp, s, "lsw_decode_token_host",
-                        /*early_w=*/l > 0 || g > 0);
-        if (st != LSW_OK) return st;
-      }
-      e = cudaEventRecord(ctx->st_ev[1 + l], s);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->st_ev[1 + l], 0);
-      if (e == cudaSuccess)
-        e = cudaMemcpyAsync(ys_h + l * ctx->y_per_layer, ctx->st_ys + l * ctx->y_per_layer,
-                            ctx->y_per_layer * sizeof(float), cudaMemcpyDeviceToHost, side);
-      if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: D2H");
+  cudaStream_t side = ctx->st_side;
+  // the side stream starts after everything already on `s` (the previous
+  // token's readers of st_xs / st_ys are done)
+  e = cudaEventRecord(ctx->st_ev[0], s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->st_ev[0], 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->st_xs, xs_h, ctx->xs_elems * es, cudaMemcpyHostToDevice, side);
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->st_ev[0], side);
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: H2D");
+  lsw_status st = lsw_router_topk(ctx, ctx->st_x1, ctx->st_idx, ctx->st_gate, stream);          // Alg. 1 l.1
+  if (st != LSW_OK) return st;
+  st = lsw_merge_all_layers(ctx, ctx->st_idx, ctx->st_gate, stream);                          // l.2-4
+  if (st != LSW_OK) return st;
+  e = cudaStreamWaitEvent(s, ctx->st_ev[0], 0);                                                 // xs landed
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: wait");
+  for (int l = 0; l < ctx->cfg.n_layers; ++l) {                                                // l.5
+    for (int g = 0; g < LSW_NGROUP; ++g) {
+      const uint8_t* xp = (const uint8_t*)ctx->st_xs + (size_t)(l * ctx->x_per_layer + ctx->x_off[g]) * es;
+      float* yp = ctx->st_ys + l * ctx->y_per_layer + ctx->y_off[g];
+      st = gemv_sites(ctx, l, kGroupKinds[g], kGroupSize[g], xp, yp, s, "lsw_decode_token_host",
+                      /*early_w=*/l > 0 || g > 0);
+      if (st != LSW_OK) return st;
     }
+    e = cudaEventRecord(ctx->st_ev[1 + l], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ctx->st_ev[1 + l], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ys_h + l * ctx->y_per_layer, ctx->st_ys + l * ctx->y_per_layer,
+                          ctx->y_per_layer * sizeof(float), cudaMemcpyDeviceToHost, side);
+    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: D2H");
   }
   if (e == cudaSuccess) e = cudaMemcpyAsync(idx_h, ctx->st_idx, ctx->cfg.top_k * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(gate_h, ctx->st_gate, ctx->cfg.top_k * sizeof(float), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e == cudaSuccess && overlap) e = cudaStreamSynchronize(ctx->st_side);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st_side);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: D2H");
   return LSW_OK;
 }
@@ -745,10 +722,11 @@ lsw_status lsw_debug_merge_per_matrix(lsw_ctx* ctx, const int32_t* idx, const fl
   return LSW_OK;
 }
 
-lsw_status lsw_debug_switch_trace(lsw_ctx* ctx, uint64_t* host_out, int64_t n, int64_t* n_out) {
-  if (!ctx || !host_out || !n_out) return fail(LSW_E_ARG, "lsw_debug_switch_trace: null argument");
-  cudaDeviceSynchronize();
-  *n_out = ctx->tc ? tc_plan_trace(ctx->tc, host_out, n) : 0;
+lsw_status lsw_debug_set_option(const char* key, const char* value) {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  if (!key) { g_opts.clear(); return LSW_OK; }
+  if (!value) g_opts.erase(key);
+  else g_opts[key] = value;
   return LSW_OK;
 }
 

@@ -10,6 +10,14 @@
 
 namespace lsw {
 
+// Variant and tuning options (include/lsw_debug.h lsw_debug_set_option): set
+// explicitly by the caller, read when a ctx is created; the library never
+// reads the environment.  Options that produce wrong results on purpose
+// (measurement probes) take effect only in a -DLSW_TUNING build.
+const char* opt_str(const char* key);      // nullptr if unset
+long opt_int(const char* key, long dflt);  // dflt if unset
+long probe_int(const char* key);           // 0 unless built with LSW_TUNING
+
 constexpr int kMaxTerms = 2 * LSW_MAX_TOPK;   // |S_t u S_{t-1}| <= 2k
 
 // Switch modes (K1).  MERGE: Eq. 6; SWITCH: Eq. 10; UNMERGE: Eq. 7;
@@ -20,14 +28,18 @@ enum SwitchMode : int32_t { MODE_MERGE = 0, MODE_SWITCH = 1, MODE_UNMERGE = 2, M
 // Ctx-owned device state.  slot[parity] holds the merged decision; a switch
 // pass writes the new decision into slot[parity^1] and the LAST CTA to finish
 // flips parity (every CTA has read slot[parity] before it counts itself done).
+// `merged` is the device's own record of the state machine: set by
+// a merge / switch / restore pass that ran, cleared by an unmerge; a pass whose
+// decision was rejected (latched error) leaves it unchanged.  SWITCH and
+// UNMERGE subtract the slot's decision only while it is set, so a rejected
+// merge can never make a later pass subtract a decision W does not contain.
 struct DevState {
   int32_t parity;
   uint32_t done;
   int32_t err;        // first latched LSW_DEV_* code
-  int32_t pad;
+  int32_t merged;     // 1: slot[parity] is merged into W
   int32_t idx[2][LSW_MAX_TOPK];
   float g[2][LSW_MAX_TOPK];
-  unsigned long long tok_done;   // group-completion counter of the whole-token GEMV (gemv.cu)
   uint32_t lora_arrive;          // unmerged GEMV: LoRA-down products published in this launch
   uint32_t lora_depart;          // unmerged GEMV: CTAs done (the last one resets both)
 };
@@ -71,7 +83,8 @@ __device__ __forceinline__ void build_coefs(const SwitchParams& p, int32_t parit
   int32_t ci[LSW_MAX_TOPK], pi[LSW_MAX_TOPK];
   float cg[LSW_MAX_TOPK], pg[LSW_MAX_TOPK];
   const bool has_cur = p.mode != MODE_UNMERGE;
-  const bool has_prev = p.mode == MODE_SWITCH || p.mode == MODE_UNMERGE;
+  const bool has_prev = (p.mode == MODE_SWITCH || p.mode == MODE_UNMERGE) &&
+                        *reinterpret_cast<volatile const int32_t*>(&p.state->merged) != 0;
   for (int j = 0; j < k; ++j) {
     if (has_cur) {
       ci[j] = p.cur_idx[j];
@@ -115,11 +128,14 @@ __device__ __forceinline__ void finish_pass(const SwitchParams& p, int32_t parit
   __threadfence();
   const uint32_t prev = atomicAdd(&p.state->done, 1u);
   if (prev == gridDim.x - 1) {
+    volatile DevState* s = p.state;
     if (cf.bad) {
-      atomicCAS(&p.state->err, 0, cf.bad);
+      atomicCAS(&p.state->err, 0, cf.bad);       // state unchanged
     } else if (p.mode != MODE_UNMERGE) {
-      volatile DevState* s = p.state;
       s->parity = parity ^ 1;
+      s->merged = 1;
+    } else {
+      s->merged = 0;                             // state none: the slot is stale
     }
     p.state->done = 0;
     __threadfence();
@@ -167,56 +183,27 @@ struct GemvLora {
   const int32_t* idx;        // [k] device
   const float* gate;         // [k] device
   float scale;               // alpha / r
-  int32_t k, r;
+  int32_t k, r, n_experts;
   float* u;                  // scratch [n_sites * k * r] fp32
+  int32_t* err;              // DevState::err: an invalid decision latches LSW_DEV_* and drops the LoRA terms
   uint32_t* arrive;          // DevState::lora_arrive / lora_depart (zero between launches)
   uint32_t* depart;
-  int32_t flags;             // tuning probe (LSW_UNMERGED_FLAGS): 4 = no LoRA-up term (results wrong)
+  int32_t flags;             // tuning builds only (probe unmerged_flags): 4 = no LoRA-up term (results wrong)
+};
+// Launch plan of the decode GEMV (gemv.cu), fixed per ctx at lsw_create.
+struct GemvTune {
+  int grid_cap = 148;               // CTAs at most (the SM count)
+  uint32_t op_bytes = 32768;        // bytes per bulk copy (R rows of ~32 KB)
+  size_t budget = 176 * 1024;       // ring + x staging, merged-weight GEMV
+  size_t budget_lora = 208 * 1024;  // same, unmerged form
+  int probe = 0;                    // tuning builds only: 1 = stream W without the dot products
+  bool ldg = false;                 // variant option gemv=ldg: the warp-per-row LDG kernel
 };
 // early_w: the previous launch on `s` was a GEMV (W may be prefetched before
-// griddepcontrol.wait; see gemv.cu).  lora: null for the merged-weight GEMV.
-// Unmerged decode: pull the selected experts' LoRA-down rows of every layer
-// into L2 at the start of the token (the pre-gated decision is known for all).
-struct LoraPrefetch {
-  const void* A[LSW_NKIND];   // [L, N, r, d_in] per kind
-  int64_t d_in[LSW_NKIND];
-  int32_t n_layers, n_experts, r, k, es;
-  const int32_t* idx;         // [k] device
-};
-cudaError_t launch_lora_prefetch(const LoraPrefetch& q, cudaStream_t s);
-// lora: the unmerged form (LoRA-down and LoRA-up inside the same launch).
-cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, int num_sms, cudaStream_t s, bool early_w = false,
+// griddepcontrol.wait; see gemv.cu).  lora: null for the merged-weight GEMV,
+// else the unmerged form (LoRA-down and LoRA-up inside the same launch).
+cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, const GemvTune& t, cudaStream_t s, bool early_w = false,
                         GemvLora* lora = nullptr);
-
-// Whole-token decode GEMV (gemv.cu, K4b): every group of every layer in ONE
-// persistent launch.  The W stream runs ahead across group boundaries; group
-// g's x is read only after every CTA has finished group g-1 (a device-wide
-// counter), so the launch keeps the layer-by-layer dependency of a decoder.
-struct TokGroup {
-  const void* W[3];         // site matrices [d_out, d_in] of this (layer, group)
-  int64_t row_begin[3];     // first output row of each site (row_begin[0] = 0)
-  int64_t rows;             // group output rows (sum of the sites' d_out)
-  int64_t x_off, y_off;     // offsets (elements) into the packed xs / ys
-  int64_t chunk_begin;      // first global chunk of this group (filled by the planner)
-  int32_t n_sites, R;       // R: rows per chunk (filled by the planner)
-  uint32_t row_bytes, pad;
-};
-struct TokPlan {
-  TokGroup* d_groups = nullptr;   // device copy of the table
-  int32_t n_groups = 0;
-  int64_t total_chunks = 0;
-  uint32_t slot_bytes = 0, x_cap = 0;
-  int32_t slots = 0, grid = 0;
-  int32_t flags = 0;              // tuning only (LSW_GEMV_TOKEN_FLAGS): bit 0 = skip the group wait,
-                                  // bit 1 = skip the dot products (stream-only probe)
-  size_t smem = 0;
-};
-// groups: host table with W/row_begin/rows/x_off/y_off/n_sites/row_bytes set.
-cudaError_t tok_plan_create(TokPlan* plan, TokGroup* groups, int32_t n_groups, int num_sms, bool bf16);
-void tok_plan_destroy(TokPlan* plan);
-// done: DevState::tok_done; base: its value when this launch starts.
-cudaError_t launch_gemv_token(const TokPlan& plan, const void* xs, float* ys, unsigned long long* done,
-                              unsigned long long base, int32_t dtype, cudaStream_t s);
 
 // Unmerged prefill of one group for T tokens (prefill.cu).
 struct PrefillParams {
@@ -240,7 +227,7 @@ cudaError_t launch_prefill(const PrefillParams& P, int32_t dtype, void* cublas_h
 cudaError_t prefill_cublas_create(void** handle);
 void prefill_cublas_destroy(void* handle);
 
-// Tensor-core switch (switch_tc.cu).
+// Tensor-core switch (switch_tc_dispatch.cu / switch_tc_fc.cu).
 struct TcPlan;   // opaque: packed operands + TMA descriptors
 cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, const char** why);
 void tc_plan_destroy(TcPlan* plan);
@@ -252,13 +239,12 @@ int64_t tc_plan_tiles(const TcPlan* plan);
 cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, int64_t t0 = 0,
                              int64_t t_count = 0);
 int64_t tc_plan_matrix_tiles(const TcPlan* plan, int kind, int layer, int64_t* t0);   // tiles of one matrix
-// Fused switch + decode (v1 kernel only, else cudaErrorNotSupported)
+// Fused switch + decode (the fold mode only, else cudaErrorNotSupported)
 cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
                               int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]);
 cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, const void* xs,
                                    float* ys);
-int64_t tc_plan_trace(const TcPlan* plan, uint64_t* host, int64_t n);   // tuning trace (lsw_debug.h)
-int tc_plan_kernel(const TcPlan* plan);   // 1: v1 (switch_tc.cu), 2: term groups (switch_tc_tg.cu)
+int tc_plan_kernel(const TcPlan* plan);   // 3: fc fold, 4: fc per-term, 5: fc per-term with B per unit
 // RESTORE source: encode tensor maps over geom.kind[k].P (lsw_attach_pristine)
 cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
 

@@ -75,6 +75,10 @@ struct Geom {
                                         //    accumulator of 128 columns, kPtGroup terms per commit
   int32_t acc_bufs;                     // TMEM accumulator buffers of acc_cols columns
   uint32_t acc_cols;
+  int32_t bu;                           // per-term mode with the B slices staged per unit (next to
+                                        //    the unit's A^T slices) instead of per strip: the plan
+                                        //    when a whole strip of 2k raw B slices does not fit
+                                        //    (r = 64, k = 4: 128 KB)
 };
 
 // Fused switch + decode: one segment per (layer, GEMV group),
@@ -100,7 +104,8 @@ struct TcPlan {
   int32_t n_segs = 0;
   int64_t fused_tiles = 0;
   int32_t chunk = 48;
-  int32_t probe = 0;          // tuning only (LSW_TC_PROBE=1): W stream alone, W written back unchanged
+  int32_t probe = 0;          // tuning builds only (tc_probe=1): W stream alone, W written back unchanged
+  int32_t fused_probe = 0;    // tuning builds only (fc_fused_probe)
   void* packed_At[LSW_NKIND] = {};
   void* packed_B[LSW_NKIND] = {};
   int64_t bytes = 0;
@@ -420,7 +425,10 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
   const TileKinds& tk = g.tk;
   const uint32_t tmem_base = s_tmem_base;
 
-  if (nt > 0) {
+  // Nothing to add (nt == 0: the new decision equals the merged one, R12, or
+  // the decision was rejected): the plain pass is a no-op; the fused pass still
+  // streams W (unchanged, not stored back) and computes its GEMV outputs.
+  if (nt > 0 || kF) {
     if (warp == 0) {
       // ============================ W producer =============================
       if (lane == 0) {
@@ -448,6 +456,11 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         Ring wring{0, 0, (uint32_t)g.w_stages};
         for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
           mbar_wait(smem_u32(&bar_wdone[wring.i]), wring.phase);     // epilogue wrote the tile
+          if (nt == 0) {                                             // fused, W unchanged: no store
+            mbar_arrive(smem_u32(&bar_wempty[wring.i]));
+            wring.next();
+            continue;
+          }
           uint8_t* wsrc = wst0 + (size_t)wring.i * (2 * kSubBytes);
           if (g.wrm)
             tma_store_4d(&maps.w[c.kd], smem_u32(wsrc), 0, c.cb * 2, c.rb * kTM, c.layer, pol_stream);
@@ -462,7 +475,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         }
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
-    } else if (warp == 3 && !(args.probe & 1)) {
+    } else if (warp == 3 && nt > 0 && !(args.probe & 1)) {
       if constexpr (kPT) {
         // per-term mode: raw B slices per strip and A^T slices per (tile, term
         // group), all by bulk copies completing on the consumers' barriers
@@ -474,7 +487,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           Ring bring{0, 0, (uint32_t)g.b_bufs};
           Ring aring{0, 0, (uint32_t)g.a_stages};
           for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
-            if (strip_id(c) != strip_prev) {
+            if (!g.bu && strip_id(c) != strip_prev) {
               if (strip_prev >= 0) bring.next();
               strip_prev = strip_id(c);
               mbar_wait(smem_u32(&bar_bempty[bring.i]), bring.phase ^ 1);
@@ -494,9 +507,15 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
               mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
               uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
               const uint32_t bar = smem_u32(&bar_afull[aring.i]);
-              mbar_expect_tx(bar, n_in * tb);
+              mbar_expect_tx(bar, (g.bu ? 2 : 1) * n_in * tb);
               for (int jj = 0; jj < n_in; ++jj)
                 bulk_load(smem_u32(adst + jj * tb), blk + (size_t)cf.e[j0 + jj] * kTN * rpe, tb, bar, pol_keep);
+              if (g.bu)                              // the unit's B slices of this strip, after its A^T slices
+                for (int jj = 0; jj < n_in; ++jj)
+                  bulk_load(smem_u32(adst + (kPtGroup + jj) * tb),
+                            g.Bp[c.kd] + (((size_t)c.layer * g.n_experts + cf.e[j0 + jj]) * g.dout_pad[c.kd] +
+                                          (size_t)c.rb * kTM) * rpe,
+                            tb, bar, pol_keep);
               aring.next();
             }
           }
@@ -553,7 +572,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         aring.next();
       }
       }  // !kPT
-    } else if (warp == 1 && !(args.probe & 1)) {
+    } else if (warp == 1 && nt > 0 && !(args.probe & 1)) {
       // ============================ MMA issuer ==============================
       // One chain per tile: for every term, the hi and lo parts times the A^T
       // slice, K = rp each in steps of 16, into the tile's single accumulator;
@@ -570,7 +589,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       Ring acc{0, 0, (uint32_t)g.acc_bufs};
       int64_t strip_prev = -1;
       for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
-        if (strip_id(c) != strip_prev) {
+        if (!g.bu && strip_id(c) != strip_prev) {
           if (strip_prev >= 0) {
             // every MMA of the previous strip is issued: its B buffer is free
             // once they complete -- released by a commit here, not after the
@@ -597,18 +616,20 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         if constexpr (kPT) {
           // per-term mode: kPtGroup terms per group, each into its own 128-column
           // accumulator of the group's TMEM buffer, one commit per group
-          const uint64_t b_desc = desc0 + (smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes) >> 4);
+          const uint64_t b_strip = desc0 + (smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes) >> 4);
           for (int j0 = 0; j0 < nt; j0 += kPtGroup) {
             const int n_in = nt - j0 < kPtGroup ? nt - j0 : kPtGroup;
             mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
             mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
             tc_fence_after();
             const uint64_t a_desc = desc0 + (smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes) >> 4);
+            // B of term j0 + jj: the strip buffer, or (bu) the unit's own slices
+            const uint64_t b_desc = g.bu ? a_desc + kPtGroup * term : b_strip + j0 * term;
             const uint32_t d = tmem_base + acc.i * g.acc_cols;
             if (elect_one()) {
               for (int jj = 0; jj < n_in; ++jj)
                 for (int kk = 0; kk < ksteps; ++kk)
-                  umma_f16(d + jj * kTN, b_desc + (j0 + jj) * term + kk * 2, a_desc + jj * term + kk * 2, idesc,
+                  umma_f16(d + jj * kTN, b_desc + jj * term + kk * 2, a_desc + jj * term + kk * 2, idesc,
                            kk > 0 ? 1u : 0u);
               umma_commit(smem_u32(&bar_accfull[acc.i]));
             }
@@ -737,19 +758,26 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           wring.next();
           continue;
         }
-        mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);      // the tile's MMAs are complete
-        if (releaser) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
-        aring.next();
-        tc_fence_after();
-        const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTN + half * kSubCols;
         uint32_t a[4][16];
+        if (nt > 0) {
+          mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);      // the tile's MMAs are complete
+          if (releaser) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
+          aring.next();
+          tc_fence_after();
+          const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTN + half * kSubCols;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) tmem_ld16(tm + q * 16, a[q]);
-        tmem_wait_ld();
-        tc_fence_before();                         // accumulator consumed -> MMA may reuse the buffer
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
-        acc.next();
+          for (int q = 0; q < 4; ++q) tmem_ld16(tm + q * 16, a[q]);
+          tmem_wait_ld();
+          tc_fence_before();                       // accumulator consumed -> MMA may reuse the buffer
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+          acc.next();
+        } else {                                   // fused, nothing to add: y from the unchanged W
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int v = 0; v < 16; ++v) a[q][v] = 0u;
+        }
         mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);      // W tile landed
         // default: two [128 rows][64 cols] boxes; wrm: one [128 rows][2 x 64 cols] box
         const int unit = g.wrm ? 2 * row + half : half * kTM + row;
@@ -855,13 +883,6 @@ static bool encode_any(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t
 
 static uint32_t align1k(uint32_t x) { return (x + 1023) & ~1023u; }
 
-// The tensor-core work of a tile relative to its HBM time: 2 * nt * rp / 16
-// MMAs of 128 x 128 x 16 (~35-55 ns each) against ~1.5 us of W traffic.
-int fc_mmas_per_tile(const SwitchParams& sp) {
-  const int rp = sp.rank <= 16 ? 16 : sp.rank <= 32 ? 32 : 64;
-  return 2 * (2 * sp.top_k) * rp / 16;
-}
-
 cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, const char** why, int pt) {
   *out = nullptr;
   int dev = 0, major = 0, minor = 0;
@@ -882,13 +903,13 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   const int mt = 2 * sp.top_k;
   // per-term mode (LSW_FC_PT=1, or chosen by the dispatcher): B raw, A units of
   // kPtGroup terms, TMEM buffers of kPtGroup x 128 columns
-  g.pt = pt;
-  if (const char* v = getenv("LSW_FC_PT")) g.pt = atoi(v) != 0;
+  g.pt = pt != 0;
+  g.bu = pt == 2;
   if (g.pt) {
     g.acc_cols = kPtGroup * kTN;
     g.acc_bufs = 512 / (int)g.acc_cols;
-    g.a_stage_bytes = align1k((uint32_t)kPtGroup * g.term_bytes);
-    g.b_buf_bytes = align1k((uint32_t)mt * g.term_bytes);
+    g.a_stage_bytes = align1k((uint32_t)(g.bu ? 2 : 1) * kPtGroup * g.term_bytes);
+    g.b_buf_bytes = g.bu ? 0 : align1k((uint32_t)mt * g.term_bytes);
   } else {
     g.acc_cols = kTN;
     g.acc_bufs = kAccBufs;
@@ -914,35 +935,36 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   struct Cand { int ws, bb; };
   const Cand cands[] = {{3, 2}, {3, 1}, {4, 2}, {4, 1}};
   const int u = g.pt ? (mt + kPtGroup - 1) / kPtGroup : 1;
-  int bb_env = 0, as_env = 0, ws_env = 0;
-  if (const char* v = getenv("LSW_FC_BBUFS")) bb_env = atoi(v);
-  if (const char* v = getenv("LSW_FC_ASTAGES")) as_env = atoi(v);
-  if (const char* v = getenv("LSW_FC_STAGES")) ws_env = atoi(v);
+  const int bb_min = g.bu ? 0 : 1;           // bu: no strip buffer
+  const int bb_opt = (int)opt_int("fc_bbufs", 0), as_opt = (int)opt_int("fc_astages", 0),
+            ws_opt = (int)opt_int("fc_stages", 0);
   bool ok = false;
-  if (bb_env >= 1 && bb_env <= 2 && as_env >= 2 && as_env <= kMaxAStages && ws_env >= 2 && ws_env <= kMaxStages &&
-      budget >= (int64_t)bb_env * g.b_buf_bytes + (int64_t)as_env * g.a_stage_bytes + (int64_t)ws_env * w_stage) {
-    g.w_stages = ws_env;                     // tuning: an explicit plan (all three knobs set)
-    g.a_stages = as_env;
-    g.b_bufs = bb_env;
+  if (bb_opt >= bb_min && bb_opt <= 2 && as_opt >= 2 && as_opt <= kMaxAStages && ws_opt >= 2 &&
+      ws_opt <= kMaxStages &&
+      budget >= (int64_t)bb_opt * g.b_buf_bytes + (int64_t)as_opt * g.a_stage_bytes + (int64_t)ws_opt * w_stage) {
+    g.w_stages = ws_opt;                     // variant option: an explicit plan (all three set)
+    g.a_stages = as_opt;
+    g.b_bufs = g.bu ? 0 : bb_opt;
     ok = true;
   }
   for (int pass = 0; pass < 3 && !ok; ++pass) {
     const int a_min = pass == 0 ? 2 * u + 1 : pass == 1 ? u + 1 : 2;
     for (const Cand& c : cands) {
-      const int64_t rest = budget - (int64_t)c.ws * w_stage - (int64_t)c.bb * g.b_buf_bytes;
+      const int bb = g.bu ? 0 : c.bb;
+      const int64_t rest = budget - (int64_t)c.ws * w_stage - (int64_t)bb * g.b_buf_bytes;
       if (rest < 0) continue;
       int as = (int)(rest / g.a_stage_bytes);
       if (as > kMaxAStages) as = kMaxAStages;
       if (as < a_min) continue;
       g.w_stages = c.ws;
       g.a_stages = as;
-      g.b_bufs = c.bb;
+      g.b_bufs = bb;
       ok = true;
       break;
     }
   }
   if (!ok) {                                 // last resort: two W stages
-    for (int bb = 2; bb >= 1 && !ok; --bb) {
+    for (int bb = g.bu ? 0 : 2; bb >= bb_min && !ok; --bb) {
       const int64_t rest = budget - 2 * (int64_t)w_stage - (int64_t)bb * g.b_buf_bytes;
       int as = rest > 0 ? (int)(rest / g.a_stage_bytes) : 0;
       if (as > kMaxAStages) as = kMaxAStages;
@@ -954,12 +976,13 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     }
   }
   if (!ok) { delete plan; *why = "shared memory: rank * top_k too large for the folded kernel"; return cudaErrorNotSupported; }
-  if (const char* v = getenv("LSW_TC_CHUNK")) { int x = atoi(v); if (x >= 1) plan->chunk = x; }
-  if (const char* v = getenv("LSW_TC_PROBE")) plan->probe = atoi(v) & 17;   // 1: W stream only, 16: no fold math
+  plan->chunk = (int)opt_int("tc_chunk", plan->chunk);
+  if (plan->chunk < 1) plan->chunk = 1;
+  plan->probe = (int)probe_int("tc_probe") & 17;
+  plan->fused_probe = (int)probe_int("fc_fused_probe") & 12;   // tuning builds only: 1 W stream only, 16 no fold math
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
   // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
-  g.wrm = 1;
-  if (const char* v = getenv("LSW_FC_WRM")) g.wrm = atoi(v) != 0;
+  g.wrm = opt_int("fc_wrm", 1) != 0;
   for (int k = 0; k < LSW_NKIND; ++k) if (sp.kind[k].d_in % 64) g.wrm = 0;   // ragged TP shards: 3-D boxes
   g.smem_bytes = g.w_stages * w_stage + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
   // tiles
@@ -976,7 +999,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   }
   g.tiles_total = t;
   plan->grid = (int)(t < num_sms ? t : num_sms);
-  if (const char* v = getenv("LSW_TC_GRID")) { int x = atoi(v); if (x >= 1 && x < plan->grid) plan->grid = x; }
+  { const int x = (int)opt_int("tc_grid", 0); if (x >= 1 && x < plan->grid) plan->grid = x; }
   if (plan->grid < 1) plan->grid = 1;
   // pack operands + encode maps (same packed images as the term-group kernel,
   // with 128-column A^T blocks)
@@ -1136,8 +1159,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   a.t_count = plan->fused_tiles;
   a.g = plan->geom;
   a.chunk = 1;                     // unused: per-segment ranges (fused_from)
-  a.probe = 0;            // tuning only (LSW_FC_FUSED_PROBE): 4 = no segment wait, 8 = no GEMV (results wrong)
-  if (const char* v = getenv("LSW_FC_FUSED_PROBE")) a.probe = atoi(v) & 12;
+  a.probe = plan->fused_probe;     // tuning builds only: 4 = no segment wait, 8 = no GEMV (results wrong)
   a.mode = p.mode;
   a.top_k = p.top_k;
   a.n_experts = p.n_experts;

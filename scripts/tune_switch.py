@@ -1,8 +1,9 @@
-"""Time the all-layer switch kernel at a BASELINE shape under tuning knobs
-(LSW_TC_* environment variables read at lsw_create).  Prints one line per
-setting: median switch GB/s (algorithmic bytes) and fraction of the measured
-copy peak.  Usage: python scripts/tune_switch.py [--config llama2-7b] SETTING...
-where SETTING is like 'order=sweep,chunk=4,stages=6,probe=0'."""
+"""Time the all-layer switch kernel at a BASELINE shape under variant options
+(include/lsw_debug.h lsw_debug_set_option, read at lsw_create).  Prints one
+line per setting: median switch GB/s (algorithmic bytes) and fraction of the
+measured copy peak.  Usage: python scripts/tune_switch.py [--config llama2-7b]
+SETTING... where SETTING is like 'tc_kernel=pt,tc_chunk=32,fc_wrm=0' (probe
+options need a -DLSW_TUNING build)."""
 import argparse
 import json
 import os
@@ -24,10 +25,10 @@ ap.add_argument("--repeat", type=int, default=1)
 ap.add_argument("--rank", type=int, default=0, help="override the config's LoRA rank (sweep cells)")
 ap.add_argument("--topk", type=int, default=0, help="override the config's top-k (sweep cells)")
 ap.add_argument("--lib", default="", help="load this liblsw.so instead of the package's (A/B of two builds)")
-ap.add_argument("settings", nargs="*", default=["order=strip", "order=sweep,chunk=1", "order=sweep,chunk=4"])
+ap.add_argument("settings", nargs="*", default=["", "tc_chunk=32", "tc_chunk=64"])
 a = ap.parse_args()
+from paper_2405_17741_b200 import binding as _B  # noqa: E402
 if a.lib:
-    from paper_2405_17741_b200 import binding as _B
     _B._LIB = _B.load_library(a.lib, strict=False)
 cfg = synth.get_config(a.config)
 if a.layers:
@@ -43,20 +44,16 @@ idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
 gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6452.8
 for setting in [x for _ in range(a.repeat) for x in a.settings]:
-    for k in ("LSW_TC_ORDER", "LSW_TC_CHUNK", "LSW_TC_STAGES", "LSW_TC_PROBE", "LSW_TC_NSUB", "LSW_TC_AALL", "LSW_TC_STORE", "LSW_TC_ASTAGES", "LSW_TC_SPLIT", "LSW_TC_TG", "LSW_TC_BACKOFF", "LSW_TC_ACOPY", "LSW_TC_ADEPTH", "LSW_TC_ALOADER", "LSW_TC_KERNEL", "LSW_TC_W4D", "LSW_TC_MMA2", "LSW_TC_L2PROMO", "LSW_TC_WPOLICY",
-              "LSW_TC_GRID", "LSW_FC_BBUFS", "LSW_FC_ASTAGES", "LSW_FC_STAGES", "LSW_FC_WRM", "LSW_FC_PT"):
-        os.environ.pop(k, None)
-    for kv in setting.split(","):
-        if not kv:
-            continue
-        k, v = kv.split("=")
-        os.environ[("LSW_" if k.startswith("fc_") else "LSW_TC_") + k.upper()] = v
+    _B.set_option(None)
+    opts = dict(kv.split("=") for kv in setting.split(",") if kv)
+    for k, v in opts.items():
+        _B.set_option(k, v)
     try:
         sw = H.make_switch(cfg, W, A, B, router, impl=a.impl)
     except Exception as e:  # noqa: BLE001  (no plan for this shape under these knobs)
         print(json.dumps({"setting": setting, "error": str(e)[:120]}), flush=True)
         continue
-    probe = os.environ.get("LSW_TC_PROBE", "0") == "1"
+    probe = opts.get("tc_probe", "0") == "1"
     sw.router_topk(X1[0], idx, gate)
     sw.merge_all_layers(idx, gate)
     ms = []

@@ -114,6 +114,9 @@ CONFIGS: Dict[str, Config] = {
     "mini-r4k4": Config("mini-r4k4", 2, 256, 704, 2, 1, 128, 16, 4, 4, 16.0, "bf16"),
     "mini-r64k3": Config("mini-r64k3", 1, 256, 704, 2, 1, 128, 4, 64, 3, 16.0, "bf16"),
     "mini-r48": Config("mini-r48", 1, 256, 704, 2, 1, 128, 4, 48, 2, 16.0, "bf16"),
+    "mini-r64k4": Config("mini-r64k4", 1, 256, 704, 2, 1, 128, 8, 64, 4, 16.0, "bf16"),
+    "mini-kN": Config("mini-kN", 1, 256, 704, 2, 1, 128, 4, 16, 4, 16.0, "bf16"),
+    "mini-N64": Config("mini-N64", 1, 256, 704, 2, 1, 128, 64, 4, 2, 16.0, "bf16"),
     "mini-k1": Config("mini-k1", 2, 256, 704, 2, 1, 128, 4, 8, 1, 16.0, "bf16"),
 }
 

@@ -1,8 +1,8 @@
 """Fused switch + decode on the GPU (-m gpu).
 
-lsw_decode_token_fused runs the router and ONE launch (the ctx's fc kernel, or
-v1) that switches every adapted matrix and computes the group GEMVs from the
-freshly rounded tiles,
+lsw_decode_token_fused runs the router and ONE launch (the fold mode of the fc
+kernel) that switches every adapted matrix and computes the group GEMVs from
+the freshly rounded tiles,
 in decoder order with a segment barrier per (layer, group).  Checked through
 the C ABI: the weights after every token are bitwise those of the separate
 path (lsw_decode_token: switch launch + GEMV launches), the outputs equal its
@@ -29,15 +29,10 @@ def _f64(t):
     return t.detach().to("cpu").to(torch.float64).numpy()
 
 
-@pytest.mark.parametrize("kernel", ["v1", "fc"])
 @pytest.mark.parametrize("name,grid", [("mini", None), ("mini", "3"), ("mini", "1"), ("mini-r32", None),
                                        ("mini-k1", "5"), ("mini-r4k4", "2")])
-def test_fused_token_equals_separate_path(monkeypatch, name, grid, kernel):
-    if kernel == "v1" and name == "mini-r4k4":
-        pytest.skip("v1 has no plan for 2k = 8 terms")
-    monkeypatch.setenv("LSW_TC_KERNEL", kernel)
-    if grid:
-        monkeypatch.setenv("LSW_TC_GRID", grid)
+def test_fused_token_equals_separate_path(lsw_opts, name, grid):
+    lsw_opts(tc_kernel="fold", tc_grid=grid)
     cfg = synth.get_config(name)
     ctxs = []
     for _ in range(2):
@@ -45,7 +40,7 @@ def test_fused_token_equals_separate_path(monkeypatch, name, grid, kernel):
         sw = H.make_switch(cfg, W, A, B, router, impl="tc")
         ctxs.append((sw, W, A, B))
     info = ctxs[0][0].info()
-    assert info["switch_kernel"] == {"v1": 1, "fc": 3}[kernel]
+    assert info["switch_kernel"] == 3
     X1 = synth.gen_x1(cfg, 5, "cuda")
     xs_d = synth.gen_xs(cfg, "cuda")
     xs = H.pack_xs(cfg, xs_d)
@@ -83,19 +78,15 @@ def test_fused_token_equals_separate_path(monkeypatch, name, grid, kernel):
                         yo += d_out
 
 
-@pytest.mark.parametrize("kernel", ["fc", "tg"])
-def test_fused_on_a_ctx_that_switches_with_another_kernel(monkeypatch, kernel):
-    """The fused launch exists in the v1 and fc kernels; a ctx whose switch
-    kernel is tg builds a v1 plan for it on first use.  Plain tokens (the ctx's
-    own kernel) and fused tokens (v1) alternate on the same W and decision
-    slot: W stays on the oracle's stored trajectory and every token's outputs
-    match the oracle's GEMV on it."""
-    monkeypatch.setenv("LSW_TC_KERNEL", kernel)
+def test_fused_and_plain_tokens_alternate_on_one_ctx():
+    """Plain tokens (switch launch + GEMV launches) and fused tokens alternate
+    on the same W and decision slot: W stays on the oracle's stored
+    trajectory and every token's outputs match the oracle's GEMV on it."""
     cfg = synth.get_config("mini")
     W, A, B, router = H.build_weights(cfg, "cuda")
     sw = H.make_switch(cfg, W, A, B, router, impl="tc")
     info = sw.info()
-    assert info["switch_kernel"] == {"tg": 2, "fc": 3}[kernel]
+    assert info["switch_kernel"] == 3
     Ws = {(kd, l): _f64(W[kd][l]) for kd in synth.KINDS for l in range(cfg.n_layers)}
     As = {(kd, l): _f64(A[kd][l]) for kd in synth.KINDS for l in range(cfg.n_layers)}
     Bs = {(kd, l): _f64(B[kd][l]) for kd in synth.KINDS for l in range(cfg.n_layers)}
@@ -130,14 +121,12 @@ def test_fused_on_a_ctx_that_switches_with_another_kernel(monkeypatch, kernel):
 
 
 @pytest.mark.parametrize("name,grid", [("mini", None), ("mini", "3"), ("mini-r32", None)])
-def test_fused_outputs_are_bitwise_reproducible(monkeypatch, name, grid):
+def test_fused_outputs_are_bitwise_reproducible(lsw_opts, name, grid):
     """The fc fused launch accumulates each row's per-tile contributions in
     64-bit fixed point (integer adds commute), so two runs on identical inputs
     give bitwise-identical outputs whatever order the tiles finish in
     (SURVEY §8c.5 item 5), not only bitwise-identical weights."""
-    monkeypatch.setenv("LSW_TC_KERNEL", "fc")
-    if grid:
-        monkeypatch.setenv("LSW_TC_GRID", grid)
+    lsw_opts(tc_kernel="fold", tc_grid=grid)
     cfg = synth.get_config(name)
     X1 = synth.gen_x1(cfg, 3, "cuda")
     xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
@@ -161,3 +150,46 @@ def test_fused_outputs_are_bitwise_reproducible(monkeypatch, name, grid):
         assert torch.equal(ya, yb)
         for kd in synth.KINDS:
             assert torch.equal(Wa[kd], Wb[kd])
+
+
+@pytest.mark.parametrize("grid", [None, "3"])
+def test_fused_repeated_decision_still_computes_outputs(lsw_opts, grid):
+    """A token whose decision equals the merged one has an empty coefficient
+    list (R12): W is unchanged, but the fused launch must still stream W and
+    compute y = W x (it used to return zeros).  Checked against the
+    separate path on the same ctx state, and an invalid decision (latched,
+    W untouched) likewise still yields W x."""
+    lsw_opts(tc_kernel="fold", tc_grid=grid)
+    cfg = synth.get_config("mini")
+    W, A, B, router = H.build_weights(cfg, "cuda")
+    sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+    info = sw.info()
+    X1 = synth.gen_x1(cfg, 2, "cuda")
+    xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
+    ya = torch.empty(info["ys_elems"], device="cuda")
+    yb = torch.empty(info["ys_elems"], device="cuda")
+    idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
+    gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
+    sw.decode_token_fused(X1[0], xs, ya, idx, gate)
+    torch.cuda.synchronize()
+    snap = {kd: W[kd].clone() for kd in synth.KINDS}
+    sw.decode_token_fused(X1[0], xs, yb, idx, gate)          # same x1 -> same decision: nothing to add
+    torch.cuda.synchronize()
+    assert sw.device_status() == 0
+    for kd in synth.KINDS:
+        assert torch.equal(W[kd], snap[kd])
+    assert torch.equal(ya, yb)                              # same W, same x: bitwise (fixed-point sums)
+    yc = torch.empty(info["ys_elems"], device="cuda")
+    sw.decode_all_layers(xs, yc)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(yb.cpu().numpy(), yc.cpu().numpy(), rtol=1e-4,
+                               atol=1e-4 * float(yc.abs().max()))
+    assert float(yb.abs().max()) > 0
+    x1 = X1[1].clone()
+    x1[0] = float("nan")                                     # non-finite logits: rejected decision
+    sw.decode_token_fused(x1, xs, yb, idx, gate)
+    torch.cuda.synchronize()
+    assert sw.device_status() == 1
+    for kd in synth.KINDS:
+        assert torch.equal(W[kd], snap[kd])
+    assert torch.equal(ya, yb)

@@ -3,7 +3,7 @@
 lsw_restore_merge_all_layers writes W <- RNE(P + Delta(d_t)) from a pristine
 copy P in one launch.  Checked through the C ABI against oracle.restore on
 the same seeded inputs (allclose on every element, at most a few 1-ulp
-flips), for SIMT and both tensor-core kernels; its defining property -- no
+flips), for SIMT and every mode of the tensor-core kernel; its defining property -- no
 history -- bitwise: after any trajectory the result equals a fresh ctx's
 restore of the same decision; and the state machine around it (restore from
 `none`, fused switch and unmerge after a restore, restore without P refused).
@@ -35,14 +35,13 @@ def _ctx(cfg, impl):
     return sw, W, A, B, router, P
 
 
-CASES = [("toy", "simt", None), ("mini", "tc", "v1"), ("mini", "tc", "tg"), ("mini", "tc", "fc"), ("mini-r4k4", "tc", None),
-         ("mini-r64k3", "tc", None), ("mini-k1", "tc", None)]
+CASES = [("toy", "simt", None), ("mini", "tc", "fold"), ("mini", "tc", "pt"), ("mini", "tc", "bu"),
+         ("mini-r4k4", "tc", None), ("mini-r64k3", "tc", None), ("mini-r64k4", "tc", None), ("mini-k1", "tc", None)]
 
 
 @pytest.mark.parametrize("name,impl,kernel", CASES)
-def test_restore_matches_oracle_and_has_no_history(monkeypatch, name, impl, kernel):
-    if kernel:
-        monkeypatch.setenv("LSW_TC_KERNEL", kernel)
+def test_restore_matches_oracle_and_has_no_history(lsw_opts, name, impl, kernel):
+    lsw_opts(tc_kernel=kernel)
     cfg = synth.get_config(name)
     store = "bf16" if cfg.dtype == "bf16" else "f32"
     scale = cfg.alpha / cfg.rank
@@ -118,17 +117,14 @@ def test_restore_state_machine():
     assert sw.device_status() == 0
 
 
-@pytest.mark.parametrize("name,kernel,grid", [("mini", "v1", None), ("mini", "tg", "3"), ("mini", "fc", "3"),
-                                                  ("mini-r4k4", None, None)])
-def test_per_matrix_merge_ablation_is_bitwise_the_single_launch(monkeypatch, name, kernel, grid):
+@pytest.mark.parametrize("name,kernel,grid", [("mini", "fold", None), ("mini", "pt", "3"), ("mini", "fold", "3"),
+                                                  ("mini-r4k4", None, None), ("mini-r64k4", "bu", "2")])
+def test_per_matrix_merge_ablation_is_bitwise_the_single_launch(lsw_opts, name, kernel, grid):
     """SURVEY 8f #4 (launch-count ablation): the merge as one launch per matrix
     (7 x L launches of the same kernel over that matrix's tiles) gives bitwise
     the same weights as the single all-layer launch, and records the decision
     (a fused switch afterwards is correct)."""
-    if kernel:
-        monkeypatch.setenv("LSW_TC_KERNEL", kernel)
-    if grid:
-        monkeypatch.setenv("LSW_TC_GRID", grid)
+    lsw_opts(tc_kernel=kernel, tc_grid=grid)
     cfg = synth.get_config(name)
     outs = []
     for mode in ("single", "per_matrix"):

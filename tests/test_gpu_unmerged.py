@@ -31,12 +31,11 @@ def _f64(t):
 @pytest.mark.parametrize("name,impl,grid", [("toy", "simt", None), ("mini", "tc", None), ("mini-r32", "tc", None),
                                             ("mini-r64k3", "tc", None), ("mini-r4k4", "tc", None),
                                             ("mini-k1", "tc", None), ("mini", "tc", "3"), ("mini-r64k3", "tc", "2")])
-def test_unmerged_decode_matches_oracle(monkeypatch, name, impl, grid):
+def test_unmerged_decode_matches_oracle(lsw_opts, name, impl, grid):
     """grid: a GEMV grid of a few CTAs, so each CTA computes many LoRA-down
     products over several warps and the device counters are reset and reused
     across many launches."""
-    if grid:
-        monkeypatch.setenv("LSW_GEMV_GRID", grid)
+    lsw_opts(gemv_grid=grid)
     cfg = synth.get_config(name)
     W, A, B, router = H.build_weights(cfg, "cuda")
     sw = H.make_switch(cfg, W, A, B, router, impl=impl)
@@ -82,3 +81,33 @@ def test_unmerged_decode_matches_oracle(monkeypatch, name, impl, grid):
     with pytest.raises(L.LswError) as ei:                 # merged ctx: W is no longer pristine
         sw.decode_all_layers_unmerged(xs_p, ys_all, idx, gate)
     assert "STATE" in str(ei.value)
+
+
+@pytest.mark.parametrize("bad", ["out_of_range", "negative", "duplicate", "nan_gate"])
+def test_unmerged_decode_invalid_decision_latches_and_drops_lora(bad):
+    """An invalid decision (e.g. idx = -1 from non-finite router logits) is
+    never used to index A or B: every CTA validates it, the LoRA terms are
+    dropped (y = W x, Eq. 3 on the pristine W) and LSW_DEV_* is latched."""
+    cfg = synth.get_config("mini")
+    W, A, B, router = H.build_weights(cfg, "cuda")
+    sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+    xs = synth.gen_xs(cfg, "cuda")
+    idx = torch.tensor([1, 2], dtype=torch.int32, device="cuda")
+    gate = torch.tensor([0.75, 0.25], dtype=torch.float32, device="cuda")
+    if bad == "out_of_range":
+        idx[1] = cfg.n_experts
+    elif bad == "negative":
+        idx[0] = -1
+    elif bad == "duplicate":
+        idx[1] = 1
+    else:
+        gate[0] = float("nan")
+    for gi, grp in enumerate(synth.GROUPS):
+        n_out = sum(cfg.kind_shape(kd)[0] for kd in grp)
+        y = torch.full((n_out,), float("nan"), device="cuda")
+        sw.decode_group_unmerged(0, gi, xs[(0, gi)], y, idx, gate)
+        torch.cuda.synchronize()
+        ref = np.concatenate([O.gemv(_f64(W[kd][0]), _f64(xs[(0, gi)])) for kd in grp])
+        np.testing.assert_allclose(y.cpu().numpy(), ref, rtol=1e-4, atol=1e-4 * float(np.abs(ref).max()))
+    assert sw.device_status() == (3 if bad == "nan_gate" else 2)
+    assert sw.device_status() == 0
