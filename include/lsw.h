@@ -193,6 +193,19 @@ LSW_API lsw_status lsw_get_info(const lsw_ctx* ctx, lsw_info* info);
  */
 LSW_API lsw_status lsw_nccl_get_unique_id(void* id_out_128B_h);
 LSW_API lsw_status lsw_attach_nccl(lsw_ctx* ctx, const void* id_128B_h);
+/*
+ * NCCL is not linked: the first NCCL call binds libnccl.so.2 with dlopen --
+ * the copy already loaded in the process if there is one (torch's, after
+ * `import torch`), else the variant option nccl_path (lsw_debug.h), else the
+ * loader's search path.  Reports NCCL_VERSION_CODE of the bound library
+ * (e.g. 22809 for 2.28.9) and, if path_h is non-null, its file name (HOST
+ * buffer of path_len bytes, NUL-terminated, truncated).  LSW_E_NCCL if no
+ * NCCL can be loaded.  Needs no GPU.
+ * A tp_size = 1 ctx accepts lsw_attach_nccl too (a 1-rank communicator): its
+ * row-parallel decode GEMVs then run the all-reduce call (an identity) --
+ * the TP call site on one GPU.
+ */
+LSW_API lsw_status lsw_nccl_version(int32_t* version_h, char* path_h, int64_t path_len);
 
 /*
  * Eq. 2: z = W_g x1 accumulated in fp64 (R6), S = top-k by
@@ -235,7 +248,8 @@ LSW_API lsw_status lsw_restore_merge_all_layers(lsw_ctx* ctx, const int32_t* idx
 /*
  * Eq. 3: y = W*[layer, kind] x, batch 1, fp32 accumulate.
  *   x [d_in] device cfg dtype;  y [d_out] fp32 device, overwritten.
- * Row-parallel kinds with tp_size > 1: y is sum-allreduced over the TP group.
+ * Row-parallel kinds with tp_size > 1 (or a communicator attached): y is
+ * sum-allreduced (fp32, in place, on `stream`) over the TP group.
  */
 LSW_API lsw_status lsw_decode_linear(lsw_ctx* ctx, int32_t layer, int32_t kind, const void* x, float* y,
                              void* stream);

@@ -27,6 +27,8 @@ extern "C" {
  *   gemv_op_kb     N      bytes per bulk copy, KB                     [32]
  *   gemv_smem_kb   N      ring budget, KB                             [176 / 208]
  *   prefill_gather 0 | 1  LoRA-up of the prefill by the gather kernel [0]
+ *   nccl_path      file   libnccl.so.2 to dlopen when none is loaded yet
+ *                         (read at the first NCCL call, lsw_nccl_version)
  * Probes (deliberately WRONG results; only in a build with -DLSW_TUNING,
  * ignored otherwise): tc_probe (1: W stream only; 16: no fold math),
  * fc_fused_probe (4: no segment wait; 8: no GEMV), gemv_probe (stream only),

@@ -31,7 +31,7 @@ IMPL_NAME = {v: k for k, v in IMPL.items()}
 # Exported symbols the header declares (checked by tests/test_abi.py).
 SYMBOLS = (
     "lsw_abi_version", "lsw_last_error", "lsw_create", "lsw_destroy", "lsw_get_info",
-    "lsw_nccl_get_unique_id", "lsw_attach_nccl", "lsw_router_topk", "lsw_merge_all_layers",
+    "lsw_nccl_get_unique_id", "lsw_attach_nccl", "lsw_nccl_version", "lsw_router_topk", "lsw_merge_all_layers",
     "lsw_unmerge_all_layers", "lsw_attach_pristine", "lsw_restore_merge_all_layers", "lsw_decode_linear", "lsw_decode_group", "lsw_decode_all_layers",
     "lsw_decode_group_unmerged", "lsw_decode_all_layers_unmerged", "lsw_decode_token", "lsw_decode_token_fused",
     "lsw_decode_token_host", "lsw_device_status", "lsw_prefill_group",
@@ -82,6 +82,7 @@ def load_library(path: str = LIB_PATH, strict: bool = True) -> ctypes.CDLL:
         "lsw_get_info": (i32, [vp, ctypes.POINTER(Info)]),
         "lsw_nccl_get_unique_id": (i32, [vp]),
         "lsw_attach_nccl": (i32, [vp, vp]),
+        "lsw_nccl_version": (i32, [ctypes.POINTER(i32), ctypes.c_char_p, i64]),
         "lsw_router_topk": (i32, [vp, vp, vp, vp, vp]),
         "lsw_merge_all_layers": (i32, [vp, vp, vp, vp]),
         "lsw_unmerge_all_layers": (i32, [vp, vp]),
@@ -133,6 +134,14 @@ class options:
     def __exit__(self, *exc):
         for k in self.kv:
             set_option(k, None)
+
+
+def nccl_version():
+    """(NCCL_VERSION_CODE, file) of the libnccl.so.2 liblsw bound (lsw_nccl_version)."""
+    v = ctypes.c_int32(0)
+    buf = ctypes.create_string_buffer(4096)
+    _check(lib().lsw_nccl_version(ctypes.byref(v), buf, len(buf)))
+    return v.value, buf.value.decode()
 
 
 def lib() -> ctypes.CDLL:

@@ -2,7 +2,7 @@
 
 Every .cu under csrc/ is compiled in parallel with
 ``-gencode arch=compute_100a,code=sm_100a -lineinfo -O3`` and linked into
-``paper_2405_17741_b200/liblsw.so`` (static cudart, dynamic NCCL).  The oracle
+``paper_2405_17741_b200/liblsw.so`` (static cudart; NCCL is bound with dlopen at first use).  The oracle
 is pure numpy and needs no build.
 """
 from __future__ import annotations
@@ -56,7 +56,7 @@ def build(verbose: bool = False) -> str:
     if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lnccl", "-lcublas"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcublas", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")

@@ -359,11 +359,13 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   const int64_t G = gridDim.x;
   const int64_t n_chunks = (p.rows_total + R - 1) / R;            // chunk c = rows [c*R, c*R + R)
   const int64_t my_chunks = n_chunks > blockIdx.x ? (n_chunks - blockIdx.x + G - 1) / G : 0;
-  // Chunks issued so far.  A consumer warp takes only every 8th row, so it can
+  // Chunks issued so far.  A consumer warp takes only every 16th row, so it can
   // reach a slot's NEXT-but-one fill while the next fill is not yet issued; the
   // full barrier's parity would then alias an already completed phase.  Waiting
-  // for the ticket first makes the parity wait unambiguous.
-  __shared__ volatile int64_t issued;
+  // for the ticket first makes the parity wait unambiguous.  Written with
+  // st.release and read with ld.acquire (CTA scope): the consumer's parity
+  // wait then sees at least the producer's expect_tx of that chunk.
+  __shared__ int64_t issued;
   if (threadIdx.x == 0) {
     for (int s = 0; s < slots; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&full[s])), "r"(1));
@@ -410,7 +412,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
               : "memory");
           r = run_end;
         }
-        issued = i + 1;                             // ticket: chunk i's fill is armed
+        asm volatile("st.release.cta.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&issued)), "l"(i + 1) : "memory");
       }
     }
     return;
@@ -472,6 +474,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
       if (lane == 0) part[dw] = acc;
+      __syncwarp();
       asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");
       if (dw == 0 && lane == 0) {
         float u = 0.f;
@@ -479,6 +482,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
         L.u[d] = u;
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(L.arrive) : "memory");
       }
+      __syncwarp();
       asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");   // part[] reusable
     }
     if (dw == 0 && lane == 0) {
@@ -491,8 +495,10 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
         if (g_globaltimer() - t0 > 20000000000ull) __trap();
       }
     }
+    __syncwarp();
     asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");
     for (int d = threadIdx.x - 32 * (1 + kBulkConsumers); d < n_dots; d += 32 * kLoraWarps) us[d] = __ldcg(L.u + d);
+    __syncwarp();
     asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");
     // LoRA-up terms of this CTA's rows, one lane per row, while the consumers
     // still stream (their row sums wait in acc_s; joined at the end)
@@ -501,11 +507,13 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
         const int64_t row = (blockIdx.x + (t / R) * G) * R + t % R;
         e_s[t] = row < p.rows_total ? lora_up_row<kBf16>(p, L, us, row, kr) : 0.f;
       }
+    __syncwarp();
     asm volatile("bar.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");
     return;
   }
   // x -> shared (consumer warps), then a named barrier among the consumers only
   stage_x<kBf16 && !kXB>(p.x, xs, row_bytes, threadIdx.x - 32, 32 * kBulkConsumers);
+  __syncwarp();
   asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
   // consumers: unit u = (local chunk i, row k in chunk); warp cw takes u = cw mod 16
   const int cw = warp - 1;
@@ -516,7 +524,12 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     const int k = (int)(u - i * R);
     const int s = (int)(i % slots);
     const int64_t row = (blockIdx.x + i * G) * R + k;
-    while (issued <= i) __nanosleep(64);
+    for (;;) {                                    // ticket: chunk i's fill is armed
+      int64_t v;
+      asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(s_u32(&issued)) : "memory");
+      if (v > i) break;
+      __nanosleep(64);
+    }
     g_mbar_wait(s_u32(&full[s]), (uint32_t)((i / slots) & 1));
     if (row < p.rows_total && !(early_w & 2)) {    // early_w bit 1: tuning probe, stream only
       const float acc = row_dot<kBf16, kXB>(ring + s * slot_bytes + (size_t)k * row_bytes, xs, nchunk16, lane);
@@ -530,6 +543,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   }
   if (kLora) {
     // Eq. 2: y = (W x) + LoRA-up term, one rounding of the sum per row
+    __syncwarp();
     asm volatile("bar.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");   // e_s / us ready
     const bool up = !(L.flags & 4) && !(early_w & 2) && lora_ok;
     if (in_smem) {
@@ -546,6 +560,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     }
     // the last CTA to leave resets both counters for the next launch (which
     // publishes its dots only after this grid has completed: griddepcontrol.wait)
+    __syncwarp();
     asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
     if (cw == 0 && lane == 0) {
       uint32_t prev;

@@ -9,7 +9,8 @@
 #include <string>
 #include <vector>
 
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h>        // types and enums only: the functions are bound at run time (Nccl below)
 
 #include "lsw_internal.cuh"
 #include "../../include/lsw_debug.h"
@@ -17,6 +18,53 @@
 using namespace lsw;
 
 namespace {
+
+// NCCL, bound with dlopen on first use rather than linked: a process that has
+// imported torch already holds torch's libnccl.so.2 (its own build, 2.28.x
+// here), and a second NCCL under the same soname would be a different library
+// in the same process.  RTLD_NOLOAD finds the one already loaded; otherwise
+// the variant option nccl_path (the binding sets it to torch's copy), else the
+// loader's search path.  lsw_nccl_version reports which one is bound.
+struct Nccl {
+  bool tried = false;
+  void* h = nullptr;
+  std::string path;
+  ncclResult_t (*GetVersion)(int*) = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+std::mutex g_nccl_mu;
+Nccl g_nccl;
+
+const Nccl* nccl() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  Nccl& n = g_nccl;
+  if (n.tried) return n.h ? &n : nullptr;
+  n.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) {
+    const char* p = lsw::opt_str("nccl_path");
+    if (p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+  }
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return nullptr;
+  n.GetVersion = reinterpret_cast<decltype(n.GetVersion)>(dlsym(h, "ncclGetVersion"));
+  n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+  n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+  n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+  n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(dlsym(h, "ncclAllReduce"));
+  n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+  if (!n.GetVersion || !n.GetUniqueId || !n.CommInitRank || !n.CommDestroy || !n.AllReduce || !n.GetErrorString)
+    return nullptr;
+  Dl_info info;
+  if (dladdr(reinterpret_cast<void*>(n.AllReduce), &info) && info.dli_fname) n.path = info.dli_fname;
+  n.h = h;
+  return &n;
+}
 
 thread_local std::string g_last_error;
 
@@ -229,7 +277,7 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
 lsw_status lsw_destroy(lsw_ctx* ctx) {
   if (!ctx) return fail(LSW_E_ARG, "lsw_destroy: null ctx");
   cudaDeviceSynchronize();
-  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->comm) nccl()->CommDestroy(ctx->comm);
   if (ctx->tc) tc_plan_destroy(ctx->tc);
   cudaFree(ctx->lora_u);
   cudaFree(ctx->d_state);
@@ -272,21 +320,40 @@ lsw_status lsw_get_info(const lsw_ctx* ctx, lsw_info* info) {
   return LSW_OK;
 }
 
+lsw_status lsw_nccl_version(int32_t* version, char* path, int64_t path_len) {
+  if (!version) return fail(LSW_E_ARG, "lsw_nccl_version: null version");
+  const Nccl* n = nccl();
+  if (!n) return fail(LSW_E_NCCL, "lsw_nccl_version: libnccl.so.2 could not be loaded (%s)", dlerror());
+  int v = 0;
+  ncclResult_t r = n->GetVersion(&v);
+  if (r != ncclSuccess) return fail(LSW_E_NCCL, "ncclGetVersion: %s", n->GetErrorString(r));
+  *version = v;
+  if (path && path_len > 0) {
+    strncpy(path, n->path.c_str(), (size_t)path_len - 1);
+    path[path_len - 1] = 0;
+  }
+  return LSW_OK;
+}
+
 lsw_status lsw_nccl_get_unique_id(void* id_out) {
   if (!id_out) return fail(LSW_E_ARG, "lsw_nccl_get_unique_id: null");
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
-  ncclResult_t r = ncclGetUniqueId(reinterpret_cast<ncclUniqueId*>(id_out));
-  if (r != ncclSuccess) return fail(LSW_E_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  const Nccl* n = nccl();
+  if (!n) return fail(LSW_E_NCCL, "lsw_nccl_get_unique_id: libnccl.so.2 could not be loaded");
+  ncclResult_t r = n->GetUniqueId(reinterpret_cast<ncclUniqueId*>(id_out));
+  if (r != ncclSuccess) return fail(LSW_E_NCCL, "ncclGetUniqueId: %s", n->GetErrorString(r));
   return LSW_OK;
 }
 
 lsw_status lsw_attach_nccl(lsw_ctx* ctx, const void* id) {
   if (!ctx || !id) return fail(LSW_E_ARG, "lsw_attach_nccl: null argument");
   if (ctx->comm) return fail(LSW_E_STATE, "lsw_attach_nccl: communicator already attached");
+  const Nccl* n = nccl();
+  if (!n) return fail(LSW_E_NCCL, "lsw_attach_nccl: libnccl.so.2 could not be loaded");
   ncclUniqueId uid;
   memcpy(&uid, id, sizeof(uid));
-  ncclResult_t r = ncclCommInitRank(&ctx->comm, ctx->cfg.tp_size, uid, ctx->cfg.tp_rank);
-  if (r != ncclSuccess) { ctx->comm = nullptr; return fail(LSW_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)); }
+  ncclResult_t r = n->CommInitRank(&ctx->comm, ctx->cfg.tp_size, uid, ctx->cfg.tp_rank);
+  if (r != ncclSuccess) { ctx->comm = nullptr; return fail(LSW_E_NCCL, "ncclCommInitRank: %s", n->GetErrorString(r)); }
   return LSW_OK;
 }
 
@@ -378,17 +445,20 @@ static lsw_status gemv_sites(lsw_ctx* ctx, int layer, const int* kinds, int n, c
   p.x = x;
   p.y = y;
   // Row-parallel kinds under TP need the communicator: checked before anything
-  // is enqueued (header contract).
-  const bool allreduce = ctx->cfg.tp_size > 1 && ctx->kinds[kinds[0]].row_parallel;
-  if (allreduce && !ctx->comm)
+  // is enqueued (header contract).  A tp_size = 1 ctx with a (1-rank)
+  // communicator attached all-reduces too: the identity, through the same call.
+  const bool row_par = ctx->kinds[kinds[0]].row_parallel != 0;
+  if (row_par && ctx->cfg.tp_size > 1 && !ctx->comm)
     return fail(LSW_E_NCCL, "%s: tp_size=%d but no NCCL communicator attached", who, ctx->cfg.tp_size);
+  const bool allreduce = row_par && ctx->comm;
   cudaError_t e = launch_gemv(p, ctx->cfg.dtype, ctx->gemv, s, early_w);
   if (e != cudaSuccess) return cuda_fail(e, "decode GEMV launch");
   ++ctx->launches;
   // Row-parallel kinds under TP: partial sums -> allreduce.
   if (allreduce) {
-    ncclResult_t r = ncclAllReduce(y, y, (size_t)rows, ncclFloat, ncclSum, ctx->comm, s);
-    if (r != ncclSuccess) return fail(LSW_E_NCCL, "%s: ncclAllReduce: %s", who, ncclGetErrorString(r));
+    const Nccl* nc = nccl();
+    ncclResult_t r = nc->AllReduce(y, y, (size_t)rows, ncclFloat, ncclSum, ctx->comm, s);
+    if (r != ncclSuccess) return fail(LSW_E_NCCL, "%s: ncclAllReduce: %s", who, nc->GetErrorString(r));
   }
   return LSW_OK;
 }

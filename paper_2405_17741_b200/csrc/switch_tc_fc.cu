@@ -671,13 +671,25 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       int cur_seg = -1;                            // fused: segment of the previous tile
       int conv_next = 0;                           // fused: first segment whose outputs this CTA has not converted
       unsigned long long seg_mine = 0;             // fused: tiles of cur_seg this CTA finished
+      // fused: this thread's partial output of one row, summed in fp32 over the
+      // consecutive column tiles of a strip (a CTA's range walks cb fastest)
+      // and added to the fixed-point accumulator once per strip, not per tile
+      float y_run = 0.f;
+      int64_t y_at = -1;                           // ys_fx index y_run belongs to (-1: none)
+      auto y_flush = [&]() {
+        if (y_at >= 0) atomicAdd(args.ys_fx + y_at, (unsigned long long)__double2ll_rn((double)y_run * kFx));
+        y_at = -1;
+        y_run = 0.f;
+      };
       for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
         uint4 xv[8];                               // fused: x of this thread's 64 columns
         if constexpr (kF) {
           if (c.seg != cur_seg) {
+            y_flush();                             // before the segment's count is published
             // decoder order: x of segment s is final only once every tile of
             // segment s-1 is done -- one thread per CTA publishes the CTA's
             // count of the segment it leaves and waits for the previous total
+            __syncwarp();
             asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
             if (releaser && cur_seg >= 0) {
               __threadfence();
@@ -689,9 +701,11 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             for (; conv_next < c.seg; ++conv_next) {
               if (releaser && !(args.probe & 4))
                 wait_count(&args.seg_done[conv_next], (unsigned long long)args.segs[conv_next].tile_count);
+              __syncwarp();
               asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
               fx_convert(args, conv_next, threadIdx.x - 32 * kFirstEpiWarp, 32 * kEpiWarps);
             }
+            __syncwarp();
             asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
             cur_seg = c.seg;
             seg_mine = 0;
@@ -783,14 +797,17 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         const int unit = g.wrm ? 2 * row + half : half * kTM + row;
         uint8_t* wrow = wst0 + (size_t)wring.i * (2 * kSubBytes) + unit * 128;
         if (kF && !(args.probe & 8)) {
-          float y = 0.f;
+          const int64_t grow = (int64_t)c.rb * kTM + row;
+          const int64_t at = grow < g.d_out[c.kd] ? args.segs[c.seg].y_off[c.kidx] + grow : -1;
+          if (at != y_at) {
+            y_flush();
+            y_at = at;
+          }
+          float y = y_run;
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             y = epi16_dot(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q], xv[2 * q], xv[2 * q + 1], y);
-          const int64_t grow = (int64_t)c.rb * kTM + row;
-          if (grow < g.d_out[c.kd])
-            atomicAdd(args.ys_fx + args.segs[c.seg].y_off[c.kidx] + grow,
-                      (unsigned long long)__double2ll_rn((double)y * kFx));
+          y_run = y;
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q) epi16(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q]);
@@ -802,7 +819,9 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         wring.next();
       }
       if constexpr (kF) {
+        y_flush();
         if (cur_seg >= 0) {                        // publish the last segment this CTA worked on
+          __syncwarp();
           asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
           if (releaser) {
             __threadfence();
@@ -813,6 +832,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         for (; conv_next < args.n_seg; ++conv_next) {   // the remaining segments' outputs
           if (releaser && !(args.probe & 4))
             wait_count(&args.seg_done[conv_next], (unsigned long long)args.segs[conv_next].tile_count);
+          __syncwarp();
           asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
           fx_convert(args, conv_next, threadIdx.x - 32 * kFirstEpiWarp, 32 * kEpiWarps);
         }

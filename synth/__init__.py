@@ -118,6 +118,10 @@ CONFIGS: Dict[str, Config] = {
     "mini-kN": Config("mini-kN", 1, 256, 704, 2, 1, 128, 4, 16, 4, 16.0, "bf16"),
     "mini-N64": Config("mini-N64", 1, 256, 704, 2, 1, 128, 64, 4, 2, 16.0, "bf16"),
     "mini-k1": Config("mini-k1", 2, 256, 704, 2, 1, 128, 4, 8, 1, 16.0, "bf16"),
+    # Full router widths of configs[1..3] (d_model 4096 / 5120) on one thin layer:
+    # GPU router parity at the real reduction length.
+    "wide-d4096": Config("wide-d4096", 1, 4096, 128, 1, 1, 128, 8, 16, 2, 16.0, "bf16"),
+    "wide-d5120": Config("wide-d5120", 1, 5120, 128, 1, 1, 128, 8, 32, 2, 16.0, "bf16"),
 }
 
 

@@ -106,3 +106,16 @@ def test_null_ctx_is_refused_by_every_entry_point(L):
     assert lib.lsw_decode_token_host(None, None, None, None, None, None, None) == E_ARG
     assert lib.lsw_prefill_group(None, 0, 0, None, 1, None, None, None, None) == E_ARG
     assert b"null" in lib.lsw_last_error()
+
+
+def test_nccl_is_the_process_copy_torch_loaded(L):
+    """liblsw does not link NCCL; its first NCCL call binds
+    the libnccl.so.2 already in the process (torch's), so the TP all-reduce
+    and torch.distributed share one NCCL.  Needs no GPU."""
+    import torch
+    v, path = L.binding.nccl_version()
+    major, minor, patch = torch.cuda.nccl.version()
+    assert v == major * 10000 + minor * 100 + patch, (v, path)
+    maps = [ln.split()[-1] for ln in open("/proc/self/maps") if "libnccl" in ln]
+    assert os.path.realpath(path) in {os.path.realpath(m) for m in maps}
+    assert L.lib().lsw_nccl_version(None, None, 0) == 1

@@ -152,15 +152,22 @@ def test_router_rejects_nonfinite_and_bad_k():
         O.router(np.ones((4, 2)), np.ones(2), 5)
 
 
-def test_router_fast_matches_router_indices():
-    cfg = synth.CONFIGS["toy"]
+@pytest.mark.parametrize("name,n_tok", [("toy", 64), ("llama2-7b", 6), ("llama2-13b", 6)])
+def test_router_fast_matches_router_indices(name, n_tok):
+    """router_fast (numpy matvec) routes every parity test; pin it against the
+    ascending-order Python loop of ``router`` at the toy width and at the full
+    router widths of the BASELINE shapes (d_model 4096 and 5120; bf16 inputs)."""
+    cfg = synth.get_config(name)
     Wg = synth.to_f64_numpy(synth.gen_router(cfg))
-    X = synth.to_f64_numpy(synth.gen_x1(cfg, 64))
-    for t in range(64):
+    X = synth.to_f64_numpy(synth.gen_x1(cfg, n_tok))
+    assert Wg.shape == (cfg.n_experts, cfg.d_model)
+    for t in range(n_tok):
         a = O.router(Wg, X[t], cfg.top_k)
         b = O.router_fast(Wg, X[t], cfg.top_k)
         assert a[0].tolist() == b[0].tolist()
         np.testing.assert_allclose(a[1], b[1], rtol=1e-13)
+        z = np.sort(b[3])[::-1]
+        assert z[cfg.top_k - 1] - z[cfg.top_k] > 1e-9     # margins far above fp64 summation-order noise
 
 
 # ----------------------------------------------------------------------------- delta / merge
@@ -360,6 +367,27 @@ def test_drift_random_walk_closed_form(store, eps_tol):
     assert O.drift(W64, O.rne(cfgW, store) + O.delta(A, B, O.coef_list(p2, None, scale)))["rel_fro"] < 1e-9
 
 
+def test_drift_fields_golden_hand_computed():
+    """O8's three fields on a hand-worked 2x2 case (allclose is strict '>' in
+    |d| > atol + rtol |exact|, torch.allclose's complement):
+      exact [[1, -2], [0.5, 0]], W_T - exact [[0.031, 0.04], [0, -0.011]]
+      (0,0): 0.031 > 0.01 + 0.02*1 = 0.03  fails;  (0,1): 0.04 <= 0.05  passes;
+      (1,0): 0 passes;  (1,1): 0.011 > 0.01  fails  ->  frac_fail = 2/4;
+      max_abs = 0.04;  rel_fro = sqrt(0.031^2 + 0.04^2 + 0.011^2) / sqrt(1 + 4 + 0.25)."""
+    exact = np.array([[1.0, -2.0], [0.5, 0.0]])
+    d = np.array([[0.031, 0.04], [0.0, -0.011]])
+    got = O.drift(exact + d, exact)
+    assert got["frac_fail"] == 0.5
+    assert abs(got["max_abs"] - 0.04) < 1e-15
+    assert abs(got["rel_fro"] - math.sqrt(0.031 ** 2 + 0.04 ** 2 + 0.011 ** 2) / math.sqrt(5.25)) < 1e-15
+    # a sign error in the difference, or |exact| replaced by exact, is caught:
+    assert O.drift(exact - d, exact)["frac_fail"] == 0.5
+    z = np.array([[0.0, 1.0]])
+    assert O.drift(z + 0.011, z)["frac_fail"] == 0.5                # 0.011 > 0.01 but <= 0.03
+    m = np.array([[-1.0, 2.0]])
+    assert O.drift(m - 0.029, m)["frac_fail"] == 0.0                # |exact|, not exact, in the bound
+
+
 # ----------------------------------------------------------------------------- row sampling (O9)
 
 def test_row_sampled_oracle_is_exact():
@@ -399,3 +427,34 @@ def test_oracle_model_alg1_sequence_matches_exact_shadow_toy():
         assert O.drift(m.W[key], Ws[key])["rel_fro"] < 1e-5
     with pytest.raises(RuntimeError):
         m.unmerge_all_layers()
+
+
+def test_oracle_model_restore_ends_any_chain_and_unmerges_to_pristine_dyadic():
+    """OracleModel.restore_merge_all_layers: on dyadic inputs in
+    exact mode, restoring d from the pristine copies equals the end of any
+    Eq. 6 / Eq. 10 chain that ends at d (every site), records d as merged (a
+    following Eq. 7 unmerge gives P back bit for bit), and a following switch
+    is Eq. 10 from d."""
+    Ws, As, Bs = {}, {}, {}
+    for i, kd in enumerate(("q", "down")):
+        W, A, B = _dyadic_site(40 + 3 * i)
+        Ws[(kd, 0)], As[(kd, 0)], Bs[(kd, 0)] = W, A, B
+    Wg = np.eye(4, 8)
+    chain = O.OracleModel(Wg, Ws, As, Bs, 2, 8.0, 4, None)      # scale 2
+    rest = O.OracleModel(Wg, Ws, As, Bs, 2, 8.0, 4, None)
+    d1, d2, d3 = ([1, 3], [0.5, 0.5]), ([3, 2], [0.625, 0.375]), ([0, 2], [0.75, 0.25])
+    for d in (d1, d2):
+        chain.merge_all_layers(d)
+    rest.merge_all_layers(d3)                                    # some other history
+    rest.restore_merge_all_layers(Ws, d2)
+    for key in Ws:
+        assert np.array_equal(rest.W[key], chain.W[key])
+        assert not np.array_equal(rest.W[key], Ws[key])
+    assert rest.prev == chain.prev
+    rest.merge_all_layers(d3)                                    # Eq. 10 from d2
+    chain.merge_all_layers(d3)
+    for key in Ws:
+        assert np.array_equal(rest.W[key], chain.W[key])
+    rest.unmerge_all_layers()
+    for key in Ws:
+        assert np.array_equal(rest.W[key], Ws[key])
