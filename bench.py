@@ -429,9 +429,9 @@ def run_ours(args, cfg):
             un_ms.append(a.elapsed_time(b))
 
     # unmerged prefill: a 512-token prompt, every token with its
-    # own pre-gated decision, through every group of every layer (Eq. 2; the
-    # dense part is cuBLAS, the LoRA parts our kernels) -- reported, not timed
-    # into the decode metric
+    # own pre-gated decision, through every group of every layer (Eq. 2; our
+    # tcgen05 LoRA-down GEMM, Z build and dense + LoRA-up GEMM per group) --
+    # reported, not timed into the decode metric
     pf = None
     if world == 1:
         T_pf = 512
@@ -460,10 +460,15 @@ def run_ours(args, cfg):
             b.record(stream)
             torch.cuda.synchronize()
             pf_ms.append(a.elapsed_time(b))
+        pf_fl = 2.0 * T_pf * cfg.n_layers * sum(
+            cfg.kind_shape(kd)[0] * (cfg.kind_shape(kd)[1] + 2 * cfg.n_experts * ((cfg.rank + 15) // 16 * 16))
+            + cfg.n_experts * cfg.rank * cfg.kind_shape(kd)[1] for kd in synth.KINDS)
         pf = {"tokens": T_pf, "ms": statistics.median(pf_ms),
               "tokens_per_s": T_pf / (statistics.median(pf_ms) * 1e-3),
-              "note": "adapted-linear GEMMs of all layers (cuBLAS) + per-token LoRA (our kernels), "
-                      "router per token excluded"}
+              "tflops_issued": pf_fl / (statistics.median(pf_ms) * 1e-3) / 1e12,
+              "note": "adapted-linear prefill of all layers on our tcgen05 kernels (dense + LoRA-up in one "
+                      "contraction per tile, every expert's LoRA-down); router per token excluded; "
+                      "tflops_issued counts the MMA work issued (dense d_in + 2 N rp LoRA-up K + N r LoRA-down)"}
 
     # end-to-end through the public API with host buffers
     x1h = torch.empty(cfg.d_model, dtype=cfg.torch_dtype).pin_memory()

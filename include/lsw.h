@@ -293,15 +293,20 @@ LSW_API lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_
  * prompt tokens, each with its OWN pre-gated decision, so nothing can be
  * merged -- Eq. 2 as written:
  *   Y[t] = W x_t + sum_j (alpha/r) gate[t][j] B[idx[t][j]] (A[idx[t][j]] x_t).
- *   X: device [T, d_in] (storage dtype, row-major); idx: device int32 [T, top_k];
- *   gate: device fp32 [T, top_k]; Y: device fp32 [T, rows], rows = the group's
- *   output rows in site order (as lsw_decode_group).  The dense part and the
- *   LoRA-down products of every expert are cuBLAS GEMMs per site (fp32
- *   accumulate); the LoRA-up step scales them by each token's gates (our
- *   kernel) and adds one fp32 GEMM against a packed fp32 copy of B, which the
- *   ctx builds on the first call (L * sum(d_out) * N * r * 4 bytes).
+ *   X: device [T, d_in] (storage dtype, row-major, 16-byte aligned); idx:
+ *   device int32 [T, top_k]; gate: device fp32 [T, top_k]; Y: device fp32
+ *   [T, rows], rows = the group's output rows in site order (as
+ *   lsw_decode_group), overwritten.  bf16 with the tensor-core switch: three
+ *   launches of our tcgen05 kernels -- the LoRA-down products of every expert
+ *   (one GEMM over the bank A [N*r, d_in], K split over the grid), the
+ *   gate-scaled products of each token's selected experts as an exact-to-2^-16
+ *   (hi, lo) bf16 pair, and ONE tcgen05 contraction per 128-row x 128-token
+ *   tile over K = d_in (W x^T) + 2 N rp (the LoRA-up term against the ctx's
+ *   packed B) -- fp32 accumulation; otherwise two CUDA-core kernels (only the
+ *   k selected experts).  Deterministic.  Scratch is ctx-owned, grown on
+ *   demand (not graph-capturable when it grows).
  *   LSW_E_STATE if the ctx is merged; LSW_E_UNSUPPORTED if tp_size > 1;
- *   LSW_E_ARG for T outside [1, 2^20].  Invalid idx values are undefined.
+ *   LSW_E_ARG for T outside [1, 2^20].  Invalid idx values contribute nothing.
  */
 LSW_API lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const void* X, int64_t T,
                                      const int32_t* idx, const float* gate, float* Y, void* stream);

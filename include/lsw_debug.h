@@ -26,7 +26,6 @@ extern "C" {
  *   gemv_grid      N      GEMV grid cap                               [#SMs]
  *   gemv_op_kb     N      bytes per bulk copy, KB                     [32]
  *   gemv_smem_kb   N      ring budget, KB                             [176 / 208]
- *   prefill_gather 0 | 1  LoRA-up of the prefill by the gather kernel [0]
  *   nccl_path      file   libnccl.so.2 to dlopen when none is loaded yet
  *                         (read at the first NCCL call, lsw_nccl_version)
  * Probes (deliberately WRONG results; only in a build with -DLSW_TUNING,

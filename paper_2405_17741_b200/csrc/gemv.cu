@@ -362,9 +362,9 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   // Chunks issued so far.  A consumer warp takes only every 16th row, so it can
   // reach a slot's NEXT-but-one fill while the next fill is not yet issued; the
   // full barrier's parity would then alias an already completed phase.  Waiting
-  // for the ticket first makes the parity wait unambiguous.  Written with
-  // st.release and read with ld.acquire (CTA scope): the consumer's parity
-  // wait then sees at least the producer's expect_tx of that chunk.
+  // for the ticket first makes the parity wait unambiguous.  Written and read
+  // with release / acquire atomics (CTA scope): the consumer's parity wait then
+  // sees at least the producer's expect_tx of that chunk.
   __shared__ int64_t issued;
   if (threadIdx.x == 0) {
     for (int s = 0; s < slots; ++s) {
@@ -412,7 +412,8 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
               : "memory");
           r = run_end;
         }
-        asm volatile("st.release.cta.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&issued)), "l"(i + 1) : "memory");
+        asm volatile("atom.release.cta.shared::cta.exch.b64 _, [%0], %1;" ::"r"(s_u32(&issued)), "l"(i + 1)
+                     : "memory");
       }
     }
     return;
@@ -508,7 +509,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
         e_s[t] = row < p.rows_total ? lora_up_row<kBf16>(p, L, us, row, kr) : 0.f;
       }
     __syncwarp();
-    asm volatile("bar.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");
+    asm volatile("barrier.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");   // two code sites: not .aligned
     return;
   }
   // x -> shared (consumer warps), then a named barrier among the consumers only
@@ -526,7 +527,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     const int64_t row = (blockIdx.x + i * G) * R + k;
     for (;;) {                                    // ticket: chunk i's fill is armed
       int64_t v;
-      asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(s_u32(&issued)) : "memory");
+      asm volatile("atom.acquire.cta.shared::cta.add.u64 %0, [%1], 0;" : "=l"(v) : "r"(s_u32(&issued)) : "memory");
       if (v > i) break;
       __nanosleep(64);
     }
@@ -538,13 +539,16 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
         else p.y[row] = acc;
       }
     }
+    // the warp's generic-proxy reads of the slot are ordered before the next
+    // bulk copy (async proxy) into it: proxy fence, then the release arrive
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[s])) : "memory");
   }
   if (kLora) {
     // Eq. 2: y = (W x) + LoRA-up term, one rounding of the sum per row
     __syncwarp();
-    asm volatile("bar.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");   // e_s / us ready
+    asm volatile("barrier.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");   // two code sites: not .aligned   // e_s / us ready
     const bool up = !(L.flags & 4) && !(early_w & 2) && lora_ok;
     if (in_smem) {
       for (int64_t t = threadIdx.x - 32; t < n_local; t += 32 * kBulkConsumers) {

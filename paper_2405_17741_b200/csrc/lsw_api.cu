@@ -144,10 +144,11 @@ struct lsw_ctx {
   int32_t* st_idx = nullptr;
   float* st_gate = nullptr;
   cudaStream_t st_side = nullptr;       // lsw_decode_token_host: copies overlapped with the token
-  void* cublas = nullptr;               // lsw_prefill_group: cuBLAS handle (dense part)
-  float* prefill_u = nullptr;           // lsw_prefill_group: LoRA-down scratch (U, then Z)
+  PfPlan* pf = nullptr;                 // lsw_prefill_group: tensor-core plan (maps), built on first use
+  float* prefill_u = nullptr;           // lsw_prefill_group: LoRA-down scratch
   int64_t prefill_u_elems = 0;
-  float* bcat[LSW_NKIND] = {};          // lsw_prefill_group: packed fp32 B [L, d_out, N*r] per kind
+  void* prefill_z = nullptr;            // lsw_prefill_group (tc): (hi, lo) LoRA-up operand scratch
+  int64_t prefill_z_elems = 0;
   std::vector<cudaEvent_t> st_ev;       // [0]: xs landed; [1 + l]: layer l's outputs final
 };
 
@@ -287,9 +288,9 @@ lsw_status lsw_destroy(lsw_ctx* ctx) {
   cudaFree(ctx->st_idx);
   cudaFree(ctx->st_gate);
   for (cudaEvent_t ev : ctx->st_ev) cudaEventDestroy(ev);
-  prefill_cublas_destroy(ctx->cublas);
+  pf_plan_destroy(ctx->pf);
   cudaFree(ctx->prefill_u);
-  for (int k = 0; k < LSW_NKIND; ++k) cudaFree(ctx->bcat[k]);
+  cudaFree(ctx->prefill_z);
   if (ctx->st_side) cudaStreamDestroy(ctx->st_side);
   delete ctx;
   return LSW_OK;
@@ -530,53 +531,45 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
   if (group < 0 || group >= LSW_NGROUP) return fail(LSW_E_ARG, "%s: group=%d invalid", who, group);
   if (ctx->merged) return fail(LSW_E_STATE, "%s: the ctx is merged (prefill reads the pristine W)", who);
   if (ctx->cfg.tp_size > 1) return fail(LSW_E_UNSUPPORTED, "%s: tp_size > 1", who);
-  if (!ctx->cublas && prefill_cublas_create(&ctx->cublas) != cudaSuccess)
-    return fail(LSW_E_CUDA, "%s: cublasCreate failed", who);
-  const int64_t need = T * 3 * ctx->cfg.n_experts * ctx->cfg.rank;
-  if (need > ctx->prefill_u_elems) {
+  if (reinterpret_cast<uintptr_t>(X) % 16) return fail(LSW_E_ARG, "%s: X not 16-byte aligned", who);
+  const bool tc = ctx->tc != nullptr;
+  if (tc && !ctx->pf) {
+    cudaError_t e = pf_plan_create(&ctx->pf, ctx->simt_geom, ctx->tc, ctx->num_sms);
+    if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: tensor-core prefill plan");
+  }
+  const int n = kGroupSize[group];
+  int64_t need_u = T * n * ctx->cfg.top_k * ctx->cfg.rank, need_z = 0;
+  if (tc) pf_scratch(ctx->pf, n, T, &need_u, &need_z);
+  if (need_u > ctx->prefill_u_elems) {
     cudaFree(ctx->prefill_u);
     ctx->prefill_u = nullptr;
-    if (cudaMalloc(&ctx->prefill_u, 2 * need * sizeof(float)) != cudaSuccess)
+    ctx->prefill_u_elems = 0;
+    if (cudaMalloc(&ctx->prefill_u, need_u * sizeof(float)) != cudaSuccess)
       return fail(LSW_E_OOM, "%s: scratch allocation failed", who);
-    ctx->prefill_u_elems = need;
+    ctx->prefill_u_elems = need_u;
   }
-  // packed fp32 B of every layer, per kind, built on the first call (stream-ordered):
-  // the LoRA-up step becomes one GEMM per site (LSW_PREFILL_GATHER=1: the gather kernel)
-  const bool gather = opt_int("prefill_gather", 0) != 0;
-  if (!gather) {
-    const int nr = ctx->cfg.n_experts * ctx->cfg.rank;
-    for (int k = 0; k < LSW_NKIND; ++k) {
-      if (ctx->bcat[k]) continue;
-      const lsw_kind_desc& d = ctx->kinds[k];
-      if (cudaMalloc(&ctx->bcat[k], (size_t)ctx->cfg.n_layers * d.d_out * nr * sizeof(float)) != cudaSuccess)
-        return fail(LSW_E_OOM, "%s: packed B allocation failed", who);
-      for (int l = 0; l < ctx->cfg.n_layers; ++l) {
-        const void* Bl = (const uint8_t*)d.B + (size_t)l * ctx->cfg.n_experts * d.d_out * ctx->cfg.rank * esize(ctx);
-        cudaError_t e = launch_pack_bcat(Bl, ctx->bcat[k] + (size_t)l * d.d_out * nr, d.d_out, ctx->cfg.n_experts,
-                                         ctx->cfg.rank, ctx->cfg.dtype, (cudaStream_t)stream);
-        if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: pack");
-        ++ctx->launches;
-      }
-      // built once for the ctx's lifetime: finished before any stream may read it
-      cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
-      if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: pack");
-    }
+  if (need_z > ctx->prefill_z_elems) {
+    cudaFree(ctx->prefill_z);
+    ctx->prefill_z = nullptr;
+    ctx->prefill_z_elems = 0;
+    if (cudaMalloc(&ctx->prefill_z, need_z * 2) != cudaSuccess)
+      return fail(LSW_E_OOM, "%s: scratch allocation failed", who);
+    ctx->prefill_z_elems = need_z;
   }
   const size_t es = esize(ctx);
   PrefillParams P{};
   int64_t rows = 0;
-  const int n = kGroupSize[group];
+  int kinds[3] = {0, 0, 0};
   for (int i = 0; i < n; ++i) {
-    const lsw_kind_desc& d = ctx->kinds[kGroupKinds[group][i]];
+    const int kd = kGroupKinds[group][i];
+    const lsw_kind_desc& d = ctx->kinds[kd];
+    kinds[i] = kd;
     P.W[i] = (const uint8_t*)d.W + (size_t)layer * d.d_out * d.d_in * es;
     P.A[i] = (const uint8_t*)d.A + (size_t)layer * ctx->cfg.n_experts * ctx->cfg.rank * d.d_in * es;
     P.B[i] = (const uint8_t*)d.B + (size_t)layer * ctx->cfg.n_experts * d.d_out * ctx->cfg.rank * es;
     P.d_out[i] = d.d_out;
     P.row_begin[i] = rows;
     rows += d.d_out;
-    const int kd = kGroupKinds[group][i];
-    P.Bcat[i] = ctx->bcat[kd] ? ctx->bcat[kd] + (size_t)layer * d.d_out * ctx->cfg.n_experts * ctx->cfg.rank
-                              : nullptr;
   }
   P.n_sites = n;
   P.k = ctx->cfg.top_k;
@@ -590,11 +583,12 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
   P.idx = idx;
   P.gate = gate;
   P.U = ctx->prefill_u;
-  P.Z = ctx->prefill_u + need;
+  P.Z = ctx->prefill_z;
   P.Y = Y;
-  cudaError_t e = launch_prefill(P, ctx->cfg.dtype, ctx->cublas, (cudaStream_t)stream);
+  cudaError_t e = tc ? launch_prefill_tc(ctx->pf, P, layer, kinds, (cudaStream_t)stream)
+                     : launch_prefill_simt(P, ctx->cfg.dtype, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: launch");
-  ctx->launches += 1;                       // LoRA-up (the dense and LoRA-down GEMMs are cuBLAS calls)
+  ctx->launches += tc ? 3 : 2;              // tc: LoRA-down GEMM, Z build, dense + LoRA-up GEMM
   return LSW_OK;
 }
 

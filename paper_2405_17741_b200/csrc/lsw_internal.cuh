@@ -205,7 +205,10 @@ struct GemvTune {
 cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, const GemvTune& t, cudaStream_t s, bool early_w = false,
                         GemvLora* lora = nullptr);
 
-// Unmerged prefill of one group for T tokens (prefill.cu).
+// Unmerged prefill of one group for T tokens: prefill_tc.cu
+// (bf16 with a tensor-core plan: tcgen05 LoRA-down GEMM, Z build, one tcgen05
+// GEMM for the dense part + LoRA-up), prefill.cu (SIMT, fp32 storage or the
+// SIMT switch).
 struct PrefillParams {
   const void* W[3];          // site q: W [d_out_q, d_in] of this layer (pristine)
   const void* A[3];          // site q: A [N, r, d_in] of this layer
@@ -217,15 +220,18 @@ struct PrefillParams {
   const void* X;             // [T, d_in]
   const int32_t* idx;        // [T, k]
   const float* gate;         // [T, k]
-  float* U;                  // scratch [T, 3, N*r]: every expert's LoRA-down products
-  float* Z;                  // scratch [T, 3, N*r]: U gate-scaled at the selected experts, else 0
-  const float* Bcat[3];      // site q: packed fp32 [d_out_q, N*r] of this layer, or null (gather path)
+  float* U;                  // scratch: LoRA-down products (tc: per K split)
+  void* Z;                   // scratch (tc): gate-scaled (hi, lo) bf16 operand of the LoRA-up step
   float* Y;                  // [T, rows]
 };
-cudaError_t launch_pack_bcat(const void* B, float* out, int64_t d_out, int N, int r, int32_t dtype, cudaStream_t s);
-cudaError_t launch_prefill(const PrefillParams& P, int32_t dtype, void* cublas_handle, cudaStream_t s);
-cudaError_t prefill_cublas_create(void** handle);
-void prefill_cublas_destroy(void* handle);
+cudaError_t launch_prefill_simt(const PrefillParams& P, int32_t dtype, cudaStream_t s);
+struct PfPlan;               // prefill_tc.cu: TMA maps + launch geometry
+struct TcPlan;
+cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& geom, const TcPlan* tc, int num_sms);
+void pf_plan_destroy(PfPlan* plan);
+void pf_scratch(const PfPlan* plan, int n_sites, int64_t T, int64_t* u_elems, int64_t* z_elems);
+cudaError_t launch_prefill_tc(const PfPlan* plan, const PrefillParams& P, int layer, const int kinds[3],
+                              cudaStream_t s);
 
 // Tensor-core switch (switch_tc_dispatch.cu / switch_tc_fc.cu).
 struct TcPlan;   // opaque: packed operands + TMA descriptors
@@ -245,6 +251,8 @@ cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4]
 cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, const void* xs,
                                    float* ys);
 int tc_plan_kernel(const TcPlan* plan);   // 3: fc fold, 4: fc per-term, 5: fc per-term with B per unit
+// packed, pre-swizzled B of one kind [L*N, dout_pad, rp] (also the prefill's LoRA-up operand)
+const void* tc_plan_packed_B(const TcPlan* plan, int kind, int64_t* dout_pad, int* rp);
 // RESTORE source: encode tensor maps over geom.kind[k].P (lsw_attach_pristine)
 cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& geom);
 

@@ -1,0 +1,473 @@
+// prefill_tc.cu -- the unmerged prefill of one GEMV group for T prompt tokens
+// on the 5th-gen tensor cores ("For the prefilling
+// phase, we have not implemented specific optimizations"): every token t
+// carries its own pre-gated decision (idx[t], gate[t]), so nothing can be
+// merged and Eq. 2 is evaluated as written,
+//     Y[t] = W x_t + sum_j (alpha/r) g_tj B_{e_tj} (A_{e_tj} x_t).
+//
+// Three launches per group, all our kernels (no library GEMM):
+//  1. LoRA-down, prefill_gemm<MODE_U>: U[t][q][e*r + rho] = A_q[e][rho, :] . x_t
+//     for EVERY expert e of every site q -- the bank A_q [N, r, d_in] is one
+//     [N*r, d_in] K-major matrix, so this is a dense GEMM with N*r rows (N/k
+//     times the products a gather would need, on tensor cores, reading A once).
+//     Few row tiles, so K is split over the grid; fp32 partials per split.
+//  2. prefill_zbuild: Z[t][q][e*rp + rho] = c_t(e) * sum_split U, with
+//     c_t(e) = sum_j [e_tj == e] (alpha/r) g_tj (zero for experts t did not
+//     select), stored as an exact-to-2^-16 pair of bf16 parts (hi, lo) --
+//     the coefficient and U are not rounded to bf16 (R13) -- in the
+//     pre-swizzled K-major layout of a tcgen05 operand.
+//  3. prefill_gemm<MODE_Y>: one tile = 128 output rows x 128 tokens,
+//        D = W_tile . X_tile^T                    (K = d_in, TMA 128B-swizzled boxes)
+//          + sum_e B_e,tile . (Zhi_e + Zlo_e)^T   (K = 2 N rp, bulk copies)
+//     accumulated in fp32 in TMEM by one chain of tcgen05.mma (M = 128,
+//     N = 128) -- the LoRA-up term is just N*2*rp more K of the same
+//     contraction -- then written to Y (fp32) by the epilogue warps.
+// Warp roles: 0 TMA/bulk producer, 1 MMA issuer (+ TMEM alloc), 2-5 epilogue
+// (TMEM lane quarter = warp % 4).  Persistent grid, tiles dealt round-robin
+// with the token tile fastest, so the CTAs that share a W strip run together
+// (one HBM read of W per strip, the X tiles stay in L2).
+#include <cstring>
+
+#include "tc_common.cuh"
+
+namespace lsw {
+namespace pf {
+
+using namespace tcx;
+
+constexpr int kTM = 128;        // output rows per tile (UMMA M, TMEM lanes)
+constexpr int kTT = 128;        // tokens per tile (UMMA N, accumulator columns)
+constexpr int kKB = 64;         // K per dense stage: one 128-B swizzle box
+constexpr int kBoxBytes = kTM * kKB * 2;       // 16 KB
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 32 * (2 + kEpiWarps);
+constexpr int kMaxStages = 8;
+constexpr int kAccBufs = 2;
+constexpr int MODE_Y = 0, MODE_U = 1;
+
+struct Maps {
+  CUtensorMap op[3];   // MODE_Y: W of site q [L, d_out, d_in]; MODE_U: A of site q [L, N*r, d_in]
+  CUtensorMap x;       // X [T, d_in]
+};
+
+struct Args {
+  int32_t mode, n_sites, layer, n_tt, n_kb, splits, total_tiles;
+  int32_t row_tiles_total;
+  int32_t tile_row0[4];          // prefix sums of the sites' row tiles
+  int64_t rows_valid[3];         // output rows per site (d_out or N*r)
+  int64_t col0[3];               // column of site q's row 0 in the output row
+  int64_t ld;                    // output row stride (elements)
+  int64_t T;
+  float* out;                    // MODE_Y: Y [T, ld]; MODE_U: U [splits, T, ld]
+  // MODE_Y LoRA-up stages
+  int32_t n_experts, rp;
+  uint32_t term_bytes;           // 128 x rp bf16 (one B slice / one Z part)
+  uint32_t swz;                  // UMMA layout type of the rp-wide operands
+  const __nv_bfloat16* Bp[3];    // site q: packed B of this layer [N, dout_pad, rp], pre-swizzled
+  int64_t dout_pad[3];
+  const __nv_bfloat16* Z;        // [n_tt][n_sites][N][2][128][rp], pre-swizzled
+  uint32_t stage_bytes, b_off;   // stage = [A part | B part at b_off]
+  int32_t stages;
+};
+
+struct TileAt {
+  int q, rb, tt, kb0, kb1;
+};
+
+__device__ __forceinline__ TileAt tile_at(const Args& a, int t) {
+  TileAt r;
+  r.tt = t % a.n_tt;
+  int rest = t / a.n_tt;
+  int split = 0;
+  if (a.mode == MODE_U) {
+    split = rest / a.row_tiles_total;
+    rest -= split * a.row_tiles_total;
+  }
+  r.q = (a.n_sites > 2 && rest >= a.tile_row0[2]) ? 2 : (a.n_sites > 1 && rest >= a.tile_row0[1]) ? 1 : 0;
+  r.rb = rest - a.tile_row0[r.q];
+  if (a.mode == MODE_U) {
+    r.kb0 = (int)((int64_t)a.n_kb * split / a.splits);
+    r.kb1 = (int)((int64_t)a.n_kb * (split + 1) / a.splits);
+  } else {
+    r.kb0 = 0;
+    r.kb1 = a.n_kb;
+  }
+  return r;
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint32_t s_tmem_base;
+  __shared__ __align__(8) uint64_t bar_full[kMaxStages], bar_empty[kMaxStages];
+  __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool lora = a.mode == MODE_Y && a.n_experts > 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(smem_u32(&bar_full[s]), 1);
+      mbar_init(smem_u32(&bar_empty[s]), 1);
+    }
+    for (int s = 0; s < kAccBufs; ++s) {
+      mbar_init(smem_u32(&bar_accfull[s]), 1);
+      mbar_init(smem_u32(&bar_accempty[s]), kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    for (int q = 0; q < a.n_sites; ++q) prefetch_map(&maps.op[q]);
+    prefetch_map(&maps.x);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(&s_tmem_base)), "r"(kAccBufs * kTT) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = s_tmem_base;
+
+  if (warp == 0) {
+    // ============================ producer ==================================
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();     // W / A: streamed once per strip
+      const uint64_t pol_x = policy_evict_last();      // X, B, Z: reused by many tiles
+      Ring ring{0, 0, (uint32_t)a.stages};
+      for (int t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {
+        const TileAt ta = tile_at(a, t);
+        for (int kb = ta.kb0; kb < ta.kb1; ++kb) {
+          mbar_wait(smem_u32(&bar_empty[ring.i]), ring.phase ^ 1);
+          uint8_t* st = base + (size_t)ring.i * a.stage_bytes;
+          const uint32_t bar = smem_u32(&bar_full[ring.i]);
+          mbar_expect_tx(bar, 2 * kBoxBytes);
+          tma_load_3d(smem_u32(st), &maps.op[ta.q], kb * kKB, ta.rb * kTM, a.layer, bar, pol_w);
+          tma_load_2d(smem_u32(st + a.b_off), &maps.x, kb * kKB, ta.tt * kTT, bar, pol_x);
+          ring.next();
+        }
+        if (lora) {
+          for (int e = 0; e < a.n_experts; ++e) {
+            mbar_wait(smem_u32(&bar_empty[ring.i]), ring.phase ^ 1);
+            uint8_t* st = base + (size_t)ring.i * a.stage_bytes;
+            const uint32_t bar = smem_u32(&bar_full[ring.i]);
+            mbar_expect_tx(bar, 3 * a.term_bytes);
+            bulk_load(smem_u32(st), a.Bp[ta.q] + ((size_t)e * a.dout_pad[ta.q] + (size_t)ta.rb * kTM) * a.rp,
+                      a.term_bytes, bar, pol_x);
+            const __nv_bfloat16* z =
+                a.Z + ((((size_t)ta.tt * a.n_sites + ta.q) * a.n_experts + e) * 2) * (size_t)kTT * a.rp;
+            bulk_load(smem_u32(st + a.b_off), z, 2 * a.term_bytes, bar, pol_x);     // hi, lo: contiguous
+            ring.next();
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer ================================
+    // D f32, A/B bf16, both K-major, N = 128 (tokens), M = 128 (rows)
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTT >> 3) << 17) |
+                           ((uint32_t)(kTM >> 4) << 24);
+    const uint64_t dense0 = umma_desc(0, 1024, 2);                       // 128-B rows, SWIZZLE_128B
+    const uint64_t lora0 = umma_desc(0, 8 * (uint32_t)a.rp * 2, a.swz);  // rp-wide rows
+    const uint64_t zpart = a.term_bytes >> 4;
+    Ring ring{0, 0, (uint32_t)a.stages};
+    Ring acc{0, 0, kAccBufs};
+    for (int t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {
+      const TileAt ta = tile_at(a, t);
+      mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc.i * kTT;
+      uint32_t accum = 0;
+      for (int kb = ta.kb0; kb < ta.kb1; ++kb) {
+        mbar_wait(smem_u32(&bar_full[ring.i]), ring.phase);
+        tc_fence_after();
+        const uint32_t st = smem_u32(base + (size_t)ring.i * a.stage_bytes);
+        const uint64_t da = dense0 + (st >> 4), db = dense0 + ((st + a.b_off) >> 4);
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < kKB / 16; ++kk) umma_f16(d, da + kk * 2, db + kk * 2, idesc, accum | kk);
+          umma_commit(smem_u32(&bar_empty[ring.i]));      // stage free once these MMAs complete
+        }
+        __syncwarp();
+        accum = 1;
+        ring.next();
+      }
+      if (lora) {
+        const int ksteps = a.rp / 16;
+        for (int e = 0; e < a.n_experts; ++e) {
+          mbar_wait(smem_u32(&bar_full[ring.i]), ring.phase);
+          tc_fence_after();
+          const uint32_t st = smem_u32(base + (size_t)ring.i * a.stage_bytes);
+          const uint64_t da = lora0 + (st >> 4), db = lora0 + ((st + a.b_off) >> 4);
+          if (elect_one()) {
+            for (int part = 0; part < 2; ++part)
+              for (int kk = 0; kk < ksteps; ++kk)
+                umma_f16(d, da + kk * 2, db + part * zpart + kk * 2, idesc, 1u);
+            umma_commit(smem_u32(&bar_empty[ring.i]));
+          }
+          __syncwarp();
+          ring.next();
+        }
+      }
+      if (elect_one()) umma_commit(smem_u32(&bar_accfull[acc.i]));   // accumulator complete
+      __syncwarp();
+      acc.next();
+    }
+  } else {
+    // ============================ epilogue ==================================
+    // thread = one output row of the tile (TMEM lane); 16 token columns per
+    // tcgen05.ld; a warp's 32 stores of one token are 128 contiguous bytes
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    Ring acc{0, 0, kAccBufs};
+    for (int t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {
+      const TileAt ta = tile_at(a, t);
+      mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);
+      tc_fence_after();
+      const int64_t grow = (int64_t)ta.rb * kTM + row;
+      const bool ok = grow < a.rows_valid[ta.q];
+      const int split = a.mode == MODE_U ? t / a.n_tt / a.row_tiles_total : 0;
+      float* outp = a.out + (int64_t)split * a.T * a.ld + a.col0[ta.q] + grow;
+      const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTT;
+      for (int c0 = 0; c0 < kTT; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tm + c0, v);
+        tmem_wait_ld();
+        const int64_t tok0 = (int64_t)ta.tt * kTT + c0;
+        if (ok) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (tok0 + i < a.T) outp[(tok0 + i) * a.ld] = __uint_as_float(v[i]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+      acc.next();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAccBufs * kTT)
+                 : "memory");
+  }
+}
+
+// Z (hi, lo) parts from the split-K LoRA-down partials: one thread per
+// (token tile, site, expert, token in tile, rho < rp).
+__global__ void prefill_zbuild(const float* __restrict__ U, int splits, int64_t T, int64_t ldu, int n_sites, int N,
+                               int r, int rp, int k, float scale, const int32_t* __restrict__ idx,
+                               const float* __restrict__ gate, __nv_bfloat16* __restrict__ Z, int n_tt) {
+  const int64_t total = (int64_t)n_tt * n_sites * N * kTT * rp;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int rho = (int)(i % rp);
+    int64_t rest = i / rp;
+    const int tin = (int)(rest % kTT);
+    rest /= kTT;
+    const int e = (int)(rest % N);
+    rest /= N;
+    const int q = (int)(rest % n_sites);
+    const int tt = (int)(rest / n_sites);
+    const int64_t t = (int64_t)tt * kTT + tin;
+    float z = 0.f;
+    if (t < T && rho < r) {
+      float c = 0.f;
+      for (int j = 0; j < k; ++j)
+        if (idx[t * k + j] == e) c += scale * gate[t * k + j];
+      if (c != 0.f) {
+        const int64_t col = (int64_t)q * N * r + (int64_t)e * r + rho;
+        float u = 0.f;
+        for (int s = 0; s < splits; ++s) u += U[((int64_t)s * T + t) * ldu + col];    // split order: deterministic
+        z = c * u;
+      }
+    }
+    const __nv_bfloat16 hi = __float2bfloat16_rn(z);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(z - __bfloat162float(hi));    // z - hi exact in fp32
+    __nv_bfloat16* blk = Z + ((((int64_t)tt * n_sites + q) * N + e) * 2) * (int64_t)kTT * rp;
+    const int64_t off = swz_off(tin, rho, rp);
+    blk[off] = hi;
+    blk[(int64_t)kTT * rp + off] = lo;
+  }
+}
+
+}  // namespace pf
+
+// ------------------------------------------------------------------ host side
+
+struct PfPlan {
+  CUtensorMap w[LSW_NKIND], a[LSW_NKIND];
+  const __nv_bfloat16* Bp[LSW_NKIND];
+  int64_t dout_pad[LSW_NKIND], d_out[LSW_NKIND], d_in[LSW_NKIND];
+  int n_layers, n_experts, r, rp, num_sms;
+  int stages;
+  uint32_t stage_bytes, b_off, smem;
+};
+
+static PFN_cuTensorMapEncodeTiled_v12000 pf_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// bf16 [.., rows, cols] row-major, box {64, 128(, 1)}, 128-B swizzle, zero OOB fill
+static bool pf_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t L) {
+  auto enc = pf_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {cols, rows, L};
+  cuuint64_t strides[2] = {cols * 2, cols * rows * 2};
+  cuuint32_t box[3] = {(cuuint32_t)pf::kKB, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L ? 3 : 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* tc, int num_sms) {
+  *out = nullptr;
+  PfPlan* p = new PfPlan();
+  memset(p, 0, sizeof(*p));
+  p->n_layers = sp.n_layers;
+  p->n_experts = sp.n_experts;
+  p->r = sp.rank;
+  p->num_sms = num_sms;
+  for (int k = 0; k < LSW_NKIND; ++k) {
+    const KindGeom& g = sp.kind[k];
+    int rp = 0;
+    p->Bp[k] = static_cast<const __nv_bfloat16*>(tc_plan_packed_B(tc, k, &p->dout_pad[k], &rp));
+    p->rp = rp;
+    p->d_out[k] = g.d_out;
+    p->d_in[k] = g.d_in;
+    if (!p->Bp[k] || !pf_map(&p->w[k], g.W, g.d_in, g.d_out, sp.n_layers) ||
+        !pf_map(&p->a[k], g.A, g.d_in, (uint64_t)sp.n_experts * sp.rank, sp.n_layers)) {
+      delete p;
+      return cudaErrorInvalidValue;
+    }
+  }
+  // stage = [128 x 64 A box | B part]: the dense B part is a 128 x 64 box, the
+  // LoRA stage's B part the (hi, lo) pair of one expert's Z slice
+  const uint32_t term = (uint32_t)pf::kTM * p->rp * 2;
+  p->b_off = pf::kBoxBytes;
+  const uint32_t bpart = 2 * term > (uint32_t)pf::kBoxBytes ? 2 * term : (uint32_t)pf::kBoxBytes;
+  p->stage_bytes = p->b_off + bpart;
+  const uint32_t budget = 220 * 1024;
+  p->stages = (int)(budget / p->stage_bytes);
+  if (p->stages > pf::kMaxStages) p->stages = pf::kMaxStages;
+  if (p->stages < 2) { delete p; return cudaErrorNotSupported; }
+  p->smem = p->stages * p->stage_bytes + 1024;
+  cudaError_t e = cudaFuncSetAttribute(pf::prefill_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
+  if (e != cudaSuccess) { delete p; return e; }
+  *out = p;
+  return cudaSuccess;
+}
+
+void pf_plan_destroy(PfPlan* p) { delete p; }
+
+// scratch sizes (elements) a launch with T tokens needs
+void pf_scratch(const PfPlan* p, int n_sites, int64_t T, int64_t* u_elems, int64_t* z_elems) {
+  const int64_t nr = (int64_t)p->n_experts * p->r;
+  const int64_t n_tt = (T + pf::kTT - 1) / pf::kTT;
+  *u_elems = (int64_t)p->num_sms * T * n_sites * nr;          // splits <= num_sms
+  *z_elems = n_tt * n_sites * p->n_experts * 2 * pf::kTT * p->rp;
+}
+
+cudaError_t launch_prefill_tc(const PfPlan* p, const PrefillParams& P, int layer, const int kinds[3],
+                              cudaStream_t s) {
+  using namespace pf;
+  Maps maps;
+  memset(&maps, 0, sizeof(maps));
+  if (!pf_map(&maps.x, P.X, P.d_in, P.T, 0)) return cudaErrorInvalidValue;
+  const int n_tt = (int)((P.T + kTT - 1) / kTT);
+  const int n_kb = (int)((P.d_in + kKB - 1) / kKB);
+  const int64_t nr = (int64_t)p->n_experts * p->r;
+  // ---- 1. LoRA-down (every expert), K split over the grid
+  Args a;
+  memset(&a, 0, sizeof(a));
+  a.mode = MODE_U;
+  a.n_sites = P.n_sites;
+  a.layer = layer;
+  a.n_tt = n_tt;
+  a.n_kb = n_kb;
+  a.T = P.T;
+  int rt = 0;
+  for (int q = 0; q < P.n_sites; ++q) {
+    maps.op[q] = p->a[kinds[q]];
+    a.tile_row0[q] = rt;
+    rt += (int)((nr + kTM - 1) / kTM);
+    a.rows_valid[q] = nr;
+    a.col0[q] = q * nr;
+  }
+  a.tile_row0[P.n_sites] = rt;
+  a.row_tiles_total = rt;
+  int splits = p->num_sms / (rt * n_tt);
+  if (splits < 1) splits = 1;
+  if (splits > n_kb) splits = n_kb;
+  a.splits = splits;
+  a.total_tiles = rt * n_tt * splits;
+  a.ld = P.n_sites * nr;
+  a.out = P.U;
+  a.stages = p->stages;
+  a.stage_bytes = p->stage_bytes;
+  a.b_off = p->b_off;
+  a.rp = p->rp;
+  int grid = a.total_tiles < p->num_sms ? a.total_tiles : p->num_sms;
+  prefill_gemm<<<grid, kThreads, p->smem, s>>>(maps, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // ---- 2. gate-scaled (hi, lo) LoRA-down products of the selected experts
+  {
+    const int64_t n = (int64_t)n_tt * P.n_sites * p->n_experts * kTT * p->rp;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 4 * p->num_sms) blocks = 4 * p->num_sms;
+    prefill_zbuild<<<blocks, 256, 0, s>>>(P.U, splits, P.T, a.ld, P.n_sites, p->n_experts, p->r, p->rp, P.k,
+                                          P.scale, P.idx, P.gate, reinterpret_cast<__nv_bfloat16*>(P.Z), n_tt);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  // ---- 3. dense part + LoRA-up in one contraction per tile
+  Args y = a;
+  y.mode = MODE_Y;
+  y.splits = 1;
+  rt = 0;
+  for (int q = 0; q < P.n_sites; ++q) {
+    const int kd = kinds[q];
+    maps.op[q] = p->w[kd];
+    y.tile_row0[q] = rt;
+    rt += (int)((p->d_out[kd] + kTM - 1) / kTM);
+    y.rows_valid[q] = p->d_out[kd];
+    y.col0[q] = P.row_begin[q];
+    y.Bp[q] = p->Bp[kd] + (size_t)layer * p->n_experts * p->dout_pad[kd] * p->rp;
+    y.dout_pad[q] = p->dout_pad[kd];
+  }
+  y.tile_row0[P.n_sites] = rt;
+  y.row_tiles_total = rt;
+  y.total_tiles = rt * n_tt;
+  y.ld = P.rows;
+  y.out = P.Y;
+  y.n_experts = p->n_experts;
+  y.term_bytes = (uint32_t)kTM * p->rp * 2;
+  y.swz = p->rp == 16 ? 6u : p->rp == 32 ? 4u : 2u;     // SWIZZLE_32B / 64B / 128B
+  y.Z = reinterpret_cast<const __nv_bfloat16*>(P.Z);
+  grid = y.total_tiles < p->num_sms ? y.total_tiles : p->num_sms;
+  prefill_gemm<<<grid, kThreads, p->smem, s>>>(maps, y);
+  return cudaGetLastError();
+}
+
+}  // namespace lsw

@@ -63,6 +63,9 @@ int tc_plan_grid(const TcPlan* p) { return fc::tc_plan_grid(p->c); }
 int tc_plan_tile_n(const TcPlan* p) { return fc::tc_plan_tile_n(p->c); }
 int64_t tc_plan_tiles(const TcPlan* p) { return fc::tc_plan_tiles(p->c); }
 int tc_plan_kernel(const TcPlan* p) { return p->which; }
+const void* tc_plan_packed_B(const TcPlan* p, int kind, int64_t* dout_pad, int* rp) {
+  return fc::tc_plan_packed_B(p->c, kind, dout_pad, rp);
+}
 
 cudaError_t launch_switch_tc(const TcPlan* p, const SwitchParams& sp, cudaStream_t s, int64_t t0, int64_t t_count) {
   return fc::launch_switch_tc(p->c, sp, s, t0, t_count);

@@ -1082,6 +1082,11 @@ int64_t tc_plan_bytes(const TcPlan* plan) { return plan ? plan->bytes : 0; }
 int tc_plan_grid(const TcPlan* plan) { return plan ? plan->grid : 0; }
 int tc_plan_tile_n(const TcPlan* plan) { return plan ? kTN : 0; }
 int64_t tc_plan_tiles(const TcPlan* plan) { return plan ? plan->geom.tiles_total : 0; }
+const void* tc_plan_packed_B(const TcPlan* plan, int kind, int64_t* dout_pad, int* rp) {
+  *dout_pad = plan->geom.dout_pad[kind];
+  *rp = plan->geom.rp;
+  return plan->packed_B[kind];
+}
 
 cudaError_t tc_plan_set_pristine(TcPlan* plan, const SwitchParams& sp) {
   for (int k = 0; k < LSW_NKIND; ++k)

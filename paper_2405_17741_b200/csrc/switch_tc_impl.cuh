@@ -30,6 +30,7 @@ cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4]
                               int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]);
 cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, const void* xs,
                                    float* ys);
+const void* tc_plan_packed_B(const TcPlan* plan, int kind, int64_t* dout_pad, int* rp);
 }  // namespace fc
 
 }  // namespace lsw

@@ -1,11 +1,14 @@
 """Unmerged prefill vs the oracle (-m gpu).
 
 lsw_prefill_group evaluates Eq. 2 for T prompt tokens, each with its
-own pre-gated decision (the router applied to that token's x¹): the dense part
-by cuBLAS, the LoRA-down / LoRA-up parts by two kernels.  Checked through the C
-ABI against oracle.unmerged_forward token by token (fp64), for bf16 and fp32
-storage, k*r below and above a warp, ragged T; the result is deterministic;
-a merged ctx is refused.
+own pre-gated decision (the router applied to that token's x¹): bf16 on the
+tcgen05 path (LoRA-down GEMM over every expert, split K; (hi, lo) Z build; one
+contraction per tile over d_in + 2 N rp), fp32 / SIMT switch on the CUDA-core
+path.  Checked through the C ABI against oracle.unmerged_forward token by
+token (fp64): every row at mini sizes (several 128-token tiles with a ragged
+tail, rp = 16 / 32 / 64, k = 1 .. 4), sampled rows at the full widths of the
+7B and 13B shapes (K = 4096 / 5120 / 11008 / 13824, split-K LoRA-down); the
+result is deterministic; a merged ctx is refused.
 """
 import numpy as np
 import pytest
@@ -26,7 +29,8 @@ def _f64(t):
 
 
 @pytest.mark.parametrize("name,impl,T", [("toy", "simt", 5), ("mini", "tc", 7), ("mini-r64k3", "tc", 3),
-                                         ("mini-r4k4", "tc", 33)])
+                                         ("mini-r4k4", "tc", 33), ("mini", "tc", 300), ("mini-r32", "tc", 129),
+                                         ("mini-k1", "tc", 130), ("mini-r64k4", "tc", 64), ("mini", "simt", 9)])
 def test_prefill_matches_oracle(name, impl, T):
     cfg = synth.get_config(name)
     W, A, B, router = H.build_weights(cfg, "cuda")
@@ -80,3 +84,50 @@ def test_prefill_refused_on_a_merged_ctx():
     with pytest.raises(L.LswError) as ei:
         sw.prefill_group(0, 0, X, idx, gate, Y)
     assert "STATE" in str(ei.value)
+
+
+def _rows(d_out, seed):
+    base = {0, 1, 127, 128, 129, d_out - 1}
+    base |= set(np.random.default_rng(seed).choice(d_out, size=12, replace=False).tolist())
+    return sorted(r for r in base if 0 <= r < d_out)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,T", [("llama2-7b", 300), ("llama2-13b", 200)])
+def test_prefill_full_width_sampled_rows(name, T):
+    """One layer at the real widths: every group (K = d_model and K = d_ff),
+    every token, sampled rows of every site (row sampling is exact: row i of Y
+    needs row i of W and B and all of A)."""
+    cfg = synth.get_config(name).with_(n_layers=1)
+    W, A, B, router = H.build_weights(cfg, "cuda")
+    sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+    X1 = synth.gen_x1(cfg, T, "cuda")
+    k = cfg.top_k
+    idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    gate = torch.empty(T, k, dtype=torch.float32, device="cuda")
+    for t in range(T):
+        sw.router_topk(X1[t], idx[t], gate[t])
+    scale = cfg.alpha / cfg.rank
+    g = torch.Generator(device="cpu").manual_seed(2405177410 + 98)
+    idx_h, gate_h = idx.cpu().tolist(), gate.cpu().tolist()
+    for gi, grp in enumerate(synth.GROUPS):
+        d_in = cfg.kind_shape(grp[0])[1]
+        rows = sum(cfg.kind_shape(kd)[0] for kd in grp)
+        X = torch.randn(T, d_in, generator=g).to(torch.bfloat16).cuda()
+        Y = torch.full((T, rows), float("nan"), device="cuda")
+        sw.prefill_group(0, gi, X, idx, gate, Y)
+        torch.cuda.synchronize()
+        Yh, Xh = Y.cpu().numpy(), _f64(X)
+        o = 0
+        for i, kd in enumerate(grp):
+            d_out = cfg.kind_shape(kd)[0]
+            rs = _rows(d_out, 31 + 7 * gi + i)
+            Wr, Ar, Br = _f64(W[kd][0][rs]), _f64(A[kd][0]), _f64(B[kd][0][:, rs, :])
+            for t in range(T):
+                coefs = [(int(e), scale * float(gv)) for e, gv in zip(idx_h[t], gate_h[t])]
+                ref = O.unmerged_forward(Wr, Ar, Br, coefs, Xh[t])
+                np.testing.assert_allclose(Yh[t, o + np.array(rs)], ref, rtol=1e-4,
+                                           atol=1e-4 * float(np.abs(ref).max()), err_msg=f"{kd} t={t}")
+            o += d_out
+        assert not np.isnan(Yh).any()
+    assert sw.device_status() == 0
