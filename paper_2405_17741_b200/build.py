@@ -29,15 +29,15 @@ def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
-def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+def _compile(src: str, verbose: bool, tuning: bool = False) -> str:
+    obj = os.path.join(BUILD + ("_tuning" if tuning else ""), os.path.basename(src) + ".o")
     # headers, and every .cu (switch_tc_fused.cu #includes switch_tc.cu)
     deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".cu"))]
     inc = os.path.join(ROOT, "include")
     deps += [os.path.join(inc, f) for f in os.listdir(inc) if f.endswith(".h")]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *(["-DLSW_TUNING"] if tuning else []), "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{res.stdout}\n{res.stderr}")
@@ -48,12 +48,20 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, tuning: bool = False) -> str:
+    """tuning=True: the measurement build (-DLSW_TUNING: probe options that
+    produce deliberately wrong results take effect), objects in build_tuning/,
+    linked to the same liblsw.so -- for tuning scripts only; rebuild without
+    it before tests or the bench."""
+    bdir = BUILD + ("_tuning" if tuning else "")
+    os.makedirs(bdir, exist_ok=True)
     srcs = sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
+        objs = list(ex.map(lambda s: _compile(s, verbose, tuning), srcs))
+    stamp = LIB + ".flavor"
+    flavor = "tuning" if tuning else "release"
+    same = os.path.exists(stamp) and open(stamp).read() == flavor
+    if same and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
@@ -61,8 +69,10 @@ def build(verbose: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
     os.replace(tmp, LIB)
+    with open(stamp, "w") as f:
+        f.write(flavor)
     return LIB
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, tuning="--tuning" in sys.argv))

@@ -36,7 +36,7 @@ namespace pf {
 using namespace tcx;
 
 constexpr int kTM = 128;        // output rows per tile (UMMA M, TMEM lanes)
-constexpr int kTT = 128;        // tokens per tile (UMMA N, accumulator columns)
+constexpr int kTTMax = 256;     // tokens per tile (UMMA N, accumulator columns): 128 or 256
 constexpr int kKB = 64;         // K per dense stage: one 128-B swizzle box
 constexpr int kBoxBytes = kTM * kKB * 2;       // 16 KB
 constexpr int kEpiWarps = 4;
@@ -61,11 +61,12 @@ struct Args {
   float* out;                    // MODE_Y: Y [T, ld]; MODE_U: U [splits, T, ld]
   // MODE_Y LoRA-up stages
   int32_t n_experts, rp;
-  uint32_t term_bytes;           // 128 x rp bf16 (one B slice / one Z part)
+  uint32_t term_bytes;           // 128 x rp bf16 (one B slice)
+  uint32_t zpart_bytes;          // kTT x rp bf16 (one Z part)
   uint32_t swz;                  // UMMA layout type of the rp-wide operands
   const __nv_bfloat16* Bp[3];    // site q: packed B of this layer [N, dout_pad, rp], pre-swizzled
   int64_t dout_pad[3];
-  const __nv_bfloat16* Z;        // [n_tt][n_sites][N][2][128][rp], pre-swizzled
+  const __nv_bfloat16* Z;        // [n_tt][n_sites][N][2][kTT][rp], pre-swizzled
   uint32_t stage_bytes, b_off;   // stage = [A part | B part at b_off]
   int32_t stages;
 };
@@ -74,7 +75,7 @@ struct TileAt {
   int q, rb, tt, kb0, kb1;
 };
 
-__device__ __forceinline__ TileAt tile_at(const Args& a, int t) {
+__device__ __forceinline__ TileAt tile_at(const Args& a, int t) {  // token tile fastest
   TileAt r;
   r.tt = t % a.n_tt;
   int rest = t / a.n_tt;
@@ -104,6 +105,7 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+template <int kTT>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -151,9 +153,9 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
           mbar_wait(smem_u32(&bar_empty[ring.i]), ring.phase ^ 1);
           uint8_t* st = base + (size_t)ring.i * a.stage_bytes;
           const uint32_t bar = smem_u32(&bar_full[ring.i]);
-          mbar_expect_tx(bar, 2 * kBoxBytes);
+          mbar_expect_tx(bar, kBoxBytes + kTT * kKB * 2);
           tma_load_3d(smem_u32(st), &maps.op[ta.q], kb * kKB, ta.rb * kTM, a.layer, bar, pol_w);
-          tma_load_2d(smem_u32(st + a.b_off), &maps.x, kb * kKB, ta.tt * kTT, bar, pol_x);
+          tma_load_2d(smem_u32(st + a.b_off), &maps.x, kb * kKB, ta.tt * kTT, bar, pol_x);   // box {64, kTT}
           ring.next();
         }
         if (lora) {
@@ -161,12 +163,12 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
             mbar_wait(smem_u32(&bar_empty[ring.i]), ring.phase ^ 1);
             uint8_t* st = base + (size_t)ring.i * a.stage_bytes;
             const uint32_t bar = smem_u32(&bar_full[ring.i]);
-            mbar_expect_tx(bar, 3 * a.term_bytes);
+            mbar_expect_tx(bar, a.term_bytes + 2 * a.zpart_bytes);
             bulk_load(smem_u32(st), a.Bp[ta.q] + ((size_t)e * a.dout_pad[ta.q] + (size_t)ta.rb * kTM) * a.rp,
                       a.term_bytes, bar, pol_x);
             const __nv_bfloat16* z =
                 a.Z + ((((size_t)ta.tt * a.n_sites + ta.q) * a.n_experts + e) * 2) * (size_t)kTT * a.rp;
-            bulk_load(smem_u32(st + a.b_off), z, 2 * a.term_bytes, bar, pol_x);     // hi, lo: contiguous
+            bulk_load(smem_u32(st + a.b_off), z, 2 * a.zpart_bytes, bar, pol_x);    // hi, lo: contiguous
             ring.next();
           }
         }
@@ -179,7 +181,7 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
                            ((uint32_t)(kTM >> 4) << 24);
     const uint64_t dense0 = umma_desc(0, 1024, 2);                       // 128-B rows, SWIZZLE_128B
     const uint64_t lora0 = umma_desc(0, 8 * (uint32_t)a.rp * 2, a.swz);  // rp-wide rows
-    const uint64_t zpart = a.term_bytes >> 4;
+    const uint64_t zpart = a.zpart_bytes >> 4;
     Ring ring{0, 0, (uint32_t)a.stages};
     Ring acc{0, 0, kAccBufs};
     for (int t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {
@@ -269,7 +271,7 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
 // (token tile, site, expert, token in tile, rho < rp).
 __global__ void prefill_zbuild(const float* __restrict__ U, int splits, int64_t T, int64_t ldu, int n_sites, int N,
                                int r, int rp, int k, float scale, const int32_t* __restrict__ idx,
-                               const float* __restrict__ gate, __nv_bfloat16* __restrict__ Z, int n_tt) {
+                               const float* __restrict__ gate, __nv_bfloat16* __restrict__ Z, int n_tt, int kTT) {
   const int64_t total = (int64_t)n_tt * n_sites * N * kTT * rp;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int rho = (int)(i % rp);
@@ -311,9 +313,28 @@ struct PfPlan {
   const __nv_bfloat16* Bp[LSW_NKIND];
   int64_t dout_pad[LSW_NKIND], d_out[LSW_NKIND], d_in[LSW_NKIND];
   int n_layers, n_experts, r, rp, num_sms;
-  int stages;
-  uint32_t stage_bytes, b_off, smem;
+  int tt_opt;                    // variant option pf_tt (128 | 256), 0: chosen per launch
 };
+
+// shared-memory plan of one token-tile width: stage = [128 x 64 A box | B
+// part], the B part a TT x 64 X box (dense) or the (hi, lo) pair of one
+// expert's TT x rp Z slice (LoRA-up)
+struct PfGeom {
+  uint32_t stage_bytes, b_off, smem;
+  int stages;
+};
+static constexpr uint32_t kPfBudget = 220 * 1024;
+
+static PfGeom pf_geom(int tt, int rp) {
+  PfGeom g;
+  g.b_off = pf::kBoxBytes;
+  const uint32_t dense_b = (uint32_t)tt * pf::kKB * 2, lora_b = 2u * tt * rp * 2;
+  g.stage_bytes = g.b_off + (dense_b > lora_b ? dense_b : lora_b);
+  g.stages = (int)(kPfBudget / g.stage_bytes);
+  if (g.stages > pf::kMaxStages) g.stages = pf::kMaxStages;
+  g.smem = g.stages * g.stage_bytes + 1024;
+  return g;
+}
 
 static PFN_cuTensorMapEncodeTiled_v12000 pf_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -327,13 +348,14 @@ static PFN_cuTensorMapEncodeTiled_v12000 pf_encode() {
   return fn;
 }
 
-// bf16 [.., rows, cols] row-major, box {64, 128(, 1)}, 128-B swizzle, zero OOB fill
-static bool pf_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t L) {
+// bf16 [.., rows, cols] row-major, box {64, box_rows(, 1)}, 128-B swizzle, zero OOB fill
+static bool pf_map(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t L,
+                   uint32_t box_rows = 128) {
   auto enc = pf_encode();
   if (!enc) return false;
   cuuint64_t dims[3] = {cols, rows, L};
   cuuint64_t strides[2] = {cols * 2, cols * rows * 2};
-  cuuint32_t box[3] = {(cuuint32_t)pf::kKB, 128, 1};
+  cuuint32_t box[3] = {(cuuint32_t)pf::kKB, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, L ? 3 : 2, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -361,18 +383,14 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
       return cudaErrorInvalidValue;
     }
   }
-  // stage = [128 x 64 A box | B part]: the dense B part is a 128 x 64 box, the
-  // LoRA stage's B part the (hi, lo) pair of one expert's Z slice
-  const uint32_t term = (uint32_t)pf::kTM * p->rp * 2;
-  p->b_off = pf::kBoxBytes;
-  const uint32_t bpart = 2 * term > (uint32_t)pf::kBoxBytes ? 2 * term : (uint32_t)pf::kBoxBytes;
-  p->stage_bytes = p->b_off + bpart;
-  const uint32_t budget = 220 * 1024;
-  p->stages = (int)(budget / p->stage_bytes);
-  if (p->stages > pf::kMaxStages) p->stages = pf::kMaxStages;
-  if (p->stages < 2) { delete p; return cudaErrorNotSupported; }
-  p->smem = p->stages * p->stage_bytes + 1024;
-  cudaError_t e = cudaFuncSetAttribute(pf::prefill_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p->smem);
+  p->tt_opt = (int)opt_int("pf_tt", 0);
+  if (p->tt_opt != 128 && p->tt_opt != 256) p->tt_opt = 0;
+  if (pf_geom(128, p->rp).stages < 3) { delete p; return cudaErrorNotSupported; }
+  cudaError_t e = cudaFuncSetAttribute(pf::prefill_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(kPfBudget + 1024));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(pf::prefill_gemm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kPfBudget + 1024));
   if (e != cudaSuccess) { delete p; return e; }
   *out = p;
   return cudaSuccess;
@@ -380,20 +398,31 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
 
 void pf_plan_destroy(PfPlan* p) { delete p; }
 
+// token-tile width of a launch: 256 halves the shared-memory operand traffic
+// per MAC when the stage plan still holds >= 3 stages (rp <= 32) and the
+// extra rows of a partial 256-token tile are few
+static int pf_tt(const PfPlan* p, int64_t T) {
+  if (p->tt_opt) return p->tt_opt == 256 && pf_geom(256, p->rp).stages >= 3 ? 256 : 128;
+  return 128;
+}
+
 // scratch sizes (elements) a launch with T tokens needs
 void pf_scratch(const PfPlan* p, int n_sites, int64_t T, int64_t* u_elems, int64_t* z_elems) {
   const int64_t nr = (int64_t)p->n_experts * p->r;
-  const int64_t n_tt = (T + pf::kTT - 1) / pf::kTT;
+  const int tt = pf_tt(p, T);
+  const int64_t n_tt = (T + tt - 1) / tt;
   *u_elems = (int64_t)p->num_sms * T * n_sites * nr;          // splits <= num_sms
-  *z_elems = n_tt * n_sites * p->n_experts * 2 * pf::kTT * p->rp;
+  *z_elems = n_tt * n_sites * p->n_experts * 2 * (int64_t)tt * p->rp;
 }
 
-cudaError_t launch_prefill_tc(const PfPlan* p, const PrefillParams& P, int layer, const int kinds[3],
-                              cudaStream_t s) {
+template <int kTT>
+static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int layer, const int kinds[3],
+                                 cudaStream_t s) {
   using namespace pf;
+  const PfGeom geo = pf_geom(kTT, p->rp);
   Maps maps;
   memset(&maps, 0, sizeof(maps));
-  if (!pf_map(&maps.x, P.X, P.d_in, P.T, 0)) return cudaErrorInvalidValue;
+  if (!pf_map(&maps.x, P.X, P.d_in, P.T, 0, kTT)) return cudaErrorInvalidValue;
   const int n_tt = (int)((P.T + kTT - 1) / kTT);
   const int n_kb = (int)((P.d_in + kKB - 1) / kKB);
   const int64_t nr = (int64_t)p->n_experts * p->r;
@@ -423,12 +452,12 @@ cudaError_t launch_prefill_tc(const PfPlan* p, const PrefillParams& P, int layer
   a.total_tiles = rt * n_tt * splits;
   a.ld = P.n_sites * nr;
   a.out = P.U;
-  a.stages = p->stages;
-  a.stage_bytes = p->stage_bytes;
-  a.b_off = p->b_off;
+  a.stages = geo.stages;
+  a.stage_bytes = geo.stage_bytes;
+  a.b_off = geo.b_off;
   a.rp = p->rp;
   int grid = a.total_tiles < p->num_sms ? a.total_tiles : p->num_sms;
-  prefill_gemm<<<grid, kThreads, p->smem, s>>>(maps, a);
+  prefill_gemm<kTT><<<grid, kThreads, geo.smem, s>>>(maps, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // ---- 2. gate-scaled (hi, lo) LoRA-down products of the selected experts
@@ -437,7 +466,7 @@ cudaError_t launch_prefill_tc(const PfPlan* p, const PrefillParams& P, int layer
     int blocks = (int)((n + 255) / 256);
     if (blocks > 4 * p->num_sms) blocks = 4 * p->num_sms;
     prefill_zbuild<<<blocks, 256, 0, s>>>(P.U, splits, P.T, a.ld, P.n_sites, p->n_experts, p->r, p->rp, P.k,
-                                          P.scale, P.idx, P.gate, reinterpret_cast<__nv_bfloat16*>(P.Z), n_tt);
+                                          P.scale, P.idx, P.gate, reinterpret_cast<__nv_bfloat16*>(P.Z), n_tt, kTT);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -463,11 +492,17 @@ cudaError_t launch_prefill_tc(const PfPlan* p, const PrefillParams& P, int layer
   y.out = P.Y;
   y.n_experts = p->n_experts;
   y.term_bytes = (uint32_t)kTM * p->rp * 2;
+  y.zpart_bytes = (uint32_t)kTT * p->rp * 2;
   y.swz = p->rp == 16 ? 6u : p->rp == 32 ? 4u : 2u;     // SWIZZLE_32B / 64B / 128B
   y.Z = reinterpret_cast<const __nv_bfloat16*>(P.Z);
   grid = y.total_tiles < p->num_sms ? y.total_tiles : p->num_sms;
-  prefill_gemm<<<grid, kThreads, p->smem, s>>>(maps, y);
+  prefill_gemm<kTT><<<grid, kThreads, geo.smem, s>>>(maps, y);
   return cudaGetLastError();
+}
+
+cudaError_t launch_prefill_tc(const PfPlan* p, const PrefillParams& P, int layer, const int kinds[3],
+                              cudaStream_t s) {
+  return pf_tt(p, P.T) == 256 ? prefill_tc_tt<256>(p, P, layer, kinds, s) : prefill_tc_tt<128>(p, P, layer, kinds, s);
 }
 
 }  // namespace lsw

@@ -999,7 +999,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   plan->chunk = (int)opt_int("tc_chunk", plan->chunk);
   if (plan->chunk < 1) plan->chunk = 1;
   plan->probe = (int)probe_int("tc_probe") & 17;
-  plan->fused_probe = (int)probe_int("fc_fused_probe") & 12;   // tuning builds only: 1 W stream only, 16 no fold math
+  plan->fused_probe = (int)probe_int("fc_fused_probe") & 13;   // tuning builds only: 1 W stream only, 4 no segment wait, 8 no GEMV
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
   // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
   g.wrm = opt_int("fc_wrm", 1) != 0;
@@ -1184,7 +1184,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   a.t_count = plan->fused_tiles;
   a.g = plan->geom;
   a.chunk = 1;                     // unused: per-segment ranges (fused_from)
-  a.probe = plan->fused_probe;     // tuning builds only: 4 = no segment wait, 8 = no GEMV (results wrong)
+  a.probe = plan->fused_probe;     // tuning builds only: 1 = W stream only, 4 = no segment wait, 8 = no GEMV (results wrong)
   a.mode = p.mode;
   a.top_k = p.top_k;
   a.n_experts = p.n_experts;

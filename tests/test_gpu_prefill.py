@@ -28,10 +28,15 @@ def _f64(t):
     return t.detach().to("cpu").to(torch.float64).numpy()
 
 
-@pytest.mark.parametrize("name,impl,T", [("toy", "simt", 5), ("mini", "tc", 7), ("mini-r64k3", "tc", 3),
-                                         ("mini-r4k4", "tc", 33), ("mini", "tc", 300), ("mini-r32", "tc", 129),
-                                         ("mini-k1", "tc", 130), ("mini-r64k4", "tc", 64), ("mini", "simt", 9)])
-def test_prefill_matches_oracle(name, impl, T):
+@pytest.mark.parametrize("name,impl,T,tt", [("toy", "simt", 5, None), ("mini", "tc", 7, None),
+                                            ("mini-r64k3", "tc", 3, None), ("mini-r4k4", "tc", 33, None),
+                                            ("mini", "tc", 300, None), ("mini-r32", "tc", 129, None),
+                                            ("mini-k1", "tc", 130, None), ("mini-r64k4", "tc", 64, None),
+                                            ("mini", "simt", 9, None), ("mini", "tc", 300, 256),
+                                            ("mini-r32", "tc", 257, 256), ("mini-r4k4", "tc", 20, 256)])
+def test_prefill_matches_oracle(lsw_opts, name, impl, T, tt):
+    """tt: the token tile of the tensor-core path forced to 256 (variant option pf_tt)."""
+    lsw_opts(pf_tt=tt)
     cfg = synth.get_config(name)
     W, A, B, router = H.build_weights(cfg, "cuda")
     sw = H.make_switch(cfg, W, A, B, router, impl=impl)
