@@ -596,7 +596,10 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, const GemvTune& t, c
     // 72 KB 3.49 ms -- a deep ring per SM beats letting the next GEMV's CTA
     // co-reside under PDL; with the bf16 x staging (same box, 2 runs each):
     // 220 KB 2.172, 176 KB 2.164, 144 KB 2.32, 112 KB 2.53 ms -- five 32-KB
-    // slots in flight rather than six.
+    // slots in flight rather than six.  Two CTAs per SM (8 consumer warps and
+    // a half ring each, so that the next launch's CTA streams before this
+    // one's last CTA on the SM ends; r02, same box): 104 KB 2.42, 110 KB 2.36,
+    // 80 KB 2.60 ms vs 2.19 for one CTA with 176 KB -- dropped.
     // (the unmerged form keeps ~12 KB of static shared memory: u, row sums, terms)
     const size_t budget = lora ? t.budget_lora : t.budget;
     int slots = budget > x_bytes ? (int)((budget - x_bytes) / slot_bytes) : 0;

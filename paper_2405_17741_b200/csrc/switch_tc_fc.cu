@@ -153,13 +153,18 @@ __device__ __forceinline__ void fx_convert(const Args& a, int q, int t, int nthr
 // group), kind within the group, rb, cb.
 struct FCursor : Cursor {
   int32_t seg, kidx;
+  int64_t end;        // fused: end (exclusive) of this CTA's range in segment seg
+  int64_t x_off;      // fused: xs offset of the segment's input
+  int64_t y_base;     // fused: ys offset of the current kind's row 0
 };
 
 // fused order: CTA b takes, in every segment s (T_s tiles), the contiguous
 // range [T_s * b / G, T_s * (b + 1) / G) -- every CTA finishes each segment at
 // about the same time, so the decoder-order barrier between segments waits
-// for ~one tile of imbalance, not for a whole chunk of another CTA.
-__device__ __forceinline__ void fused_at(const TileKinds& g, const Args& a, FCursor& c, int seg, int64_t t) {
+// for ~one tile of imbalance, not for a whole chunk of another CTA.  The
+// segment's constants are read once per segment into the cursor (not per tile).
+__device__ __forceinline__ void fused_at(const TileKinds& g, const Args& a, FCursor& c, int seg, int64_t t,
+                                         int64_t end) {
   const FusedSeg& S = a.segs[seg];
   int64_t off = t - S.tile_begin;
   int ki = 0, kd = S.kinds[0];
@@ -176,6 +181,9 @@ __device__ __forceinline__ void fused_at(const TileKinds& g, const Args& a, FCur
   c.layer = S.layer;
   c.rb = (int)(off / g.col_tiles[kd]);
   c.cb = (int)(off - (int64_t)c.rb * g.col_tiles[kd]);
+  c.end = end;
+  c.x_off = S.x_off;
+  c.y_base = S.y_off[ki];
 }
 
 // this CTA's first tile in segment >= seg (t = -1: none left)
@@ -183,7 +191,7 @@ __device__ __forceinline__ void fused_from(const TileKinds& g, const TileSeq& q,
   for (; seg < a.n_seg; ++seg) {
     const FusedSeg& S = a.segs[seg];
     const int64_t lo = S.tile_count * q.b / q.G, hi = S.tile_count * (q.b + 1) / q.G;
-    if (lo < hi) { fused_at(g, a, c, seg, S.tile_begin + lo); return; }
+    if (lo < hi) { fused_at(g, a, c, seg, S.tile_begin + lo, S.tile_begin + hi); return; }
   }
   c.t = -1;
 }
@@ -202,15 +210,16 @@ __device__ __forceinline__ FCursor cur_first(const TileKinds& g, const TileSeq& 
 template <bool kF>
 __device__ __forceinline__ void cur_next(const TileKinds& g, const TileSeq& q, const Args& a, FCursor& c) {
   if constexpr (kF) {
-    const FusedSeg& S = a.segs[c.seg];
-    if (c.t + 1 < S.tile_begin + S.tile_count * (q.b + 1) / q.G) {
+    if (c.t + 1 < c.end) {
       ++c.t;
       if (++c.cb == g.col_tiles[c.kd]) {
         c.cb = 0;
         if (++c.rb == g.row_tiles[c.kd]) {
           c.rb = 0;
           ++c.kidx;
+          const FusedSeg& S = a.segs[c.seg];
           c.kd = S.kinds[c.kidx];
+          c.y_base = S.y_off[c.kidx];
         }
       }
       return;
@@ -712,7 +721,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           }
           const int64_t col0 = (int64_t)c.cb * kTN + half * kSubCols;
           const int64_t lim = g.d_in[c.kd] - col0;      // columns of this half inside d_in
-          const uint4* xp = reinterpret_cast<const uint4*>(args.xs + args.segs[c.seg].x_off + col0);
+          const uint4* xp = reinterpret_cast<const uint4*>(args.xs + c.x_off + col0);
 #pragma unroll
           for (int v = 0; v < 8; ++v) xv[v] = 8 * v < lim ? __ldg(xp + v) : make_uint4(0, 0, 0, 0);
         }
@@ -798,7 +807,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         uint8_t* wrow = wst0 + (size_t)wring.i * (2 * kSubBytes) + unit * 128;
         if (kF && !(args.probe & 8)) {
           const int64_t grow = (int64_t)c.rb * kTM + row;
-          const int64_t at = grow < g.d_out[c.kd] ? args.segs[c.seg].y_off[c.kidx] + grow : -1;
+          const int64_t at = grow < g.d_out[c.kd] ? c.y_base + grow : -1;
           if (at != y_at) {
             y_flush();
             y_at = at;

@@ -185,6 +185,7 @@ __device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t v) {
 struct Cursor {
   int64_t t;             // global tile index, -1 when done
   int32_t kd, layer, rb, cb;
+  int32_t left;          // tiles of the current chunk after this one (no per-tile division)
 };
 
 struct TileSeq {
@@ -212,17 +213,25 @@ __device__ __forceinline__ void cursor_set(const TileKinds& g, Cursor& c, int64_
   c.cb = (int)(local - (int64_t)c.rb * g.col_tiles[kd]);
 }
 
+// start of chunk number n of the launch: its first tile and length
+__device__ __forceinline__ void cursor_chunk(const TileKinds& g, const TileSeq& q, Cursor& c, int64_t n) {
+  const int64_t r0 = n * q.chunk;
+  if (r0 >= q.T) { c.t = -1; return; }
+  const int64_t len = q.T - r0 < q.chunk ? q.T - r0 : q.chunk;
+  cursor_set(g, c, q.t0 + r0);
+  c.left = (int32_t)len - 1;
+}
+
 __device__ __forceinline__ Cursor cursor_first(const TileKinds& g, const TileSeq& q) {
   Cursor c;
-  const int64_t t = (int64_t)q.b * q.chunk < q.T ? (int64_t)q.b * q.chunk : -1;
-  cursor_set(g, c, t < 0 ? -1 : q.t0 + t);
+  cursor_chunk(g, q, c, q.b);
   return c;
 }
 
 __device__ __forceinline__ void cursor_next(const TileKinds& g, const TileSeq& q, Cursor& c) {
-  const int64_t t1 = c.t + 1, r1 = t1 - q.t0;
-  if (r1 % q.chunk != 0 && r1 < q.T) {
-    c.t = t1;
+  if (c.left > 0) {
+    --c.left;
+    ++c.t;
     if (++c.cb == g.col_tiles[c.kd]) {
       c.cb = 0;
       if (++c.rb == g.row_tiles[c.kd]) {
@@ -232,8 +241,7 @@ __device__ __forceinline__ void cursor_next(const TileKinds& g, const TileSeq& q
     }
     return;
   }
-  const int64_t nq = (c.t - q.t0) / q.chunk + q.G;
-  cursor_set(g, c, nq * q.chunk < q.T ? q.t0 + nq * q.chunk : -1);
+  cursor_chunk(g, q, c, (c.t - q.t0) / q.chunk + q.G);     // once per chunk
 }
 
 __device__ __forceinline__ int64_t strip_id(const Cursor& c) { return c.t - c.cb; }

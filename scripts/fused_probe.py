@@ -6,7 +6,6 @@ deliberately WRONG results.  Times per token (CUDA events, 30 tokens after 5):
   fused_nogemv     fc_fused_probe=8: decoder-order switch without the GEMV epilogue
   fused_bare       fc_fused_probe=12
   fused_wstream    fc_fused_probe=5: the W stream alone in decoder order, no waits
-  fused_wstream_wait fc_fused_probe=1: the same with the segment waits
   switch           the plain sweep-order switch (lsw_merge_all_layers)
   switch_wstream   tc_probe=1: the W stream alone (load + store, no math)
 JSON to stdout."""
@@ -32,7 +31,7 @@ def main():
     out = {"config": name}
     cases = [("fused", {}, True), ("fused_nowait", {"fc_fused_probe": 4}, True),
              ("fused_nogemv", {"fc_fused_probe": 8}, True), ("fused_bare", {"fc_fused_probe": 12}, True),
-             ("fused_wstream", {"fc_fused_probe": 5}, True), ("fused_wstream_wait", {"fc_fused_probe": 1}, True),
+             ("fused_wstream", {"fc_fused_probe": 5}, True),
              ("switch", {}, False), ("switch_wstream", {"tc_probe": 1}, False)]
     for label, opts, fused in cases:
         with binding.options(**opts):
