@@ -134,6 +134,47 @@ def _ncu_traffic(cfg, info):
         return None
 
 
+def _drift_profile(cfg):
+    """R22 drift of the committed 1000-token report (scripts/drift_report.py,
+    GPU and oracle side by side on sampled rows) for this config, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "drift_%s.json" % cfg.name)) as f:
+            d = json.load(f)
+        return {"tokens": d["tokens"],
+                "switch_rel_fro_gpu": d["switch"]["gpu_vs_exact"]["rel_fro"],
+                "switch_rel_fro_oracle": d["switch"]["oracle_vs_exact"]["rel_fro"],
+                "switch_ratio": d["switch"]["drift_ratio_gpu_over_oracle"],
+                "switch_gpu_vs_oracle_rel_fro": d["switch"]["gpu_vs_oracle"]["rel_fro"],
+                "cycles_rel_fro_gpu": d["cycles"]["gpu_vs_pristine"]["rel_fro"],
+                "cycles_ratio": d["cycles"]["drift_ratio_gpu_over_oracle"],
+                "source": "profiles/drift_%s.json (scripts/drift_report.py)" % cfg.name}
+    except Exception:
+        return None
+
+
+def _host_cpu():
+    """Host identity for the CPU baseline (SURVEY d.6): model, threads allowed,
+    the BLAS / OpenMP thread setting."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": i.get("user_api"), "lib": i.get("internal_api"), "threads": i.get("num_threads")}
+                for i in threadpool_info()]
+    except Exception:
+        pass
+    return {"model": model, "affinity_cpus": len(os.sched_getaffinity(0)),
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"), "threadpools": blas}
+
+
 # ----------------------------------------------------------------------------- CPU oracle leg
 
 _SAMPLE_CACHE = {}
@@ -290,6 +331,20 @@ def run_ours(args, cfg):
             dist.barrier()
     launches = sw.info()["kernel_launches"] - launches0
     ms_total = t_start.elapsed_time(t_end)
+    # routing statistics of the timed tokens (SURVEY d.2): their decisions again
+    # through the router kernel, read back after the timed region
+    decs = []
+    for t in range(args.warmup - 1, n_tok):
+        sw.router_topk(X1[t], idx, gate, stream)
+        decs.append(idx.clone())
+    decs = torch.stack(decs).cpu().tolist()
+    sets = [set(d) for d in decs]
+    same = [sets[i] == sets[i - 1] for i in range(1, len(sets))]
+    union = [len(sets[i] | sets[i - 1]) for i in range(1, len(sets))]
+    routing = {"tokens": len(same), "same_experts_as_prev": sum(same) / max(1, len(same)),
+               "mean_union_size": sum(union) / max(1, len(union)),
+               "expected_independent_uniform": {"same": 1.0 / math.comb(cfg.n_experts, cfg.top_k),
+                                                "union": 2 * cfg.top_k - cfg.top_k ** 2 / cfg.n_experts}}
     if world > 1:
         tt = torch.tensor([ms_total], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -508,7 +563,8 @@ def run_ours(args, cfg):
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             v, sample, cores, _ = oracle_sample(cfg, seconds_budget=max(args.ref_seconds, 10.0))
-            cpu = {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample}
+            cpu = {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample,
+                   "host": _host_cpu()}
         h2d = x1h.numel() * x1h.element_size() + xsh.numel() * xsh.element_size()
         d2h = ysh.numel() * 4 + cfg.top_k * 8
         res = {
@@ -534,8 +590,12 @@ def run_ours(args, cfg):
             "unmerged_decode_GBps": (tb["unmerged_token"] / (statistics.median(un_ms) * 1e-3) / 1e9
                                      if un_ms else None),
             "prefill": pf,
+            "decode_frac_of_nominal_8TBps": (tb["token"] / 8.0e12) * 1e3 / ms_step,
+            "routing": routing,
+            "drift": _drift_profile(cfg),
             "roofline": {"bound": "hbm", "achieved": sw_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": sw_gbs / peak, "traffic": _ncu_traffic(cfg, info),
+                         "frac": sw_gbs / peak, "frac_of_nominal_8TBps": sw_gbs / 8000.0,
+                         "traffic": _ncu_traffic(cfg, info),
                          "traffic_source": "profiles/ncu_switch_traffic.json (dram__bytes_read.sum + "
                                            "dram__bytes_write.sum of one ncu --set full capture of the same "
                                            "kernel on an identical-tile slice of the model, per layer x layers)",

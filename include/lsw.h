@@ -154,9 +154,9 @@ typedef struct {
   uint64_t kernel_launches;  /* kernels this ctx has launched so far                 */
   int64_t  packed_bytes;     /* ctx-owned packed operand bytes on the device         */
   int64_t  xs_elems, ys_elems; /* token I/O sizes (lsw_decode_token)                  */
-  int32_t  switch_kernel;    /* tensor-core switch kernel: 1 = per-term TMEM (v1),    */
-                             /* 2 = term groups (any k <= 4, r <= 64), 3 = folded    */
-                             /* coefficients, one accumulator per tile; 0 = SIMT     */
+  int32_t  switch_kernel;    /* tensor-core switch mode: 3 = folded coefficients, one */
+                             /* accumulator per tile; 4 = per-term accumulators;     */
+                             /* 5 = per-term, B staged per unit; 0 = SIMT            */
   int32_t  reserved;
 } lsw_info;
 
@@ -329,15 +329,12 @@ LSW_API lsw_status lsw_decode_token(lsw_ctx* ctx, const void* x1, const void* xs
  * B/element instead of 6).  Tiles are walked in decoder order, one segment per
  * (layer, group); a segment's outputs are accumulated only after every tile of
  * the previous segment is done (y final), as a decoder needs.  The fused
- * launch is a build of the switch kernel: W ends exactly as after
- * lsw_merge_all_layers with that kernel (bitwise: the fc kernel's own
- * fused build for a ctx that switches with fc in its fold mode; else a v1
- * plan, built on the first call, whose W stays within the parity tolerance of
- * the oracle's trajectory); ys equals lsw_decode_all_layers on those weights up
- * to fp32 summation order (fc: accumulated in 64-bit fixed point, bitwise
- * reproducible; v1: fp32 atomics, not bitwise reproducible).
- * Layouts as lsw_decode_token.  LSW_E_UNSUPPORTED unless one of the two has a
- * plan for the shape and tp_size == 1.
+ * launch is the fold mode of the tensor-core switch: W ends bitwise as after
+ * lsw_merge_all_layers; ys equals lsw_decode_all_layers on those weights up
+ * to fp32 summation order (accumulated in 64-bit fixed point: bitwise
+ * reproducible).  A decision equal to the merged one (nothing to add) still
+ * computes ys.  Layouts as lsw_decode_token.  LSW_E_UNSUPPORTED unless the
+ * ctx switches with the fold mode and tp_size == 1.
  */
 LSW_API lsw_status lsw_decode_token_fused(lsw_ctx* ctx, const void* x1, const void* xs, float* ys, int32_t* idx,
                                           float* gate, void* stream);

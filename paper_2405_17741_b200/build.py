@@ -31,7 +31,7 @@ def sources():
 
 def _compile(src: str, verbose: bool, tuning: bool = False) -> str:
     obj = os.path.join(BUILD + ("_tuning" if tuning else ""), os.path.basename(src) + ".o")
-    # headers, and every .cu (switch_tc_fused.cu #includes switch_tc.cu)
+    # the source, every header and every .cu (a conservative rebuild rule)
     deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".cu"))]
     inc = os.path.join(ROOT, "include")
     deps += [os.path.join(inc, f) for f in os.listdir(inc) if f.endswith(".h")]

@@ -1,33 +1,32 @@
-// switch_tc_fc.cu -- K1-tc (folded-coefficient variant): the all-layer in-place
-// switch on the 5th-gen tensor cores with ONE accumulator per tile.
+// switch_tc_fc.cu -- K1-tc: the all-layer in-place switch on the 5th-gen
+// tensor cores (SURVEY a-3 / a-4; the bf16 switch of every ctx).
 //
-// What it computes (identical to K1-simt / v1 / tg): for every adapted matrix m
-// of every layer, in ONE persistent launch (SGMM Eq. 11; "a single
-// CUDA kernel operation" P:240; in place P:328):
+// What it computes (identical to K1-simt): for every adapted matrix m of every
+// layer, in ONE persistent launch (SGMM Eq. 11; "a single CUDA
+// kernel operation" P:240; in place P:328):
 //     W_m <- RNE( W_m + sum_j c_j * B_{m,e_j} @ A_{m,e_j} )
 // with the Eq. 5/9/10 coefficient list (Eq. 9 sign corrected, R1; compacted,
 // lsw_internal.cuh build_coefs).
 //
-// How it differs from v1 / tg: Eq. 5 concatenates
-// the selected experts along the rank dimension and folds the gate into one
+// Fold mode (the default): Eq. 5 concatenates the
+// selected experts along the rank dimension and folds the gate into one
 // factor, so the whole update of a tile is ONE contraction of depth sum_j r_j.
 // Folding c_j into a bf16 factor would round it (R13), so each folded factor is
 // stored as an exact-to-2^-16 pair of bf16 parts, hi_j = bf16(c_j B_j) and
 // lo_j = bf16(c_j B_j - hi_j), and the tile is
 //     D = sum_j (hi_j + lo_j) @ A_j          (K = 2 * sum_j rp)
 // accumulated in fp32 in ONE TMEM buffer by one chain of tcgen05.mma (M = 128,
-// N = 128) and ONE commit per tile.  The epilogue then only adds D to W and
-// rounds once.  Against per-term accumulators (v1 / tg) this removes one TMEM
-// read and one FFMA per term and element and all but one commit per tile -- the
-// costs that bound those kernels at 2k >= 4 terms -- for twice
-// the tensor-core work, which stays far below the HBM time while
-// 2 * sum_j rp <= ~320 (rp = 16: k <= 4; rp = 32: k <= 2).
+// N = 128) and ONE commit per tile (a commit drains the tensor pipe: commits,
+// not MMA work, pace the MMA warp).  The epilogue only adds D to W and rounds
+// once.  Per-term modes (large k * r): raw B, one fp32 TMEM accumulator per
+// term, the epilogue's running sum W + sum_j c_j acc_j in FFMA2.
 //  * The fold runs once per 128-row strip (B slices are reused along the
 //    strip): the operand warp bulk-copies the raw pre-swizzled B slices into
 //    the strip buffer and rewrites them in place as (hi, lo) parts; the
 //    element positions of the swizzled image do not change.
-//  * W tiles 128 x 128 (two 64-column 128B-swizzled TMA boxes), TMA loads (warp
-//    0), TMA bulk stores (warp 2), chunked sweep tile order -- as in tg.
+//  * W tiles 128 x 128 (one 4-D row-major TMA box, or two 64-column 128B-swizzled
+//    3-D boxes for ragged shards), TMA loads (warp 0), TMA bulk stores (warp 2),
+//    chunked sweep tile order; the fused switch + decode walks decoder order.
 #include <cstdlib>
 #include <cstring>
 

@@ -1,7 +1,7 @@
-// tc_common.cuh -- PTX wrappers, tile walk and operand packing for the
-// folded-coefficient tensor-core switch kernel (switch_tc_fc.cu).  Internal;
-// the v1 and term-group kernels keep their own copies so that their compiled
-// code stays exactly as measured.
+// tc_common.cuh -- PTX wrappers (mbarrier, TMA, bulk copies, tcgen05 MMA /
+// commit / TMEM loads, UMMA descriptors), the switch's tile walk and the
+// pre-swizzled operand packing; shared by the tensor-core switch
+// (switch_tc_fc.cu) and the tensor-core prefill (prefill_tc.cu).  Internal.
 #pragma once
 
 #include <cuda.h>
