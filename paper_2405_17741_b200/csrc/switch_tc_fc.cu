@@ -332,29 +332,35 @@ __device__ __forceinline__ void w_store16(uint8_t* wrow, int key, int flip, int 
 }
 
 
-// As epi16, and y += RNE(W + D) . x over the 16 columns (fp32 FMA in column
-// order; x: 16 bf16 of this thread's columns).
-__device__ __forceinline__ float epi16_dot(uint8_t* wrow, int key, int flip, int col16, const uint32_t* acc,
-                                           const uint4 x0, const uint4 x1, float y) {
+// As epi16, keeping the 8 rounded bf16x2 words of the 16 columns for the dot
+// product the fused decode computes after the tile has been handed to the store.
+__device__ __forceinline__ void epi16_keep(uint8_t* wrow, int key, int flip, int col16, const uint32_t* acc,
+                                           uint32_t* o) {
   uint4* pa = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + flip) ^ key) << 4));
   uint4* pb = reinterpret_cast<uint4*>(wrow + (((col16 * 2 + (flip ^ 1)) ^ key) << 4));
   const uint4 ua = *pa, ub = *pb;
   const uint4 u0 = flip ? ub : ua, u1 = flip ? ua : ub;
   const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-  const uint32_t xw[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-  uint32_t o[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const uint64_t v = fadd2(f2_pack(__uint_as_float(w[q] << 16), __uint_as_float(w[q] & 0xffff0000u)),
                              f2_pack(__uint_as_float(acc[2 * q]), __uint_as_float(acc[2 * q + 1])));
     o[q] = f2_to_bf16x2(v);
-    y = fmaf(__uint_as_float(o[q] << 16), __uint_as_float(xw[q] << 16), y);
-    y = fmaf(__uint_as_float(o[q] & 0xffff0000u), __uint_as_float(xw[q] & 0xffff0000u), y);
   }
   const uint4 o0 = make_uint4(o[0], o[1], o[2], o[3]), o1 = make_uint4(o[4], o[5], o[6], o[7]);
   *pa = flip ? o1 : o0;
   *pb = flip ? o0 : o1;
-  return y;
+}
+
+// y2 (fp32 pairs) += RNE(W + D) . x over 16 columns: packed FMA of the element
+// pairs in column order (x: 16 bf16 of this thread's columns)
+__device__ __forceinline__ uint64_t dot16(const uint32_t* o, const uint4 x0, const uint4 x1, uint64_t y2) {
+  const uint32_t xw[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    y2 = ffma2(f2_pack(__uint_as_float(o[q] << 16), __uint_as_float(o[q] & 0xffff0000u)),
+               f2_pack(__uint_as_float(xw[q] << 16), __uint_as_float(xw[q] & 0xffff0000u)), y2);
+  return y2;
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -805,21 +811,32 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         const int unit = g.wrm ? 2 * row + half : half * kTM + row;
         uint8_t* wrow = wst0 + (size_t)wring.i * (2 * kSubBytes) + unit * 128;
         if (kF && !(args.probe & 8)) {
+          // new W first, handed to the store at once; the dot product from the
+          // rounded words in registers while the store reads the stage
+          uint32_t o[4][8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) epi16_keep(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q], o[q]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> TMA store
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
+          wring.next();
+          ++seg_mine;
           const int64_t grow = (int64_t)c.rb * kTM + row;
           const int64_t at = grow < g.d_out[c.kd] ? c.y_base + grow : -1;
           if (at != y_at) {
             y_flush();
             y_at = at;
           }
-          float y = y_run;
+          uint64_t y2 = 0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            y = epi16_dot(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q], xv[2 * q], xv[2 * q + 1], y);
-          y_run = y;
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) epi16(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q]);
+          for (int q = 0; q < 4; ++q) y2 = dot16(o[q], xv[2 * q], xv[2 * q + 1], y2);
+          float ylo, yhi;
+          asm("mov.b64 {%0, %1}, %2;" : "=f"(ylo), "=f"(yhi) : "l"(y2));
+          y_run += ylo + yhi;
+          continue;
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) epi16(wrow, unit & 7, g.wrm ? (row >> 2) & 1 : 0, q, a[q]);
         if constexpr (kF) ++seg_mine;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> TMA store
         __syncwarp();
