@@ -1024,7 +1024,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   plan->chunk = (int)opt_int("tc_chunk", plan->chunk);
   if (plan->chunk < 1) plan->chunk = 1;
   plan->probe = (int)probe_int("tc_probe") & 17;
-  plan->fused_probe = (int)probe_int("fc_fused_probe") & 13;   // tuning builds only: 1 W stream only, 4 no segment wait, 8 no GEMV
+  plan->fused_probe = (int)probe_int("fc_fused_probe") & 29;   // tuning builds only: 1 W stream only, 4 no segment wait, 8 no GEMV, 16 no fold math
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
   // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
   g.wrm = opt_int("fc_wrm", 1) != 0;

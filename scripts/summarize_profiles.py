@@ -1,5 +1,5 @@
 """Summarize a round's GPU evidence into profiles/ (committed):
-  profiles/<tag>_ncu_summary.json   key ncu --set full metrics of the switch / GEMV captures
+  profiles/<tag>_ncu_summary.json   key ncu --set full metrics of the switch / GEMV / fused / prefill captures
   profiles/<tag>_launches.md        per-kernel share of a bench step from the ncu launch list
   profiles/ncu_switch_traffic.json  DRAM bytes per layer of the switch capture (bench.py roofline.traffic)
 Usage: python scripts/summarize_profiles.py TAG [gpurun_out]"""
@@ -42,7 +42,7 @@ def raw(rep):
 
 
 summary = {}
-for name in ("switch", "gemv"):
+for name in ("switch", "gemv", "fused", "prefill"):
     rep = os.path.join(src, f"{name}_{tag}.ncu-rep")
     if os.path.exists(rep):
         summary[name] = raw(rep)
@@ -63,8 +63,9 @@ if "switch" in summary and summary["switch"]:
         json.dump({"config": "llama2-7b", "switch_impl": "tc", "capture_layers": 4, "round_tag": tag,
                    "kernel": kname, "switch_kernel": 3 if "switch_fc" in kname else None,
                    "dram_bytes_capture": tot, "dram_bytes_per_layer": tot / 4,
-                   "note": "ncu --set full of the switch kernel (fused switch) on the 7B shape with 4 layers "
-                           "(identical per-matrix tiles); bench.py scales per layer x layers"}, f, indent=1)
+                   "note": "ncu --set full of the switch kernel (second pass: Eq. 10 fused switch) on the 7B "
+                           "shape with 4 layers (identical per-matrix tiles); bench.py scales per layer x layers"},
+                  f, indent=1)
 
 # launch list shares
 lfile = os.path.join(src, f"launches_{tag}.csv")
