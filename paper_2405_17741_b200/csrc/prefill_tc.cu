@@ -105,7 +105,67 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-template <int kTT>
+// Thread-block clusters of kC CTAs along the token-tile dimension (MODE_Y):
+// the CTAs of a cluster compute the same 128-row block for kC consecutive
+// token tiles in lockstep, so each loads 128/kC rows of the W box and
+// multicasts them to all kC CTAs -- W crosses L2 -> SM once per cluster instead
+// of once per token tile.  Every stage's MMA completion is committed to the
+// `empty` barrier of every CTA of the cluster (count kC), so no CTA refills a
+// stage -- its own or, by multicast, a peer's -- before all kC have consumed it.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                               int32_t c2, uint32_t bar, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6, %7;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask),
+        "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(bar), "h"(mask) : "memory");
+}
+
+// Tile of iteration `it` of this CTA: kC == 1 -- global tile index (tile_at);
+// kC > 1 -- cluster tile (row block, token-tile group), this CTA's token tile
+// = group * kC + rank (may lie past the last token tile: OOB-zero operands,
+// masked stores).
+template <int kC>
+__device__ __forceinline__ TileAt tile_for(const Args& a, int it, int crank) {
+  if constexpr (kC == 1) {
+    return tile_at(a, it);
+  } else {
+    const int n_ttg = (a.n_tt + kC - 1) / kC;
+    const int rest = it / n_ttg;
+    TileAt r;
+    r.tt = (it - rest * n_ttg) * kC + crank;
+    r.q = (a.n_sites > 2 && rest >= a.tile_row0[2]) ? 2 : (a.n_sites > 1 && rest >= a.tile_row0[1]) ? 1 : 0;
+    r.rb = rest - a.tile_row0[r.q];
+    r.kb0 = 0;
+    r.kb1 = a.n_kb;
+    return r;
+  }
+}
+
+template <int kTT, int kC>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -116,10 +176,15 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool lora = a.mode == MODE_Y && a.n_experts > 0;
 
+  const int crank = kC > 1 ? (int)cluster_rank() : 0;
+  const uint16_t cmask = (uint16_t)((1u << kC) - 1);
+  const int it0 = kC > 1 ? (int)cluster_id() : blockIdx.x;
+  const int istep = kC > 1 ? (int)cluster_count() : gridDim.x;
+  const int n_it = kC > 1 ? a.row_tiles_total * ((a.n_tt + kC - 1) / kC) : a.total_tiles;
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(smem_u32(&bar_full[s]), 1);
-      mbar_init(smem_u32(&bar_empty[s]), 1);
+      mbar_init(smem_u32(&bar_empty[s]), kC);         // one MMA commit per CTA of the cluster
     }
     for (int s = 0; s < kAccBufs; ++s) {
       mbar_init(smem_u32(&bar_accfull[s]), 1);
@@ -138,6 +203,7 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kC > 1) cluster_sync();          // peers' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem_base = s_tmem_base;
 
@@ -147,14 +213,20 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
       const uint64_t pol_w = policy_evict_first();     // W / A: streamed once per strip
       const uint64_t pol_x = policy_evict_last();      // X, B, Z: reused by many tiles
       Ring ring{0, 0, (uint32_t)a.stages};
-      for (int t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {
-        const TileAt ta = tile_at(a, t);
+      for (int it = it0; it < n_it; it += istep) {
+        const TileAt ta = tile_for<kC>(a, it, crank);
         for (int kb = ta.kb0; kb < ta.kb1; ++kb) {
           mbar_wait(smem_u32(&bar_empty[ring.i]), ring.phase ^ 1);
           uint8_t* st = base + (size_t)ring.i * a.stage_bytes;
           const uint32_t bar = smem_u32(&bar_full[ring.i]);
-          mbar_expect_tx(bar, kBoxBytes + kTT * kKB * 2);
-          tma_load_3d(smem_u32(st), &maps.op[ta.q], kb * kKB, ta.rb * kTM, a.layer, bar, pol_w);
+          mbar_expect_tx(bar, kBoxBytes + kTT * kKB * 2);   // W box (all kC slices) + own X box
+          if constexpr (kC > 1) {
+            // this CTA's 128/kC rows of the W box, to the same offset of every CTA
+            tma_load_3d_mc(smem_u32(st) + crank * (kBoxBytes / kC), &maps.op[ta.q], kb * kKB,
+                           ta.rb * kTM + crank * (kTM / kC), a.layer, bar, cmask, pol_w);
+          } else {
+            tma_load_3d(smem_u32(st), &maps.op[ta.q], kb * kKB, ta.rb * kTM, a.layer, bar, pol_w);
+          }
           tma_load_2d(smem_u32(st + a.b_off), &maps.x, kb * kKB, ta.tt * kTT, bar, pol_x);   // box {64, kTT}
           ring.next();
         }
@@ -173,6 +245,14 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
           }
         }
       }
+      if constexpr (kC > 1) {
+        // drain: every stage's last fill released by all kC CTAs, so no peer's
+        // commit still targets this CTA's barriers when it leaves
+        for (int i = 0; i < a.stages; ++i) {
+          mbar_wait(smem_u32(&bar_empty[ring.i]), ring.phase ^ 1);
+          ring.next();
+        }
+      }
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ================================
@@ -184,8 +264,8 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
     const uint64_t zpart = a.zpart_bytes >> 4;
     Ring ring{0, 0, (uint32_t)a.stages};
     Ring acc{0, 0, kAccBufs};
-    for (int t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {
-      const TileAt ta = tile_at(a, t);
+    for (int it = it0; it < n_it; it += istep) {
+      const TileAt ta = tile_for<kC>(a, it, crank);
       mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + acc.i * kTT;
@@ -198,7 +278,8 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < kKB / 16; ++kk) umma_f16(d, da + kk * 2, db + kk * 2, idesc, accum | kk);
-          umma_commit(smem_u32(&bar_empty[ring.i]));      // stage free once these MMAs complete
+          if constexpr (kC > 1) umma_commit_mc(smem_u32(&bar_empty[ring.i]), cmask);   // every CTA's copy
+          else umma_commit(smem_u32(&bar_empty[ring.i]));  // stage free once these MMAs complete
         }
         __syncwarp();
         accum = 1;
@@ -215,7 +296,8 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
             for (int part = 0; part < 2; ++part)
               for (int kk = 0; kk < ksteps; ++kk)
                 umma_f16(d, da + kk * 2, db + part * zpart + kk * 2, idesc, 1u);
-            umma_commit(smem_u32(&bar_empty[ring.i]));
+            if constexpr (kC > 1) umma_commit_mc(smem_u32(&bar_empty[ring.i]), cmask);
+            else umma_commit(smem_u32(&bar_empty[ring.i]));
           }
           __syncwarp();
           ring.next();
@@ -232,13 +314,13 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     Ring acc{0, 0, kAccBufs};
-    for (int t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {
-      const TileAt ta = tile_at(a, t);
+    for (int it = it0; it < n_it; it += istep) {
+      const TileAt ta = tile_for<kC>(a, it, crank);
       mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);
       tc_fence_after();
       const int64_t grow = (int64_t)ta.rb * kTM + row;
       const bool ok = grow < a.rows_valid[ta.q];
-      const int split = a.mode == MODE_U ? t / a.n_tt / a.row_tiles_total : 0;
+      const int split = a.mode == MODE_U ? it / a.n_tt / a.row_tiles_total : 0;
       float* outp = a.out + (int64_t)split * a.T * a.ld + a.col0[ta.q] + grow;
       const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTT;
       for (int c0 = 0; c0 < kTT; c0 += 16) {
@@ -260,6 +342,7 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kC > 1) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAccBufs * kTT)
@@ -310,10 +393,12 @@ __global__ void prefill_zbuild(const float* __restrict__ U, int splits, int64_t 
 
 struct PfPlan {
   CUtensorMap w[LSW_NKIND], a[LSW_NKIND];
+  CUtensorMap w2[LSW_NKIND], w4[LSW_NKIND];   // W boxes of 64 / 32 rows: one CTA's slice in a cluster of 2 / 4
   const __nv_bfloat16* Bp[LSW_NKIND];
   int64_t dout_pad[LSW_NKIND], d_out[LSW_NKIND], d_in[LSW_NKIND];
   int n_layers, n_experts, r, rp, num_sms;
   int tt_opt;                    // variant option pf_tt (128 | 256), 0: chosen per launch
+  int cl_opt;                    // variant option pf_cluster (1 | 2 | 4), 0: chosen per launch
 };
 
 // shared-memory plan of one token-tile width: stage = [128 x 64 A box | B
@@ -378,6 +463,8 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
     p->d_out[k] = g.d_out;
     p->d_in[k] = g.d_in;
     if (!p->Bp[k] || !pf_map(&p->w[k], g.W, g.d_in, g.d_out, sp.n_layers) ||
+        !pf_map(&p->w2[k], g.W, g.d_in, g.d_out, sp.n_layers, 64) ||
+        !pf_map(&p->w4[k], g.W, g.d_in, g.d_out, sp.n_layers, 32) ||
         !pf_map(&p->a[k], g.A, g.d_in, (uint64_t)sp.n_experts * sp.rank, sp.n_layers)) {
       delete p;
       return cudaErrorInvalidValue;
@@ -385,12 +472,14 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
   }
   p->tt_opt = (int)opt_int("pf_tt", 0);
   if (p->tt_opt != 128 && p->tt_opt != 256) p->tt_opt = 0;
+  p->cl_opt = (int)opt_int("pf_cluster", 0);
+  if (p->cl_opt != 1 && p->cl_opt != 2 && p->cl_opt != 4) p->cl_opt = 0;
   if (pf_geom(128, p->rp).stages < 3) { delete p; return cudaErrorNotSupported; }
-  cudaError_t e = cudaFuncSetAttribute(pf::prefill_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(kPfBudget + 1024));
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(pf::prefill_gemm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kPfBudget + 1024));
+  const int smem = (int)(kPfBudget + 1024);
+  cudaError_t e = cudaSuccess;
+  for (auto fn : {pf::prefill_gemm<128, 1>, pf::prefill_gemm<128, 2>, pf::prefill_gemm<128, 4>,
+                  pf::prefill_gemm<256, 1>, pf::prefill_gemm<256, 2>, pf::prefill_gemm<256, 4>})
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) { delete p; return e; }
   *out = p;
   return cudaSuccess;
@@ -406,13 +495,24 @@ static int pf_tt(const PfPlan* p, int64_t T) {
   return 128;
 }
 
+// cluster size of the dense launch (variant option pf_cluster; default 1).
+// Measured (7B, 512 tokens, same box): clusters of 4 token tiles sharing each
+// W block by multicast 0.41 ms per layer vs 0.34 without -- the lockstep the
+// multicast protocol imposes on the cluster's CTAs costs more than the L2
+// traffic it saves.
+static int pf_cluster(const PfPlan* p, int64_t n_tt) {
+  (void)n_tt;
+  return p->cl_opt ? p->cl_opt : 1;
+}
+
 // scratch sizes (elements) a launch with T tokens needs
 void pf_scratch(const PfPlan* p, int n_sites, int64_t T, int64_t* u_elems, int64_t* z_elems) {
   const int64_t nr = (int64_t)p->n_experts * p->r;
   const int tt = pf_tt(p, T);
-  const int64_t n_tt = (T + tt - 1) / tt;
+  const int64_t n_tt = (T + tt - 1) / tt, c = pf_cluster(p, n_tt);
+  const int64_t n_tt_pad = (n_tt + c - 1) / c * c;               // Z of padded token tiles: zeros
   *u_elems = (int64_t)p->num_sms * T * n_sites * nr;          // splits <= num_sms
-  *z_elems = n_tt * n_sites * p->n_experts * 2 * (int64_t)tt * p->rp;
+  *z_elems = n_tt_pad * n_sites * p->n_experts * 2 * (int64_t)tt * p->rp;
 }
 
 template <int kTT>
@@ -457,16 +557,19 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   a.b_off = geo.b_off;
   a.rp = p->rp;
   int grid = a.total_tiles < p->num_sms ? a.total_tiles : p->num_sms;
-  prefill_gemm<kTT><<<grid, kThreads, geo.smem, s>>>(maps, a);
+  prefill_gemm<kTT, 1><<<grid, kThreads, geo.smem, s>>>(maps, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   // ---- 2. gate-scaled (hi, lo) LoRA-down products of the selected experts
+  const int C = pf_cluster(p, n_tt);
+  const int n_tt_pad = (n_tt + C - 1) / C * C;
   {
-    const int64_t n = (int64_t)n_tt * P.n_sites * p->n_experts * kTT * p->rp;
+    const int64_t n = (int64_t)n_tt_pad * P.n_sites * p->n_experts * kTT * p->rp;
     int blocks = (int)((n + 255) / 256);
     if (blocks > 4 * p->num_sms) blocks = 4 * p->num_sms;
     prefill_zbuild<<<blocks, 256, 0, s>>>(P.U, splits, P.T, a.ld, P.n_sites, p->n_experts, p->r, p->rp, P.k,
-                                          P.scale, P.idx, P.gate, reinterpret_cast<__nv_bfloat16*>(P.Z), n_tt, kTT);
+                                          P.scale, P.idx, P.gate, reinterpret_cast<__nv_bfloat16*>(P.Z), n_tt_pad,
+                                          kTT);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -477,7 +580,7 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   rt = 0;
   for (int q = 0; q < P.n_sites; ++q) {
     const int kd = kinds[q];
-    maps.op[q] = p->w[kd];
+    maps.op[q] = C == 4 ? p->w4[kd] : C == 2 ? p->w2[kd] : p->w[kd];
     y.tile_row0[q] = rt;
     rt += (int)((p->d_out[kd] + kTM - 1) / kTM);
     y.rows_valid[q] = p->d_out[kd];
@@ -495,9 +598,27 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   y.zpart_bytes = (uint32_t)kTT * p->rp * 2;
   y.swz = p->rp == 16 ? 6u : p->rp == 32 ? 4u : 2u;     // SWIZZLE_32B / 64B / 128B
   y.Z = reinterpret_cast<const __nv_bfloat16*>(P.Z);
-  grid = y.total_tiles < p->num_sms ? y.total_tiles : p->num_sms;
-  prefill_gemm<kTT><<<grid, kThreads, geo.smem, s>>>(maps, y);
-  return cudaGetLastError();
+  if (C == 1) {
+    grid = y.total_tiles < p->num_sms ? y.total_tiles : p->num_sms;
+    prefill_gemm<kTT, 1><<<grid, kThreads, geo.smem, s>>>(maps, y);
+    return cudaGetLastError();
+  }
+  const int n_ct = rt * (n_tt_pad / C);                      // cluster tiles
+  const int n_cl = n_ct < p->num_sms / C ? n_ct : p->num_sms / C;
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(n_cl * C);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = geo.smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return C == 4 ? cudaLaunchKernelEx(&lc, prefill_gemm<kTT, 4>, maps, y)
+                : cudaLaunchKernelEx(&lc, prefill_gemm<kTT, 2>, maps, y);
 }
 
 cudaError_t launch_prefill_tc(const PfPlan* p, const PrefillParams& P, int layer, const int kinds[3],

@@ -105,6 +105,7 @@ struct TcPlan {
   int32_t chunk = 48;
   int32_t probe = 0;          // tuning builds only (tc_probe=1): W stream alone, W written back unchanged
   int32_t fused_probe = 0;    // tuning builds only (fc_fused_probe)
+  uint32_t* trace = nullptr;  // tuning builds only (trace_buf: device buffer of kTraceCtas * kTraceTiles * 8 u32)
   void* packed_At[LSW_NKIND] = {};
   void* packed_B[LSW_NKIND] = {};
   int64_t bytes = 0;
@@ -127,7 +128,24 @@ struct Args {
   float* ys;
   unsigned long long* ys_fx;      // fixed-point accumulators of ys, zeroed before the launch
   unsigned long long* seg_done;   // [n_seg], zeroed before the launch
+  uint32_t* trace;                // tuning builds only (option trace_buf): per-tile role timestamps
 };
+
+// Tuning builds only: %globaltimer (low 32 bits, ns) of pipeline events for the
+// first kTraceTiles tiles of CTAs 0 .. kTraceCtas-1, slot = role event:
+// 0 W load issued, 1 A stage issued, 2 MMA saw its operands, 3 MMA committed,
+// 4 epilogue saw the accumulator, 5 epilogue saw W, 6 tile handed to the store,
+// 7 store has read the stage.
+constexpr int kTraceCtas = 4, kTraceTiles = 1024;
+#ifdef LSW_TUNING
+#define FC_TRACE(slot, n)                                                                                 \
+  do {                                                                                                    \
+    if (args.trace && blockIdx.x < kTraceCtas && (n) < kTraceTiles)                                       \
+      args.trace[((size_t)blockIdx.x * kTraceTiles + (n)) * 8 + (slot)] = (uint32_t)globaltimer();      \
+  } while (0)
+#else
+#define FC_TRACE(slot, n) do {} while (0)
+#endif
 
 // Fused outputs are accumulated in 64-bit fixed point (2^-40 units): integer
 // adds are associative, so y is bitwise reproducible whatever the order of the
@@ -449,8 +467,10 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         const uint64_t pol_stream = policy_evict_first();
         const CUtensorMap* src = args.mode == MODE_RESTORE ? maps.p : maps.w;   // RESTORE reads P
         Ring wring{0, 0, (uint32_t)g.w_stages};
+        int nt_tr = 0;
         for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
           mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
+          FC_TRACE(0, nt_tr++);
           const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
           mbar_expect_tx(wbar, 2 * kSubBytes);
           uint8_t* wdst = wst0 + (size_t)wring.i * (2 * kSubBytes);
@@ -468,6 +488,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       if (lane == 0) {
         const uint64_t pol_stream = policy_evict_first();
         Ring wring{0, 0, (uint32_t)g.w_stages};
+        int ns_tr = 0;
         for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
           mbar_wait(smem_u32(&bar_wdone[wring.i]), wring.phase);     // epilogue wrote the tile
           if (nt == 0) {                                             // fused, W unchanged: no store
@@ -484,6 +505,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
                            c.rb * kTM, c.layer, pol_stream);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read -> stage reusable
+          FC_TRACE(7, ns_tr++);
           mbar_arrive(smem_u32(&bar_wempty[wring.i]));
           wring.next();
         }
@@ -548,6 +570,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       int64_t strip_prev = -1;
       Ring bring{0, 0, (uint32_t)g.b_bufs};
       Ring aring{0, 0, (uint32_t)g.a_stages};
+      int na_tr = 0;
       for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
         if (strip_id(c) != strip_prev) {
           if (strip_prev >= 0) bring.next();
@@ -576,6 +599,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           const __nv_bfloat16* blk =
               g.At[c.kd] + (((size_t)c.layer * tk.col_tiles[c.kd] + c.cb) * g.n_experts) * (size_t)kTN * rpe;
           mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
+          FC_TRACE(1, na_tr);
           uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
           const uint32_t bar = smem_u32(&bar_afull[aring.i]);
           mbar_expect_tx(bar, nt * tb);
@@ -584,6 +608,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         }
         __syncwarp();
         aring.next();
+        ++na_tr;
       }
       }  // !kPT
     } else if (warp == 1 && nt > 0 && !(args.probe & 1)) {
@@ -602,6 +627,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       Ring aring{0, 0, (uint32_t)g.a_stages};
       Ring acc{0, 0, (uint32_t)g.acc_bufs};
       int64_t strip_prev = -1;
+      int nm_tr = 0;
       for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
         if (!g.bu && strip_id(c) != strip_prev) {
           if (strip_prev >= 0) {
@@ -654,6 +680,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           continue;
         }
         mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
+        if (lane == 0) FC_TRACE(2, nm_tr);
         mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
         tc_fence_after();
         const uint64_t b_desc = desc0 + (smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes) >> 4);
@@ -667,6 +694,8 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
                          (j | part | kk) != 0 ? 1u : 0u);
           umma_commit(smem_u32(&bar_accfull[acc.i]));
         }
+        if (lane == 0) FC_TRACE(3, nm_tr);
+        ++nm_tr;
         __syncwarp();
         acc.next();
         aring.next();
@@ -682,6 +711,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       Ring wring{0, 0, (uint32_t)g.w_stages};
       Ring acc{0, 0, (uint32_t)g.acc_bufs};
       Ring aring{0, 0, (uint32_t)g.a_stages};
+      int ne_tr = 0;
       int cur_seg = -1;                            // fused: segment of the previous tile
       int conv_next = 0;                           // fused: first segment whose outputs this CTA has not converted
       unsigned long long seg_mine = 0;             // fused: tiles of cur_seg this CTA finished
@@ -789,6 +819,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         uint32_t a[4][16];
         if (nt > 0) {
           mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);      // the tile's MMAs are complete
+          if (releaser) FC_TRACE(4, ne_tr);
           if (releaser) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
           aring.next();
           tc_fence_after();
@@ -807,6 +838,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             for (int v = 0; v < 16; ++v) a[q][v] = 0u;
         }
         mbar_wait(smem_u32(&bar_wfull[wring.i]), wring.phase);      // W tile landed
+        if (releaser) FC_TRACE(5, ne_tr);
         // default: two [128 rows][64 cols] boxes; wrm: one [128 rows][2 x 64 cols] box
         const int unit = g.wrm ? 2 * row + half : half * kTM + row;
         uint8_t* wrow = wst0 + (size_t)wring.i * (2 * kSubBytes) + unit * 128;
@@ -819,6 +851,8 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> TMA store
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
+          if (releaser) FC_TRACE(6, ne_tr);
+          ++ne_tr;
           wring.next();
           ++seg_mine;
           const int64_t grow = (int64_t)c.rb * kTM + row;
@@ -841,6 +875,8 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> TMA store
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&bar_wdone[wring.i]));
+        if (releaser) FC_TRACE(6, ne_tr);
+        ++ne_tr;
         wring.next();
       }
       if constexpr (kF) {
@@ -1024,6 +1060,9 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   plan->chunk = (int)opt_int("tc_chunk", plan->chunk);
   if (plan->chunk < 1) plan->chunk = 1;
   plan->probe = (int)probe_int("tc_probe") & 17;
+#ifdef LSW_TUNING
+  { const char* v = opt_str("trace_buf"); plan->trace = v ? reinterpret_cast<uint32_t*>(strtoull(v, nullptr, 10)) : nullptr; }
+#endif
   plan->fused_probe = (int)probe_int("fc_fused_probe") & 29;   // tuning builds only: 1 W stream only, 4 no segment wait, 8 no GEMV, 16 no fold math
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
   // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
@@ -1149,6 +1188,7 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   a.ys = nullptr;
   a.ys_fx = nullptr;
   a.seg_done = nullptr;
+  a.trace = plan->trace;
   if (plan->geom.pt)
     switch_fc_kernel<false, true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   else
@@ -1223,6 +1263,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   a.ys = ys;
   a.ys_fx = plan->d_ys_fx;
   a.seg_done = plan->d_seg_done;
+  a.trace = plan->trace;
   switch_fc_kernel<true, false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   return cudaGetLastError();
 }

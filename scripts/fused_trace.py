@@ -1,0 +1,75 @@
+"""Per-tile pipeline trace of the switch kernel (tuning build only:
+python paper_2405_17741_b200/build.py --tuning): %globaltimer stamps of
+every role for the first 1024 tiles of CTAs 0-3, for one plain sweep-order
+switch and one fused switch + decode token (7B).  Prints medians of the
+per-tile intervals (ns): where a tile's time goes."""
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import synth  # noqa: E402
+from paper_2405_17741_b200 import binding  # noqa: E402
+from paper_2405_17741_b200 import harness as H  # noqa: E402
+
+SLOTS = ["w_issue", "a_issue", "mma_operands", "mma_commit", "epi_acc", "epi_w", "epi_done", "store_read"]
+
+
+def analyse(tr):
+    out = {}
+    for cta in range(tr.shape[0]):
+        t = tr[cta].astype("int64")
+        n = int((t[:, 6] != 0).sum())
+        if n < 10:
+            continue
+        t = t[:n]
+        t = t - t[0, 0]
+        rows = {}
+        def med(x):
+            return float(statistics.median(x)) if len(x) else None
+        rows["period_epi_done"] = med([t[i, 6] - t[i - 1, 6] for i in range(1, n)])
+        rows["w_load_latency(issue->epi_w)"] = med([t[i, 5] - t[i, 0] for i in range(n)])
+        rows["a_load(issue->mma_operands)"] = med([t[i, 2] - t[i, 1] for i in range(n)])
+        rows["mma(operands->commit)"] = med([t[i, 3] - t[i, 2] for i in range(n)])
+        rows["commit->epi_acc"] = med([t[i, 4] - t[i, 3] for i in range(n)])
+        rows["epi_acc_after_w"] = med([t[i, 4] - t[i, 5] for i in range(n)])
+        rows["epi_work(max(acc,w)->done)"] = med([t[i, 6] - max(t[i, 4], t[i, 5]) for i in range(n)])
+        rows["store(done->read)"] = med([t[i, 7] - t[i, 6] for i in range(n)])
+        rows["frac_tiles_acc_last"] = float(sum(1 for i in range(n) if t[i, 4] > t[i, 5]) / n)
+        out[f"cta{cta}"] = rows
+    return out
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "llama2-7b"
+    cfg = synth.get_config(name)
+    W, A, B, router = H.build_weights(cfg, "cuda")
+    tr = torch.zeros(4, 1024, 8, dtype=torch.int32, device="cuda")
+    with binding.options(trace_buf=tr.data_ptr()):
+        sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+    X1 = synth.gen_x1(cfg, 8, "cuda")
+    xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
+    ys = torch.empty(sw.info()["ys_elems"], device="cuda")
+    idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
+    gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
+    res = {}
+    for t in range(3):
+        sw.router_topk(X1[t], idx, gate)
+        tr.zero_()
+        sw.merge_all_layers(idx, gate)
+        torch.cuda.synchronize()
+    res["sweep_switch"] = analyse(tr.cpu().numpy())
+    for t in range(3, 6):
+        tr.zero_()
+        sw.decode_token_fused(X1[t], xs, ys, idx, gate)
+        torch.cuda.synchronize()
+    res["fused"] = analyse(tr.cpu().numpy())
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()

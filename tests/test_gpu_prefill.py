@@ -33,10 +33,20 @@ def _f64(t):
                                             ("mini", "tc", 300, None), ("mini-r32", "tc", 129, None),
                                             ("mini-k1", "tc", 130, None), ("mini-r64k4", "tc", 64, None),
                                             ("mini", "simt", 9, None), ("mini", "tc", 300, 256),
-                                            ("mini-r32", "tc", 257, 256), ("mini-r4k4", "tc", 20, 256)])
+                                            ("mini-r32", "tc", 257, 256), ("mini-r4k4", "tc", 20, 256),
+                                            ("mini", "tc", 512, "128/4"), ("mini", "tc", 300, "128/4"),
+                                            ("mini-r32", "tc", 256, "128/2"), ("mini-r64k3", "tc", 384, "128/2"),
+                                            ("mini", "tc", 1024, "256/4"), ("mini-k1", "tc", 200, "128/1")])
 def test_prefill_matches_oracle(lsw_opts, name, impl, T, tt):
-    """tt: the token tile of the tensor-core path forced to 256 (variant option pf_tt)."""
-    lsw_opts(pf_tt=tt)
+    """tt: the token tile of the tensor-core path forced to 256 (variant option
+    pf_tt), or "tile/cluster": also the cluster of the dense launch forced
+    (pf_cluster: W rows multicast across the token tiles of a cluster; T = 300
+    with 4 pads a cluster with an all-out-of-range token tile)."""
+    if isinstance(tt, str):
+        t_, c_ = tt.split("/")
+        lsw_opts(pf_tt=int(t_), pf_cluster=int(c_))
+    else:
+        lsw_opts(pf_tt=tt)
     cfg = synth.get_config(name)
     W, A, B, router = H.build_weights(cfg, "cuda")
     sw = H.make_switch(cfg, W, A, B, router, impl=impl)
