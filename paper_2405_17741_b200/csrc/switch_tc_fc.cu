@@ -132,16 +132,17 @@ struct Args {
 };
 
 // Tuning builds only: %globaltimer (low 32 bits, ns) of pipeline events for the
-// first kTraceTiles tiles of CTAs 0 .. kTraceCtas-1, slot = role event:
+// first kTraceTiles tiles of CTAs 0 .. kTraceCtas-1 (the whole pass at the BASELINE shapes), slot = role event:
 // 0 W load issued, 1 A stage issued, 2 MMA saw its operands, 3 MMA committed,
 // 4 epilogue saw the accumulator, 5 epilogue saw W, 6 tile handed to the store,
 // 7 store has read the stage.
-constexpr int kTraceCtas = 4, kTraceTiles = 1024;
+constexpr int kTraceCtas = 2, kTraceTiles = 8192;
 #ifdef LSW_TUNING
 #define FC_TRACE(slot, n)                                                                                 \
   do {                                                                                                    \
-    if (args.trace && blockIdx.x < kTraceCtas && (n) < kTraceTiles)                                       \
-      args.trace[((size_t)blockIdx.x * kTraceTiles + (n)) * 8 + (slot)] = (uint32_t)globaltimer();      \
+    const int n_ = (n);                                                                                   \
+    if (args.trace && blockIdx.x < kTraceCtas && n_ < kTraceTiles)                                        \
+      args.trace[((size_t)blockIdx.x * kTraceTiles + n_) * 8 + (slot)] = (uint32_t)globaltimer();        \
   } while (0)
 #else
 #define FC_TRACE(slot, n) do {} while (0)

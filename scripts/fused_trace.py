@@ -1,6 +1,6 @@
 """Per-tile pipeline trace of the switch kernel (tuning build only:
 python paper_2405_17741_b200/build.py --tuning): %globaltimer stamps of
-every role for the first 1024 tiles of CTAs 0-3, for one plain sweep-order
+every role for the first 8192 tiles (a whole pass) of CTAs 0-1, for one plain sweep-order
 switch and one fused switch + decode token (7B).  Prints medians of the
 per-tile intervals (ns): where a tile's time goes."""
 import json
@@ -22,12 +22,13 @@ SLOTS = ["w_issue", "a_issue", "mma_operands", "mma_commit", "epi_acc", "epi_w",
 def analyse(tr):
     out = {}
     for cta in range(tr.shape[0]):
-        t = tr[cta].astype("int64")
+        t = tr[cta].view("uint32").astype("int64")
         n = int((t[:, 6] != 0).sum())
         if n < 10:
             continue
         t = t[:n]
-        t = t - t[0, 0]
+        t = (t - t[0, 6]) % (1 << 32)          # 32-bit timer: differences modulo the wrap
+        t = (t + (1 << 31)) % (1 << 32) - (1 << 31)
         rows = {}
         def med(x):
             return float(statistics.median(x)) if len(x) else None
@@ -39,7 +40,14 @@ def analyse(tr):
         rows["epi_acc_after_w"] = med([t[i, 4] - t[i, 5] for i in range(n)])
         rows["epi_work(max(acc,w)->done)"] = med([t[i, 6] - max(t[i, 4], t[i, 5]) for i in range(n)])
         rows["store(done->read)"] = med([t[i, 7] - t[i, 6] for i in range(n)])
+        rows["w_stage_cycle(issue->store_read)"] = med([t[i, 7] - t[i, 0] for i in range(n)])
+        rows["period_w_issue"] = med([t[i, 0] - t[i - 1, 0] for i in range(1, n)])
         rows["frac_tiles_acc_last"] = float(sum(1 for i in range(n) if t[i, 4] > t[i, 5]) / n)
+        rows["tiles"] = n
+        rows["pass_us"] = float((t[n - 1, 6] - t[0, 6]) / 1e3)
+        # period per eighth of the pass (the kinds come in order in the sweep)
+        rows["period_by_eighth"] = [float(statistics.median([t[i, 6] - t[i - 1, 6] for i in range(max(1, n * j // 8), n * (j + 1) // 8)]))
+                                    for j in range(8)]
         out[f"cta{cta}"] = rows
     return out
 
@@ -47,8 +55,10 @@ def analyse(tr):
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "llama2-7b"
     cfg = synth.get_config(name)
+    if len(sys.argv) > 2:
+        cfg = cfg.with_(n_layers=int(sys.argv[2]))
     W, A, B, router = H.build_weights(cfg, "cuda")
-    tr = torch.zeros(4, 1024, 8, dtype=torch.int32, device="cuda")
+    tr = torch.zeros(2, 8192, 8, dtype=torch.int32, device="cuda")
     with binding.options(trace_buf=tr.data_ptr()):
         sw = H.make_switch(cfg, W, A, B, router, impl="tc")
     X1 = synth.gen_x1(cfg, 8, "cuda")
@@ -63,11 +73,12 @@ def main():
         sw.merge_all_layers(idx, gate)
         torch.cuda.synchronize()
     res["sweep_switch"] = analyse(tr.cpu().numpy())
-    for t in range(3, 6):
-        tr.zero_()
-        sw.decode_token_fused(X1[t], xs, ys, idx, gate)
-        torch.cuda.synchronize()
-    res["fused"] = analyse(tr.cpu().numpy())
+    if sw.info()["switch_kernel"] == 3:
+        for t in range(3, 6):
+            tr.zero_()
+            sw.decode_token_fused(X1[t], xs, ys, idx, gate)
+            torch.cuda.synchronize()
+        res["fused"] = analyse(tr.cpu().numpy())
     print(json.dumps(res, indent=1))
 
 
