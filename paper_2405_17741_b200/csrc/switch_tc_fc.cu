@@ -106,6 +106,7 @@ struct TcPlan {
   int32_t probe = 0;          // tuning builds only (tc_probe=1): W stream alone, W written back unchanged
   int32_t fused_probe = 0;    // tuning builds only (fc_fused_probe)
   uint32_t* trace = nullptr;  // tuning builds only (trace_buf: device buffer of kTraceCtas * kTraceTiles * 8 u32)
+  uint32_t* seg_trace = nullptr;  // tuning builds only (seg_trace_buf: grid * 512 * 2 u32)
   void* packed_At[LSW_NKIND] = {};
   void* packed_B[LSW_NKIND] = {};
   int64_t bytes = 0;
@@ -129,6 +130,7 @@ struct Args {
   unsigned long long* ys_fx;      // fixed-point accumulators of ys, zeroed before the launch
   unsigned long long* seg_done;   // [n_seg], zeroed before the launch
   uint32_t* trace;                // tuning builds only (option trace_buf): per-tile role timestamps
+  uint32_t* seg_trace;            // tuning builds only (option seg_trace_buf): [CTA][segment][2] publish / wait-done
 };
 
 // Tuning builds only: %globaltimer (low 32 bits, ns) of pipeline events for the
@@ -144,8 +146,14 @@ constexpr int kTraceCtas = 2, kTraceTiles = 8192;
     if (args.trace && blockIdx.x < kTraceCtas && n_ < kTraceTiles)                                        \
       args.trace[((size_t)blockIdx.x * kTraceTiles + n_) * 8 + (slot)] = (uint32_t)globaltimer();        \
   } while (0)
+#define FC_SEG_TRACE(seg, which)                                                                          \
+  do {                                                                                                    \
+    if (args.seg_trace && (seg) < 512)                                                                    \
+      args.seg_trace[((size_t)blockIdx.x * 512 + (seg)) * 2 + (which)] = (uint32_t)globaltimer();        \
+  } while (0)
 #else
 #define FC_TRACE(slot, n) do {} while (0)
+#define FC_SEG_TRACE(seg, which) do {} while (0)
 #endif
 
 // Fused outputs are accumulated in 64-bit fixed point (2^-40 units): integer
@@ -740,12 +748,14 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
               __threadfence();
               asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(args.seg_done + cur_seg),
                            "l"(seg_mine) : "memory");
+              FC_SEG_TRACE(cur_seg, 0);
             }
             // every earlier segment complete (decoder order), then this CTA's
             // slice of its outputs converted from fixed point
             for (; conv_next < c.seg; ++conv_next) {
               if (releaser && !(args.probe & 4))
                 wait_count(&args.seg_done[conv_next], (unsigned long long)args.segs[conv_next].tile_count);
+              if (releaser) FC_SEG_TRACE(conv_next, 1);
               __syncwarp();
               asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
               fx_convert(args, conv_next, threadIdx.x - 32 * kFirstEpiWarp, 32 * kEpiWarps);
@@ -1058,11 +1068,20 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     }
   }
   if (!ok) { delete plan; *why = "shared memory: rank * top_k too large for the folded kernel"; return cudaErrorNotSupported; }
+  // sweep chunk: one q-row strip (d_model / 128 tiles) when that is 24..64,
+  // else 48.  Measured (r02, same box, median of 2 x 12 passes): 13B (40-tile
+  // strips) 48 -> 40: 10.04 -> 9.77 ms; 7B (32-tile strips) 48 vs 32: equal
+  // within 0.3 %
+  {
+    const int64_t strip = ((int64_t)sp.kind[LSW_Q].d_in + kTN - 1) / kTN;
+    if (strip >= 24 && strip <= 64) plan->chunk = (int)strip;
+  }
   plan->chunk = (int)opt_int("tc_chunk", plan->chunk);
   if (plan->chunk < 1) plan->chunk = 1;
   plan->probe = (int)probe_int("tc_probe") & 17;
 #ifdef LSW_TUNING
   { const char* v = opt_str("trace_buf"); plan->trace = v ? reinterpret_cast<uint32_t*>(strtoull(v, nullptr, 10)) : nullptr; }
+  { const char* v = opt_str("seg_trace_buf"); plan->seg_trace = v ? reinterpret_cast<uint32_t*>(strtoull(v, nullptr, 10)) : nullptr; }
 #endif
   plan->fused_probe = (int)probe_int("fc_fused_probe") & 29;   // tuning builds only: 1 W stream only, 4 no segment wait, 8 no GEMV, 16 no fold math
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
@@ -1190,6 +1209,7 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   a.ys_fx = nullptr;
   a.seg_done = nullptr;
   a.trace = plan->trace;
+  a.seg_trace = plan->seg_trace;
   if (plan->geom.pt)
     switch_fc_kernel<false, true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   else
@@ -1265,6 +1285,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   a.ys_fx = plan->d_ys_fx;
   a.seg_done = plan->d_seg_done;
   a.trace = plan->trace;
+  a.seg_trace = plan->seg_trace;
   switch_fc_kernel<true, false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   return cudaGetLastError();
 }

@@ -44,6 +44,12 @@ def analyse(tr):
         rows["period_w_issue"] = med([t[i, 0] - t[i - 1, 0] for i in range(1, n)])
         rows["frac_tiles_acc_last"] = float(sum(1 for i in range(n) if t[i, 4] > t[i, 5]) / n)
         rows["tiles"] = n
+        per = [t[i, 6] - t[i - 1, 6] for i in range(1, n)]
+        medp = statistics.median(per)
+        big = [x for x in per if x > 2.5 * medp]
+        rows["stalls_over_2.5x_median"] = len(big)
+        rows["stall_excess_us"] = float(sum(x - medp for x in big) / 1e3)
+        rows["all_excess_us"] = float(sum(x - medp for x in per if x > medp) / 1e3)
         rows["pass_us"] = float((t[n - 1, 6] - t[0, 6]) / 1e3)
         # period per eighth of the pass (the kinds come in order in the sweep)
         rows["period_by_eighth"] = [float(statistics.median([t[i, 6] - t[i - 1, 6] for i in range(max(1, n * j // 8), n * (j + 1) // 8)]))
@@ -59,7 +65,8 @@ def main():
         cfg = cfg.with_(n_layers=int(sys.argv[2]))
     W, A, B, router = H.build_weights(cfg, "cuda")
     tr = torch.zeros(2, 8192, 8, dtype=torch.int32, device="cuda")
-    with binding.options(trace_buf=tr.data_ptr()):
+    st = torch.zeros(148, 512, 2, dtype=torch.int32, device="cuda")
+    with binding.options(trace_buf=tr.data_ptr(), seg_trace_buf=st.data_ptr()):
         sw = H.make_switch(cfg, W, A, B, router, impl="tc")
     X1 = synth.gen_x1(cfg, 8, "cuda")
     xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
@@ -76,9 +83,30 @@ def main():
     if sw.info()["switch_kernel"] == 3:
         for t in range(3, 6):
             tr.zero_()
+            st.zero_()
             sw.decode_token_fused(X1[t], xs, ys, idx, gate)
             torch.cuda.synchronize()
         res["fused"] = analyse(tr.cpu().numpy())
+        # segment barrier: per segment, the spread of the CTAs' publish times
+        # (their own last tile of the segment done) and the wait each CTA sees
+        S = st.cpu().numpy().view("uint32").astype("int64")
+        n_cta = int((S[:, 0, 0] != 0).sum())
+        S = S[:n_cta]
+        nseg = int((S[0, :, 0] != 0).sum())
+        ref = S[0, 0, 0]
+        S = ((S - ref) % (1 << 32) + (1 << 31)) % (1 << 32) - (1 << 31)
+        spread, waits, lag = [], [], []
+        for g in range(nseg - 1):
+            pub = sorted(S[:, g, 0])
+            spread.append(float(pub[-1] - pub[len(pub) // 2]))
+            waits.append(float(statistics.median(S[:, g, 1] - S[:, g, 0])))
+            lag.append(float(statistics.median(S[:, g, 1]) - pub[-1]))
+        res["segments"] = {"ctas": n_cta, "segments": nseg,
+                           "publish_spread_last_minus_median_ns": statistics.median(spread),
+                           "publish_spread_mean_ns": sum(spread) / len(spread),
+                           "median_wait_ns": statistics.median(waits),
+                           "wait_after_last_publish_ns": statistics.median(lag),
+                           "per_segment_spread_first_8": [round(x) for x in spread[:8]]}
     print(json.dumps(res, indent=1))
 
 

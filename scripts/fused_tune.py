@@ -15,6 +15,10 @@ from paper_2405_17741_b200 import harness as H  # noqa: E402
 
 
 def main():
+    if sys.argv[1] == "--lib":                  # A/B of two builds: --lib path config specs...
+        lib = sys.argv[2]
+        del sys.argv[1:3]
+        binding._LIB = binding.load_library(lib, strict=False)
     name = sys.argv[1]
     cfg = synth.get_config(name)
     W, A, B, router = H.build_weights(cfg, "cuda")
