@@ -156,7 +156,8 @@ typedef struct {
   int64_t  xs_elems, ys_elems; /* token I/O sizes (lsw_decode_token)                  */
   int32_t  switch_kernel;    /* tensor-core switch mode: 3 = folded coefficients, one */
                              /* accumulator per tile; 4 = per-term accumulators;     */
-                             /* 5 = per-term, B staged per unit; 0 = SIMT            */
+                             /* 5 = per-term, B staged per unit; 6 = the fold on     */
+                             /* CTA pairs (cta_group::2); 0 = SIMT                   */
   int32_t  reserved;
 } lsw_info;
 

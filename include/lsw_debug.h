@@ -19,6 +19,8 @@ extern "C" {
  *   tc_kernel      fold | pt | bu   force a mode of the tensor-core switch
  *                                   [chosen from r, k: DESIGN.md §5]
  *   tc_grid        N      switch grid (CTAs) below the SM count      [#SMs]
+ *   tc_pair        0 | 1  the fold mode on CTA pairs (cta_group::2, M = 256;
+ *                         each CTA stages half of the A^T columns)     [0]
  *   tc_chunk       N      tiles per CTA chunk of the sweep order     [48]
  *   fc_stages / fc_astages / fc_bbufs   explicit shared-memory plan (all three)
  *   fc_wrm         0 | 1  W tile moved by one 4-D TMA op             [1]

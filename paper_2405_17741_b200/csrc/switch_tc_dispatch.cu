@@ -8,6 +8,8 @@
 //               r = 32 with k >= 3)
 //   5 per-term, B per unit: the B slices staged with each unit's A^T slices
 //               when a whole strip of 2k raw B slices does not fit (r = 64, k = 4)
+//   6 the fold on CTA pairs (cta_group::2; option tc_pair = 1, off by
+//               default: measured slower)
 // The variant option "tc_kernel" (lsw_debug.h) = fold | pt | bu forces one.
 #include <cstring>
 
@@ -62,7 +64,7 @@ int64_t tc_plan_bytes(const TcPlan* p) { return fc::tc_plan_bytes(p->c); }
 int tc_plan_grid(const TcPlan* p) { return fc::tc_plan_grid(p->c); }
 int tc_plan_tile_n(const TcPlan* p) { return fc::tc_plan_tile_n(p->c); }
 int64_t tc_plan_tiles(const TcPlan* p) { return fc::tc_plan_tiles(p->c); }
-int tc_plan_kernel(const TcPlan* p) { return p->which; }
+int tc_plan_kernel(const TcPlan* p) { return p->which == 3 && fc::tc_plan_pair(p->c) ? 6 : p->which; }
 const void* tc_plan_packed_B(const TcPlan* p, int kind, int64_t* dout_pad, int* rp) {
   return fc::tc_plan_packed_B(p->c, kind, dout_pad, rp);
 }

@@ -74,6 +74,11 @@ struct Geom {
                                         //    accumulator of 128 columns, kPtGroup terms per commit
   int32_t acc_bufs;                     // TMEM accumulator buffers of acc_cols columns
   uint32_t acc_cols;
+  int32_t pair;                         // fold mode on CTA pairs (cta_group::2, M = 256): each CTA of a
+                                        //   cluster of 2 owns one of two vertically adjacent tiles and loads
+                                        //   HALF of the A^T columns; the leader issues the pair's MMAs
+  TileKinds tkp;                        // pair geometry: row tiles = pairs of 128-row tiles
+  int64_t tiles_pair;
   int32_t bu;                           // per-term mode with the B slices staged per unit (next to
                                         //    the unit's A^T slices) instead of per strip: the plan
                                         //    when a whole strip of 2k raw B slices does not fit
@@ -111,6 +116,7 @@ struct TcPlan {
   void* packed_B[LSW_NKIND] = {};
   int64_t bytes = 0;
   int grid = 0;
+  int pair_grid = 0;          // CTA-pair launches (geom.pair): an even grid
 };
 
 struct Args {
@@ -390,11 +396,44 @@ __device__ __forceinline__ uint64_t dot16(const uint32_t* o, const uint4 x0, con
   return y2;
 }
 
+// ------------------------------------------------------------------ CTA pairs
+
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the mbarrier at the same shared offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(bar), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+// the pair's MMA (leader only): D[256 x 128] += A[256 x K] . B[128 x K]^T, A = the
+// two CTAs' B strips (M halves), B = their A^T halves (N halves), same offsets
+__device__ __forceinline__ void umma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// commit the pair's MMAs to the barrier at this offset in both CTAs
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(bar), "h"((uint16_t)3) : "memory");
+}
+
 // ------------------------------------------------------------------ the kernel
 
-template <bool kF, bool kPT>
+template <bool kF, bool kPT, bool kPair = false>
 __global__ void __launch_bounds__(kThreads, 1)
 switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args args) {
+  static_assert(!kPair || (!kF && !kPT), "CTA pairs: the plain fold mode only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ Coefs cf;
   __shared__ int32_t s_parity;
@@ -403,8 +442,11 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
   __shared__ __align__(8) uint64_t bar_afull[kMaxAStages], bar_aempty[kMaxAStages];
   __shared__ __align__(8) uint64_t bar_braw[2], bar_bfull[2], bar_bempty[2];
   __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
+  __shared__ __align__(8) uint64_t bar_apeer[kMaxAStages], bar_bpeer[2];   // pair: the follower's stages landed
 
   const Geom& g = args.g;
+  const uint32_t crank = kPair ? cta_rank_in_cluster() : 0;
+  const bool leader = crank == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // shared layout (1 KB aligned): [w_stages x W tile][a_stages x A slices][b_bufs x (hi, lo) B strip]
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -433,37 +475,48 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
     for (int s = 0; s < g.a_stages; ++s) {
       mbar_init(smem_u32(&bar_afull[s]), 1);
       mbar_init(smem_u32(&bar_aempty[s]), 1);
+      mbar_init(smem_u32(&bar_apeer[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&bar_braw[s]), 1);
       mbar_init(smem_u32(&bar_bfull[s]), g.b_bufs == 1 && !g.pt ? 2 : 1);   // fold: + the MMA warp's half
       mbar_init(smem_u32(&bar_bempty[s]), 1);
+      mbar_init(smem_u32(&bar_bpeer[s]), 1);
     }
     for (int s = 0; s < g.acc_bufs; ++s) {
       mbar_init(smem_u32(&bar_accfull[s]), 1);
-      mbar_init(smem_u32(&bar_accempty[s]), kEpiWarps);
+      mbar_init(smem_u32(&bar_accempty[s]), kPair ? 2 * kEpiWarps : kEpiWarps);   // pair: both CTAs' epilogues
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0)
     for (int k = 0; k < LSW_NKIND; ++k) prefetch_map(args.mode == MODE_RESTORE ? &maps.p[k] : &maps.w[k]);
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(smem_u32(&s_tmem_base)), "r"(kAccBufs * kTN) : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(&s_tmem_base)), "r"(kAccBufs * kTN) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                   ::"r"(smem_u32(&s_tmem_base)), "r"(kAccBufs * kTN) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync_all();      // the peer's barriers exist before any remote arrive / commit
   tc_fence_after();
 
   const int nt = cf.bad ? 0 : cf.n;
   TileSeq seq;
-  seq.T = args.t_count > 0 ? args.t_count : g.tiles_total;
+  seq.T = args.t_count > 0 ? args.t_count : kPair ? g.tiles_pair : g.tiles_total;
   seq.t0 = args.t0;
   seq.chunk = args.chunk < 1 ? 1 : args.chunk;
-  seq.G = gridDim.x;
-  seq.b = blockIdx.x;
-  const TileKinds& tk = g.tk;
+  seq.G = kPair ? gridDim.x / 2 : gridDim.x;      // pair: both CTAs of a cluster walk the same pair tiles
+  seq.b = kPair ? blockIdx.x / 2 : blockIdx.x;
+  const TileKinds& tk = kPair ? g.tkp : g.tk;
+  // pair: this CTA's 128-row tile of the pair tile's 256 rows
+  auto rbr = [&](int rb) { return kPair ? 2 * rb + (int)crank : rb; };
   const uint32_t tmem_base = s_tmem_base;
 
   // Nothing to add (nt == 0: the new decision equals the merged one, R12, or
@@ -484,10 +537,10 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           mbar_expect_tx(wbar, 2 * kSubBytes);
           uint8_t* wdst = wst0 + (size_t)wring.i * (2 * kSubBytes);
           if (g.wrm)
-            tma_load_4d(smem_u32(wdst), &src[c.kd], 0, c.cb * 2, c.rb * kTM, c.layer, wbar, pol_stream);
+            tma_load_4d(smem_u32(wdst), &src[c.kd], 0, c.cb * 2, rbr(c.rb) * kTM, c.layer, wbar, pol_stream);
           else
             for (int sb = 0; sb < 2; ++sb)
-              tma_load_3d(smem_u32(wdst + sb * kSubBytes), &src[c.kd], c.cb * kTN + sb * kSubCols, c.rb * kTM,
+              tma_load_3d(smem_u32(wdst + sb * kSubBytes), &src[c.kd], c.cb * kTN + sb * kSubCols, rbr(c.rb) * kTM,
                           c.layer, wbar, pol_stream);
           wring.next();
         }
@@ -507,11 +560,11 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           }
           uint8_t* wsrc = wst0 + (size_t)wring.i * (2 * kSubBytes);
           if (g.wrm)
-            tma_store_4d(&maps.w[c.kd], smem_u32(wsrc), 0, c.cb * 2, c.rb * kTM, c.layer, pol_stream);
+            tma_store_4d(&maps.w[c.kd], smem_u32(wsrc), 0, c.cb * 2, rbr(c.rb) * kTM, c.layer, pol_stream);
           else
             for (int sb = 0; sb < 2; ++sb)
               tma_store_3d(&maps.w[c.kd], smem_u32(wsrc + sb * kSubBytes), c.cb * kTN + sb * kSubCols,
-                           c.rb * kTM, c.layer, pol_stream);
+                           rbr(c.rb) * kTM, c.layer, pol_stream);
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read -> stage reusable
           FC_TRACE(7, ns_tr++);
@@ -591,7 +644,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             mbar_expect_tx(rbar, nt * tb);
             for (int j = 0; j < nt; ++j) {
               const __nv_bfloat16* src = g.Bp[c.kd] + (((size_t)c.layer * g.n_experts + cf.e[j]) * g.dout_pad[c.kd] +
-                                                       (size_t)c.rb * kTM) * rpe;
+                                                       (size_t)rbr(c.rb) * kTM) * rpe;
               bulk_load(smem_u32(dst + (2 * j + 1) * tb), src, tb, rbar, pol_keep);
             }
           }
@@ -611,9 +664,12 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           FC_TRACE(1, na_tr);
           uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
           const uint32_t bar = smem_u32(&bar_afull[aring.i]);
-          mbar_expect_tx(bar, nt * tb);
+          // pair: this CTA's half of the tile's 128 columns (rows 64 * rank.. of each A^T slice)
+          const uint32_t ta = kPair ? tb / 2 : tb;
+          mbar_expect_tx(bar, nt * ta);
           for (int j = 0; j < nt; ++j)
-            bulk_load(smem_u32(adst + j * tb), blk + (size_t)cf.e[j] * kTN * rpe, tb, bar, pol_keep);
+            bulk_load(smem_u32(adst + j * ta), blk + (size_t)cf.e[j] * kTN * rpe + (size_t)crank * (kTN / 2) * rpe,
+                      ta, bar, pol_keep);
         }
         __syncwarp();
         aring.next();
@@ -626,12 +682,14 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       // slice, K = rp each in steps of 16, into the tile's single accumulator;
       // ONE commit per tile.
       // instruction descriptor: D f32, A/B bf16, both K-major, N = 128, M = 128
+      // (pair: M = 256 -- the two CTAs' 128-row tiles)
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTN >> 3) << 17) |
-                             ((uint32_t)(kTM >> 4) << 24);
+                             ((uint32_t)((kPair ? 2 : 1) * kTM >> 4) << 24);
       const uint32_t sbo = 8 * (uint32_t)g.rp * 2;
       const int ksteps = g.rp / 16;
       const uint64_t desc0 = umma_desc(0, sbo, g.swz_mode);
       const uint64_t term = g.term_bytes >> 4;
+      const uint64_t aterm = (kPair ? g.term_bytes / 2 : g.term_bytes) >> 4;   // A^T slice per term in a stage
       Ring bring{0, 0, (uint32_t)g.b_bufs};
       Ring aring{0, 0, (uint32_t)g.a_stages};
       Ring acc{0, 0, (uint32_t)g.acc_bufs};
@@ -644,7 +702,12 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             // once they complete -- released by a commit here, not after the
             // epilogue (up to kAccBufs tiles behind) has seen them, so a single
             // B buffer is refolded while the epilogue drains the accumulators
-            if (elect_one()) umma_commit(smem_u32(&bar_bempty[bring.i]));
+            // (pair: the leader's commit frees both CTAs' buffers)
+            if constexpr (kPair) {
+              if (leader && elect_one()) umma_commit_pair(smem_u32(&bar_bempty[bring.i]));
+            } else {
+              if (elect_one()) umma_commit(smem_u32(&bar_bempty[bring.i]));
+            }
             __syncwarp();
             bring.next();
           }
@@ -661,6 +724,23 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             if (lane == 0) mbar_arrive(smem_u32(&bar_bfull[bring.i]));
           }
           mbar_wait(smem_u32(&bar_bfull[bring.i]), bring.phase);
+          if constexpr (kPair) {
+            // the leader's MMAs read both strips: the follower reports its own
+            if (!leader) {
+              if (lane == 0) mbar_arrive_remote(smem_u32(&bar_bpeer[bring.i]), 0);
+            } else {
+              mbar_wait(smem_u32(&bar_bpeer[bring.i]), bring.phase);
+            }
+          }
+        }
+        if constexpr (kPair) {
+          if (!leader) {                         // follower: report the A stage, no MMA
+            mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(smem_u32(&bar_apeer[aring.i]), 0);
+            aring.next();
+            continue;
+          }
         }
         if constexpr (kPT) {
           // per-term mode: kPtGroup terms per group, each into its own 128-column
@@ -689,13 +769,24 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           continue;
         }
         mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
+        if constexpr (kPair) mbar_wait(smem_u32(&bar_apeer[aring.i]), aring.phase);
         if (lane == 0) FC_TRACE(2, nm_tr);
         mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
         tc_fence_after();
         const uint64_t b_desc = desc0 + (smem_u32(bst0 + (size_t)bring.i * g.b_buf_bytes) >> 4);
         const uint64_t a_desc = desc0 + (smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes) >> 4);
         const uint32_t d = tmem_base + acc.i * kTN;
-        if (elect_one()) {
+        if constexpr (kPair) {
+          if (elect_one()) {
+            for (int j = 0; j < nt; ++j)
+              for (int part = 0; part < 2; ++part)
+                for (int kk = 0; kk < ksteps; ++kk)
+                  umma_f16_pair(d, b_desc + (2 * j + part) * term + kk * 2, a_desc + j * aterm + kk * 2, idesc,
+                                (j | part | kk) != 0 ? 1u : 0u);
+            umma_commit_pair(smem_u32(&bar_aempty[aring.i]));   // both CTAs' A stages free when these complete
+            umma_commit_pair(smem_u32(&bar_accfull[acc.i]));
+          }
+        } else if (elect_one()) {
           for (int j = 0; j < nt; ++j)
             for (int part = 0; part < 2; ++part)
               for (int kk = 0; kk < ksteps; ++kk)
@@ -831,7 +922,8 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         if (nt > 0) {
           mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);      // the tile's MMAs are complete
           if (releaser) FC_TRACE(4, ne_tr);
-          if (releaser) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
+          // (pair: the leader's commit released both CTAs' A stages)
+          if (releaser && !kPair) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
           aring.next();
           tc_fence_after();
           const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTN + half * kSubCols;
@@ -840,7 +932,10 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           tmem_wait_ld();
           tc_fence_before();                       // accumulator consumed -> MMA may reuse the buffer
           __syncwarp();
-          if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+          if (lane == 0) {
+            if (kPair && !leader) mbar_arrive_remote(smem_u32(&bar_accempty[acc.i]), 0);   // the leader's MMA
+            else mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+          }
           acc.next();
         } else {                                   // fused, nothing to add: y from the unchanged W
 #pragma unroll
@@ -913,10 +1008,15 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPair) cluster_sync_all();      // no remote arrive / commit may target a CTA that left
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAccBufs * kTN)
-                 : "memory");
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAccBufs * kTN)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAccBufs * kTN)
+                   : "memory");
   }
   if (threadIdx.x == 0) {
     SwitchParams p{};
@@ -1009,62 +1109,85 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     g.b_buf_bytes = align1k((uint32_t)(2 * mt) * g.term_bytes);
   }
   const uint32_t w_stage = 2 * kSubBytes;
-  // Shared-memory plan, in order of preference (measured, 7B shape: W 3 + B 2 +
-  // A 3 0.895 of the copy peak vs W 4 + B 1 + A 3 0.868 -- a single B buffer
-  // drains the MMA pipeline at every strip change, a 4th W stage buys nothing);
-  // what is left goes to more W stages.
-  const int64_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
-  // A ring depth in units per tile u (fold: the whole tile's slices; per-term:
-  // one unit per kPtGroup terms).  Candidates (W stages, B buffers) in order of
-  // preference -- three W stages first: a fourth puts more W requests in flight
-  // than the HBM stream wants (k = 1, same box: W 3 + B 2 + A 4 0.895 vs W 4 +
-  // B 2 + A 3 0.85; the W-stream probe itself 0.872 with 4 stages vs 0.91 with
-  // 3); for each the A stages that fit.  Pass 0 wants 2u + 1 A units
-  // (a tile of lookahead), pass 1 u + 1, pass 2 any >= 2; W stays >= 3 before
-  // the last resort (measured, 16-layer 7B shape: W 2 costs 7-15 %; W 3 + B 1
-  // + A 3 0.860 vs W 4 + B 1 + A 2 0.846 at k = 3; per-term r = 32 k = 3:
-  // W 3 + B 1 + A 5 0.656 vs W 3 + B 2 + A 2 0.626).
-  struct Cand { int ws, bb; };
-  const Cand cands[] = {{3, 2}, {3, 1}, {4, 2}, {4, 1}};
-  const int u = g.pt ? (mt + kPtGroup - 1) / kPtGroup : 1;
-  const int bb_min = g.bu ? 0 : 1;           // bu: no strip buffer
   const int bb_opt = (int)opt_int("fc_bbufs", 0), as_opt = (int)opt_int("fc_astages", 0),
             ws_opt = (int)opt_int("fc_stages", 0);
-  bool ok = false;
-  if (bb_opt >= bb_min && bb_opt <= 2 && as_opt >= 2 && as_opt <= kMaxAStages && ws_opt >= 2 &&
-      ws_opt <= kMaxStages &&
-      budget >= (int64_t)bb_opt * g.b_buf_bytes + (int64_t)as_opt * g.a_stage_bytes + (int64_t)ws_opt * w_stage) {
-    g.w_stages = ws_opt;                     // variant option: an explicit plan (all three set)
-    g.a_stages = as_opt;
-    g.b_bufs = g.bu ? 0 : bb_opt;
-    ok = true;
-  }
-  for (int pass = 0; pass < 3 && !ok; ++pass) {
-    const int a_min = pass == 0 ? 2 * u + 1 : pass == 1 ? u + 1 : 2;
-    for (const Cand& c : cands) {
-      const int bb = g.bu ? 0 : c.bb;
-      const int64_t rest = budget - (int64_t)c.ws * w_stage - (int64_t)bb * g.b_buf_bytes;
-      if (rest < 0) continue;
-      int as = (int)(rest / g.a_stage_bytes);
-      if (as > kMaxAStages) as = kMaxAStages;
-      if (as < a_min) continue;
-      g.w_stages = c.ws;
-      g.a_stages = as;
-      g.b_bufs = bb;
-      ok = true;
-      break;
+  // Shared-memory plan for an A stage of `asb` bytes, in order of preference
+  // (measured, 7B shape: W 3 + B 2 + A 3 0.895 of the copy peak vs W 4 + B 1 +
+  // A 3 0.868 -- a single B buffer drains the MMA pipeline at every strip
+  // change, a 4th W stage buys nothing); what is left goes to more W stages.
+  auto make_plan = [&](uint32_t asb) -> bool {
+    const int64_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
+    // A ring depth in units per tile u (fold: the whole tile's slices; per-term:
+    // one unit per kPtGroup terms).  Candidates (W stages, B buffers) in order of
+    // preference -- three W stages first: a fourth puts more W requests in flight
+    // than the HBM stream wants (k = 1, same box: W 3 + B 2 + A 4 0.895 vs W 4 +
+    // B 2 + A 3 0.85; the W-stream probe itself 0.872 with 4 stages vs 0.91 with
+    // 3); for each the A stages that fit.  Pass 0 wants 2u + 1 A units
+    // (a tile of lookahead), pass 1 u + 1, pass 2 any >= 2; W stays >= 3 before
+    // the last resort (measured, 16-layer 7B shape: W 2 costs 7-15 %; W 3 + B 1
+    // + A 3 0.860 vs W 4 + B 1 + A 2 0.846 at k = 3; per-term r = 32 k = 3:
+    // W 3 + B 1 + A 5 0.656 vs W 3 + B 2 + A 2 0.626).
+    struct Cand { int ws, bb; };
+    const Cand cands[] = {{3, 2}, {3, 1}, {4, 2}, {4, 1}};
+    const int u = g.pt ? (mt + kPtGroup - 1) / kPtGroup : 1;
+    const int bb_min = g.bu ? 0 : 1;           // bu: no strip buffer
+    if (bb_opt >= bb_min && bb_opt <= 2 && as_opt >= 2 && as_opt <= kMaxAStages && ws_opt >= 2 &&
+        ws_opt <= kMaxStages &&
+        budget >= (int64_t)bb_opt * g.b_buf_bytes + (int64_t)as_opt * asb + (int64_t)ws_opt * w_stage) {
+      g.w_stages = ws_opt;                     // variant option: an explicit plan (all three set)
+      g.a_stages = as_opt;
+      g.b_bufs = g.bu ? 0 : bb_opt;
+      return true;
     }
-  }
-  if (!ok) {                                 // last resort: two W stages
-    for (int bb = g.bu ? 0 : 2; bb >= bb_min && !ok; --bb) {
+    for (int pass = 0; pass < 3; ++pass) {
+      const int a_min = pass == 0 ? 2 * u + 1 : pass == 1 ? u + 1 : 2;
+      for (const Cand& c : cands) {
+        const int bb = g.bu ? 0 : c.bb;
+        const int64_t rest = budget - (int64_t)c.ws * w_stage - (int64_t)bb * g.b_buf_bytes;
+        if (rest < 0) continue;
+        int as = (int)(rest / asb);
+        if (as > kMaxAStages) as = kMaxAStages;
+        if (as < a_min) continue;
+        g.w_stages = c.ws;
+        g.a_stages = as;
+        g.b_bufs = bb;
+        return true;
+      }
+    }
+    for (int bb = g.bu ? 0 : 2; bb >= bb_min; --bb) {   // last resort: two W stages
       const int64_t rest = budget - 2 * (int64_t)w_stage - (int64_t)bb * g.b_buf_bytes;
-      int as = rest > 0 ? (int)(rest / g.a_stage_bytes) : 0;
+      int as = rest > 0 ? (int)(rest / asb) : 0;
       if (as > kMaxAStages) as = kMaxAStages;
       if (as < 2) continue;
       g.w_stages = 2;
       g.a_stages = as;
       g.b_bufs = bb;
-      ok = true;
+      return true;
+    }
+    return false;
+  };
+  bool ok = make_plan(g.a_stage_bytes);
+  // CTA pairs (fold mode, variant option tc_pair = 1; off by default): each
+  // CTA stages half of a tile's A^T columns (the same shared memory holds twice
+  // the A lookahead) and the leader issues the pair's M = 256 MMAs.  Measured
+  // (13B, same box): 12.6 vs 9.57 ms per switch -- the per-tile trace shows the
+  // A stage cycle stretched from 1.4 to 6.5 us by the cross-CTA chain (the
+  // leader's commit frees the follower's stage, the follower refills it and
+  // reports it back before the leader's next MMA) and the W stages held longer
+  // by the pair's lockstep.
+  {
+    const long pair_opt = opt_int("tc_pair", 0);
+    const bool want = !g.pt && pair_opt == 1 && num_sms >= 2 && opt_int("tc_grid", 0) != 1;
+    if (want) {
+      const uint32_t half = align1k((uint32_t)mt * g.term_bytes / 2);
+      const Geom keep = g;
+      if (make_plan(half)) {
+        g.pair = 1;
+        g.a_stage_bytes = half;
+        ok = true;
+      } else {
+        g = keep;
+      }
     }
   }
   if (!ok) { delete plan; *why = "shared memory: rank * top_k too large for the folded kernel"; return cudaErrorNotSupported; }
@@ -1095,16 +1218,35 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     const KindGeom& kg = sp.kind[k];
     g.tk.row_tiles[k] = (int32_t)((kg.d_out + kTM - 1) / kTM);
     g.tk.col_tiles[k] = (int32_t)((kg.d_in + kTN - 1) / kTN);
-    g.dout_pad[k] = (int64_t)g.tk.row_tiles[k] * kTM;
+    // packed B rows padded to an even number of row tiles: a pair's second
+    // tile past d_out reads zeros
+    g.dout_pad[k] = (int64_t)((g.tk.row_tiles[k] + 1) / 2 * 2) * kTM;
     g.d_in[k] = kg.d_in;
     g.d_out[k] = kg.d_out;
     g.tk.tile_begin[k] = t;
     t += (int64_t)sp.n_layers * g.tk.row_tiles[k] * g.tk.col_tiles[k];
   }
   g.tiles_total = t;
+  // pair geometry: the row tiles of each matrix taken two by two
+  g.tkp = g.tk;
+  {
+    int64_t tp = 0;
+    for (int k = 0; k < LSW_NKIND; ++k) {
+      g.tkp.row_tiles[k] = (g.tk.row_tiles[k] + 1) / 2;
+      g.tkp.tile_begin[k] = tp;
+      tp += (int64_t)sp.n_layers * g.tkp.row_tiles[k] * g.tkp.col_tiles[k];
+    }
+    g.tiles_pair = tp;
+  }
   plan->grid = (int)(t < num_sms ? t : num_sms);
   { const int x = (int)opt_int("tc_grid", 0); if (x >= 1 && x < plan->grid) plan->grid = x; }
   if (plan->grid < 1) plan->grid = 1;
+  if (g.pair) {                                  // clusters of 2: an even grid, <= 2 per pair tile
+    int gp = num_sms / 2 * 2;
+    if (gp > 2 * g.tiles_pair) gp = (int)(2 * g.tiles_pair);
+    { const int x = (int)opt_int("tc_grid", 0); if (x >= 2 && x < gp) gp = x / 2 * 2; }
+    plan->pair_grid = gp < 2 ? 2 : gp;
+  }
   // pack operands + encode maps (same packed images as the term-group kernel,
   // with 128-column A^T blocks)
   const int64_t M = (int64_t)sp.n_layers * sp.n_experts;
@@ -1141,6 +1283,9 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(switch_fc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)g.smem_bytes);
+  if (e == cudaSuccess && g.pair)
+    e = cudaFuncSetAttribute(switch_fc_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)g.smem_bytes);
   if (e != cudaSuccess) {
     if (!*why || !**why) *why = cudaGetErrorString(e);
     tc_plan_destroy(plan);
@@ -1163,8 +1308,9 @@ void tc_plan_destroy(TcPlan* plan) {
 }
 
 int64_t tc_plan_bytes(const TcPlan* plan) { return plan ? plan->bytes : 0; }
-int tc_plan_grid(const TcPlan* plan) { return plan ? plan->grid : 0; }
+int tc_plan_grid(const TcPlan* plan) { return plan ? (plan->geom.pair ? plan->pair_grid : plan->grid) : 0; }
 int tc_plan_tile_n(const TcPlan* plan) { return plan ? kTN : 0; }
+int tc_plan_pair(const TcPlan* plan) { return plan ? plan->geom.pair : 0; }
 int64_t tc_plan_tiles(const TcPlan* plan) { return plan ? plan->geom.tiles_total : 0; }
 const void* tc_plan_packed_B(const TcPlan* plan, int kind, int64_t* dout_pad, int* rp) {
   *dout_pad = plan->geom.dout_pad[kind];
@@ -1210,10 +1356,26 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   a.seg_done = nullptr;
   a.trace = plan->trace;
   a.seg_trace = plan->seg_trace;
-  if (plan->geom.pt)
+  if (plan->geom.pt) {
     switch_fc_kernel<false, true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
-  else
+  } else if (plan->geom.pair && t_count == 0) {
+    // CTA pairs (the per-matrix ablation keeps single CTAs: its tile ranges are single-CTA tiles)
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(plan->pair_grid);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = plan->geom.smem_bytes;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, switch_fc_kernel<false, false, true>, plan->maps, a);
+  } else {
     switch_fc_kernel<false, false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  }
   return cudaGetLastError();
 }
 

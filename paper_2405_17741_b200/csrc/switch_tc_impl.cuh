@@ -31,6 +31,7 @@ cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4]
 cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cudaStream_t s, const void* xs,
                                    float* ys);
 const void* tc_plan_packed_B(const TcPlan* plan, int kind, int64_t* dout_pad, int* rp);
+int tc_plan_pair(const TcPlan* plan);   // 1: the plain switch runs on CTA pairs
 }  // namespace fc
 
 }  // namespace lsw

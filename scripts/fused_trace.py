@@ -63,10 +63,11 @@ def main():
     cfg = synth.get_config(name)
     if len(sys.argv) > 2:
         cfg = cfg.with_(n_layers=int(sys.argv[2]))
+    extra = dict(kv.split("=") for kv in sys.argv[3:])        # variant options, e.g. tc_pair=1
     W, A, B, router = H.build_weights(cfg, "cuda")
     tr = torch.zeros(2, 8192, 8, dtype=torch.int32, device="cuda")
     st = torch.zeros(148, 512, 2, dtype=torch.int32, device="cuda")
-    with binding.options(trace_buf=tr.data_ptr(), seg_trace_buf=st.data_ptr()):
+    with binding.options(trace_buf=tr.data_ptr(), seg_trace_buf=st.data_ptr(), **extra):
         sw = H.make_switch(cfg, W, A, B, router, impl="tc")
     X1 = synth.gen_x1(cfg, 8, "cuda")
     xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))

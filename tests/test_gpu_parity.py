@@ -116,11 +116,12 @@ def test_switch_trajectory_full_elements(name, impl):
 
 # (mode of the fc kernel, extra variant options); KERNEL_ID = lsw_info.switch_kernel
 TC_VARIANTS = [("fold", {}), ("fold", {"fc_stages": 3, "fc_astages": 2, "fc_bbufs": 1}), ("fold", {"fc_wrm": 0}),
-               ("pt", {}), ("pt", {"fc_wrm": 0}), ("bu", {}), ("bu", {"fc_wrm": 0})]
-KERNEL_ID = {"fold": 3, "pt": 4, "bu": 5}
+               ("pt", {}), ("pt", {"fc_wrm": 0}), ("bu", {}), ("bu", {"fc_wrm": 0}),
+               ("fold", {"tc_pair": 1}), ("fold", {"tc_pair": 1, "fc_wrm": 0}), ("fold", {"tc_pair": 0})]
+KERNEL_ID = {"fold": (3, 6), "pt": (4,), "bu": (5,)}
 
 
-@pytest.mark.parametrize("grid", [1, 3])
+@pytest.mark.parametrize("grid", [1, 2, 3])
 @pytest.mark.parametrize("variant", range(len(TC_VARIANTS)))
 @pytest.mark.parametrize("name", ["mini", "mini-r32", "mini-r4k4", "mini-r64k3", "mini-r64k4"])
 def test_tc_switch_many_tiles_per_cta(lsw_opts, name, variant, grid):
@@ -128,8 +129,10 @@ def test_tc_switch_many_tiles_per_cta(lsw_opts, name, variant, grid):
     tiny grid so every ring (W, A, B, TMEM accumulators) wraps many times, for
     each mode of the tensor-core kernel: the fold (one accumulator per tile;
     with a single B buffer every strip change waits for the previous strip's
-    MMAs), per-term (one accumulator per term, B per strip) and per-term with
-    the B slices staged per unit."""
+    MMAs), the fold on CTA pairs (cta_group::2, grid 2: one pair walking every
+    pair tile; odd row-tile counts give pairs whose second tile is past d_out),
+    per-term (one accumulator per term, B per strip) and per-term with the B
+    slices staged per unit."""
     mode, opts = TC_VARIANTS[variant]
     lsw_opts(tc_grid=grid, tc_kernel=mode, **opts)
     try:
@@ -138,7 +141,13 @@ def test_tc_switch_many_tiles_per_cta(lsw_opts, name, variant, grid):
         assert mode in ("fold", "pt") and "UNSUPPORTED" in str(e)
         pytest.skip(str(e))
     info = S.sw.info()
-    assert info["grid"] == grid and info["switch_kernel"] == KERNEL_ID[mode]
+    assert info["switch_kernel"] in KERNEL_ID[mode]
+    if opts.get("tc_pair") == 1 and grid >= 2:
+        assert info["switch_kernel"] == 6
+    if opts.get("tc_pair") == 0:
+        assert info["switch_kernel"] == 3
+    # CTA pairs run an even grid (grid 1: no pair)
+    assert info["grid"] == (grid // 2 * 2 if info["switch_kernel"] == 6 else grid)
     worst = _run_token_checks(S, 5)
     print(f"{name} {mode} {opts} grid={grid}: worst {worst}")
 
