@@ -1,4 +1,4 @@
 #!/bin/bash
 python -c "import __graft_entry__ as g; g.build()" > /dev/null || exit 1
-timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "mini-r32 and tc and (test_switch_trajectory or many_tiles)" 2>&1 | tail -15
-timeout 300 python scripts/tune_switch.py --config llama2-13b --repeat 2 "tc_pair=0" "tc_pair=1" 2>&1 | tail -4
+timeout 600 python -m pytest tests/test_gpu_fused.py -q -x 2>&1 | tail -2
+for i in 1 2 3; do python scripts/fused_tune.py --lib build/liblsw_A.so llama2-7b "old:" 2>&1 | grep "^old"; python scripts/fused_tune.py llama2-7b "new:" 2>&1 | grep "^new"; done
