@@ -1,6 +1,7 @@
 """Full-size parity at BASELINE.json's shapes -- Llama-2-7B (configs[1]),
-Mistral-7B (configs[2]: GQA k/v 1024 x 4096, d_ff 14336) and Llama-2-13B
-(configs[3]: r = 32, the fc fold plan with a single B buffer) -- in the launch
+Mistral-7B (configs[2]: GQA k/v 1024 x 4096, d_ff 14336), Llama-2-13B
+(configs[3]: r = 32, the fc fold plan with a single B buffer) and two
+configs[4] sweep cells that run the switch's per-term modes -- in the launch
 configuration bench.py times (auto -> tcgen05 switch, persistent grid = #SMs,
 lsw_decode_token), on sampled rows the oracle computes one by one (-m gpu).
 
@@ -32,6 +33,10 @@ CASES = {
     "llama2-7b": ((0, 1, 15, 31), 1000, (1, 2, 10, 100, 1000)),
     "mistral-7b": ((0, 1, 15, 31), 10, (1, 2, 10)),
     "llama2-13b": ((0, 1, 19, 39), 10, (1, 2, 10)),
+    # configs[4] sweep cells on the 7B shape in the switch's other modes:
+    # per-term accumulators (r = 32, k = 3) and B staged per unit (r = 64, k = 4)
+    "sweep-n16-r32-k3": ((0, 31), 10, (1, 2, 10)),
+    "sweep-n8-r64-k4": ((0, 31), 10, (1, 2, 10)),
 }
 # Trajectory divergence at token 1000 with the hi+lo coefficient split of the
 # fc fold (R13): ~1e-3 of the elements take a 1-ulp double-rounding
