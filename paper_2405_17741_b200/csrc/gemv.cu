@@ -362,8 +362,9 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   // Chunks issued so far.  A consumer warp takes only every 16th row, so it can
   // reach a slot's NEXT-but-one fill while the next fill is not yet issued; the
   // full barrier's parity would then alias an already completed phase.  Waiting
-  // for the ticket first makes the parity wait unambiguous.  Written and read
-  // with release / acquire atomics (CTA scope): the consumer's parity wait then
+  // for the ticket first makes the parity wait unambiguous.  Written with
+  // st.release and read with ld.acquire (CTA scope, morally strong -- not a
+  // data race, though racecheck reports it): the consumer's parity wait then
   // sees at least the producer's expect_tx of that chunk.
   __shared__ int64_t issued;
   if (threadIdx.x == 0) {
@@ -412,8 +413,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
               : "memory");
           r = run_end;
         }
-        asm volatile("atom.release.cta.shared::cta.exch.b64 _, [%0], %1;" ::"r"(s_u32(&issued)), "l"(i + 1)
-                     : "memory");
+        asm volatile("st.release.cta.shared::cta.b64 [%0], %1;" ::"r"(s_u32(&issued)), "l"(i + 1) : "memory");
       }
     }
     return;
@@ -422,9 +422,13 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after our wait: see above
   // unmerged form: the decision is validated by every CTA alike (indices in
   // [0, N) and distinct, gates finite -- as the switch's build_coefs); an
-  // invalid one drops the LoRA terms (y = W x) and latches the error
-  bool lora_ok = kLora;
-  if (kLora) {
+  // invalid one drops the LoRA terms (y = W x) and latches the error.  Only
+  // the LoRA warps look at it (the consumers start streaming at once: the
+  // check's dependent global loads cost 5 % of the token when every warp ran
+  // it); the consumers read the verdict after their final barrier with them.
+  __shared__ int32_t s_lora_ok;
+  bool lora_ok = false;
+  if (kLora && warp > kBulkConsumers) {
     int bad = 0;
     for (int j = 0; j < L.k; ++j) {
       const int32_t e = L.idx[j];
@@ -433,7 +437,10 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
       if (!bad && !isfinite(L.gate[j])) bad = LSW_DEV_BAD_GATE;
     }
     lora_ok = bad == 0;
-    if (bad && blockIdx.x == 0 && threadIdx.x == 32) atomicCAS(L.err, 0, bad);
+    if (threadIdx.x == 32 * (1 + kBulkConsumers)) {
+      s_lora_ok = lora_ok;
+      if (bad && blockIdx.x == 0) atomicCAS(L.err, 0, bad);
+    }
   }
   const int kr = lora_ok ? L.k * L.r : 0;
   const int n_dots = kLora ? p.n_sites * kr : 0;
@@ -527,7 +534,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     const int64_t row = (blockIdx.x + i * G) * R + k;
     for (;;) {                                    // ticket: chunk i's fill is armed
       int64_t v;
-      asm volatile("atom.acquire.cta.shared::cta.add.u64 %0, [%1], 0;" : "=l"(v) : "r"(s_u32(&issued)) : "memory");
+      asm volatile("ld.acquire.cta.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(s_u32(&issued)) : "memory");
       if (v > i) break;
       __nanosleep(64);
     }
@@ -539,9 +546,9 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
         else p.y[row] = acc;
       }
     }
-    // the warp's generic-proxy reads of the slot are ordered before the next
-    // bulk copy (async proxy) into it: proxy fence, then the release arrive
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // (the slot's reads have returned before the release arrive; the producer's
+    // acquire wait orders the next bulk copy after them -- no proxy fence, as in
+    // TMA pipelines: measured, one per row costs 5 % of the unmerged decode)
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[s])) : "memory");
   }
@@ -549,6 +556,7 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     // Eq. 2: y = (W x) + LoRA-up term, one rounding of the sum per row
     __syncwarp();
     asm volatile("barrier.sync 3, %0;" ::"r"(32 * (kBulkConsumers + kLoraWarps)) : "memory");   // two code sites: not .aligned   // e_s / us ready
+    lora_ok = s_lora_ok != 0;                      // written by the LoRA warps before the barrier
     const bool up = !(L.flags & 4) && !(early_w & 2) && lora_ok;
     if (in_smem) {
       for (int64_t t = threadIdx.x - 32; t < n_local; t += 32 * kBulkConsumers) {
