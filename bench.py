@@ -115,7 +115,8 @@ class ClockSampler:
 
 SWITCH_KERNELS = {3: "switch_fc_kernel [fold: folded coefficients, one accumulator per tile]",
                   4: "switch_fc_kernel [per-term accumulators, B per strip]",
-                  5: "switch_fc_kernel [per-term accumulators, B per unit]"}
+                  5: "switch_fc_kernel [per-term accumulators, B per unit]",
+                  7: "switch_fc_kernel [fold, (hi, lo) B strip in TMEM: one accumulator per tile]"}
 
 
 def _ncu_traffic(cfg, info):

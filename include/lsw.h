@@ -157,7 +157,8 @@ typedef struct {
   int32_t  switch_kernel;    /* tensor-core switch mode: 3 = folded coefficients, one */
                              /* accumulator per tile; 4 = per-term accumulators;     */
                              /* 5 = per-term, B staged per unit; 6 = the fold on     */
-                             /* CTA pairs (cta_group::2); 0 = SIMT                   */
+                             /* CTA pairs (cta_group::2); 7 = the fold with its      */
+                             /* (hi, lo) B strip in TMEM; 0 = SIMT                   */
   int32_t  reserved;
 } lsw_info;
 

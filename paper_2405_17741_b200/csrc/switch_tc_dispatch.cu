@@ -10,6 +10,10 @@
 //               when a whole strip of 2k raw B slices does not fit (r = 64, k = 4)
 //   6 the fold on CTA pairs (cta_group::2; option tc_pair = 1, off by
 //               default: measured slower)
+//   7 the fold with the (hi, lo) B strip in TMEM (the MMA's M-side operand
+//               read from TMEM, folded there by the epilogue warps; shared
+//               memory keeps only a raw strip; option tc_tb = 1 where
+//               2k * rp <= 256; off by default: measured slower)
 // The variant option "tc_kernel" (lsw_debug.h) = fold | pt | bu forces one.
 #include <cstring>
 
@@ -35,6 +39,9 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& geom, int num_sms, 
     // per-term mode for r = 64 and for r = 32 with k >= 3; each falls back to
     // the other, then to B per unit, if its shared-memory plan does not fit
     const int rp = geom.rank <= 16 ? 16 : geom.rank <= 32 ? 32 : 64;
+    // measured: the fold up to 2k * rp = 128 at r <= 32, the
+    // per-term mode for r = 64 and for r = 32 with k >= 3; each falls back to
+    // the other, then to B per unit, if its shared-memory plan does not fit
     const bool pt_first = rp == 64 || (rp == 32 && geom.top_k >= 3);
     order[n++] = pt_first ? 1 : 0;
     order[n++] = pt_first ? 0 : 1;
@@ -64,7 +71,11 @@ int64_t tc_plan_bytes(const TcPlan* p) { return fc::tc_plan_bytes(p->c); }
 int tc_plan_grid(const TcPlan* p) { return fc::tc_plan_grid(p->c); }
 int tc_plan_tile_n(const TcPlan* p) { return fc::tc_plan_tile_n(p->c); }
 int64_t tc_plan_tiles(const TcPlan* p) { return fc::tc_plan_tiles(p->c); }
-int tc_plan_kernel(const TcPlan* p) { return p->which == 3 && fc::tc_plan_pair(p->c) ? 6 : p->which; }
+int tc_plan_kernel(const TcPlan* p) {
+  if (p->which == 3 && fc::tc_plan_pair(p->c)) return 6;
+  if (p->which == 3 && fc::tc_plan_tb(p->c)) return 7;
+  return p->which;
+}
 const void* tc_plan_packed_B(const TcPlan* p, int kind, int64_t* dout_pad, int* rp) {
   return fc::tc_plan_packed_B(p->c, kind, dout_pad, rp);
 }

@@ -83,6 +83,16 @@ struct Geom {
                                         //    the unit's A^T slices) instead of per strip: the plan
                                         //    when a whole strip of 2k raw B slices does not fit
                                         //    (r = 64, k = 4: 128 KB)
+  int32_t tb;                           // fold mode with the (hi, lo) B strip in TMEM (the MMA's M-side
+                                        //    operand read from TMEM): the epilogue warps fold each strip
+                                        //    from a raw shared-memory copy straight into one of b_bufs
+                                        //    TMEM buffers of bcols columns at b_col0; A^T slices staged
+                                        //    in units of unit_terms terms
+  int32_t pf_mode, pf_dist, pf_n;       // W L2 prefetch ahead of the loads (see the W producer)
+  int32_t unit_terms;
+  int32_t unit_commit;                  // tb: each A unit freed by its own MMA commit (default), else
+                                        //    by the epilogue with its tile
+  uint32_t bcols, b_col0, raw_bytes;
 };
 
 // Fused switch + decode: one segment per (layer, GEMV group),
@@ -262,6 +272,13 @@ __device__ __forceinline__ void cur_next(const TileKinds& g, const TileSeq& q, c
   }
 }
 
+// c -> the first tile of the next strip of this CTA's walk (t = -1: none)
+template <bool kF>
+__device__ __forceinline__ void strip_advance(const TileKinds& g, const TileSeq& q, const Args& a, FCursor& c) {
+  const int64_t s = strip_id(c);
+  do cur_next<kF>(g, q, a, c); while (c.t >= 0 && strip_id(c) == s);
+}
+
 __device__ __forceinline__ void wait_count(const unsigned long long* p, unsigned long long target) {
   unsigned long long v;
   const uint64_t t0 = globaltimer();
@@ -316,6 +333,27 @@ __device__ __forceinline__ void fold_range(uint8_t* dst, uint32_t tb, int nt, co
       plo[v] = lo;
     }
   }
+}
+
+// TMEM fold (tb mode): this thread's row of one raw B slice (the pre-swizzled
+// [128, RP] image in shared memory) -> (hi, lo) parts of c * b written to the
+// row's TMEM lane, hi at columns [taddr, taddr + RP/2), lo at the next RP/2
+// (column c of a 16-wide K step = elements 2c, 2c + 1: the MMA's M-side layout).
+template <int RP>
+__device__ __forceinline__ void fold_row_tmem(const uint8_t* slice, int row, float c, uint32_t taddr) {
+  constexpr int kChunks = RP / 8;   // 16-B chunks per row
+  const int f = RP == 16 ? (row >> 2) & 1 : RP == 32 ? (row >> 1) & 3 : row & 7;   // swz_off's phase
+  uint32_t h[RP / 2], l[RP / 2];
+#pragma unroll
+  for (int ch = 0; ch < kChunks; ++ch) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(slice + row * (2 * RP) + ((ch ^ f) << 4));
+    uint4 hi, lo;
+    fold8(raw, c, hi, lo);
+    h[4 * ch] = hi.x; h[4 * ch + 1] = hi.y; h[4 * ch + 2] = hi.z; h[4 * ch + 3] = hi.w;
+    l[4 * ch] = lo.x; l[4 * ch + 1] = lo.y; l[4 * ch + 2] = lo.z; l[4 * ch + 3] = lo.w;
+  }
+  tmem_st<RP / 2>(taddr, h);
+  tmem_st<RP / 2>(taddr + RP / 2, l);
 }
 
 // ------------------------------------------------------------------ epilogue
@@ -443,6 +481,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
   __shared__ __align__(8) uint64_t bar_braw[2], bar_bfull[2], bar_bempty[2];
   __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
   __shared__ __align__(8) uint64_t bar_apeer[kMaxAStages], bar_bpeer[2];   // pair: the follower's stages landed
+  __shared__ __align__(8) uint64_t bar_rawfull, bar_rawempty;                // tb: the raw B strip copy
 
   const Geom& g = args.g;
   const uint32_t crank = kPair ? cta_rank_in_cluster() : 0;
@@ -479,10 +518,13 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&bar_braw[s]), 1);
-      mbar_init(smem_u32(&bar_bfull[s]), g.b_bufs == 1 && !g.pt ? 2 : 1);   // fold: + the MMA warp's half
+      // fold: + the MMA warp's half; tb: every epilogue warp's TMEM stores
+      mbar_init(smem_u32(&bar_bfull[s]), g.tb ? kEpiWarps : g.b_bufs == 1 && !g.pt ? 2 : 1);
       mbar_init(smem_u32(&bar_bempty[s]), 1);
       mbar_init(smem_u32(&bar_bpeer[s]), 1);
     }
+    mbar_init(smem_u32(&bar_rawfull), 1);
+    mbar_init(smem_u32(&bar_rawempty), kEpiWarps);
     for (int s = 0; s < g.acc_bufs; ++s) {
       mbar_init(smem_u32(&bar_accfull[s]), 1);
       mbar_init(smem_u32(&bar_accempty[s]), kPair ? 2 * kEpiWarps : kEpiWarps);   // pair: both CTAs' epilogues
@@ -530,7 +572,31 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         const CUtensorMap* src = args.mode == MODE_RESTORE ? maps.p : maps.w;   // RESTORE reads P
         Ring wring{0, 0, (uint32_t)g.w_stages};
         int nt_tr = 0;
+        // L2 prefetch pf_dist tiles ahead of the loads: of the first pf_n tiles
+        // of every run of consecutive tiles (pf_mode 1: a chunk or segment range
+        // starts in a new region of W, whose first loads otherwise wait ~2x the
+        // usual latency), or of every tile (pf_mode 2)
+        FCursor pc = cur_first<kF>(tk, seq, args);
+        int64_t pc_prev = -2;
+        int pf_left = 0;
+        for (int i = 0; i < g.pf_dist && pc.t >= 0; ++i) {
+          pc_prev = pc.t;
+          cur_next<kF>(tk, seq, args, pc);
+        }
         for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
+          if (g.pf_mode && pc.t >= 0) {
+            if (pc.t != pc_prev + 1) pf_left = g.pf_n;
+            if (g.pf_mode == 2 || pf_left > 0) {
+              if (g.wrm)
+                tma_prefetch_4d(&src[pc.kd], 0, pc.cb * 2, rbr(pc.rb) * kTM, pc.layer);
+              else
+                for (int sb = 0; sb < 2; ++sb)
+                  tma_prefetch_3d(&src[pc.kd], pc.cb * kTN + sb * kSubCols, rbr(pc.rb) * kTM, pc.layer);
+              --pf_left;
+            }
+            pc_prev = pc.t;
+            cur_next<kF>(tk, seq, args, pc);
+          }
           mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
           FC_TRACE(0, nt_tr++);
           const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
@@ -614,6 +680,54 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
                             g.Bp[c.kd] + (((size_t)c.layer * g.n_experts + cf.e[j0 + jj]) * g.dout_pad[c.kd] +
                                           (size_t)c.rb * kTM) * rpe,
                             tb, bar, pol_keep);
+              aring.next();
+            }
+          }
+        }
+      } else if (g.tb) {
+        // tb mode: raw B strips (one or two ahead of the walk, as many as TMEM
+        // buffers) for the epilogue to fold into TMEM, and per tile the A^T
+        // slices in units of unit_terms terms (freed by the epilogue with the tile)
+        if (lane == 0) {
+          const uint64_t pol_keep = policy_evict_last();
+          const size_t rpe = (size_t)g.rp;
+          const uint32_t tb = g.term_bytes;
+          const int U = g.unit_terms;
+          FCursor rc = cur_first<kF>(tk, seq, args);
+          uint32_t raw_phase = 0;
+          auto load_raw = [&]() {                  // the strip at rc, then rc -> the next strip
+            if (rc.t < 0) return;
+            mbar_wait(smem_u32(&bar_rawempty), raw_phase ^ 1);
+            const uint32_t bar = smem_u32(&bar_rawfull);
+            mbar_expect_tx(bar, nt * tb);
+            for (int j = 0; j < nt; ++j)
+              bulk_load(smem_u32(bst0 + j * tb),
+                        g.Bp[rc.kd] + (((size_t)rc.layer * g.n_experts + cf.e[j]) * g.dout_pad[rc.kd] +
+                                       (size_t)rc.rb * kTM) * rpe,
+                        tb, bar, pol_keep);
+            raw_phase ^= 1;
+            strip_advance<kF>(tk, seq, args, rc);
+          };
+          for (int i = 0; i < g.b_bufs; ++i) load_raw();
+          Ring aring{0, 0, (uint32_t)g.a_stages};
+          int64_t strip_prev = -1;
+          int na_tr = 0;
+          for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
+            if (strip_id(c) != strip_prev) {
+              if (strip_prev >= 0) load_raw();
+              strip_prev = strip_id(c);
+            }
+            const __nv_bfloat16* blk =
+                g.At[c.kd] + (((size_t)c.layer * tk.col_tiles[c.kd] + c.cb) * g.n_experts) * (size_t)kTN * rpe;
+            FC_TRACE(1, na_tr++);
+            for (int j0 = 0; j0 < nt; j0 += U) {
+              const int n_in = nt - j0 < U ? nt - j0 : U;
+              mbar_wait(smem_u32(&bar_aempty[aring.i]), aring.phase ^ 1);
+              uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
+              const uint32_t bar = smem_u32(&bar_afull[aring.i]);
+              mbar_expect_tx(bar, n_in * tb);
+              for (int jj = 0; jj < n_in; ++jj)
+                bulk_load(smem_u32(adst + jj * tb), blk + (size_t)cf.e[j0 + jj] * kTN * rpe, tb, bar, pol_keep);
               aring.next();
             }
           }
@@ -706,13 +820,15 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             if constexpr (kPair) {
               if (leader && elect_one()) umma_commit_pair(smem_u32(&bar_bempty[bring.i]));
             } else {
-              if (elect_one()) umma_commit(smem_u32(&bar_bempty[bring.i]));
+              // (tb: the epilogue refolds a TMEM buffer only after the strip's
+              // last accumulator, which completes after its MMAs)
+              if (!g.tb && elect_one()) umma_commit(smem_u32(&bar_bempty[bring.i]));
             }
             __syncwarp();
             bring.next();
           }
           strip_prev = strip_id(c);
-          if (!kPT && g.b_bufs == 1) {
+          if (!kPT && !g.tb && g.b_bufs == 1) {
             // single B buffer: fold the second half of every term here (the
             // operand warp folds the first half), then publish it
             uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
@@ -724,6 +840,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             if (lane == 0) mbar_arrive(smem_u32(&bar_bfull[bring.i]));
           }
           mbar_wait(smem_u32(&bar_bfull[bring.i]), bring.phase);
+          tc_fence_after();                          // tb: the epilogue's TMEM stores -> the MMAs
           if constexpr (kPair) {
             // the leader's MMAs read both strips: the follower reports its own
             if (!leader) {
@@ -766,6 +883,44 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             acc.next();
             aring.next();
           }
+          continue;
+        }
+        if (g.tb) {
+          // tb: the M-side operand (the strip's (hi, lo) parts) read from TMEM;
+          // the A^T slices unit by unit as they land
+          mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
+          tc_fence_after();
+          if (lane == 0) FC_TRACE(2, nm_tr);
+          const uint32_t d = tmem_base + acc.i * kTN;
+          const uint32_t bt = tmem_base + g.b_col0 + bring.i * g.bcols;
+          const int U = g.unit_terms;
+          const uint32_t hrp = (uint32_t)g.rp / 2;
+          for (int j0 = 0; j0 < nt; j0 += U) {
+            const int n_in = nt - j0 < U ? nt - j0 : U;
+            mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
+            tc_fence_after();
+            const uint64_t a_desc = desc0 + (smem_u32(ast0 + (size_t)aring.i * g.a_stage_bytes) >> 4);
+            if (elect_one()) {
+              for (int jj = 0; jj < n_in; ++jj) {
+                const int j = j0 + jj;
+                for (int part = 0; part < 2; ++part)
+                  for (int kk = 0; kk < ksteps; ++kk)
+                    umma_f16_ts(d, bt + (uint32_t)j * g.rp + part * hrp + kk * 8, a_desc + jj * term + kk * 2, idesc,
+                                (j | part | kk) != 0 ? 1u : 0u);
+              }
+              if (g.unit_commit) umma_commit(smem_u32(&bar_aempty[aring.i]));
+            }
+            __syncwarp();
+            aring.next();
+          }
+          // each unit freed by its own commit (unit_commit, the default), or,
+          // with option fc_unit_commit = 0 where the ring holds two tiles'
+          // units, by the epilogue with its tile (one commit per tile)
+          if (elect_one()) umma_commit(smem_u32(&bar_accfull[acc.i]));
+          if (lane == 0) FC_TRACE(3, nm_tr);
+          ++nm_tr;
+          __syncwarp();
+          acc.next();
           continue;
         }
         mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
@@ -825,8 +980,47 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         y_at = -1;
         y_run = 0.f;
       };
+      // tb: the strips are folded into TMEM here, in walk order, as many ahead as
+      // there are TMEM buffers (buffer f % b_bufs for the f-th fold): the first
+      // b_bufs at the start, then at the start of strip s the strip s + b_bufs - 1
+      // -- its buffer last held strip s - 1, whose accumulators are all consumed.
+      // (Measured: folding the next strip as soon as its raw copy lands,
+      // tried at every tile, is slower.)
+      const bool tbm = g.tb && nt > 0 && !(args.probe & 1);
+      FCursor rc = cur_first<kF>(tk, seq, args);
+      int64_t ep_strip = -1;
+      uint32_t nf = 0;
+      auto fold_next = [&]() {
+        if (rc.t < 0) return;
+        const uint32_t buf = nf % (uint32_t)g.b_bufs;
+        mbar_wait(smem_u32(&bar_rawfull), nf & 1);
+        const uint32_t bt = tmem_base + ((uint32_t)(quarter * 32) << 16) + g.b_col0 + buf * g.bcols;
+        for (int j = half; j < nt; j += 2) {
+          const uint8_t* slice = bst0 + (size_t)j * g.term_bytes;
+          const uint32_t ta = bt + (uint32_t)j * g.rp;
+          if (g.rp == 16) fold_row_tmem<16>(slice, row, cf.c[j], ta);
+          else if (g.rp == 32) fold_row_tmem<32>(slice, row, cf.c[j], ta);
+          else fold_row_tmem<64>(slice, row, cf.c[j], ta);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(smem_u32(&bar_bfull[buf]));
+          mbar_arrive(smem_u32(&bar_rawempty));
+        }
+        ++nf;
+        strip_advance<kF>(tk, seq, args, rc);
+      };
       for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
         uint4 xv[8];                               // fused: x of this thread's 64 columns
+        if (tbm && strip_id(c) != ep_strip) {
+          if (ep_strip < 0)
+            for (int i = 0; i < g.b_bufs; ++i) fold_next();
+          else
+            fold_next();
+          ep_strip = strip_id(c);
+        }
         if constexpr (kF) {
           if (c.seg != cur_seg) {
             y_flush();                             // before the segment's count is published
@@ -923,8 +1117,16 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);      // the tile's MMAs are complete
           if (releaser) FC_TRACE(4, ne_tr);
           // (pair: the leader's commit released both CTAs' A stages)
-          if (releaser && !kPair) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
-          aring.next();
+          if (g.tb) {                              // tb: the tile's A units (unless the MMA's commits free them)
+            for (int u = 0; u < nt; u += g.unit_terms) {
+              if (g.unit_commit) { aring.next(); continue; }
+              if (releaser) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
+              aring.next();
+            }
+          } else {
+            if (releaser && !kPair) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
+            aring.next();
+          }
           tc_fence_after();
           const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTN + half * kSubCols;
 #pragma unroll
@@ -1166,7 +1368,46 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     }
     return false;
   };
-  bool ok = make_plan(g.a_stage_bytes);
+  // tb (fold mode with k >= 3, or option tc_tb = 1): the (hi, lo) B strip in TMEM --
+  // b_bufs buffers of mt * rp columns next to >= 2 accumulators -- so shared
+  // memory holds only the W stages, ONE raw B strip and the A^T units; the
+  // strip change costs no MMA drain (measured: DESIGN.md §5)
+  bool ok = false;
+  if (!g.pt && opt_int("tc_tb", 0) == 1) {
+    const int bcols = mt * rp;                 // (hi, lo) of a term: rp 32-bit columns
+    int bb = 0, accb = 0;
+    if (512 - 2 * bcols >= 2 * kTN && opt_int("tc_tb_bbufs", 2) != 1) { bb = 2; accb = (512 - 2 * bcols) / kTN; }
+    else if (512 - bcols >= 2 * kTN) { bb = 1; accb = (512 - bcols) / kTN; }
+    if (accb > kAccBufs) accb = kAccBufs;
+    int U = (int)(16384 / g.term_bytes);
+    if (U < 1) U = 1;
+    if (U > mt) U = mt;
+    const uint32_t unit = align1k((uint32_t)U * g.term_bytes), raw = align1k((uint32_t)mt * g.term_bytes);
+    const int64_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
+    const int ws = ws_opt >= 2 && ws_opt <= kMaxStages ? ws_opt : 3;
+    const int64_t rest = budget - (int64_t)ws * w_stage - raw;
+    int as = rest > 0 ? (int)(rest / unit) : 0;
+    if (as > kMaxAStages) as = kMaxAStages;
+    if (as_opt >= 2 && as_opt <= as) as = as_opt;
+    if (bb > 0 && as >= 2) {
+      g.tb = 1;
+      g.b_bufs = bb;
+      g.acc_bufs = accb;
+      g.acc_cols = kTN;
+      g.w_stages = ws;
+      g.a_stages = as;
+      g.unit_terms = U;
+      g.a_stage_bytes = unit;
+      g.bcols = (uint32_t)bcols;
+      g.b_col0 = (uint32_t)accb * kTN;
+      g.raw_bytes = raw;
+      // measured (7B, r = 16 k = 3 / 4): releasing a tile's units from the
+      // epilogue (one commit per tile) is 5-10 % slower than a commit per unit
+      g.unit_commit = opt_int("fc_unit_commit", 1) != 0 || as < 2 * ((mt + U - 1) / U);
+      ok = true;
+    }
+  }
+  if (!ok) ok = make_plan(g.a_stage_bytes);
   // CTA pairs (fold mode, variant option tc_pair = 1; off by default): each
   // CTA stages half of a tile's A^T columns (the same shared memory holds twice
   // the A lookahead) and the leader issues the pair's M = 256 MMAs.  Measured
@@ -1177,7 +1418,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   // by the pair's lockstep.
   {
     const long pair_opt = opt_int("tc_pair", 0);
-    const bool want = !g.pt && pair_opt == 1 && num_sms >= 2 && opt_int("tc_grid", 0) != 1;
+    const bool want = !g.pt && !g.tb && pair_opt == 1 && num_sms >= 2 && opt_int("tc_grid", 0) != 1;
     if (want) {
       const uint32_t half = align1k((uint32_t)mt * g.term_bytes / 2);
       const Geom keep = g;
@@ -1210,8 +1451,14 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
   // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
   g.wrm = opt_int("fc_wrm", 1) != 0;
+  g.pf_mode = (int)opt_int("fc_pf", 0);   // measured: no gain (mode 1), slower (mode 2), DESIGN.md §5
+  g.pf_dist = (int)opt_int("fc_pf_dist", 6);
+  g.pf_n = (int)opt_int("fc_pf_n", 3);
+  if (g.pf_mode < 0 || g.pf_mode > 2) g.pf_mode = 0;
+  if (g.pf_dist < 1) g.pf_dist = 1;
   for (int k = 0; k < LSW_NKIND; ++k) if (sp.kind[k].d_in % 64) g.wrm = 0;   // ragged TP shards: 3-D boxes
-  g.smem_bytes = g.w_stages * w_stage + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
+  g.smem_bytes = g.w_stages * w_stage + g.a_stages * g.a_stage_bytes + (g.tb ? g.raw_bytes : g.b_bufs * g.b_buf_bytes) +
+                 1024;
   // tiles
   int64_t t = 0;
   for (int k = 0; k < LSW_NKIND; ++k) {
@@ -1311,6 +1558,7 @@ int64_t tc_plan_bytes(const TcPlan* plan) { return plan ? plan->bytes : 0; }
 int tc_plan_grid(const TcPlan* plan) { return plan ? (plan->geom.pair ? plan->pair_grid : plan->grid) : 0; }
 int tc_plan_tile_n(const TcPlan* plan) { return plan ? kTN : 0; }
 int tc_plan_pair(const TcPlan* plan) { return plan ? plan->geom.pair : 0; }
+int tc_plan_tb(const TcPlan* plan) { return plan ? plan->geom.tb : 0; }
 int64_t tc_plan_tiles(const TcPlan* plan) { return plan ? plan->geom.tiles_total : 0; }
 const void* tc_plan_packed_B(const TcPlan* plan, int kind, int64_t* dout_pad, int* rp) {
   *dout_pad = plan->geom.dout_pad[kind];

@@ -2,7 +2,8 @@
 // (switch_tc_dispatch.cu picks its mode per ctx at create time).  fc
 // (switch_tc_fc.cu): the coefficients folded into the B factors as exact
 // (hi, lo) bf16 pairs, ONE accumulator and one commit per 128 x 128 tile
-// (Eq. 5's concatenation, K = 2 * sum_j rp; 7B: 0.89 of the copy peak); its
+// (Eq. 5's concatenation, K = 2 * sum_j rp), the folded strip held in TMEM
+// as the MMA's M-side operand where it fits (2k * rp <= 256); its
 // per-term mode (raw B, one accumulator per term, N = 128) for r = 64 and r =
 // 32 with k >= 3, with the B slices staged per unit where a whole strip does
 // not fit (r = 64, k = 4).
@@ -32,6 +33,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
                                    float* ys);
 const void* tc_plan_packed_B(const TcPlan* plan, int kind, int64_t* dout_pad, int* rp);
 int tc_plan_pair(const TcPlan* plan);   // 1: the plain switch runs on CTA pairs
+int tc_plan_tb(const TcPlan* plan);     // 1: the fold with its (hi, lo) B strip in TMEM
 }  // namespace fc
 
 }  // namespace lsw

@@ -1,7 +1,8 @@
 """A/B of the decode paths of two liblsw builds on one box (7B): per token,
 the merged-weight GEMVs (lsw_decode_all_layers) and the unmerged decode
 (router + lsw_decode_all_layers_unmerged).  Usage:
-python scripts/decode_ab.py [--lib path] config"""
+python scripts/decode_ab.py [--lib path] config [option=value ...] (variant
+options, include/lsw_debug.h, for the ctx)"""
 import os
 import sys
 
@@ -34,8 +35,12 @@ def main():
         label = os.path.basename(sys.argv[2])
         del sys.argv[1:3]
     cfg = synth.get_config(sys.argv[1])
+    opts = dict(kv.split("=") for kv in sys.argv[2:])
+    if opts:
+        label += " " + ",".join(sys.argv[2:])
     W, A, B, router = H.build_weights(cfg, "cuda")
-    sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+    with binding.options(**opts):
+        sw = H.make_switch(cfg, W, A, B, router, impl="tc")
     xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
     ys = torch.empty(sw.info()["ys_elems"], device="cuda")
     X1 = synth.gen_x1(cfg, 2, "cuda")

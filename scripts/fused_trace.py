@@ -81,6 +81,9 @@ def main():
         sw.merge_all_layers(idx, gate)
         torch.cuda.synchronize()
     res["sweep_switch"] = analyse(tr.cpu().numpy())
+    if os.environ.get("TRACE_SAVE"):                     # raw stamps for offline analysis
+        import numpy as np
+        np.save(os.environ["TRACE_SAVE"], tr.cpu().numpy())
     if sw.info()["switch_kernel"] == 3:
         for t in range(3, 6):
             tr.zero_()

@@ -117,8 +117,12 @@ def test_switch_trajectory_full_elements(name, impl):
 # (mode of the fc kernel, extra variant options); KERNEL_ID = lsw_info.switch_kernel
 TC_VARIANTS = [("fold", {}), ("fold", {"fc_stages": 3, "fc_astages": 2, "fc_bbufs": 1}), ("fold", {"fc_wrm": 0}),
                ("pt", {}), ("pt", {"fc_wrm": 0}), ("bu", {}), ("bu", {"fc_wrm": 0}),
-               ("fold", {"tc_pair": 1}), ("fold", {"tc_pair": 1, "fc_wrm": 0}), ("fold", {"tc_pair": 0})]
-KERNEL_ID = {"fold": (3, 6), "pt": (4,), "bu": (5,)}
+               ("fold", {"tc_pair": 1, "tc_tb": 0}), ("fold", {"tc_pair": 1, "fc_wrm": 0, "tc_tb": 0}),
+               ("fold", {"tc_pair": 0}), ("fold", {"tc_tb": 0}), ("fold", {"tc_tb": 1}),
+               ("fold", {"tc_tb": 1, "fc_wrm": 0}), ("fold", {"tc_tb": 1, "fc_astages": 2}),
+               ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1}), ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1, "fc_astages": 2}),
+               ("fold", {"fc_pf": 1}), ("fold", {"fc_pf": 2, "fc_pf_dist": 2})]
+KERNEL_ID = {"fold": (3, 6, 7), "pt": (4,), "bu": (5,)}
 
 
 @pytest.mark.parametrize("grid", [1, 2, 3])
@@ -144,8 +148,12 @@ def test_tc_switch_many_tiles_per_cta(lsw_opts, name, variant, grid):
     assert info["switch_kernel"] in KERNEL_ID[mode]
     if opts.get("tc_pair") == 1 and grid >= 2:
         assert info["switch_kernel"] == 6
-    if opts.get("tc_pair") == 0:
+    if opts.get("tc_tb") == 0 and opts.get("tc_pair") != 1:
         assert info["switch_kernel"] == 3
+    if opts.get("tc_tb") == 1:
+        assert info["switch_kernel"] in (3, 7)       # 3 where the TMEM strip does not fit
+        if S.cfg.rank <= 32 and S.cfg.top_k * (16 if S.cfg.rank <= 16 else 32) <= 128:
+            assert info["switch_kernel"] == 7
     # CTA pairs run an even grid (grid 1: no pair)
     assert info["grid"] == (grid // 2 * 2 if info["switch_kernel"] == 6 else grid)
     worst = _run_token_checks(S, 5)
