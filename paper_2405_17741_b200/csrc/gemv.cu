@@ -596,9 +596,26 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, const GemvTune& t, c
     // x staged in shared memory as raw bf16 / fp32
     const uint32_t row_bytes = (uint32_t)(p.d_in * (bf16 ? 2 : 4));
     const uint32_t x_bytes = x_stage_bytes(row_bytes, false);
-    int R = (int)(t.op_bytes / row_bytes);
-    if (R < 1) R = 1;
-    if (R > 16) R = 16;
+    const size_t budget = lora ? t.budget_lora : t.budget;
+    // rows per op: of the R with op_min <= R * row_bytes <= op_bytes (R = 1
+    // when one row is already larger), the one that puts the most bytes in
+    // flight (slots * R * row_bytes), ties to the smaller op.  Measured (r02,
+    // 7B, groups of every layer back to back): 8 KB rows R = 3 (24 KB ops,
+    // 7 slots) vs R = 4 (32 KB, 5 slots): q|k|v 6.14 vs 5.81 TB/s, o 4.40 vs
+    // 3.07, gate|up 6.68 vs 6.34; 16 KB ops (R = 2) 4.7-5.0 -- token 2.12-2.14
+    // vs 2.19 ms; 13B (10 KB rows) keeps R = 3 (R = 2, 20 KB ops: 4.40 vs 4.27)
+    int R = 1;
+    {
+      size_t best = 0;
+      for (int r = 1; r <= 16; ++r) {
+        const size_t op = (size_t)r * row_bytes;
+        if (op > t.op_bytes && r > 1) break;
+        if (op < t.op_min && (size_t)(r + 1) * row_bytes <= t.op_bytes) continue;
+        const size_t sl = budget > x_bytes ? (budget - x_bytes) / op : 0;
+        const size_t fly = (sl > (size_t)kBulkMaxSlots ? (size_t)kBulkMaxSlots : sl) * op;
+        if (sl >= 2 && fly > best) { best = fly; R = r; }
+      }
+    }
     const size_t slot_bytes = (size_t)R * row_bytes;
     // Ring budget.  Measured (7B token of GEMVs): 220 KB 2.37 ms, 110 KB 2.59 ms,
     // 72 KB 3.49 ms -- a deep ring per SM beats letting the next GEMV's CTA
@@ -609,7 +626,6 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, const GemvTune& t, c
     // one's last CTA on the SM ends; r02, same box): 104 KB 2.42, 110 KB 2.36,
     // 80 KB 2.60 ms vs 2.19 for one CTA with 176 KB -- dropped.
     // (the unmerged form keeps ~12 KB of static shared memory: u, row sums, terms)
-    const size_t budget = lora ? t.budget_lora : t.budget;
     int slots = budget > x_bytes ? (int)((budget - x_bytes) / slot_bytes) : 0;
     if (slots > kBulkMaxSlots) slots = kBulkMaxSlots;
     if (slots >= 2) {

@@ -239,7 +239,7 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device);
   ctx->gemv.grid_cap = ctx->num_sms;
   { const long x = opt_int("gemv_grid", 0); if (x >= 1 && x < ctx->gemv.grid_cap) ctx->gemv.grid_cap = (int)x; }
-  { const long x = opt_int("gemv_op_kb", 0); if (x >= 4 && x <= 96) ctx->gemv.op_bytes = (uint32_t)x * 1024; }
+  { const long x = opt_int("gemv_op_kb", 0); if (x >= 4 && x <= 96) ctx->gemv.op_bytes = ctx->gemv.op_min = (uint32_t)x * 1024; }
   { const long x = opt_int("gemv_smem_kb", 0); if (x >= 32 && x <= 224) ctx->gemv.budget = ctx->gemv.budget_lora = (size_t)x * 1024; }
   { const char* v = opt_str("gemv"); ctx->gemv.ldg = v && strcmp(v, "ldg") == 0; }
   ctx->gemv.probe = (int)probe_int("gemv_probe");

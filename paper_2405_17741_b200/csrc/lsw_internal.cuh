@@ -193,7 +193,8 @@ struct GemvLora {
 // Launch plan of the decode GEMV (gemv.cu), fixed per ctx at lsw_create.
 struct GemvTune {
   int grid_cap = 148;               // CTAs at most (the SM count)
-  uint32_t op_bytes = 32768;        // bytes per bulk copy (R rows of ~32 KB)
+  uint32_t op_bytes = 32768;        // bytes per bulk copy at most (R rows per op, see launch_gemv)
+  uint32_t op_min = 24576;          // ... and at least, unless one row is larger
   size_t budget = 176 * 1024;       // ring + x staging, merged-weight GEMV
   size_t budget_lora = 208 * 1024;  // same, unmerged form
   int probe = 0;                    // tuning builds only: 1 = stream W without the dot products
