@@ -661,7 +661,7 @@ lsw_status lsw_decode_token_fused(lsw_ctx* ctx, const void* x1, const void* xs, 
     cudaError_t e = tc_plan_set_fused(ctx->tc, ctx->cfg.n_layers, ctx->x_off, ctx->y_off, ctx->x_per_layer,
                                       ctx->y_per_layer, kGroupKinds, nk);
     if (e == cudaErrorNotSupported)
-      return fail(LSW_E_UNSUPPORTED, "lsw_decode_token_fused: the fused decode is built on the fold mode, and this ctx switches with a per-term mode (rank / top-k)");
+      return fail(LSW_E_UNSUPPORTED, "lsw_decode_token_fused: the fused decode is built on the shared-memory fold (switch_kernel 3), and this ctx switches with another mode (per-term for its rank / top-k, or the TMEM strip option)");
     if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_fused: segment table");
     ctx->fused_ready = true;
   }

@@ -88,7 +88,6 @@ struct Geom {
                                         //    from a raw shared-memory copy straight into one of b_bufs
                                         //    TMEM buffers of bcols columns at b_col0; A^T slices staged
                                         //    in units of unit_terms terms
-  int32_t pf_mode, pf_dist, pf_n;       // W L2 prefetch ahead of the loads (see the W producer)
   int32_t unit_terms;
   int32_t unit_commit;                  // tb: each A unit freed by its own MMA commit (default), else
                                         //    by the epilogue with its tile
@@ -468,10 +467,11 @@ __device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
 
 // ------------------------------------------------------------------ the kernel
 
-template <bool kF, bool kPT, bool kPair = false>
+template <bool kF, bool kPT, bool kPair = false, bool kTB = false>
 __global__ void __launch_bounds__(kThreads, 1)
 switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args args) {
   static_assert(!kPair || (!kF && !kPT), "CTA pairs: the plain fold mode only");
+  static_assert(!kTB || (!kF && !kPT && !kPair), "TMEM strip: the plain fold mode only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ Coefs cf;
   __shared__ int32_t s_parity;
@@ -519,7 +519,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&bar_braw[s]), 1);
       // fold: + the MMA warp's half; tb: every epilogue warp's TMEM stores
-      mbar_init(smem_u32(&bar_bfull[s]), g.tb ? kEpiWarps : g.b_bufs == 1 && !g.pt ? 2 : 1);
+      mbar_init(smem_u32(&bar_bfull[s]), kTB ? kEpiWarps : g.b_bufs == 1 && !g.pt ? 2 : 1);
       mbar_init(smem_u32(&bar_bempty[s]), 1);
       mbar_init(smem_u32(&bar_bpeer[s]), 1);
     }
@@ -572,31 +572,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
         const CUtensorMap* src = args.mode == MODE_RESTORE ? maps.p : maps.w;   // RESTORE reads P
         Ring wring{0, 0, (uint32_t)g.w_stages};
         int nt_tr = 0;
-        // L2 prefetch pf_dist tiles ahead of the loads: of the first pf_n tiles
-        // of every run of consecutive tiles (pf_mode 1: a chunk or segment range
-        // starts in a new region of W, whose first loads otherwise wait ~2x the
-        // usual latency), or of every tile (pf_mode 2)
-        FCursor pc = cur_first<kF>(tk, seq, args);
-        int64_t pc_prev = -2;
-        int pf_left = 0;
-        for (int i = 0; i < g.pf_dist && pc.t >= 0; ++i) {
-          pc_prev = pc.t;
-          cur_next<kF>(tk, seq, args, pc);
-        }
         for (FCursor c = cur_first<kF>(tk, seq, args); c.t >= 0; cur_next<kF>(tk, seq, args, c)) {
-          if (g.pf_mode && pc.t >= 0) {
-            if (pc.t != pc_prev + 1) pf_left = g.pf_n;
-            if (g.pf_mode == 2 || pf_left > 0) {
-              if (g.wrm)
-                tma_prefetch_4d(&src[pc.kd], 0, pc.cb * 2, rbr(pc.rb) * kTM, pc.layer);
-              else
-                for (int sb = 0; sb < 2; ++sb)
-                  tma_prefetch_3d(&src[pc.kd], pc.cb * kTN + sb * kSubCols, rbr(pc.rb) * kTM, pc.layer);
-              --pf_left;
-            }
-            pc_prev = pc.t;
-            cur_next<kF>(tk, seq, args, pc);
-          }
           mbar_wait(smem_u32(&bar_wempty[wring.i]), wring.phase ^ 1);
           FC_TRACE(0, nt_tr++);
           const uint32_t wbar = smem_u32(&bar_wfull[wring.i]);
@@ -684,7 +660,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             }
           }
         }
-      } else if (g.tb) {
+      } else if (kTB) {
         // tb mode: raw B strips (one or two ahead of the walk, as many as TMEM
         // buffers) for the epilogue to fold into TMEM, and per tile the A^T
         // slices in units of unit_terms terms (freed by the epilogue with the tile)
@@ -822,13 +798,13 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             } else {
               // (tb: the epilogue refolds a TMEM buffer only after the strip's
               // last accumulator, which completes after its MMAs)
-              if (!g.tb && elect_one()) umma_commit(smem_u32(&bar_bempty[bring.i]));
+              if (!kTB && elect_one()) umma_commit(smem_u32(&bar_bempty[bring.i]));
             }
             __syncwarp();
             bring.next();
           }
           strip_prev = strip_id(c);
-          if (!kPT && !g.tb && g.b_bufs == 1) {
+          if (!kPT && !kTB && g.b_bufs == 1) {
             // single B buffer: fold the second half of every term here (the
             // operand warp folds the first half), then publish it
             uint8_t* dst = bst0 + (size_t)bring.i * g.b_buf_bytes;
@@ -885,7 +861,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           }
           continue;
         }
-        if (g.tb) {
+        if constexpr (kTB) {
           // tb: the M-side operand (the strip's (hi, lo) parts) read from TMEM;
           // the A^T slices unit by unit as they land
           mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
@@ -986,7 +962,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       // -- its buffer last held strip s - 1, whose accumulators are all consumed.
       // (Measured: folding the next strip as soon as its raw copy lands,
       // tried at every tile, is slower.)
-      const bool tbm = g.tb && nt > 0 && !(args.probe & 1);
+      const bool tbm = kTB && nt > 0 && !(args.probe & 1);
       FCursor rc = cur_first<kF>(tk, seq, args);
       int64_t ep_strip = -1;
       uint32_t nf = 0;
@@ -1117,7 +1093,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);      // the tile's MMAs are complete
           if (releaser) FC_TRACE(4, ne_tr);
           // (pair: the leader's commit released both CTAs' A stages)
-          if (g.tb) {                              // tb: the tile's A units (unless the MMA's commits free them)
+          if constexpr (kTB) {                     // tb: the tile's A units (unless the MMA's commits free them)
             for (int u = 0; u < nt; u += g.unit_terms) {
               if (g.unit_commit) { aring.next(); continue; }
               if (releaser) mbar_arrive(smem_u32(&bar_aempty[aring.i]));
@@ -1451,11 +1427,6 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
   // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
   g.wrm = opt_int("fc_wrm", 1) != 0;
-  g.pf_mode = (int)opt_int("fc_pf", 0);   // measured: no gain (mode 1), slower (mode 2), DESIGN.md §5
-  g.pf_dist = (int)opt_int("fc_pf_dist", 6);
-  g.pf_n = (int)opt_int("fc_pf_n", 3);
-  if (g.pf_mode < 0 || g.pf_mode > 2) g.pf_mode = 0;
-  if (g.pf_dist < 1) g.pf_dist = 1;
   for (int k = 0; k < LSW_NKIND; ++k) if (sp.kind[k].d_in % 64) g.wrm = 0;   // ragged TP shards: 3-D boxes
   g.smem_bytes = g.w_stages * w_stage + g.a_stages * g.a_stage_bytes + (g.tb ? g.raw_bytes : g.b_bufs * g.b_buf_bytes) +
                  1024;
@@ -1533,6 +1504,9 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   if (e == cudaSuccess && g.pair)
     e = cudaFuncSetAttribute(switch_fc_kernel<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)g.smem_bytes);
+  if (e == cudaSuccess && g.tb)
+    e = cudaFuncSetAttribute(switch_fc_kernel<false, false, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem_bytes);
   if (e != cudaSuccess) {
     if (!*why || !**why) *why = cudaGetErrorString(e);
     tc_plan_destroy(plan);
@@ -1606,6 +1580,8 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   a.seg_trace = plan->seg_trace;
   if (plan->geom.pt) {
     switch_fc_kernel<false, true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  } else if (plan->geom.tb) {
+    switch_fc_kernel<false, false, false, true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   } else if (plan->geom.pair && t_count == 0) {
     // CTA pairs (the per-matrix ablation keeps single CTAs: its tile ranges are single-CTA tiles)
     cudaLaunchConfig_t lc{};
@@ -1632,7 +1608,7 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
 cudaError_t tc_plan_set_fused(TcPlan* plan, int n_layers, const int64_t x_off[4], const int64_t y_off[4],
                               int64_t x_per_layer, int64_t y_per_layer, const int kinds[4][3], const int nk[4]) {
   const Geom& g = plan->geom;
-  if (g.pt) return cudaErrorNotSupported;                     // the fused epilogue is the folded one
+  if (g.pt || g.tb) return cudaErrorNotSupported;            // the fused epilogue is the shared-memory fold's
   for (int k = 0; k < LSW_NKIND; ++k) if (g.d_in[k] % 8) return cudaErrorNotSupported;   // 16-B x loads
   const int n = 4 * n_layers;
   FusedSeg* h = new FusedSeg[n];

@@ -31,10 +31,11 @@ def _f64(t):
 
 @pytest.mark.parametrize("name,grid,tb", [("mini", None, None), ("mini", "3", None), ("mini", "1", None),
                                           ("mini-r32", None, None), ("mini-k1", "5", None), ("mini-r4k4", "2", None),
-                                          ("mini", "3", 1), ("mini-r32", "2", 1), ("mini-r4k4", "2", 0)])
+                                          ("mini-r4k4", "2", 0)])
 def test_fused_token_equals_separate_path(lsw_opts, name, grid, tb):
-    """tb: the fold's B strip in TMEM (mode 7, the default for k >= 3) forced
-    on / off."""
+    """tb = 0: the shared-memory fold explicitly (the fused decode is built on
+    it; a ctx whose switch holds its strip in TMEM, option tc_tb = 1, refuses
+    the fused decode: test_fused_refuses_tmem_strip_ctx)."""
     lsw_opts(tc_kernel="fold", tc_grid=grid, tc_tb=tb)
     cfg = synth.get_config(name)
     ctxs = []
@@ -196,3 +197,23 @@ def test_fused_repeated_decision_still_computes_outputs(lsw_opts, grid):
     for kd in synth.KINDS:
         assert torch.equal(W[kd], snap[kd])
     assert torch.equal(ya, yb)
+
+
+def test_fused_refuses_tmem_strip_ctx(lsw_opts):
+    """The fused decode runs the shared-memory fold's epilogue: a ctx created
+    with the TMEM-strip switch (option tc_tb = 1, mode 7) refuses it with
+    LSW_E_UNSUPPORTED before enqueuing anything."""
+    from paper_2405_17741_b200 import binding as L
+    lsw_opts(tc_tb=1)
+    cfg = synth.get_config("mini")
+    W, A, B, router = H.build_weights(cfg, "cuda")
+    sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+    assert sw.info()["switch_kernel"] == 7
+    X1 = synth.gen_x1(cfg, 1, "cuda")
+    xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))
+    ys = torch.empty(sw.info()["ys_elems"], device="cuda")
+    idx = torch.empty(cfg.top_k, dtype=torch.int32, device="cuda")
+    gate = torch.empty(cfg.top_k, dtype=torch.float32, device="cuda")
+    with pytest.raises(L.LswError, match="UNSUPPORTED"):
+        sw.decode_token_fused(X1[0], xs, ys, idx, gate)
+    assert sw.device_status() == 0

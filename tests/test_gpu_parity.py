@@ -120,8 +120,7 @@ TC_VARIANTS = [("fold", {}), ("fold", {"fc_stages": 3, "fc_astages": 2, "fc_bbuf
                ("fold", {"tc_pair": 1, "tc_tb": 0}), ("fold", {"tc_pair": 1, "fc_wrm": 0, "tc_tb": 0}),
                ("fold", {"tc_pair": 0}), ("fold", {"tc_tb": 0}), ("fold", {"tc_tb": 1}),
                ("fold", {"tc_tb": 1, "fc_wrm": 0}), ("fold", {"tc_tb": 1, "fc_astages": 2}),
-               ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1}), ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1, "fc_astages": 2}),
-               ("fold", {"fc_pf": 1}), ("fold", {"fc_pf": 2, "fc_pf_dist": 2})]
+               ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1}), ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1, "fc_astages": 2})]
 KERNEL_ID = {"fold": (3, 6, 7), "pt": (4,), "bu": (5,)}
 
 
