@@ -102,6 +102,20 @@ __device__ __forceinline__ float lora_up_row(const GemvParams& p, const GemvLora
   return e;
 }
 
+// L1 prefetch of the B rows lora_up_row will read for this row
+template <bool kBf16>
+__device__ __forceinline__ void lora_up_prefetch(const GemvParams& p, const GemvLora& L, int64_t row) {
+  const int q = site_of(p, row);
+  const int64_t rl = row - sel3(q, p.site[0].row_begin, p.site[1].row_begin, p.site[2].row_begin);
+  const int64_t dq = sel3(q, p.site[0].d_out, p.site[1].d_out, p.site[2].d_out);
+  const uint8_t* Bq = reinterpret_cast<const uint8_t*>(sel3(q, L.B[0], L.B[1], L.B[2]));
+  const int64_t rbytes = (int64_t)L.r * (kBf16 ? 2 : 4);
+  for (int j = 0; j < L.k; ++j) {
+    const uint8_t* a = Bq + ((int64_t)L.idx[j] * dq + rl) * rbytes;
+    for (int64_t o = 0; o < rbytes; o += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(a + o));
+  }
+}
+
 // Both operands in registers (16 B each: 8 bf16 or 4 fp32), fp32 sum in order.
 template <bool kBf16>
 __device__ __forceinline__ float dot_chunk_vv(const uint4 a, const uint4 x) {
@@ -493,6 +507,13 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
       __syncwarp();
       asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");   // part[] reusable
     }
+    // the LoRA-up operands of this CTA's rows (B rows of the selected
+    // experts) requested into L1 while the other CTAs' products arrive
+    if (n_local <= kMaxLocal && lora_ok)
+      for (int64_t t = threadIdx.x - 32 * (1 + kBulkConsumers); t < n_local; t += 32 * kLoraWarps) {
+        const int64_t row = (blockIdx.x + (t / R) * G) * R + t % R;
+        if (row < p.rows_total) lora_up_prefetch<kBf16>(p, L, row);
+      }
     if (dw == 0 && lane == 0) {
       uint32_t v;
       const uint64_t t0 = g_globaltimer();
@@ -508,6 +529,20 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     for (int d = threadIdx.x - 32 * (1 + kBulkConsumers); d < n_dots; d += 32 * kLoraWarps) us[d] = __ldcg(L.u + d);
     __syncwarp();
     asm volatile("bar.sync 2, %0;" ::"r"(32 * kLoraWarps) : "memory");
+    // every CTA's products read: this CTA is done with the counters; the last
+    // one resets both for the next launch (which publishes its products only
+    // after this grid has completed: griddepcontrol.wait).  Here, not at the
+    // CTA's end: the atomic's round trip stays off the path to the CTA's exit
+    // (the next launch's CTA on this SM starts only then).
+    if (dw == 0 && lane == 0) {
+      uint32_t prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(L.depart) : "memory");
+      if (prev == gridDim.x - 1) {
+        *reinterpret_cast<volatile uint32_t*>(L.arrive) = 0;
+        *reinterpret_cast<volatile uint32_t*>(L.depart) = 0;
+        __threadfence();
+      }
+    }
     // LoRA-up terms of this CTA's rows, one lane per row, while the consumers
     // still stream (their row sums wait in acc_s; joined at the end)
     if (n_local <= kMaxLocal && !(L.flags & 4) && lora_ok)
@@ -568,19 +603,6 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
       for (int64_t t = threadIdx.x - 32; t < n_local; t += 32 * kBulkConsumers) {
         const int64_t row = (blockIdx.x + (t / R) * G) * R + t % R;
         if (row < p.rows_total) p.y[row] = p.y[row] + lora_up_row<kBf16>(p, L, us, row, kr);
-      }
-    }
-    // the last CTA to leave resets both counters for the next launch (which
-    // publishes its dots only after this grid has completed: griddepcontrol.wait)
-    __syncwarp();
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
-    if (cw == 0 && lane == 0) {
-      uint32_t prev;
-      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(L.depart) : "memory");
-      if (prev == gridDim.x - 1) {
-        *reinterpret_cast<volatile uint32_t*>(L.arrive) = 0;
-        *reinterpret_cast<volatile uint32_t*>(L.depart) = 0;
-        __threadfence();
       }
     }
   }
@@ -651,7 +673,8 @@ cudaError_t launch_gemv(const GemvParams& p, int32_t dtype, const GemvTune& t, c
       lc.attrs = at;
       lc.numAttrs = 1;
       const GemvLora none{};
-      return cudaLaunchKernelEx(&lc, fn, p, slots, R, (int32_t)((early_w || lora ? 1 : 0) | (t.probe ? 2 : 0)),
+      return cudaLaunchKernelEx(&lc, fn, p, slots, R,
+                                (int32_t)((early_w || lora ? 1 : 0) | (t.probe ? 2 : 0)),
                                 lora ? *lora : none);
     }
   }
