@@ -43,6 +43,7 @@ constexpr int kEpiWarps = 4;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr int kMaxStages = 8;
 constexpr int kAccBufs = 2;
+constexpr int kMaxSplits = 16;  // LoRA-down K splits at most
 constexpr int MODE_Y = 0, MODE_U = 1;
 
 struct Maps {
@@ -216,6 +217,10 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
       const uint64_t pol_x = policy_evict_last();      // X, B, Z: reused by many tiles
       Ring ring{0, 0, (uint32_t)a.stages};
       bool z_ready = false;
+      // MODE_U is a programmatic dependent of the previous group's dense
+      // launch: its setup (barriers, TMEM, tensor maps) ran already; X (and U,
+      // read by the previous Z build) only after that grid has completed
+      if (a.mode == MODE_U) asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int it = it0; it < n_it; it += istep) {
         const TileAt ta = tile_for<kC>(a, it, crank);
         for (int kb = ta.kb0; kb < ta.kb1; ++kb) {
@@ -384,8 +389,13 @@ __global__ void prefill_zbuild(const float* __restrict__ U, int splits, int64_t 
         if (idx[t * k + j] == e) c += scale * gate[t * k + j];
       if (c != 0.f) {
         const int64_t col = (int64_t)q * N * r + (int64_t)e * r + rho;
+        float us[kMaxSplits];             // every split's partial in flight at once
+#pragma unroll
+        for (int s = 0; s < kMaxSplits; ++s) us[s] = s < splits ? __ldcg(U + ((int64_t)s * T + t) * ldu + col) : 0.f;
         float u = 0.f;
-        for (int s = 0; s < splits; ++s) u += U[((int64_t)s * T + t) * ldu + col];    // split order: deterministic
+#pragma unroll
+        for (int s = 0; s < kMaxSplits; ++s)
+          if (s < splits) u += us[s];      // split order: deterministic
         z = c * u;
       }
     }
@@ -498,13 +508,23 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
 
 void pf_plan_destroy(PfPlan* p) { delete p; }
 
-// token-tile width of a launch: 256 halves the shared-memory operand traffic
-// per MAC when the stage plan still holds >= 3 stages (rp <= 32) and the
-// extra rows of a partial 256-token tile are few
-static int pf_tt(const PfPlan* p, int64_t T) {
+// token-tile width of a group's launches (rt: the dense launch's row tiles).
+// A 256-token tile moves 2/3 of the operand bytes per MAC of a 128-token one
+// (48 vs 32 KB per 64-deep stage for twice the MACs), so it takes ~1/0.65 of
+// the 128-token tile's time for twice the work -- but the dense launch is
+// persistent over ONE wave of num_sms CTAs, and with few row tiles the
+// 256-token tiles leave SMs idle (7B o / down at 512 tokens: 64 tiles on 148
+// SMs).  Chosen by rounds x relative tile time; 256 needs >= 3 stages (rp <=
+// 32) and T a multiple of 256 (no half-empty tiles).  Measured (7B, 512
+// tokens): o 38.3 vs 43.9 us, down 67.8 vs 81.3 with 128; q|k|v 73.1 vs 84.5,
+// gate|up 99.2 vs 122.8 with 256.
+static int pf_tt(const PfPlan* p, int64_t T, int64_t rt) {
+  const bool ok256 = T % 256 == 0 && pf_geom(256, p->rp).stages >= 3;
   if (p->tt_opt) return p->tt_opt == 256 && pf_geom(256, p->rp).stages >= 3 ? 256 : 128;
-  // measured (7B, 512 tokens, PDL-chained launches): 0.318 vs 0.324 ms per layer
-  return T % 256 == 0 && pf_geom(256, p->rp).stages >= 3 ? 256 : 128;
+  if (!ok256) return 128;
+  const int64_t G = p->num_sms;
+  const int64_t r128 = (rt * ((T + 127) / 128) + G - 1) / G, r256 = (rt * (T / 256) + G - 1) / G;
+  return 100 * r256 <= 65 * r128 + 5 ? 256 : 128;
 }
 
 // cluster size of the dense launch (variant option pf_cluster; default 1).
@@ -517,14 +537,17 @@ static int pf_cluster(const PfPlan* p, int64_t n_tt) {
   return p->cl_opt ? p->cl_opt : 1;
 }
 
-// scratch sizes (elements) a launch with T tokens needs
+// scratch sizes (elements) a launch with T tokens needs (either token tile)
 void pf_scratch(const PfPlan* p, int n_sites, int64_t T, int64_t* u_elems, int64_t* z_elems) {
   const int64_t nr = (int64_t)p->n_experts * p->r;
-  const int tt = pf_tt(p, T);
-  const int64_t n_tt = (T + tt - 1) / tt, c = pf_cluster(p, n_tt);
-  const int64_t n_tt_pad = (n_tt + c - 1) / c * c;               // Z of padded token tiles: zeros
-  *u_elems = (int64_t)p->num_sms * T * n_sites * nr;          // splits <= num_sms
-  *z_elems = n_tt_pad * n_sites * p->n_experts * 2 * (int64_t)tt * p->rp;
+  *u_elems = (int64_t)pf::kMaxSplits * T * n_sites * nr;
+  *z_elems = 0;
+  for (int64_t tt : {128, 256}) {
+    const int64_t n_tt = (T + tt - 1) / tt, c = pf_cluster(p, n_tt);
+    const int64_t n_tt_pad = (n_tt + c - 1) / c * c;             // Z of padded token tiles: zeros
+    const int64_t z = n_tt_pad * n_sites * p->n_experts * 2 * tt * p->rp;
+    if (z > *z_elems) *z_elems = z;
+  }
 }
 
 template <int kTT>
@@ -557,7 +580,12 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   }
   a.tile_row0[P.n_sites] = rt;
   a.row_tiles_total = rt;
+  // K split over the grid, at most kMaxSplits ways: the Z build sums the
+  // splits' fp32 partials per element (and they cross L2), so a 74-way split
+  // (7B o at 512 tokens: every SM a 64-deep slice) made the Z build, not the
+  // products, the LoRA chain's cost
   int splits = p->num_sms / (rt * n_tt);
+  if (splits > kMaxSplits) splits = kMaxSplits;
   if (splits < 1) splits = 1;
   if (splits > n_kb) splits = n_kb;
   a.splits = splits;
@@ -569,9 +597,21 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   a.b_off = geo.b_off;
   a.rp = p->rp;
   int grid = a.total_tiles < p->num_sms ? a.total_tiles : p->num_sms;
-  prefill_gemm<kTT, 1><<<grid, kThreads, geo.smem, s>>>(maps, a);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  cudaError_t e;
+  {
+    cudaLaunchConfig_t uc{};
+    uc.gridDim = dim3(grid);
+    uc.blockDim = dim3(kThreads);
+    uc.dynamicSmemBytes = geo.smem;
+    uc.stream = s;
+    cudaLaunchAttribute ua[1];
+    ua[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    ua[0].val.programmaticStreamSerializationAllowed = 1;
+    uc.attrs = ua;
+    uc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&uc, prefill_gemm<kTT, 1>, maps, a);
+    if (e != cudaSuccess) return e;
+  }
   // ---- 2. gate-scaled (hi, lo) LoRA-down products of the selected experts
   const int C = pf_cluster(p, n_tt);
   const int n_tt_pad = (n_tt + C - 1) / C * C;
@@ -648,7 +688,10 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
 
 cudaError_t launch_prefill_tc(const PfPlan* p, const PrefillParams& P, int layer, const int kinds[3],
                               cudaStream_t s) {
-  return pf_tt(p, P.T) == 256 ? prefill_tc_tt<256>(p, P, layer, kinds, s) : prefill_tc_tt<128>(p, P, layer, kinds, s);
+  int64_t rt = 0;                          // row tiles of the dense launch
+  for (int q = 0; q < P.n_sites; ++q) rt += (p->d_out[kinds[q]] + pf::kTM - 1) / pf::kTM;
+  return pf_tt(p, P.T, rt) == 256 ? prefill_tc_tt<256>(p, P, layer, kinds, s)
+                                  : prefill_tc_tt<128>(p, P, layer, kinds, s);
 }
 
 }  // namespace lsw

@@ -1,5 +1,5 @@
 """Prefill timing per GEMV group (7B widths, T tokens): lsw_prefill_group with
-the token tile forced to 128 / 256 (variant option pf_tt), next to the same
+the token tile chosen per group (auto) or forced to 128 / 256 (variant option pf_tt), next to the same
 dense products by torch.matmul (cuBLAS, reference only) -- JSON to stdout."""
 import json
 import os
@@ -33,13 +33,19 @@ def main():
     W, A, B, router = H.build_weights(cfg, "cuda")
     out = {"config": name, "T": T}
     X1 = synth.gen_x1(cfg, T, "cuda")
-    for tt in (128, 256):
-        with binding.options(pf_tt=tt):
-            sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+    for tt in (0, 128, 256):
         idx = torch.empty(T, cfg.top_k, dtype=torch.int32, device="cuda")
         gate = torch.empty(T, cfg.top_k, dtype=torch.float32, device="cuda")
-        for t in range(T):
-            sw.router_topk(X1[t], idx[t], gate[t])
+        # the prefill plan is built at the first prefill call: inside the
+        # options block, or the option would not reach it
+        with binding.options(**({"pf_tt": tt} if tt else {})):
+            sw = H.make_switch(cfg, W, A, B, router, impl="tc")
+            for t in range(T):
+                sw.router_topk(X1[t], idx[t], gate[t])
+            d_in0 = cfg.kind_shape(synth.GROUPS[1][0])[1]
+            rows0 = cfg.kind_shape(synth.GROUPS[1][0])[0]
+            sw.prefill_group(1, 1, torch.zeros(T, d_in0, device="cuda", dtype=torch.bfloat16), idx, gate,
+                             torch.empty(T, rows0, device="cuda"))
         res = {}
         for gi, grp in enumerate(synth.GROUPS):
             d_in = cfg.kind_shape(grp[0])[1]
@@ -49,14 +55,15 @@ def main():
             ms = timed(lambda: sw.prefill_group(1, gi, X, idx, gate, Y))
             fl = 2.0 * T * rows * d_in
             res["+".join(grp)] = {"ms": ms, "dense_tflops": fl / ms / 1e9}
-            if tt == 128:
+            if tt == 0:
                 Wc = torch.cat([W[kd][1] for kd in grp])
                 ms_ref = timed(lambda: torch.matmul(X, Wc.t(), out=None))
                 res["+".join(grp)]["torch_matmul_bf16_ms"] = ms_ref
-        out[f"tt{tt}"] = res
-        out[f"tt{tt}_layer_ms"] = sum(v["ms"] for v in res.values())
+        key = f"tt{tt}" if tt else "auto"
+        out[key] = res
+        out[f"{key}_layer_ms"] = sum(v["ms"] for v in res.values())
         sw.close()
-    out["torch_dense_layer_ms"] = sum(v["torch_matmul_bf16_ms"] for v in out["tt128"].values())
+    out["torch_dense_layer_ms"] = sum(v["torch_matmul_bf16_ms"] for v in out["auto"].values())
     print(json.dumps(out, indent=1))
 
 

@@ -36,7 +36,8 @@ def _f64(t):
                                             ("mini-r32", "tc", 257, 256), ("mini-r4k4", "tc", 20, 256),
                                             ("mini", "tc", 512, "128/4"), ("mini", "tc", 300, "128/4"),
                                             ("mini-r32", "tc", 256, "128/2"), ("mini-r64k3", "tc", 384, "128/2"),
-                                            ("mini", "tc", 1024, "256/4"), ("mini-k1", "tc", 200, "128/1")])
+                                            ("mini", "tc", 1024, "256/4"), ("mini-k1", "tc", 200, "128/1"),
+                                            ("mini", "tc", 512, None), ("mini-r32", "tc", 256, None)])
 def test_prefill_matches_oracle(lsw_opts, name, impl, T, tt):
     """tt: the token tile of the tensor-core path forced to 256 (variant option
     pf_tt), or "tile/cluster": also the cluster of the dense launch forced
