@@ -50,6 +50,14 @@ struct Maps {
   CUtensorMap op[3];   // MODE_Y: W of site q [L, d_out, d_in]; MODE_U: A of site q [L, N*r, d_in]
   CUtensorMap x;       // X [T, d_in]
 };
+// CTA pairs: every operand moved by a tensor copy (so that the follower's
+// copies can complete on the leader's barrier)
+struct PairMaps {
+  CUtensorMap op[3];   // W of site q [L, d_out, d_in], box {64, 128}, 128-B swizzle
+  CUtensorMap x;       // X [T, d_in], box {64, kTT/2}, 128-B swizzle
+  CUtensorMap b[3];    // packed B of site q's kind as [L*N*dout_pad, rp] (pre-swizzled), box {rp, 128}, no swizzle
+  CUtensorMap z;       // Z as [rows, rp] (pre-swizzled), box {rp, kTT/2}, no swizzle
+};
 
 struct Args {
   int32_t mode, n_sites, layer, n_tt, n_kb, splits, total_tiles;
@@ -70,6 +78,7 @@ struct Args {
   const __nv_bfloat16* Z;        // [n_tt][n_sites][N][2][kTT][rp], pre-swizzled
   uint32_t stage_bytes, b_off;   // stage = [A part | B part at b_off]
   int32_t stages;
+  int32_t pair_row0[4];          // CTA pairs: prefix sums of the sites' row-tile PAIRS
 };
 
 struct TileAt {
@@ -143,6 +152,28 @@ __device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* 
 __device__ __forceinline__ void umma_commit_mc(uint32_t bar, uint16_t mask) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
                ::"r"(bar), "h"(mask) : "memory");
+}
+
+// CTA pairs: arrive on the mbarrier at the same shared offset in CTA `rank`
+// of the cluster; the pair's MMA (leader only, M = 256 over both CTAs' A
+// halves, N over both CTAs' B halves, same shared offsets); the pair's commit
+// multicast to the barrier at this offset in both CTAs
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(bar), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+               ::"r"(bar), "h"((uint16_t)3) : "memory");
 }
 
 // Tile of iteration `it` of this CTA: kC == 1 -- global tile index (tile_at);
@@ -362,6 +393,232 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
   }
 }
 
+// ---------------------------------------------------------------------------
+// MODE_Y on CTA pairs (cta_group::2): a pair tile is 256 output rows (two
+// row tiles of ONE site, one per CTA of a cluster of 2) x kTT tokens.  Each
+// CTA loads its own 128 W rows and HALF of the tile's tokens (X box of kTT/2
+// rows; for the LoRA-up stages its B slice and half of Z's hi and lo parts),
+// and the leader issues tcgen05.mma.cta_group::2 (M = 256, N = kTT) reading
+// both CTAs' shared memory: per CTA and 64-deep K step 32 KB of operands
+// instead of 48 KB for the same MACs as a 128 x 256 tile, the dense GEMM's
+// bound being the operand feed from L2.  Every copy is a tensor copy with
+// .cta_group::2 completing on the LEADER's full barrier (which expects both
+// CTAs' bytes), so no stage is relayed between the CTAs; the leader's commits
+// are multicast to both CTAs' empty / accumulator barriers; each CTA's
+// epilogue reads its own TMEM lanes (its 128 rows) and the follower's
+// epilogue releases the accumulator to the leader by a remote arrive.  Pairs
+// never straddle two sites: Z (the N operand of the LoRA-up stages) belongs
+// to one site.
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                                uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_cg2(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                                int32_t c2, uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+template <int kTT>
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_gemm_pair(const __grid_constant__ PairMaps maps, const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ uint32_t s_tmem_base;
+  __shared__ __align__(8) uint64_t bar_full[kMaxStages], bar_empty[kMaxStages];
+  __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool lora = a.n_experts > 0;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  constexpr int kHalf = kTT / 2;                  // tokens per CTA of a pair tile
+  const int it0 = (int)cluster_id(), istep = (int)cluster_count();
+  const int n_it = a.pair_row0[a.n_sites] * a.n_tt;
+  const uint32_t zhalf = (uint32_t)kHalf * a.rp * 2;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(smem_u32(&bar_full[s]), 1);          // leader: its producer's arrive + both CTAs' bytes
+      mbar_init(smem_u32(&bar_empty[s]), 1);         // the leader's commit, multicast to both CTAs
+    }
+    for (int s = 0; s < kAccBufs; ++s) {
+      mbar_init(smem_u32(&bar_accfull[s]), 1);
+      mbar_init(smem_u32(&bar_accempty[s]), 2 * kEpiWarps);   // leader: both CTAs' epilogues
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    for (int q = 0; q < a.n_sites; ++q) {
+      prefetch_map(&maps.op[q]);
+      if (lora) prefetch_map(&maps.b[q]);
+    }
+    prefetch_map(&maps.x);
+    if (lora) prefetch_map(&maps.z);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(&s_tmem_base)), "r"(kAccBufs * kTT) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                                 // the peer's barriers exist before any copy / commit targets them
+  tc_fence_after();
+  const uint32_t tmem_base = s_tmem_base;
+  // pair tile `it` -> this CTA's (site, row tile, token tile)
+  auto tile = [&](int it) {
+    TileAt r;
+    r.tt = it % a.n_tt;
+    const int p = it / a.n_tt;
+    r.q = (a.n_sites > 2 && p >= a.pair_row0[2]) ? 2 : (a.n_sites > 1 && p >= a.pair_row0[1]) ? 1 : 0;
+    r.rb = 2 * (p - a.pair_row0[r.q]) + (int)crank;
+    r.kb0 = 0;
+    r.kb1 = a.n_kb;
+    return r;
+  };
+
+  if (warp == 0) {
+    // ============================ producer ==================================
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      Ring ring{0, 0, (uint32_t)a.stages};
+      bool z_ready = false;
+      const uint32_t dense_bytes = kBoxBytes + kHalf * kKB * 2, lora_bytes = a.term_bytes + 2 * zhalf;
+      for (int it = it0; it < n_it; it += istep) {
+        const TileAt ta = tile(it);
+        const int units = a.n_kb + (lora ? a.n_experts : 0);
+        for (int k = 0; k < units; ++k) {
+          if (k == a.n_kb && !z_ready) {          // Z is written by the preceding (Z build) grid
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            z_ready = true;
+          }
+          mbar_wait(smem_u32(&bar_empty[ring.i]), ring.phase ^ 1);
+          uint8_t* st = base + (size_t)ring.i * a.stage_bytes;
+          const uint32_t fb = smem_u32(&bar_full[ring.i]);
+          // the leader's barrier expects both CTAs' bytes; the follower's copies complete on it
+          if (leader) mbar_expect_tx(fb, 2 * (k < a.n_kb ? dense_bytes : lora_bytes));
+          const uint32_t bar = leader ? fb : mapa_rank(fb, 0);
+          if (k < a.n_kb) {
+            tma_load_3d_cg2(smem_u32(st), &maps.op[ta.q], k * kKB, ta.rb * kTM, a.layer, bar, pol_w);
+            tma_load_2d_cg2(smem_u32(st + a.b_off), &maps.x, k * kKB, ta.tt * kTT + (int)crank * kHalf, bar, pol_x);
+          } else {
+            const int e = k - a.n_kb;
+            tma_load_2d_cg2(smem_u32(st), &maps.b[ta.q], 0,
+                            (int)(((int64_t)a.layer * a.n_experts + e) * a.dout_pad[ta.q] + (int64_t)ta.rb * kTM),
+                            bar, pol_x);
+            const int zr = (int)(((((int64_t)ta.tt * a.n_sites + ta.q) * a.n_experts + e) * 2) * kTT) +
+                           (int)crank * kHalf;
+            tma_load_2d_cg2(smem_u32(st + a.b_off), &maps.z, 0, zr, bar, pol_x);                  // hi half
+            tma_load_2d_cg2(smem_u32(st + a.b_off + zhalf), &maps.z, 0, zr + kTT, bar, pol_x);    // lo half
+          }
+          ring.next();
+        }
+      }
+      // drain: every stage's last fill consumed by the leader's MMAs, so no
+      // commit still targets this CTA's barriers when it leaves
+      for (int i = 0; i < a.stages; ++i) {
+        mbar_wait(smem_u32(&bar_empty[ring.i]), ring.phase ^ 1);
+        ring.next();
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer (leader) =======================
+    // D f32, A/B bf16, both K-major, M = 256 (both CTAs' rows), N = kTT
+    if (leader) {
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTT >> 3) << 17) |
+                             ((uint32_t)((2 * kTM) >> 4) << 24);
+      const uint64_t dense0 = umma_desc(0, 1024, 2);
+      const uint64_t lora0 = umma_desc(0, 8 * (uint32_t)a.rp * 2, a.swz);
+      const uint64_t zpart = zhalf >> 4;
+      const int ksteps = a.rp / 16;
+      Ring ring{0, 0, (uint32_t)a.stages};
+      Ring acc{0, 0, kAccBufs};
+      const int units = a.n_kb + (lora ? a.n_experts : 0);
+      for (int it = it0; it < n_it; it += istep) {
+        mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc.i * kTT;
+        for (int k = 0; k < units; ++k) {
+          mbar_wait(smem_u32(&bar_full[ring.i]), ring.phase);
+          tc_fence_after();
+          const uint32_t st = smem_u32(base + (size_t)ring.i * a.stage_bytes);
+          if (elect_one()) {
+            if (k < a.n_kb) {
+              const uint64_t da = dense0 + (st >> 4), db = dense0 + ((st + a.b_off) >> 4);
+#pragma unroll
+              for (int kk = 0; kk < kKB / 16; ++kk)
+                umma_f16_pair(d, da + kk * 2, db + kk * 2, idesc, (k | kk) ? 1u : 0u);
+            } else {
+              const uint64_t da = lora0 + (st >> 4), db = lora0 + ((st + a.b_off) >> 4);
+              for (int part = 0; part < 2; ++part)
+                for (int kk = 0; kk < ksteps; ++kk)
+                  umma_f16_pair(d, da + kk * 2, db + part * zpart + kk * 2, idesc, 1u);
+            }
+            umma_commit_pair(smem_u32(&bar_empty[ring.i]));   // both CTAs' stages free when these complete
+          }
+          __syncwarp();
+          ring.next();
+        }
+        if (elect_one()) umma_commit_pair(smem_u32(&bar_accfull[acc.i]));
+        __syncwarp();
+        acc.next();
+      }
+    }
+  } else {
+    // ============================ epilogue ==================================
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    Ring acc{0, 0, kAccBufs};
+    for (int it = it0; it < n_it; it += istep) {
+      const TileAt ta = tile(it);
+      mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);
+      tc_fence_after();
+      const int64_t grow = (int64_t)ta.rb * kTM + row;
+      const bool ok = grow < a.rows_valid[ta.q];
+      float* outp = a.out + a.col0[ta.q] + grow;
+      const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTT;
+      for (int c0 = 0; c0 < kTT; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tm + c0, v);
+        tmem_wait_ld();
+        const int64_t tok0 = (int64_t)ta.tt * kTT + c0;
+        if (ok) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (tok0 + i < a.T) outp[(tok0 + i) * a.ld] = __uint_as_float(v[i]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+        else mbar_arrive_remote(smem_u32(&bar_accempty[acc.i]), 0);
+      }
+      acc.next();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();                                 // no copy / commit / remote arrive may target a CTA that left
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAccBufs * kTT)
+                 : "memory");
+  }
+}
+
 // Z (hi, lo) parts from the split-K LoRA-down partials: one thread per
 // (token tile, site, expert, token in tile, rho < rp).
 __global__ void prefill_zbuild(const float* __restrict__ U, int splits, int64_t T, int64_t ldu, int n_sites, int N,
@@ -420,6 +677,10 @@ struct PfPlan {
   int n_layers, n_experts, r, rp, num_sms;
   int tt_opt;                    // variant option pf_tt (128 | 256), 0: chosen per launch
   int cl_opt;                    // variant option pf_cluster (1 | 2 | 4), 0: chosen per launch
+  int pair_opt;                  // variant option pf_pair: 0 never, 1 (default) for groups with a wave of
+                                 // 256-token tiles, 2 whenever the sites' row tiles pair up: dense + LoRA-up
+                                 // on CTA pairs
+  CUtensorMap bmap[LSW_NKIND];   // pairs: the packed B of every kind as [L*N*dout_pad, rp]
 };
 
 // shared-memory plan of one token-tile width: stage = [128 x 64 A box | B
@@ -440,6 +701,34 @@ static PfGeom pf_geom(int tt, int rp) {
   if (g.stages > pf::kMaxStages) g.stages = pf::kMaxStages;
   g.smem = g.stages * g.stage_bytes + 1024;
   return g;
+}
+
+// CTA pairs: stage = [128 x 64 W box | kTT/2 x 64 X box], or [B slice | the
+// hi and lo halves of the token half of one expert's Z slice]
+static PfGeom pf_geom_pair(int tt, int rp) {
+  PfGeom g;
+  g.b_off = pf::kBoxBytes;
+  const uint32_t dense_b = (uint32_t)(tt / 2) * pf::kKB * 2, lora_b = 2u * (tt / 2) * rp * 2;
+  g.stage_bytes = g.b_off + (dense_b > lora_b ? dense_b : lora_b);
+  g.stages = (int)(kPfBudget / g.stage_bytes);
+  if (g.stages > pf::kMaxStages) g.stages = pf::kMaxStages;
+  g.smem = g.stages * g.stage_bytes + 1024;
+  return g;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 pf_encode();
+// bf16 [rows, rp] row-major, already laid out as the operand (pre-swizzled):
+// box {rp, box_rows}, no TMA swizzle -- a plain 2-D block copy
+static bool pf_map_rows(CUtensorMap* m, const void* base, uint64_t rows, uint32_t rp, uint32_t box_rows) {
+  auto enc = pf_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {rp, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)rp * 2};
+  cuuint32_t box[2] = {rp, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 pf_encode() {
@@ -486,7 +775,8 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
     if (!p->Bp[k] || !pf_map(&p->w[k], g.W, g.d_in, g.d_out, sp.n_layers) ||
         !pf_map(&p->w2[k], g.W, g.d_in, g.d_out, sp.n_layers, 64) ||
         !pf_map(&p->w4[k], g.W, g.d_in, g.d_out, sp.n_layers, 32) ||
-        !pf_map(&p->a[k], g.A, g.d_in, (uint64_t)sp.n_experts * sp.rank, sp.n_layers)) {
+        !pf_map(&p->a[k], g.A, g.d_in, (uint64_t)sp.n_experts * sp.rank, sp.n_layers) ||
+        !pf_map_rows(&p->bmap[k], p->Bp[k], (uint64_t)sp.n_layers * sp.n_experts * p->dout_pad[k], (uint32_t)rp, 128)) {
       delete p;
       return cudaErrorInvalidValue;
     }
@@ -494,6 +784,7 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
   p->tt_opt = (int)opt_int("pf_tt", 0);
   if (p->tt_opt != 128 && p->tt_opt != 256) p->tt_opt = 0;
   p->cl_opt = (int)opt_int("pf_cluster", 0);
+  p->pair_opt = (int)opt_int("pf_pair", 1);
   if (p->cl_opt != 1 && p->cl_opt != 2 && p->cl_opt != 4) p->cl_opt = 0;
   if (pf_geom(128, p->rp).stages < 3) { delete p; return cudaErrorNotSupported; }
   const int smem = (int)(kPfBudget + 1024);
@@ -501,12 +792,24 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
   for (auto fn : {pf::prefill_gemm<128, 1>, pf::prefill_gemm<128, 2>, pf::prefill_gemm<128, 4>,
                   pf::prefill_gemm<256, 1>, pf::prefill_gemm<256, 2>, pf::prefill_gemm<256, 4>})
     if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (auto fn : {pf::prefill_gemm_pair<128>, pf::prefill_gemm_pair<256>})
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) { delete p; return e; }
   *out = p;
   return cudaSuccess;
 }
 
 void pf_plan_destroy(PfPlan* p) { delete p; }
+
+// cluster size of the dense launch (variant option pf_cluster; default 1).
+// Measured (7B, 512 tokens, same box): clusters of 4 token tiles sharing each
+// W block by multicast 0.41 ms per layer vs 0.34 without -- the lockstep the
+// multicast protocol imposes on the cluster's CTAs costs more than the L2
+// traffic it saves.
+static int pf_cluster(const PfPlan* p, int64_t n_tt) {
+  (void)n_tt;
+  return p->cl_opt ? p->cl_opt : 1;
+}
 
 // token-tile width of a group's launches (rt: the dense launch's row tiles).
 // A 256-token tile moves 2/3 of the operand bytes per MAC of a 128-token one
@@ -518,24 +821,29 @@ void pf_plan_destroy(PfPlan* p) { delete p; }
 // 32) and T a multiple of 256 (no half-empty tiles).  Measured (7B, 512
 // tokens): o 38.3 vs 43.9 us, down 67.8 vs 81.3 with 128; q|k|v 73.1 vs 84.5,
 // gate|up 99.2 vs 122.8 with 256.
-static int pf_tt(const PfPlan* p, int64_t T, int64_t rt) {
+static int pf_tt(const PfPlan* p, int64_t T, int64_t rt, bool pair) {
   const bool ok256 = T % 256 == 0 && pf_geom(256, p->rp).stages >= 3;
   if (p->tt_opt) return p->tt_opt == 256 && pf_geom(256, p->rp).stages >= 3 ? 256 : 128;
   if (!ok256) return 128;
   const int64_t G = p->num_sms;
   const int64_t r128 = (rt * ((T + 127) / 128) + G - 1) / G, r256 = (rt * (T / 256) + G - 1) / G;
-  return 100 * r256 <= 65 * r128 + 5 ? 256 : 128;
+  // pairs: 32 vs 24 KB per CTA and K step (256- vs 128-token tile) -> 0.75
+  return 100 * r256 <= (pair ? 75 : 65) * r128 + 5 ? 256 : 128;
 }
 
-// cluster size of the dense launch (variant option pf_cluster; default 1).
-// Measured (7B, 512 tokens, same box): clusters of 4 token tiles sharing each
-// W block by multicast 0.41 ms per layer vs 0.34 without -- the lockstep the
-// multicast protocol imposes on the cluster's CTAs costs more than the L2
-// traffic it saves.
-static int pf_cluster(const PfPlan* p, int64_t n_tt) {
-  (void)n_tt;
-  return p->cl_opt ? p->cl_opt : 1;
+// the dense + LoRA-up launch runs on CTA pairs: option on, no multicast
+// cluster, every site's row tiles pair up within the site, and at least a
+// wave of 256-token tiles (measured, 7B at 512 tokens: q|k|v 68.8 vs 70.5
+// us, gate|up 90.6 vs 98.7 on pairs; o / down -- 64 tiles of 256 tokens, the
+// LoRA chain their bound -- 40.6 vs 35.3 and 73.9 vs 64.6: single CTAs)
+static bool pf_pair(const PfPlan* p, int n_sites, const int kinds[3], int64_t T, int64_t rt) {
+  if (!p->pair_opt || pf_cluster(p, 0) != 1) return false;
+  if (p->pair_opt == 1 && rt * ((T + 255) / 256) < p->num_sms) return false;   // (pf_pair=2: always)
+  for (int q = 0; q < n_sites; ++q)
+    if (((p->d_out[kinds[q]] + pf::kTM - 1) / pf::kTM) % 2) return false;
+  return true;
 }
+
 
 // scratch sizes (elements) a launch with T tokens needs (either token tile)
 void pf_scratch(const PfPlan* p, int n_sites, int64_t T, int64_t* u_elems, int64_t* z_elems) {
@@ -552,7 +860,7 @@ void pf_scratch(const PfPlan* p, int n_sites, int64_t T, int64_t* u_elems, int64
 
 template <int kTT>
 static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int layer, const int kinds[3],
-                                 cudaStream_t s) {
+                                 cudaStream_t s, bool pair) {
   using namespace pf;
   const PfGeom geo = pf_geom(kTT, p->rp);
   Maps maps;
@@ -670,6 +978,38 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
+  if (C == 1 && pair) {
+    const PfGeom gp = pf_geom_pair(kTT, p->rp);
+    PairMaps mp;
+    memset(&mp, 0, sizeof(mp));
+    for (int q = 0; q < P.n_sites; ++q) {
+      mp.op[q] = maps.op[q];
+      mp.b[q] = p->bmap[kinds[q]];
+    }
+    const int64_t z_rows = (int64_t)n_tt_pad * P.n_sites * p->n_experts * 2 * kTT;
+    if (!pf_map(&mp.x, P.X, P.d_in, P.T, 0, kTT / 2) ||                                  // token halves
+        !pf_map_rows(&mp.z, P.Z, (uint64_t)z_rows, (uint32_t)p->rp, kTT / 2))
+      return cudaErrorInvalidValue;
+    int pr = 0;
+    for (int q = 0; q < P.n_sites; ++q) {
+      y.pair_row0[q] = pr;
+      pr += (int)((p->d_out[kinds[q]] + kTM - 1) / kTM) / 2;
+    }
+    y.pair_row0[P.n_sites] = pr;
+    y.stages = gp.stages;
+    y.stage_bytes = gp.stage_bytes;
+    y.b_off = gp.b_off;
+    const int n_pt = pr * n_tt;                               // pair tiles
+    const int n_cl = n_pt < p->num_sms / 2 ? n_pt : p->num_sms / 2;
+    lc.gridDim = dim3(2 * n_cl);
+    lc.dynamicSmemBytes = gp.smem;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 2;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    lc.numAttrs = 2;
+    return cudaLaunchKernelEx(&lc, prefill_gemm_pair<kTT>, mp, y);
+  }
   if (C == 1) {
     lc.gridDim = dim3(y.total_tiles < p->num_sms ? y.total_tiles : p->num_sms);
     return cudaLaunchKernelEx(&lc, prefill_gemm<kTT, 1>, maps, y);
@@ -690,8 +1030,9 @@ cudaError_t launch_prefill_tc(const PfPlan* p, const PrefillParams& P, int layer
                               cudaStream_t s) {
   int64_t rt = 0;                          // row tiles of the dense launch
   for (int q = 0; q < P.n_sites; ++q) rt += (p->d_out[kinds[q]] + pf::kTM - 1) / pf::kTM;
-  return pf_tt(p, P.T, rt) == 256 ? prefill_tc_tt<256>(p, P, layer, kinds, s)
-                                  : prefill_tc_tt<128>(p, P, layer, kinds, s);
+  const bool pair = pf_pair(p, P.n_sites, kinds, P.T, rt);
+  return pf_tt(p, P.T, rt, pair) == 256 ? prefill_tc_tt<256>(p, P, layer, kinds, s, pair)
+                                        : prefill_tc_tt<128>(p, P, layer, kinds, s, pair);
 }
 
 }  // namespace lsw

@@ -37,13 +37,25 @@ def _f64(t):
                                             ("mini", "tc", 512, "128/4"), ("mini", "tc", 300, "128/4"),
                                             ("mini-r32", "tc", 256, "128/2"), ("mini-r64k3", "tc", 384, "128/2"),
                                             ("mini", "tc", 1024, "256/4"), ("mini-k1", "tc", 200, "128/1"),
-                                            ("mini", "tc", 512, None), ("mini-r32", "tc", 256, None)])
+                                            ("mini", "tc", 512, None), ("mini-r32", "tc", 256, None),
+                                            ("mini", "tc", 300, "nopair"), ("mini-r64k3", "tc", 512, "nopair"),
+                                            ("mini-r64k4", "tc", 257, 128), ("mini-r4k4", "tc", 512, 256),
+                                            ("mini", "tc", 300, "pair"), ("mini-r32", "tc", 512, "pair"),
+                                            ("mini-r64k4", "tc", 200, "pair"), ("mini-k1", "tc", 77, "pair")])
 def test_prefill_matches_oracle(lsw_opts, name, impl, T, tt):
-    """tt: the token tile of the tensor-core path forced to 256 (variant option
-    pf_tt), or "tile/cluster": also the cluster of the dense launch forced
+    """The dense + LoRA-up launch runs on CTA pairs (cta_group::2, M = 256)
+    for groups with a wave of 256-token tiles whose sites' row tiles pair up;
+    "pair": on pairs whenever the row tiles pair up (mini: o, gate|up, down;
+    not q|k|v, k being one row tile; option pf_pair=2); "nopair": single
+    CTAs everywhere (pf_pair=0).  tt: the token tile of the tensor-core path forced to 128 /
+    256 (variant option pf_tt), or "tile/cluster": also the cluster of the dense launch forced
     (pf_cluster: W rows multicast across the token tiles of a cluster; T = 300
     with 4 pads a cluster with an all-out-of-range token tile)."""
-    if isinstance(tt, str):
+    if tt == "nopair":                              # dense + LoRA-up on single CTAs (pf_pair=0)
+        lsw_opts(pf_pair=0)
+    elif tt == "pair":                              # on CTA pairs whenever the row tiles pair up (pf_pair=2)
+        lsw_opts(pf_pair=2)
+    elif isinstance(tt, str):
         t_, c_ = tt.split("/")
         lsw_opts(pf_tt=int(t_), pf_cluster=int(c_))
     else:
@@ -109,7 +121,7 @@ def _rows(d_out, seed):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name,T", [("llama2-7b", 300), ("llama2-13b", 200)])
+@pytest.mark.parametrize("name,T", [("llama2-7b", 300), ("llama2-7b", 512), ("llama2-13b", 200)])
 def test_prefill_full_width_sampled_rows(name, T):
     """One layer at the real widths: every group (K = d_model and K = d_ff),
     every token, sampled rows of every site (row sampling is exact: row i of Y
