@@ -53,6 +53,7 @@ constexpr int kPtGroup = 2;                 // per-term mode: terms per MMA grou
 struct Maps {
   CUtensorMap w[LSW_NKIND];   // W [L, d_out, d_in], box {64, 128, 1}, 128B swizzle
   CUtensorMap p[LSW_NKIND];   // pristine copies (RESTORE source), same geometry
+  CUtensorMap at[LSW_NKIND];  // pair mode: packed A^T as [L*col_tiles*N*128, rp] (pre-swizzled), box {rp, 64}
 };
 
 struct Geom {
@@ -443,6 +444,22 @@ __device__ __forceinline__ uint32_t cta_rank_in_cluster() {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// the shared::cluster address of the same shared offset in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// pair: a tensor copy into this CTA's shared memory completing on `bar`,
+// which may be the leader's barrier (shared::cluster address)
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                                uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(policy)
+      : "memory");
+}
 // arrive on the mbarrier at the same shared offset in CTA `rank` of the cluster
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) {
   uint32_t r;
@@ -754,12 +771,24 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           FC_TRACE(1, na_tr);
           uint8_t* adst = ast0 + (size_t)aring.i * g.a_stage_bytes;
           const uint32_t bar = smem_u32(&bar_afull[aring.i]);
-          // pair: this CTA's half of the tile's 128 columns (rows 64 * rank.. of each A^T slice)
-          const uint32_t ta = kPair ? tb / 2 : tb;
-          mbar_expect_tx(bar, nt * ta);
-          for (int j = 0; j < nt; ++j)
-            bulk_load(smem_u32(adst + j * ta), blk + (size_t)cf.e[j] * kTN * rpe + (size_t)crank * (kTN / 2) * rpe,
-                      ta, bar, pol_keep);
+          if constexpr (kPair) {
+            // this CTA's half of the tile's 128 columns (rows 64 * rank.. of
+            // each A^T slice) by .cta_group::2 tensor copies completing on the
+            // LEADER's barrier, which expects both halves: no relay of the
+            // stage from the follower to the leader's MMA warp
+            const uint32_t ta = tb / 2;
+            if (leader) mbar_expect_tx(bar, 2 * nt * ta);
+            const uint32_t lbar = leader ? bar : mapa_u32(bar, 0);
+            const int64_t row0 = (((int64_t)c.layer * tk.col_tiles[c.kd] + c.cb) * g.n_experts) * kTN +
+                                 (int64_t)crank * (kTN / 2);
+            for (int j = 0; j < nt; ++j)
+              tma_load_2d_cg2(smem_u32(adst + j * ta), &maps.at[c.kd], 0, (int32_t)(row0 + (int64_t)cf.e[j] * kTN),
+                              lbar, pol_keep);
+          } else {
+            mbar_expect_tx(bar, nt * tb);
+            for (int j = 0; j < nt; ++j)
+              bulk_load(smem_u32(adst + j * tb), blk + (size_t)cf.e[j] * kTN * rpe, tb, bar, pol_keep);
+          }
         }
         __syncwarp();
         aring.next();
@@ -827,10 +856,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           }
         }
         if constexpr (kPair) {
-          if (!leader) {                         // follower: report the A stage, no MMA
-            mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(smem_u32(&bar_apeer[aring.i]), 0);
+          if (!leader) {                         // follower: no MMA (its A halves land on the leader's barrier)
             aring.next();
             continue;
           }
@@ -899,8 +925,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           acc.next();
           continue;
         }
-        mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);
-        if constexpr (kPair) mbar_wait(smem_u32(&bar_apeer[aring.i]), aring.phase);
+        mbar_wait(smem_u32(&bar_afull[aring.i]), aring.phase);   // (pair: both CTAs' A halves)
         if (lane == 0) FC_TRACE(2, nm_tr);
         mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
         tc_fence_after();
@@ -1251,6 +1276,20 @@ static bool encode_any(CUtensorMap* m, const void* base, uint64_t d_in, uint64_t
   return rm ? encode_w_rm(m, base, d_in, d_out, L) : encode_w(m, base, d_in, d_out, L);
 }
 
+// bf16 [rows, rp] already laid out as an operand (pre-swizzled): box {rp,
+// box_rows}, no TMA swizzle -- a plain 2-D block copy
+static bool encode_rows(CUtensorMap* m, const void* base, uint64_t rows, uint32_t rp, uint32_t box_rows) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {rp, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)rp * 2};
+  cuuint32_t box[2] = {rp, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 static uint32_t align1k(uint32_t x) { return (x + 1023) & ~1023u; }
 
 cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, const char** why, int pt) {
@@ -1485,7 +1524,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
                                  kg.d_out, g.dout_pad[k]);
     g.At[k] = (const __nv_bfloat16*)plan->packed_At[k];
     g.Bp[k] = (const __nv_bfloat16*)plan->packed_B[k];
-    if (!encode_any(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers, g.wrm)) {
+    if (!encode_any(&plan->maps.w[k], kg.W, kg.d_in, kg.d_out, sp.n_layers, g.wrm) ||
+        !encode_rows(&plan->maps.at[k], plan->packed_At[k], (uint64_t)M * din_pad, (uint32_t)rp, kTN / 2)) {
       *why = "cuTensorMapEncodeTiled failed";
       e = cudaErrorInvalidValue;
     }
