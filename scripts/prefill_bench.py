@@ -29,6 +29,7 @@ def timed(fn, n=10):
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "llama2-7b"
     T = int(sys.argv[2]) if len(sys.argv) > 2 else 512
+    extra = dict(kv.split("=") for kv in sys.argv[3:])       # variant options for every run
     cfg = synth.get_config(name).with_(n_layers=2)
     W, A, B, router = H.build_weights(cfg, "cuda")
     out = {"config": name, "T": T}
@@ -38,7 +39,7 @@ def main():
         gate = torch.empty(T, cfg.top_k, dtype=torch.float32, device="cuda")
         # the prefill plan is built at the first prefill call: inside the
         # options block, or the option would not reach it
-        with binding.options(**({"pf_tt": tt} if tt else {})):
+        with binding.options(**({"pf_tt": tt} if tt else {}), **extra):
             sw = H.make_switch(cfg, W, A, B, router, impl="tc")
             for t in range(T):
                 sw.router_topk(X1[t], idx[t], gate[t])
