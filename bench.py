@@ -471,18 +471,17 @@ def run_ours(args, cfg):
 
     # unmerged decode (the honest comparison): router + Eq. 2 on the
     # pristine weights, W read once (2 B/element) instead of switched and read (6)
-    un_ms = []
-    if world == 1:
-        if sw.info()["merged"]:
-            sw.unmerge_all_layers(stream)
-        for t in range(min(args.steps, 10)):
-            a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
-            a.record(stream)
-            sw.router_topk(X1[t], idx, gate, stream)
-            sw.decode_all_layers_unmerged(xs, ys, idx, gate, stream)
-            b.record(stream)
-            torch.cuda.synchronize()
-            un_ms.append(a.elapsed_time(b))
+    un_ms = []   # (TP: the o / down partials are all-reduced by the library)
+    if sw.info()["merged"]:
+        sw.unmerge_all_layers(stream)
+    for t in range(min(args.steps, 10)):
+        a, b = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+        a.record(stream)
+        sw.router_topk(X1[t], idx, gate, stream)
+        sw.decode_all_layers_unmerged(xs, ys, idx, gate, stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        un_ms.append(a.elapsed_time(b))
 
     # unmerged prefill: a 512-token prompt, every token with its
     # own pre-gated decision, through every group of every layer (Eq. 2; our

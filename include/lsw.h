@@ -284,8 +284,11 @@ LSW_API lsw_status lsw_decode_all_layers(lsw_ctx* ctx, const void* xs, float* ys
  * terms of the CTA's rows while its W rows stream; y = (W x) + term, one
  * rounding of the sum per row; deterministic (fixed reduction orders).
  *   idx/gate: device [top_k] (from lsw_router_topk).  x, y as lsw_decode_group.
- *   LSW_E_STATE if the ctx is merged (W must be the pristine weight);
- *   LSW_E_UNSUPPORTED if tp_size > 1 (o/down would need an all-reduce of A x).
+ *   LSW_E_STATE if the ctx is merged (W must be the pristine weight).
+ *   Tensor parallel: as lsw_decode_linear -- a row-parallel group (o, down:
+ *   W[:, shard], A[:, shard]) writes its partial sum, all-reduced in place
+ *   (Eq. 2 is linear in the d_in shards, so no all-reduce of A x is needed);
+ *   LSW_E_NCCL before enqueuing if tp_size > 1 and no communicator.
  */
 LSW_API lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_t group, const void* x, float* y,
                                              const int32_t* idx, const float* gate, void* stream);
@@ -307,8 +310,10 @@ LSW_API lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_
  *   packed B) -- fp32 accumulation; otherwise two CUDA-core kernels (only the
  *   k selected experts).  Deterministic.  Scratch is ctx-owned, grown on
  *   demand (not graph-capturable when it grows).
- *   LSW_E_STATE if the ctx is merged; LSW_E_UNSUPPORTED if tp_size > 1;
- *   LSW_E_ARG for T outside [1, 2^20].  Invalid idx values contribute nothing.
+ *   LSW_E_STATE if the ctx is merged; LSW_E_ARG for T outside [1, 2^20].
+ *   Invalid idx values contribute nothing.  Tensor parallel: row-parallel
+ *   groups' partial Y all-reduced in place (as lsw_decode_group_unmerged);
+ *   LSW_E_NCCL before enqueuing if tp_size > 1 and no communicator.
  */
 LSW_API lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const void* X, int64_t T,
                                      const int32_t* idx, const float* gate, float* Y, void* stream);

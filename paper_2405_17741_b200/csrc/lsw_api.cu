@@ -472,7 +472,15 @@ static lsw_status gemv_unmerged(lsw_ctx* ctx, int layer, int group, const void* 
   if (group < 0 || group >= LSW_NGROUP) return fail(LSW_E_ARG, "%s: group=%d invalid", who, group);
   if (reinterpret_cast<uintptr_t>(x) % 16) return fail(LSW_E_ARG, "%s: x not 16-byte aligned", who);
   if (ctx->merged) return fail(LSW_E_STATE, "%s: the ctx is merged (unmerged decode reads the pristine W)", who);
-  if (ctx->cfg.tp_size > 1) return fail(LSW_E_UNSUPPORTED, "%s: tp_size > 1", who);
+  // Tensor parallelism: a column-parallel group's rows are complete on each
+  // rank (x and A whole, W / B rows of the shard); a row-parallel kind (o,
+  // down) holds W[:, shard] and A[:, shard], and its partial
+  // W_s x_s + sum_j c_j B_j (A_j,s x_s) sums over the ranks to W x + sum_j c_j
+  // B_j (A_j x) -- Eq. 2 is linear in the shards -- so the same all-reduce as
+  // the merged decode's finishes it.  Checked before anything is enqueued.
+  const bool row_par = ctx->kinds[kGroupKinds[group][0]].row_parallel != 0;
+  if (row_par && ctx->cfg.tp_size > 1 && !ctx->comm)
+    return fail(LSW_E_NCCL, "%s: tp_size=%d but no NCCL communicator attached", who, ctx->cfg.tp_size);
   if (!ctx->lora_u) {
     const size_t n = (size_t)3 * ctx->cfg.top_k * ctx->cfg.rank;
     if (cudaMalloc(&ctx->lora_u, n * sizeof(float)) != cudaSuccess)
@@ -512,6 +520,11 @@ static lsw_status gemv_unmerged(lsw_ctx* ctx, int layer, int group, const void* 
   if (e == cudaErrorNotSupported) return fail(LSW_E_UNSUPPORTED, "%s: needs the bulk GEMV (option gemv=ldg set)", who);
   if (e != cudaSuccess) return cuda_fail(e, "unmerged decode GEMV launch");
   ctx->launches += 1;                       // LoRA-down, GEMV and LoRA-up in one launch
+  if (row_par && ctx->comm) {
+    const Nccl* nc = nccl();
+    ncclResult_t r = nc->AllReduce(y, y, (size_t)rows, ncclFloat, ncclSum, ctx->comm, s);
+    if (r != ncclSuccess) return fail(LSW_E_NCCL, "%s: ncclAllReduce: %s", who, nc->GetErrorString(r));
+  }
   return LSW_OK;
 }
 
@@ -530,7 +543,12 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
     return fail(LSW_E_ARG, "%s: layer=%d not in [0,%d)", who, layer, ctx->cfg.n_layers);
   if (group < 0 || group >= LSW_NGROUP) return fail(LSW_E_ARG, "%s: group=%d invalid", who, group);
   if (ctx->merged) return fail(LSW_E_STATE, "%s: the ctx is merged (prefill reads the pristine W)", who);
-  if (ctx->cfg.tp_size > 1) return fail(LSW_E_UNSUPPORTED, "%s: tp_size > 1", who);
+  // tensor parallelism: as the unmerged decode -- column-parallel rows are
+  // complete per rank, row-parallel partial outputs all-reduced (Eq. 2 is
+  // linear in the d_in shards of W and A)
+  const bool row_par = ctx->kinds[kGroupKinds[group][0]].row_parallel != 0;
+  if (row_par && ctx->cfg.tp_size > 1 && !ctx->comm)
+    return fail(LSW_E_NCCL, "%s: tp_size=%d but no NCCL communicator attached", who, ctx->cfg.tp_size);
   if (reinterpret_cast<uintptr_t>(X) % 16) return fail(LSW_E_ARG, "%s: X not 16-byte aligned", who);
   const bool tc = ctx->tc != nullptr;
   if (tc && !ctx->pf) {
@@ -589,6 +607,11 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
                      : launch_prefill_simt(P, ctx->cfg.dtype, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_prefill_group: launch");
   ctx->launches += tc ? 3 : 2;              // tc: LoRA-down GEMM, Z build, dense + LoRA-up GEMM
+  if (row_par && ctx->comm) {
+    const Nccl* nc = nccl();
+    ncclResult_t r = nc->AllReduce(Y, Y, (size_t)(T * rows), ncclFloat, ncclSum, ctx->comm, (cudaStream_t)stream);
+    if (r != ncclSuccess) return fail(LSW_E_NCCL, "%s: ncclAllReduce: %s", who, nc->GetErrorString(r));
+  }
   return LSW_OK;
 }
 

@@ -7,7 +7,9 @@ fp32 all-reduce of o / down), and checks against the oracle on the FULL
 weights: identical decisions on every rank, each W shard within the parity
 tolerance of the oracle's slice, column-parallel outputs equal to the oracle's
 rows, row-parallel outputs (after the all-reduce) equal to the oracle's full
-output.  Rank 0 prints one JSON line; exit code 0 iff every rank passed.
+output; then the unmerged decode (lsw_decode_all_layers_unmerged, o / down
+partials all-reduced) against the oracle's Eq. 2.  Rank 0 prints one JSON
+line; exit code 0 iff every rank passed.
 
   python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \
       --master-port 29533 scripts/tp_check.py [--config mini] [--tokens 3]
@@ -102,6 +104,28 @@ def main():
                 if PT.allclose_frac_fail(Wg, ref) or div > PT.DIVERGENCE_TOL:
                     errs.append(f"t{t} W {kd}[{l}] shard {rank}: div {div:.3e}")
     sw.unmerge_all_layers()
+    orc.unmerge_all_layers()
+    # the unmerged decode (Eq. 2 on the unmerged weights): column-parallel rows
+    # complete per rank, row-parallel partials all-reduced by the library
+    sw.router_topk(X1[0], idx, gate)
+    sw.decode_all_layers_unmerged(xs, ys, idx, gate)
+    torch.cuda.synchronize()
+    io, go, _ = orc.route(f64(X1[0]))
+    coefs = [(int(e), cfg.alpha / cfg.rank * float(gv)) for e, gv in zip(io.tolist(), go.tolist())]
+    yh = ys.cpu().numpy()
+    worst["y_unmerged_fail"] = 0.0
+    for (l, kd, off, n) in layout:
+        gi = next(i for i, g in enumerate(synth.GROUPS) if kd in g)
+        y_full = O.unmerged_forward(orc.W[(kd, l)], As[(kd, l)], Bs[(kd, l)], coefs, f64(xs_full[(l, gi)]))
+        if kd in synth.ROW_PARALLEL:
+            ref = y_full
+        else:
+            lo, hi = synth.shard_range(cfg.kind_shape(kd)[0], rank, world)
+            ref = y_full[lo:hi]
+        fail = PT.allclose_frac_fail(yh[off:off + n], ref)
+        worst["y_unmerged_fail"] = max(worst["y_unmerged_fail"], fail)
+        if fail:
+            errs.append(f"unmerged y {kd}[{l}]: {fail:.3e} outside allclose")
     st = sw.device_status()
     if st:
         errs.append(f"device status {st}")

@@ -4,7 +4,8 @@
   ncclAllReduce after every row-parallel (o, down) GEMV -- the identity, so
   the token's outputs must equal those of a ctx without a communicator bit
   for bit -- eagerly and replayed from a CUDA graph that captured the
-  all-reduces (stream ordering, in-place use, capture).
+  all-reduces (stream ordering, in-place use, capture); likewise the
+  unmerged decode's and the prefill's all-reduce call sites.
 * Two or more GPUs: scripts/tp_check.py under torchrun, every rank through
   lsw_attach_nccl + lsw_decode_token, compared with the oracle's full y and
   W slices.  Skipped when fewer than 2 GPUs are visible, so a multi-GPU box
@@ -64,6 +65,21 @@ def test_one_rank_allreduce_is_identity_eager_and_graph(name):
         torch.cuda.synchronize()
         res.append(ys2.clone())
         assert torch.equal(ys2, res[-2])               # same weights as token 2
+        # the unmerged decode and prefill call sites too (all-reduce after o / down)
+        sw.unmerge_all_layers()
+        sw.router_topk(X1[2], idx, gate)
+        sw.decode_all_layers_unmerged(xs, ys, idx, gate)
+        torch.cuda.synchronize()
+        res.append(ys.clone())
+        if cfg.dtype == "bf16":
+            T = 5
+            gi = 3                                      # down: row-parallel
+            d_in = cfg.kind_shape("down")[1]
+            X = torch.randn(T, d_in, generator=torch.Generator().manual_seed(7)).to(torch.bfloat16).cuda()
+            Y = torch.empty(T, cfg.kind_shape("down")[0], device="cuda")
+            sw.prefill_group(0, gi, X, idx.repeat(T, 1), gate.repeat(T, 1), Y)
+            torch.cuda.synchronize()
+            res.append(Y.clone())
         assert sw.device_status() == 0
         outs.append(res)
         sw.close()

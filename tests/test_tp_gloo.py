@@ -7,7 +7,8 @@ row-parallel kind needs one sum-allreduce of the partial outputs.  Here each
 rank runs the oracle on its shard (built by synth.shard_*), and the test
 checks (i) each shard equals the slice of the full result bitwise, (ii) the
 router decision is identical on every rank, (iii) gathered / allreduced GEMV
-outputs equal the full GEMV.
+outputs equal the full GEMV, (iv) the unmerged forward (Eq. 2, the unmerged
+decode / prefill) on the pristine shards gathers / all-reduces to the full one.
 """
 import os
 import socket
@@ -82,6 +83,22 @@ def _worker(rank, world, port, q):
                              for r_ in range(world)]
                     dist.all_gather(parts, y_loc)
                     ok &= bool(np.array_equal(torch.cat(parts).numpy(), y_full))
+                # (iv) unmerged forward (Eq. 2) on the pristine shards: the row-parallel
+                # partials W_s x_s + sum_j c_j B_j (A_j,s x_s) all-reduce to the full
+                # result (linear in the d_in shards: no all-reduce of A x needed)
+                coefs = [(int(e), scale * float(gv)) for e, gv in zip(*decisions[2])]
+                P_loc = synth.to_f64_numpy(synth.shard_W(cfg, kd, Wf, rank, world))
+                u_loc = torch.from_numpy(O.unmerged_forward(P_loc, Al, Bl, coefs, x_loc))
+                u_full = O.unmerged_forward(synth.to_f64_numpy(Wf), synth.to_f64_numpy(Af),
+                                            synth.to_f64_numpy(Bf), coefs, x_full)
+                if kd in synth.ROW_PARALLEL:
+                    dist.all_reduce(u_loc)
+                    ok &= bool(np.allclose(u_loc.numpy(), u_full, rtol=1e-12, atol=1e-12))
+                else:
+                    parts = [torch.zeros(cfg.local_shape(kd, r_, world)[0], dtype=torch.float64)
+                             for r_ in range(world)]
+                    dist.all_gather(parts, u_loc)
+                    ok &= bool(np.allclose(torch.cat(parts).numpy(), u_full, rtol=1e-12, atol=1e-12))
         q.put((rank, ok))
     finally:
         dist.destroy_process_group()
