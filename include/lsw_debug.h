@@ -28,6 +28,8 @@ extern "C" {
  *   gemv_grid      N      GEMV grid cap                               [#SMs]
  *   gemv_op_kb     N      bytes per bulk copy, KB                     [32]
  *   gemv_smem_kb   N      ring budget, KB                             [176 / 208]
+ *   gemv_split     0|1|2  rows over 24 KB reduced by two warps (1);    [1]
+ *                         never (0); every row (2, tests)
  *   nccl_path      file   libnccl.so.2 to dlopen when none is loaded yet
  *                         (read at the first NCCL call, lsw_nccl_version)
  * Probes (deliberately WRONG results; only in a build with -DLSW_TUNING,

@@ -242,6 +242,7 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
   { const long x = opt_int("gemv_op_kb", 0); if (x >= 4 && x <= 96) ctx->gemv.op_bytes = ctx->gemv.op_min = (uint32_t)x * 1024; }
   { const long x = opt_int("gemv_smem_kb", 0); if (x >= 32 && x <= 224) ctx->gemv.budget = ctx->gemv.budget_lora = (size_t)x * 1024; }
   { const char* v = opt_str("gemv"); ctx->gemv.ldg = v && strcmp(v, "ldg") == 0; }
+  { const long v = opt_int("gemv_split", 1); ctx->gemv.split_rows = v < 0 || v > 2 ? 1 : (int)v; }
   ctx->gemv.probe = (int)probe_int("gemv_probe");
   ctx->unmerged_flags = (int)probe_int("unmerged_flags");
   e = cudaMalloc(&ctx->d_state, sizeof(DevState));

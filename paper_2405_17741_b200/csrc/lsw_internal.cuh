@@ -199,6 +199,7 @@ struct GemvTune {
   size_t budget_lora = 208 * 1024;  // same, unmerged form
   int probe = 0;                    // tuning builds only: 1 = stream W without the dot products
   bool ldg = false;                 // variant option gemv=ldg: the warp-per-row LDG kernel
+  int split_rows = 1;               // option gemv_split: 1 rows over 24 KB reduced by two warps, 0 never, 2 always
 };
 // early_w: the previous launch on `s` was a GEMV (W may be prefetched before
 // griddepcontrol.wait; see gemv.cu).  lora: null for the merged-weight GEMV,

@@ -331,13 +331,16 @@ def test_decode_token_host_matches_device_path():
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("split", [None, "2"])
 @pytest.mark.parametrize("grid,op_kb", [(None, None), (1, None), (3, "4"), (7, "6")])
 @pytest.mark.parametrize("name,impl", [("toy", "simt"), ("mini", "tc"), ("mini-r32", "tc")])
-def test_decode_all_layers_ring_wrap(lsw_opts, name, impl, grid, op_kb):
+def test_decode_all_layers_ring_wrap(lsw_opts, name, impl, grid, op_kb, split):
     """lsw_decode_all_layers equals the per-group launches bitwise and the
     oracle within the GEMV tolerance; small grids and bulk-copy sizes make
-    every CTA wrap its ring many times within a group."""
-    lsw_opts(gemv_grid=grid, gemv_op_kb=op_kb)
+    every CTA wrap its ring many times within a group.  split "2": every row
+    reduced by two warps (halves added by the second one to finish; by
+    default only rows over 24 KB, the Mistral / 13B down projections)."""
+    lsw_opts(gemv_grid=grid, gemv_op_kb=op_kb, gemv_split=split)
     S = Setup(name, impl, n_tokens=2)
     cfg = S.cfg
     info = S.sw.info()
