@@ -33,6 +33,8 @@ enum SwitchMode : int32_t { MODE_MERGE = 0, MODE_SWITCH = 1, MODE_UNMERGE = 2, M
 // decision was rejected (latched error) leaves it unchanged.  SWITCH and
 // UNMERGE subtract the slot's decision only while it is set, so a rejected
 // merge can never make a later pass subtract a decision W does not contain.
+constexpr int kFusedMaxCtas = 256;
+
 struct DevState {
   int32_t parity;
   uint32_t done;
@@ -42,6 +44,14 @@ struct DevState {
   float g[2][LSW_MAX_TOPK];
   uint32_t lora_arrive;          // unmerged GEMV: LoRA-down products published in this launch
   uint32_t lora_depart;          // unmerged GEMV: CTAs done (the last one resets both)
+  // fused decode's adaptive split (fc kernel): CTA b takes, in every segment
+  // of T tiles, [T * fused_w[b], T * fused_w[b + 1]) >> 24; fused_perf[b] its
+  // last pass's ns per tile (segment processing only, waits excluded); the
+  // pass's last CTA turns them into the next pass's split
+  int32_t fused_w_valid;          // 0: uniform split (b / G)
+  uint32_t fused_done;            // CTAs done with the pass (the last one updates and resets)
+  uint32_t fused_w[kFusedMaxCtas + 1];
+  float fused_perf[kFusedMaxCtas];
 };
 
 // One kind's stacked tensors, as the kernels see them.

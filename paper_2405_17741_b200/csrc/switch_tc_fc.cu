@@ -120,6 +120,7 @@ struct TcPlan {
   int32_t chunk = 48;
   int32_t probe = 0;          // tuning builds only (tc_probe=1): W stream alone, W written back unchanged
   int32_t fused_probe = 0;    // tuning builds only (fc_fused_probe)
+  int32_t fused_adapt = 1;    // option fc_adapt: adaptive split of the fused decode's segments
   uint32_t* trace = nullptr;  // tuning builds only (trace_buf: device buffer of kTraceCtas * kTraceTiles * 8 u32)
   uint32_t* seg_trace = nullptr;  // tuning builds only (seg_trace_buf: grid * 512 * 2 u32)
   void* packed_At[LSW_NKIND] = {};
@@ -147,6 +148,7 @@ struct Args {
   unsigned long long* seg_done;   // [n_seg], zeroed before the launch
   uint32_t* trace;                // tuning builds only (option trace_buf): per-tile role timestamps
   uint32_t* seg_trace;            // tuning builds only (option seg_trace_buf): [CTA][segment][2] publish / wait-done
+  int32_t adapt;                  // fused: adaptive split of the segments (DevState fused_w)
 };
 
 // Tuning builds only: %globaltimer (low 32 bits, ns) of pipeline events for the
@@ -232,7 +234,10 @@ __device__ __forceinline__ void fused_at(const TileKinds& g, const Args& a, FCur
 __device__ __forceinline__ void fused_from(const TileKinds& g, const TileSeq& q, const Args& a, FCursor& c, int seg) {
   for (; seg < a.n_seg; ++seg) {
     const FusedSeg& S = a.segs[seg];
-    const int64_t lo = S.tile_count * q.b / q.G, hi = S.tile_count * (q.b + 1) / q.G;
+    // uniform, or the adaptive split: boundaries from the cumulative weights
+    // (the same value bounds both neighbours: the ranges tile the segment)
+    const int64_t lo = q.adapt ? (int64_t)(((uint64_t)S.tile_count * q.wlo) >> 24) : S.tile_count * q.b / q.G;
+    const int64_t hi = q.adapt ? (int64_t)(((uint64_t)S.tile_count * q.whi) >> 24) : S.tile_count * (q.b + 1) / q.G;
     if (lo < hi) { fused_at(g, a, c, seg, S.tile_begin + lo, S.tile_begin + hi); return; }
   }
   c.t = -1;
@@ -492,6 +497,9 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ Coefs cf;
   __shared__ int32_t s_parity;
+  __shared__ unsigned long long s_fz_t0, s_fz_proc;   // fused: this CTA's segment processing time
+  __shared__ uint32_t s_fz_n;                          //        and tiles (adaptive split)
+  __shared__ int32_t s_fz_last;
   __shared__ uint32_t s_tmem_base;
   __shared__ __align__(8) uint64_t bar_wfull[kMaxStages], bar_wempty[kMaxStages], bar_wdone[kMaxStages];
   __shared__ __align__(8) uint64_t bar_afull[kMaxAStages], bar_aempty[kMaxAStages];
@@ -521,6 +529,9 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
     p.state = args.state;
     const int32_t parity = *(volatile int32_t*)&args.state->parity;
     s_parity = parity;
+    s_fz_t0 = globaltimer();
+    s_fz_proc = 0;
+    s_fz_n = 0;
     build_coefs(p, parity, cf);
     if (blockIdx.x == 0 && !cf.bad) stage_decision(p, parity);
     for (int s = 0; s < g.w_stages; ++s) {
@@ -573,6 +584,17 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
   seq.chunk = args.chunk < 1 ? 1 : args.chunk;
   seq.G = kPair ? gridDim.x / 2 : gridDim.x;      // pair: both CTAs of a cluster walk the same pair tiles
   seq.b = kPair ? blockIdx.x / 2 : blockIdx.x;
+  seq.adapt = 0;
+  seq.wlo = seq.whi = 0;
+  if constexpr (kF) {
+    // adaptive split (written by the previous fused pass's last CTA; stream-ordered)
+    if (args.adapt && gridDim.x <= kFusedMaxCtas &&
+        *reinterpret_cast<volatile const int32_t*>(&args.state->fused_w_valid) == (int32_t)gridDim.x) {
+      seq.adapt = 1;
+      seq.wlo = args.state->fused_w[blockIdx.x];
+      seq.whi = args.state->fused_w[blockIdx.x + 1];
+    }
+  }
   const TileKinds& tk = kPair ? g.tkp : g.tk;
   // pair: this CTA's 128-row tile of the pair tile's 256 rows
   auto rbr = [&](int rb) { return kPair ? 2 * rb + (int)crank : rb; };
@@ -968,18 +990,27 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       Ring acc{0, 0, (uint32_t)g.acc_bufs};
       Ring aring{0, 0, (uint32_t)g.a_stages};
       int ne_tr = 0;
+#ifdef LSW_TUNING
+      if (kF && releaser && args.seg_trace) {     // slot 511: this CTA's SM (per-SM lateness analysis)
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        args.seg_trace[((size_t)blockIdx.x * 512 + 511) * 2 + 0] = smid + 1;
+      }
+#endif
       int cur_seg = -1;                            // fused: segment of the previous tile
       int conv_next = 0;                           // fused: first segment whose outputs this CTA has not converted
       unsigned long long seg_mine = 0;             // fused: tiles of cur_seg this CTA finished
-      // fused: this thread's partial output of one row, summed in fp32 over the
-      // consecutive column tiles of a strip (a CTA's range walks cb fastest)
-      // and added to the fixed-point accumulator once per strip, not per tile
-      float y_run = 0.f;
+      // fused: this thread's partial output of one row over the consecutive
+      // column tiles of a strip (a CTA's range walks cb fastest), added to the
+      // fixed-point accumulator once per strip, not per tile
+      long long y_run = 0;                         // 2^-40 units: each tile's fp32 partial converted, then
+                                                   // integer adds -- independent of how a strip's tiles are
+                                                   // split among CTAs (the adaptive split moves them)
       int64_t y_at = -1;                           // ys_fx index y_run belongs to (-1: none)
       auto y_flush = [&]() {
-        if (y_at >= 0) atomicAdd(args.ys_fx + y_at, (unsigned long long)__double2ll_rn((double)y_run * kFx));
+        if (y_at >= 0) atomicAdd(args.ys_fx + y_at, (unsigned long long)y_run);
         y_at = -1;
-        y_run = 0.f;
+        y_run = 0;
       };
       // tb: the strips are folded into TMEM here, in walk order, as many ahead as
       // there are TMEM buffers (buffer f % b_bufs for the f-th fold): the first
@@ -1035,6 +1066,8 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
               asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(args.seg_done + cur_seg),
                            "l"(seg_mine) : "memory");
               FC_SEG_TRACE(cur_seg, 0);
+              s_fz_proc += globaltimer() - s_fz_t0;
+              s_fz_n += (uint32_t)seg_mine;
             }
             // every earlier segment complete (decoder order), then this CTA's
             // slice of its outputs converted from fixed point
@@ -1048,6 +1081,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             }
             __syncwarp();
             asm volatile("bar.sync 3, %0;" ::"r"(32 * kEpiWarps) : "memory");
+            if (releaser) s_fz_t0 = globaltimer();    // the segment's processing starts
             cur_seg = c.seg;
             seg_mine = 0;
           }
@@ -1175,7 +1209,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
           for (int q = 0; q < 4; ++q) y2 = dot16(o[q], xv[2 * q], xv[2 * q + 1], y2);
           float ylo, yhi;
           asm("mov.b64 {%0, %1}, %2;" : "=f"(ylo), "=f"(yhi) : "l"(y2));
-          y_run += ylo + yhi;
+          y_run += __double2ll_rn((double)(ylo + yhi) * kFx);
           continue;
         }
 #pragma unroll
@@ -1197,8 +1231,12 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
             __threadfence();
             asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(args.seg_done + cur_seg),
                          "l"(seg_mine) : "memory");
+            s_fz_proc += globaltimer() - s_fz_t0;
+            s_fz_n += (uint32_t)seg_mine;
           }
         }
+        if (releaser && args.adapt && blockIdx.x < kFusedMaxCtas)
+          args.state->fused_perf[blockIdx.x] = s_fz_n ? (float)((double)s_fz_proc / s_fz_n) : 0.f;
         for (; conv_next < args.n_seg; ++conv_next) {   // the remaining segments' outputs
           if (releaser && !(args.probe & 4))
             wait_count(&args.seg_done[conv_next], (unsigned long long)args.segs[conv_next].tile_count);
@@ -1220,6 +1258,59 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
     else
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAccBufs * kTN)
                    : "memory");
+  }
+  if constexpr (kF) {
+    // adaptive split: the pass's last CTA weighs every CTA by its measured
+    // speed (1 / ns per tile), half-and-half with the current split, each
+    // weight within [1/2, 2] of uniform; the cumulative bounds (2^-24 units,
+    // 0 and 2^24 at the ends) are the next pass's ranges.  Results do not
+    // depend on the split (tiles are independent; y is fixed-point).
+    if (args.adapt && gridDim.x <= kFusedMaxCtas) {
+      DevState* st = args.state;
+      const int G = (int)gridDim.x;
+      if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(&st->fused_done, 1u);
+        s_fz_last = prev == (uint32_t)G - 1;
+      }
+      __syncthreads();
+      if (s_fz_last) {
+        __threadfence();
+        float* wsh = reinterpret_cast<float*>(smem_raw);   // the stages are idle now
+        for (int b = threadIdx.x; b < G; b += blockDim.x) {
+          const float pf = *reinterpret_cast<volatile const float*>(&st->fused_perf[b]);
+          wsh[b] = pf > 0.f ? 1.f / pf : 0.f;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const bool valid = *reinterpret_cast<volatile const int32_t*>(&st->fused_w_valid) == G;
+          float spd_sum = 0.f;
+          int n_ok = 0;
+          for (int b = 0; b < G; ++b)
+            if (wsh[b] > 0.f) { spd_sum += wsh[b]; ++n_ok; }
+          const float mean = n_ok ? spd_sum / n_ok : 1.f;
+          float tot = 0.f;
+          for (int b = 0; b < G; ++b) {
+            const float meas = (wsh[b] > 0.f ? wsh[b] : mean) / (mean * G);          // measured share
+            const float old = valid ? (float)(st->fused_w[b + 1] - st->fused_w[b]) * (1.f / 16777216.f)
+                                    : 1.f / G;
+            float w = 0.5f * old + 0.5f * meas;
+            w = fminf(fmaxf(w, 0.5f / G), 2.f / G);
+            wsh[b] = w;
+            tot += w;
+          }
+          float run = 0.f;
+          st->fused_w[0] = 0;
+          for (int b = 0; b < G; ++b) {
+            run += wsh[b];
+            st->fused_w[b + 1] = b + 1 == G ? 16777216u : (uint32_t)fminf(run / tot * 16777216.f, 16777216.f);
+          }
+          st->fused_w_valid = G;
+          st->fused_done = 0;
+          __threadfence();
+        }
+      }
+    }
   }
   if (threadIdx.x == 0) {
     SwitchParams p{};
@@ -1462,7 +1553,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   { const char* v = opt_str("trace_buf"); plan->trace = v ? reinterpret_cast<uint32_t*>(strtoull(v, nullptr, 10)) : nullptr; }
   { const char* v = opt_str("seg_trace_buf"); plan->seg_trace = v ? reinterpret_cast<uint32_t*>(strtoull(v, nullptr, 10)) : nullptr; }
 #endif
-  plan->fused_probe = (int)probe_int("fc_fused_probe") & 29;   // tuning builds only: 1 W stream only, 4 no segment wait, 8 no GEMV, 16 no fold math
+  plan->fused_probe = (int)probe_int("fc_fused_probe") & 29;
+  plan->fused_adapt = opt_int("fc_adapt", 1) != 0;   // tuning builds only: 1 W stream only, 4 no segment wait, 8 no GEMV, 16 no fold math
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
   // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
   g.wrm = opt_int("fc_wrm", 1) != 0;
@@ -1712,6 +1804,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   a.seg_done = plan->d_seg_done;
   a.trace = plan->trace;
   a.seg_trace = plan->seg_trace;
+  a.adapt = plan->fused_adapt;
   switch_fc_kernel<true, false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   return cudaGetLastError();
 }

@@ -224,6 +224,8 @@ struct Cursor {
 struct TileSeq {
   int64_t T, t0;         // T tiles of this launch, starting at global tile t0
   int32_t chunk, G, b;
+  uint32_t wlo, whi;     // fused decode, adaptive split: this CTA's range bounds (2^-24 units of a segment)
+  int32_t adapt;         // 0: uniform split
 };
 
 struct TileKinds {
