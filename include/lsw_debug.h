@@ -22,6 +22,10 @@ extern "C" {
  *   tc_pair        0 | 1  the fold mode on CTA pairs (cta_group::2, M = 256;
  *                         each CTA stages half of the A^T columns)     [0]
  *   tc_chunk       N      tiles per CTA chunk of the sweep order     [48]
+ *   fc_dyn         0|1    sweep chunks claimed at run time (1) or      [1]
+ *                         dealt c -> CTA c mod G (0)
+ *   fc_adapt       0|1    fused decode: segments split by measured CTA  [1]
+ *                         speed (1) or evenly (0)
  *   fc_stages / fc_astages / fc_bbufs   explicit shared-memory plan (all three)
  *   fc_wrm         0 | 1  W tile moved by one 4-D TMA op             [1]
  *   gemv           ldg    the warp-per-row LDG GEMV instead of the bulk ring

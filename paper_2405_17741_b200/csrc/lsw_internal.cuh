@@ -48,6 +48,7 @@ struct DevState {
   // of T tiles, [T * fused_w[b], T * fused_w[b + 1]) >> 24; fused_perf[b] its
   // last pass's ns per tile (segment processing only, waits excluded); the
   // pass's last CTA turns them into the next pass's split
+  uint32_t sweep_next;            // plain sweep, dynamic chunks: chunks claimed in this pass (the last CTA resets)
   int32_t fused_w_valid;          // 0: uniform split (b / G)
   uint32_t fused_done;            // CTAs done with the pass (the last one updates and resets)
   uint32_t fused_w[kFusedMaxCtas + 1];
@@ -148,6 +149,7 @@ __device__ __forceinline__ void finish_pass(const SwitchParams& p, int32_t parit
       s->merged = 0;                             // state none: the slot is stale
     }
     p.state->done = 0;
+    p.state->sweep_next = 0;                       // every CTA has run out of chunks
     __threadfence();
   }
 }

@@ -121,6 +121,7 @@ struct TcPlan {
   int32_t probe = 0;          // tuning builds only (tc_probe=1): W stream alone, W written back unchanged
   int32_t fused_probe = 0;    // tuning builds only (fc_fused_probe)
   int32_t fused_adapt = 1;    // option fc_adapt: adaptive split of the fused decode's segments
+  int32_t sweep_dyn = 1;      // option fc_dyn: plain sweep's chunks claimed dynamically
   uint32_t* trace = nullptr;  // tuning builds only (trace_buf: device buffer of kTraceCtas * kTraceTiles * 8 u32)
   uint32_t* seg_trace = nullptr;  // tuning builds only (seg_trace_buf: grid * 512 * 2 u32)
   void* packed_At[LSW_NKIND] = {};
@@ -149,6 +150,7 @@ struct Args {
   uint32_t* trace;                // tuning builds only (option trace_buf): per-tile role timestamps
   uint32_t* seg_trace;            // tuning builds only (option seg_trace_buf): [CTA][segment][2] publish / wait-done
   int32_t adapt;                  // fused: adaptive split of the segments (DevState fused_w)
+  int32_t dyn;                    // plain sweep: chunks claimed from a device counter
 };
 
 // Tuning builds only: %globaltimer (low 32 bits, ns) of pipeline events for the
@@ -500,6 +502,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
   __shared__ unsigned long long s_fz_t0, s_fz_proc;   // fused: this CTA's segment processing time
   __shared__ uint32_t s_fz_n;                          //        and tiles (adaptive split)
   __shared__ int32_t s_fz_last;
+  __shared__ int32_t s_claim[2 + 16];            // plain sweep, dynamic chunks: [claimed, claimer, id[16]]
   __shared__ uint32_t s_tmem_base;
   __shared__ __align__(8) uint64_t bar_wfull[kMaxStages], bar_wempty[kMaxStages], bar_wdone[kMaxStages];
   __shared__ __align__(8) uint64_t bar_afull[kMaxAStages], bar_aempty[kMaxAStages];
@@ -532,6 +535,8 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
     s_fz_t0 = globaltimer();
     s_fz_proc = 0;
     s_fz_n = 0;
+    s_claim[0] = 0;
+    s_claim[1] = 0;
     build_coefs(p, parity, cf);
     if (blockIdx.x == 0 && !cf.bad) stage_decision(p, parity);
     for (int s = 0; s < g.w_stages; ++s) {
@@ -586,6 +591,9 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
   seq.b = kPair ? blockIdx.x / 2 : blockIdx.x;
   seq.adapt = 0;
   seq.wlo = seq.whi = 0;
+  seq.dyn = !kF && !kPair && args.dyn && seq.chunk >= 2;
+  seq.ctr = &args.state->sweep_next;
+  seq.ring = s_claim;
   if constexpr (kF) {
     // adaptive split (written by the previous fused pass's last CTA; stream-ordered)
     if (args.adapt && gridDim.x <= kFusedMaxCtas &&
@@ -1312,6 +1320,14 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
       }
     }
   }
+#ifdef LSW_TUNING
+  if (threadIdx.x == 0 && args.seg_trace) {      // slot 510: this CTA's end time and SM (tail analysis)
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    args.seg_trace[((size_t)blockIdx.x * 512 + 510) * 2 + 0] = (uint32_t)globaltimer();
+    args.seg_trace[((size_t)blockIdx.x * 512 + 510) * 2 + 1] = smid + 1;
+  }
+#endif
   if (threadIdx.x == 0) {
     SwitchParams p{};
     p.mode = args.mode;
@@ -1554,7 +1570,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   { const char* v = opt_str("seg_trace_buf"); plan->seg_trace = v ? reinterpret_cast<uint32_t*>(strtoull(v, nullptr, 10)) : nullptr; }
 #endif
   plan->fused_probe = (int)probe_int("fc_fused_probe") & 29;
-  plan->fused_adapt = opt_int("fc_adapt", 1) != 0;   // tuning builds only: 1 W stream only, 4 no segment wait, 8 no GEMV, 16 no fold math
+  plan->fused_adapt = opt_int("fc_adapt", 1) != 0;
+  plan->sweep_dyn = opt_int("fc_dyn", 1) != 0;   // tuning builds only: 1 W stream only, 4 no segment wait, 8 no GEMV, 16 no fold math
   // measured (7B, same box, 3 pairs): W-stream probe 0.865 -> 0.878 of the copy
   // peak, full kernel +0.3-1.5 % with the conflict-free epilogue order
   g.wrm = opt_int("fc_wrm", 1) != 0;
@@ -1710,6 +1727,8 @@ cudaError_t launch_switch_tc(const TcPlan* plan, const SwitchParams& p, cudaStre
   a.seg_done = nullptr;
   a.trace = plan->trace;
   a.seg_trace = plan->seg_trace;
+  a.dyn = plan->sweep_dyn;
+  a.adapt = 0;
   if (plan->geom.pt) {
     switch_fc_kernel<false, true><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   } else if (plan->geom.tb) {
@@ -1805,6 +1824,7 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   a.trace = plan->trace;
   a.seg_trace = plan->seg_trace;
   a.adapt = plan->fused_adapt;
+  a.dyn = 0;
   switch_fc_kernel<true, false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
   return cudaGetLastError();
 }

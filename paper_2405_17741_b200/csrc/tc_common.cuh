@@ -219,6 +219,7 @@ struct Cursor {
   int64_t t;             // global tile index, -1 when done
   int32_t kd, layer, rb, cb;
   int32_t left;          // tiles of the current chunk after this one (no per-tile division)
+  int32_t k;             // dynamic chunks: ordinal of the current chunk in this CTA's walk
 };
 
 struct TileSeq {
@@ -226,6 +227,13 @@ struct TileSeq {
   int32_t chunk, G, b;
   uint32_t wlo, whi;     // fused decode, adaptive split: this CTA's range bounds (2^-24 units of a segment)
   int32_t adapt;         // 0: uniform split
+  // plain sweep, dynamic chunks (dyn): chunk n -> the CTA that claims it from
+  // the device counter ctr (in claim order, so the CTAs still sweep about one
+  // region at a time, and a faster SM takes more chunks); ring = this CTA's
+  // shared [claimed, claimer, id[16]]: every role reads its k-th chunk from it
+  int32_t dyn;
+  uint32_t* ctr;
+  int32_t* ring;
 };
 
 struct TileKinds {
@@ -251,15 +259,39 @@ __device__ __forceinline__ void cursor_set(const TileKinds& g, Cursor& c, int64_
 // start of chunk number n of the launch: its first tile and length
 __device__ __forceinline__ void cursor_chunk(const TileKinds& g, const TileSeq& q, Cursor& c, int64_t n) {
   const int64_t r0 = n * q.chunk;
-  if (r0 >= q.T) { c.t = -1; return; }
+  if (n < 0 || r0 >= q.T) { c.t = -1; return; }
   const int64_t len = q.T - r0 < q.chunk ? q.T - r0 : q.chunk;
   cursor_set(g, c, q.t0 + r0);
   c.left = (int32_t)len - 1;
 }
 
+// dynamic chunks: the chunk of ordinal k of this CTA's walk (-1: none left).
+// The first role of the CTA to need ordinal k claims it (election on
+// ring[1]); the others wait for it (ring[0] > k).  Ring slot k & 15 is reused
+// 16 chunks later -- the CTA's roles run within ~12 tiles of each other (their
+// stage rings), and dyn needs chunks of >= 2 tiles.
+__device__ __forceinline__ int64_t seq_claim(const TileSeq& q, int32_t k) {
+  int32_t* claimed = q.ring;
+  int32_t* claimer = q.ring + 1;
+  volatile int32_t* ids = q.ring + 2;
+  for (;;) {
+    int32_t cl;
+    asm volatile("ld.acquire.cta.b32 %0, [%1];" : "=r"(cl) : "l"(claimed) : "memory");
+    if (cl > k) return ids[k & 15];
+    if (atomicCAS(claimer, k, k + 1) == k) {
+      const uint32_t id = atomicAdd(q.ctr, 1u);
+      const int64_t n_chunks = (q.T + q.chunk - 1) / q.chunk;
+      ids[k & 15] = (int64_t)id < n_chunks ? (int32_t)id : -1;
+      asm volatile("st.release.cta.b32 [%0], %1;" ::"l"(claimed), "r"(k + 1) : "memory");
+      return ids[k & 15];
+    }
+  }
+}
+
 __device__ __forceinline__ Cursor cursor_first(const TileKinds& g, const TileSeq& q) {
   Cursor c;
-  cursor_chunk(g, q, c, q.b);
+  c.k = 0;
+  cursor_chunk(g, q, c, q.dyn ? seq_claim(q, 0) : q.b);
   return c;
 }
 
@@ -276,7 +308,12 @@ __device__ __forceinline__ void cursor_next(const TileKinds& g, const TileSeq& q
     }
     return;
   }
-  cursor_chunk(g, q, c, (c.t - q.t0) / q.chunk + q.G);     // once per chunk
+  if (q.dyn) {
+    ++c.k;
+    cursor_chunk(g, q, c, seq_claim(q, c.k));
+  } else {
+    cursor_chunk(g, q, c, (c.t - q.t0) / q.chunk + q.G);   // once per chunk
+  }
 }
 
 __device__ __forceinline__ int64_t strip_id(const Cursor& c) { return c.t - c.cb; }
