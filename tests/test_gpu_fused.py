@@ -124,13 +124,17 @@ def test_fused_and_plain_tokens_alternate_on_one_ctx():
                     yo += d_out
 
 
+@pytest.mark.parametrize("adapt", [None, "0"])
 @pytest.mark.parametrize("name,grid", [("mini", None), ("mini", "3"), ("mini-r32", None)])
-def test_fused_outputs_are_bitwise_reproducible(lsw_opts, name, grid):
+def test_fused_outputs_are_bitwise_reproducible(lsw_opts, name, grid, adapt):
     """The fc fused launch accumulates each row's per-tile contributions in
     64-bit fixed point (integer adds commute), so two runs on identical inputs
     give bitwise-identical outputs whatever order the tiles finish in
-    (SURVEY §8c.5 item 5), not only bitwise-identical weights."""
-    lsw_opts(tc_kernel="fold", tc_grid=grid)
+    (SURVEY §8c.5 item 5), not only bitwise-identical weights -- also under the
+    adaptive split (default), which moves tiles between CTAs from pass to
+    pass by measured speed (each tile's partial is converted to fixed point
+    before any sum), and with the even split (adapt "0")."""
+    lsw_opts(tc_kernel="fold", tc_grid=grid, fc_adapt=adapt)
     cfg = synth.get_config(name)
     X1 = synth.gen_x1(cfg, 3, "cuda")
     xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda"))

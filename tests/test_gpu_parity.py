@@ -120,7 +120,11 @@ TC_VARIANTS = [("fold", {}), ("fold", {"fc_stages": 3, "fc_astages": 2, "fc_bbuf
                ("fold", {"tc_pair": 1, "tc_tb": 0}), ("fold", {"tc_pair": 1, "fc_wrm": 0, "tc_tb": 0}),
                ("fold", {"tc_pair": 0}), ("fold", {"tc_tb": 0}), ("fold", {"tc_tb": 1}),
                ("fold", {"tc_tb": 1, "fc_wrm": 0}), ("fold", {"tc_tb": 1, "fc_astages": 2}),
-               ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1}), ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1, "fc_astages": 2})]
+               ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1}), ("fold", {"tc_tb": 1, "tc_tb_bbufs": 1, "fc_astages": 2}),
+               # the static chunk deal (c -> CTA c mod G) instead of run-time claims
+               ("fold", {"fc_dyn": 0}), ("pt", {"fc_dyn": 0}), ("bu", {"fc_dyn": 0}),
+               # run-time claims of 2-tile chunks: every ring wraps, claims 16 apart reuse a slot
+               ("fold", {"tc_chunk": 2}), ("pt", {"tc_chunk": 2})]
 KERNEL_ID = {"fold": (3, 6, 7), "pt": (4,), "bu": (5,)}
 
 
