@@ -16,6 +16,13 @@
 
 namespace lsw {
 
+#ifdef LSW_TUNING
+// tuning builds: per-CTA end time and SM of the last merged-GEMV launch
+// (lsw_debug option gemv_trace_buf: device u32 [2][256])
+__device__ uint32_t* g_gemv_trace = nullptr;
+void gemv_set_trace(uint32_t* p) { cudaMemcpyToSymbol(g_gemv_trace, &p, sizeof(p)); }
+#endif
+
 constexpr int kGemvThreads = 512;
 constexpr int kGemvUnroll = 8;        // independent 16-B loads in flight per lane
 
@@ -619,6 +626,18 @@ gemv_bulk_kernel(const GemvParams p, int32_t slots, int32_t R, int32_t early_w, 
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[s])) : "memory");
   }
+#ifdef LSW_TUNING
+  if (!kLora && g_gemv_trace) {
+    __syncwarp();
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kBulkConsumers) : "memory");
+    if (cw == 0 && lane == 0 && blockIdx.x < 256) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_gemv_trace[blockIdx.x] = (uint32_t)g_globaltimer();
+      g_gemv_trace[256 + blockIdx.x] = smid + 1;
+    }
+  }
+#endif
   if (kLora) {
     // Eq. 2: y = (W x) + LoRA-up term, one rounding of the sum per row
     __syncwarp();

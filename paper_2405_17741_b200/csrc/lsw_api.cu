@@ -152,6 +152,9 @@ struct lsw_ctx {
   std::vector<cudaEvent_t> st_ev;       // [0]: xs landed; [1 + l]: layer l's outputs final
 };
 
+#ifdef LSW_TUNING
+namespace lsw { void gemv_set_trace(uint32_t* p); }
+#endif
 static size_t esize(const lsw_ctx* c) { return c->cfg.dtype == LSW_BF16 ? 2 : 4; }
 
 static void fill_switch_params(const lsw_ctx* c, SwitchParams& p, int tm, int tn) {
@@ -244,6 +247,9 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
   { const char* v = opt_str("gemv"); ctx->gemv.ldg = v && strcmp(v, "ldg") == 0; }
   { const long v = opt_int("gemv_split", 1); ctx->gemv.split_rows = v < 0 || v > 2 ? 1 : (int)v; }
   ctx->gemv.probe = (int)probe_int("gemv_probe");
+#ifdef LSW_TUNING
+  { const char* v = opt_str("gemv_trace_buf"); if (v) gemv_set_trace(reinterpret_cast<uint32_t*>(strtoull(v, nullptr, 10))); }
+#endif
   ctx->unmerged_flags = (int)probe_int("unmerged_flags");
   e = cudaMalloc(&ctx->d_state, sizeof(DevState));
   if (e != cudaSuccess) { delete ctx; return fail(LSW_E_OOM, "lsw_create: cudaMalloc(state) failed"); }
