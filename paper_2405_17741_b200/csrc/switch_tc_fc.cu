@@ -121,6 +121,8 @@ struct TcPlan {
   int32_t probe = 0;          // tuning builds only (tc_probe=1): W stream alone, W written back unchanged
   int32_t fused_probe = 0;    // tuning builds only (fc_fused_probe)
   int32_t fused_adapt = 1;    // option fc_adapt: adaptive split of the fused decode's segments
+  int32_t fw_stages = 0, fa_stages = 0, fb_bufs = 0;   // the fused decode's shared-memory plan (W 3 first)
+  uint32_t fsmem_bytes = 0;
   int32_t sweep_dyn = 1;      // option fc_dyn: plain sweep's chunks claimed dynamically
   uint32_t* trace = nullptr;  // tuning builds only (trace_buf: device buffer of kTraceCtas * kTraceTiles * 8 u32)
   uint32_t* seg_trace = nullptr;  // tuning builds only (seg_trace_buf: grid * 512 * 2 u32)
@@ -508,7 +510,7 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
   __shared__ __align__(8) uint64_t bar_afull[kMaxAStages], bar_aempty[kMaxAStages];
   __shared__ __align__(8) uint64_t bar_braw[2], bar_bfull[2], bar_bempty[2];
   __shared__ __align__(8) uint64_t bar_accfull[kAccBufs], bar_accempty[kAccBufs];
-  __shared__ __align__(8) uint64_t bar_apeer[kMaxAStages], bar_bpeer[2];   // pair: the follower's stages landed
+  __shared__ __align__(8) uint64_t bar_bpeer[2];   // pair: the follower's B strip folded
   __shared__ __align__(8) uint64_t bar_rawfull, bar_rawempty;                // tb: the raw B strip copy
 
   const Geom& g = args.g;
@@ -547,7 +549,6 @@ switch_fc_kernel(const __grid_constant__ Maps maps, const __grid_constant__ Args
     for (int s = 0; s < g.a_stages; ++s) {
       mbar_init(smem_u32(&bar_afull[s]), 1);
       mbar_init(smem_u32(&bar_aempty[s]), 1);
-      mbar_init(smem_u32(&bar_apeer[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&bar_braw[s]), 1);
@@ -1439,7 +1440,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   // (measured, 7B shape: W 3 + B 2 + A 3 0.895 of the copy peak vs W 4 + B 1 +
   // A 3 0.868 -- a single B buffer drains the MMA pipeline at every strip
   // change, a 4th W stage buys nothing); what is left goes to more W stages.
-  auto make_plan = [&](uint32_t asb) -> bool {
+  auto make_plan = [&](uint32_t asb, bool w3_first = false) -> bool {
     const int64_t budget = 227 * 1024 - 1024 /*align*/ - 2048 /*static*/;
     // A ring depth in units per tile u (fold: the whole tile's slices; per-term:
     // one unit per kPtGroup terms).  Candidates (W stages, B buffers) in order of
@@ -1451,8 +1452,15 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     // the last resort (measured, 16-layer 7B shape: W 2 costs 7-15 %; W 3 + B 1
     // + A 3 0.860 vs W 4 + B 1 + A 2 0.846 at k = 3; per-term r = 32 k = 3:
     // W 3 + B 1 + A 5 0.656 vs W 3 + B 2 + A 2 0.626).
+    // Fold mode with run-time chunk claims (r02): four W stages and one B
+    // buffer first -- W 4 + B 1 + A 4 vs W 3 + B 2 + A 4, same box: 7B 0.930
+    // vs 0.918 of the copy peak, Mistral 0.932 vs 0.918, r = 8 k = 2 0.926 vs
+    // 0.914, r = 4 k = 1 0.937 vs 0.924 (the static deal preferred W 3, see
+    // above: its tail hid the difference)
     struct Cand { int ws, bb; };
-    const Cand cands[] = {{3, 2}, {3, 1}, {4, 2}, {4, 1}};
+    const Cand cands_pt[] = {{3, 2}, {3, 1}, {4, 2}, {4, 1}};
+    const Cand cands_fold[] = {{4, 1}, {3, 2}, {3, 1}, {4, 2}};
+    const Cand* cands = g.pt || w3_first ? cands_pt : cands_fold;
     const int u = g.pt ? (mt + kPtGroup - 1) / kPtGroup : 1;
     const int bb_min = g.bu ? 0 : 1;           // bu: no strip buffer
     if (bb_opt >= bb_min && bb_opt <= 2 && as_opt >= 2 && as_opt <= kMaxAStages && ws_opt >= 2 &&
@@ -1465,7 +1473,8 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
     }
     for (int pass = 0; pass < 3; ++pass) {
       const int a_min = pass == 0 ? 2 * u + 1 : pass == 1 ? u + 1 : 2;
-      for (const Cand& c : cands) {
+      for (int ci = 0; ci < 4; ++ci) {
+        const Cand& c = cands[ci];
         const int bb = g.bu ? 0 : c.bb;
         const int64_t rest = budget - (int64_t)c.ws * w_stage - (int64_t)bb * g.b_buf_bytes;
         if (rest < 0) continue;
@@ -1578,6 +1587,18 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
   for (int k = 0; k < LSW_NKIND; ++k) if (sp.kind[k].d_in % 64) g.wrm = 0;   // ragged TP shards: 3-D boxes
   g.smem_bytes = g.w_stages * w_stage + g.a_stages * g.a_stage_bytes + (g.tb ? g.raw_bytes : g.b_bufs * g.b_buf_bytes) +
                  1024;
+  // the fused decode keeps three W stages first (measured, 7B, same box: W 3
+  // + B 2 + A 4 5.74-5.77 vs W 4 + B 1 + A 4 5.84 ms per token)
+  if (!g.pt && !g.tb && !g.pair) {
+    const Geom keep = g;
+    if (make_plan(g.a_stage_bytes, true)) {
+      plan->fw_stages = g.w_stages;
+      plan->fa_stages = g.a_stages;
+      plan->fb_bufs = g.b_bufs;
+      plan->fsmem_bytes = g.w_stages * w_stage + g.a_stages * g.a_stage_bytes + g.b_bufs * g.b_buf_bytes + 1024;
+    }
+    g = keep;
+  }
   // tiles
   int64_t t = 0;
   for (int k = 0; k < LSW_NKIND; ++k) {
@@ -1646,7 +1667,7 @@ cudaError_t tc_plan_create(TcPlan** out, const SwitchParams& sp, int num_sms, co
                              (int)g.smem_bytes);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(switch_fc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)g.smem_bytes);
+                             (int)(plan->fsmem_bytes > g.smem_bytes ? plan->fsmem_bytes : g.smem_bytes));
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(switch_fc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)g.smem_bytes);
@@ -1825,7 +1846,14 @@ cudaError_t launch_switch_tc_fused(const TcPlan* plan, const SwitchParams& p, cu
   a.seg_trace = plan->seg_trace;
   a.adapt = plan->fused_adapt;
   a.dyn = 0;
-  switch_fc_kernel<true, false><<<plan->grid, kThreads, plan->geom.smem_bytes, s>>>(plan->maps, a);
+  uint32_t smem = plan->geom.smem_bytes;
+  if (plan->fsmem_bytes) {                        // the fused decode's own stage plan (W 3 first)
+    a.g.w_stages = plan->fw_stages;
+    a.g.a_stages = plan->fa_stages;
+    a.g.b_bufs = plan->fb_bufs;
+    smem = plan->fsmem_bytes;
+  }
+  switch_fc_kernel<true, false><<<plan->grid, kThreads, smem, s>>>(plan->maps, a);
   return cudaGetLastError();
 }
 
