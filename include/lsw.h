@@ -351,7 +351,11 @@ LSW_API lsw_status lsw_decode_token_fused(lsw_ctx* ctx, const void* x1, const vo
  * `stream` (and a ctx-owned side stream).  The copies overlap the token: xs
  * travels on the side stream while the router and the switch run, and each
  * layer's outputs return as soon as that layer's GEMVs are done.  Host buffers
- * should be pinned for asynchronous copies. */
+ * should be pinned for asynchronous copies.  From the second call on, the
+ * token is replayed as ONE CUDA graph (captured on a ctx-owned stream, one per
+ * state of the decision slot: merge / switch; captured again when any of the
+ * five host pointers changes), so the host adds one launch per token; results
+ * are bitwise those of the eager path (variant option host_graph=0). */
 LSW_API lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_h, float* ys_h,
                                  int32_t* idx_h, float* gate_h, void* stream);
 

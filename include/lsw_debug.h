@@ -34,6 +34,7 @@ extern "C" {
  *   gemv_smem_kb   N      ring budget, KB                             [176 / 208]
  *   gemv_split     0|1|2  rows over 24 KB reduced by two warps (1);    [1]
  *                         never (0); every row (2, tests)
+ *   host_graph     0|1    lsw_decode_token_host replayed as a CUDA graph [1]
  *   nccl_path      file   libnccl.so.2 to dlopen when none is loaded yet
  *                         (read at the first NCCL call, lsw_nccl_version)
  * Probes (deliberately WRONG results; only in a build with -DLSW_TUNING,

@@ -149,7 +149,18 @@ struct lsw_ctx {
   int64_t prefill_u_elems = 0;
   void* prefill_z = nullptr;            // lsw_prefill_group (tc): (hi, lo) LoRA-up operand scratch
   int64_t prefill_z_elems = 0;
-  std::vector<cudaEvent_t> st_ev;       // [0]: xs landed; [1 + l]: layer l's outputs final
+  std::vector<cudaEvent_t> st_ev;       // [0]: xs landed; [1 + l]: layer l's outputs final, [1 + L]: side joined
+  // lsw_decode_token_host as a CUDA graph (option host_graph, default 1): one
+  // per state (first token: merge; later: switch), captured on the second call
+  // with the same host buffers, replayed on the caller's stream
+  struct HostGraph {
+    cudaGraphExec_t exec = nullptr;
+    const void* key[5] = {};
+    uint64_t launches = 0;
+  } hgraph[2];
+  cudaStream_t st_cap = nullptr;
+  bool host_graph = true;
+  uint64_t host_calls = 0;
 };
 
 #ifdef LSW_TUNING
@@ -247,6 +258,7 @@ lsw_status lsw_create(const lsw_config* cfg, const lsw_kind_desc kinds[LSW_NKIND
   { const char* v = opt_str("gemv"); ctx->gemv.ldg = v && strcmp(v, "ldg") == 0; }
   { const long v = opt_int("gemv_split", 1); ctx->gemv.split_rows = v < 0 || v > 2 ? 1 : (int)v; }
   ctx->gemv.probe = (int)probe_int("gemv_probe");
+  ctx->host_graph = opt_int("host_graph", 1) != 0;
 #ifdef LSW_TUNING
   { const char* v = opt_str("gemv_trace_buf"); if (v) gemv_set_trace(reinterpret_cast<uint32_t*>(strtoull(v, nullptr, 10))); }
 #endif
@@ -295,6 +307,8 @@ lsw_status lsw_destroy(lsw_ctx* ctx) {
   cudaFree(ctx->st_idx);
   cudaFree(ctx->st_gate);
   for (cudaEvent_t ev : ctx->st_ev) cudaEventDestroy(ev);
+  for (auto& hg : ctx->hgraph) if (hg.exec) cudaGraphExecDestroy(hg.exec);
+  if (ctx->st_cap) cudaStreamDestroy(ctx->st_cap);
   pf_plan_destroy(ctx->pf);
   cudaFree(ctx->prefill_u);
   cudaFree(ctx->prefill_z);
@@ -712,31 +726,12 @@ lsw_status lsw_decode_token_fused(lsw_ctx* ctx, const void* x1, const void* xs, 
   return LSW_OK;
 }
 
-lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_h, float* ys_h, int32_t* idx_h,
-                                 float* gate_h, void* stream) {
-  if (!ctx || !x1_h || !xs_h || !ys_h || !idx_h || !gate_h) return fail(LSW_E_ARG, "lsw_decode_token_host: null argument");
+// The token's work from host buffers, enqueued on `s` (its side stream forked
+// and joined back through events, so the whole sequence can be captured).
+static lsw_status host_token_enqueue(lsw_ctx* ctx, const void* x1_h, const void* xs_h, float* ys_h, int32_t* idx_h,
+                                     float* gate_h, cudaStream_t s) {
   const size_t es = esize(ctx);
-  cudaStream_t s = (cudaStream_t)stream;
-  if (!ctx->st_x1) {
-    if (cudaMalloc(&ctx->st_x1, ctx->cfg.d_model * es) != cudaSuccess ||
-        cudaMalloc(&ctx->st_xs, ctx->xs_elems * es) != cudaSuccess ||
-        cudaMalloc(&ctx->st_ys, ctx->ys_elems * sizeof(float)) != cudaSuccess ||
-        cudaMalloc(&ctx->st_idx, LSW_MAX_TOPK * sizeof(int32_t)) != cudaSuccess ||
-        cudaMalloc(&ctx->st_gate, LSW_MAX_TOPK * sizeof(float)) != cudaSuccess)
-      return fail(LSW_E_OOM, "lsw_decode_token_host: staging allocation failed");
-  }
-  // Copies overlap the token: x1 goes first on the token's stream (the router
-  // needs it); the GEMV inputs on a side stream while the router and the
-  // switch run; each layer's outputs go back on the side stream as soon as
-  // that layer's GEMVs are done.
-  if (!ctx->st_side) {
-    if (cudaStreamCreateWithFlags(&ctx->st_side, cudaStreamNonBlocking) != cudaSuccess)
-      return fail(LSW_E_CUDA, "lsw_decode_token_host: side stream");
-    ctx->st_ev.resize(1 + ctx->cfg.n_layers);
-    for (auto& ev : ctx->st_ev)
-      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
-        return fail(LSW_E_CUDA, "lsw_decode_token_host: events");
-  }
+  void* stream = (void*)s;
   cudaError_t e = cudaMemcpyAsync(ctx->st_x1, x1_h, ctx->cfg.d_model * es, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: H2D");
   cudaStream_t side = ctx->st_side;
@@ -770,9 +765,85 @@ lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_
   }
   if (e == cudaSuccess) e = cudaMemcpyAsync(idx_h, ctx->st_idx, ctx->cfg.top_k * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(gate_h, ctx->st_gate, ctx->cfg.top_k * sizeof(float), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st_side);
+  // join the side stream back into `s`
+  if (e == cudaSuccess) e = cudaEventRecord(ctx->st_ev[1 + ctx->cfg.n_layers], side);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->st_ev[1 + ctx->cfg.n_layers], 0);
   if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: D2H");
+  return LSW_OK;
+}
+
+lsw_status lsw_decode_token_host(lsw_ctx* ctx, const void* x1_h, const void* xs_h, float* ys_h, int32_t* idx_h,
+                                 float* gate_h, void* stream) {
+  if (!ctx || !x1_h || !xs_h || !ys_h || !idx_h || !gate_h) return fail(LSW_E_ARG, "lsw_decode_token_host: null argument");
+  const size_t es = esize(ctx);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!ctx->st_x1) {
+    if (cudaMalloc(&ctx->st_x1, ctx->cfg.d_model * es) != cudaSuccess ||
+        cudaMalloc(&ctx->st_xs, ctx->xs_elems * es) != cudaSuccess ||
+        cudaMalloc(&ctx->st_ys, ctx->ys_elems * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&ctx->st_idx, LSW_MAX_TOPK * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&ctx->st_gate, LSW_MAX_TOPK * sizeof(float)) != cudaSuccess)
+      return fail(LSW_E_OOM, "lsw_decode_token_host: staging allocation failed");
+  }
+  // Copies overlap the token: x1 goes first on the token's stream (the router
+  // needs it); the GEMV inputs on a side stream while the router and the
+  // switch run; each layer's outputs go back on the side stream as soon as
+  // that layer's GEMVs are done.
+  if (!ctx->st_side) {
+    if (cudaStreamCreateWithFlags(&ctx->st_side, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(LSW_E_CUDA, "lsw_decode_token_host: side stream");
+    ctx->st_ev.resize(2 + ctx->cfg.n_layers);
+    for (auto& ev : ctx->st_ev)
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+        return fail(LSW_E_CUDA, "lsw_decode_token_host: events");
+  }
+  // From the second call on, the token is ONE graph launch: its ~130 kernels
+  // and copies enqueued once (captured on a ctx stream), so the host adds a
+  // single launch per token.  One graph per state of the decision slot (the
+  // first token merges, later ones switch); captured again if the host
+  // buffers change.  The graph's kernels read the same device state (decision
+  // slot, error latch) as the eager path.
+  const int mode = ctx->merged ? 1 : 0;
+  auto& hg = ctx->hgraph[mode];
+  const void* key[5] = {x1_h, xs_h, ys_h, idx_h, gate_h};
+  if (ctx->host_graph && ctx->host_calls > 0) {
+    if (hg.exec && memcmp(hg.key, key, sizeof(key)) != 0) {
+      cudaGraphExecDestroy(hg.exec);
+      hg.exec = nullptr;
+    }
+    if (!hg.exec) {
+      if (!ctx->st_cap && cudaStreamCreateWithFlags(&ctx->st_cap, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(LSW_E_CUDA, "lsw_decode_token_host: capture stream");
+      const bool merged0 = ctx->merged;
+      const uint64_t launches0 = ctx->launches;
+      cudaError_t e = cudaStreamBeginCapture(ctx->st_cap, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: capture");
+      lsw_status st = host_token_enqueue(ctx, x1_h, xs_h, ys_h, idx_h, gate_h, ctx->st_cap);
+      cudaGraph_t graph = nullptr;
+      e = cudaStreamEndCapture(ctx->st_cap, &graph);
+      hg.launches = ctx->launches - launches0;
+      ctx->merged = merged0;                       // nothing ran yet
+      ctx->launches = launches0;
+      if (st != LSW_OK) { if (graph) cudaGraphDestroy(graph); return st; }
+      if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: capture");
+      e = cudaGraphInstantiate(&hg.exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) { hg.exec = nullptr; return cuda_fail(e, "lsw_decode_token_host: instantiate"); }
+      memcpy(hg.key, key, sizeof(key));
+    }
+    cudaError_t e = cudaGraphLaunch(hg.exec, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: graph");
+    ctx->merged = true;
+    ctx->launches += hg.launches;
+    ++ctx->host_calls;
+    return LSW_OK;
+  }
+  lsw_status st = host_token_enqueue(ctx, x1_h, xs_h, ys_h, idx_h, gate_h, s);
+  if (st != LSW_OK) return st;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "lsw_decode_token_host: D2H");
+  ++ctx->host_calls;
   return LSW_OK;
 }
 

@@ -379,3 +379,42 @@ def test_decode_all_layers_ring_wrap(lsw_opts, name, impl, grid, op_kb, split):
             yo_ = S.orc.decode_linear(kd, l, x)
             assert PT.allclose_frac_fail(ys_h[yo:yo + n], yo_) == 0.0
             yo += n
+
+
+@pytest.mark.parametrize("name", ["mini", "toy"])
+def test_decode_token_host_graph_matches_eager(lsw_opts, name):
+    """lsw_decode_token_host replays its token as one CUDA graph from the
+    second call on (one per state of the decision slot; captured again when
+    the host buffers change): outputs, decisions and W bitwise equal to the
+    eager path (option host_graph=0) over tokens that merge, switch, switch
+    with other host buffers, and merge again after an unmerge."""
+    cfg = synth.get_config(name)
+    runs = []
+    for graph in ("1", "0"):
+        lsw_opts(host_graph=graph)
+        W, A, B, router = H.build_weights(cfg, "cuda")
+        sw = H.make_switch(cfg, W, A, B, router)
+        info = sw.info()
+        X1 = synth.gen_x1(cfg, 6, "cuda").cpu()
+        xs = H.pack_xs(cfg, synth.gen_xs(cfg, "cuda")).cpu()
+        bufs = [dict(x1=torch.empty(cfg.d_model, dtype=X1.dtype).pin_memory(), xs=xs.clone().pin_memory(),
+                     ys=torch.empty(info["ys_elems"], dtype=torch.float32).pin_memory(),
+                     idx=torch.empty(cfg.top_k, dtype=torch.int32).pin_memory(),
+                     g=torch.empty(cfg.top_k, dtype=torch.float32).pin_memory()) for _ in range(2)]
+        out = []
+        for t, (b, unmerge) in enumerate([(0, False), (0, False), (0, False), (1, False), (1, True), (1, False)]):
+            if unmerge:
+                sw.unmerge_all_layers()
+                torch.cuda.synchronize()
+            bb = bufs[b]
+            bb["x1"].copy_(X1[t])
+            sw.decode_token_host(bb["x1"], bb["xs"], bb["ys"], bb["idx"], bb["g"])
+            out.append((bb["ys"].clone(), bb["idx"].clone(), bb["g"].clone()))
+        torch.cuda.synchronize()
+        out.append(tuple(W[kd].clone() for kd in synth.KINDS))
+        assert sw.device_status() == 0
+        runs.append(out)
+        sw.close()
+    for a, b in zip(*runs):
+        for u, v in zip(a, b):
+            assert torch.equal(u, v)
