@@ -35,6 +35,14 @@ extern "C" {
  *   gemv_split     0|1|2  rows over 24 KB reduced by two warps (1);    [1]
  *                         never (0); every row (2, tests)
  *   host_graph     0|1    lsw_decode_token_host replayed as a CUDA graph [1]
+ *   Prefill (lsw_prefill_group, read at its first call; results may differ
+ *   in fp32 summation order between values, each deterministic):
+ *   pf_tt          128|256  token tile                       [per group]
+ *   pf_cluster     1|2|4  dense launch on W-multicast clusters          [1]
+ *   pf_pair        0|1|2  dense + LoRA-up on CTA pairs: never / groups  [1]
+ *                         with a wave of 256-token tiles / always
+ *   pf_fuse_u      0|1    single-CTA groups: LoRA-down and Z built in   [1]
+ *                         the dense launch (1) or by two launches (0)
  *   nccl_path      file   libnccl.so.2 to dlopen when none is loaded yet
  *                         (read at the first NCCL call, lsw_nccl_version)
  * Probes (deliberately WRONG results; only in a build with -DLSW_TUNING,

@@ -593,6 +593,10 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
     ctx->prefill_z_elems = 0;
     if (cudaMalloc(&ctx->prefill_z, need_z * 2) != cudaSuccess)
       return fail(LSW_E_OOM, "%s: scratch allocation failed", who);
+    // the fused LoRA-down writes only the slots rho < r; the padding slots
+    // (rho in [r, rp)) meet zero B columns and must hold finite values
+    if (cudaMemset(ctx->prefill_z, 0, need_z * 2) != cudaSuccess)
+      return fail(LSW_E_CUDA, "%s: scratch initialisation failed", who);
     ctx->prefill_z_elems = need_z;
   }
   const size_t es = esize(ctx);

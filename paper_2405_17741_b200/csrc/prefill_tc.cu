@@ -22,6 +22,13 @@
 //     accumulated in fp32 in TMEM by one chain of tcgen05.mma (M = 128,
 //     N = 128) -- the LoRA-up term is just N*2*rp more K of the same
 //     contraction -- then written to Y (fp32) by the epilogue warps.
+// Single-CTA launches (no CTA pairs; option pf_fuse_u, default on) fold 1 and
+// 2 into 3: the launch's first tiles are A-bank tiles (128 bank rows x one
+// token tile, full K -- the LoRA-down without split), whose epilogue forms z =
+// c_t(e) u from TMEM and stores the (hi, lo) Z slots itself, then counts the
+// tile in a monotonic device word; a W tile's producer waits for this launch's
+// count before its first LoRA-up stage.  One launch instead of three, no fp32
+// U round trip through L2.
 // Warp roles: 0 TMA/bulk producer, 1 MMA issuer (+ TMEM alloc), 2-5 epilogue
 // (TMEM lane quarter = warp % 4).  Persistent grid, tiles dealt round-robin
 // with the token tile fastest, so the CTAs that share a W strip run together
@@ -49,6 +56,7 @@ constexpr int MODE_Y = 0, MODE_U = 1;
 struct Maps {
   CUtensorMap op[3];   // MODE_Y: W of site q [L, d_out, d_in]; MODE_U: A of site q [L, N*r, d_in]
   CUtensorMap x;       // X [T, d_in]
+  CUtensorMap a[3];    // MODE_Y with fuse_u: A of site q [L, N*r, d_in]
 };
 // CTA pairs: every operand moved by a tensor copy (so that the follower's
 // copies can complete on the leader's barrier)
@@ -79,6 +87,20 @@ struct Args {
   uint32_t stage_bytes, b_off;   // stage = [A part | B part at b_off]
   int32_t stages;
   int32_t pair_row0[4];          // CTA pairs: prefix sums of the sites' row-tile PAIRS
+  // MODE_Y, fuse_u: the LoRA-down products and Z built by the same launch.  The
+  // first a_tiles tiles are A-bank tiles (site q's rows e*r + rho of A_q x one
+  // token tile, full K); their epilogue writes the gate-scaled (hi, lo) Z slots
+  // straight from TMEM and counts itself in *zdone; a W tile's producer waits
+  // for *zdone == a_tiles before its first LoRA-up stage
+  int32_t a_tiles;
+  int32_t a_row0[4];             // prefix sums of the sites' A-bank row tiles
+  int32_t k, r;
+  float scale;
+  uint32_t* zdone;               // monotonic count of A-bank tiles done (plan-owned word)
+  uint32_t z_target;             // *zdone after this launch's A-bank tiles (mod 2^32)
+  const int32_t* idx;            // [T, k]
+  const float* gate;             // [T, k]
+  __nv_bfloat16* Zw;             // = Z, written by the A-bank tiles
 };
 
 struct TileAt {
@@ -104,6 +126,12 @@ __device__ __forceinline__ TileAt tile_at(const Args& a, int t) {  // token tile
     r.kb1 = a.n_kb;
   }
   return r;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
@@ -181,9 +209,21 @@ __device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
 // = group * kC + rank (may lie past the last token tile: OOB-zero operands,
 // masked stores).
 template <int kC>
-__device__ __forceinline__ TileAt tile_for(const Args& a, int it, int crank) {
+__device__ __forceinline__ TileAt tile_for(const Args& a, int it, int crank, bool& bank) {
+  bank = false;
   if constexpr (kC == 1) {
-    return tile_at(a, it);
+    if (it >= a.a_tiles) {
+      return tile_at(a, it - a.a_tiles);
+    }
+    bank = true;                                 // A-bank tile (fuse_u)
+    TileAt r;
+    r.tt = it % a.n_tt;
+    const int rest = it / a.n_tt;
+    r.q = (a.n_sites > 2 && rest >= a.a_row0[2]) ? 2 : (a.n_sites > 1 && rest >= a.a_row0[1]) ? 1 : 0;
+    r.rb = rest - a.a_row0[r.q];
+    r.kb0 = 0;
+    r.kb1 = a.n_kb;
+    return r;
   } else {
     const int n_ttg = (a.n_tt + kC - 1) / kC;
     const int rest = it / n_ttg;
@@ -194,6 +234,73 @@ __device__ __forceinline__ TileAt tile_for(const Args& a, int it, int crank) {
     r.kb0 = 0;
     r.kb1 = a.n_kb;
     return r;
+  }
+}
+
+// A-bank tile epilogue (fuse_u): this thread's bank row is expert e, rank
+// index rho; for every token t of the tile z = c_t(e) * u_t with u_t the
+// full-K fp32 product in TMEM and c_t(e) = sum_j [idx_tj == e] scale * gate_tj
+// (j ascending, as the Z build), stored as (hi, lo) bf16 at the pre-swizzled
+// slot of Z.  Lane l fetches the decision of token l of each 32-token chunk
+// (the next chunk's in flight while this one is processed) and the warp reads
+// each token's K entries by shuffle -- K a template parameter, so the 16
+// tokens of a TMEM load carry no branches and their shuffles overlap.
+template <int K, int kTT>
+__device__ __forceinline__ void bank_z(const Args& a, int tt, uint32_t tm, int e, int rho, bool okr,
+                                       __nv_bfloat16* blk, int lane) {
+  const int64_t t0 = (int64_t)tt * kTT;
+  const int rp = a.rp, fmask = rp / 8 - 1, zpart = kTT * rp;
+  int id[K];
+  float gv[K];
+  auto fetch = [&](int c32, int* idr, float* gvr) {
+    const int64_t tl = t0 + c32 + lane;
+    const bool in = tl < a.T;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      idr[j] = in ? __ldg(a.idx + tl * K + j) : -1;
+      gvr[j] = in ? a.scale * __ldg(a.gate + tl * K + j) : 0.f;
+    }
+  };
+  fetch(0, id, gv);
+  for (int c32 = 0; c32 < kTT; c32 += 32) {
+    int idn[K];
+    float gvn[K];
+    if (c32 + 32 < kTT) fetch(c32 + 32, idn, gvn);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t v[16];
+      tmem_ld16(tm + c32 + 16 * h, v);
+      tmem_wait_ld();
+      float c[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        c[i] = 0.f;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int ij = __shfl_sync(0xffffffffu, id[j], 16 * h + i);
+          const float gj = __shfl_sync(0xffffffffu, gv[j], 16 * h + i);
+          if (ij == e) c[i] += gj;
+        }
+      }
+      if (okr) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int tin = c32 + 16 * h + i;
+          const float z = c[i] != 0.f ? c[i] * __uint_as_float(v[i]) : 0.f;
+          const __nv_bfloat16 hi = __float2bfloat16_rn(z);
+          const __nv_bfloat16 lo = __float2bfloat16_rn(z - __bfloat162float(hi));
+          // swz_off(tin, rho, rp) in 32-bit arithmetic
+          const int off = tin * rp + ((((rho >> 3) ^ ((tin * rp) >> 6)) & fmask) << 3) + (rho & 7);
+          blk[off] = hi;
+          blk[zpart + off] = lo;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      id[j] = idn[j];
+      gv[j] = gvn[j];
+    }
   }
 }
 
@@ -208,8 +315,9 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool lora = a.mode == MODE_Y && a.n_experts > 0;
 
-  // MODE_U: the Z build launched next (programmatic dependent) may start at once
-  if (a.mode == MODE_U) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // MODE_U: the Z build launched next (programmatic dependent) may start at
+  // once; fused MODE_Y: the next group's launch may take SMs as they free up
+  if (a.mode == MODE_U || a.a_tiles) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int crank = kC > 1 ? (int)cluster_rank() : 0;
   const uint16_t cmask = (uint16_t)((1u << kC) - 1);
   const int it0 = kC > 1 ? (int)cluster_id() : blockIdx.x;
@@ -227,7 +335,10 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
-    for (int q = 0; q < a.n_sites; ++q) prefetch_map(&maps.op[q]);
+    for (int q = 0; q < a.n_sites; ++q) {
+      prefetch_map(&maps.op[q]);
+      if (a.a_tiles) prefetch_map(&maps.a[q]);
+    }
     prefetch_map(&maps.x);
   }
   if (warp == 1) {
@@ -251,9 +362,12 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
       // MODE_U is a programmatic dependent of the previous group's dense
       // launch: its setup (barriers, TMEM, tensor maps) ran already; X (and U,
       // read by the previous Z build) only after that grid has completed
-      if (a.mode == MODE_U) asm volatile("griddepcontrol.wait;" ::: "memory");
+      // (fused MODE_Y likewise: X, and Z / Y still read by the previous group)
+      if (a.mode == MODE_U || a.a_tiles) asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int it = it0; it < n_it; it += istep) {
-        const TileAt ta = tile_for<kC>(a, it, crank);
+        bool bank;
+        const TileAt ta = tile_for<kC>(a, it, crank, bank);
+        const CUtensorMap* opmap = bank ? &maps.a[ta.q] : &maps.op[ta.q];
         for (int kb = ta.kb0; kb < ta.kb1; ++kb) {
           mbar_wait(smem_u32(&bar_empty[ring.i]), ring.phase ^ 1);
           uint8_t* st = base + (size_t)ring.i * a.stage_bytes;
@@ -264,14 +378,19 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
             tma_load_3d_mc(smem_u32(st) + crank * (kBoxBytes / kC), &maps.op[ta.q], kb * kKB,
                            ta.rb * kTM + crank * (kTM / kC), a.layer, bar, cmask, pol_w);
           } else {
-            tma_load_3d(smem_u32(st), &maps.op[ta.q], kb * kKB, ta.rb * kTM, a.layer, bar, pol_w);
+            tma_load_3d(smem_u32(st), opmap, kb * kKB, ta.rb * kTM, a.layer, bar, pol_w);
           }
           tma_load_2d(smem_u32(st + a.b_off), &maps.x, kb * kKB, ta.tt * kTT, bar, pol_x);   // box {64, kTT}
           ring.next();
         }
-        if (lora) {
-          if (!z_ready) {                        // Z is written by the preceding (Z build) grid
-            asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (lora && !bank) {
+          if (!z_ready) {
+            if (a.a_tiles) {                     // Z is written by this grid's A-bank tiles
+              while ((int32_t)(ld_acquire_gpu_u32(a.zdone) - a.z_target) < 0) __nanosleep(32);
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+            } else {                             // Z is written by the preceding (Z build) grid
+              asm volatile("griddepcontrol.wait;" ::: "memory");
+            }
             z_ready = true;
           }
           for (int e = 0; e < a.n_experts; ++e) {
@@ -308,7 +427,8 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
     Ring ring{0, 0, (uint32_t)a.stages};
     Ring acc{0, 0, kAccBufs};
     for (int it = it0; it < n_it; it += istep) {
-      const TileAt ta = tile_for<kC>(a, it, crank);
+      bool bank;
+      const TileAt ta = tile_for<kC>(a, it, crank, bank);
       mbar_wait(smem_u32(&bar_accempty[acc.i]), acc.phase ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + acc.i * kTT;
@@ -328,7 +448,7 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
         accum = 1;
         ring.next();
       }
-      if (lora) {
+      if (lora && !bank) {
         const int ksteps = a.rp / 16;
         for (int e = 0; e < a.n_experts; ++e) {
           mbar_wait(smem_u32(&bar_full[ring.i]), ring.phase);
@@ -358,9 +478,46 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
     const int row = quarter * 32 + lane;
     Ring acc{0, 0, kAccBufs};
     for (int it = it0; it < n_it; it += istep) {
-      const TileAt ta = tile_for<kC>(a, it, crank);
+      bool bank;
+      const TileAt ta = tile_for<kC>(a, it, crank, bank);
       mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);
       tc_fence_after();
+      if (bank) {
+        // Z slots of A-bank row R = e*r + rho: z = c_t(e) * u, u from TMEM
+        // (full-K fp32), c_t(e) = sum_j [idx_tj == e] scale * gate_tj -- the
+        // Z build's arithmetic, split into (hi, lo) bf16
+        const int R = ta.rb * kTM + row;
+        const int e = R / a.r, rho = R - e * a.r;
+        const bool okr = e < a.n_experts;
+        __nv_bfloat16* blk =
+            a.Zw + ((((int64_t)ta.tt * a.n_sites + ta.q) * a.n_experts + e) * 2) * (int64_t)kTT * a.rp;
+        const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTT;
+        {
+          switch (a.k) {
+            case 1: bank_z<1, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
+            case 2: bank_z<2, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
+            case 3: bank_z<3, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
+            case 4: bank_z<4, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
+            case 5: bank_z<5, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
+            case 6: bank_z<6, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
+            case 7: bank_z<7, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
+            default: bank_z<8, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+        // every epilogue thread's Z stores before the count; the W tiles read
+        // Z by bulk copies (async proxy)
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpiWarps) : "memory");
+        if (warp == 2 && lane == 0) {
+          __threadfence();
+          atomicAdd(a.zdone, 1u);
+        }
+        acc.next();
+        continue;
+      }
       const int64_t grow = (int64_t)ta.rb * kTM + row;
       const bool ok = grow < a.rows_valid[ta.q];
       const int split = a.mode == MODE_U ? it / a.n_tt / a.row_tiles_total : 0;
@@ -681,6 +838,10 @@ struct PfPlan {
                                  // 256-token tiles, 2 whenever the sites' row tiles pair up: dense + LoRA-up
                                  // on CTA pairs
   CUtensorMap bmap[LSW_NKIND];   // pairs: the packed B of every kind as [L*N*dout_pad, rp]
+  uint32_t* zdone;               // device word: A-bank tiles done, monotonic over the plan's launches
+  mutable uint32_t z_count;      // host copy of *zdone once every launch so far has completed
+  int fuse_opt;                  // variant option pf_fuse_u: 1 (default) the single-CTA dense launch also
+                                 // computes the LoRA-down and builds Z (A-bank tiles); 0 three launches
 };
 
 // shared-memory plan of one token-tile width: stage = [128 x 64 A box | B
@@ -785,6 +946,7 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
   if (p->tt_opt != 128 && p->tt_opt != 256) p->tt_opt = 0;
   p->cl_opt = (int)opt_int("pf_cluster", 0);
   p->pair_opt = (int)opt_int("pf_pair", 1);
+  p->fuse_opt = (int)opt_int("pf_fuse_u", 1);
   if (p->cl_opt != 1 && p->cl_opt != 2 && p->cl_opt != 4) p->cl_opt = 0;
   if (pf_geom(128, p->rp).stages < 3) { delete p; return cudaErrorNotSupported; }
   const int smem = (int)(kPfBudget + 1024);
@@ -794,12 +956,17 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
     if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (auto fn : {pf::prefill_gemm_pair<128>, pf::prefill_gemm_pair<256>})
     if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) { delete p; return e; }
+  if (e == cudaSuccess) e = cudaMalloc(&p->zdone, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(p->zdone, 0, sizeof(uint32_t));
+  if (e != cudaSuccess) { cudaFree(p->zdone); delete p; return e; }
   *out = p;
   return cudaSuccess;
 }
 
-void pf_plan_destroy(PfPlan* p) { delete p; }
+void pf_plan_destroy(PfPlan* p) {
+  if (p) cudaFree(p->zdone);
+  delete p;
+}
 
 // cluster size of the dense launch (variant option pf_cluster; default 1).
 // Measured (7B, 512 tokens, same box): clusters of 4 token tiles sharing each
@@ -906,7 +1073,17 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   a.rp = p->rp;
   int grid = a.total_tiles < p->num_sms ? a.total_tiles : p->num_sms;
   cudaError_t e;
-  {
+  const int C = pf_cluster(p, n_tt);
+  const int n_tt_pad = (n_tt + C - 1) / C * C;
+  // fused LoRA-down (single CTAs, no pairs): the A-bank tiles lead the dense
+  // launch's tile order, so every CTA runs its A-bank tiles before any W
+  // tile and no W tile's wait on them can block one
+  // (not under stream capture: the count target is baked into the launch)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) return cudaGetLastError();
+  const bool fuse = p->fuse_opt && C == 1 && !pair && cap == cudaStreamCaptureStatusNone;
+  const int a_tiles = rt * n_tt;                 // A-bank tiles (full K)
+  if (!fuse) {
     cudaLaunchConfig_t uc{};
     uc.gridDim = dim3(grid);
     uc.blockDim = dim3(kThreads);
@@ -921,9 +1098,7 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
     if (e != cudaSuccess) return e;
   }
   // ---- 2. gate-scaled (hi, lo) LoRA-down products of the selected experts
-  const int C = pf_cluster(p, n_tt);
-  const int n_tt_pad = (n_tt + C - 1) / C * C;
-  {
+  if (!fuse) {
     const int64_t n = (int64_t)n_tt_pad * P.n_sites * p->n_experts * kTT * p->rp;
     int blocks = (int)((n + 255) / 256);
     if (blocks > 4 * p->num_sms) blocks = 4 * p->num_sms;
@@ -945,6 +1120,19 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   Args y = a;
   y.mode = MODE_Y;
   y.splits = 1;
+  if (fuse) {
+    for (int q = 0; q <= P.n_sites; ++q) y.a_row0[q] = a.tile_row0[q];
+    for (int q = 0; q < P.n_sites; ++q) maps.a[q] = p->a[kinds[q]];
+    y.a_tiles = a_tiles;
+    y.k = P.k;
+    y.r = p->r;
+    y.scale = P.scale;
+    y.idx = P.idx;
+    y.gate = P.gate;
+    y.Zw = reinterpret_cast<__nv_bfloat16*>(P.Z);
+    y.zdone = p->zdone;
+    y.z_target = p->z_count + (uint32_t)a_tiles;
+  }
   rt = 0;
   for (int q = 0; q < P.n_sites; ++q) {
     const int kd = kinds[q];
@@ -958,7 +1146,7 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   }
   y.tile_row0[P.n_sites] = rt;
   y.row_tiles_total = rt;
-  y.total_tiles = rt * n_tt;
+  y.total_tiles = y.a_tiles + rt * n_tt;
   y.ld = P.rows;
   y.out = P.Y;
   y.n_experts = p->n_experts;
@@ -1012,7 +1200,9 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   }
   if (C == 1) {
     lc.gridDim = dim3(y.total_tiles < p->num_sms ? y.total_tiles : p->num_sms);
-    return cudaLaunchKernelEx(&lc, prefill_gemm<kTT, 1>, maps, y);
+    e = cudaLaunchKernelEx(&lc, prefill_gemm<kTT, 1>, maps, y);
+    if (e == cudaSuccess && fuse) p->z_count = y.z_target;
+    return e;
   }
   const int n_ct = rt * (n_tt_pad / C);                      // cluster tiles
   const int n_cl = n_ct < p->num_sms / C ? n_ct : p->num_sms / C;
