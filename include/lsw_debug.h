@@ -43,6 +43,8 @@ extern "C" {
  *                         with a wave of 256-token tiles / always
  *   pf_fuse_u      0|1    single-CTA groups: LoRA-down and Z built in   [1]
  *                         the dense launch (1) or by two launches (0)
+ *   pf_bank_split  0|1    fused: each A-bank tile's K in two halves on  [1]
+ *                         two CTAs when the launch is one wave
  *   nccl_path      file   libnccl.so.2 to dlopen when none is loaded yet
  *                         (read at the first NCCL call, lsw_nccl_version)
  * Probes (deliberately WRONG results; only in a build with -DLSW_TUNING,

@@ -626,6 +626,7 @@ lsw_status lsw_prefill_group(lsw_ctx* ctx, int32_t layer, int32_t group, const v
   P.idx = idx;
   P.gate = gate;
   P.U = ctx->prefill_u;
+  P.u_elems = ctx->prefill_u_elems;
   P.Z = ctx->prefill_z;
   P.Y = Y;
   cudaError_t e = tc ? launch_prefill_tc(ctx->pf, P, layer, kinds, (cudaStream_t)stream)

@@ -234,7 +234,8 @@ struct PrefillParams {
   const void* X;             // [T, d_in]
   const int32_t* idx;        // [T, k]
   const float* gate;         // [T, k]
-  float* U;                  // scratch: LoRA-down products (tc: per K split)
+  float* U;                  // scratch: LoRA-down products (tc: per K split; fused: split-K bank partials)
+  int64_t u_elems;           // its size (elements)
   void* Z;                   // scratch (tc): gate-scaled (hi, lo) bf16 operand of the LoRA-up step
   float* Y;                  // [T, rows]
 };

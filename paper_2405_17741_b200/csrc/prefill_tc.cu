@@ -98,6 +98,14 @@ struct Args {
   float scale;
   uint32_t* zdone;               // monotonic count of A-bank tiles done (plan-owned word)
   uint32_t z_target;             // *zdone after this launch's A-bank tiles (mod 2^32)
+  // a_split == 2: each A-bank tile's K in two halves on two CTAs (iterations
+  // 2j, 2j+1): half 0 stores its fp32 partial to Pp [j][kTT][128] and counts
+  // in *pdone; half 1 waits for *pdone == p_target, adds the partial (half 0
+  // first: fixed order) and builds Z.  a_tiles counts iterations.
+  int32_t a_split;
+  uint32_t* pdone;
+  uint32_t p_target;
+  float* Pp;
   const int32_t* idx;            // [T, k]
   const float* gate;             // [T, k]
   __nv_bfloat16* Zw;             // = Z, written by the A-bank tiles
@@ -105,6 +113,7 @@ struct Args {
 
 struct TileAt {
   int q, rb, tt, kb0, kb1;
+  int half, j;                   // fuse_u, split bank tiles: K half (0 | 1), bank tile index
 };
 
 __device__ __forceinline__ TileAt tile_at(const Args& a, int t) {  // token tile fastest
@@ -217,12 +226,14 @@ __device__ __forceinline__ TileAt tile_for(const Args& a, int it, int crank, boo
     }
     bank = true;                                 // A-bank tile (fuse_u)
     TileAt r;
-    r.tt = it % a.n_tt;
-    const int rest = it / a.n_tt;
+    r.j = a.a_split == 2 ? it >> 1 : it;
+    r.half = a.a_split == 2 ? it & 1 : 0;
+    r.tt = r.j % a.n_tt;
+    const int rest = r.j / a.n_tt;
     r.q = (a.n_sites > 2 && rest >= a.a_row0[2]) ? 2 : (a.n_sites > 1 && rest >= a.a_row0[1]) ? 1 : 0;
     r.rb = rest - a.a_row0[r.q];
-    r.kb0 = 0;
-    r.kb1 = a.n_kb;
+    r.kb0 = r.half ? a.n_kb / 2 : 0;
+    r.kb1 = a.a_split == 2 && !r.half ? a.n_kb / 2 : a.n_kb;
     return r;
   } else {
     const int n_ttg = (a.n_tt + kC - 1) / kC;
@@ -245,9 +256,15 @@ __device__ __forceinline__ TileAt tile_for(const Args& a, int it, int crank, boo
 // (the next chunk's in flight while this one is processed) and the warp reads
 // each token's K entries by shuffle -- K a template parameter, so the 16
 // tokens of a TMEM load carry no branches and their shuffles overlap.
+__device__ __forceinline__ int shfl_ordered(int v, int src) {
+  int r;
+  asm volatile("shfl.sync.idx.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(r) : "r"(v), "r"(src));
+  return r;
+}
+
 template <int K, int kTT>
 __device__ __forceinline__ void bank_z(const Args& a, int tt, uint32_t tm, int e, int rho, bool okr,
-                                       __nv_bfloat16* blk, int lane) {
+                                       __nv_bfloat16* blk, int lane, const float* pp) {
   const int64_t t0 = (int64_t)tt * kTT;
   const int rp = a.rp, fmask = rp / 8 - 1, zpart = kTT * rp;
   int id[K];
@@ -270,15 +287,26 @@ __device__ __forceinline__ void bank_z(const Args& a, int tt, uint32_t tm, int e
     for (int h = 0; h < 2; ++h) {
       uint32_t v[16];
       tmem_ld16(tm + c32 + 16 * h, v);
+      float pv[16];
+      if (pp) {                                  // half 0's partial of these 16 tokens (this row)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pv[i] = __ldcg(pp + (c32 + 16 * h + i) * kTM);
+      }
       tmem_wait_ld();
+      if (pp) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(pv[i] + __uint_as_float(v[i]));
+      }
       float c[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         c[i] = 0.f;
 #pragma unroll
         for (int j = 0; j < K; ++j) {
-          const int ij = __shfl_sync(0xffffffffu, id[j], 16 * h + i);
-          const float gj = __shfl_sync(0xffffffffu, gv[j], 16 * h + i);
+          // volatile: the shuffles stay in token order, so their results are
+          // consumed as they come instead of all being hoisted (registers)
+          const int ij = shfl_ordered(id[j], 16 * h + i);
+          const float gj = __int_as_float(shfl_ordered(__float_as_int(gv[j]), 16 * h + i));
           if (ij == e) c[i] += gj;
         }
       }
@@ -492,16 +520,41 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
         __nv_bfloat16* blk =
             a.Zw + ((((int64_t)ta.tt * a.n_sites + ta.q) * a.n_experts + e) * 2) * (int64_t)kTT * a.rp;
         const uint32_t tm = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc.i * kTT;
+        float* pj = a.Pp + (int64_t)ta.j * kTT * kTM + row;   // [j][token][row]
+        if (a.a_split == 2 && ta.half == 0) {
+          // half 0: the fp32 partial to Pp, counted in *pdone (no Z)
+          for (int c0 = 0; c0 < kTT; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(tm + c0, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) __stcg(pj + (c0 + i) * kTM, __uint_as_float(v[i]));
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
+          asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpiWarps) : "memory");
+          if (warp == 2 && lane == 0) {
+            __threadfence();
+            atomicAdd(a.pdone, 1u);
+          }
+          acc.next();
+          continue;
+        }
+        const float* pp = nullptr;
+        if (a.a_split == 2) {                    // half 1: every half 0 of this launch stored
+          if (lane == 0)
+            while ((int32_t)(ld_acquire_gpu_u32(a.pdone) - a.p_target) < 0) __nanosleep(32);
+          __syncwarp();
+          pp = pj;
+        }
         {
           switch (a.k) {
-            case 1: bank_z<1, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
-            case 2: bank_z<2, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
-            case 3: bank_z<3, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
-            case 4: bank_z<4, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
-            case 5: bank_z<5, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
-            case 6: bank_z<6, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
-            case 7: bank_z<7, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
-            default: bank_z<8, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane); break;
+            case 1: bank_z<1, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane, pp); break;
+            case 2: bank_z<2, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane, pp); break;
+            case 3: bank_z<3, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane, pp); break;
+            case 4: bank_z<4, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane, pp); break;
+            default: bank_z<4, kTT>(a, ta.tt, tm, e, rho, okr, blk, lane, pp); break;   // (k <= 4: host)
           }
         }
         tc_fence_before();
@@ -838,8 +891,12 @@ struct PfPlan {
                                  // 256-token tiles, 2 whenever the sites' row tiles pair up: dense + LoRA-up
                                  // on CTA pairs
   CUtensorMap bmap[LSW_NKIND];   // pairs: the packed B of every kind as [L*N*dout_pad, rp]
-  uint32_t* zdone;               // device word: A-bank tiles done, monotonic over the plan's launches
-  mutable uint32_t z_count;      // host copy of *zdone once every launch so far has completed
+  uint32_t* zdone;               // device words: [0] A-bank tiles done, [1] split-K half-0 partials
+                                 // stored -- monotonic over the plan's launches
+  mutable uint32_t z_count;      // host copy of zdone[0] once every launch so far has completed
+  mutable uint32_t p_count;      // host copy of zdone[1]
+  int split_opt;                 // variant option pf_bank_split: 1 (default) A-bank tiles split in two K
+                                 // halves when the launch is one wave; 0 never
   int fuse_opt;                  // variant option pf_fuse_u: 1 (default) the single-CTA dense launch also
                                  // computes the LoRA-down and builds Z (A-bank tiles); 0 three launches
 };
@@ -947,6 +1004,7 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
   p->cl_opt = (int)opt_int("pf_cluster", 0);
   p->pair_opt = (int)opt_int("pf_pair", 1);
   p->fuse_opt = (int)opt_int("pf_fuse_u", 1);
+  p->split_opt = (int)opt_int("pf_bank_split", 1);
   if (p->cl_opt != 1 && p->cl_opt != 2 && p->cl_opt != 4) p->cl_opt = 0;
   if (pf_geom(128, p->rp).stages < 3) { delete p; return cudaErrorNotSupported; }
   const int smem = (int)(kPfBudget + 1024);
@@ -956,8 +1014,8 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
     if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (auto fn : {pf::prefill_gemm_pair<128>, pf::prefill_gemm_pair<256>})
     if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) e = cudaMalloc(&p->zdone, sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemset(p->zdone, 0, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&p->zdone, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(p->zdone, 0, 2 * sizeof(uint32_t));
   if (e != cudaSuccess) { cudaFree(p->zdone); delete p; return e; }
   *out = p;
   return cudaSuccess;
@@ -1019,6 +1077,9 @@ void pf_scratch(const PfPlan* p, int n_sites, int64_t T, int64_t* u_elems, int64
   *z_elems = 0;
   for (int64_t tt : {128, 256}) {
     const int64_t n_tt = (T + tt - 1) / tt, c = pf_cluster(p, n_tt);
+    // fused, split bank tiles: one fp32 [tt, 128] partial per bank tile
+    const int64_t bank = n_sites * ((nr + pf::kTM - 1) / pf::kTM) * n_tt * tt * pf::kTM;
+    if (bank > *u_elems) *u_elems = bank;
     const int64_t n_tt_pad = (n_tt + c - 1) / c * c;             // Z of padded token tiles: zeros
     const int64_t z = n_tt_pad * n_sites * p->n_experts * 2 * tt * p->rp;
     if (z > *z_elems) *z_elems = z;
@@ -1081,7 +1142,7 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   // (not under stream capture: the count target is baked into the launch)
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) return cudaGetLastError();
-  const bool fuse = p->fuse_opt && C == 1 && !pair && cap == cudaStreamCaptureStatusNone;
+  const bool fuse = p->fuse_opt && C == 1 && !pair && P.k <= 4 && cap == cudaStreamCaptureStatusNone;
   const int a_tiles = rt * n_tt;                 // A-bank tiles (full K)
   if (!fuse) {
     cudaLaunchConfig_t uc{};
@@ -1132,6 +1193,22 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
     y.Zw = reinterpret_cast<__nv_bfloat16*>(P.Z);
     y.zdone = p->zdone;
     y.z_target = p->z_count + (uint32_t)a_tiles;
+    // each bank tile's K in two halves on two CTAs when the whole launch is
+    // one wave (every half 0 then runs beside its half 1, so the wait for the
+    // launch's half-0 count cannot block), and the partials fit in U
+    const int64_t w_tiles = (int64_t)n_tt * [&] {
+      int64_t t = 0;
+      for (int q = 0; q < P.n_sites; ++q) t += (p->d_out[kinds[q]] + kTM - 1) / kTM;
+      return t;
+    }();
+    if (p->split_opt && n_kb >= 2 && 2 * (int64_t)a_tiles + w_tiles <= p->num_sms &&
+        (int64_t)a_tiles * kTT * kTM <= P.u_elems) {
+      y.a_split = 2;
+      y.a_tiles = 2 * a_tiles;
+      y.pdone = p->zdone + 1;
+      y.p_target = p->p_count + (uint32_t)a_tiles;
+      y.Pp = P.U;
+    }
   }
   rt = 0;
   for (int q = 0; q < P.n_sites; ++q) {
@@ -1201,7 +1278,10 @@ static cudaError_t prefill_tc_tt(const PfPlan* p, const PrefillParams& P, int la
   if (C == 1) {
     lc.gridDim = dim3(y.total_tiles < p->num_sms ? y.total_tiles : p->num_sms);
     e = cudaLaunchKernelEx(&lc, prefill_gemm<kTT, 1>, maps, y);
-    if (e == cudaSuccess && fuse) p->z_count = y.z_target;
+    if (e == cudaSuccess && fuse) {
+      p->z_count = y.z_target;
+      if (y.a_split == 2) p->p_count = y.p_target;
+    }
     return e;
   }
   const int n_ct = rt * (n_tt_pad / C);                      // cluster tiles

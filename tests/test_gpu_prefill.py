@@ -45,7 +45,9 @@ def _f64(t):
                                             ("mini", "tc", 300, "unfused"), ("mini-r64k3", "tc", 512, "unfused"),
                                             ("mini-r4k4", "tc", 129, "unfused"), ("mini-r32", "tc", 1, "nopair"),
                                             ("mini", "tc", 300, "pair-unfused"), ("mini-r64k4", "tc", 512, "pair-unfused"),
-                                            ("mini-N64", "tc", 200, None), ("mini-r48", "tc", 300, "pair")])
+                                            ("mini-N64", "tc", 200, None), ("mini-r48", "tc", 300, "pair"),
+                                            ("mini", "tc", 300, "nosplit"), ("mini-r64k4", "tc", 257, "nosplit"),
+                                            ("mini-r4k4", "tc", 64, "nosplit")])
 def test_prefill_matches_oracle(lsw_opts, name, impl, T, tt):
     """The dense + LoRA-up launch runs on CTA pairs (cta_group::2, M = 256)
     for groups with a wave of 256-token tiles whose sites' row tiles pair up;
@@ -53,7 +55,8 @@ def test_prefill_matches_oracle(lsw_opts, name, impl, T, tt):
     not q|k|v, k being one row tile; option pf_pair=2); "nopair": single
     CTAs everywhere (pf_pair=0).  The single-CTA dense launch computes the
     LoRA-down and builds Z itself (A-bank tiles, option pf_fuse_u=1, the
-    default); "unfused" / "pair-unfused": three launches (LoRA-down, Z build,
+    default; each bank tile's K in two halves on two CTAs when the launch is
+    one wave, "nosplit": pf_bank_split=0); "unfused" / "pair-unfused": three launches (LoRA-down, Z build,
     dense + LoRA-up; pf_fuse_u=0).  tt: the token tile of the tensor-core path forced to 128 /
     256 (variant option pf_tt), or "tile/cluster": also the cluster of the dense launch forced
     (pf_cluster: W rows multicast across the token tiles of a cluster; T = 300
@@ -66,6 +69,8 @@ def test_prefill_matches_oracle(lsw_opts, name, impl, T, tt):
         lsw_opts(pf_pair=0, pf_fuse_u=0)
     elif tt == "pair-unfused":
         lsw_opts(pf_pair=2, pf_fuse_u=0)
+    elif tt == "nosplit":                           # fused, each A-bank tile's whole K on one CTA
+        lsw_opts(pf_pair=0, pf_bank_split=0)
     elif isinstance(tt, str):
         t_, c_ = tt.split("/")
         lsw_opts(pf_tt=int(t_), pf_cluster=int(c_))
