@@ -307,9 +307,13 @@ LSW_API lsw_status lsw_decode_group_unmerged(lsw_ctx* ctx, int32_t layer, int32_
  *   gate-scaled products of each token's selected experts as an exact-to-2^-16
  *   (hi, lo) bf16 pair, and ONE tcgen05 contraction per 128-row x 128-token
  *   tile over K = d_in (W x^T) + 2 N rp (the LoRA-up term against the ctx's
- *   packed B) -- fp32 accumulation; otherwise two CUDA-core kernels (only the
- *   k selected experts).  Deterministic.  Scratch is ctx-owned, grown on
- *   demand (not graph-capturable when it grows).
+ *   packed B) -- fp32 accumulation; for the single-CTA groups (o, down) with
+ *   top_k <= 4 the first two are folded into the third launch (A-bank tiles
+ *   whose epilogue builds the operand; variant option pf_fuse_u); otherwise
+ *   two CUDA-core kernels (only the k selected experts).  Deterministic.
+ *   Scratch and the tensor-core plan are ctx-owned, built / grown on demand
+ *   (the first call, or a larger T: not graph-capturable then); a captured
+ *   call takes the three-launch path (tests/test_gpu_graph.py).
  *   LSW_E_STATE if the ctx is merged; LSW_E_ARG for T outside [1, 2^20].
  *   Invalid idx values contribute nothing.  Tensor parallel: row-parallel
  *   groups' partial Y all-reduced in place (as lsw_decode_group_unmerged);

@@ -64,3 +64,52 @@ def test_token_graph_replay_equals_eager(name, impl, fused):
         for kd in synth.KINDS:
             assert torch.equal(Wg[kd], We[kd]), (t, kd)
     assert swg.device_status() == 0 and swe.device_status() == 0
+
+
+@pytest.mark.parametrize("name,T", [("mini", 300), ("mini-r4k4", 129), ("mini-r64k3", 512)])
+def test_prefill_graph_replay(lsw_opts, name, T):
+    """lsw_prefill_group captured in a CUDA graph, after one eager call built
+    the plan and the scratch: under capture the dense launch does not fold in
+    the LoRA-down (the fused launch's completion-count target is fixed per
+    launch), so the captured layer -- all four groups -- replays the
+    three-launch path: bitwise equal, for new inputs copied into the captured
+    buffers, to an eager ctx whose plan has the fusion off (pf_fuse_u=0)."""
+    cfg = synth.get_config(name)
+    W, A, B, router = H.build_weights(cfg, "cuda")
+    swg = H.make_switch(cfg, W, A, B, router, impl="tc")           # default options: fused when eager
+    k = cfg.top_k
+    g = torch.Generator(device="cpu").manual_seed(2405177410 + 97)
+    idx = torch.stack([torch.randperm(cfg.n_experts, generator=g)[:k] for _ in range(T)]).to(torch.int32).cuda()
+    gate = torch.softmax(torch.randn(T, k, generator=g), dim=1).cuda()
+    Xs, Ys_g, Ys_e = [], [], []
+    for grp in synth.GROUPS:
+        d_in = cfg.kind_shape(grp[0])[1]
+        rows = sum(cfg.kind_shape(kd)[0] for kd in grp)
+        Xs.append(torch.empty(T, d_in, dtype=W[grp[0]].dtype, device="cuda"))
+        Ys_g.append(torch.empty(T, rows, device="cuda"))
+        Ys_e.append(torch.empty(T, rows, device="cuda"))
+
+    def fill():
+        for X in Xs:
+            X.copy_(torch.randn(X.shape, generator=g).to(X.dtype))
+
+    fill()
+    for gi in range(len(synth.GROUPS)):                          # eager: plan + scratch
+        swg.prefill_group(0, gi, Xs[gi], idx, gate, Ys_g[gi])
+    torch.cuda.synchronize()
+    lsw_opts(pf_fuse_u=0)
+    swe = H.make_switch(cfg, W, A, B, router, impl="tc")
+    s = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        for gi in range(len(synth.GROUPS)):
+            swg.prefill_group(0, gi, Xs[gi], idx, gate, Ys_g[gi], s)
+    for rep in range(3):
+        fill()
+        graph.replay()
+        for gi in range(len(synth.GROUPS)):
+            swe.prefill_group(0, gi, Xs[gi], idx, gate, Ys_e[gi])
+        torch.cuda.synchronize()
+        for gi in range(len(synth.GROUPS)):
+            assert torch.equal(Ys_g[gi], Ys_e[gi]), (rep, gi)
+    assert swg.device_status() == 0 and swe.device_status() == 0
