@@ -143,6 +143,23 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
   return v;
 }
 
+// Wait until the monotonic count *p reaches target (mod 2^32), with a ~20 s
+// watchdog: a protocol bug traps (sticky error) instead of hanging the GPU.
+__device__ __forceinline__ void wait_count(const uint32_t* p, uint32_t target) {
+  if ((int32_t)(ld_acquire_gpu_u32(p) - target) >= 0) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (uint32_t n = 1;; ++n) {
+    __nanosleep(32);
+    if ((int32_t)(ld_acquire_gpu_u32(p) - target) >= 0) return;
+    if ((n & 1023) == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) __trap();
+    }
+  }
+}
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
                                             uint32_t bar, uint64_t policy) {
   asm volatile(
@@ -414,7 +431,7 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
         if (lora && !bank) {
           if (!z_ready) {
             if (a.a_tiles) {                     // Z is written by this grid's A-bank tiles
-              while ((int32_t)(ld_acquire_gpu_u32(a.zdone) - a.z_target) < 0) __nanosleep(32);
+              wait_count(a.zdone, a.z_target);
               asm volatile("fence.proxy.async.global;" ::: "memory");
             } else {                             // Z is written by the preceding (Z build) grid
               asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -543,8 +560,7 @@ prefill_gemm(const __grid_constant__ Maps maps, const __grid_constant__ Args a) 
         }
         const float* pp = nullptr;
         if (a.a_split == 2) {                    // half 1: every half 0 of this launch stored
-          if (lane == 0)
-            while ((int32_t)(ld_acquire_gpu_u32(a.pdone) - a.p_target) < 0) __nanosleep(32);
+          if (lane == 0) wait_count(a.pdone, a.p_target);
           __syncwarp();
           pp = pj;
         }
