@@ -50,7 +50,8 @@ extern "C" {
  * Probes (deliberately WRONG results; only in a build with -DLSW_TUNING,
  * ignored otherwise): tc_probe (1: W stream only; 16: no fold math),
  * fc_fused_probe (4: no segment wait; 8: no GEMV), gemv_probe (stream only),
- * unmerged_flags (4: no LoRA-up term). */
+ * unmerged_flags (4: no LoRA-up term); timing traces into a caller's device
+ * buffer (value = its address): gemv_trace_buf, pf_trace_buf. */
 LSW_API lsw_status lsw_debug_set_option(const char* key, const char* value);
 
 /* Launch-count ablation (the paper's "simple merge" row of

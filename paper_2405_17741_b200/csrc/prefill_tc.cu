@@ -33,6 +33,7 @@
 // (TMEM lane quarter = warp % 4).  Persistent grid, tiles dealt round-robin
 // with the token tile fastest, so the CTAs that share a W strip run together
 // (one HBM read of W per strip, the X tiles stay in L2).
+#include <cstdlib>
 #include <cstring>
 
 #include "tc_common.cuh"
@@ -657,6 +658,32 @@ __device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
   return r;
 }
 
+#ifdef LSW_TUNING
+// Tuning builds only (option pf_trace_buf = a device pointer): per CTA of the
+// pair launch, per unit: [tile, %smid, accumulator ready, epilogue done]
+// (%globaltimer low 32 bits), 16 units per CTA, slot 0 the CTA's start time.
+__device__ uint32_t* g_pf_trace = nullptr;
+#define PF_TRACE(unit, a0, a1, a2, a3)                                                          \
+  do {                                                                                        \
+    if (g_pf_trace && (unit) < 15) {                                                          \
+      uint32_t* t_ = g_pf_trace + (blockIdx.x * 16 + 1 + (unit)) * 4;                         \
+      t_[0] = (a0); t_[1] = (a1); t_[2] = (a2); t_[3] = (a3);                                 \
+    }                                                                                         \
+  } while (0)
+__device__ __forceinline__ uint32_t pf_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (uint32_t)t;
+}
+__device__ __forceinline__ uint32_t pf_smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+#else
+#define PF_TRACE(unit, a0, a1, a2, a3) do {} while (0)
+#endif
+
 template <int kTT>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_gemm_pair(const __grid_constant__ PairMaps maps, const __grid_constant__ Args a) {
@@ -672,6 +699,13 @@ prefill_gemm_pair(const __grid_constant__ PairMaps maps, const __grid_constant__
   constexpr int kHalf = kTT / 2;                  // tokens per CTA of a pair tile
   const int it0 = (int)cluster_id(), istep = (int)cluster_count();
   const int n_it = a.pair_row0[a.n_sites] * a.n_tt;
+#ifdef LSW_TUNING
+  if (g_pf_trace && threadIdx.x == 0) {
+    uint32_t* t_ = g_pf_trace + blockIdx.x * 16 * 4;
+    t_[0] = pf_now(); t_[1] = pf_smid(); t_[2] = (uint32_t)it0; t_[3] = (uint32_t)istep;
+  }
+  uint32_t tr_ready = 0, tr_unit = 0;
+#endif
   const uint32_t zhalf = (uint32_t)kHalf * a.rp * 2;
   if (threadIdx.x == 0) {
     for (int s = 0; s < a.stages; ++s) {
@@ -811,6 +845,9 @@ prefill_gemm_pair(const __grid_constant__ PairMaps maps, const __grid_constant__
       const TileAt ta = tile(it);
       mbar_wait(smem_u32(&bar_accfull[acc.i]), acc.phase);
       tc_fence_after();
+#ifdef LSW_TUNING
+      tr_ready = pf_now();
+#endif
       const int64_t grow = (int64_t)ta.rb * kTM + row;
       const bool ok = grow < a.rows_valid[ta.q];
       float* outp = a.out + a.col0[ta.q] + grow;
@@ -832,6 +869,10 @@ prefill_gemm_pair(const __grid_constant__ PairMaps maps, const __grid_constant__
         if (leader) mbar_arrive(smem_u32(&bar_accempty[acc.i]));
         else mbar_arrive_remote(smem_u32(&bar_accempty[acc.i]), 0);
       }
+#ifdef LSW_TUNING
+      if (warp == 2 && lane == 0) PF_TRACE(tr_unit, (uint32_t)it, pf_smid(), tr_ready, pf_now());
+      ++tr_unit;
+#endif
       acc.next();
     }
   }
@@ -1019,6 +1060,13 @@ cudaError_t pf_plan_create(PfPlan** out, const SwitchParams& sp, const TcPlan* t
   if (p->tt_opt != 128 && p->tt_opt != 256) p->tt_opt = 0;
   p->cl_opt = (int)opt_int("pf_cluster", 0);
   p->pair_opt = (int)opt_int("pf_pair", 1);
+#ifdef LSW_TUNING
+  {
+    const char* v = opt_str("pf_trace_buf");
+    uint32_t* buf = v ? reinterpret_cast<uint32_t*>(strtoull(v, nullptr, 10)) : nullptr;
+    cudaMemcpyToSymbol(pf::g_pf_trace, &buf, sizeof(buf));
+  }
+#endif
   p->fuse_opt = (int)opt_int("pf_fuse_u", 1);
   p->split_opt = (int)opt_int("pf_bank_split", 1);
   if (p->cl_opt != 1 && p->cl_opt != 2 && p->cl_opt != 4) p->cl_opt = 0;
