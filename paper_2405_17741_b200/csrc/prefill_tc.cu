@@ -22,13 +22,15 @@
 //     accumulated in fp32 in TMEM by one chain of tcgen05.mma (M = 128,
 //     N = 128) -- the LoRA-up term is just N*2*rp more K of the same
 //     contraction -- then written to Y (fp32) by the epilogue warps.
-// Single-CTA launches (no CTA pairs; option pf_fuse_u, default on) fold 1 and
-// 2 into 3: the launch's first tiles are A-bank tiles (128 bank rows x one
-// token tile, full K -- the LoRA-down without split), whose epilogue forms z =
+// Single-CTA launches (no CTA pairs, top_k <= 4, not under stream capture;
+// option pf_fuse_u, default on) fold 1 and 2 into 3: the launch's first tiles
+// are A-bank tiles (128 bank rows x one token tile), whose epilogue forms z =
 // c_t(e) u from TMEM and stores the (hi, lo) Z slots itself, then counts the
 // tile in a monotonic device word; a W tile's producer waits for this launch's
-// count before its first LoRA-up stage.  One launch instead of three, no fp32
-// U round trip through L2.
+// count before its first LoRA-up stage.  When the launch is one wave each bank
+// tile's K is split over two CTAs (option pf_bank_split): half 0's fp32
+// partial goes through U, half 1 adds it (fixed order) and builds Z.  One
+// launch instead of three.
 // Warp roles: 0 TMA/bulk producer, 1 MMA issuer (+ TMEM alloc), 2-5 epilogue
 // (TMEM lane quarter = warp % 4).  Persistent grid, tiles dealt round-robin
 // with the token tile fastest, so the CTAs that share a W strip run together
